@@ -1,0 +1,147 @@
+/*
+ * ircur_b200.h — C-ABI of the B200-native IRCUR hot path.
+ *
+ * The reference (`/root/reference/pkg/src/ircur`) is a pure Python/numpy
+ * package with no FFI layer: its boundary for this path is the Python
+ * function `ircur.solver.solve(D, config, observer)` (solver.py:304-416) and
+ * the public phase helpers it is built from.  Each export below replaces one
+ * piece of that function; the reference-side binding (ctypes, as used by
+ * `paper_2010_07422_b200/_capi.py`) is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Plain C types only.  Matrices are device pointers unless stated; D is
+ *     row-major with leading dimension `ldd` (elements), BORROWED (read-only,
+ *     must outlive the context's use of it).
+ *   - Every function returns an ircur_status (0 = OK, <0 = error) and sets a
+ *     thread-local message readable with ircur_last_error().
+ *   - dtype selects storage AND arithmetic of the strip kernels: F64 data is
+ *     processed in fp64 end to end; F32 data in fp32 with fp64 norm
+ *     accumulation.  The core SVD/pinv always runs in fp64.
+ *   - A context is bound to one device and one stream and is not thread-safe;
+ *     independent contexts may share the same D.
+ *   - Row sharding: a context may own rows [row0, row0+local_rows) of an
+ *     n1 x n2 matrix (multi-GPU); single-GPU callers pass row0=0,
+ *     local_rows=n1.
+ */
+#ifndef IRCUR_B200_H
+#define IRCUR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IRCUR_ABI_VERSION 1
+
+typedef enum {
+  IRCUR_OK = 0,
+  IRCUR_EINVAL = -1,     /* bad argument / config  -> ValueError          */
+  IRCUR_ENONFINITE = -2, /* NaN/Inf in D            -> ValueError          */
+  IRCUR_ECUDA = -3,      /* CUDA runtime error      -> RuntimeError        */
+  IRCUR_ENCCL = -4,      /* collective failure      -> RuntimeError        */
+  IRCUR_ENOMEM = -5,     /* device allocation       -> MemoryError         */
+  IRCUR_EEMPTY = -6      /* empty D                 -> ValueError          */
+} ircur_status;
+
+typedef enum { IRCUR_F32 = 0, IRCUR_F64 = 1 } ircur_dtype;
+typedef enum { IRCUR_FIXED = 0, IRCUR_RESAMPLED = 1 } ircur_mode;
+
+typedef struct ircur_ctx* ircur_ctx_t;
+
+/* Library identity. */
+int ircur_abi_version(void);
+const char* ircur_last_error(void);
+
+/* Create a solver context (workspace for strips' factors, core, SVD scratch,
+ * index sets, trace).  max_rows/max_cols bound |I|,|J| (the draw counts m),
+ * max_iter bounds the loop.  `stream` is a cudaStream_t (NULL = default).
+ * Replaces the allocations solve() makes up front (solver.py:346-356). */
+int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_t n2,
+                     int rank, int max_rows, int max_cols, int max_iter,
+                     int64_t row0, int64_t local_rows, void* stream);
+int ircur_ctx_destroy(ircur_ctx_t ctx);
+
+/* One pass over the local rows of D: finiteness check, max|D| and (optional)
+ * column-major copy used by the column-strip kernel.
+ * Replaces matcore.require_finite (matcore.py:70-77, called solver.py:319)
+ * and inf_norm (matcore.py:87-91, solver.py:342-344).  Host-blocking. */
+int ircur_prepare(ircur_ctx_t ctx, const void* D, int64_t ldd, int make_colmajor,
+                  int* all_finite, double* max_abs);
+
+/* Upload the pre-generated index sets (host int64, strictly increasing),
+ * n_sets consecutive (I_k, J_k) pairs packed with strides max_rows/max_cols.
+ * The host draws them with the reference's numpy call sequence
+ * (sampling.py:93-104 in the order of solver.py:325-329, 362-364). */
+int ircur_set_indices(ircur_ctx_t ctx, int n_sets, const int64_t* rows,
+                      const int32_t* row_counts, const int64_t* cols,
+                      const int32_t* col_counts);
+
+/* den = ||D(I_s,:)||_F^2, ||D(:,J_s)||_F^2 partial sums of the LOCAL rows
+ * for index set s (fp64; host-blocking).  Replaces the pre-loop frob_norm
+ * pair of solver.py:331-333 used by the den == 0 early exit (:335-341). */
+int ircur_slab_sqnorms(ircur_ctx_t ctx, int set, double* rows_sq, double* cols_sq);
+
+/* The device-resident loop, single device (solver.py:358-414): for
+ * k = 0..max_iter-1 runs core -> SVD/pinv -> fused strips -> stop check.
+ * zetas[k] = gamma**k * zeta0 is evaluated by the caller exactly as the
+ * reference does (solver.py:372) and passed in.  mode IRCUR_FIXED uses index
+ * set 0 for every k, IRCUR_RESAMPLED set k.  Outputs are host arrays of
+ * length max_iter (e_k and per-iteration milliseconds from CUDA events).
+ * Host-blocking; stops as soon as e_k <= eps (no per-iteration host sync:
+ * the stop flag is written by the device into mapped host memory). */
+int ircur_run(ircur_ctx_t ctx, const double* zetas, double eps, int mode, int max_iter,
+              int* iterations, int* converged, double* errors, float* iter_ms);
+
+/* Exactly one iteration k on index set `set` with threshold zeta (the
+ * observer path, solver.py:410-411).  Returns e_k.  Host-blocking. */
+int ircur_iterate(ircur_ctx_t ctx, int k, int set, double zeta, double* e);
+
+/* Final CUR/sparse strips of the last completed iteration, fp64, written to
+ * device or host pointers (cudaMemcpyDefault):  C  local_rows x |J|,
+ * R |I_loc| x n2, S_rows |I_loc| x n2, S_cols local_rows x |J| (row-major).
+ * Replaces CurFactors.C/R and SparseEstimate (solver.py:375-391). Any
+ * pointer may be NULL. */
+int ircur_get_strips(ircur_ctx_t ctx, double* C, double* R, double* S_rows, double* S_cols);
+
+/* Core pinv factor of the last iteration (PinvFactor, matcore.py:142-165):
+ * W |I| x k, sigma k, V |J| x k, inv_sigma k (fp64, host or device), plus
+ * k = min(rank, |I|, |J|) and the final |I|, |J|. */
+int ircur_get_core(ircur_ctx_t ctx, double* W, double* sigma, double* V,
+                   double* inv_sigma, int* k, int* n_rows, int* n_cols);
+
+/* Rank-r factors of L = P Q of the last iteration: P = C V diag(inv_sigma)
+ * (local_rows x rank), Q = W^T R (rank x n2), in the context dtype. */
+int ircur_get_factors(ircur_ctx_t ctx, void* P, void* Q);
+
+/* Stream L = P Q for the local rows into L (device, row-major, ldl),
+ * out_dtype IRCUR_F32/F64.  Replaces solver.materialize (solver.py:211-213)
+ * with a K=rank streaming writer. */
+int ircur_materialize(ircur_ctx_t ctx, void* L, int64_t ldl, int out_dtype);
+
+/* Stateless variant: stream L = P Q from caller-held factors Pt (rank x
+ * nrows, row stride ldp) and Q (rank x n2, row stride ldq), dtype
+ * IRCUR_F32/F64, into L (nrows x n2, ldl) in out_dtype. */
+int ircur_materialize_factors(const void* Pt, int64_t ldp, const void* Q, int64_t ldq,
+                              int64_t nrows, int64_t n2, int rank, int dtype, void* L,
+                              int64_t ldl, int out_dtype, void* stream);
+
+/* BASELINE.json synthetic generator on the device (configs 1-5): rows
+ * [row0, row0+nrows) of D = W V^T + S, S = Bernoulli(alpha) support with
+ * U[-amp_a, amp_a] values, drawn from the SAME numpy PCG64 stream the host
+ * generator uses (oracle/ircur_oracle.py baseline_problem): cell (i,j) takes
+ * mask draw i*n2+j and value draw n1*n2+i*n2+j after `pcg` = {state_lo,
+ * state_hi, inc_lo, inc_hi}.  Any row sharding reproduces the same matrix.
+ * W (n1 x rank) and V (n2 x rank) are fp64 device arrays.  If D is NULL only
+ * the statistics are computed: max|L| and the quantised sum
+ * sum(rint(|L| * 2^24)) from which a = mean|L| is derived order-free.
+ * Host-blocking. */
+int ircur_gen_baseline(void* D, int dtype, int64_t ldd, int64_t n1, int64_t n2,
+                       int64_t row0, int64_t nrows, int rank, const double* W,
+                       const double* V, double alpha, double amp_a, const uint64_t* pcg,
+                       double* max_abs_L, int64_t* qsum_abs_L, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IRCUR_B200_H */

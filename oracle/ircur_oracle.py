@@ -204,11 +204,16 @@ def materialize(C, V, inv_sigma, W, R):
 # ----------------------------------------------- BASELINE.json generators
 def baseline_problem(n1: int, n2: int, rank: int, alpha: float, seed: int,
                      amp: float = 10.0):
-    """BASELINE.json configs 1/2/4 restated (Gaussian factors, Bernoulli(alpha)
+    """BASELINE.json configs 1/2/4/5 restated (Gaussian factors, Bernoulli(alpha)
     support, outliers U[-amp*a, amp*a] with a = mean|L|), in float64.
 
-    L is accumulated elementwise in t order (multiply, then add) so that the
-    device generator reproduces it bitwise.  Returns D, L, S, max|L|.
+    Draw order from one numpy Generator (PCG64): W (n1 x r) and V (n2 x r)
+    standard normals, then one `random()` per cell for the mask, then one
+    `uniform()` per cell for the value (row-major).  L is accumulated
+    elementwise in t order (multiply, then add); a = mean|L| is taken as an
+    exact integer sum of |L| quantised to 2^-24, so it does not depend on
+    summation order.  The device generator (ircur_gen_baseline) reproduces D
+    bit for bit from the same PCG64 state.  Returns D, L, S, max|L|.
     """
     rng = np.random.default_rng(seed)
     W = rng.standard_normal((n1, rank))
@@ -216,9 +221,16 @@ def baseline_problem(n1: int, n2: int, rank: int, alpha: float, seed: int,
     L = W[:, 0:1] * V[:, 0][None, :]
     for t in range(1, rank):
         L = L + W[:, t:t + 1] * V[:, t][None, :]
-    a = float(np.abs(L).mean())
+    a = mean_abs_quantised(L)
+    A = amp * a
     mask = rng.random((n1, n2)) < alpha
-    vals = rng.uniform(-amp * a, amp * a, size=(n1, n2))
+    vals = rng.uniform(-A, A, size=(n1, n2))
     S = np.where(mask, vals, 0.0)
     D = L + S
     return D, L, S, float(np.abs(L).max())
+
+
+def mean_abs_quantised(L: np.ndarray) -> float:
+    """mean|L| from an exact int64 sum of rint(|L| * 2^24) (order-free)."""
+    q = np.rint(np.abs(L) * 16777216.0).astype(np.int64).sum()
+    return float(q) / 16777216.0 / L.size

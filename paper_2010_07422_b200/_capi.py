@@ -1,0 +1,84 @@
+"""ctypes binding of libircur_b200.so (the C-ABI in include/ircur_b200.h).
+
+This is the "thin C-ABI/ctypes layer" of the design: plain pointers and
+sizes cross it, no torch types.  Errors come back as negative status codes
+plus ircur_last_error() and are mapped to the exceptions the reference
+raises (ValueError for bad input, matcore.py:70-77 / solver.py:320-321).
+
+There is no fallback: if the shared library is missing or fails to load,
+every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libircur_b200.so")
+
+OK, EINVAL, ENONFINITE, ECUDA, ENCCL, ENOMEM, EEMPTY = 0, -1, -2, -3, -4, -5, -6
+F32, F64 = 0, 1
+FIXED, RESAMPLED = 0, 1
+
+# (name, restype, argtypes) — mirrors include/ircur_b200.h one to one.
+_vp, _i, _i64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
+_pi, _pd, _pf, _pi64, _pu64 = (C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_float),
+                               C.POINTER(C.c_int64), C.POINTER(C.c_uint64))
+PROTOTYPES = [
+    ("ircur_abi_version", _i, []),
+    ("ircur_last_error", C.c_char_p, []),
+    ("ircur_ctx_create", _i, [C.POINTER(_vp), _i, _i, _i64, _i64, _i, _i, _i, _i, _i64, _i64, _vp]),
+    ("ircur_ctx_destroy", _i, [_vp]),
+    ("ircur_prepare", _i, [_vp, _vp, _i64, _i, _pi, _pd]),
+    ("ircur_set_indices", _i, [_vp, _i, _pi64, C.POINTER(C.c_int32), _pi64, C.POINTER(C.c_int32)]),
+    ("ircur_slab_sqnorms", _i, [_vp, _i, _pd, _pd]),
+    ("ircur_run", _i, [_vp, _pd, _d, _i, _i, _pi, _pi, _pd, _pf]),
+    ("ircur_iterate", _i, [_vp, _i, _i, _d, _pd]),
+    ("ircur_get_strips", _i, [_vp, _vp, _vp, _vp, _vp]),
+    ("ircur_get_core", _i, [_vp, _vp, _vp, _vp, _vp, _pi, _pi, _pi]),
+    ("ircur_get_factors", _i, [_vp, _vp, _vp]),
+    ("ircur_materialize", _i, [_vp, _vp, _i64, _i]),
+    ("ircur_materialize_factors", _i, [_vp, _i64, _vp, _i64, _i64, _i64, _i, _i, _vp, _i64, _i, _vp]),
+    ("ircur_gen_baseline", _i, [_vp, _i, _i64, _i64, _i64, _i64, _i64, _i, _vp, _vp, _d, _d,
+                                _pu64, _pd, _pi64, _vp]),
+]
+
+_lib = None
+
+
+class IrcurError(RuntimeError):
+    """A CUDA/NCCL-level failure inside libircur_b200."""
+
+
+def load() -> C.CDLL:
+    """Load (once) and type the shared library; raise if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2010_07422_b200._build` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in PROTOTYPES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = load().ircur_last_error().decode(errors="replace")
+    if rc in (EINVAL, ENONFINITE, EEMPTY):
+        raise ValueError(msg)
+    if rc == ENOMEM:
+        raise MemoryError(msg)
+    raise IrcurError(f"libircur_b200 error {rc}: {msg}")
+
+
+def exported_symbols() -> list[str]:
+    return [name for name, _, _ in PROTOTYPES]

@@ -1,0 +1,674 @@
+// extern "C" boundary of libircur_b200.so (see include/ircur_b200.h).
+//
+// A context owns the device workspace of one solve (factor ping-pong
+// buffers, core, SVD scratch, index sets, trace) on one device + stream and
+// drives the device-resident iteration loop of solver.py:358-414.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ircur_b200.h"
+#include "launchers.cuh"
+
+using namespace ircur;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define IR_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(_e == cudaErrorMemoryAllocation ? IRCUR_ENOMEM : IRCUR_ECUDA,         \
+                  std::string(#call) + ": " + cudaGetErrorString(_e));                  \
+  } while (0)
+
+}  // namespace
+
+struct ircur_ctx {
+  int device = 0, dtype = 0;
+  int64_t n1 = 0, n2 = 0, row0 = 0, nloc = 0;
+  int r = 1, max_rows = 0, max_cols = 0, max_iter = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  size_t esz = 4;
+  // borrowed input
+  const void* D = nullptr;
+  int64_t ldd = 0;
+  // owned
+  void* Dt = nullptr;
+  int64_t ldt = 0;
+  int* d_rows = nullptr;
+  int* d_cols = nullptr;
+  int n_sets = 0;
+  std::vector<int> h_row_cnt, h_col_cnt, h_row_lo;  // h_row_lo: first local entry in set
+  std::vector<int> h_row_loc_cnt;
+  void* Pt[2] = {nullptr, nullptr};
+  void* Qt[2] = {nullptr, nullptr};
+  int64_t ldp = 0, ldq = 0;
+  double* U = nullptr;
+  void* PoldI = nullptr;
+  void* QoldJ = nullptr;
+  void* Wr = nullptr;
+  void* PI = nullptr;
+  void* VS = nullptr;
+  void* QJ = nullptr;
+  double* W = nullptr;
+  double* sigma = nullptr;
+  double* V = nullptr;
+  double* inv = nullptr;
+  double* G = nullptr;
+  double* svd_scratch = nullptr;
+  double* partials = nullptr;
+  int max_partials = 0;
+  double* errors = nullptr;
+  int* flags = nullptr;  // [0]=done [1]=iters [2]=converged [3]=nonfinite [4]=svd steps
+  unsigned long long* maxbits = nullptr;
+  int* h_flags = nullptr;  // mapped pinned: [0]=done [1]=iters
+  int* h_flags_dev = nullptr;
+  std::vector<cudaEvent_t> ev;
+  int strips_cs = 1;
+  // last completed iteration
+  int last_k = -1, last_set = 0;
+  double last_zeta = 0.0;
+  bool has_state = false;
+};
+
+namespace {
+
+template <typename T>
+T storage_zeta(double z);
+template <>
+float storage_zeta<float>(double z) {
+  float f = (float)z;
+  if ((double)f > z) f = std::nextafter(f, -INFINITY);
+  return f;
+}
+template <>
+double storage_zeta<double>(double z) {
+  return z;
+}
+
+int64_t pad4(int64_t n) { return (n + 3) & ~int64_t(3); }
+
+int svd_cluster_size(int n, int m, int kk) {
+  int cs = std::max(1, std::min(8, (n + 63) / 64));
+  while (cs <= 16 && svd_smem_bytes(n, m, kk, cs) > 227 * 1024) ++cs;
+  return cs;
+}
+
+template <typename T>
+int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int max_iter,
+                     bool host_flags) {
+  cudaStream_t st = c->stream;
+  const int old = k & 1, nw = old ^ 1;
+  const int* I = c->d_rows + (size_t)set * c->max_rows;
+  const int* J = c->d_cols + (size_t)set * c->max_cols;
+  const int mI_all = c->h_row_cnt[set];
+  const int i_lo = c->h_row_lo[set];
+  const int mI = c->h_row_loc_cnt[set];  // local rows of I (single GPU: all)
+  const int nJ = c->h_col_cnt[set];
+  (void)mI_all;
+  const T zt = storage_zeta<T>(zeta);
+  const int R = c->r;
+  const int* done = c->flags;
+
+  CoreArgs<T> ca;
+  ca.D = (const T*)c->D; ca.ldd = c->ldd; ca.row0 = c->row0;
+  ca.I = I + i_lo; ca.mI = mI; ca.J = J; ca.nJ = nJ;
+  ca.Pt = (const T*)c->Pt[old]; ca.ldp = c->ldp;
+  ca.Qt = (const T*)c->Qt[old]; ca.ldq = c->ldq;
+  ca.zt = zt; ca.U = c->U; ca.ldu = c->max_cols;
+  ca.PoldI = (T*)c->PoldI; ca.QoldJ = (T*)c->QoldJ; ca.done = done;
+  IR_CUDA(launch_core<T>(ca, R, st));
+
+  SvdArgs sa;
+  sa.U = c->U; sa.ldu = c->max_cols; sa.G = c->G; sa.ldg = c->max_cols;
+  sa.m = mI; sa.n = nJ; sa.r = R;
+  sa.kk = std::min(std::min(2 * R, 32), std::min(mI, nJ));
+  sa.warm = k > 0 ? c->QoldJ : nullptr; sa.warm_ld = R; sa.warm_cols = k > 0 ? R : 0;
+  sa.W = c->W; sa.sigma = c->sigma; sa.V = c->V; sa.inv = c->inv;
+  sa.Wr = c->Wr; sa.PI = c->PI; sa.VS = c->VS; sa.QJ = c->QJ;
+  sa.scratch = c->svd_scratch; sa.done = done; sa.steps_out = c->flags + 4;
+  sa.tol = sizeof(T) == 8 ? 2e-14 : 1e-11;
+  sa.maxsteps = 100;
+  sa.salt = 0x1234567ull + (uint64_t)k * 7919ull;
+  const int svd_cs = svd_cluster_size(nJ, mI, sa.kk);
+  IR_CUDA(launch_svd<T>(sa, svd_cs, st));
+
+  StripsArgs<T> pa;
+  const int TX = strips_tx();
+  StripDesc<T>& rs = pa.s[0];
+  rs.src = (const T*)c->D; rs.line_stride = c->ldd; rs.pos_stride = 1;
+  rs.vec_ok = (c->ldd % 2 == 0) && ((uintptr_t)c->D % (2 * sizeof(T)) == 0);
+  rs.lines = I + i_lo; rs.line_off = (int)c->row0; rs.nk = mI; rs.npos = (int)c->n2;
+  rs.lineA = (const T*)c->PoldI; rs.lineW = (const T*)c->Wr; rs.lineRes = (const T*)c->PI;
+  rs.Bold = (const T*)c->Qt[old]; rs.ldb = c->ldq; rs.Fnew = (T*)c->Qt[nw]; rs.ldf = c->ldq;
+  rs.other = J; rs.other_off = 0; rs.nother = nJ; rs.otherF = (const T*)c->QJ;
+  rs.tiles = (int)((c->n2 + TX - 1) / TX);
+  StripDesc<T>& cs = pa.s[1];
+  if (c->Dt) {
+    cs.src = (const T*)c->Dt; cs.line_stride = c->ldt; cs.pos_stride = 1;
+    cs.vec_ok = (c->ldt % 2 == 0);
+  } else {
+    cs.src = (const T*)c->D; cs.line_stride = 1; cs.pos_stride = c->ldd; cs.vec_ok = 0;
+  }
+  cs.lines = J; cs.line_off = 0; cs.nk = nJ; cs.npos = (int)c->nloc;
+  cs.lineA = (const T*)c->QoldJ; cs.lineW = (const T*)c->VS; cs.lineRes = (const T*)c->QJ;
+  cs.Bold = (const T*)c->Pt[old]; cs.ldb = c->ldp; cs.Fnew = (T*)c->Pt[nw]; cs.ldf = c->ldp;
+  cs.other = I + i_lo; cs.other_off = (int)c->row0; cs.nother = mI; cs.otherF = (const T*)c->PI;
+  cs.tiles = (int)((c->nloc + TX - 1) / TX);
+  pa.zt = zt; pa.partials = c->partials; pa.done = done;
+  IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, st));
+
+  FinalizeArgs fa;
+  fa.partials = c->partials;
+  fa.ncta_rows = rs.tiles * c->strips_cs;
+  fa.ncta_cols = cs.tiles * c->strips_cs;
+  fa.k = k; fa.eps = eps; fa.max_iter = max_iter;
+  fa.errors = c->errors; fa.done = c->flags; fa.iters = c->flags + 1; fa.converged = c->flags + 2;
+  fa.host_done = host_flags ? c->h_flags_dev : nullptr;
+  fa.host_iters = host_flags ? c->h_flags_dev + 1 : nullptr;
+  IR_CUDA(launch_finalize(fa, st));
+  return IRCUR_OK;
+}
+
+int iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int max_iter, bool hf) {
+  return c->dtype == IRCUR_F32 ? launch_iteration<float>(c, k, set, zeta, eps, max_iter, hf)
+                               : launch_iteration<double>(c, k, set, zeta, eps, max_iter, hf);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ircur_abi_version(void) { return IRCUR_ABI_VERSION; }
+const char* ircur_last_error(void) { return g_last_error.c_str(); }
+
+int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_t n2, int rank,
+                     int max_rows, int max_cols, int max_iter, int64_t row0, int64_t local_rows,
+                     void* stream) {
+  if (!out) return fail(IRCUR_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (dtype != IRCUR_F32 && dtype != IRCUR_F64) return fail(IRCUR_EINVAL, "dtype must be F32 or F64");
+  if (n1 < 1 || n2 < 1) return fail(IRCUR_EEMPTY, "D must be nonempty");
+  if (rank < 1 || rank > kMaxRank)
+    return fail(IRCUR_EINVAL, "rank must lie in [1, " + std::to_string(kMaxRank) + "]");
+  if (max_rows < 1 || max_cols < 1 || max_rows > n1 || max_cols > n2)
+    return fail(IRCUR_EINVAL, "need 1 <= max_rows <= n1 and 1 <= max_cols <= n2");
+  if (max_iter < 1) return fail(IRCUR_EINVAL, "max_iter must be >= 1");
+  if (row0 < 0 || local_rows < 1 || row0 + local_rows > n1)
+    return fail(IRCUR_EINVAL, "row shard out of range");
+  if (n1 > INT32_MAX || n2 > INT32_MAX) return fail(IRCUR_EINVAL, "dimensions must fit int32");
+  const int kk = std::min(std::min(2 * rank, 32), std::min(max_rows, max_cols));
+  if (svd_smem_bytes(max_cols, max_rows, kk, 16) > 227 * 1024)
+    return fail(IRCUR_EINVAL, "sampled column count too large for the core SVD kernel");
+  const int lpc = strips_lines_per_cta();
+  const int need_cs = (std::max(max_rows, max_cols) + lpc - 1) / lpc;
+  if (need_cs > 16) return fail(IRCUR_EINVAL, "sampled index sets too large for the strip kernel");
+
+  ircur_ctx* c = new ircur_ctx();
+  c->device = device; c->dtype = dtype; c->n1 = n1; c->n2 = n2; c->r = rank;
+  c->max_rows = max_rows; c->max_cols = max_cols; c->max_iter = max_iter;
+  c->row0 = row0; c->nloc = local_rows; c->stream = (cudaStream_t)stream;
+  c->esz = dtype == IRCUR_F32 ? 4 : 8;
+  c->strips_cs = std::max(1, need_cs);
+  auto cleanup = [&](int code) {
+    ircur_ctx_destroy(c);
+    return code;
+  };
+#define IR_CUDA_C(call)                                                                 \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return cleanup(fail(_e == cudaErrorMemoryAllocation ? IRCUR_ENOMEM : IRCUR_ECUDA, \
+                          std::string(#call) + ": " + cudaGetErrorString(_e)));         \
+  } while (0)
+  IR_CUDA_C(cudaSetDevice(device));
+  IR_CUDA_C(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  c->ldp = pad4(local_rows);
+  c->ldq = pad4(n2);
+  for (int b = 0; b < 2; ++b) {
+    IR_CUDA_C(cudaMalloc(&c->Pt[b], (size_t)rank * c->ldp * c->esz));
+    IR_CUDA_C(cudaMalloc(&c->Qt[b], (size_t)rank * c->ldq * c->esz));
+  }
+  IR_CUDA_C(cudaMalloc(&c->U, (size_t)max_rows * max_cols * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->PoldI, (size_t)max_rows * rank * c->esz));
+  IR_CUDA_C(cudaMalloc(&c->QoldJ, (size_t)max_cols * rank * c->esz));
+  IR_CUDA_C(cudaMalloc(&c->Wr, (size_t)max_rows * rank * c->esz));
+  IR_CUDA_C(cudaMalloc(&c->PI, (size_t)max_rows * rank * c->esz));
+  IR_CUDA_C(cudaMalloc(&c->VS, (size_t)max_cols * rank * c->esz));
+  IR_CUDA_C(cudaMalloc(&c->QJ, (size_t)max_cols * rank * c->esz));
+  IR_CUDA_C(cudaMalloc(&c->W, (size_t)max_rows * rank * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->sigma, (size_t)rank * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->V, (size_t)max_cols * rank * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->inv, (size_t)rank * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->G, (size_t)max_cols * max_cols * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->svd_scratch, (size_t)max_cols * 32 * sizeof(double)));
+  const int TX = strips_tx();
+  c->max_partials = (int)(((n2 + TX - 1) / TX + (local_rows + TX - 1) / TX) * c->strips_cs) * 2 + 4096;
+  IR_CUDA_C(cudaMalloc(&c->partials, (size_t)c->max_partials * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->errors, (size_t)max_iter * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->flags, 16 * sizeof(int)));
+  IR_CUDA_C(cudaMalloc(&c->maxbits, sizeof(unsigned long long)));
+  IR_CUDA_C(cudaHostAlloc(&c->h_flags, 16 * sizeof(int), cudaHostAllocMapped));
+  IR_CUDA_C(cudaHostGetDevicePointer((void**)&c->h_flags_dev, c->h_flags, 0));
+  c->ev.resize(max_iter + 1);
+  for (auto& e : c->ev) IR_CUDA_C(cudaEventCreate(&e));
+  IR_CUDA_C(cudaMemsetAsync(c->flags, 0, 16 * sizeof(int), c->stream));
+  *out = c;
+  return IRCUR_OK;
+#undef IR_CUDA_C
+}
+
+int ircur_ctx_destroy(ircur_ctx_t c) {
+  if (!c) return IRCUR_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U,
+                  c->PoldI, c->QoldJ, c->Wr, c->PI, c->VS, c->QJ, c->W, c->sigma, c->V, c->inv,
+                  c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  delete c;
+  return IRCUR_OK;
+}
+
+int ircur_prepare(ircur_ctx_t c, const void* D, int64_t ldd, int make_colmajor, int* all_finite,
+                  double* max_abs) {
+  if (!c || !D) return fail(IRCUR_EINVAL, "null context or D");
+  if (ldd < c->n2) return fail(IRCUR_EINVAL, "ldd < n2");
+  IR_CUDA(cudaSetDevice(c->device));
+  c->D = D;
+  c->ldd = ldd;
+  c->has_state = false;
+  if (make_colmajor && !c->Dt) {
+    c->ldt = pad4(c->nloc);
+    IR_CUDA(cudaMalloc(&c->Dt, (size_t)c->n2 * c->ldt * c->esz));
+  }
+  if (!make_colmajor && c->Dt) {
+    cudaFree(c->Dt);
+    c->Dt = nullptr;
+  }
+  IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), c->stream));
+  IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), c->stream));
+  if (c->dtype == IRCUR_F32)
+    IR_CUDA(launch_prep<float>((const float*)D, ldd, c->nloc, c->n2, (float*)c->Dt, c->ldt, c->maxbits,
+                               c->flags + 3, c->num_sms, c->stream));
+  else
+    IR_CUDA(launch_prep<double>((const double*)D, ldd, c->nloc, c->n2, (double*)c->Dt, c->ldt,
+                                c->maxbits, c->flags + 3, c->num_sms, c->stream));
+  unsigned long long mb = 0;
+  int nf = 0;
+  IR_CUDA(cudaMemcpyAsync(&mb, c->maxbits, sizeof(mb), cudaMemcpyDeviceToHost, c->stream));
+  IR_CUDA(cudaMemcpyAsync(&nf, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  double mx;
+  std::memcpy(&mx, &mb, sizeof(mx));
+  if (all_finite) *all_finite = nf ? 0 : 1;
+  if (max_abs) *max_abs = mx;
+  if (nf) return fail(IRCUR_ENONFINITE, "matrix contains non-finite entries");
+  return IRCUR_OK;
+}
+
+int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int32_t* row_counts,
+                      const int64_t* cols, const int32_t* col_counts) {
+  if (!c || n_sets < 1 || !rows || !cols || !row_counts || !col_counts)
+    return fail(IRCUR_EINVAL, "bad index-set arguments");
+  IR_CUDA(cudaSetDevice(c->device));
+  std::vector<int> hr((size_t)n_sets * c->max_rows, 0), hc((size_t)n_sets * c->max_cols, 0);
+  c->h_row_cnt.assign(n_sets, 0);
+  c->h_col_cnt.assign(n_sets, 0);
+  c->h_row_lo.assign(n_sets, 0);
+  c->h_row_loc_cnt.assign(n_sets, 0);
+  for (int s = 0; s < n_sets; ++s) {
+    const int mr = row_counts[s], mc = col_counts[s];
+    if (mr < 1 || mr > c->max_rows || mc < 1 || mc > c->max_cols)
+      return fail(IRCUR_EINVAL, "index set size out of range");
+    int lo = -1, cnt = 0;
+    for (int i = 0; i < mr; ++i) {
+      const int64_t v = rows[(size_t)s * c->max_rows + i];
+      if (v < 0 || v >= c->n1 || (i > 0 && v <= rows[(size_t)s * c->max_rows + i - 1]))
+        return fail(IRCUR_EINVAL, "row indices must be strictly increasing and in range");
+      hr[(size_t)s * c->max_rows + i] = (int)v;
+      if (v >= c->row0 && v < c->row0 + c->nloc) {
+        if (lo < 0) lo = i;
+        ++cnt;
+      }
+    }
+    for (int j = 0; j < mc; ++j) {
+      const int64_t v = cols[(size_t)s * c->max_cols + j];
+      if (v < 0 || v >= c->n2 || (j > 0 && v <= cols[(size_t)s * c->max_cols + j - 1]))
+        return fail(IRCUR_EINVAL, "column indices must be strictly increasing and in range");
+      hc[(size_t)s * c->max_cols + j] = (int)v;
+    }
+    c->h_row_cnt[s] = mr;
+    c->h_col_cnt[s] = mc;
+    c->h_row_lo[s] = lo < 0 ? 0 : lo;
+    c->h_row_loc_cnt[s] = cnt;
+  }
+  if (n_sets > c->n_sets) {
+    if (c->d_rows) cudaFree(c->d_rows);
+    if (c->d_cols) cudaFree(c->d_cols);
+    c->d_rows = nullptr;
+    c->d_cols = nullptr;
+    IR_CUDA(cudaMalloc(&c->d_rows, hr.size() * sizeof(int)));
+    IR_CUDA(cudaMalloc(&c->d_cols, hc.size() * sizeof(int)));
+  }
+  c->n_sets = n_sets;
+  IR_CUDA(cudaMemcpyAsync(c->d_rows, hr.data(), hr.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  IR_CUDA(cudaMemcpyAsync(c->d_cols, hc.data(), hc.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+  return IRCUR_OK;
+}
+
+int ircur_slab_sqnorms(ircur_ctx_t c, int set, double* rows_sq, double* cols_sq) {
+  if (!c || !c->D || set < 0 || set >= c->n_sets) return fail(IRCUR_EINVAL, "bad context/set");
+  IR_CUDA(cudaSetDevice(c->device));
+  const int nb_rows = std::max(1, std::min(c->num_sms * 2, (int)((int64_t)c->h_row_loc_cnt[set] * c->n2 / 4096 + 1)));
+  const int nb_cols = std::max(1, std::min(c->num_sms * 2, (int)(c->nloc * c->h_col_cnt[set] / 4096 + 1)));
+  if (nb_rows + nb_cols > c->max_partials) return fail(IRCUR_EINVAL, "partials buffer too small");
+  const int* I = c->d_rows + (size_t)set * c->max_rows + c->h_row_lo[set];
+  const int* J = c->d_cols + (size_t)set * c->max_cols;
+  if (c->dtype == IRCUR_F32)
+    IR_CUDA(launch_slab_sq<float>((const float*)c->D, c->ldd, c->row0, c->nloc, c->n2, I,
+                                  c->h_row_loc_cnt[set], J, c->h_col_cnt[set], nb_rows, nb_cols,
+                                  c->partials, c->stream));
+  else
+    IR_CUDA(launch_slab_sq<double>((const double*)c->D, c->ldd, c->row0, c->nloc, c->n2, I,
+                                   c->h_row_loc_cnt[set], J, c->h_col_cnt[set], nb_rows, nb_cols,
+                                   c->partials, c->stream));
+  std::vector<double> h(nb_rows + nb_cols);
+  IR_CUDA(cudaMemcpyAsync(h.data(), c->partials, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  double a = 0.0, b = 0.0;
+  for (int i = 0; i < nb_rows; ++i) a += h[i];
+  for (int i = 0; i < nb_cols; ++i) b += h[nb_rows + i];
+  if (rows_sq) *rows_sq = a;
+  if (cols_sq) *cols_sq = b;
+  return IRCUR_OK;
+}
+
+int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_iter, int* iterations,
+              int* converged, double* errors, float* iter_ms) {
+  if (!c || !c->D || !zetas) return fail(IRCUR_EINVAL, "null context, D or zetas");
+  if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
+  if (mode == IRCUR_RESAMPLED && c->n_sets < max_iter)
+    return fail(IRCUR_EINVAL, "resampled mode needs max_iter index sets");
+  if (c->n_sets < 1) return fail(IRCUR_EINVAL, "no index sets uploaded");
+  IR_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  // L_0 = 0: P_0 = Q_0 = 0 (solver.py:352-353)
+  IR_CUDA(cudaMemsetAsync(c->Pt[0], 0, (size_t)c->r * c->ldp * c->esz, st));
+  IR_CUDA(cudaMemsetAsync(c->Qt[0], 0, (size_t)c->r * c->ldq * c->esz, st));
+  IR_CUDA(cudaMemsetAsync(c->flags, 0, 16 * sizeof(int), st));
+  volatile int* hf = c->h_flags;
+  hf[0] = 0;
+  hf[1] = 0;
+  IR_CUDA(cudaEventRecord(c->ev[0], st));
+  constexpr int kAhead = 3;
+  int launched = 0;
+  while (true) {
+    const int seen = hf[1];
+    const bool fin = hf[0] != 0;
+    while (!fin && launched < max_iter && launched < seen + kAhead) {
+      const int set = mode == IRCUR_FIXED ? 0 : launched;
+      int rc = iteration(c, launched, set, zetas[launched], eps, max_iter, true);
+      if (rc) return rc;
+      IR_CUDA(cudaEventRecord(c->ev[launched + 1], st));
+      ++launched;
+    }
+    if (fin || launched == max_iter) break;
+    // spin until the device reports progress (mapped memory, no API sync)
+    const int before = seen;
+    while (hf[0] == 0 && hf[1] == before) {
+      cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) break;  // everything queued has finished
+      if (q != cudaErrorNotReady) return fail(IRCUR_ECUDA, std::string("stream: ") + cudaGetErrorString(q));
+    }
+  }
+  IR_CUDA(cudaStreamSynchronize(st));
+  int hflags[3] = {0, 0, 0};
+  IR_CUDA(cudaMemcpy(hflags, c->flags, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  const int iters = hflags[1];
+  if (iterations) *iterations = iters;
+  if (converged) *converged = hflags[2];
+  if (errors && iters > 0) IR_CUDA(cudaMemcpy(errors, c->errors, iters * sizeof(double), cudaMemcpyDeviceToHost));
+  if (iter_ms) {
+    for (int k = 0; k < iters; ++k) {
+      float ms = 0.f;
+      IR_CUDA(cudaEventElapsedTime(&ms, c->ev[k], c->ev[k + 1]));
+      iter_ms[k] = ms;
+    }
+  }
+  if (iters > 0) {
+    c->last_k = iters - 1;
+    c->last_set = mode == IRCUR_FIXED ? 0 : iters - 1;
+    c->last_zeta = zetas[iters - 1];
+    c->has_state = true;
+  }
+  return IRCUR_OK;
+}
+
+int ircur_iterate(ircur_ctx_t c, int k, int set, double zeta, double* e) {
+  if (!c || !c->D) return fail(IRCUR_EINVAL, "null context or D");
+  if (k < 0 || k >= c->max_iter || set < 0 || set >= c->n_sets) return fail(IRCUR_EINVAL, "bad k/set");
+  IR_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  if (k == 0) {
+    IR_CUDA(cudaMemsetAsync(c->Pt[0], 0, (size_t)c->r * c->ldp * c->esz, st));
+    IR_CUDA(cudaMemsetAsync(c->Qt[0], 0, (size_t)c->r * c->ldq * c->esz, st));
+  }
+  IR_CUDA(cudaMemsetAsync(c->flags, 0, 3 * sizeof(int), st));
+  int rc = iteration(c, k, set, zeta, 0.0, c->max_iter + 1, false);
+  if (rc) return rc;
+  double ek = 0.0;
+  IR_CUDA(cudaMemcpyAsync(&ek, c->errors + k, sizeof(double), cudaMemcpyDeviceToHost, st));
+  IR_CUDA(cudaStreamSynchronize(st));
+  if (e) *e = ek;
+  c->last_k = k;
+  c->last_set = set;
+  c->last_zeta = zeta;
+  c->has_state = true;
+  return IRCUR_OK;
+}
+
+int ircur_get_strips(ircur_ctx_t c, double* C, double* R, double* S_rows, double* S_cols) {
+  if (!c || !c->has_state) return fail(IRCUR_EINVAL, "no completed iteration");
+  IR_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const int set = c->last_set, old = c->last_k & 1;
+  const int mI = c->h_row_loc_cnt[set], nJ = c->h_col_cnt[set];
+  const size_t nr = (size_t)mI * c->n2, nc = (size_t)c->nloc * nJ;
+  double* out[4] = {C, R, S_rows, S_cols};
+  const size_t cnt[4] = {nc, nr, nr, nc};
+  double* dev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool tmp[4] = {false, false, false, false};
+  for (int q = 0; q < 4; ++q) {
+    if (!out[q] || cnt[q] == 0) continue;
+    cudaPointerAttributes at;
+    const bool is_dev = cudaPointerGetAttributes(&at, out[q]) == cudaSuccess &&
+                        (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    if (is_dev) {
+      dev[q] = out[q];
+    } else {
+      IR_CUDA(cudaMalloc(&dev[q], cnt[q] * sizeof(double)));
+      tmp[q] = true;
+    }
+  }
+  int rc = IRCUR_OK;
+  const int* I = c->d_rows + (size_t)set * c->max_rows + c->h_row_lo[set];
+  const int* J = c->d_cols + (size_t)set * c->max_cols;
+  auto run = [&](auto tag) -> cudaError_t {
+    using T = decltype(tag);
+    WriteoutArgs<T> w;
+    w.D = (const T*)c->D; w.ldd = c->ldd; w.row0 = c->row0; w.nloc = c->nloc; w.n2 = c->n2;
+    w.I = I; w.mI = mI; w.J = J; w.nJ = nJ;
+    w.Pt = (const T*)c->Pt[old]; w.ldp = c->ldp; w.Qt = (const T*)c->Qt[old]; w.ldq = c->ldq;
+    w.zt = storage_zeta<T>(c->last_zeta);
+    w.C = dev[0]; w.R = dev[1]; w.Srows = dev[2]; w.Scols = dev[3];
+    return launch_writeout<T>(w, c->r, st);
+  };
+  cudaError_t e = c->dtype == IRCUR_F32 ? run(float{}) : run(double{});
+  if (e != cudaSuccess) rc = fail(IRCUR_ECUDA, std::string("writeout: ") + cudaGetErrorString(e));
+  for (int q = 0; q < 4 && rc == IRCUR_OK; ++q) {
+    if (tmp[q]) {
+      e = cudaMemcpyAsync(out[q], dev[q], cnt[q] * sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) rc = fail(IRCUR_ECUDA, std::string("copy-out: ") + cudaGetErrorString(e));
+    }
+  }
+  cudaError_t se = cudaStreamSynchronize(st);
+  if (se != cudaSuccess && rc == IRCUR_OK) rc = fail(IRCUR_ECUDA, cudaGetErrorString(se));
+  for (int q = 0; q < 4; ++q)
+    if (tmp[q]) cudaFree(dev[q]);
+  return rc;
+}
+
+int ircur_get_core(ircur_ctx_t c, double* W, double* sigma, double* V, double* inv_sigma, int* k,
+                   int* n_rows, int* n_cols) {
+  if (!c || !c->has_state) return fail(IRCUR_EINVAL, "no completed iteration");
+  IR_CUDA(cudaSetDevice(c->device));
+  const int set = c->last_set;
+  const int mI = c->h_row_loc_cnt[set], nJ = c->h_col_cnt[set];
+  const int kk = std::min(c->r, std::min(mI, nJ));
+  if (k) *k = kk;
+  if (n_rows) *n_rows = mI;
+  if (n_cols) *n_cols = nJ;
+  const size_t R = (size_t)c->r;
+  if (W && kk > 0)
+    IR_CUDA(cudaMemcpy2DAsync(W, kk * sizeof(double), c->W, R * sizeof(double), kk * sizeof(double), mI,
+                              cudaMemcpyDefault, c->stream));
+  if (V && kk > 0)
+    IR_CUDA(cudaMemcpy2DAsync(V, kk * sizeof(double), c->V, R * sizeof(double), kk * sizeof(double), nJ,
+                              cudaMemcpyDefault, c->stream));
+  if (sigma && kk > 0) IR_CUDA(cudaMemcpyAsync(sigma, c->sigma, kk * sizeof(double), cudaMemcpyDefault, c->stream));
+  if (inv_sigma && kk > 0)
+    IR_CUDA(cudaMemcpyAsync(inv_sigma, c->inv, kk * sizeof(double), cudaMemcpyDefault, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  return IRCUR_OK;
+}
+
+int ircur_get_factors(ircur_ctx_t c, void* P, void* Q) {
+  if (!c || !c->has_state) return fail(IRCUR_EINVAL, "no completed iteration");
+  IR_CUDA(cudaSetDevice(c->device));
+  const int nw = (c->last_k & 1) ^ 1;
+  if (P)
+    IR_CUDA(cudaMemcpy2DAsync(P, c->nloc * c->esz, c->Pt[nw], c->ldp * c->esz, c->nloc * c->esz, c->r,
+                              cudaMemcpyDefault, c->stream));
+  if (Q)
+    IR_CUDA(cudaMemcpy2DAsync(Q, c->n2 * c->esz, c->Qt[nw], c->ldq * c->esz, c->n2 * c->esz, c->r,
+                              cudaMemcpyDefault, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  return IRCUR_OK;
+}
+
+int ircur_materialize(ircur_ctx_t c, void* L, int64_t ldl, int out_dtype) {
+  if (!c || !c->has_state || !L) return fail(IRCUR_EINVAL, "no completed iteration or null L");
+  if (ldl < c->n2) return fail(IRCUR_EINVAL, "ldl < n2");
+  IR_CUDA(cudaSetDevice(c->device));
+  const int nw = (c->last_k & 1) ^ 1;
+  cudaError_t e;
+  if (c->dtype == IRCUR_F32) {
+    if (out_dtype == IRCUR_F32)
+      e = launch_materialize<float, float>((const float*)c->Pt[nw], c->ldp, (const float*)c->Qt[nw], c->ldq,
+                                           c->nloc, c->n2, (float*)L, ldl, c->r, c->stream);
+    else
+      e = launch_materialize<float, double>((const float*)c->Pt[nw], c->ldp, (const float*)c->Qt[nw], c->ldq,
+                                            c->nloc, c->n2, (double*)L, ldl, c->r, c->stream);
+  } else {
+    if (out_dtype == IRCUR_F32)
+      e = launch_materialize<double, float>((const double*)c->Pt[nw], c->ldp, (const double*)c->Qt[nw],
+                                            c->ldq, c->nloc, c->n2, (float*)L, ldl, c->r, c->stream);
+    else
+      e = launch_materialize<double, double>((const double*)c->Pt[nw], c->ldp, (const double*)c->Qt[nw],
+                                             c->ldq, c->nloc, c->n2, (double*)L, ldl, c->r, c->stream);
+  }
+  if (e != cudaSuccess) return fail(IRCUR_ECUDA, std::string("materialize: ") + cudaGetErrorString(e));
+  return IRCUR_OK;
+}
+
+int ircur_materialize_factors(const void* Pt, int64_t ldp, const void* Q, int64_t ldq, int64_t nrows,
+                              int64_t n2, int rank, int dtype, void* L, int64_t ldl, int out_dtype,
+                              void* stream) {
+  if (!Pt || !Q || !L || rank < 1 || rank > kMaxRank || ldp < nrows || ldq < n2 || ldl < n2)
+    return fail(IRCUR_EINVAL, "bad materialize arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (dtype == IRCUR_F32) {
+    if (out_dtype == IRCUR_F32)
+      e = launch_materialize<float, float>((const float*)Pt, ldp, (const float*)Q, ldq, nrows, n2, (float*)L, ldl, rank, st);
+    else
+      e = launch_materialize<float, double>((const float*)Pt, ldp, (const float*)Q, ldq, nrows, n2, (double*)L, ldl, rank, st);
+  } else {
+    if (out_dtype == IRCUR_F32)
+      e = launch_materialize<double, float>((const double*)Pt, ldp, (const double*)Q, ldq, nrows, n2, (float*)L, ldl, rank, st);
+    else
+      e = launch_materialize<double, double>((const double*)Pt, ldp, (const double*)Q, ldq, nrows, n2, (double*)L, ldl, rank, st);
+  }
+  if (e != cudaSuccess) return fail(IRCUR_ECUDA, std::string("materialize: ") + cudaGetErrorString(e));
+  return IRCUR_OK;
+}
+
+int ircur_gen_baseline(void* D, int dtype, int64_t ldd, int64_t n1, int64_t n2, int64_t row0,
+                       int64_t nrows, int rank, const double* W, const double* V, double alpha,
+                       double amp_a, const uint64_t* pcg, double* max_abs_L, int64_t* qsum_abs_L,
+                       void* stream) {
+  if (!W || !V || !pcg || rank < 1 || n1 < 1 || n2 < 1 || row0 < 0 || nrows < 0 || row0 + nrows > n1)
+    return fail(IRCUR_EINVAL, "bad generator arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  GenArgs a;
+  a.D = D; a.dtype = dtype; a.ldd = ldd; a.n1 = n1; a.n2 = n2; a.row0 = row0; a.nrows = nrows;
+  a.rank = rank; a.W = W; a.V = V; a.alpha = alpha; a.amp_a = amp_a;
+  a.st0 = u128{pcg[0], pcg[1]};
+  a.inc = u128{pcg[2], pcg[3]};
+  a.stats_only = D == nullptr;
+  a.blk_max = nullptr;
+  a.blk_qsum = nullptr;
+  const int64_t nb = gen_blocks(nrows, n2);
+  if (a.stats_only && nb > 0) {
+    IR_CUDA(cudaMalloc(&a.blk_max, nb * sizeof(double)));
+    IR_CUDA(cudaMalloc(&a.blk_qsum, nb * sizeof(long long)));
+  }
+  cudaError_t e = launch_gen(a, nullptr, st);
+  int rc = IRCUR_OK;
+  if (e != cudaSuccess) rc = fail(IRCUR_ECUDA, std::string("gen: ") + cudaGetErrorString(e));
+  if (a.stats_only && nb > 0 && rc == IRCUR_OK) {
+    std::vector<double> hm(nb);
+    std::vector<long long> hq(nb);
+    cudaMemcpyAsync(hm.data(), a.blk_max, nb * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hq.data(), a.blk_qsum, nb * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(IRCUR_ECUDA, std::string("gen stats: ") + cudaGetErrorString(e));
+    double mx = 0.0;
+    long long q = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+      mx = std::max(mx, hm[b]);
+      q += hq[b];
+    }
+    if (max_abs_L) *max_abs_L = mx;
+    if (qsum_abs_L) *qsum_abs_L = q;
+  } else if (rc == IRCUR_OK) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(IRCUR_ECUDA, std::string("gen: ") + cudaGetErrorString(e));
+  }
+  if (a.blk_max) cudaFree(a.blk_max);
+  if (a.blk_qsum) cudaFree(a.blk_qsum);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// Per-iteration kernels of the IRCUR hot path (declarations + arg structs).
+#pragma once
+#include "ircur_common.cuh"
+
+namespace ircur {
+
+// ------------------------------------------------------------------ core
+// U = (D - T_zeta(D - L_k))(I, J) in fp64, plus the compact gathers
+// Pold_I (|I| x R) = P_k(I,:) and Qold_J (|J| x R) = Q_k(:,J)^T used by the
+// strip kernels.  Mirrors solver.py:375-382 restricted to I x J.
+template <typename T>
+struct CoreArgs {
+  const T* D; int64_t ldd; int64_t row0;      // local rows [row0, row0+nloc)
+  const int* I; int mI;                        // local sampled rows (global ids)
+  const int* J; int nJ;
+  const T* Pt; int64_t ldp;                    // P_k^T  (R x nloc)
+  const T* Qt; int64_t ldq;                    // Q_k^T  (R x n2)
+  T zt;
+  double* U; int ldu;                          // mI x nJ
+  T* PoldI; T* QoldJ;                          // mI x R, nJ x R
+  const int* done;
+};
+
+// ---------------------------------------------------------------- strips
+// One "strip" = a set of sampled lines (rows I of D, or columns J of D read
+// from the column-major copy) times every position along the other axis.
+// For each entry: l = <lineA[k], Bold[:,x]>, c = d - T_zeta(d - l)
+// (Phase I+II), the new factor Fnew[:,x] = sum_k lineW[k] c[k][x] (Q = W^T R
+// or P = C V Sigma^+), then the residual c - <lineRes[k], Fnew[:,x]> whose
+// squared norm, with ||d||^2, feeds e_k (solver.py:393-400).
+template <typename T>
+struct StripDesc {
+  const T* src; int64_t line_stride; int64_t pos_stride; int vec_ok;
+  const int* lines; int line_off; int nk;      // element (k, x) = src[(lines[k]-line_off)*line_stride + x*pos_stride]
+  int npos;
+  const T* lineA; const T* lineW; const T* lineRes;  // nk x R each
+  const T* Bold; int64_t ldb;                  // R x npos (padded ld)
+  T* Fnew; int64_t ldf;                        // R x npos
+  const int* other; int other_off; int nother; // sorted positions whose Fnew is fixed
+  const T* otherF;                             // nother x R
+  int tiles;                                   // ceil(npos / TX)
+};
+
+template <typename T>
+struct StripsArgs {
+  StripDesc<T> s[2];                           // [0] row strip, [1] column strip
+  T zt;
+  double* partials;                            // per CTA: {den, res}
+  const int* done;
+};
+
+// ------------------------------------------------------------- finalize
+struct FinalizeArgs {
+  const double* partials; int ncta_rows; int ncta_cols;
+  int k; double eps; int max_iter;
+  double* errors; int* done; int* iters; int* converged;
+  volatile int* host_done; volatile int* host_iters;   // mapped pinned memory (may be null)
+};
+
+// --------------------------------------------------------------- writeout
+template <typename T>
+struct WriteoutArgs {
+  const T* D; int64_t ldd; int64_t row0; int64_t nloc; int64_t n2;
+  const int* I; int mI; const int* J; int nJ;
+  const T* Pt; int64_t ldp; const T* Qt; int64_t ldq;
+  T zt;
+  double* C; double* R; double* Srows; double* Scols;   // device fp64, any may be null
+};
+
+}  // namespace ircur

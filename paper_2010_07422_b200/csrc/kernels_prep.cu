@@ -1,0 +1,321 @@
+// Per-solve passes over D and the BASELINE synthetic generator (sm_100a).
+//
+//   prep     : one read of D -> non-finite flag, max|D|, optional column-major
+//              copy Dt for the column strip (matcore.require_finite,
+//              matcore.py:70-77, and inf_norm, matcore.py:87-91).
+//   slab norm: ||D(I,:)||^2, ||D(:,J)||^2 for the den == 0 early exit
+//              (solver.py:331-341).
+//   generator: BASELINE.json configs — W V^T + Bernoulli/uniform outliers,
+//              drawing the SAME PCG64 stream numpy's Generator.random() /
+//              .uniform() would (see oracle.ircur_oracle.baseline_problem).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ircur_common.cuh"
+#include "launchers.cuh"
+#include <type_traits>
+
+namespace ircur {
+
+// ------------------------------------------------------------------- prep
+constexpr int kTT = 32;  // transpose tile
+
+template <typename T>
+__global__ void __launch_bounds__(256) prep_transpose_kernel(const T* __restrict__ D, int64_t ldd,
+                                                             int64_t nloc, int64_t n2, T* __restrict__ Dt,
+                                                             int64_t ldt, unsigned long long* maxbits,
+                                                             int* nonfinite) {
+  __shared__ T tile[kTT][kTT + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t cb = (int64_t)blockIdx.x * kTT, rb = (int64_t)blockIdx.y * kTT;
+  double mx = 0.0;
+  int bad = 0;
+#pragma unroll
+  for (int k = 0; k < kTT; k += 8) {
+    const int64_t r = rb + ty + k, c = cb + tx;
+    T v = T(0);
+    if (r < nloc && c < n2) {
+      v = __ldcs(D + r * ldd + c);
+      const double av = fabs((double)v);
+      if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
+    }
+    tile[ty + k][tx] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kTT; k += 8) {
+    const int64_t c = cb + ty + k, r = rb + tx;
+    if (r < nloc && c < n2) __stcs(Dt + c * ldt + r, tile[tx][ty + k]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if (tx == 0) {
+    if (mx > 0.0) atomicMax(maxbits, dbits(mx));
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) prep_scan_kernel(const T* __restrict__ D, int64_t ldd,
+                                                        int64_t nloc, int64_t n2,
+                                                        unsigned long long* maxbits, int* nonfinite) {
+  double mx = 0.0;
+  int bad = 0;
+  const int64_t total = nloc * n2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t r = e / n2, c = e - r * n2;
+    const double av = fabs((double)__ldcs(D + r * ldd + c));
+    if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mx > 0.0) atomicMax(maxbits, dbits(mx));
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
+// contiguous rows, 16-byte vector loads (ldd*sizeof(T) % 16 == 0, aligned base)
+template <typename T>
+__global__ void __launch_bounds__(256) prep_scan_vec_kernel(const T* __restrict__ D, int64_t ldd,
+                                                            int64_t nloc, int64_t n2,
+                                                            unsigned long long* maxbits, int* nonfinite) {
+  constexpr int VW = 16 / sizeof(T);
+  using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  double mx = 0.0;
+  int bad = 0;
+  const int64_t vpr = n2 / VW;  // full vectors per row
+  const int64_t total = nloc * vpr;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t r = e / vpr, cv = e - r * vpr;
+    const V4 v = __ldcs(reinterpret_cast<const V4*>(D + r * ldd) + cv);
+    const T* pv = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int u = 0; u < VW; ++u) {
+      const double av = fabs((double)pv[u]);
+      if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
+    }
+  }
+  // row tails
+  const int64_t tail = n2 - vpr * VW;
+  if (tail > 0) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * tail; e += stride) {
+      const int64_t r = e / tail, c = vpr * VW + (e - r * tail);
+      const double av = fabs((double)D[r * ldd + c]);
+      if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mx > 0.0) atomicMax(maxbits, dbits(mx));
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
+template <typename T>
+cudaError_t launch_prep(const T* D, int64_t ldd, int64_t nloc, int64_t n2, T* Dt, int64_t ldt,
+                        unsigned long long* maxbits, int* nonfinite, int num_sms, cudaStream_t st) {
+  if (nloc == 0 || n2 == 0) return cudaSuccess;
+  if (Dt) {
+    dim3 grid((unsigned)((n2 + kTT - 1) / kTT), (unsigned)((nloc + kTT - 1) / kTT));
+    prep_transpose_kernel<T><<<grid, 256, 0, st>>>(D, ldd, nloc, n2, Dt, ldt, maxbits, nonfinite);
+  } else {
+    const int64_t total = nloc * n2;
+    int64_t want = (total + 256 * 8 - 1) / (256 * 8);
+    const int64_t cap = (int64_t)num_sms * 8;
+    const unsigned blocks = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
+    const bool vec = ((ldd * (int64_t)sizeof(T)) % 16 == 0) && ((uintptr_t)D % 16 == 0);
+    if (vec)
+      prep_scan_vec_kernel<T><<<blocks, 256, 0, st>>>(D, ldd, nloc, n2, maxbits, nonfinite);
+    else
+      prep_scan_kernel<T><<<blocks, 256, 0, st>>>(D, ldd, nloc, n2, maxbits, nonfinite);
+  }
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------- slab norms
+// partials[blockIdx.x] = sum of squares of this CTA's share; rows part uses
+// blocks [0, nb_rows), cols part blocks [nb_rows, nb_rows + nb_cols).
+template <typename T>
+__global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, int64_t row0, int64_t nloc,
+                                                      int64_t n2, const int* I, int mI, const int* J,
+                                                      int nJ, int nb_rows, double* partials) {
+  __shared__ double sh[8];
+  double acc = 0.0;
+  if ((int)blockIdx.x < nb_rows) {
+    const int64_t total = (int64_t)mI * n2;
+    for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)nb_rows * 256) {
+      const int64_t k = e / n2, x = e - k * n2;
+      const double v = (double)D[((int64_t)I[k] - row0) * ldd + x];
+      acc = fma(v, v, acc);
+    }
+  } else {
+    const int nb_cols = gridDim.x - nb_rows;
+    const int64_t total = nloc * nJ;
+    for (int64_t e = (int64_t)(blockIdx.x - nb_rows) * 256 + threadIdx.x; e < total;
+         e += (int64_t)nb_cols * 256) {
+      const int64_t x = e / nJ, k = e - x * nJ;
+      const double v = (double)D[x * ldd + J[k]];
+      acc = fma(v, v, acc);
+    }
+  }
+  const double s = block_sum<256>(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+template <typename T>
+cudaError_t launch_slab_sq(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2,
+                           const int* I, int mI, const int* J, int nJ, int nb_rows, int nb_cols,
+                           double* partials, cudaStream_t st) {
+  slab_sq_kernel<T><<<nb_rows + nb_cols, 256, 0, st>>>(D, ldd, row0, nloc, n2, I, mI, J, nJ, nb_rows,
+                                                       partials);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------- generator
+// numpy PCG64 (XSL-RR 128/64): state' = state * M + inc; out = rotr(hi^lo, state'>>122)
+__device__ __forceinline__ u128 mul128(u128 a, u128 b) {
+  u128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+  return r;
+}
+__device__ __forceinline__ u128 add128(u128 a, u128 b) {
+  u128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+  return r;
+}
+__device__ __constant__ u128 kPcgMult = {4865540595714422341ull, 2549297995355413924ull};
+
+// advance the LCG by `delta` steps (Brown's algorithm, O(log delta))
+__device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
+  u128 acc_mult = {1ull, 0ull}, acc_plus = {0ull, 0ull};
+  u128 cur_mult = kPcgMult, cur_plus = inc;
+  while (delta > 0) {
+    if (delta & 1ull) {
+      acc_mult = mul128(acc_mult, cur_mult);
+      acc_plus = add128(mul128(acc_plus, cur_mult), cur_plus);
+    }
+    cur_plus = mul128(add128(cur_mult, u128{1ull, 0ull}), cur_plus);
+    cur_mult = mul128(cur_mult, cur_mult);
+    delta >>= 1;
+  }
+  return add128(mul128(acc_mult, state), acc_plus);
+}
+__device__ __forceinline__ uint64_t pcg_next(u128& st, u128 inc) {
+  st = add128(mul128(st, kPcgMult), inc);
+  const uint64_t x = st.hi ^ st.lo;
+  const unsigned rot = (unsigned)(st.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+__device__ __forceinline__ double pcg_double(u128& st, u128 inc) {
+  return (double)(pcg_next(st, inc) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+constexpr int kGenNT = 256;
+constexpr int kGenPer = 16;  // consecutive cells per thread
+
+// L_ij accumulated exactly as the numpy restatement: W[:,0]*V[:,0], then
+// + W[:,t]*V[:,t] (separate multiply and add, no FMA).
+__device__ __forceinline__ double gen_L(const double* W, const double* V, int rank, int64_t i, int64_t j) {
+  double l = __dmul_rn(W[i * rank], V[j * rank]);
+  for (int t = 1; t < rank; ++t) l = __dadd_rn(l, __dmul_rn(W[i * rank + t], V[j * rank + t]));
+  return l;
+}
+
+__global__ void __launch_bounds__(kGenNT) gen_kernel(GenArgs a) {
+  __shared__ double shm[kGenNT / 32];
+  __shared__ long long shq[kGenNT / 32];
+  const int64_t cells = a.nrows * a.n2;
+  const int64_t first = ((int64_t)blockIdx.x * kGenNT + threadIdx.x) * kGenPer;
+  double mx = 0.0;
+  long long q = 0;
+  if (first < cells) {
+    const int64_t gfirst = a.row0 * a.n2 + first;  // global row-major cell id
+    const int64_t total = a.n1 * a.n2;
+    u128 sm = a.st0, sv = a.st0;
+    if (!a.stats_only) {
+      sm = pcg_advance(a.st0, a.inc, (uint64_t)gfirst);
+      sv = pcg_advance(a.st0, a.inc, (uint64_t)(total + gfirst));
+    }
+    const double A = a.amp_a;
+    const double span = A - (-A);
+    const int64_t last = min(cells, first + kGenPer);
+    for (int64_t e = first; e < last; ++e) {
+      const int64_t il = e / a.n2, j = e - il * a.n2;
+      const double l = gen_L(a.W, a.V, a.rank, a.row0 + il, j);
+      if (a.stats_only) {
+        const double al = fabs(l);
+        mx = fmax(mx, al);
+        q += (long long)rint(al * 16777216.0);
+      } else {
+        const double um = pcg_double(sm, a.inc);
+        const double uv = pcg_double(sv, a.inc);
+        const double s = (um < a.alpha) ? __dadd_rn(-A, __dmul_rn(span, uv)) : 0.0;
+        const double d = __dadd_rn(l, s);
+        if (a.dtype == 0)
+          reinterpret_cast<float*>(a.D)[il * a.ldd + j] = (float)d;
+        else
+          reinterpret_cast<double*>(a.D)[il * a.ldd + j] = d;
+      }
+    }
+  }
+  if (a.stats_only) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      q += __shfl_xor_sync(0xffffffffu, q, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      shm[threadIdx.x >> 5] = mx;
+      shq[threadIdx.x >> 5] = q;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m2 = 0.0;
+      long long q2 = 0;
+      for (int i = 0; i < kGenNT / 32; ++i) {
+        m2 = fmax(m2, shm[i]);
+        q2 += shq[i];
+      }
+      a.blk_max[blockIdx.x] = m2;
+      a.blk_qsum[blockIdx.x] = q2;
+    }
+  }
+}
+
+cudaError_t launch_gen(const GenArgs& a, int64_t* nblocks_out, cudaStream_t st) {
+  const int64_t cells = a.nrows * a.n2;
+  const int64_t nb = (cells + (int64_t)kGenNT * kGenPer - 1) / ((int64_t)kGenNT * kGenPer);
+  if (nblocks_out) *nblocks_out = nb;
+  if (nb == 0) return cudaSuccess;
+  gen_kernel<<<(unsigned)nb, kGenNT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+int64_t gen_blocks(int64_t nrows, int64_t n2) {
+  const int64_t cells = nrows * n2;
+  return (cells + (int64_t)kGenNT * kGenPer - 1) / ((int64_t)kGenNT * kGenPer);
+}
+
+#define IRCUR_PREP_INST(T)                                                                       \
+  template cudaError_t launch_prep<T>(const T*, int64_t, int64_t, int64_t, T*, int64_t,          \
+                                      unsigned long long*, int*, int, cudaStream_t);              \
+  template cudaError_t launch_slab_sq<T>(const T*, int64_t, int64_t, int64_t, int64_t, const int*, \
+                                         int, const int*, int, int, int, double*, cudaStream_t);
+IRCUR_PREP_INST(float)
+IRCUR_PREP_INST(double)
+
+}  // namespace ircur

@@ -1,0 +1,60 @@
+// Host-visible launcher declarations for the IRCUR kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels_iter.cuh"
+
+namespace ircur {
+
+struct u128 {
+  uint64_t lo, hi;
+};
+
+// Core SVD/pinv arguments (kernels_svd.cu).
+struct SvdArgs {
+  const double* U; int ldu;       // m x n core (row-major)
+  const double* G; int ldg;       // n x n Gram scratch (written by gram_kernel)
+  int m, n, r, kk;
+  const void* warm; int warm_ld; int warm_cols;  // n x warm_cols start block (storage type) or null
+  double* W; double* sigma; double* V; double* inv;  // fp64 outputs: m x r, r, n x r, r
+  void* Wr; void* PI; void* VS; void* QJ;            // storage-type strip inputs: m x r, m x r, n x r, n x r
+  double* scratch;                // n x 32 doubles
+  const int* done;
+  int* steps_out;
+  double tol; int maxsteps;
+  uint64_t salt;
+};
+
+struct GenArgs {
+  void* D; int dtype; int64_t ldd; int64_t n1, n2, row0, nrows; int rank;
+  const double* W; const double* V;
+  double alpha, amp_a;
+  u128 st0, inc;
+  double* blk_max; long long* blk_qsum;
+  int stats_only;
+};
+
+template <typename T> cudaError_t launch_core(const CoreArgs<T>& a, int R, cudaStream_t st);
+template <typename T> size_t strips_smem_bytes(int R);
+template <typename T> cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, cudaStream_t st);
+int strips_lines_per_cta();
+int strips_tx();
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
+template <typename T, typename O>
+cudaError_t launch_materialize(const T* Pt, int64_t ldp, const T* Qt, int64_t ldq, int64_t nloc,
+                               int64_t n2, O* L, int64_t ldl, int R, cudaStream_t st);
+template <typename T>
+cudaError_t launch_prep(const T* D, int64_t ldd, int64_t nloc, int64_t n2, T* Dt, int64_t ldt,
+                        unsigned long long* maxbits, int* nonfinite, int num_sms, cudaStream_t st);
+template <typename T>
+cudaError_t launch_slab_sq(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2,
+                           const int* I, int mI, const int* J, int nJ, int nb_rows, int nb_cols,
+                           double* partials, cudaStream_t st);
+size_t svd_smem_bytes(int n, int m, int kk, int cs);
+template <typename T> cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st);
+cudaError_t launch_gen(const GenArgs& a, int64_t* nblocks_out, cudaStream_t st);
+int64_t gen_blocks(int64_t nrows, int64_t n2);
+
+}  // namespace ircur

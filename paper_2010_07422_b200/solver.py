@@ -1,0 +1,389 @@
+"""`solve(D, config, observer=None)` on a B200 — drop-in for `ircur.solver.solve`.
+
+Reference: /root/reference/pkg/src/ircur/solver.py:304-416.  The Python
+layer keeps the reference's signature, types, draw order, threshold schedule
+and error behaviour; every arithmetic step of the loop runs in
+libircur_b200.so (sm_100a kernels) through the C-ABI in
+include/ircur_b200.h:
+
+    require_finite / inf_norm  (matcore.py:70-91)   -> ircur_prepare
+    pre-loop den == 0 check    (solver.py:331-341)  -> ircur_slab_sqnorms
+    loop body + stop rule      (solver.py:358-414)  -> ircur_run / ircur_iterate
+    returned C, R, S strips    (solver.py:375-391)  -> ircur_get_strips
+    PinvFactor of the core     (matcore.py:142-165) -> ircur_get_core
+    materialize                (solver.py:211-213)  -> ircur_materialize_factors
+
+PyTorch provides device memory and the CUDA stream only.  There is no CPU
+fallback: without a CUDA device or without the built library, solve raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from collections import OrderedDict
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _capi
+from .sampling import IndexSet, draw_index_sets, sample_count
+from .types import CurFactors, PinvFactor, SolverConfig, SolverTrace, SparseEstimate
+
+__all__ = ["solve", "solve_device", "materialize", "materialize_device", "threshold_at",
+           "Context", "DeviceResult"]
+
+
+def threshold_at(config: SolverConfig, k: int) -> float:
+    """gamma**k * zeta0 (solver.py:171-177)."""
+    if k < 0:
+        raise ValueError(f"k must be >= 0, got {k}")
+    if config.zeta0 is None:
+        raise ValueError("config.zeta0 is unresolved (None)")
+    return config.gamma**k * config.zeta0
+
+
+# --------------------------------------------------------------- context
+def _ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+class Context:
+    """One libircur_b200 solver context (device workspace + stream)."""
+
+    def __init__(self, device: int, dtype: int, n1: int, n2: int, rank: int, max_rows: int,
+                 max_cols: int, max_iter: int, row0: int = 0, local_rows: int | None = None,
+                 stream: int | None = None):
+        self.lib = _capi.load()
+        self.device, self.dtype, self.n1, self.n2, self.rank = device, dtype, n1, n2, rank
+        self.max_rows, self.max_cols, self.max_iter = max_rows, max_cols, max_iter
+        self.row0 = row0
+        self.local_rows = n1 if local_rows is None else local_rows
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device).cuda_stream
+        h = C.c_void_p()
+        _capi.check(self.lib.ircur_ctx_create(C.byref(h), device, dtype, n1, n2, rank, max_rows,
+                                              max_cols, max_iter, row0, self.local_rows,
+                                              C.c_void_p(self.stream)))
+        self.h = h
+        self._D = None
+        self.sets: list = []
+        self.colmajor = False
+
+    def close(self) -> None:
+        if self.h is not None and self.h.value:
+            self.lib.ircur_ctx_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prepare(self, D: torch.Tensor, colmajor: bool) -> float:
+        self._D = D
+        self.colmajor = bool(colmajor)
+        ok = C.c_int(0)
+        mx = C.c_double(0.0)
+        _capi.check(self.lib.ircur_prepare(self.h, C.c_void_p(_ptr(D)), D.stride(0), int(colmajor),
+                                           C.byref(ok), C.byref(mx)))
+        return float(mx.value)
+
+    def set_indices(self, sets) -> None:
+        n = len(sets)
+        rows = np.zeros((n, self.max_rows), dtype=np.int64)
+        cols = np.zeros((n, self.max_cols), dtype=np.int64)
+        rc = np.zeros(n, dtype=np.int32)
+        cc = np.zeros(n, dtype=np.int32)
+        for s, (I, J) in enumerate(sets):
+            rows[s, :I.size] = I
+            cols[s, :J.size] = J
+            rc[s], cc[s] = I.size, J.size
+        p64 = C.POINTER(C.c_int64)
+        p32 = C.POINTER(C.c_int32)
+        _capi.check(self.lib.ircur_set_indices(self.h, n, rows.ctypes.data_as(p64), rc.ctypes.data_as(p32),
+                                               cols.ctypes.data_as(p64), cc.ctypes.data_as(p32)))
+        self.sets = sets
+
+    def slab_sqnorms(self, s: int) -> tuple[float, float]:
+        a, b = C.c_double(), C.c_double()
+        _capi.check(self.lib.ircur_slab_sqnorms(self.h, s, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def run(self, zetas, eps: float, mode: int, max_iter: int):
+        z = np.ascontiguousarray(zetas, dtype=np.float64)
+        errors = np.zeros(max_iter, dtype=np.float64)
+        ms = np.zeros(max_iter, dtype=np.float32)
+        it, conv = C.c_int(0), C.c_int(0)
+        pd = C.POINTER(C.c_double)
+        _capi.check(self.lib.ircur_run(self.h, z.ctypes.data_as(pd), eps, mode, max_iter, C.byref(it),
+                                       C.byref(conv), errors.ctypes.data_as(pd),
+                                       ms.ctypes.data_as(C.POINTER(C.c_float))))
+        n = it.value
+        return n, bool(conv.value), errors[:n], ms[:n]
+
+    def iterate(self, k: int, s: int, zeta: float) -> float:
+        e = C.c_double()
+        _capi.check(self.lib.ircur_iterate(self.h, k, s, zeta, C.byref(e)))
+        return e.value
+
+    def strips(self, set_idx: int, on_device: bool = False):
+        I, J = self.sets[set_idx]
+        mI = int(np.count_nonzero((I >= self.row0) & (I < self.row0 + self.local_rows)))
+        nJ = J.size
+        shapes = [(self.local_rows, nJ), (mI, self.n2), (mI, self.n2), (self.local_rows, nJ)]
+        if on_device:
+            outs = [torch.empty(s, dtype=torch.float64, device=f"cuda:{self.device}") for s in shapes]
+            ptrs = [C.c_void_p(_ptr(t)) for t in outs]
+        else:
+            outs = [np.empty(s, dtype=np.float64) for s in shapes]
+            ptrs = [C.c_void_p(o.ctypes.data) for o in outs]
+        _capi.check(self.lib.ircur_get_strips(self.h, *ptrs))
+        return outs  # C, R, S_rows, S_cols
+
+    def core(self):
+        k, m, n = C.c_int(), C.c_int(), C.c_int()
+        _capi.check(self.lib.ircur_get_core(self.h, None, None, None, None, C.byref(k), C.byref(m), C.byref(n)))
+        k, m, n = k.value, m.value, n.value
+        W = np.zeros((m, k)); V = np.zeros((n, k)); s = np.zeros(k); inv = np.zeros(k)
+        vp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+        _capi.check(self.lib.ircur_get_core(self.h, vp(W), vp(s), vp(V), vp(inv), None, None, None))
+        return W, s, V, inv
+
+    def factors(self):
+        tdt = torch.float32 if self.dtype == _capi.F32 else torch.float64
+        dev = f"cuda:{self.device}"
+        Pt = torch.empty((self.rank, self.local_rows), dtype=tdt, device=dev)
+        Qt = torch.empty((self.rank, self.n2), dtype=tdt, device=dev)
+        _capi.check(self.lib.ircur_get_factors(self.h, C.c_void_p(_ptr(Pt)), C.c_void_p(_ptr(Qt))))
+        return Pt, Qt
+
+
+_CACHE: "OrderedDict[tuple, Context]" = OrderedDict()
+_CACHE_MAX = 4
+
+
+def _context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream) -> Context:
+    key = (device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream)
+    ctx = _CACHE.get(key)
+    if ctx is not None:
+        _CACHE.move_to_end(key)
+        return ctx
+    while len(_CACHE) >= _CACHE_MAX:
+        _, old = _CACHE.popitem(last=False)
+        old.close()
+    try:
+        ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream=stream)
+    except MemoryError:
+        for _, old in _CACHE.items():
+            old.close()
+        _CACHE.clear()
+        torch.cuda.empty_cache()
+        ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream=stream)
+    _CACHE[key] = ctx
+    return ctx
+
+
+def clear_cache() -> None:
+    for _, ctx in _CACHE.items():
+        ctx.close()
+    _CACHE.clear()
+
+
+# ------------------------------------------------------------ device input
+def _device_matrix(D, device, compute_dtype) -> torch.Tensor:
+    """D as a row-major CUDA tensor in the storage/compute dtype (fp32 stays
+    fp32, everything else becomes fp64 as in matcore.require_finite)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2010_07422_b200.solve needs a CUDA device (no CPU fallback)")
+    if isinstance(D, torch.Tensor):
+        t = D
+    else:
+        a = np.asarray(D)
+        if a.dtype != np.float32:
+            a = np.asarray(a, dtype=np.float64)
+        t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.ndim != 2:
+        raise ValueError(f"expected a 2-D matrix, got ndim={t.ndim}")
+    want = compute_dtype
+    if want is None:
+        want = torch.float32 if t.dtype == torch.float32 else torch.float64
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+    t = t.to(device=dev, dtype=want)
+    if t.numel() and (t.stride(1) != 1 or t.stride(0) < t.shape[1]):
+        t = t.contiguous()
+    return t
+
+
+def _want_colmajor(colmajor, n1, n2, m_cols, dtype_size, mode) -> bool:
+    env = os.environ.get("IRCUR_COLMAJOR")
+    if env is not None:
+        return env not in ("0", "false", "False", "")
+    if colmajor != "auto":
+        return bool(colmajor)
+    # copy costs one extra write of D; without it every iteration reads the
+    # column strip in 32-byte sectors (32/s x amplification).
+    amp = 32 // dtype_size
+    expected_iters = 25
+    return n2 * dtype_size < expected_iters * m_cols * dtype_size * (amp - 1) * 0.5
+
+
+@dataclass
+class DeviceHandle:
+    """Final rank-r factors on the device: L = P Q with P^T (r x n1) and Q (r x n2)."""
+
+    Pt: torch.Tensor
+    Qt: torch.Tensor
+    dtype: int
+
+
+@dataclass
+class DeviceResult:
+    trace: SolverTrace
+    cfg: SolverConfig
+    ctx: Context | None
+    rows: IndexSet
+    cols: IndexSet
+    handle: DeviceHandle | None
+    zero_state: bool = False
+
+
+def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
+                 colmajor="auto", fetch_factors=True) -> DeviceResult:
+    """Run the loop on the device; results stay on the device (see solve)."""
+    cfg = config
+    Dd = _device_matrix(D, device, compute_dtype)
+    if Dd.numel() == 0:
+        raise ValueError("D must be nonempty")
+    n1, n2 = int(Dd.shape[0]), int(Dd.shape[1])
+    dev = Dd.device.index
+    dtype = _capi.F32 if Dd.dtype == torch.float32 else _capi.F64
+    m_rows = sample_count(n1, cfg.rank, cfg.c_rows)
+    m_cols = sample_count(n2, cfg.rank, cfg.c_cols)
+    resampled = cfg.mode == "resampled"
+    n_sets = cfg.max_iter if resampled else 1
+    sets = draw_index_sets(n1, n2, m_rows, m_cols, cfg.seed, n_sets)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
+    cm = _want_colmajor(colmajor, n1, n2, m_cols, Dd.element_size(), cfg.mode)
+    max_abs = ctx.prepare(Dd, cm)  # ValueError on NaN/Inf (matcore.py:75-76)
+    ctx.set_indices(sets)
+    rows0, cols0 = sets[0]
+    a, b = ctx.slab_sqnorms(0)
+    trace = SolverTrace()
+    if np.sqrt(a) + np.sqrt(b) == 0.0:
+        # solver.py:335-341: sampled slabs identically zero
+        trace.errors.append(0.0)
+        trace.converged = True
+        return DeviceResult(trace, cfg, None, IndexSet(rows0, n1), IndexSet(cols0, n2), None, True)
+    if cfg.zeta0 is None:
+        cfg = replace(cfg, zeta0=max_abs)  # solver.py:342-344
+    zetas = [cfg.gamma**k * cfg.zeta0 for k in range(cfg.max_iter)]
+    mode = _capi.RESAMPLED if resampled else _capi.FIXED
+    if observer is None:
+        iters, conv, errors, ms = ctx.run(zetas, cfg.eps, mode, cfg.max_iter)
+        trace.errors = [float(e) for e in errors]
+        trace.seconds = [float(t) / 1e3 for t in ms]
+    else:
+        iters, conv = 0, False
+        for k in range(cfg.max_iter):
+            s = k if resampled else 0
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            e = ctx.iterate(k, s, zetas[k])
+            ev1.record()
+            ev1.synchronize()
+            iters = k + 1
+            trace.errors.append(float(e))
+            trace.seconds.append(ev0.elapsed_time(ev1) / 1e3)
+            cur, sparse = _host_results(ctx, s, n1, n2, None)
+            observer(k + 1, zetas[k], cur, sparse, float(e))
+            if e <= cfg.eps:
+                conv = True
+                break
+    trace.iterations = iters
+    trace.converged = conv
+    trace.thresholds = zetas[:iters]
+    trace.allocated = [0] * iters
+    last = (iters - 1) if resampled else 0
+    trace.sampled_rows = [int(sets[k if resampled else 0][0].size) for k in range(iters)]
+    trace.sampled_cols = [int(sets[k if resampled else 0][1].size) for k in range(iters)]
+    I, J = sets[last]
+    handle = None
+    if fetch_factors:
+        Pt, Qt = ctx.factors()
+        handle = DeviceHandle(Pt, Qt, dtype)
+    return DeviceResult(trace, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), handle)
+
+
+def _host_results(ctx: Context, set_idx: int, n1: int, n2: int, handle):
+    I, J = ctx.sets[set_idx]
+    Cm, Rm, Sr, Sc = ctx.strips(set_idx)
+    W, s, V, inv = ctx.core()
+    rows, cols = IndexSet(I, n1), IndexSet(J, n2)
+    cur = CurFactors(C=Cm, core_pinv=PinvFactor(W=W, sigma=s, V=V, inv_sigma=inv), R=Rm, rows=rows,
+                     cols=cols, device=handle)
+    return cur, SparseEstimate(Sr, Sc, rows, cols)
+
+
+def _zero_results(n1, n2, rows: IndexSet, cols: IndexSet, rank: int):
+    """_zero_state (solver.py:283-301): L_0 = 0, S_0 = 0 in factor form."""
+    m, n = rows.size, cols.size
+    k = min(rank, m, n)
+    W = np.eye(m, k)
+    V = np.eye(n, k)
+    z = np.zeros(k)
+    cur = CurFactors(C=np.zeros((n1, n)), core_pinv=PinvFactor(W, z.copy(), V, z.copy()),
+                     R=np.zeros((m, n2)), rows=rows, cols=cols, device=None)
+    return cur, SparseEstimate(np.zeros((m, n2)), np.zeros((n1, n)), rows, cols)
+
+
+def solve(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
+          colmajor="auto"):
+    """Drop-in for ircur.solver.solve (solver.py:304-416).
+
+    Returns (CurFactors, SparseEstimate, SolverTrace) with float64 host
+    arrays.  Extra keyword arguments (not in the reference): `device` (CUDA
+    ordinal), `compute_dtype` (torch dtype; default keeps fp32 input in fp32
+    and runs everything else in fp64) and `colmajor` (build the column-major
+    copy of D used by the column-strip kernel: True/False/"auto").
+    """
+    res = solve_device(D, config, observer, device=device, compute_dtype=compute_dtype,
+                       colmajor=colmajor)
+    n1, n2 = res.rows.bound, res.cols.bound
+    if res.zero_state:
+        cur, sparse = _zero_results(n1, n2, res.rows, res.cols, config.rank)
+        return cur, sparse, res.trace
+    last = (res.trace.iterations - 1) if res.cfg.mode == "resampled" else 0
+    cur, sparse = _host_results(res.ctx, last, n1, n2, res.handle)
+    return cur, sparse, res.trace
+
+
+# ------------------------------------------------------------ materialise
+def materialize_device(cur_or_handle, out_dtype=torch.float64) -> torch.Tensor:
+    """Full L = C U^+ R = P Q streamed by the K=rank writer (solver.py:211-213)."""
+    h = cur_or_handle.device if isinstance(cur_or_handle, CurFactors) else cur_or_handle
+    if h is None:
+        raise ValueError("CurFactors carry no device factors (zero state or foreign object)")
+    lib = _capi.load()
+    r, n1 = h.Pt.shape
+    n2 = h.Qt.shape[1]
+    L = torch.empty((n1, n2), dtype=out_dtype, device=h.Pt.device)
+    od = _capi.F32 if out_dtype == torch.float32 else _capi.F64
+    stream = torch.cuda.current_stream(h.Pt.device).cuda_stream
+    _capi.check(lib.ircur_materialize_factors(C.c_void_p(_ptr(h.Pt)), h.Pt.stride(0),
+                                              C.c_void_p(_ptr(h.Qt)), h.Qt.stride(0), n1, n2, r,
+                                              h.dtype, C.c_void_p(_ptr(L)), L.stride(0), od,
+                                              C.c_void_p(stream)))
+    return L
+
+
+def materialize(cur: CurFactors) -> np.ndarray:
+    """Dense L as a float64 host array (test scale), like the reference."""
+    if cur.device is None:
+        if not cur.C.any() and not cur.R.any():
+            return np.zeros(cur.shape)
+        raise ValueError("CurFactors carry no device factors")
+    return materialize_device(cur, torch.float64).cpu().numpy()

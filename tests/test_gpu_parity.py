@@ -1,0 +1,131 @@
+"""GPU parity: the B200 solve (through the C-ABI) vs the reference's golden
+vectors and the CPU oracle, on the same seeded inputs.
+
+fp64 inputs run fp64 kernels and must match to 1e-9 (relative Frobenius for
+C, R, S strips and W Sigma V^T; relative for e_k), with identical index
+sets, thresholds, iteration counts and convergence flags — the tolerance
+BASELINE.json's north_star states.  fp32 inputs run fp32 strip kernels
+against the reference's fp64 arithmetic on the same fp32 values: 1e-4
+relative Frobenius on L/S (north_star), iteration count within one.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_names, load_golden, solver_kwargs
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-9
+TOL32 = 1e-4
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def ir():
+    import paper_2010_07422_b200 as m
+    from paper_2010_07422_b200 import _build
+    _build.build()
+    return m
+
+
+def _cfg(ir, meta):
+    kw = solver_kwargs(meta)
+    seed = kw.pop("seed", 0)
+    return ir.SolverConfig(seed=ir.RngSeed(seed), **kw)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_solve_matches_reference_golden(ir, name):
+    D, meta, g = load_golden(name)
+    cur, sparse, trace = ir.solve(D, _cfg(ir, meta), device=0)
+    f32 = D.dtype == np.float32
+    tol = TOL32 if f32 else TOL64
+    if f32:
+        assert abs(trace.iterations - meta["iterations"]) <= 1
+    else:
+        assert trace.iterations == meta["iterations"]
+        assert trace.converged == meta["converged"]
+        np.testing.assert_array_equal(cur.rows.indices, g["rows"])
+        np.testing.assert_array_equal(cur.cols.indices, g["cols"])
+        assert trace.thresholds == list(g["thresholds"])
+        e = np.asarray(trace.errors)
+        ref_e = g["errors"]
+        assert np.all(np.abs(e - ref_e) <= TOL64 * np.abs(ref_e) + 1e-14), (e, ref_e)
+    if meta["iterations"] == 0:
+        assert trace.errors == [0.0]
+        return
+    if trace.iterations != meta["iterations"]:
+        return  # fp32 stopped one iteration apart: strips belong to different k
+    for key, mine in (("C", cur.C), ("R", cur.R), ("S_rows", sparse.row_values),
+                      ("S_cols", sparse.col_values)):
+        assert rel(mine, g[key]) <= tol, (key, rel(mine, g[key]))
+    assert rel(cur.core_pinv.sigma, g["sigma"]) <= tol
+    mine_core = (cur.core_pinv.W * cur.core_pinv.sigma) @ cur.core_pinv.V.T
+    ref_core = (g["W"] * g["sigma"]) @ g["V"].T
+    assert rel(mine_core, ref_core) <= tol
+    np.testing.assert_array_equal(cur.core_pinv.inv_sigma > 0, g["inv_sigma"] > 0)
+
+
+def test_intersection_blocks_agree_bitwise(ir):
+    # SparseEstimate invariant (solver.py:117-129; test_solver.py:169-177)
+    D, meta, g = load_golden("bl_sq200_r5_resampled")
+    seen = []
+
+    def obs(k, zeta, cur, sparse, e):
+        a = sparse.row_values[:, sparse.cols.indices]
+        b = sparse.col_values[sparse.rows.indices, :]
+        seen.append(np.array_equal(a, b) and np.array_equal(cur.R[:, cur.cols.indices],
+                                                            cur.C[cur.rows.indices, :]))
+
+    cfg = _cfg(ir, meta)
+    _, _, trace = ir.solve(D, cfg, observer=obs, device=0)
+    assert seen and all(seen)
+    assert trace.iterations == meta["iterations"]
+
+
+@pytest.mark.parametrize("mode", ["fixed", "resampled"])
+def test_bitwise_run_to_run_determinism(ir, mode):
+    from oracle.ircur_oracle import baseline_problem
+    D = baseline_problem(180, 170, 4, 0.15, 3)[0]
+    cfg = ir.SolverConfig(rank=4, gamma=0.7, mode=mode, seed=ir.RngSeed(4))
+    a = ir.solve(D, cfg, device=0)
+    b = ir.solve(D, cfg, device=0)
+    assert a[2].errors == b[2].errors
+    np.testing.assert_array_equal(a[0].C, b[0].C)
+    np.testing.assert_array_equal(a[0].R, b[0].R)
+    np.testing.assert_array_equal(a[1].row_values, b[1].row_values)
+    np.testing.assert_array_equal(a[1].col_values, b[1].col_values)
+
+
+def test_nonfinite_rejected(ir):
+    D = np.ones((40, 30))
+    D[3, 4] = np.nan
+    with pytest.raises(ValueError):
+        ir.solve(D, ir.SolverConfig(rank=2), device=0)
+    D[3, 4] = np.inf
+    with pytest.raises(ValueError):
+        ir.solve(D.astype(np.float32), ir.SolverConfig(rank=2), device=0)
+
+
+def test_colmajor_copy_and_strided_paths_agree(ir):
+    from oracle.ircur_oracle import baseline_problem
+    D = baseline_problem(150, 130, 3, 0.1, 8)[0]
+    cfg = ir.SolverConfig(rank=3, gamma=0.7, mode="resampled", seed=ir.RngSeed(9))
+    a = ir.solve(D, cfg, device=0, colmajor=True)
+    b = ir.solve(D, cfg, device=0, colmajor=False)
+    assert a[2].errors == b[2].errors
+    np.testing.assert_array_equal(a[0].C, b[0].C)
+
+
+def test_materialize_matches_oracle(ir):
+    from oracle import ircur_oracle as orc
+    D, meta, g = load_golden("bl_sq120_r3_resampled")
+    cur, _, _ = ir.solve(D, _cfg(ir, meta), device=0)
+    L_ref = orc.materialize(g["C"], g["V"], g["inv_sigma"], g["W"], g["R"])
+    assert rel(ir.materialize(cur), L_ref) <= TOL64
