@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""IRCUR time-to-tol benchmark on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
+    python bench.py --impl reference ...      # reference CPU path (oracle port)
+
+One step = one complete IRCUR solve to tol 1e-5 (prep pass over D, index
+draws, the device-resident loop, final factors) on a synthetic problem of
+the BASELINE.json shape, generated on the device with the same PCG64 stream
+numpy would use.  Prints ONE JSON line (rank 0).
+
+Timing: W warm-up solves, then K timed solves bracketed by barrier +
+cuda.synchronize, CUDA events on the solver stream, max over ranks.  D
+(>= 400 MB) is larger than the 126 MB L2, so no flush is needed between
+steps.  The strip kernel is timed live with CUDA events recorded around it
+on its own stream inside the timed region (roofline.achieved).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (n1, n2, rank, alpha, dtype, BASELINE.json configs index)
+    "cfg1": (1000, 1000, 5, 0.1, "f64", 0),
+    "cfg2": (10000, 10000, 5, 0.2, "f32", 1),
+    "cfg2f64": (10000, 10000, 5, 0.2, "f64", 1),
+    "cfg5": (100000, 100000, 10, 0.2, "f32", 4),
+}
+DATA_SEED = 0
+SOLVER_SEED = 1
+GAMMA = 0.7
+EPS = 1e-5
+MAX_ITER = 100
+METRIC = "IRCUR time-to-tol=1e-5 (n=1e4..1e5) & strip-kernel HBM GB/s vs B200 peak"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="resampled", choices=["fixed", "resampled"])
+    ap.add_argument("--colmajor", default="auto")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_strip_bytes(s: int, n1: int, n2: int, r: int, mI: int, nJ: int) -> int:
+    """one read of each sampled strip + read/write of P, Q."""
+    return s * (mI * n2 + n1 * nJ) + 2 * s * r * (n1 + n2)
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_07422_b200 as ir
+    from paper_2010_07422_b200 import _build, gen
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2010_07422_b200 import dist as irdist
+        return irdist.bench_sharded(args, CONFIGS, rank, world, local)
+    _build.build()
+    n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
+    tdt = torch.float32 if dts == "f32" else torch.float64
+    s = 4 if dts == "f32" else 8
+    D, linf, a = gen.baseline_problem_device(n1, n2, r, alpha, DATA_SEED, dtype=tdt)
+    cfg = ir.SolverConfig(rank=r, eps=EPS, zeta0=linf, gamma=GAMMA, mode=args.mode,
+                          max_iter=MAX_ITER, seed=ir.RngSeed(SOLVER_SEED))
+    cm = args.colmajor if args.colmajor == "auto" else args.colmajor in ("1", "true", "True")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        res = ir.solve_device(D, cfg, colmajor=cm, profile=True)
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            results.append(ir.solve_device(D, cfg, colmajor=cm, profile=True))
+        stop.record(stream)
+        torch.cuda.synchronize()
+    total_ms = start.elapsed_time(stop)
+    ms_per_step = total_ms / args.steps
+    res = results[-1]
+    iters = res.trace.iterations
+    # roofline of the dominant kernel (fused strips), from the live events
+    strip_ms, strip_bytes, launches = 0.0, 0, 0
+    svd_ms = core_ms = 0.0
+    for rr in results:
+        p = rr.profile
+        for k in range(rr.trace.iterations):
+            strip_ms += float(p["strips_ms"][k])
+            svd_ms += float(p["svd_ms"][k])
+            core_ms += float(p["core_ms"][k])
+            strip_bytes += algorithmic_strip_bytes(s, n1, n2, r, rr.trace.sampled_rows[k],
+                                                   rr.trace.sampled_cols[k])
+        launches += 2 + p["kernel_launches"]  # prep + slab norm + 5 per launched iteration
+    n_strip = sum(rr.trace.iterations for rr in results)
+    peak, peak_kind = peaks()
+    achieved = strip_bytes / (strip_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "strips_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.config)
+    line = {
+        "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if dts == "f32" else "f64",
+        "data": "synthetic (BASELINE.json generator on device, numpy-PCG64-exact)",
+        "config": {"workload": args.config, "n1": n1, "n2": n2, "rank": r, "alpha": alpha,
+                   "mode": args.mode, "gamma": GAMMA, "eps": EPS, "zeta0": "max|L|",
+                   "iterations": iters, "converged": res.trace.converged,
+                   "final_e": res.trace.errors[-1], "colmajor_copy": bool(res.colmajor),
+                   "l2": "inputs larger than L2 (D >= 400 MB), no flush",
+                   "parallelism": "single GPU"},
+        "breakdown_ms_per_solve": {
+            "strips": strip_ms / len(results), "svd": svd_ms / len(results),
+            "core": core_ms / len(results),
+            "other": ms_per_step - (strip_ms + svd_ms + core_ms) / len(results)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "strips_kernel", "avg_launch_us": strip_ms / n_strip * 1e3,
+                     "bytes_per_launch": strip_bytes / n_strip},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    # end to end through the public API from pinned host memory
+    if args.e2e_steps > 0:
+        Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
+        Dh.copy_(D)
+        del D, results, res
+        ir.clear_cache()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        ir.solve(Dh, cfg, colmajor=cm)  # warm (allocations, context)
+        times = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cur, sparse, trace = ir.solve(Dh, cfg, colmajor=cm)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        d2h = 8 * (cur.C.size + cur.R.size + sparse.row_values.size + sparse.col_values.size
+                   + cur.core_pinv.W.size + cur.core_pinv.V.size) + 8 * len(trace.errors)
+        line["e2e"] = {"value": float(np.mean(times)), "unit": "s", "h2d_bytes_per_step": int(Dh.numel() * s),
+                       "d2h_bytes_per_step": int(d2h), "api": "paper_2010_07422_b200.solve(pinned host D)"}
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(Dh.numpy(), args.config, cfg, iters, args.cpu_budget)
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- CPU oracle
+def cpu_baseline(Dh, config, cfg, gpu_iters, budget):
+    """Reference algorithm (oracle port, fp64 arithmetic like the reference)
+    on this host's cores.  Small problems: full solves.  n = 1e5: a bounded
+    sample (first iterations + a slice of the finite/upcast pass), scaled."""
+    from oracle import ircur_oracle as orc
+
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [d.get("num_threads") for d in threadpool_info()]
+    except Exception:
+        blas = []
+    cores = os.cpu_count()
+    n1, n2 = Dh.shape
+    kw = dict(rank=cfg.rank, eps=cfg.eps, zeta0=cfg.zeta0, gamma=cfg.gamma, mode=cfg.mode,
+              max_iter=cfg.max_iter, seed=SOLVER_SEED)
+    t0 = time.perf_counter()
+    if n1 * n2 <= 2e8:
+        res = orc.solve(Dh, **kw)
+        tt = time.perf_counter() - t0
+        return {"value": tt, "unit": "s", "cores": cores, "kind": "port", "blas_threads": blas,
+                "sample": f"one full oracle solve ({res.iterations} iterations, converged={res.converged})"}
+    # bounded sample: finite+upcast pass on a row slice, first iterations
+    rows = max(1, n1 // 100)
+    ts = time.perf_counter()
+    np.isfinite(np.asarray(Dh[:rows], dtype=np.float64)).all()
+    t_prep = (time.perf_counter() - ts) * (n1 / rows)
+    times = []
+
+    def on_iter(k, sec):
+        times.append(sec)
+        return sum(times) >= budget or len(times) >= 3
+
+    orc.solve(Dh, upcast=False, on_iter=on_iter, **kw)
+    per_iter = float(np.mean(times[1:] if len(times) > 1 else times))
+    est = t_prep + times[0] + per_iter * (gpu_iters - 1)
+    return {"value": est, "unit": "s", "cores": cores, "kind": "port", "blas_threads": blas,
+            "sample": (f"extrapolated: fp64 finite/upcast pass timed on {rows} of {n1} rows "
+                       f"({t_prep:.1f} s scaled), {len(times)} oracle iterations timed "
+                       f"({per_iter:.2f} s/iter after the first), x{gpu_iters} iterations")}
+
+
+def run_reference(args):
+    """`--impl reference`: the reference algorithm on this host's CPU cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ircur_oracle as orc
+
+    n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
+    dt = np.float32 if dts == "f32" else np.float64
+    D, linf, a = orc.baseline_problem_blocked(n1, n2, r, alpha, DATA_SEED, dtype=dt)
+
+    class Cfg:  # the solver settings of our arm
+        rank, eps, zeta0, gamma, mode, max_iter = r, EPS, linf, GAMMA, args.mode, MAX_ITER
+
+    expected_iters = 23  # this generator family converges in 22-24 iterations
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(D, args.config, Cfg, expected_iters, args.cpu_budget)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = float(np.mean(vals))
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64 arithmetic on " + dts + " data",
+            "data": "synthetic (BASELINE.json generator, numpy PCG64)",
+            "config": {"workload": args.config, "n1": n1, "n2": n2, "rank": r, "alpha": alpha,
+                       "mode": args.mode, "gamma": GAMMA, "eps": EPS},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

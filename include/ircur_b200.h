@@ -119,6 +119,15 @@ int ircur_get_factors(ircur_ctx_t ctx, void* P, void* Q);
  * with a K=rank streaming writer. */
 int ircur_materialize(ircur_ctx_t ctx, void* L, int64_t ldl, int out_dtype);
 
+/* Measurement hooks for bench.py: per-phase CUDA events recorded on the
+ * context stream around core | SVD | strips | stop-check of each iteration
+ * (ircur_set_profiling), read back as per-iteration milliseconds, plus the
+ * number of iterations launched and kernels launched by the last ircur_run. */
+int ircur_set_profiling(ircur_ctx_t ctx, int on);
+int ircur_get_profile(ircur_ctx_t ctx, int n_iters, int* launched_iters,
+                      long long* kernel_launches, float* core_ms, float* svd_ms,
+                      float* strips_ms, float* finalize_ms);
+
 /* Stateless variant: stream L = P Q from caller-held factors Pt (rank x
  * nrows, row stride ldp) and Q (rank x n2, row stride ldq), dtype
  * IRCUR_F32/F64, into L (nrows x n2, ldl) in out_dtype. */

@@ -129,21 +129,33 @@ def _eval_cols(C, W, V, inv, R, cols):
 
 
 def solve(D, rank, eps=1e-5, zeta0=None, gamma=0.65, c_rows=4.0, c_cols=4.0,
-          mode="fixed", max_iter=200, seed=0, stream=0) -> OracleResult:
+          mode="fixed", max_iter=200, seed=0, stream=0, upcast=True,
+          on_iter=None) -> OracleResult:
     """Algorithm 1 exactly as the reference loop runs it (solver.py:304-416),
-    in float64 regardless of D's dtype (matcore.require_finite, :70-77)."""
-    D = np.asarray(D, dtype=np.float64)
+    in float64 regardless of D's dtype (matcore.require_finite, :70-77).
+
+    upcast=False keeps a float32 D as is and upcasts each gathered strip
+    instead (the same fp64 values; used only to time bounded CPU samples of
+    matrices whose fp64 copy would not fit in host memory).  on_iter(k,
+    seconds) is called after every iteration; returning True stops the loop
+    (bounded timing samples)."""
+    import time as _time
+    if upcast:
+        D = np.asarray(D, dtype=np.float64)
+    else:
+        D = np.asarray(D)
     if D.ndim != 2:
         raise ValueError("expected a 2-D matrix")
-    if not np.isfinite(D).all():
+    if upcast and not np.isfinite(D).all():
         raise ValueError("matrix contains non-finite entries")
     if D.size == 0:
         raise ValueError("D must be nonempty")
     n1, n2 = D.shape
+    f64 = lambda a: np.asarray(a, dtype=np.float64)  # noqa: E731
     sets = index_stream(n1, n2, rank, c_rows, c_cols, mode, max_iter, seed, stream)
     rows, cols = sets[0]
-    d_rows = D[rows, :]
-    d_cols = D[:, cols]
+    d_rows = f64(D[rows, :])
+    d_cols = f64(D[:, cols])
     den = frob(d_rows) + frob(d_cols)
     res = OracleResult(None, None, None, None, None, None, None, None, rows, cols)
     if den == 0.0:  # solver.py:335-341 / _zero_state :283-301
@@ -161,10 +173,11 @@ def solve(D, rank, eps=1e-5, zeta0=None, gamma=0.65, c_rows=4.0, c_cols=4.0,
     l_cols = np.zeros((n1, cols.size))
     fac = None
     for k in range(max_iter):
+        t0 = _time.perf_counter()
         if mode == "resampled" and k > 0:  # solver.py:362-370
             rows, cols = sets[k]
-            d_rows = D[rows, :]
-            d_cols = D[:, cols]
+            d_rows = f64(D[rows, :])
+            d_cols = f64(D[:, cols])
             den = frob(d_rows) + frob(d_cols)
             C, W, V, inv, R = fac
             l_rows = _eval_rows(C, W, V, inv, R, rows)
@@ -192,6 +205,8 @@ def solve(D, rank, eps=1e-5, zeta0=None, gamma=0.65, c_rows=4.0, c_cols=4.0,
         res.rows, res.cols = rows, cols
         if e <= eps:
             res.converged = True
+            break
+        if on_iter is not None and on_iter(k, _time.perf_counter() - t0):
             break
     return res
 
@@ -228,6 +243,57 @@ def baseline_problem(n1: int, n2: int, rank: int, alpha: float, seed: int,
     S = np.where(mask, vals, 0.0)
     D = L + S
     return D, L, S, float(np.abs(L).max())
+
+
+def _L_rows(W, V, r0, r1):
+    L = W[r0:r1, 0:1] * V[:, 0][None, :]
+    for t in range(1, W.shape[1]):
+        L = L + W[r0:r1, t:t + 1] * V[:, t][None, :]
+    return L
+
+
+def baseline_problem_blocked(n1: int, n2: int, rank: int, alpha: float, seed: int,
+                             amp: float = 10.0, dtype=np.float64, block_rows: int = 256,
+                             threads: int | None = None):
+    """Same D as baseline_problem (bit for bit, then cast to `dtype`), built
+    in row blocks with PCG64.advance so large matrices (n = 1e5) fit in host
+    memory and generate on all cores.  Returns D, max|L|, a."""
+    import concurrent.futures as cf
+    import os as _os
+    rng = np.random.default_rng(seed)
+    W = rng.standard_normal((n1, rank))
+    V = rng.standard_normal((n2, rank))
+    state = rng.bit_generator.state
+    blocks = [(r0, min(n1, r0 + block_rows)) for r0 in range(0, n1, block_rows)]
+    nt = threads or (_os.cpu_count() or 1)
+
+    def stats(b):
+        L = _L_rows(W, V, *b)
+        return float(np.abs(L).max()), int(np.rint(np.abs(L) * 16777216.0).astype(np.int64).sum())
+
+    with cf.ThreadPoolExecutor(nt) as ex:
+        st = list(ex.map(stats, blocks))
+    linf = max(s[0] for s in st)
+    q = sum(s[1] for s in st)
+    a = float(q) / 16777216.0 / (n1 * n2)
+    A = amp * a
+    D = np.empty((n1, n2), dtype=dtype)
+
+    def fill(b):
+        r0, r1 = b
+        g1 = np.random.PCG64()
+        g1.state = state
+        g1.advance(r0 * n2)
+        mask = np.random.Generator(g1).random((r1 - r0, n2)) < alpha
+        g2 = np.random.PCG64()
+        g2.state = state
+        g2.advance(n1 * n2 + r0 * n2)
+        vals = np.random.Generator(g2).uniform(-A, A, size=(r1 - r0, n2))
+        D[r0:r1] = _L_rows(W, V, r0, r1) + np.where(mask, vals, 0.0)
+
+    with cf.ThreadPoolExecutor(nt) as ex:
+        list(ex.map(fill, blocks))
+    return D, linf, a
 
 
 def mean_abs_quantised(L: np.ndarray) -> float:

@@ -39,6 +39,8 @@ PROTOTYPES = [
     ("ircur_get_core", _i, [_vp, _vp, _vp, _vp, _vp, _pi, _pi, _pi]),
     ("ircur_get_factors", _i, [_vp, _vp, _vp]),
     ("ircur_materialize", _i, [_vp, _vp, _i64, _i]),
+    ("ircur_set_profiling", _i, [_vp, _i]),
+    ("ircur_get_profile", _i, [_vp, _i, _pi, C.POINTER(C.c_longlong), _pf, _pf, _pf, _pf]),
     ("ircur_materialize_factors", _i, [_vp, _i64, _vp, _i64, _i64, _i64, _i, _i, _vp, _i64, _i, _vp]),
     ("ircur_gen_baseline", _i, [_vp, _i, _i64, _i64, _i64, _i64, _i64, _i, _vp, _vp, _d, _d,
                                 _pu64, _pd, _pi64, _vp]),

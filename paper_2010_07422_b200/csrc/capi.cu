@@ -78,6 +78,11 @@ struct ircur_ctx {
   int* h_flags = nullptr;  // mapped pinned: [0]=done [1]=iters
   int* h_flags_dev = nullptr;
   std::vector<cudaEvent_t> ev;
+  // optional per-phase profiling: events [k][0..4] around core | svd | strips | finalize
+  bool profiling = false;
+  std::vector<cudaEvent_t> evp;
+  int launched_iters = 0;
+  long long kernel_launches = 0;
   int strips_cs = 1;
   // last completed iteration
   int last_k = -1, last_set = 0;
@@ -131,7 +136,10 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   ca.Qt = (const T*)c->Qt[old]; ca.ldq = c->ldq;
   ca.zt = zt; ca.U = c->U; ca.ldu = c->max_cols;
   ca.PoldI = (T*)c->PoldI; ca.QoldJ = (T*)c->QoldJ; ca.done = done;
+  cudaEvent_t* pe = c->profiling ? &c->evp[(size_t)k * 5] : nullptr;
+  if (pe) IR_CUDA(cudaEventRecord(pe[0], st));
   IR_CUDA(launch_core<T>(ca, R, st));
+  if (pe) IR_CUDA(cudaEventRecord(pe[1], st));
 
   SvdArgs sa;
   sa.U = c->U; sa.ldu = c->max_cols; sa.G = c->G; sa.ldg = c->max_cols;
@@ -146,6 +154,7 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   sa.salt = 0x1234567ull + (uint64_t)k * 7919ull;
   const int svd_cs = svd_cluster_size(nJ, mI, sa.kk);
   IR_CUDA(launch_svd<T>(sa, svd_cs, st));
+  if (pe) IR_CUDA(cudaEventRecord(pe[2], st));
 
   StripsArgs<T> pa;
   const int TX = strips_tx();
@@ -171,6 +180,7 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   cs.tiles = (int)((c->nloc + TX - 1) / TX);
   pa.zt = zt; pa.partials = c->partials; pa.done = done;
   IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, st));
+  if (pe) IR_CUDA(cudaEventRecord(pe[3], st));
 
   FinalizeArgs fa;
   fa.partials = c->partials;
@@ -181,6 +191,9 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   fa.host_done = host_flags ? c->h_flags_dev : nullptr;
   fa.host_iters = host_flags ? c->h_flags_dev + 1 : nullptr;
   IR_CUDA(launch_finalize(fa, st));
+  if (pe) IR_CUDA(cudaEventRecord(pe[4], st));
+  c->kernel_launches += 5;  // core, gram, svd, strips, finalize
+  ++c->launched_iters;
   return IRCUR_OK;
 }
 
@@ -283,6 +296,8 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
   for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->evp)
     if (e) cudaEventDestroy(e);
   delete c;
   return IRCUR_OK;
@@ -420,6 +435,8 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   hf[0] = 0;
   hf[1] = 0;
   IR_CUDA(cudaEventRecord(c->ev[0], st));
+  c->launched_iters = 0;
+  c->kernel_launches = 0;
   constexpr int kAhead = 3;
   int launched = 0;
   while (true) {
@@ -599,6 +616,36 @@ int ircur_materialize(ircur_ctx_t c, void* L, int64_t ldl, int out_dtype) {
                                              c->ldq, c->nloc, c->n2, (double*)L, ldl, c->r, c->stream);
   }
   if (e != cudaSuccess) return fail(IRCUR_ECUDA, std::string("materialize: ") + cudaGetErrorString(e));
+  return IRCUR_OK;
+}
+
+int ircur_set_profiling(ircur_ctx_t c, int on) {
+  if (!c) return fail(IRCUR_EINVAL, "null context");
+  IR_CUDA(cudaSetDevice(c->device));
+  if (on && c->evp.empty()) {
+    c->evp.resize((size_t)c->max_iter * 5);
+    for (auto& e : c->evp) IR_CUDA(cudaEventCreate(&e));
+  }
+  c->profiling = on != 0;
+  return IRCUR_OK;
+}
+
+int ircur_get_profile(ircur_ctx_t c, int n_iters, int* launched_iters, long long* kernel_launches,
+                      float* core_ms, float* svd_ms, float* strips_ms, float* finalize_ms) {
+  if (!c) return fail(IRCUR_EINVAL, "null context");
+  if (launched_iters) *launched_iters = c->launched_iters;
+  if (kernel_launches) *kernel_launches = c->kernel_launches;
+  if (!c->profiling || n_iters <= 0) return IRCUR_OK;
+  IR_CUDA(cudaSetDevice(c->device));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < n_iters && k < c->max_iter; ++k) {
+    float t[4] = {0, 0, 0, 0};
+    for (int q = 0; q < 4; ++q) IR_CUDA(cudaEventElapsedTime(&t[q], c->evp[(size_t)k * 5 + q], c->evp[(size_t)k * 5 + q + 1]));
+    if (core_ms) core_ms[k] = t[0];
+    if (svd_ms) svd_ms[k] = t[1];
+    if (strips_ms) strips_ms[k] = t[2];
+    if (finalize_ms) finalize_ms[k] = t[3];
+  }
   return IRCUR_OK;
 }
 

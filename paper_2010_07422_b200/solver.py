@@ -151,6 +151,19 @@ class Context:
         _capi.check(self.lib.ircur_get_core(self.h, vp(W), vp(s), vp(V), vp(inv), None, None, None))
         return W, s, V, inv
 
+    def set_profiling(self, on: bool) -> None:
+        _capi.check(self.lib.ircur_set_profiling(self.h, int(on)))
+
+    def profile(self, n_iters: int) -> dict:
+        li, kl = C.c_int(), C.c_longlong()
+        arrs = [np.zeros(max(n_iters, 1), dtype=np.float32) for _ in range(4)]
+        pf = C.POINTER(C.c_float)
+        _capi.check(self.lib.ircur_get_profile(self.h, n_iters, C.byref(li), C.byref(kl),
+                                               *[a.ctypes.data_as(pf) for a in arrs]))
+        return dict(launched_iters=li.value, kernel_launches=kl.value,
+                    core_ms=arrs[0][:n_iters], svd_ms=arrs[1][:n_iters],
+                    strips_ms=arrs[2][:n_iters], finalize_ms=arrs[3][:n_iters])
+
     def factors(self):
         tdt = torch.float32 if self.dtype == _capi.F32 else torch.float64
         dev = f"cuda:{self.device}"
@@ -247,10 +260,13 @@ class DeviceResult:
     cols: IndexSet
     handle: DeviceHandle | None
     zero_state: bool = False
+    profile: dict | None = None
+    colmajor: bool = False
+    sets: list | None = None
 
 
 def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
-                 colmajor="auto", fetch_factors=True) -> DeviceResult:
+                 colmajor="auto", fetch_factors=True, profile=False) -> DeviceResult:
     """Run the loop on the device; results stay on the device (see solve)."""
     cfg = config
     Dd = _device_matrix(D, device, compute_dtype)
@@ -281,8 +297,12 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
         cfg = replace(cfg, zeta0=max_abs)  # solver.py:342-344
     zetas = [cfg.gamma**k * cfg.zeta0 for k in range(cfg.max_iter)]
     mode = _capi.RESAMPLED if resampled else _capi.FIXED
+    ctx.set_profiling(profile)
+    prof = None
     if observer is None:
         iters, conv, errors, ms = ctx.run(zetas, cfg.eps, mode, cfg.max_iter)
+        if profile:
+            prof = ctx.profile(iters)
         trace.errors = [float(e) for e in errors]
         trace.seconds = [float(t) / 1e3 for t in ms]
     else:
@@ -315,7 +335,11 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     if fetch_factors:
         Pt, Qt = ctx.factors()
         handle = DeviceHandle(Pt, Qt, dtype)
-    return DeviceResult(trace, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), handle)
+    res = DeviceResult(trace, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), handle)
+    res.profile = prof
+    res.colmajor = cm
+    res.sets = sets
+    return res
 
 
 def _host_results(ctx: Context, set_idx: int, n1: int, n2: int, handle):
