@@ -128,6 +128,10 @@ int ircur_get_profile(ircur_ctx_t ctx, int n_iters, int* launched_iters,
                       long long* kernel_launches, float* core_ms, float* svd_ms,
                       float* strips_ms, float* finalize_ms);
 
+/* Subspace-iteration steps the core SVD needed in each of the first n_iters
+ * iterations of the last run (diagnostics). */
+int ircur_get_svd_steps(ircur_ctx_t ctx, int n_iters, int* steps);
+
 /* Stateless variant: stream L = P Q from caller-held factors Pt (rank x
  * nrows, row stride ldp) and Q (rank x n2, row stride ldq), dtype
  * IRCUR_F32/F64, into L (nrows x n2, ldl) in out_dtype. */

@@ -73,7 +73,8 @@ struct ircur_ctx {
   double* partials = nullptr;
   int max_partials = 0;
   double* errors = nullptr;
-  int* flags = nullptr;  // [0]=done [1]=iters [2]=converged [3]=nonfinite [4]=svd steps
+  int* flags = nullptr;  // [0]=done [1]=iters [2]=converged [3]=nonfinite
+  int* svd_steps = nullptr;  // subspace steps taken by the core SVD, per iteration
   unsigned long long* maxbits = nullptr;
   int* h_flags = nullptr;  // mapped pinned: [0]=done [1]=iters
   int* h_flags_dev = nullptr;
@@ -148,7 +149,7 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   sa.warm = k > 0 ? c->QoldJ : nullptr; sa.warm_ld = R; sa.warm_cols = k > 0 ? R : 0;
   sa.W = c->W; sa.sigma = c->sigma; sa.V = c->V; sa.inv = c->inv;
   sa.Wr = c->Wr; sa.PI = c->PI; sa.VS = c->VS; sa.QJ = c->QJ;
-  sa.scratch = c->svd_scratch; sa.done = done; sa.steps_out = c->flags + 4;
+  sa.scratch = c->svd_scratch; sa.done = done; sa.steps_out = c->svd_steps + k;
   sa.tol = sizeof(T) == 8 ? 2e-14 : 1e-11;
   sa.maxsteps = 100;
   sa.salt = 0x1234567ull + (uint64_t)k * 7919ull;
@@ -274,6 +275,7 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->partials, (size_t)c->max_partials * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->errors, (size_t)max_iter * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->flags, 16 * sizeof(int)));
+  IR_CUDA_C(cudaMalloc(&c->svd_steps, (size_t)max_iter * sizeof(int)));
   IR_CUDA_C(cudaMalloc(&c->maxbits, sizeof(unsigned long long)));
   IR_CUDA_C(cudaHostAlloc(&c->h_flags, 16 * sizeof(int), cudaHostAllocMapped));
   IR_CUDA_C(cudaHostGetDevicePointer((void**)&c->h_flags_dev, c->h_flags, 0));
@@ -291,7 +293,7 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U,
                   c->PoldI, c->QoldJ, c->Wr, c->PI, c->VS, c->QJ, c->W, c->sigma, c->V, c->inv,
-                  c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits};
+                  c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -646,6 +648,14 @@ int ircur_get_profile(ircur_ctx_t c, int n_iters, int* launched_iters, long long
     if (strips_ms) strips_ms[k] = t[2];
     if (finalize_ms) finalize_ms[k] = t[3];
   }
+  return IRCUR_OK;
+}
+
+int ircur_get_svd_steps(ircur_ctx_t c, int n_iters, int* steps) {
+  if (!c || !steps || n_iters < 0 || n_iters > c->max_iter) return fail(IRCUR_EINVAL, "bad arguments");
+  IR_CUDA(cudaSetDevice(c->device));
+  IR_CUDA(cudaMemcpyAsync(steps, c->svd_steps, n_iters * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
   return IRCUR_OK;
 }
 

@@ -107,6 +107,11 @@ __device__ void jacobi_eig(SvdSmem& S, int kk) {
   const int np = (kk + 1) / 2;
   const int nply = 2 * np;  // even number of players
   __syncthreads();
+  // rotation threshold: absolute, a few ulps of the largest diagonal entry
+  // (a relative test on tiny/zero eigenvalues never settles under round-off)
+  double scale = 0.0;
+  for (int i = 0; i < kk; ++i) scale = fmax(scale, fabs(S.H[i * kHLd + i]));
+  const double thr = 4e-16 * scale;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (tid == 0) S.flags[0] = 0;
     __syncthreads();
@@ -120,7 +125,7 @@ __device__ void jacobi_eig(SvdSmem& S, int kk) {
         if (q < kk) {
           const double hpq = S.H[p * kHLd + q];
           const double hpp = S.H[p * kHLd + p], hqq = S.H[q * kHLd + q];
-          if (fabs(hpq) > 1e-300 && fabs(hpq) > 1e-16 * sqrt(fabs(hpp) * fabs(hqq))) {
+          if (fabs(hpq) > 1e-300 && fabs(hpq) > thr) {
             const double tau = (hqq - hpp) / (2.0 * hpq);
             const double t = fabs(tau) > 1e150 ? 0.5 / tau
                                                : (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));

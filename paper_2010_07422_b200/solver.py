@@ -160,7 +160,9 @@ class Context:
         pf = C.POINTER(C.c_float)
         _capi.check(self.lib.ircur_get_profile(self.h, n_iters, C.byref(li), C.byref(kl),
                                                *[a.ctypes.data_as(pf) for a in arrs]))
-        return dict(launched_iters=li.value, kernel_launches=kl.value,
+        steps = np.zeros(max(n_iters, 1), dtype=np.int32)
+        _capi.check(self.lib.ircur_get_svd_steps(self.h, n_iters, steps.ctypes.data_as(C.POINTER(C.c_int))))
+        return dict(launched_iters=li.value, kernel_launches=kl.value, svd_steps=steps[:n_iters],
                     core_ms=arrs[0][:n_iters], svd_ms=arrs[1][:n_iters],
                     strips_ms=arrs[2][:n_iters], finalize_ms=arrs[3][:n_iters])
 

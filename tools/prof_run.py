@@ -1,0 +1,34 @@
+"""Run solves of a bench config (for ncu captures / per-iteration breakdowns).
+
+    python tools/prof_run.py cfg5 [--colmajor 0|1] [--solves 2] [--detail]
+"""
+import argparse, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np, torch
+import bench
+import paper_2010_07422_b200 as ir
+from paper_2010_07422_b200 import gen
+
+ap = argparse.ArgumentParser()
+ap.add_argument("config"); ap.add_argument("--colmajor", default="auto")
+ap.add_argument("--solves", type=int, default=2); ap.add_argument("--detail", action="store_true")
+ap.add_argument("--mode", default="resampled")
+a = ap.parse_args()
+n1, n2, r, alpha, dts, _ = bench.CONFIGS[a.config]
+tdt = torch.float32 if dts == "f32" else torch.float64
+D, linf, amp = gen.baseline_problem_device(n1, n2, r, alpha, bench.DATA_SEED, dtype=tdt)
+cfg = ir.SolverConfig(rank=r, eps=bench.EPS, zeta0=linf, gamma=bench.GAMMA, mode=a.mode,
+                      max_iter=bench.MAX_ITER, seed=ir.RngSeed(bench.SOLVER_SEED))
+cm = a.colmajor if a.colmajor == "auto" else a.colmajor == "1"
+for i in range(a.solves):
+    st = torch.cuda.Event(enable_timing=True); en = torch.cuda.Event(enable_timing=True)
+    st.record(); res = ir.solve_device(D, cfg, colmajor=cm, profile=True); en.record(); en.synchronize()
+    p = res.profile
+    print(f"solve {i}: {st.elapsed_time(en):.2f} ms, iters {res.trace.iterations}, colmajor {res.colmajor}, "
+          f"strips {p['strips_ms'].sum():.2f} svd {p['svd_ms'].sum():.2f} core {p['core_ms'].sum():.2f} "
+          f"fin {p['finalize_ms'].sum():.2f} ms", flush=True)
+    if a.detail and i == a.solves - 1:
+        for k in range(res.trace.iterations):
+            print(f"  k={k:2d} e={res.trace.errors[k]:.3e} svd_steps={p['svd_steps'][k]:3d} svd={p['svd_ms'][k]:.3f} "
+                  f"strips={p['strips_ms'][k]:.3f} core={p['core_ms'][k]:.3f} ms")
