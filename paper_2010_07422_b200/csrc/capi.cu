@@ -108,11 +108,7 @@ double storage_zeta<double>(double z) {
 
 int64_t pad4(int64_t n) { return (n + 3) & ~int64_t(3); }
 
-int svd_cluster_size(int n, int m, int kk) {
-  int cs = std::max(1, std::min(8, (n + 63) / 64));
-  while (cs <= 16 && svd_smem_bytes(n, m, kk, cs) > 227 * 1024) ++cs;
-  return cs;
-}
+int svd_cluster_size(int n, int m, int kk) { return svd_pick_cluster(n, m, kk); }
 
 template <typename T>
 int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int max_iter,

@@ -108,9 +108,24 @@ strips_kernel(const __grid_constant__ StripsArgs<T> a) {
   T* part = reinterpret_cast<T*>(smraw + SM::lvec + SM::red);
   T* fnew = reinterpret_cast<T*>(smraw + SM::lvec + SM::red + SM::part);
   double* dred = reinterpret_cast<double*>(smraw + SM::lvec + SM::red + SM::part + SM::fnew);
-  int* lidx = reinterpret_cast<int*>(smraw + SM::lvec + SM::red + SM::part + SM::fnew + SM::dred);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int xa = x0 + 2 * lane;
+  const bool v0 = xa < s.npos, v1 = xa + 1 < s.npos;
+  const bool vec = s.vec_ok != 0;
+  // Issue every strip load of this thread first (all lines in flight at
+  // once: memory-level parallelism = lines per thread), then stage the small
+  // per-line vectors while the DRAM requests are outstanding.
+  Pair<T> cv[kStripLPT];  // holds d, then c = d - s
+  if (nmy > 0) {
+    const int kl_last = nmy - 1;
+#pragma unroll
+    for (int j = 0; j < kStripLPT; ++j) {
+      const int kl = min(w + kStripNW * j, kl_last);
+      const int64_t base = (int64_t)(__ldg(s.lines + kb + kl) - s.line_off) * s.line_stride;
+      cv[j] = load_pair<T>(s.src, base, xa, s.pos_stride, vec, v0, v1);
+    }
+  }
   for (int e = tid; e < nmy * 3 * R; e += kStripNT) {
     const int kl = e / (3 * R);
     const int rem = e - kl * 3 * R;
@@ -119,10 +134,6 @@ strips_kernel(const __grid_constant__ StripsArgs<T> a) {
     const T* sv = vv == 0 ? s.lineA : (vv == 1 ? s.lineW : s.lineRes);
     lvec[(kl * 3 + vv) * RP + t] = sv[(int64_t)(kb + kl) * R + t];
   }
-  for (int e = tid; e < nmy; e += kStripNT) lidx[e] = s.lines[kb + e] - s.line_off;
-
-  const int xa = x0 + 2 * lane;
-  const bool v0 = xa < s.npos, v1 = xa + 1 < s.npos;
   Pair<T> b[R];
 #pragma unroll
   for (int t = 0; t < R; ++t) {
@@ -135,16 +146,13 @@ strips_kernel(const __grid_constant__ StripsArgs<T> a) {
   Pair<T> acc[R];
 #pragma unroll
   for (int t = 0; t < R; ++t) acc[t] = Pair<T>::splat(T(0));
-  Pair<T> cv[kStripLPT];
   T den = T(0);
-  const bool vec = s.vec_ok != 0;
 #pragma unroll
   for (int j = 0; j < kStripLPT; ++j) {
     const int kl = w + kStripNW * j;
-    cv[j] = Pair<T>::splat(T(0));
+    if (kl >= nmy) cv[j] = Pair<T>::splat(T(0));
     if (kl < nmy) {
-      const int64_t base = (int64_t)lidx[kl] * s.line_stride;
-      const Pair<T> d = load_pair<T>(s.src, base, xa, s.pos_stride, vec, v0, v1);
+      const Pair<T> d = cv[j];
       const T* av = lvec + (kl * 3) * RP;
       Pair<T> l = pmul(Pair<T>::splat(av[0]), b[0]);
 #pragma unroll
@@ -231,27 +239,37 @@ strips_kernel(const __grid_constant__ StripsArgs<T> a) {
 }
 
 // ------------------------------------------------------------- finalize
-__global__ void finalize_kernel(FinalizeArgs a) {
+constexpr int kFinNT = 512;
+
+__global__ void __launch_bounds__(kFinNT) finalize_kernel(FinalizeArgs a) {
   if (*a.done) return;
-  __shared__ double sh[4][32];
+  __shared__ double sh[4][kFinNT / 32];
   const int tid = threadIdx.x;
-  // deterministic: each thread sums a fixed strided subset, then a fixed tree
+  // deterministic: each thread sums a fixed strided subset (loads unrolled,
+  // adds in order), then a fixed butterfly per warp and a fixed warp order.
   double v[4] = {0, 0, 0, 0};
-  for (int c = tid; c < a.ncta_rows; c += 32) {
-    v[0] += a.partials[2 * c];
-    v[1] += a.partials[2 * c + 1];
+#pragma unroll 4
+  for (int c = tid; c < a.ncta_rows; c += kFinNT) {
+    const double2 p = *reinterpret_cast<const double2*>(a.partials + 2 * c);
+    v[0] += p.x;
+    v[1] += p.y;
   }
-  for (int c = tid; c < a.ncta_cols; c += 32) {
-    v[2] += a.partials[2 * (a.ncta_rows + c)];
-    v[3] += a.partials[2 * (a.ncta_rows + c) + 1];
+#pragma unroll 4
+  for (int c = tid; c < a.ncta_cols; c += kFinNT) {
+    const double2 p = *reinterpret_cast<const double2*>(a.partials + 2 * (a.ncta_rows + c));
+    v[2] += p.x;
+    v[3] += p.y;
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) sh[q][tid] = v[q];
-  __syncwarp();
+  for (int q = 0; q < 4; ++q) {
+    const double ws = warp_sum(v[q]);
+    if ((tid & 31) == 0) sh[q][tid >> 5] = ws;
+  }
+  __syncthreads();
   if (tid == 0) {
     double s[4] = {0, 0, 0, 0};
     for (int q = 0; q < 4; ++q)
-      for (int i = 0; i < 32; ++i) s[q] += sh[q][i];
+      for (int i = 0; i < kFinNT / 32; ++i) s[q] += sh[q][i];
     const double den = sqrt(s[0]) + sqrt(s[2]);
     const double e = (sqrt(s[1]) + sqrt(s[3])) / den;
     a.errors[a.k] = e;
@@ -406,7 +424,7 @@ int strips_lines_per_cta() { return kStripLPC; }
 int strips_tx() { return kStripTX; }
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
-  finalize_kernel<<<1, 32, 0, st>>>(a);
+  finalize_kernel<<<1, kFinNT, 0, st>>>(a);
   return cudaGetLastError();
 }
 
