@@ -75,6 +75,8 @@ struct ircur_ctx {
   double* errors = nullptr;
   int* flags = nullptr;  // [0]=done [1]=iters [2]=converged [3]=nonfinite
   int* svd_steps = nullptr;  // subspace steps taken by the core SVD, per iteration
+  int* rowmap = nullptr;     // local row -> position in I (or -1), per iteration
+  int* colmap = nullptr;     // column -> position in J (or -1), per iteration
   unsigned long long* maxbits = nullptr;
   int* h_flags = nullptr;  // mapped pinned: [0]=done [1]=iters
   int* h_flags_dev = nullptr;
@@ -133,6 +135,7 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   ca.Qt = (const T*)c->Qt[old]; ca.ldq = c->ldq;
   ca.zt = zt; ca.U = c->U; ca.ldu = c->max_cols;
   ca.PoldI = (T*)c->PoldI; ca.QoldJ = (T*)c->QoldJ; ca.done = done;
+  ca.rowmap = c->rowmap; ca.colmap = c->colmap;
   cudaEvent_t* pe = c->profiling ? &c->evp[(size_t)k * 5] : nullptr;
   if (pe) IR_CUDA(cudaEventRecord(pe[0], st));
   IR_CUDA(launch_core<T>(ca, R, st));
@@ -156,33 +159,38 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   StripsArgs<T> pa;
   const int TX = strips_tx();
   StripDesc<T>& rs = pa.s[0];
+  const size_t a16 = 16;
   rs.src = (const T*)c->D; rs.line_stride = c->ldd; rs.pos_stride = 1;
-  rs.vec_ok = (c->ldd % 2 == 0) && ((uintptr_t)c->D % (2 * sizeof(T)) == 0);
+  rs.bulk_ok = ((c->ldd * (int64_t)sizeof(T)) % 16 == 0) && ((uintptr_t)c->D % a16 == 0);
   rs.lines = I + i_lo; rs.line_off = (int)c->row0; rs.nk = mI; rs.npos = (int)c->n2;
   rs.lineA = (const T*)c->PoldI; rs.lineW = (const T*)c->Wr; rs.lineRes = (const T*)c->PI;
   rs.Bold = (const T*)c->Qt[old]; rs.ldb = c->ldq; rs.Fnew = (T*)c->Qt[nw]; rs.ldf = c->ldq;
-  rs.other = J; rs.other_off = 0; rs.nother = nJ; rs.otherF = (const T*)c->QJ;
+  rs.omap = c->colmap; rs.otherF = (const T*)c->QJ;
   rs.tiles = (int)((c->n2 + TX - 1) / TX);
   StripDesc<T>& cs = pa.s[1];
   if (c->Dt) {
     cs.src = (const T*)c->Dt; cs.line_stride = c->ldt; cs.pos_stride = 1;
-    cs.vec_ok = (c->ldt % 2 == 0);
+    cs.bulk_ok = ((c->ldt * (int64_t)sizeof(T)) % 16 == 0);
   } else {
-    cs.src = (const T*)c->D; cs.line_stride = 1; cs.pos_stride = c->ldd; cs.vec_ok = 0;
+    cs.src = (const T*)c->D; cs.line_stride = 1; cs.pos_stride = c->ldd; cs.bulk_ok = 0;
   }
   cs.lines = J; cs.line_off = 0; cs.nk = nJ; cs.npos = (int)c->nloc;
   cs.lineA = (const T*)c->QoldJ; cs.lineW = (const T*)c->VS; cs.lineRes = (const T*)c->QJ;
   cs.Bold = (const T*)c->Pt[old]; cs.ldb = c->ldp; cs.Fnew = (T*)c->Pt[nw]; cs.ldf = c->ldp;
-  cs.other = I + i_lo; cs.other_off = (int)c->row0; cs.nother = mI; cs.otherF = (const T*)c->PI;
+  cs.omap = c->rowmap; cs.otherF = (const T*)c->PI;
   cs.tiles = (int)((c->nloc + TX - 1) / TX);
   pa.zt = zt; pa.partials = c->partials; pa.done = done;
-  IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, st));
+  pa.maxl = (std::max(c->max_rows, c->max_cols) + c->strips_cs - 1) / c->strips_cs;
+  int ncta = 0;
+  IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, c->num_sms, &ncta, st));
   if (pe) IR_CUDA(cudaEventRecord(pe[3], st));
 
   FinalizeArgs fa;
   fa.partials = c->partials;
-  fa.ncta_rows = rs.tiles * c->strips_cs;
-  fa.ncta_cols = cs.tiles * c->strips_cs;
+  fa.ncta_rows = ncta;
+  fa.ncta_cols = 0;
+  fa.I = I + i_lo; fa.mI = mI; fa.J = J; fa.nJ = nJ; fa.row0 = c->row0;
+  fa.rowmap = c->rowmap; fa.colmap = c->colmap;
   fa.k = k; fa.eps = eps; fa.max_iter = max_iter;
   fa.errors = c->errors; fa.done = c->flags; fa.iters = c->flags + 1; fa.converged = c->flags + 2;
   fa.host_done = host_flags ? c->h_flags_dev : nullptr;
@@ -224,9 +232,9 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   const int kk = std::min(std::min(2 * rank, 32), std::min(max_rows, max_cols));
   if (svd_smem_bytes(max_cols, max_rows, kk, 16) > 227 * 1024)
     return fail(IRCUR_EINVAL, "sampled column count too large for the core SVD kernel");
-  const int lpc = strips_lines_per_cta();
-  const int need_cs = (std::max(max_rows, max_cols) + lpc - 1) / lpc;
-  if (need_cs > 16) return fail(IRCUR_EINVAL, "sampled index sets too large for the strip kernel");
+  const int need_cs = dtype == IRCUR_F32 ? strips_pick_cluster<float>(std::max(max_rows, max_cols), rank)
+                                         : strips_pick_cluster<double>(std::max(max_rows, max_cols), rank);
+  if (need_cs < 1) return fail(IRCUR_EINVAL, "sampled index sets too large for the strip kernel");
 
   ircur_ctx* c = new ircur_ctx();
   c->device = device; c->dtype = dtype; c->n1 = n1; c->n2 = n2; c->r = rank;
@@ -266,9 +274,12 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->inv, (size_t)rank * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->G, (size_t)max_cols * max_cols * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->svd_scratch, (size_t)max_cols * 32 * sizeof(double)));
-  const int TX = strips_tx();
-  c->max_partials = (int)(((n2 + TX - 1) / TX + (local_rows + TX - 1) / TX) * c->strips_cs) * 2 + 4096;
+  c->max_partials = 4 * 2 * c->num_sms + 8192;  // strips: 4 sums per persistent CTA (<= 2/SM)
   IR_CUDA_C(cudaMalloc(&c->partials, (size_t)c->max_partials * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->rowmap, (size_t)local_rows * sizeof(int)));
+  IR_CUDA_C(cudaMalloc(&c->colmap, (size_t)n2 * sizeof(int)));
+  IR_CUDA_C(cudaMemsetAsync(c->rowmap, 0xFF, (size_t)local_rows * sizeof(int), c->stream));
+  IR_CUDA_C(cudaMemsetAsync(c->colmap, 0xFF, (size_t)n2 * sizeof(int), c->stream));
   IR_CUDA_C(cudaMalloc(&c->errors, (size_t)max_iter * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->flags, 16 * sizeof(int)));
   IR_CUDA_C(cudaMalloc(&c->svd_steps, (size_t)max_iter * sizeof(int)));
@@ -289,7 +300,8 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U,
                   c->PoldI, c->QoldJ, c->Wr, c->PI, c->VS, c->QJ, c->W, c->sigma, c->V, c->inv,
-                  c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps};
+                  c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps,
+                  c->rowmap, c->colmap};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -429,6 +441,8 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   IR_CUDA(cudaMemsetAsync(c->Pt[0], 0, (size_t)c->r * c->ldp * c->esz, st));
   IR_CUDA(cudaMemsetAsync(c->Qt[0], 0, (size_t)c->r * c->ldq * c->esz, st));
   IR_CUDA(cudaMemsetAsync(c->flags, 0, 16 * sizeof(int), st));
+  IR_CUDA(cudaMemsetAsync(c->rowmap, 0xFF, (size_t)c->nloc * sizeof(int), st));
+  IR_CUDA(cudaMemsetAsync(c->colmap, 0xFF, (size_t)c->n2 * sizeof(int), st));
   volatile int* hf = c->h_flags;
   hf[0] = 0;
   hf[1] = 0;

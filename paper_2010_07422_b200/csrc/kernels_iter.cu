@@ -36,206 +36,18 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs<T> a) {
   if (k2 == 0) {
 #pragma unroll
     for (int t = 0; t < R; ++t) a.PoldI[(int64_t)k1 * R + t] = pa[t];
+    a.rowmap[il] = k1;
   }
   if (k1 == 0) {
 #pragma unroll
     for (int t = 0; t < R; ++t) a.QoldJ[(int64_t)k2 * R + t] = qb[t];
+    a.colmap[j] = k2;
   }
   const T l = lowrank_entry<T, R>(pa, qb);
   const T d = a.D[il * a.ldd + j];
   T s;
   const T c = keep_value(d, l, a.zt, s);
   a.U[(int64_t)k1 * a.ldu + k2] = (double)c;
-}
-
-// ---------------------------------------------------------------- strips
-constexpr int kStripNT = 256;
-constexpr int kStripNW = kStripNT / 32;
-constexpr int kStripTX = 64;       // positions per CTA (2 per lane)
-constexpr int kStripLPT = 16;      // lines per thread (register-resident c values)
-constexpr int kStripLPC = kStripNW * kStripLPT;  // lines per CTA
-
-template <typename T, int R>
-struct StripSmem {
-  static constexpr int RP = ((R * (int)sizeof(T) + 15) / 16) * 16 / (int)sizeof(T);
-  static constexpr size_t lvec = (size_t)kStripLPC * 3 * RP * sizeof(T);
-  static constexpr size_t red = (size_t)kStripNW * R * kStripTX * sizeof(T);
-  static constexpr size_t part = (size_t)R * kStripTX * sizeof(T);
-  static constexpr size_t fnew = part;
-  static constexpr size_t dred = 2 * kStripNW * sizeof(double);
-  static constexpr size_t lidx = kStripLPC * sizeof(int);
-  static constexpr size_t bytes = lvec + red + part + fnew + dred + lidx;
-};
-
-template <typename T>
-__device__ __forceinline__ Pair<T> load_pair(const T* src, int64_t base, int x, int64_t ps,
-                                             bool vec, bool v0, bool v1) {
-  Pair<T> d;
-  if (vec && v1) {
-    if constexpr (sizeof(T) == 4) {
-      d.v = __ldg(reinterpret_cast<const float2*>(src + base + x));
-    } else {
-      d.v = __ldg(reinterpret_cast<const double2*>(src + base + x));
-    }
-  } else {
-    d.v.x = v0 ? __ldg(src + base + (int64_t)x * ps) : T(0);
-    d.v.y = v1 ? __ldg(src + base + (int64_t)(x + 1) * ps) : T(0);
-  }
-  return d;
-}
-
-template <typename T, int R>
-__global__ void __launch_bounds__(kStripNT, (sizeof(T) == 4 ? 2 : 1))
-strips_kernel(const __grid_constant__ StripsArgs<T> a) {
-  if (*a.done) return;  // uniform for the whole grid (flag written only by finalize)
-  cg::cluster_group cl = cg::this_cluster();
-  const int CS = (int)cl.num_blocks();
-  const int rank = (int)cl.block_rank();
-  const int cluster_id = blockIdx.x / CS;
-  const int which = cluster_id < a.s[0].tiles ? 0 : 1;
-  const StripDesc<T>& s = a.s[which];
-  const int tile = which == 0 ? cluster_id : cluster_id - a.s[0].tiles;
-  const int x0 = tile * kStripTX;
-  const int per = (s.nk + CS - 1) / CS;
-  const int kb = rank * per;
-  const int nmy = max(0, min(s.nk, kb + per) - kb);
-
-  using SM = StripSmem<T, R>;
-  constexpr int RP = SM::RP;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  T* lvec = reinterpret_cast<T*>(smraw);
-  T* red = reinterpret_cast<T*>(smraw + SM::lvec);
-  T* part = reinterpret_cast<T*>(smraw + SM::lvec + SM::red);
-  T* fnew = reinterpret_cast<T*>(smraw + SM::lvec + SM::red + SM::part);
-  double* dred = reinterpret_cast<double*>(smraw + SM::lvec + SM::red + SM::part + SM::fnew);
-
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int xa = x0 + 2 * lane;
-  const bool v0 = xa < s.npos, v1 = xa + 1 < s.npos;
-  const bool vec = s.vec_ok != 0;
-  // Issue every strip load of this thread first (all lines in flight at
-  // once: memory-level parallelism = lines per thread), then stage the small
-  // per-line vectors while the DRAM requests are outstanding.
-  Pair<T> cv[kStripLPT];  // holds d, then c = d - s
-  if (nmy > 0) {
-    const int kl_last = nmy - 1;
-#pragma unroll
-    for (int j = 0; j < kStripLPT; ++j) {
-      const int kl = min(w + kStripNW * j, kl_last);
-      const int64_t base = (int64_t)(__ldg(s.lines + kb + kl) - s.line_off) * s.line_stride;
-      cv[j] = load_pair<T>(s.src, base, xa, s.pos_stride, vec, v0, v1);
-    }
-  }
-  for (int e = tid; e < nmy * 3 * R; e += kStripNT) {
-    const int kl = e / (3 * R);
-    const int rem = e - kl * 3 * R;
-    const int vv = rem / R;
-    const int t = rem - vv * R;
-    const T* sv = vv == 0 ? s.lineA : (vv == 1 ? s.lineW : s.lineRes);
-    lvec[(kl * 3 + vv) * RP + t] = sv[(int64_t)(kb + kl) * R + t];
-  }
-  Pair<T> b[R];
-#pragma unroll
-  for (int t = 0; t < R; ++t) {
-    b[t].v.x = v0 ? s.Bold[t * s.ldb + xa] : T(0);
-    b[t].v.y = v1 ? s.Bold[t * s.ldb + xa + 1] : T(0);
-  }
-  __syncthreads();
-
-  const T zt = a.zt;
-  Pair<T> acc[R];
-#pragma unroll
-  for (int t = 0; t < R; ++t) acc[t] = Pair<T>::splat(T(0));
-  T den = T(0);
-#pragma unroll
-  for (int j = 0; j < kStripLPT; ++j) {
-    const int kl = w + kStripNW * j;
-    if (kl >= nmy) cv[j] = Pair<T>::splat(T(0));
-    if (kl < nmy) {
-      const Pair<T> d = cv[j];
-      const T* av = lvec + (kl * 3) * RP;
-      Pair<T> l = pmul(Pair<T>::splat(av[0]), b[0]);
-#pragma unroll
-      for (int t = 1; t < R; ++t) l = pfma(Pair<T>::splat(av[t]), b[t], l);
-      T s0, s1;
-      cv[j].v.x = keep_value(d.v.x, l.v.x, zt, s0);
-      cv[j].v.y = keep_value(d.v.y, l.v.y, zt, s1);
-      den = fma_rn(d.v.x, d.v.x, den);
-      den = fma_rn(d.v.y, d.v.y, den);
-      const T* wv = av + RP;
-#pragma unroll
-      for (int t = 0; t < R; ++t) acc[t] = pfma(Pair<T>::splat(wv[t]), cv[j], acc[t]);
-    }
-  }
-  // cross-warp reduction (fixed order) -> this CTA's partial factor
-#pragma unroll
-  for (int t = 0; t < R; ++t) {
-    red[(w * R + t) * kStripTX + 2 * lane] = acc[t].v.x;
-    red[(w * R + t) * kStripTX + 2 * lane + 1] = acc[t].v.y;
-  }
-  __syncthreads();
-  for (int o = tid; o < R * kStripTX; o += kStripNT) {
-    T sum = red[o];
-#pragma unroll
-    for (int ww = 1; ww < kStripNW; ++ww) sum += red[ww * R * kStripTX + o];
-    part[o] = sum;
-  }
-  // cluster reduction over the CTAs that split the lines (fixed rank order;
-  // every CTA computes the identical sum)
-  cl.sync();
-  for (int o = tid; o < R * kStripTX; o += kStripNT) {
-    T sum = *cl.map_shared_rank(part + o, 0);
-    for (int q = 1; q < CS; ++q) sum += *cl.map_shared_rank(part + o, q);
-    fnew[o] = sum;
-  }
-  __syncthreads();
-  // positions in the other index set take the factor computed from the core
-  // (Q(:,J) = W^T U, P(I,:) = U V Sigma^+), so both strips and the next
-  // iteration see one value for the I x J block.
-  if (s.nother > 0) {
-    const int e0 = lower_bound_i32(s.other, s.nother, x0 + s.other_off);
-    const int e1 = lower_bound_i32(s.other, s.nother, x0 + kStripTX + s.other_off);
-    for (int e = e0 + tid; e < e1; e += kStripNT) {
-      const int x = s.other[e] - s.other_off - x0;
-#pragma unroll
-      for (int t = 0; t < R; ++t) fnew[t * kStripTX + x] = s.otherF[(int64_t)e * R + t];
-    }
-  }
-  cl.sync();  // peers finished reading `part`; fnew complete
-  if (rank == 0) {
-    for (int o = tid; o < R * kStripTX; o += kStripNT) {
-      const int t = o / kStripTX, x = o - t * kStripTX;
-      if (x0 + x < s.npos) s.Fnew[t * s.ldf + x0 + x] = fnew[o];
-    }
-  }
-  // pass 2: stopping residual on the register-resident strip values
-  Pair<T> f[R];
-#pragma unroll
-  for (int t = 0; t < R; ++t) {
-    f[t].v.x = fnew[t * kStripTX + 2 * lane];
-    f[t].v.y = fnew[t * kStripTX + 2 * lane + 1];
-  }
-  T res = T(0);
-#pragma unroll
-  for (int j = 0; j < kStripLPT; ++j) {
-    const int kl = w + kStripNW * j;
-    if (kl < nmy) {
-      const T* rv = lvec + (kl * 3 + 2) * RP;
-      Pair<T> l = pmul(Pair<T>::splat(rv[0]), f[0]);
-#pragma unroll
-      for (int t = 1; t < R; ++t) l = pfma(Pair<T>::splat(rv[t]), f[t], l);
-      const T r0 = sub_rn(cv[j].v.x, l.v.x);
-      const T r1 = sub_rn(cv[j].v.y, l.v.y);
-      res = fma_rn(r0, r0, res);
-      res = fma_rn(r1, r1, res);
-    }
-  }
-  const double dsum = block_sum<kStripNT>((double)den, dred);
-  const double rsum = block_sum<kStripNT>((double)res, dred + kStripNW);
-  if (tid == 0) {
-    a.partials[2 * blockIdx.x] = dsum;
-    a.partials[2 * blockIdx.x + 1] = rsum;
-  }
 }
 
 // ------------------------------------------------------------- finalize
@@ -245,20 +57,19 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(FinalizeArgs a) {
   if (*a.done) return;
   __shared__ double sh[4][kFinNT / 32];
   const int tid = threadIdx.x;
+  // the strips of this iteration are finished: reset the position maps
+  for (int e = tid; e < a.mI; e += kFinNT) a.rowmap[a.I[e] - a.row0] = -1;
+  for (int e = tid; e < a.nJ; e += kFinNT) a.colmap[a.J[e]] = -1;
   // deterministic: each thread sums a fixed strided subset (loads unrolled,
   // adds in order), then a fixed butterfly per warp and a fixed warp order.
   double v[4] = {0, 0, 0, 0};
 #pragma unroll 4
   for (int c = tid; c < a.ncta_rows; c += kFinNT) {
-    const double2 p = *reinterpret_cast<const double2*>(a.partials + 2 * c);
+    const double4 p = *reinterpret_cast<const double4*>(a.partials + 4 * c);
     v[0] += p.x;
     v[1] += p.y;
-  }
-#pragma unroll 4
-  for (int c = tid; c < a.ncta_cols; c += kFinNT) {
-    const double2 p = *reinterpret_cast<const double2*>(a.partials + 2 * (a.ncta_rows + c));
-    v[2] += p.x;
-    v[3] += p.y;
+    v[2] += p.z;
+    v[3] += p.w;
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -379,49 +190,6 @@ cudaError_t launch_core(const CoreArgs<T>& a, int R, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <typename T>
-size_t strips_smem_bytes(int R) {
-  size_t b = 0;
-  IRCUR_DISPATCH_RANK(R, RR, b = StripSmem<T, RR>::bytes);
-  return b;
-}
-
-template <typename T, int R>
-static cudaError_t launch_strips_r(const StripsArgs<T>& a, int cs, cudaStream_t st) {
-  const size_t smem = StripSmem<T, R>::bytes;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(strips_kernel<T, R>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(strips_kernel<T, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_done = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((a.s[0].tiles + a.s[1].tiles) * cs), 1, 1);
-  cfg.blockDim = dim3(kStripNT, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, strips_kernel<T, R>, a);
-}
-
-template <typename T>
-cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, cudaStream_t st) {
-  if (a.s[0].tiles + a.s[1].tiles == 0) return cudaSuccess;
-  cudaError_t e = cudaErrorInvalidValue;
-  IRCUR_DISPATCH_RANK(R, RR, e = launch_strips_r<T, RR>(a, cs, st));
-  return e;
-}
-
-int strips_lines_per_cta() { return kStripLPC; }
-int strips_tx() { return kStripTX; }
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
   finalize_kernel<<<1, kFinNT, 0, st>>>(a);
@@ -456,8 +224,6 @@ cudaError_t launch_materialize(const T* Pt, int64_t ldp, const T* Qt, int64_t ld
 
 #define IRCUR_INST(T)                                                                      \
   template cudaError_t launch_core<T>(const CoreArgs<T>&, int, cudaStream_t);              \
-  template size_t strips_smem_bytes<T>(int);                                               \
-  template cudaError_t launch_strips<T>(const StripsArgs<T>&, int, int, cudaStream_t);     \
   template cudaError_t launch_writeout<T>(const WriteoutArgs<T>&, int, cudaStream_t);      \
   template cudaError_t launch_materialize<T, float>(const T*, int64_t, const T*, int64_t,  \
                                                     int64_t, int64_t, float*, int64_t, int, \

@@ -18,6 +18,7 @@ struct CoreArgs {
   T zt;
   double* U; int ldu;                          // mI x nJ
   T* PoldI; T* QoldJ;                          // mI x R, nJ x R
+  int* rowmap; int* colmap;                    // position -> index maps (set here, cleared by finalize)
   const int* done;
 };
 
@@ -30,14 +31,15 @@ struct CoreArgs {
 // squared norm, with ||d||^2, feeds e_k (solver.py:393-400).
 template <typename T>
 struct StripDesc {
-  const T* src; int64_t line_stride; int64_t pos_stride; int vec_ok;
+  const T* src; int64_t line_stride; int64_t pos_stride;
+  int bulk_ok;                                 // line segments are 16B aligned: TMA bulk copies
   const int* lines; int line_off; int nk;      // element (k, x) = src[(lines[k]-line_off)*line_stride + x*pos_stride]
   int npos;
   const T* lineA; const T* lineW; const T* lineRes;  // nk x R each
-  const T* Bold; int64_t ldb;                  // R x npos (padded ld)
+  const T* Bold; int64_t ldb;                  // R x npos (padded ld, 16B aligned rows)
   T* Fnew; int64_t ldf;                        // R x npos
-  const int* other; int other_off; int nother; // sorted positions whose Fnew is fixed
-  const T* otherF;                             // nother x R
+  const int* omap;                             // npos: index into otherF, or -1
+  const T* otherF;                             // (other set size) x R
   int tiles;                                   // ceil(npos / TX)
 };
 
@@ -45,16 +47,19 @@ template <typename T>
 struct StripsArgs {
   StripDesc<T> s[2];                           // [0] row strip, [1] column strip
   T zt;
+  int maxl;                                    // max lines per CTA (smem sizing)
   double* partials;                            // per CTA: {den, res}
   const int* done;
 };
 
 // ------------------------------------------------------------- finalize
 struct FinalizeArgs {
-  const double* partials; int ncta_rows; int ncta_cols;
+  const double* partials; int ncta_rows; int ncta_cols;  // ncta_rows = strip CTAs, 4 sums each
   int k; double eps; int max_iter;
   double* errors; int* done; int* iters; int* converged;
   volatile int* host_done; volatile int* host_iters;   // mapped pinned memory (may be null)
+  const int* I; int mI; const int* J; int nJ; int64_t row0;
+  int* rowmap; int* colmap;                    // cleared back to -1 for this iteration's sets
 };
 
 // --------------------------------------------------------------- writeout

@@ -1,0 +1,394 @@
+// Fused row + column strip kernel of the IRCUR hot path (sm_100a).
+//
+// One pass over the sampled strips per iteration:
+//   Phase I   s = T_zeta(d - L_k)            (solver.py:375-377, strict |x| > zeta)
+//   Phase II  c = d - s  (R = D(I,:) - S, C = D(:,J) - S)   (solver.py:380-382)
+//   factor    Fnew(:,x) = sum_k W_k c_k(x)   (Q_{k+1} = W_r^T R, P_{k+1} = C V_r Sigma^+)
+//   residual  sum (c - <Res_k, Fnew(:,x)>)^2 and sum d^2   (e_k, solver.py:393-400)
+//
+// Persistent CTAs (or thread-block clusters that split the sampled lines)
+// walk 64-position tiles of both strips.  Every line segment of a tile (256 B
+// fp32 / 512 B fp64) is fetched with a TMA bulk copy (cp.async.bulk) into a
+// double-buffered shared-memory stage completed on an mbarrier, so the next
+// tile streams from HBM while the current one is computed.  Tile values are
+// thresholded in place in shared memory, reduced per tile (warps, then
+// cluster CTAs over DSMEM, fixed order) and re-read for the residual.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "kernels_iter.cuh"
+#include "launchers.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ircur {
+
+constexpr int kSNT = 256;
+constexpr int kSNW = kSNT / 32;
+constexpr int kSTX = 64;  // positions per tile (2 per lane)
+
+struct StripsLayout {
+  int RP;
+  size_t seg, bars, stage, bst, lvec, lidx, red, part, fnew, dred, total;
+};
+
+__host__ __device__ inline size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
+
+__host__ __device__ inline StripsLayout strips_layout(int maxl, int R, int esz) {
+  StripsLayout L;
+  L.RP = ((R * esz + 15) / 16) * 16 / esz;
+  L.seg = (size_t)kSTX * esz;
+  size_t off = 0;
+  L.bars = off; off += 128;
+  L.stage = off; off = align128(off + 2 * (size_t)maxl * L.seg);
+  L.bst = off; off = align128(off + 2 * (size_t)R * L.seg);
+  L.lvec = off; off = align128(off + (size_t)maxl * 3 * L.RP * esz);
+  L.lidx = off; off = align128(off + 2 * (size_t)maxl * sizeof(int));
+  L.red = off; off = align128(off + (size_t)kSNW * R * L.seg);
+  L.part = off; off = align128(off + 2 * (size_t)R * L.seg);
+  L.fnew = off; off = align128(off + (size_t)R * L.seg);
+  L.dred = off; off = align128(off + 4 * kSNW * sizeof(double));
+  L.total = off;
+  return L;
+}
+
+// ---- PTX helpers: mbarrier + TMA bulk copy -------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ Pair<T> lds_pair(const T* p) {
+  Pair<T> v;
+  if constexpr (sizeof(T) == 4) v.v = *reinterpret_cast<const float2*>(p);
+  else v.v = *reinterpret_cast<const double2*>(p);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ void sts_pair(T* p, Pair<T> v) {
+  if constexpr (sizeof(T) == 4) *reinterpret_cast<float2*>(p) = v.v;
+  else *reinterpret_cast<double2*>(p) = v.v;
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__ StripsArgs<T> a) {
+  if (*a.done) return;  // uniform for the whole grid (flag written only by finalize)
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int ncl = gridDim.x / CS;
+  const int cid = blockIdx.x / CS;
+  const StripsLayout L = strips_layout(a.maxl, R, (int)sizeof(T));
+  const int RP = L.RP;
+  const int maxl = a.maxl;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
+  T* stage = reinterpret_cast<T*>(sm + L.stage);
+  T* bst = reinterpret_cast<T*>(sm + L.bst);
+  T* lvec = reinterpret_cast<T*>(sm + L.lvec);
+  int* lidx = reinterpret_cast<int*>(sm + L.lidx);
+  T* red = reinterpret_cast<T*>(sm + L.red);
+  T* part = reinterpret_cast<T*>(sm + L.part);
+  T* fnew = reinterpret_cast<T*>(sm + L.fnew);
+  double* dred = reinterpret_cast<double*>(sm + L.dred);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tiles0 = a.s[0].tiles;
+  const int total = tiles0 + a.s[1].tiles;
+  const uint32_t seg = (uint32_t)L.seg;
+
+  int kb[2], nmy[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int per = (a.s[q].nk + CS - 1) / CS;
+    kb[q] = rank * per;
+    nmy[q] = max(0, min(a.s[q].nk, kb[q] + per) - kb[q]);
+  }
+  for (int e = tid; e < nmy[0]; e += kSNT) lidx[e] = a.s[0].lines[kb[0] + e] - a.s[0].line_off;
+  for (int e = tid; e < nmy[1]; e += kSNT) lidx[maxl + e] = a.s[1].lines[kb[1] + e] - a.s[1].line_off;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto tile_of = [&](int i, int& q, int& x0) -> bool {
+    const int t = cid + i * ncl;
+    if (t >= total) return false;
+    q = t < tiles0 ? 0 : 1;
+    x0 = (t - (q ? tiles0 : 0)) * kSTX;
+    return true;
+  };
+  auto use_bulk = [&](int q, int x0) -> bool {
+    return a.s[q].bulk_ok && x0 + kSTX <= a.s[q].npos;
+  };
+  // warp 0 issues the TMA bulk copies of tile i into stage st
+  auto issue = [&](int i, int st) {
+    int q, x0;
+    if (!tile_of(i, q, x0) || !use_bulk(q, x0)) return;
+    const StripDesc<T>& s = a.s[q];
+    uint64_t* bar = &bars[st];
+    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nmy[q] + R) * seg);
+    __syncwarp();
+    const int* li = lidx + q * maxl;
+    T* stg = stage + (size_t)st * maxl * kSTX;
+    for (int k = lane; k < nmy[q]; k += 32)
+      bulk_g2s(stg + (size_t)k * kSTX, s.src + (int64_t)li[k] * s.line_stride + x0, seg, bar);
+    for (int t = lane; t < R; t += 32)
+      bulk_g2s(bst + ((size_t)st * R + t) * kSTX, s.Bold + (int64_t)t * s.ldb + x0, seg, bar);
+  };
+  if (w == 0) {
+    issue(0, 0);
+    issue(1, 1);
+  }
+
+  uint32_t phase0 = 0, phase1 = 0;
+  int cur_strip = -1;
+  double den_acc0 = 0.0, res_acc0 = 0.0, den_acc1 = 0.0, res_acc1 = 0.0;
+  const T zt = a.zt;
+  for (int i = 0;; ++i) {
+    int q, x0;
+    if (!tile_of(i, q, x0)) break;
+    const int st = i & 1;
+    const StripDesc<T>& s = a.s[q];
+    const int nl = nmy[q];
+    T* stg = stage + (size_t)st * maxl * kSTX;
+    T* bsg = bst + (size_t)st * R * kSTX;
+    if (q != cur_strip) {
+      // per-line vectors of this strip (my lines): A | W | Res, padded to RP
+      for (int e = tid; e < nl * 3 * R; e += kSNT) {
+        const int kl = e / (3 * R);
+        const int rem = e - kl * 3 * R;
+        const int vv = rem / R;
+        const int t = rem - vv * R;
+        const T* sv = vv == 0 ? s.lineA : (vv == 1 ? s.lineW : s.lineRes);
+        lvec[(kl * 3 + vv) * RP + t] = sv[(int64_t)(kb[q] + kl) * R + t];
+      }
+      cur_strip = q;
+      __syncthreads();
+    }
+    if (use_bulk(q, x0)) {
+      const uint32_t ph = st ? phase1 : phase0;
+      while (!mbar_try_wait(&bars[st], ph)) {
+      }
+      if (st) phase1 ^= 1u; else phase0 ^= 1u;
+    } else {
+      // generic path (tail tile, unaligned or strided lines): thread loads
+      const int* li = lidx + q * maxl;
+      for (int e = tid; e < nl * kSTX; e += kSNT) {
+        const int kl = e / kSTX, x = e - kl * kSTX;
+        const int pos = x0 + x;
+        stg[(size_t)kl * kSTX + x] =
+            pos < s.npos ? s.src[(int64_t)li[kl] * s.line_stride + (int64_t)pos * s.pos_stride] : T(0);
+      }
+      for (int e = tid; e < R * kSTX; e += kSNT) {
+        const int t = e / kSTX, x = e - t * kSTX;
+        bsg[e] = (x0 + x < s.npos) ? s.Bold[(int64_t)t * s.ldb + x0 + x] : T(0);
+      }
+      __syncthreads();
+    }
+
+    // ---- pass 1: Phase I/II in place + factor partials
+    Pair<T> b[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) b[t] = lds_pair(bsg + t * kSTX + 2 * lane);
+    Pair<T> acc[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) acc[t] = Pair<T>::splat(T(0));
+    T den = T(0);
+    const int pe = 2 * lane;
+    const bool v0 = x0 + pe < s.npos, v1 = x0 + pe + 1 < s.npos;
+#pragma unroll 2
+    for (int kl = w; kl < nl; kl += kSNW) {
+      T* cell = stg + (size_t)kl * kSTX + pe;
+      const Pair<T> d = lds_pair(cell);
+      const T* av = lvec + (kl * 3) * RP;
+      Pair<T> l = pmul(Pair<T>::splat(av[0]), b[0]);
+#pragma unroll
+      for (int t = 1; t < R; ++t) l = pfma(Pair<T>::splat(av[t]), b[t], l);
+      T s0, s1;
+      Pair<T> c;
+      c.v.x = keep_value(d.v.x, l.v.x, zt, s0);
+      c.v.y = keep_value(d.v.y, l.v.y, zt, s1);
+      den = fma_rn(d.v.x, d.v.x, den);
+      den = fma_rn(d.v.y, d.v.y, den);
+      sts_pair(cell, c);
+      const T* wv = av + RP;
+#pragma unroll
+      for (int t = 0; t < R; ++t) acc[t] = pfma(Pair<T>::splat(wv[t]), c, acc[t]);
+    }
+    (void)v0; (void)v1;
+    if (q == 0) den_acc0 += (double)den; else den_acc1 += (double)den;
+#pragma unroll
+    for (int t = 0; t < R; ++t) sts_pair(red + ((size_t)w * R + t) * kSTX + pe, acc[t]);
+    __syncthreads();
+    T* pbuf = part + (size_t)(i & 1) * R * kSTX;
+    T* fsum = CS > 1 ? pbuf : fnew;
+    for (int o = tid; o < R * kSTX; o += kSNT) {
+      T sum = red[o];
+#pragma unroll
+      for (int ww = 1; ww < kSNW; ++ww) sum += red[(size_t)ww * R * kSTX + o];
+      fsum[o] = sum;
+    }
+    if (CS > 1) {
+      cl.sync();
+      for (int o = tid; o < R * kSTX; o += kSNT) {
+        T sum = *cl.map_shared_rank(pbuf + o, 0);
+        for (int qq = 1; qq < CS; ++qq) sum += *cl.map_shared_rank(pbuf + o, qq);
+        fnew[o] = sum;
+      }
+    }
+    __syncthreads();
+    // positions of the other index set take the factor computed from the core
+    // (Q(:,J) = W^T U, P(I,:) = U V Sigma^+): one value for the I x J block.
+    for (int x = tid; x < kSTX; x += kSNT) {
+      const int pos = x0 + x;
+      if (pos < s.npos) {
+        const int e = s.omap[pos];
+        if (e >= 0) {
+#pragma unroll
+          for (int t = 0; t < R; ++t) fnew[t * kSTX + x] = s.otherF[(int64_t)e * R + t];
+        }
+      }
+    }
+    __syncthreads();
+    for (int o = tid; o < R * kSTX; o += kSNT) {
+      const int t = o / kSTX, x = o - t * kSTX;
+      if ((t % CS) == rank && x0 + x < s.npos) s.Fnew[(int64_t)t * s.ldf + x0 + x] = fnew[o];
+    }
+    // ---- pass 2: stopping residual on the thresholded tile
+    Pair<T> f[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) f[t] = lds_pair(fnew + t * kSTX + pe);
+    T res = T(0);
+#pragma unroll 2
+    for (int kl = w; kl < nl; kl += kSNW) {
+      const Pair<T> c = lds_pair(stg + (size_t)kl * kSTX + pe);
+      const T* rv = lvec + (kl * 3 + 2) * RP;
+      Pair<T> l = pmul(Pair<T>::splat(rv[0]), f[0]);
+#pragma unroll
+      for (int t = 1; t < R; ++t) l = pfma(Pair<T>::splat(rv[t]), f[t], l);
+      const T r0 = sub_rn(c.v.x, l.v.x);
+      const T r1 = sub_rn(c.v.y, l.v.y);
+      res = fma_rn(r0, r0, res);
+      res = fma_rn(r1, r1, res);
+    }
+    if (q == 0) res_acc0 += (double)res; else res_acc1 += (double)res;
+    fence_proxy_async();
+    __syncthreads();  // stage st, fnew, red are free again
+    if (w == 0) issue(i + 2, st);
+  }
+  const double d0 = block_sum<kSNT>(den_acc0, dred);
+  const double r0 = block_sum<kSNT>(res_acc0, dred + kSNW);
+  const double d1 = block_sum<kSNT>(den_acc1, dred + 2 * kSNW);
+  const double r1 = block_sum<kSNT>(res_acc1, dred + 3 * kSNW);
+  if (tid == 0) {
+    double4 p;
+    p.x = d0; p.y = r0; p.z = d1; p.w = r1;
+    *reinterpret_cast<double4*>(a.partials + 4 * blockIdx.x) = p;
+  }
+  if (CS > 1) cl.sync();  // peers may still read this CTA's `part`
+}
+
+// ------------------------------------------------------------------ launch
+template <typename T>
+size_t strips_smem_bytes(int maxl, int R) {
+  return strips_layout(maxl, R, (int)sizeof(T)).total;
+}
+
+// smallest cluster size whose per-CTA line share fits in shared memory
+template <typename T>
+int strips_pick_cluster(int nk_max, int R) {
+  for (int cs = 1; cs <= 16; ++cs) {
+    const int maxl = (nk_max + cs - 1) / cs;
+    if (strips_smem_bytes<T>(maxl, R) <= (size_t)227 * 1024) return cs;
+  }
+  return -1;
+}
+
+template <typename T, int R>
+static cudaError_t launch_strips_r(const StripsArgs<T>& a, int cs, int num_sms, cudaStream_t st) {
+  const size_t smem = strips_smem_bytes<T>(a.maxl, R);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(strips_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(strips_kernel<T, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  const int tiles = a.s[0].tiles + a.s[1].tiles;
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (size_t)(227 * 1024) / (smem + 1024)));
+  int ncl = std::max(1, std::min(tiles, num_sms * per_sm / cs));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncl * cs), 1, 1);
+  cfg.blockDim = dim3(kSNT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, strips_kernel<T, R>, a);
+}
+
+template <typename T>
+cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, int* ncta_out,
+                          cudaStream_t st) {
+  const int tiles = a.s[0].tiles + a.s[1].tiles;
+  if (tiles == 0) return cudaSuccess;
+  cudaError_t e = cudaErrorInvalidValue;
+  IRCUR_DISPATCH_RANK(R, RR, e = launch_strips_r<T, RR>(a, cs, num_sms, st));
+  if (ncta_out) {
+    const size_t smem = strips_smem_bytes<T>(a.maxl, R);
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (size_t)(227 * 1024) / (smem + 1024)));
+    *ncta_out = std::max(1, std::min(tiles, num_sms * per_sm / cs)) * cs;
+  }
+  return e;
+}
+
+int strips_tx() { return kSTX; }
+
+template size_t strips_smem_bytes<float>(int, int);
+template size_t strips_smem_bytes<double>(int, int);
+template int strips_pick_cluster<float>(int, int);
+template int strips_pick_cluster<double>(int, int);
+template cudaError_t launch_strips<float>(const StripsArgs<float>&, int, int, int, int*, cudaStream_t);
+template cudaError_t launch_strips<double>(const StripsArgs<double>&, int, int, int, int*, cudaStream_t);
+
+}  // namespace ircur

@@ -36,9 +36,10 @@ struct GenArgs {
 };
 
 template <typename T> cudaError_t launch_core(const CoreArgs<T>& a, int R, cudaStream_t st);
-template <typename T> size_t strips_smem_bytes(int R);
-template <typename T> cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, cudaStream_t st);
-int strips_lines_per_cta();
+template <typename T> size_t strips_smem_bytes(int maxl, int R);
+template <typename T> int strips_pick_cluster(int nk_max, int R);
+template <typename T>
+cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, int* ncta_out, cudaStream_t st);
 int strips_tx();
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
