@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -242,6 +243,10 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   c->row0 = row0; c->nloc = local_rows; c->stream = (cudaStream_t)stream;
   c->esz = dtype == IRCUR_F32 ? 4 : 8;
   c->strips_cs = std::max(1, need_cs);
+  if (const char* ov = std::getenv("IRCUR_STRIPS_CS")) {  // tuning override
+    const int v = std::atoi(ov);
+    if (v >= need_cs && v <= 16) c->strips_cs = v;
+  }
   auto cleanup = [&](int code) {
     ircur_ctx_destroy(c);
     return code;

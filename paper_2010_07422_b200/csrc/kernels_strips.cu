@@ -88,6 +88,24 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// cp.async (LDGSTS): 16-byte chunk with zero-fill beyond src_bytes, or one element
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src, bool ok) {
+  if constexpr (sizeof(T) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 4 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 template <typename T>
 __device__ __forceinline__ Pair<T> lds_pair(const T* p) {
   Pair<T> v;
@@ -136,11 +154,7 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
   }
   for (int e = tid; e < nmy[0]; e += kSNT) lidx[e] = a.s[0].lines[kb[0] + e] - a.s[0].line_off;
   for (int e = tid; e < nmy[1]; e += kSNT) lidx[maxl + e] = a.s[1].lines[kb[1] + e] - a.s[1].line_off;
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
+  (void)bars; (void)seg;
   __syncthreads();
 
   auto tile_of = [&](int i, int& q, int& x0) -> bool {
@@ -150,30 +164,52 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     x0 = (t - (q ? tiles0 : 0)) * kSTX;
     return true;
   };
-  auto use_bulk = [&](int q, int x0) -> bool {
-    return a.s[q].bulk_ok && x0 + kSTX <= a.s[q].npos;
-  };
-  // warp 0 issues the TMA bulk copies of tile i into stage st
+  // every thread issues its share of the asynchronous copies (cp.async) of
+  // tile i (the CTA's line segments + the R rows of the old factor) into
+  // stage st, then commits one group (possibly empty: uniform group count).
   auto issue = [&](int i, int st) {
     int q, x0;
-    if (!tile_of(i, q, x0) || !use_bulk(q, x0)) return;
-    const StripDesc<T>& s = a.s[q];
-    uint64_t* bar = &bars[st];
-    if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nmy[q] + R) * seg);
-    __syncwarp();
-    const int* li = lidx + q * maxl;
-    T* stg = stage + (size_t)st * maxl * kSTX;
-    for (int k = lane; k < nmy[q]; k += 32)
-      bulk_g2s(stg + (size_t)k * kSTX, s.src + (int64_t)li[k] * s.line_stride + x0, seg, bar);
-    for (int t = lane; t < R; t += 32)
-      bulk_g2s(bst + ((size_t)st * R + t) * kSTX, s.Bold + (int64_t)t * s.ldb + x0, seg, bar);
+    if (tile_of(i, q, x0)) {
+      const StripDesc<T>& s = a.s[q];
+      const int* li = lidx + q * maxl;
+      T* stg = stage + (size_t)st * maxl * kSTX;
+      T* bsg = bst + (size_t)st * R * kSTX;
+      const int nl = nmy[q];
+      if (s.bulk_ok) {
+        constexpr int EPC = 16 / (int)sizeof(T);  // elements per 16-byte chunk
+        constexpr int CPL = kSTX / EPC;           // chunks per line segment
+        const int nch = (nl + R) * CPL;
+        for (int c = tid; c < nch; c += kSNT) {
+          const int ln = c / CPL, ch = c - ln * CPL;
+          const int pos = x0 + ch * EPC;
+          const int rem = s.npos - pos;
+          const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(T) : 0);
+          const int sp = bytes ? pos : x0;
+          if (ln < nl)
+            cp_async16(stg + (size_t)ln * kSTX + ch * EPC, s.src + (int64_t)li[ln] * s.line_stride + sp, bytes);
+          else
+            cp_async16(bsg + (size_t)(ln - nl) * kSTX + ch * EPC, s.Bold + (int64_t)(ln - nl) * s.ldb + sp, bytes);
+        }
+      } else {
+        const int nel = (nl + R) * kSTX;
+        for (int e = tid; e < nel; e += kSNT) {
+          const int ln = e / kSTX, x = e - ln * kSTX;
+          const int pos = x0 + x;
+          const bool ok = pos < s.npos;
+          if (ln < nl)
+            cp_async_elem(stg + (size_t)ln * kSTX + x,
+                          s.src + (int64_t)li[ln] * s.line_stride + (int64_t)(ok ? pos : 0) * s.pos_stride, ok);
+          else
+            cp_async_elem(bsg + (size_t)(ln - nl) * kSTX + x, s.Bold + (int64_t)(ln - nl) * s.ldb + (ok ? pos : 0),
+                          ok);
+        }
+      }
+    }
+    cp_async_commit();
   };
-  if (w == 0) {
-    issue(0, 0);
-    issue(1, 1);
-  }
+  issue(0, 0);
+  issue(1, 1);
 
-  uint32_t phase0 = 0, phase1 = 0;
   int cur_strip = -1;
   double den_acc0 = 0.0, res_acc0 = 0.0, den_acc1 = 0.0, res_acc1 = 0.0;
   const T zt = a.zt;
@@ -198,26 +234,8 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
       cur_strip = q;
       __syncthreads();
     }
-    if (use_bulk(q, x0)) {
-      const uint32_t ph = st ? phase1 : phase0;
-      while (!mbar_try_wait(&bars[st], ph)) {
-      }
-      if (st) phase1 ^= 1u; else phase0 ^= 1u;
-    } else {
-      // generic path (tail tile, unaligned or strided lines): thread loads
-      const int* li = lidx + q * maxl;
-      for (int e = tid; e < nl * kSTX; e += kSNT) {
-        const int kl = e / kSTX, x = e - kl * kSTX;
-        const int pos = x0 + x;
-        stg[(size_t)kl * kSTX + x] =
-            pos < s.npos ? s.src[(int64_t)li[kl] * s.line_stride + (int64_t)pos * s.pos_stride] : T(0);
-      }
-      for (int e = tid; e < R * kSTX; e += kSNT) {
-        const int t = e / kSTX, x = e - t * kSTX;
-        bsg[e] = (x0 + x < s.npos) ? s.Bold[(int64_t)t * s.ldb + x0 + x] : T(0);
-      }
-      __syncthreads();
-    }
+    cp_async_wait1();  // this thread's copies of tile i have landed
+    __syncthreads();   // ... and everybody else's
 
     // ---- pass 1: Phase I/II in place + factor partials
     Pair<T> b[R];
@@ -305,10 +323,10 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
       res = fma_rn(r1, r1, res);
     }
     if (q == 0) res_acc0 += (double)res; else res_acc1 += (double)res;
-    fence_proxy_async();
     __syncthreads();  // stage st, fnew, red are free again
-    if (w == 0) issue(i + 2, st);
+    issue(i + 2, st);
   }
+  cp_async_wait0();
   const double d0 = block_sum<kSNT>(den_acc0, dred);
   const double r0 = block_sum<kSNT>(res_acc0, dred + kSNW);
   const double d1 = block_sum<kSNT>(den_acc1, dred + 2 * kSNW);
