@@ -23,9 +23,13 @@ namespace cg = cooperative_groups;
 
 namespace ircur {
 
-constexpr int kSNT = 256;
+constexpr int kSNT = 512;
 constexpr int kSNW = kSNT / 32;
 constexpr int kSTX = 64;  // positions per tile (2 per lane)
+// lines processed together per warp (independent chains); fewer for wide
+// (fp64 / large-rank) register footprints so nothing spills at 128 regs
+template <typename T, int R>
+__host__ __device__ constexpr int group_lines() { return (sizeof(T) == 8 && R > 5) ? 1 : ((sizeof(T) == 8 || R > 12) ? 2 : 4); }
 
 struct StripsLayout {
   int RP;
@@ -246,9 +250,38 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     for (int t = 0; t < R; ++t) acc[t] = Pair<T>::splat(T(0));
     T den = T(0);
     const int pe = 2 * lane;
-    const bool v0 = x0 + pe < s.npos, v1 = x0 + pe + 1 < s.npos;
-#pragma unroll 2
-    for (int kl = w; kl < nl; kl += kSNW) {
+    // lines in groups of kG with interleaved (independent) rank-r chains
+    constexpr int kG = group_lines<T, R>();
+    int kl = w;
+    for (; kl + (kG - 1) * kSNW < nl; kl += kG * kSNW) {
+      Pair<T> d[kG], l[kG], c[kG];
+      const T* av[kG];
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        av[g] = lvec + ((kl + g * kSNW) * 3) * RP;
+        d[g] = lds_pair(stg + (size_t)(kl + g * kSNW) * kSTX + pe);
+      }
+#pragma unroll
+      for (int g = 0; g < kG; ++g) l[g] = pmul(Pair<T>::splat(av[g][0]), b[0]);
+#pragma unroll
+      for (int t = 1; t < R; ++t)
+#pragma unroll
+        for (int g = 0; g < kG; ++g) l[g] = pfma(Pair<T>::splat(av[g][t]), b[t], l[g]);
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        T s0, s1;
+        c[g].v.x = keep_value(d[g].v.x, l[g].v.x, zt, s0);
+        c[g].v.y = keep_value(d[g].v.y, l[g].v.y, zt, s1);
+        den = fma_rn(d[g].v.x, d[g].v.x, den);
+        den = fma_rn(d[g].v.y, d[g].v.y, den);
+        sts_pair(stg + (size_t)(kl + g * kSNW) * kSTX + pe, c[g]);
+      }
+#pragma unroll
+      for (int t = 0; t < R; ++t)
+#pragma unroll
+        for (int g = 0; g < kG; ++g) acc[t] = pfma(Pair<T>::splat(av[g][RP + t]), c[g], acc[t]);
+    }
+    for (; kl < nl; kl += kSNW) {
       T* cell = stg + (size_t)kl * kSTX + pe;
       const Pair<T> d = lds_pair(cell);
       const T* av = lvec + (kl * 3) * RP;
@@ -266,7 +299,6 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
 #pragma unroll
       for (int t = 0; t < R; ++t) acc[t] = pfma(Pair<T>::splat(wv[t]), c, acc[t]);
     }
-    (void)v0; (void)v1;
     if (q == 0) den_acc0 += (double)den; else den_acc1 += (double)den;
 #pragma unroll
     for (int t = 0; t < R; ++t) sts_pair(red + ((size_t)w * R + t) * kSTX + pe, acc[t]);
@@ -310,8 +342,30 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
 #pragma unroll
     for (int t = 0; t < R; ++t) f[t] = lds_pair(fnew + t * kSTX + pe);
     T res = T(0);
-#pragma unroll 2
-    for (int kl = w; kl < nl; kl += kSNW) {
+    kl = w;
+    for (; kl + (kG - 1) * kSNW < nl; kl += kG * kSNW) {
+      Pair<T> c[kG], l[kG];
+      const T* rv[kG];
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        rv[g] = lvec + ((kl + g * kSNW) * 3 + 2) * RP;
+        c[g] = lds_pair(stg + (size_t)(kl + g * kSNW) * kSTX + pe);
+      }
+#pragma unroll
+      for (int g = 0; g < kG; ++g) l[g] = pmul(Pair<T>::splat(rv[g][0]), f[0]);
+#pragma unroll
+      for (int t = 1; t < R; ++t)
+#pragma unroll
+        for (int g = 0; g < kG; ++g) l[g] = pfma(Pair<T>::splat(rv[g][t]), f[t], l[g]);
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        const T r0 = sub_rn(c[g].v.x, l[g].v.x);
+        const T r1 = sub_rn(c[g].v.y, l[g].v.y);
+        res = fma_rn(r0, r0, res);
+        res = fma_rn(r1, r1, res);
+      }
+    }
+    for (; kl < nl; kl += kSNW) {
       const Pair<T> c = lds_pair(stg + (size_t)kl * kSTX + pe);
       const T* rv = lvec + (kl * 3 + 2) * RP;
       Pair<T> l = pmul(Pair<T>::splat(rv[0]), f[0]);
