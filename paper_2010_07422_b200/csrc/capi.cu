@@ -76,6 +76,7 @@ struct ircur_ctx {
   double* errors = nullptr;
   int* flags = nullptr;  // [0]=done [1]=iters [2]=converged [3]=nonfinite
   int* svd_steps = nullptr;  // subspace steps taken by the core SVD, per iteration
+  long long* svd_dbg = nullptr;  // per-phase clock64 totals of the SVD kernel (profiling)
   int* rowmap = nullptr;     // local row -> position in I (or -1), per iteration
   int* colmap = nullptr;     // column -> position in J (or -1), per iteration
   unsigned long long* maxbits = nullptr;
@@ -150,7 +151,13 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   sa.W = c->W; sa.sigma = c->sigma; sa.V = c->V; sa.inv = c->inv;
   sa.Wr = c->Wr; sa.PI = c->PI; sa.VS = c->VS; sa.QJ = c->QJ;
   sa.scratch = c->svd_scratch; sa.done = done; sa.steps_out = c->svd_steps + k;
+  // Ritz-residual target relative to lambda_1: round-off floor, relaxed in
+  // early iterations in proportion to e_{k-1} (an SVD perturbation delta
+  // moves e_k by ~delta/e_k relative)
   sa.tol = sizeof(T) == 8 ? 2e-14 : 1e-11;
+  sa.tol_scale = sizeof(T) == 8 ? 1e-11 : 1e-8;
+  sa.prev_err = k > 0 ? c->errors + (k - 1) : nullptr;
+  sa.dbg = c->profiling ? c->svd_dbg : nullptr;
   sa.maxsteps = 100;
   sa.salt = 0x1234567ull + (uint64_t)k * 7919ull;
   const int svd_cs = svd_cluster_size(nJ, mI, sa.kk);
@@ -278,7 +285,7 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->V, (size_t)max_cols * rank * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->inv, (size_t)rank * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->G, (size_t)max_cols * max_cols * sizeof(double)));
-  IR_CUDA_C(cudaMalloc(&c->svd_scratch, (size_t)max_cols * 32 * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->svd_scratch, 2 * (size_t)max_cols * 32 * sizeof(double)));
   c->max_partials = 4 * 2 * c->num_sms + 8192;  // strips: 4 sums per persistent CTA (<= 2/SM)
   IR_CUDA_C(cudaMalloc(&c->partials, (size_t)c->max_partials * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->rowmap, (size_t)local_rows * sizeof(int)));
@@ -288,6 +295,8 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->errors, (size_t)max_iter * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->flags, 16 * sizeof(int)));
   IR_CUDA_C(cudaMalloc(&c->svd_steps, (size_t)max_iter * sizeof(int)));
+  IR_CUDA_C(cudaMalloc(&c->svd_dbg, 16 * sizeof(long long)));
+  IR_CUDA_C(cudaMemsetAsync(c->svd_dbg, 0, 16 * sizeof(long long), c->stream));
   IR_CUDA_C(cudaMalloc(&c->maxbits, sizeof(unsigned long long)));
   IR_CUDA_C(cudaHostAlloc(&c->h_flags, 16 * sizeof(int), cudaHostAllocMapped));
   IR_CUDA_C(cudaHostGetDevicePointer((void**)&c->h_flags_dev, c->h_flags, 0));
@@ -306,7 +315,7 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U,
                   c->PoldI, c->QoldJ, c->Wr, c->PI, c->VS, c->QJ, c->W, c->sigma, c->V, c->inv,
                   c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps,
-                  c->rowmap, c->colmap};
+                  c->rowmap, c->colmap, c->svd_dbg};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -670,6 +679,15 @@ int ircur_get_svd_steps(ircur_ctx_t c, int n_iters, int* steps) {
   if (!c || !steps || n_iters < 0 || n_iters > c->max_iter) return fail(IRCUR_EINVAL, "bad arguments");
   IR_CUDA(cudaSetDevice(c->device));
   IR_CUDA(cudaMemcpyAsync(steps, c->svd_steps, n_iters * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  return IRCUR_OK;
+}
+
+int ircur_get_svd_phase_cycles(ircur_ctx_t c, long long* cycles16, int reset) {
+  if (!c || !cycles16) return fail(IRCUR_EINVAL, "bad arguments");
+  IR_CUDA(cudaSetDevice(c->device));
+  IR_CUDA(cudaMemcpyAsync(cycles16, c->svd_dbg, 16 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  if (reset) IR_CUDA(cudaMemsetAsync(c->svd_dbg, 0, 16 * sizeof(long long), c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));
   return IRCUR_OK;
 }

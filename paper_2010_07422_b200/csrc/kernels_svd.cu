@@ -4,18 +4,22 @@
 // PinvFactor.from_svd (cutoff sigma > 1e-12 sigma_max, matcore.py:156-165).
 // Only the top k = min(r, |I|, |J|) triplets are consumed, so instead of a
 // full dense SVD the core is factorised by block subspace iteration on the
-// Gram matrix G = U^T U with Rayleigh-Ritz extraction every step,
-// warm-started from the previous iterate's Q(:,J) and iterated until the
-// Ritz residuals reach fp64 round-off; a final Rayleigh-Ritz step on U
-// itself resolves small singular values to absolute fp64 accuracy, so the
-// pinv cutoff behaves like LAPACK's.  Block size kk = min(2r, |I|, |J|, 32).
+// Gram matrix G = U^T U with a Rayleigh-Ritz step every iteration,
+// warm-started from the previous iterate's Q(:,J), until the Ritz residuals
+// reach round-off (scaled by the previous e_k, see below); a final
+// Rayleigh-Ritz step on U itself resolves small singular values to absolute
+// fp64 accuracy so the pinv cutoff behaves like LAPACK's.
+// Block size kk = min(2r, |I|, |J|, 32).
 //
-// Layout: one thread-block cluster per core.  CTA q owns rows [lo_q, hi_q)
-// of G (resident in its shared memory for the whole call) and of the n x kk
-// block V; the full V is replicated in every CTA's shared memory and
-// re-assembled through L2 after each step; the small kk x kk sums go through
-// DSMEM in a fixed rank order, so every CTA holds bitwise-identical reduced
-// values and takes identical branches (deterministic, run to run).
+// One thread-block cluster per core.  CTA q owns rows [lo_q, hi_q) of G and
+// of the n x kk block V; the full V is replicated in every CTA's shared
+// memory and re-assembled through L2 after each step.  Per step there are
+// exactly two cluster-wide synchronisations: one DSMEM reduction (fixed rank
+// order) of [V^T G V | V^T V | previous Ritz residuals], and the all-gather
+// of the next block.  The Cholesky-QR of the block is folded into the
+// Rayleigh-Ritz problem (generalised eigenproblem through chol(V^T V)), and
+// the kk x kk eigenproblem runs on four warps under a named barrier.  Every
+// CTA holds bitwise-identical reduced values and takes identical branches.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -29,6 +33,7 @@ namespace ircur {
 constexpr int kSvdNT = 512;
 constexpr int kSvdNW = kSvdNT / 32;
 constexpr int kKMax = 32;
+constexpr int kEigNT = 128;  // threads running the small dense kernels
 
 // ------------------------------------------------------------------ gram
 // G = U^T U (n x n), 32x32 output tile per CTA, K = m in 32-row chunks.
@@ -66,8 +71,8 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U,
 // ------------------------------------------------------------ layout
 // Shared-memory layout in doubles; identical on host (size) and device.
 struct SvdLayout {
-  int n, m, kk, KP, HL, per, mper, rowsmax, ldgq, S, gq_smem;
-  int oV, oGq, oP, oBq, oXq, oH, oH2, oZ, oRed, oRout, oLam, oCs, oW, total;
+  int n, m, kk, KP, HL, per, mper, rowsmax, ldgq, S, gq_smem, RL;
+  int oV, oGq, oP, oBq, oXq, oH, oH2, oZ, oLc, oT, oRed, oRout, oRes, oLam, oCs, oW, total;
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -85,6 +90,7 @@ __host__ __device__ inline SvdLayout svd_layout(int n, int m, int kk, int cs) {
   int S = kSvdNW / (tasks > 0 ? tasks : 1);
   S = S < 1 ? 1 : (S > 4 ? 4 : S);
   L.S = S;
+  L.RL = 2 * kk * kk + kk;  // reduction record: H' | M | residuals
   int off = 0;
   L.oV = off; off += n * L.KP;
   L.oP = off; off += S * L.rowsmax * L.KP;
@@ -93,11 +99,14 @@ __host__ __device__ inline SvdLayout svd_layout(int n, int m, int kk, int cs) {
   L.oH = off; off += kk * L.HL;
   L.oH2 = off; off += kk * L.HL;
   L.oZ = off; off += kk * L.HL;
-  L.oRed = off; off += kk * kk + 2 * kk;
-  L.oRout = off; off += kk * kk + 2 * kk;
+  L.oLc = off; off += kk * L.HL;
+  L.oT = off; off += kk * L.HL;
+  L.oRed = off; off += 2 * L.RL;
+  L.oRout = off; off += L.RL;
+  L.oRes = off; off += kk;
   L.oLam = off; off += kk;
   L.oCs = off; off += 4 * kKMax;
-  L.oW = off; off += 2 * kKMax + 8;   // warp scratch / flags (as doubles)
+  L.oW = off; off += 2 * kKMax + 8;
   const int base = off;
   L.oGq = base;
   const size_t with_g = (size_t)(base + L.per * L.ldgq) * sizeof(double);
@@ -115,19 +124,25 @@ __device__ __forceinline__ double hash_uniform(uint64_t a, uint64_t b) {
 
 struct Sm {
   SvdLayout L;
-  double *V, *Gq, *P, *Bq, *Xq, *H, *H2, *Z, *red, *rout, *lam, *cs, *ws;
+  double *V, *Gq, *P, *Bq, *Xq, *H, *H2, *Z, *Lc, *T, *red, *rout, *res, *lam, *cs, *ws;
   int* flags;
 };
 
-__device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, Sm& S, int len) {
+// named barrier for the first kEigNT threads
+__device__ __forceinline__ void eig_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kEigNT) : "memory"); }
+
+// fixed-rank-order DSMEM reduction of red[buf][0:len) -> rout (one cluster sync;
+// red is double-buffered so peers may still be reading the other buffer)
+__device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, Sm& S, int buf, int len) {
+  double* src = S.red + buf * S.L.RL;
   cl.sync();
   const int CS = (int)cl.num_blocks();
   for (int e = threadIdx.x; e < len; e += kSvdNT) {
-    double s = *cl.map_shared_rank(S.red + e, 0);
-    for (int q = 1; q < CS; ++q) s += *cl.map_shared_rank(S.red + e, q);
+    double s = *cl.map_shared_rank(src + e, 0);
+    for (int q = 1; q < CS; ++q) s += *cl.map_shared_rank(src + e, q);
     S.rout[e] = s;
   }
-  cl.sync();
+  __syncthreads();
 }
 
 // Out(nr x kk, ld KP) = A(nr x n, lda) * V(n x kk, ld KP).  Warp tile:
@@ -182,36 +197,42 @@ __device__ void tiled_product(const double* A, int lda, int nr, int n, const dou
   __syncthreads();
 }
 
-// Cyclic Jacobi eigen-decomposition of the symmetric kk x kk S.H (round-robin
-// parallel ordering, J^T H J for all disjoint pairs of a round in one pass).
-// On exit S.lam holds eigenvalues in decreasing order and S.Z the matching
-// eigenvectors (columns).  Executed identically by every CTA of the cluster.
-__device__ void jacobi_eig(Sm& S, int kk) {
+// Cyclic Jacobi eigen-decomposition of the symmetric kk x kk S.H on the first
+// kEigNT threads (round-robin parallel ordering, J^T H J for all disjoint
+// pairs of a round in one pass, named barrier).  On exit S.lam holds the
+// eigenvalues in decreasing order and S.Z the matching eigenvectors.  Must be
+// called by the first kEigNT threads only; `thr_rel` sets the stopping
+// threshold relative to the largest diagonal entry.
+__device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullptr) {
   const int tid = threadIdx.x;
   const int HL = S.L.HL;
   double* H = S.H;
   double* Hn = S.H2;
-  for (int e = tid; e < kk * kk; e += kSvdNT) {
+  for (int e = tid; e < kk * kk; e += kEigNT) {
     const int i = e / kk, j = e - i * kk;
     S.Z[i * HL + j] = (i == j) ? 1.0 : 0.0;
   }
   const int np = (kk + 1) / 2;
   const int nply = 2 * np;
-  int* pairs = reinterpret_cast<int*>(S.cs + 2 * kKMax);  // [kKMax] partner of each index
+  int* pairs = reinterpret_cast<int*>(S.cs + 2 * kKMax);
   double scale = 0.0;
   for (int i = 0; i < kk; ++i) scale = fmax(scale, fabs(H[i * HL + i]));
-  const double thr = 4e-16 * scale;
-  __syncthreads();
+  const double thr = thr_rel * scale;
+  const double isc = scale > 0.0 ? 1.0 / scale : 1.0;  // keeps the fp32 tangent in range
+  eig_sync();
   for (int sweep = 0; sweep < 30; ++sweep) {
-    // early exit: any off-diagonal above threshold?
-    if (tid == 0) S.flags[0] = 0;
-    __syncthreads();
-    for (int e = tid; e < kk * kk; e += kSvdNT) {
+    int any = 0;
+    for (int e = tid; e < kk * kk; e += kEigNT) {
       const int i = e / kk, j = e - i * kk;
-      if (i < j && fabs(H[i * HL + j]) > thr) S.flags[0] = 1;
+      any |= (i < j && fabs(H[i * HL + j]) > thr);
     }
-    __syncthreads();
-    if (S.flags[0] == 0) break;
+    any = __any_sync(0xffffffffu, any);
+    if ((tid & 31) == 0) S.flags[2 + (tid >> 5)] = any;
+    eig_sync();
+    const int go = S.flags[2] | S.flags[3] | S.flags[4] | S.flags[5];
+    eig_sync();
+    if (!go) break;
+    if (dbg && blockIdx.x == 0 && tid == 0) dbg[13] += 1;
     for (int rd = 0; rd < nply - 1; ++rd) {
       if (tid < np) {
         const int pa = tid == 0 ? 0 : ((tid - 1 + rd) % (nply - 1)) + 1;
@@ -221,35 +242,37 @@ __device__ void jacobi_eig(Sm& S, int kk) {
         if (q < kk) {
           const double hpq = H[p * HL + q];
           if (fabs(hpq) > 1e-300 && fabs(hpq) > thr) {
+            // tan(theta) in fp32 (only the convergence rate depends on it);
+            // c = (1 + t^2)^{-1/2}, s = t c in fp64 from that t keep the
+            // transform orthogonal to fp64 round-off.
             const double hpp = H[p * HL + p], hqq = H[q * HL + q];
-            const double tau = (hqq - hpp) / (2.0 * hpq);
-            const double t = fabs(tau) > 1e150 ? 0.5 / tau
-                                               : (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            c = 1.0 / sqrt(1.0 + t * t);
+            const float d = (float)((hqq - hpp) * isc), h2 = (float)(2.0 * hpq * isc);
+            const float rt = sqrtf(fmaf(d, d, h2 * h2));
+            const float tf = __fdividef(h2, fabsf(d) + rt) * (d >= 0.f ? 1.f : -1.f);
+            const double t = (double)tf;
+            c = rsqrt(fma(t, t, 1.0));
             s = t * c;
           }
           pairs[p] = q;
           pairs[q] = p;
-          S.cs[2 * p] = c;  S.cs[2 * p + 1] = s;     // p is the "first" of its pair
-          S.cs[2 * q] = c;  S.cs[2 * q + 1] = -s;    // sign flip marks the second
+          S.cs[2 * p] = c;  S.cs[2 * p + 1] = s;     // first of the pair
+          S.cs[2 * q] = c;  S.cs[2 * q + 1] = -s;    // second (sign flip)
         } else if (p < kk) {
           pairs[p] = p;
           S.cs[2 * p] = 1.0; S.cs[2 * p + 1] = 0.0;
         }
       }
-      __syncthreads();
-      // new H = J^T H J; each entry from the 2x2 block of its row and column pairs
-      for (int e = tid; e < kk * kk; e += kSvdNT) {
+      eig_sync();
+      for (int e = tid; e < kk * kk; e += kEigNT) {
         const int a = e / kk, b = e - a * kk;
         const int pa_ = pairs[a], pb_ = pairs[b];
         const double ca = S.cs[2 * a], sa = S.cs[2 * a + 1];
         const double cb = S.cs[2 * b], sb = S.cs[2 * b + 1];
-        // row rotation: new row a = ca * row a - sa * row partner(a)   (sa < 0 for the second)
         const double r_b = ca * H[a * HL + b] - sa * H[pa_ * HL + b];
         const double r_pb = ca * H[a * HL + pb_] - sa * H[pa_ * HL + pb_];
         Hn[a * HL + b] = cb * r_b - sb * r_pb;
       }
-      for (int e = tid; e < kk * kk; e += kSvdNT) {
+      for (int e = tid; e < kk * kk; e += kEigNT) {
         const int i = e / kk, b = e - i * kk;
         const int pb_ = pairs[b];
         const double cb = S.cs[2 * b], sb = S.cs[2 * b + 1];
@@ -259,13 +282,11 @@ __device__ void jacobi_eig(Sm& S, int kk) {
           S.Z[i * HL + pb_] = sb * zp + cb * zq;
         }
       }
-      __syncthreads();
+      eig_sync();
       double* t = H; H = Hn; Hn = t;
     }
   }
-  // sort (descending, stable) via rank computation
-  int* perm = pairs;
-  __syncthreads();
+  int* perm = pairs + kKMax;
   if (tid < kk) {
     const double li = H[tid * HL + tid];
     int rk = 0;
@@ -273,28 +294,106 @@ __device__ void jacobi_eig(Sm& S, int kk) {
       const double lj = H[j * HL + j];
       rk += (lj > li) || (lj == li && j < tid);
     }
-    perm[kKMax + rk] = tid;
+    perm[rk] = tid;
   }
-  __syncthreads();
-  if (tid < kk) S.lam[tid] = H[perm[kKMax + tid] * HL + perm[kKMax + tid]];
-  for (int e = tid; e < kk * kk; e += kSvdNT) {
+  eig_sync();
+  if (tid < kk) S.lam[tid] = H[perm[tid] * HL + perm[tid]];
+  for (int e = tid; e < kk * kk; e += kEigNT) {
     const int i = e / kk, j = e - i * kk;
-    Hn[i * HL + j] = S.Z[i * HL + perm[kKMax + j]];
+    Hn[i * HL + j] = S.Z[i * HL + perm[j]];
   }
-  __syncthreads();
-  for (int e = tid; e < kk * kk; e += kSvdNT) {
+  eig_sync();
+  for (int e = tid; e < kk * kk; e += kEigNT) {
     const int i = e / kk, j = e - i * kk;
     S.Z[i * HL + j] = Hn[i * HL + j];
   }
-  __syncthreads();
+  eig_sync();
 }
 
-// X(nr x kk, ld KP) <- X Z  using tmp (nr x KP)
-__device__ void rotate_rows(double* X, int nr, int KP, int kk, const double* Z, int HL, double* tmp) {
+// Cholesky M = Lc Lc^T of the kk x kk Gram M (ld kk) by warp 0 of the eig
+// threads; returns 0 on breakdown.  Caller: first kEigNT threads.
+__device__ int cholesky_warp(const double* M, double* Lc, int HL, int kk, int* flag) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) == 0) {
+    int ok = 1;
+    for (int j = 0; j < kk; ++j) {
+      double p = 0.0;
+      for (int k2 = lane; k2 < j; k2 += 32) p = fma(Lc[j * HL + k2], Lc[j * HL + k2], p);
+      p = warp_sum(p);
+      double d = M[j * kk + j] - p;
+      if (!(d > 1e-300)) { ok = 0; d = 1.0; }
+      const double ir = rsqrt(d);  // 1 / L_jj (division-free)
+      for (int i = j + 1 + lane; i < kk; i += 32) {
+        double s2 = M[i * kk + j];
+        for (int k2 = 0; k2 < j; ++k2) s2 = fma(-Lc[i * HL + k2], Lc[j * HL + k2], s2);
+        Lc[i * HL + j] = s2 * ir;
+      }
+      if (lane == 0) {
+        Lc[j * HL + j] = d * ir;
+        Lc[j * HL + kk] = ir;  // reciprocal diagonal kept in the padding column
+      }
+      __syncwarp();
+    }
+    if (lane == 0) *flag = ok;
+  }
+  eig_sync();
+  return *flag;
+}
+
+// Rayleigh-Ritz on (H', M): H = Lc^{-1} H' Lc^{-T}, eig(H) = Z Lambda Z^T,
+// T = Lc^{-T} Z so that V T has orthonormal columns and diagonalises V^T G V.
+// Caller: first kEigNT threads.  Returns 0 if chol(M) broke down.
+__device__ int ritz_small(Sm& S, int kk, const double* Hp, const double* M, double thr_rel,
+                          long long* dbg = nullptr) {
+  const int tid = threadIdx.x, HL = S.L.HL;
+  const bool rec = dbg && blockIdx.x == 0 && tid == 0;
+  long long t0 = clock64();
+  if (!cholesky_warp(M, S.Lc, HL, kk, S.flags + 1)) return 0;
+  if (rec) { const long long t1 = clock64(); dbg[8] += t1 - t0; t0 = t1; }
+  // K = Lc^{-1} H'  (column c per thread): forward substitution
+  for (int c = tid; c < kk; c += kEigNT) {
+    for (int i = 0; i < kk; ++i) {
+      double s = Hp[i * kk + c];
+      for (int k2 = 0; k2 < i; ++k2) s = fma(-S.Lc[i * HL + k2], S.H2[k2 * HL + c], s);
+      S.H2[i * HL + c] = s * S.Lc[i * HL + kk];
+    }
+  }
+  eig_sync();
+  // H = (Lc^{-1} K^T)^T : row c of K^T is column c of K
+  for (int c = tid; c < kk; c += kEigNT) {
+    for (int i = 0; i < kk; ++i) {
+      double s = S.H2[c * HL + i];
+      for (int k2 = 0; k2 < i; ++k2) s = fma(-S.Lc[i * HL + k2], S.T[c * HL + k2], s);
+      S.T[c * HL + i] = s * S.Lc[i * HL + kk];
+    }
+  }
+  eig_sync();
+  for (int e = tid; e < kk * kk; e += kEigNT) {
+    const int i = e / kk, j = e - i * kk;
+    S.H[i * HL + j] = 0.5 * (S.T[i * HL + j] + S.T[j * HL + i]);
+  }
+  eig_sync();
+  if (rec) { const long long t1 = clock64(); dbg[9] += t1 - t0; t0 = t1; }
+  jacobi_eig(S, kk, thr_rel, dbg);
+  if (rec) { const long long t1 = clock64(); dbg[10] += t1 - t0; t0 = t1; dbg[14] += 1; }
+  // T = Lc^{-T} Z: back substitution per column
+  for (int c = tid; c < kk; c += kEigNT) {
+    for (int i = kk - 1; i >= 0; --i) {
+      double s = S.Z[i * HL + c];
+      for (int k2 = i + 1; k2 < kk; ++k2) s = fma(-S.Lc[k2 * HL + i], S.T[k2 * HL + c], s);
+      S.T[i * HL + c] = s * S.Lc[i * HL + kk];
+    }
+  }
+  eig_sync();
+  return 1;
+}
+
+// X(nr x kk, ld KP) <- X R (R kk x kk, ld HL) using tmp
+__device__ void rotate_rows(double* X, int nr, int KP, int kk, const double* Rm, int HL, double* tmp) {
   for (int e = threadIdx.x; e < nr * kk; e += kSvdNT) {
     const int i = e / kk, c = e - i * kk;
     double s = 0.0;
-    for (int j = 0; j < kk; ++j) s = fma(X[i * KP + j], Z[j * HL + c], s);
+    for (int j = 0; j < kk; ++j) s = fma(X[i * KP + j], Rm[j * HL + c], s);
     tmp[i * KP + c] = s;
   }
   __syncthreads();
@@ -305,50 +404,11 @@ __device__ void rotate_rows(double* X, int nr, int KP, int kk, const double* Z, 
   __syncthreads();
 }
 
-// Cholesky of the kk x kk Gram in G (ld kk) into Lo (lower, ld HL) by warp 0;
-// returns 0 on breakdown (non-positive pivot).
-__device__ int cholesky_warp(const double* Gr, double* Lo, int HL, int kk, int* flag) {
-  const int lane = threadIdx.x & 31;
-  if ((threadIdx.x >> 5) == 0) {
-    int ok = 1;
-    for (int j = 0; j < kk; ++j) {
-      double p = 0.0;
-      for (int k2 = lane; k2 < j; k2 += 32) p = fma(Lo[j * HL + k2], Lo[j * HL + k2], p);
-      p = warp_sum(p);
-      double d = Gr[j * kk + j] - p;
-      if (!(d > 1e-300)) { ok = 0; d = 1.0; }
-      const double ljj = sqrt(d);
-      for (int i = j + 1 + lane; i < kk; i += 32) {
-        double s2 = Gr[i * kk + j];
-        for (int k2 = 0; k2 < j; ++k2) s2 = fma(-Lo[i * HL + k2], Lo[j * HL + k2], s2);
-        Lo[i * HL + j] = s2 / ljj;
-      }
-      if (lane == 0) Lo[j * HL + j] = ljj;
-      __syncwarp();
-    }
-    if (lane == 0) *flag = ok;
-  }
-  __syncthreads();
-  return *flag;
-}
-
-// rows of X (nr x kk, ld KP): x <- x L^{-T}
-__device__ void trsm_rows(double* X, int nr, int KP, int kk, const double* Lo, int HL) {
-  for (int i = threadIdx.x; i < nr; i += kSvdNT) {
-    for (int c = 0; c < kk; ++c) {
-      double s = X[i * KP + c];
-      for (int k2 = 0; k2 < c; ++k2) s = fma(-X[i * KP + k2], Lo[c * HL + k2], s);
-      X[i * KP + c] = s / Lo[c * HL + c];
-    }
-  }
-  __syncthreads();
-}
-
 // Block-local CGS2 with random replacement on the FULL V (n x kk) — robust
-// fallback when the Cholesky-QR start breaks down (rank-deficient start).
+// path for a rank-deficient starting block.
 __device__ void cgs2_full(Sm& S, int n, int KP, int kk, uint64_t salt) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  double* dots = S.red;
+  double* dots = S.rout;
   for (int c = 0; c < kk; ++c) {
     for (int attempt = 0; attempt < 4; ++attempt) {
       double p = 0.0;
@@ -395,32 +455,6 @@ __device__ void cgs2_full(Sm& S, int n, int KP, int kk, uint64_t salt) {
   }
 }
 
-// Full-V orthonormalisation (redundant in every CTA): Cholesky-QR twice,
-// CGS2 fallback on breakdown.
-__device__ void orthonormalize_full(Sm& S, int n, int KP, int kk, uint64_t salt) {
-  const int HL = S.L.HL;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int e = threadIdx.x; e < kk * kk; e += kSvdNT) {
-      const int c1 = e / kk, c2 = e - c1 * kk;
-      double s = 0.0;
-      if (c2 <= c1)
-        for (int j = 0; j < n; ++j) s = fma(S.V[j * KP + c1], S.V[j * KP + c2], s);
-      S.rout[e] = s;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < kk * kk; e += kSvdNT) {
-      const int c1 = e / kk, c2 = e - c1 * kk;
-      if (c2 > c1) S.rout[e] = S.rout[c2 * kk + c1];
-    }
-    __syncthreads();
-    if (!cholesky_warp(S.rout, S.H2, HL, kk, S.flags + 1)) {
-      cgs2_full(S, n, KP, kk, salt);
-      return;
-    }
-    trsm_rows(S.V, n, KP, kk, S.H2, HL);
-  }
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ SvdArgs a) {
   if (a.done && *a.done) return;
@@ -433,15 +467,19 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   Sm S;
   S.L = svd_layout(n, m, kk, CS);
   const SvdLayout& L = S.L;
-  const int KP = L.KP, HL = L.HL;
+  const int KP = L.KP, HL = L.HL, RL = L.RL;
   S.V = svsm + L.oV; S.P = svsm + L.oP; S.Bq = svsm + L.oBq; S.Xq = svsm + L.oXq;
-  S.H = svsm + L.oH; S.H2 = svsm + L.oH2; S.Z = svsm + L.oZ; S.red = svsm + L.oRed;
-  S.rout = svsm + L.oRout; S.lam = svsm + L.oLam; S.cs = svsm + L.oCs; S.ws = svsm + L.oW;
+  S.H = svsm + L.oH; S.H2 = svsm + L.oH2; S.Z = svsm + L.oZ; S.Lc = svsm + L.oLc; S.T = svsm + L.oT;
+  S.red = svsm + L.oRed; S.rout = svsm + L.oRout; S.res = svsm + L.oRes; S.lam = svsm + L.oLam;
+  S.cs = svsm + L.oCs; S.ws = svsm + L.oW;
   S.flags = reinterpret_cast<int*>(svsm + L.oW + kKMax);
   S.Gq = svsm + L.oGq;
   const int lo = min(n, q * L.per), hi = min(n, lo + L.per), nr = hi - lo;
   const int mlo = min(m, q * L.mper), mhi = min(m, mlo + L.mper), mr = mhi - mlo;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x;
+  const bool eigt = tid < kEigNT;
+  const double eprev = a.prev_err ? fmin(1.0, fabs(*a.prev_err)) : 1.0;
+  const double tol = fmax(a.tol, a.tol_scale * eprev);
 
   // ---- 0. G rows of this CTA into shared memory; starting block V
   const double* Gq = a.G + (int64_t)lo * a.ldg;
@@ -462,132 +500,169 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     else v = hash_uniform(0x5EEDull + a.salt, (uint64_t)j * 64 + c);
     S.V[j * KP + c] = v;
   }
+  for (int c = tid; c < kk; c += kSvdNT) S.res[c] = 0.0;
   __syncthreads();
-  orthonormalize_full(S, n, KP, kk, a.salt);
 
+  int step = 0, buf = 0, gbuf = 0, redo = 0;
+  long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+#define PH(i) do { if (a.dbg) { const long long _t = clock64(); tph[i] += _t - tc; tc = _t; } } while (0)
+  bool prev_conv = false, have_prev = false;
   double prev_res = 1e300;
   int stall = 0;
-  int step = 0;
-  for (; step < a.maxsteps; ++step) {
+  for (;;) {
+    PH(7);
     // ---- 1. B_q = G(lo:hi, :) V
     tiled_product(Gq, ldgq, nr, n, S.V, KP, kk, S.Bq, S.P, L.S);
-    // ---- 2. H = V^T G V (partial over my rows) -> cluster sum
-    for (int e = tid; e < kk * kk; e += kSvdNT) {
-      const int c1 = e / kk, c2 = e - c1 * kk;
+    PH(0);
+    // ---- 2. one reduction: [V^T B | V^T V | previous Ritz residuals]
+    double* rb = S.red + buf * RL;
+    for (int e = tid; e < 2 * kk * kk; e += kSvdNT) {
+      const int which = e / (kk * kk);
+      const int e2 = e - which * kk * kk;
+      const int c1 = e2 / kk, c2 = e2 - c1 * kk;
+      const double* Y = which == 0 ? S.Bq : S.V + lo * KP;
       double s = 0.0;
-      for (int i = 0; i < nr; ++i) s = fma(S.V[(lo + i) * KP + c1], S.Bq[i * KP + c2], s);
-      S.red[e] = s;
+      for (int i = 0; i < nr; ++i) s = fma(S.V[(lo + i) * KP + c1], Y[i * KP + c2], s);
+      rb[e] = s;
     }
-    cluster_sum(cl, S, kk * kk);
-    for (int e = tid; e < kk * kk; e += kSvdNT) {
-      const int c1 = e / kk, c2 = e - c1 * kk;
-      S.H[c1 * HL + c2] = 0.5 * (S.rout[c1 * kk + c2] + S.rout[c2 * kk + c1]);
+    for (int c = tid; c < kk; c += kSvdNT) rb[2 * kk * kk + c] = S.res[c];
+    cluster_sum(cl, S, buf, RL);
+    buf ^= 1;
+    if (have_prev) {
+      double resmax = 0.0;
+      for (int c = 0; c < reff; ++c) resmax = fmax(resmax, sqrt(S.rout[2 * kk * kk + c]));
+      const double l0 = S.lam[0];  // Ritz values of the previous step
+      prev_conv = !(l0 > 0.0) || resmax <= tol * l0;
+      if (resmax > 0.5 * prev_res) ++stall; else stall = 0;
+      prev_res = resmax;
+      if (stall >= 3 && resmax <= 1e-11 * l0) prev_conv = true;
+    }
+    PH(1);
+    // ---- 3. Rayleigh-Ritz (generalised through chol(V^T V))
+    if (eigt) {
+      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, 4e-16, a.dbg);
+      if (tid == 0) S.flags[6] = ok;
     }
     __syncthreads();
-    jacobi_eig(S, kk);
-    // ---- 3. Ritz rotation of my rows: Xq <- V_q Z ; P <- B_q Z
+    if (!S.flags[6]) {
+      // rank-deficient start block: orthonormalise it robustly, redo the step
+      cgs2_full(S, n, KP, kk, a.salt + 77ull * (redo + 1));
+      __syncthreads();
+      if (++redo > 3) break;
+      continue;
+    }
+    PH(2);
+    // ---- 4. Ritz vectors X_q = V_q T (orthonormal), Y_q = B_q T (= G X)
     for (int e = tid; e < nr * kk; e += kSvdNT) {
       const int i = e / kk, c = e - i * kk;
-      double sv = 0.0, sb = 0.0;
+      double sx = 0.0, sy = 0.0;
       for (int j = 0; j < kk; ++j) {
-        const double z = S.Z[j * HL + c];
-        sv = fma(S.V[(lo + i) * KP + j], z, sv);
-        sb = fma(S.Bq[i * KP + j], z, sb);
+        const double t = S.T[j * HL + c];
+        sx = fma(S.V[(lo + i) * KP + j], t, sx);
+        sy = fma(S.Bq[i * KP + j], t, sy);
       }
-      S.Xq[i * KP + c] = sv;
-      S.P[i * KP + c] = sb;
+      S.Xq[i * KP + c] = sx;
+      S.P[i * KP + c] = sy;
     }
     __syncthreads();
-    // ---- 4. residuals ||B z_c - lam_c V z_c||^2 and the next block
-    //      Vn_c = B z_c / lam_c (significant lam) or V z_c (negligible lam)
+    const bool last = prev_conv || step + 1 >= a.maxsteps;
+    double* sc = a.scratch + (size_t)gbuf * n * kKMax;
+    if (last) {
+      for (int e = tid; e < nr * kk; e += kSvdNT) {
+        const int i = e / kk, c = e - i * kk;
+        sc[(int64_t)(lo + i) * kKMax + c] = S.Xq[i * KP + c];
+      }
+      break;
+    }
+    PH(3);
+    // ---- 5. this step's residuals (reduced with the next step) and next block
     const double lam0 = S.lam[0];
     const double sig_thr = 1e-10 * fabs(lam0);
-    if (tid < kk) {
-      const int c = tid;
+    for (int c = tid; c < kk; c += kSvdNT) {
       const double lc = S.lam[c];
       double rs = 0.0;
       for (int i = 0; i < nr; ++i) {
         const double d = S.P[i * KP + c] - lc * S.Xq[i * KP + c];
         rs = fma(d, d, rs);
       }
-      S.red[kk * kk + c] = rs;
+      S.res[c] = rs;
     }
     for (int e = tid; e < nr * kk; e += kSvdNT) {
       const int i = e / kk, c = e - i * kk;
       const double lc = S.lam[c];
-      S.Bq[i * KP + c] = (lc > sig_thr && lc > 0.0) ? S.P[i * KP + c] / lc : S.Xq[i * KP + c];
+      sc[(int64_t)(lo + i) * kKMax + c] = (lc > sig_thr && lc > 0.0) ? S.P[i * KP + c] / lc : S.Xq[i * KP + c];
     }
-    __syncthreads();
-    for (int e = tid; e < kk * kk; e += kSvdNT) {
-      const int c1 = e / kk, c2 = e - c1 * kk;
-      double s = 0.0;
-      for (int i = 0; i < nr; ++i) s = fma(S.Bq[i * KP + c1], S.Bq[i * KP + c2], s);
-      S.red[e] = s;
-    }
-    cluster_sum(cl, S, kk * kk + kk);
-    double resmax = 0.0;
-    for (int c = 0; c < reff; ++c) resmax = fmax(resmax, sqrt(S.rout[kk * kk + c]));
-    const bool conv = !(lam0 > 0.0) || resmax <= a.tol * lam0;
-    if (resmax > 0.5 * prev_res) ++stall; else stall = 0;
-    prev_res = resmax;
-    const bool give_up = (stall >= 3 && resmax <= 1e-11 * lam0);
-    if (conv || give_up || step + 1 == a.maxsteps) {
-      for (int e = tid; e < nr * kk; e += kSvdNT) {
-        const int i = e / kk, c = e - i * kk;
-        a.scratch[(int64_t)(lo + i) * kKMax + c] = S.Xq[i * KP + c];
-      }
-      break;
-    }
-    // ---- 5. Cholesky-QR of the next block (Gram = I + E^T E, well posed)
-    const int ok = cholesky_warp(S.rout, S.H2, HL, kk, S.flags + 1);
-    if (ok) trsm_rows(S.Bq, nr, KP, kk, S.H2, HL);
-    // ---- 6. all-gather the new block through global scratch (L2)
-    for (int e = tid; e < nr * kk; e += kSvdNT) {
-      const int i = e / kk, c = e - i * kk;
-      a.scratch[(int64_t)(lo + i) * kKMax + c] = S.Bq[i * KP + c];
-    }
+    PH(4);
+    // ---- 6. all-gather the next block through L2 (double-buffered scratch)
     __threadfence();
     cl.sync();
     for (int e = tid; e < n * kk; e += kSvdNT) {
       const int j = e / kk, c = e - j * kk;
-      S.V[j * KP + c] = a.scratch[(int64_t)j * kKMax + c];
+      S.V[j * KP + c] = sc[(int64_t)j * kKMax + c];
+    }
+    gbuf ^= 1;
+    have_prev = true;
+    PH(5);
+    ++step;
+    __syncthreads();
+  }
+  {
+    // gather the final Ritz block
+    const double* sc = a.scratch + (size_t)gbuf * n * kKMax;
+    __threadfence();
+    cl.sync();
+    for (int e = tid; e < n * kk; e += kSvdNT) {
+      const int j = e / kk, c = e - j * kk;
+      S.V[j * KP + c] = sc[(int64_t)j * kKMax + c];
     }
     __syncthreads();
-    if (!ok) orthonormalize_full(S, n, KP, kk, a.salt + 77ull * (step + 1));
-    cl.sync();  // nobody overwrites scratch before every CTA has copied it
   }
-  __threadfence();
-  cl.sync();
-  for (int e = tid; e < n * kk; e += kSvdNT) {
-    const int j = e / kk, c = e - j * kk;
-    S.V[j * KP + c] = a.scratch[(int64_t)j * kKMax + c];
-  }
-  __syncthreads();
   if (q == 0 && tid == 0 && a.steps_out) *a.steps_out = step + 1;
+  PH(6);
+  if (a.dbg && q == 0 && tid == 0)
+    for (int i = 0; i < 8; ++i) a.dbg[i] += tph[i];
+#undef PH
 
   // ---- 7. Rayleigh-Ritz on U itself: Y = U V (my m-rows), H2 = Y^T Y
   tiled_product(a.U + (int64_t)mlo * a.ldu, a.ldu, mr, n, S.V, KP, kk, S.Xq, S.P, L.S);
-  for (int e = tid; e < kk * kk; e += kSvdNT) {
-    const int c1 = e / kk, c2 = e - c1 * kk;
-    double s = 0.0;
-    for (int i = 0; i < mr; ++i) s = fma(S.Xq[i * KP + c1], S.Xq[i * KP + c2], s);
-    S.red[e] = s;
+  {
+    double* rb = S.red + buf * RL;
+    for (int e = tid; e < kk * kk; e += kSvdNT) {
+      const int c1 = e / kk, c2 = e - c1 * kk;
+      double s = 0.0;
+      for (int i = 0; i < mr; ++i) s = fma(S.Xq[i * KP + c1], S.Xq[i * KP + c2], s);
+      rb[e] = s;
+    }
+    cluster_sum(cl, S, buf, kk * kk);
+    buf ^= 1;
   }
-  cluster_sum(cl, S, kk * kk);
-  for (int e = tid; e < kk * kk; e += kSvdNT) {
-    const int c1 = e / kk, c2 = e - c1 * kk;
-    S.H[c1 * HL + c2] = 0.5 * (S.rout[c1 * kk + c2] + S.rout[c2 * kk + c1]);
+  if (eigt) {
+    for (int e = tid; e < kk * kk; e += kEigNT) {
+      const int c1 = e / kk, c2 = e - c1 * kk;
+      S.H[c1 * HL + c2] = 0.5 * (S.rout[c1 * kk + c2] + S.rout[c2 * kk + c1]);
+    }
+    eig_sync();
+    jacobi_eig(S, kk, 4e-16);
   }
   __syncthreads();
-  jacobi_eig(S, kk);
   rotate_rows(S.Xq, mr, KP, kk, S.Z, HL, S.P);
-  rotate_rows(S.V + lo * KP, nr, KP, kk, S.Z, HL, S.P);  // only my rows are written out
-  for (int c = tid; c < kk; c += kSvdNT) {
-    double s = 0.0;
-    for (int i = 0; i < mr; ++i) s = fma(S.Xq[i * KP + c], S.Xq[i * KP + c], s);
-    S.red[c] = s;
+  {
+    // full V (needed for QJ = G V Sigma^+), in chunks that fit the temp buffer
+    const int chunk = L.S * L.rowsmax;
+    for (int j0 = 0; j0 < n; j0 += chunk)
+      rotate_rows(S.V + j0 * KP, min(chunk, n - j0), KP, kk, S.Z, HL, S.P);
   }
-  cluster_sum(cl, S, kk);
+  {
+    double* rb = S.red + buf * RL;
+    for (int c = tid; c < kk; c += kSvdNT) {
+      double s = 0.0;
+      for (int i = 0; i < mr; ++i) s = fma(S.Xq[i * KP + c], S.Xq[i * KP + c], s);
+      rb[c] = s;
+    }
+    cluster_sum(cl, S, buf, kk);
+    buf ^= 1;
+  }
   if (tid < kk) S.lam[tid] = sqrt(S.rout[tid]);  // sigma
   __syncthreads();
   const double smax = S.lam[0];
@@ -633,11 +708,23 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     a.V[(int64_t)(lo + i) * r + c] = vv;
     VS[(int64_t)(lo + i) * r + c] = (T)vs;
   }
+  // QJ = U^T W = G V Sigma^{-1} for my n-rows (zero for deficient columns)
+  tiled_product(Gq, ldgq, nr, n, S.V, KP, kk, S.Bq, S.P, L.S);
+  for (int e = tid; e < nr * r; e += kSvdNT) {
+    const int i = e / r, c = e - i * r;
+    double v = 0.0;
+    if (c < reff) {
+      const double sg = S.lam[c];
+      if (sg > 1e-14 * smax && sg > 0.0) v = S.Bq[i * KP + c] / sg;
+    }
+    QJ[(int64_t)(lo + i) * r + c] = (T)v;
+  }
   __threadfence();
   cl.sync();
   if (ndef > 0 && q == 0) {
     // CGS2 completion of W's deficient columns with unit-vector candidates
-    double* dots = S.red;
+    double* dots = S.rout;
+    const int lane = tid & 31, w = tid >> 5;
     for (int c = 0; c < reff; ++c) {
       const double sg = S.lam[c];
       if (sg > 1e-14 * smax && sg > 0.0) continue;
@@ -685,38 +772,21 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     const int i = e / r, c = e - i * r;
     Wr[(int64_t)(mlo + i) * r + c] = (T)a.W[(int64_t)(mlo + i) * r + c];
   }
-  // QJ(j, c) = sum_i W(i, c) U(i, j) for my n-rows: lanes over j (coalesced U rows)
-  for (int j0 = lo + w * 32; j0 < hi; j0 += kSvdNW * 32) {
-    const int j = j0 + lane;
-    double acc[kMaxRank];
-#pragma unroll
-    for (int c = 0; c < kMaxRank; ++c) acc[c] = 0.0;
-    if (j < hi) {
-      for (int i = 0; i < m; ++i) {
-        const double u = a.U[(int64_t)i * a.ldu + j];
-        const double* wrow = a.W + (int64_t)i * r;
-#pragma unroll
-        for (int c = 0; c < kMaxRank; ++c)
-          if (c < r) acc[c] = fma(wrow[c], u, acc[c]);
-      }
-#pragma unroll
-      for (int c = 0; c < kMaxRank; ++c)
-        if (c < r) QJ[(int64_t)j * r + c] = (T)acc[c];
-    }
-  }
 }
 
 size_t svd_smem_bytes(int n, int m, int kk, int cs) {
   return (size_t)svd_layout(n, m, kk, cs).total * sizeof(double);
 }
 
-// ~32 rows of G per CTA, more CTAs (up to 16) until G's row block fits in
-// shared memory next to the replicated V.
+// ~32 rows of G per CTA; more CTAs (up to 16) while that lets G's row block
+// stay resident in shared memory next to the replicated V.
 int svd_pick_cluster(int n, int m, int kk) {
   int cs = (n + 31) / 32;
   if (cs < 1) cs = 1;
   if (cs > 16) cs = 16;
-  while (cs < 16 && !svd_layout(n, m, kk, cs).gq_smem) ++cs;
+  int c2 = cs;
+  while (c2 < 16 && !svd_layout(n, m, kk, c2).gq_smem) ++c2;
+  if (svd_layout(n, m, kk, c2).gq_smem) cs = c2;
   return cs;
 }
 
