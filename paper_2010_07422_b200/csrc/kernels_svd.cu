@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U,
 // Shared-memory layout in doubles; identical on host (size) and device.
 struct SvdLayout {
   int n, m, kk, KP, HL, per, mper, rowsmax, ldgq, S, gq_smem, RL;
-  int oV, oGq, oP, oBq, oXq, oH, oH2, oZ, oLc, oT, oRed, oRout, oRes, oLam, oCs, oW, total;
+  int oV, oGq, oP, oBq, oXq, oH, oH2, oZ, oLc, oT, oRed, oRout, oRes, oLam, oCs, oW, oPt, total;
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -107,6 +107,7 @@ __host__ __device__ inline SvdLayout svd_layout(int n, int m, int kk, int cs) {
   L.oLam = off; off += kk;
   L.oCs = off; off += 4 * kKMax;
   L.oW = off; off += 2 * kKMax + 8;
+  L.oPt = off; off += kKMax * kKMax * 3 / 4;  // partner table (1024 ints) + entry table (1024 shorts)
   const int base = off;
   L.oGq = base;
   const size_t with_g = (size_t)(base + L.per * L.ldgq) * sizeof(double);
@@ -126,6 +127,7 @@ struct Sm {
   SvdLayout L;
   double *V, *Gq, *P, *Bq, *Xq, *H, *H2, *Z, *Lc, *T, *red, *rout, *res, *lam, *cs, *ws;
   int* flags;
+  int* ptab;
 };
 
 // named barrier for the first kEigNT threads
@@ -206,25 +208,42 @@ __device__ void tiled_product(const double* A, int lda, int nr, int n, const dou
 __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullptr) {
   const int tid = threadIdx.x;
   const int HL = S.L.HL;
+  constexpr int NE = kKMax * kKMax / kEigNT;  // matrix entries per thread (<= 8)
   double* H = S.H;
   double* Hn = S.H2;
-  for (int e = tid; e < kk * kk; e += kEigNT) {
-    const int i = e / kk, j = e - i * kk;
-    S.Z[i * HL + j] = (i == j) ? 1.0 : 0.0;
+  double* Z = S.Z;
+  double* Zn = S.T;  // free while the eigenproblem is solved
+  const int nply = kk + (kk & 1);
+  const int nrd = nply - 1;
+  int* ptab = S.ptab;  // ptab[rd * nply + x] = partner of x in round rd (circle method)
+  for (int e = tid; e < nrd * nply; e += kEigNT) {
+    const int rd = e / nply, pos = e - rd * nply;
+    const int x = pos == 0 ? 0 : ((pos - 1 + rd) % nrd) + 1;
+    const int pp = nply - 1 - pos;
+    const int y = pp == 0 ? 0 : ((pp - 1 + rd) % nrd) + 1;
+    ptab[rd * nply + x] = y;
   }
-  const int np = (kk + 1) / 2;
-  const int nply = 2 * np;
-  int* pairs = reinterpret_cast<int*>(S.cs + 2 * kKMax);
+  // entry coordinates, packed (a << 8 | b), in the padding column-free tail
+  // of the partner table (kk^2 <= 1024 shorts)
+  unsigned short* etab = reinterpret_cast<unsigned short*>(ptab + kKMax * kKMax);
+  for (int e = tid; e < kk * kk; e += kEigNT) {
+    const int a = e / kk, b = e - a * kk;
+    etab[e] = (unsigned short)((a << 8) | b);
+    Z[a * HL + b] = (a == b) ? 1.0 : 0.0;
+  }
+  (void)NE;
   double scale = 0.0;
   for (int i = 0; i < kk; ++i) scale = fmax(scale, fabs(H[i * HL + i]));
   const double thr = thr_rel * scale;
   const double isc = scale > 0.0 ? 1.0 / scale : 1.0;  // keeps the fp32 tangent in range
   eig_sync();
+  const int nent = kk * kk;
   for (int sweep = 0; sweep < 30; ++sweep) {
     int any = 0;
-    for (int e = tid; e < kk * kk; e += kEigNT) {
-      const int i = e / kk, j = e - i * kk;
-      any |= (i < j && fabs(H[i * HL + j]) > thr);
+    for (int e = tid; e < nent; e += kEigNT) {
+      const int ab = etab[e];
+      const int a = ab >> 8, b = ab & 255;
+      any |= (a < b && fabs(H[a * HL + b]) > thr);
     }
     any = __any_sync(0xffffffffu, any);
     if ((tid & 31) == 0) S.flags[2 + (tid >> 5)] = any;
@@ -233,13 +252,12 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullp
     eig_sync();
     if (!go) break;
     if (dbg && blockIdx.x == 0 && tid == 0) dbg[13] += 1;
-    for (int rd = 0; rd < nply - 1; ++rd) {
-      if (tid < np) {
-        const int pa = tid == 0 ? 0 : ((tid - 1 + rd) % (nply - 1)) + 1;
-        const int pb = ((nply - 2 - tid + rd) % (nply - 1)) + 1;
-        const int p = min(pa, pb), q = max(pa, pb);
-        double c = 1.0, s = 0.0;
-        if (q < kk) {
+    for (int rd = 0; rd < nrd; ++rd) {
+      const int* pt = ptab + rd * nply;
+      if (tid < kk) {
+        const int p = tid, q = pt[p];
+        if (q < kk && p < q) {
+          double c = 1.0, s = 0.0;
           const double hpq = H[p * HL + q];
           if (fabs(hpq) > 1e-300 && fabs(hpq) > thr) {
             // tan(theta) in fp32 (only the convergence rate depends on it);
@@ -253,40 +271,38 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullp
             c = rsqrt(fma(t, t, 1.0));
             s = t * c;
           }
-          pairs[p] = q;
-          pairs[q] = p;
           S.cs[2 * p] = c;  S.cs[2 * p + 1] = s;     // first of the pair
           S.cs[2 * q] = c;  S.cs[2 * q + 1] = -s;    // second (sign flip)
-        } else if (p < kk) {
-          pairs[p] = p;
+        } else if (q >= kk) {
           S.cs[2 * p] = 1.0; S.cs[2 * p + 1] = 0.0;
         }
       }
       eig_sync();
-      for (int e = tid; e < kk * kk; e += kEigNT) {
-        const int a = e / kk, b = e - a * kk;
-        const int pa_ = pairs[a], pb_ = pairs[b];
+      for (int e = tid; e < nent; e += kEigNT) {
+        const int ab = etab[e];
+        const int a = ab >> 8, b = ab & 255;
+        const int x = pt[a], y = pt[b];
+        const int pa = x < kk ? x : a, pb = y < kk ? y : b;
         const double ca = S.cs[2 * a], sa = S.cs[2 * a + 1];
         const double cb = S.cs[2 * b], sb = S.cs[2 * b + 1];
-        const double r_b = ca * H[a * HL + b] - sa * H[pa_ * HL + b];
-        const double r_pb = ca * H[a * HL + pb_] - sa * H[pa_ * HL + pb_];
+        const double r_b = ca * H[a * HL + b] - sa * H[pa * HL + b];
+        const double r_pb = ca * H[a * HL + pb] - sa * H[pa * HL + pb];
         Hn[a * HL + b] = cb * r_b - sb * r_pb;
-      }
-      for (int e = tid; e < kk * kk; e += kEigNT) {
-        const int i = e / kk, b = e - i * kk;
-        const int pb_ = pairs[b];
-        const double cb = S.cs[2 * b], sb = S.cs[2 * b + 1];
-        if (sb != 0.0 && b < pb_) {
-          const double zp = S.Z[i * HL + b], zq = S.Z[i * HL + pb_];
-          S.Z[i * HL + b] = cb * zp - sb * zq;
-          S.Z[i * HL + pb_] = sb * zp + cb * zq;
-        }
+        Zn[a * HL + b] = cb * Z[a * HL + b] - sb * Z[a * HL + pb];  // Z <- Z J
       }
       eig_sync();
       double* t = H; H = Hn; Hn = t;
+      t = Z; Z = Zn; Zn = t;
     }
   }
-  int* perm = pairs + kKMax;
+  if (Z != S.Z) {
+    for (int e = tid; e < kk * kk; e += kEigNT) {
+      const int i = e / kk, j = e - i * kk;
+      S.Z[i * HL + j] = Z[i * HL + j];
+    }
+    eig_sync();
+  }
+  int* perm = reinterpret_cast<int*>(S.cs + 2 * kKMax) + kKMax;
   if (tid < kk) {
     const double li = H[tid * HL + tid];
     int rk = 0;
@@ -473,6 +489,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   S.red = svsm + L.oRed; S.rout = svsm + L.oRout; S.res = svsm + L.oRes; S.lam = svsm + L.oLam;
   S.cs = svsm + L.oCs; S.ws = svsm + L.oW;
   S.flags = reinterpret_cast<int*>(svsm + L.oW + kKMax);
+  S.ptab = reinterpret_cast<int*>(svsm + L.oPt);
   S.Gq = svsm + L.oGq;
   const int lo = min(n, q * L.per), hi = min(n, lo + L.per), nr = hi - lo;
   const int mlo = min(m, q * L.mper), mhi = min(m, mlo + L.mper), mr = mhi - mlo;
