@@ -6,20 +6,22 @@
 // full dense SVD the core is factorised by block subspace iteration on the
 // Gram matrix G = U^T U with a Rayleigh-Ritz step every iteration,
 // warm-started from the previous iterate's Q(:,J), until the Ritz residuals
-// reach round-off (scaled by the previous e_k, see below); a final
-// Rayleigh-Ritz step on U itself resolves small singular values to absolute
-// fp64 accuracy so the pinv cutoff behaves like LAPACK's.
+// reach round-off (scaled by the previous e_k); a final
+// Rayleigh-Ritz step on U itself (converged Jacobi) resolves small singular
+// values to absolute fp64 accuracy, so the pinv cutoff behaves like LAPACK's.
 // Block size kk = min(2r, |I|, |J|, 32).
 //
-// One thread-block cluster per core.  CTA q owns rows [lo_q, hi_q) of G and
-// of the n x kk block V; the full V is replicated in every CTA's shared
-// memory and re-assembled through L2 after each step.  Per step there are
-// exactly two cluster-wide synchronisations: one DSMEM reduction (fixed rank
-// order) of [V^T G V | V^T V | previous Ritz residuals], and the all-gather
-// of the next block.  The Cholesky-QR of the block is folded into the
-// Rayleigh-Ritz problem (generalised eigenproblem through chol(V^T V)), and
-// the kk x kk eigenproblem runs on four warps under a named barrier.  Every
-// CTA holds bitwise-identical reduced values and takes identical branches.
+// One thread-block cluster per core.  CTA q owns rows [lo_q, hi_q) of G
+// (resident in its shared memory for the whole call) and of the n x kk block
+// V.  The full V lives in a double-buffered L2 scratch and is read through
+// L1 by the G-row-block product.  Per step there are exactly two
+// cluster-wide synchronisations: one DSMEM reduction (fixed rank order) of
+// [V^T G V | V^T V | previous Ritz residuals], and the publication of the
+// next block.  The Cholesky-QR of the block is folded into the Rayleigh-Ritz
+// problem (generalised eigenproblem through chol(V^T V)); the kk x kk
+// eigenproblem runs on four warps under a named barrier.  Every CTA holds
+// bitwise-identical reduced values and takes identical branches
+// (deterministic run to run).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -34,6 +36,7 @@ constexpr int kSvdNT = 512;
 constexpr int kSvdNW = kSvdNT / 32;
 constexpr int kKMax = 32;
 constexpr int kEigNT = 128;  // threads running the small dense kernels
+constexpr int kLdV = kKMax;  // leading dimension of V in the L2 scratch
 
 // ------------------------------------------------------------------ gram
 // G = U^T U (n x n), 32x32 output tile per CTA, K = m in 32-row chunks.
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U,
 // Shared-memory layout in doubles; identical on host (size) and device.
 struct SvdLayout {
   int n, m, kk, KP, HL, per, mper, rowsmax, ldgq, S, gq_smem, RL;
-  int oV, oGq, oP, oBq, oXq, oH, oH2, oZ, oLc, oT, oRed, oRout, oRes, oLam, oCs, oW, oPt, total;
+  int oVq, oGq, oP, oBq, oXq, oH, oH2, oZ, oLc, oT, oRed, oRout, oRes, oLam, oCs, oW, oPt, total;
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -92,7 +95,7 @@ __host__ __device__ inline SvdLayout svd_layout(int n, int m, int kk, int cs) {
   L.S = S;
   L.RL = 2 * kk * kk + kk;  // reduction record: H' | M | residuals
   int off = 0;
-  L.oV = off; off += n * L.KP;
+  L.oVq = off; off += L.rowsmax * L.KP;
   L.oP = off; off += S * L.rowsmax * L.KP;
   L.oBq = off; off += L.rowsmax * L.KP;
   L.oXq = off; off += L.rowsmax * L.KP;
@@ -125,7 +128,7 @@ __device__ __forceinline__ double hash_uniform(uint64_t a, uint64_t b) {
 
 struct Sm {
   SvdLayout L;
-  double *V, *Gq, *P, *Bq, *Xq, *H, *H2, *Z, *Lc, *T, *red, *rout, *res, *lam, *cs, *ws;
+  double *Vq, *Gq, *P, *Bq, *Xq, *H, *H2, *Z, *Lc, *T, *red, *rout, *res, *lam, *cs, *ws;
   int* flags;
   int* ptab;
 };
@@ -147,13 +150,13 @@ __device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, Sm& S, int bu
   __syncthreads();
 }
 
-// Out(nr x kk, ld KP) = A(nr x n, lda) * V(n x kk, ld KP).  Warp tile:
+// Out(nr x kk, ld KP) = A(nr x n, lda) * V(n x kk, ld ldv).  Warp tile:
 // 8 rows x 16 cols, lane = (row pair, col pair) so that the A loads are
 // 4-way and the V loads 8-way broadcasts; the inner dimension is split in S
-// contiguous chunks whose partial tiles are summed in a fixed order.
-// A may live in shared or global memory (generic pointer).
-__device__ void tiled_product(const double* A, int lda, int nr, int n, const double* V, int KP, int kk,
-                              double* Out, double* partial, int S) {
+// contiguous chunks whose partial tiles are summed in a fixed order.  A and
+// V may live in shared or global memory (generic pointers).
+__device__ void tiled_product(const double* A, int lda, int nr, int n, const double* V, int ldv, int KP,
+                              int kk, double* Out, double* partial, int S) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int li = lane >> 3, lc = lane & 7;
   const int rt_n = ceil_div(nr, 8), ct_n = ceil_div(kk, 16);
@@ -173,7 +176,7 @@ __device__ void tiled_product(const double* A, int lda, int nr, int n, const dou
 #pragma unroll 4
     for (int j = j0; j < j1; ++j) {
       const double a0 = Aa[j], a1 = Ab[j];
-      const double v0 = V[j * KP + ca], v1 = V[j * KP + cb];
+      const double v0 = V[(int64_t)j * ldv + ca], v1 = V[(int64_t)j * ldv + cb];
       s00 = fma(a0, v0, s00);
       s01 = fma(a0, v1, s01);
       s10 = fma(a1, v0, s10);
@@ -200,15 +203,16 @@ __device__ void tiled_product(const double* A, int lda, int nr, int n, const dou
 }
 
 // Cyclic Jacobi eigen-decomposition of the symmetric kk x kk S.H on the first
-// kEigNT threads (round-robin parallel ordering, J^T H J for all disjoint
-// pairs of a round in one pass, named barrier).  On exit S.lam holds the
-// eigenvalues in decreasing order and S.Z the matching eigenvectors.  Must be
-// called by the first kEigNT threads only; `thr_rel` sets the stopping
-// threshold relative to the largest diagonal entry.
-__device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullptr) {
+// kEigNT threads (round-robin parallel ordering from a partner table; J^T H J
+// for all disjoint pairs of a round in one pass; named barrier).  On exit
+// S.lam holds the eigenvalues in decreasing order and S.Z the matching
+// eigenvectors.  `thr_rel` is the stopping threshold relative to the largest
+// diagonal entry, `max_sweeps` caps the work (an inexact Z only costs the
+// subspace iteration an extra step; the final extraction runs to
+// convergence).  Caller: the first kEigNT threads.
+__device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long long* dbg = nullptr) {
   const int tid = threadIdx.x;
   const int HL = S.L.HL;
-  constexpr int NE = kKMax * kKMax / kEigNT;  // matrix entries per thread (<= 8)
   double* H = S.H;
   double* Hn = S.H2;
   double* Z = S.Z;
@@ -223,22 +227,19 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullp
     const int y = pp == 0 ? 0 : ((pp - 1 + rd) % nrd) + 1;
     ptab[rd * nply + x] = y;
   }
-  // entry coordinates, packed (a << 8 | b), in the padding column-free tail
-  // of the partner table (kk^2 <= 1024 shorts)
-  unsigned short* etab = reinterpret_cast<unsigned short*>(ptab + kKMax * kKMax);
+  unsigned short* etab = reinterpret_cast<unsigned short*>(ptab + kKMax * kKMax);  // (a << 8 | b)
   for (int e = tid; e < kk * kk; e += kEigNT) {
     const int a = e / kk, b = e - a * kk;
     etab[e] = (unsigned short)((a << 8) | b);
     Z[a * HL + b] = (a == b) ? 1.0 : 0.0;
   }
-  (void)NE;
   double scale = 0.0;
   for (int i = 0; i < kk; ++i) scale = fmax(scale, fabs(H[i * HL + i]));
   const double thr = thr_rel * scale;
   const double isc = scale > 0.0 ? 1.0 / scale : 1.0;  // keeps the fp32 tangent in range
   eig_sync();
   const int nent = kk * kk;
-  for (int sweep = 0; sweep < 30; ++sweep) {
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     int any = 0;
     for (int e = tid; e < nent; e += kEigNT) {
       const int ab = etab[e];
@@ -254,6 +255,7 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullp
     if (dbg && blockIdx.x == 0 && tid == 0) dbg[13] += 1;
     for (int rd = 0; rd < nrd; ++rd) {
       const int* pt = ptab + rd * nply;
+      int rot = 0;
       if (tid < kk) {
         const int p = tid, q = pt[p];
         if (q < kk && p < q) {
@@ -270,6 +272,7 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullp
             const double t = (double)tf;
             c = rsqrt(fma(t, t, 1.0));
             s = t * c;
+            rot = 1;
           }
           S.cs[2 * p] = c;  S.cs[2 * p + 1] = s;     // first of the pair
           S.cs[2 * q] = c;  S.cs[2 * q + 1] = -s;    // second (sign flip)
@@ -277,7 +280,11 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullp
           S.cs[2 * p] = 1.0; S.cs[2 * p + 1] = 0.0;
         }
       }
+      rot = __any_sync(0xffffffffu, rot);  // rotating threads all live in warp 0 (kk <= 32)
+      int* rflag = S.flags + 8 + (rd & 1);  // alternate slots: no barrier needed when skipping
+      if (tid == 0) *rflag = rot;
       eig_sync();
+      if (!*rflag) continue;  // nothing rotates this round: H, Z unchanged
       for (int e = tid; e < nent; e += kEigNT) {
         const int ab = etab[e];
         const int a = ab >> 8, b = ab & 255;
@@ -327,7 +334,8 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, long long* dbg = nullp
 }
 
 // Cholesky M = Lc Lc^T of the kk x kk Gram M (ld kk) by warp 0 of the eig
-// threads; returns 0 on breakdown.  Caller: first kEigNT threads.
+// threads (reciprocal diagonal kept in column kk); returns 0 on breakdown.
+// Caller: first kEigNT threads.
 __device__ int cholesky_warp(const double* M, double* Lc, int HL, int kk, int* flag) {
   const int lane = threadIdx.x & 31;
   if ((threadIdx.x >> 5) == 0) {
@@ -346,7 +354,7 @@ __device__ int cholesky_warp(const double* M, double* Lc, int HL, int kk, int* f
       }
       if (lane == 0) {
         Lc[j * HL + j] = d * ir;
-        Lc[j * HL + kk] = ir;  // reciprocal diagonal kept in the padding column
+        Lc[j * HL + kk] = ir;
       }
       __syncwarp();
     }
@@ -359,15 +367,14 @@ __device__ int cholesky_warp(const double* M, double* Lc, int HL, int kk, int* f
 // Rayleigh-Ritz on (H', M): H = Lc^{-1} H' Lc^{-T}, eig(H) = Z Lambda Z^T,
 // T = Lc^{-T} Z so that V T has orthonormal columns and diagonalises V^T G V.
 // Caller: first kEigNT threads.  Returns 0 if chol(M) broke down.
-__device__ int ritz_small(Sm& S, int kk, const double* Hp, const double* M, double thr_rel,
+__device__ int ritz_small(Sm& S, int kk, const double* Hp, const double* M, double thr_rel, int max_sweeps,
                           long long* dbg = nullptr) {
   const int tid = threadIdx.x, HL = S.L.HL;
   const bool rec = dbg && blockIdx.x == 0 && tid == 0;
   long long t0 = clock64();
   if (!cholesky_warp(M, S.Lc, HL, kk, S.flags + 1)) return 0;
   if (rec) { const long long t1 = clock64(); dbg[8] += t1 - t0; t0 = t1; }
-  // K = Lc^{-1} H'  (column c per thread): forward substitution
-  for (int c = tid; c < kk; c += kEigNT) {
+  for (int c = tid; c < kk; c += kEigNT) {  // K = Lc^{-1} H' (forward substitution)
     for (int i = 0; i < kk; ++i) {
       double s = Hp[i * kk + c];
       for (int k2 = 0; k2 < i; ++k2) s = fma(-S.Lc[i * HL + k2], S.H2[k2 * HL + c], s);
@@ -375,8 +382,7 @@ __device__ int ritz_small(Sm& S, int kk, const double* Hp, const double* M, doub
     }
   }
   eig_sync();
-  // H = (Lc^{-1} K^T)^T : row c of K^T is column c of K
-  for (int c = tid; c < kk; c += kEigNT) {
+  for (int c = tid; c < kk; c += kEigNT) {  // H^T = Lc^{-1} K^T
     for (int i = 0; i < kk; ++i) {
       double s = S.H2[c * HL + i];
       for (int k2 = 0; k2 < i; ++k2) s = fma(-S.Lc[i * HL + k2], S.T[c * HL + k2], s);
@@ -390,10 +396,9 @@ __device__ int ritz_small(Sm& S, int kk, const double* Hp, const double* M, doub
   }
   eig_sync();
   if (rec) { const long long t1 = clock64(); dbg[9] += t1 - t0; t0 = t1; }
-  jacobi_eig(S, kk, thr_rel, dbg);
+  jacobi_eig(S, kk, thr_rel, max_sweeps, dbg);
   if (rec) { const long long t1 = clock64(); dbg[10] += t1 - t0; t0 = t1; dbg[14] += 1; }
-  // T = Lc^{-T} Z: back substitution per column
-  for (int c = tid; c < kk; c += kEigNT) {
+  for (int c = tid; c < kk; c += kEigNT) {  // T = Lc^{-T} Z (back substitution)
     for (int i = kk - 1; i >= 0; --i) {
       double s = S.Z[i * HL + c];
       for (int k2 = i + 1; k2 < kk; ++k2) s = fma(-S.Lc[k2 * HL + i], S.T[k2 * HL + c], s);
@@ -420,15 +425,15 @@ __device__ void rotate_rows(double* X, int nr, int KP, int kk, const double* Rm,
   __syncthreads();
 }
 
-// Block-local CGS2 with random replacement on the FULL V (n x kk) — robust
-// path for a rank-deficient starting block.
-__device__ void cgs2_full(Sm& S, int n, int KP, int kk, uint64_t salt) {
+// CGS2 with random replacement on the FULL V (n x kk, ld kLdV) in global
+// memory, by one CTA — the rare path for a rank-deficient starting block.
+__device__ void cgs2_global(Sm& S, double* V, int n, int kk, uint64_t salt) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   double* dots = S.rout;
   for (int c = 0; c < kk; ++c) {
     for (int attempt = 0; attempt < 4; ++attempt) {
       double p = 0.0;
-      for (int j = tid; j < n; j += kSvdNT) p = fma(S.V[j * KP + c], S.V[j * KP + c], p);
+      for (int j = tid; j < n; j += kSvdNT) p = fma(V[j * kLdV + c], V[j * kLdV + c], p);
       p = warp_sum(p);
       if (lane == 0) S.ws[w] = p;
       __syncthreads();
@@ -438,20 +443,20 @@ __device__ void cgs2_full(Sm& S, int n, int KP, int kk, uint64_t salt) {
       for (int pass = 0; pass < 2; ++pass) {
         for (int k = w; k < c; k += kSvdNW) {
           double d = 0.0;
-          for (int j = lane; j < n; j += 32) d = fma(S.V[j * KP + k], S.V[j * KP + c], d);
+          for (int j = lane; j < n; j += 32) d = fma(V[j * kLdV + k], V[j * kLdV + c], d);
           d = warp_sum(d);
           if (lane == 0) dots[k] = d;
         }
         __syncthreads();
         for (int j = tid; j < n; j += kSvdNT) {
-          double v = S.V[j * KP + c];
-          for (int k = 0; k < c; ++k) v = fma(-dots[k], S.V[j * KP + k], v);
-          S.V[j * KP + c] = v;
+          double v = V[j * kLdV + c];
+          for (int k = 0; k < c; ++k) v = fma(-dots[k], V[j * kLdV + k], v);
+          V[j * kLdV + c] = v;
         }
         __syncthreads();
       }
       p = 0.0;
-      for (int j = tid; j < n; j += kSvdNT) p = fma(S.V[j * KP + c], S.V[j * KP + c], p);
+      for (int j = tid; j < n; j += kSvdNT) p = fma(V[j * kLdV + c], V[j * kLdV + c], p);
       p = warp_sum(p);
       if (lane == 0) S.ws[w] = p;
       __syncthreads();
@@ -460,12 +465,12 @@ __device__ void cgs2_full(Sm& S, int n, int KP, int kk, uint64_t salt) {
       __syncthreads();
       if (nrm > 1e-20 * nrm0 && nrm > 1e-280) {
         const double inv = 1.0 / sqrt(nrm);
-        for (int j = tid; j < n; j += kSvdNT) S.V[j * KP + c] *= inv;
+        for (int j = tid; j < n; j += kSvdNT) V[j * kLdV + c] *= inv;
         __syncthreads();
         break;
       }
       for (int j = tid; j < n; j += kSvdNT)
-        S.V[j * KP + c] = hash_uniform(salt + 1000003ull * (uint64_t)(attempt + 1), (uint64_t)j * 64 + c);
+        V[j * kLdV + c] = hash_uniform(salt + 1000003ull * (uint64_t)(attempt + 1), (uint64_t)j * 64 + c);
       __syncthreads();
     }
   }
@@ -484,7 +489,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   S.L = svd_layout(n, m, kk, CS);
   const SvdLayout& L = S.L;
   const int KP = L.KP, HL = L.HL, RL = L.RL;
-  S.V = svsm + L.oV; S.P = svsm + L.oP; S.Bq = svsm + L.oBq; S.Xq = svsm + L.oXq;
+  S.Vq = svsm + L.oVq; S.P = svsm + L.oP; S.Bq = svsm + L.oBq; S.Xq = svsm + L.oXq;
   S.H = svsm + L.oH; S.H2 = svsm + L.oH2; S.Z = svsm + L.oZ; S.Lc = svsm + L.oLc; S.T = svsm + L.oT;
   S.red = svsm + L.oRed; S.rout = svsm + L.oRout; S.res = svsm + L.oRes; S.lam = svsm + L.oLam;
   S.cs = svsm + L.oCs; S.ws = svsm + L.oW;
@@ -497,8 +502,9 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   const bool eigt = tid < kEigNT;
   const double eprev = a.prev_err ? fmin(1.0, fabs(*a.prev_err)) : 1.0;
   const double tol = fmax(a.tol, a.tol_scale * eprev);
+  double* scr[2] = {a.scratch, a.scratch + (size_t)n * kLdV};
 
-  // ---- 0. G rows of this CTA into shared memory; starting block V
+  // ---- 0. G rows of this CTA into shared memory; starting block (my rows)
   const double* Gq = a.G + (int64_t)lo * a.ldg;
   int ldgq = a.ldg;
   if (L.gq_smem) {
@@ -510,27 +516,31 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     ldgq = L.ldgq;
   }
   const T* warm = reinterpret_cast<const T*>(a.warm);
-  for (int e = tid; e < n * kk; e += kSvdNT) {
-    const int j = e / kk, c = e - j * kk;
-    double v = 0.0;
+  int gbuf = 0;
+  for (int e = tid; e < nr * kk; e += kSvdNT) {
+    const int i = e / kk, c = e - i * kk;
+    const int j = lo + i;
+    double v;
     if (warm && c < a.warm_cols) v = (double)warm[(int64_t)j * a.warm_ld + c];
     else v = hash_uniform(0x5EEDull + a.salt, (uint64_t)j * 64 + c);
-    S.V[j * KP + c] = v;
+    S.Vq[i * KP + c] = v;
+    scr[gbuf][(int64_t)j * kLdV + c] = v;
   }
   for (int c = tid; c < kk; c += kSvdNT) S.res[c] = 0.0;
-  __syncthreads();
+  __threadfence();
+  cl.sync();
 
-  int step = 0, buf = 0, gbuf = 0, redo = 0;
-  long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long tc = clock64();
-#define PH(i) do { if (a.dbg) { const long long _t = clock64(); tph[i] += _t - tc; tc = _t; } } while (0)
+  int step = 0, buf = 0, redo = 0;
   bool prev_conv = false, have_prev = false;
   double prev_res = 1e300;
   int stall = 0;
+  long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+#define PH(i) do { if (a.dbg) { const long long _t = clock64(); tph[i] += _t - tc; tc = _t; } } while (0)
   for (;;) {
     PH(7);
-    // ---- 1. B_q = G(lo:hi, :) V
-    tiled_product(Gq, ldgq, nr, n, S.V, KP, kk, S.Bq, S.P, L.S);
+    // ---- 1. B_q = G(lo:hi, :) V   (V through L1 from the L2 scratch)
+    tiled_product(Gq, ldgq, nr, n, scr[gbuf], kLdV, KP, kk, S.Bq, S.P, L.S);
     PH(0);
     // ---- 2. one reduction: [V^T B | V^T V | previous Ritz residuals]
     double* rb = S.red + buf * RL;
@@ -538,9 +548,9 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       const int which = e / (kk * kk);
       const int e2 = e - which * kk * kk;
       const int c1 = e2 / kk, c2 = e2 - c1 * kk;
-      const double* Y = which == 0 ? S.Bq : S.V + lo * KP;
+      const double* Y = which == 0 ? S.Bq : S.Vq;
       double s = 0.0;
-      for (int i = 0; i < nr; ++i) s = fma(S.V[(lo + i) * KP + c1], Y[i * KP + c2], s);
+      for (int i = 0; i < nr; ++i) s = fma(S.Vq[i * KP + c1], Y[i * KP + c2], s);
       rb[e] = s;
     }
     for (int c = tid; c < kk; c += kSvdNT) rb[2 * kk * kk + c] = S.res[c];
@@ -558,13 +568,19 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     PH(1);
     // ---- 3. Rayleigh-Ritz (generalised through chol(V^T V))
     if (eigt) {
-      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, 4e-16, a.dbg);
-      if (tid == 0) S.flags[6] = ok;
+      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, 4e-16, 2, a.dbg);
+      if (tid == 0) S.flags[7] = ok;
     }
     __syncthreads();
-    if (!S.flags[6]) {
-      // rank-deficient start block: orthonormalise it robustly, redo the step
-      cgs2_full(S, n, KP, kk, a.salt + 77ull * (redo + 1));
+    if (!S.flags[7]) {
+      // rank-deficient block: CTA 0 orthonormalises the shared copy robustly
+      if (q == 0) cgs2_global(S, scr[gbuf], n, kk, a.salt + 77ull * (redo + 1));
+      __threadfence();
+      cl.sync();
+      for (int e = tid; e < nr * kk; e += kSvdNT) {
+        const int i = e / kk, c = e - i * kk;
+        S.Vq[i * KP + c] = scr[gbuf][(int64_t)(lo + i) * kLdV + c];
+      }
       __syncthreads();
       if (++redo > 3) break;
       continue;
@@ -576,23 +592,24 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       double sx = 0.0, sy = 0.0;
       for (int j = 0; j < kk; ++j) {
         const double t = S.T[j * HL + c];
-        sx = fma(S.V[(lo + i) * KP + j], t, sx);
+        sx = fma(S.Vq[i * KP + j], t, sx);
         sy = fma(S.Bq[i * KP + j], t, sy);
       }
       S.Xq[i * KP + c] = sx;
       S.P[i * KP + c] = sy;
     }
     __syncthreads();
+    PH(3);
     const bool last = prev_conv || step + 1 >= a.maxsteps;
-    double* sc = a.scratch + (size_t)gbuf * n * kKMax;
+    double* sc = scr[gbuf ^ 1];
     if (last) {
       for (int e = tid; e < nr * kk; e += kSvdNT) {
         const int i = e / kk, c = e - i * kk;
-        sc[(int64_t)(lo + i) * kKMax + c] = S.Xq[i * KP + c];
+        sc[(int64_t)(lo + i) * kLdV + c] = S.Xq[i * KP + c];
       }
+      gbuf ^= 1;
       break;
     }
-    PH(3);
     // ---- 5. this step's residuals (reduced with the next step) and next block
     const double lam0 = S.lam[0];
     const double sig_thr = 1e-10 * fabs(lam0);
@@ -608,33 +625,21 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     for (int e = tid; e < nr * kk; e += kSvdNT) {
       const int i = e / kk, c = e - i * kk;
       const double lc = S.lam[c];
-      sc[(int64_t)(lo + i) * kKMax + c] = (lc > sig_thr && lc > 0.0) ? S.P[i * KP + c] / lc : S.Xq[i * KP + c];
+      const double v = (lc > sig_thr && lc > 0.0) ? S.P[i * KP + c] / lc : S.Xq[i * KP + c];
+      S.Vq[i * KP + c] = v;
+      sc[(int64_t)(lo + i) * kLdV + c] = v;
     }
     PH(4);
-    // ---- 6. all-gather the next block through L2 (double-buffered scratch)
+    // ---- 6. publish the next block (double-buffered L2 scratch)
     __threadfence();
     cl.sync();
-    for (int e = tid; e < n * kk; e += kSvdNT) {
-      const int j = e / kk, c = e - j * kk;
-      S.V[j * KP + c] = sc[(int64_t)j * kKMax + c];
-    }
     gbuf ^= 1;
     have_prev = true;
-    PH(5);
     ++step;
-    __syncthreads();
+    PH(5);
   }
-  {
-    // gather the final Ritz block
-    const double* sc = a.scratch + (size_t)gbuf * n * kKMax;
-    __threadfence();
-    cl.sync();
-    for (int e = tid; e < n * kk; e += kSvdNT) {
-      const int j = e / kk, c = e - j * kk;
-      S.V[j * KP + c] = sc[(int64_t)j * kKMax + c];
-    }
-    __syncthreads();
-  }
+  __threadfence();
+  cl.sync();
   if (q == 0 && tid == 0 && a.steps_out) *a.steps_out = step + 1;
   PH(6);
   if (a.dbg && q == 0 && tid == 0)
@@ -642,7 +647,8 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
 #undef PH
 
   // ---- 7. Rayleigh-Ritz on U itself: Y = U V (my m-rows), H2 = Y^T Y
-  tiled_product(a.U + (int64_t)mlo * a.ldu, a.ldu, mr, n, S.V, KP, kk, S.Xq, S.P, L.S);
+  const double* Vf = scr[gbuf];
+  tiled_product(a.U + (int64_t)mlo * a.ldu, a.ldu, mr, n, Vf, kLdV, KP, kk, S.Xq, S.P, L.S);
   {
     double* rb = S.red + buf * RL;
     for (int e = tid; e < kk * kk; e += kSvdNT) {
@@ -660,15 +666,18 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       S.H[c1 * HL + c2] = 0.5 * (S.rout[c1 * kk + c2] + S.rout[c2 * kk + c1]);
     }
     eig_sync();
-    jacobi_eig(S, kk, 4e-16);
+    jacobi_eig(S, kk, 4e-16, 30);
   }
   __syncthreads();
   rotate_rows(S.Xq, mr, KP, kk, S.Z, HL, S.P);
-  {
-    // full V (needed for QJ = G V Sigma^+), in chunks that fit the temp buffer
-    const int chunk = L.S * L.rowsmax;
-    for (int j0 = 0; j0 < n; j0 += chunk)
-      rotate_rows(S.V + j0 * KP, min(chunk, n - j0), KP, kk, S.Z, HL, S.P);
+  // rotated V: my rows into Vq and into the other scratch buffer (for QJ)
+  double* Vr = scr[gbuf ^ 1];
+  for (int e = tid; e < nr * kk; e += kSvdNT) {
+    const int i = e / kk, c = e - i * kk;
+    double s = 0.0;
+    for (int j = 0; j < kk; ++j) s = fma(Vf[(int64_t)(lo + i) * kLdV + j], S.Z[j * HL + c], s);
+    S.Vq[i * KP + c] = s;
+    Vr[(int64_t)(lo + i) * kLdV + c] = s;
   }
   {
     double* rb = S.red + buf * RL;
@@ -677,7 +686,8 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       for (int i = 0; i < mr; ++i) s = fma(S.Xq[i * KP + c], S.Xq[i * KP + c], s);
       rb[c] = s;
     }
-    cluster_sum(cl, S, buf, kk);
+    __threadfence();
+    cluster_sum(cl, S, buf, kk);  // also publishes Vr
     buf ^= 1;
   }
   if (tid < kk) S.lam[tid] = sqrt(S.rout[tid]);  // sigma
@@ -717,7 +727,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     const int i = e / r, c = e - i * r;
     double vv = 0.0, vs = 0.0;
     if (c < reff) {
-      vv = S.V[(lo + i) * KP + c];
+      vv = S.Vq[i * KP + c];
       const double sg = S.lam[c];
       const double iv = (smax > 0.0 && sg > 1e-12 * smax) ? 1.0 / sg : 0.0;
       vs = vv * iv;
@@ -726,7 +736,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     VS[(int64_t)(lo + i) * r + c] = (T)vs;
   }
   // QJ = U^T W = G V Sigma^{-1} for my n-rows (zero for deficient columns)
-  tiled_product(Gq, ldgq, nr, n, S.V, KP, kk, S.Bq, S.P, L.S);
+  tiled_product(Gq, ldgq, nr, n, Vr, kLdV, KP, kk, S.Bq, S.P, L.S);
   for (int e = tid; e < nr * r; e += kSvdNT) {
     const int i = e / r, c = e - i * r;
     double v = 0.0;
@@ -796,7 +806,7 @@ size_t svd_smem_bytes(int n, int m, int kk, int cs) {
 }
 
 // ~32 rows of G per CTA; more CTAs (up to 16) while that lets G's row block
-// stay resident in shared memory next to the replicated V.
+// stay resident in shared memory.
 int svd_pick_cluster(int n, int m, int kk) {
   int cs = (n + 31) / 32;
   if (cs < 1) cs = 1;
