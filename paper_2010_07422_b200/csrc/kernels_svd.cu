@@ -173,7 +173,7 @@ __device__ void tiled_product(const double* A, int lda, int nr, int n, const dou
     const double* Aa = A + (int64_t)ia * lda;
     const double* Ab = A + (int64_t)ib * lda;
     double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
-#pragma unroll 4
+#pragma unroll 8
     for (int j = j0; j < j1; ++j) {
       const double a0 = Aa[j], a1 = Ab[j];
       const double v0 = V[(int64_t)j * ldv + ca], v1 = V[(int64_t)j * ldv + cb];
@@ -285,6 +285,7 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long l
       if (tid == 0) *rflag = rot;
       eig_sync();
       if (!*rflag) continue;  // nothing rotates this round: H, Z unchanged
+#pragma unroll 4
       for (int e = tid; e < nent; e += kEigNT) {
         const int ab = etab[e];
         const int a = ab >> 8, b = ab & 255;
@@ -337,30 +338,37 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long l
 // threads (reciprocal diagonal kept in column kk); returns 0 on breakdown.
 // Caller: first kEigNT threads.
 __device__ int cholesky_warp(const double* M, double* Lc, int HL, int kk, int* flag) {
-  const int lane = threadIdx.x & 31;
-  if ((threadIdx.x >> 5) == 0) {
-    int ok = 1;
-    for (int j = 0; j < kk; ++j) {
-      double p = 0.0;
-      for (int k2 = lane; k2 < j; k2 += 32) p = fma(Lc[j * HL + k2], Lc[j * HL + k2], p);
-      p = warp_sum(p);
-      double d = M[j * kk + j] - p;
-      if (!(d > 1e-300)) { ok = 0; d = 1.0; }
-      const double ir = rsqrt(d);  // 1 / L_jj (division-free)
-      for (int i = j + 1 + lane; i < kk; i += 32) {
-        double s2 = M[i * kk + j];
-        for (int k2 = 0; k2 < j; ++k2) s2 = fma(-Lc[i * HL + k2], Lc[j * HL + k2], s2);
-        Lc[i * HL + j] = s2 * ir;
-      }
-      if (lane == 0) {
-        Lc[j * HL + j] = d * ir;
-        Lc[j * HL + kk] = ir;
-      }
-      __syncwarp();
-    }
-    if (lane == 0) *flag = ok;
+  // right-looking: Lc starts as the lower triangle of M; column j is scaled,
+  // then the trailing lower triangle is updated by all eig threads.
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kk * kk; e += kEigNT) {
+    const int i = e / kk, j = e - i * kk;
+    if (j <= i) Lc[i * HL + j] = M[i * kk + j];
   }
+  if (tid == 0) *flag = 1;
   eig_sync();
+  for (int j = 0; j < kk; ++j) {
+    double d = Lc[j * HL + j];
+    const bool bad = !(d > 1e-300);
+    if (bad) d = 1.0;
+    const double ir = rsqrt(d);  // 1 / L_jj (division-free)
+    if (tid == 0) {
+      if (bad) *flag = 0;
+      Lc[j * HL + j] = d * ir;
+      Lc[j * HL + kk] = ir;
+    }
+    for (int i = j + 1 + tid; i < kk; i += kEigNT) Lc[i * HL + j] *= ir;
+    eig_sync();
+    const int nt = kk - j - 1;  // trailing block rows j+1..kk-1
+    for (int e = tid; e < nt * nt; e += kEigNT) {
+      const int ii = e / nt, kq = e - ii * nt;
+      if (kq <= ii) {
+        const int i = j + 1 + ii, k2 = j + 1 + kq;
+        Lc[i * HL + k2] = fma(-Lc[i * HL + j], Lc[k2 * HL + j], Lc[i * HL + k2]);
+      }
+    }
+    eig_sync();
+  }
   return *flag;
 }
 
