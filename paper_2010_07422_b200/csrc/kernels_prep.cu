@@ -13,6 +13,7 @@
 
 #include "ircur_common.cuh"
 #include "launchers.cuh"
+#include <cstdlib>
 #include <type_traits>
 
 namespace ircur {
@@ -124,13 +125,77 @@ __global__ void __launch_bounds__(256) prep_scan_vec_kernel(const T* __restrict_
   }
 }
 
+// Persistent 64x64-tile transpose fused with the finite/max scan.  Each CTA
+// walks tiles t = blockIdx.x + i*gridDim.x; `col_major_order` chooses whether
+// consecutive tiles share a column band (writes of concurrently running CTAs
+// land in the same 64 rows of Dt) or a row band (reads share 64 rows of D).
+constexpr int kPT = 64;
+template <typename T>
+__global__ void __launch_bounds__(256) prep_transpose64_kernel(const T* __restrict__ D, int64_t ldd,
+                                                               int64_t nloc, int64_t n2, T* __restrict__ Dt,
+                                                               int64_t ldt, unsigned long long* maxbits,
+                                                               int* nonfinite, int col_major_order) {
+  __shared__ T tile[kPT][kPT + 1];
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  const int64_t tr = (nloc + kPT - 1) / kPT, tcn = (n2 + kPT - 1) / kPT;
+  const int64_t ntiles = tr * tcn;
+  double mx = 0.0;
+  int bad = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int64_t br, bc;
+    if (col_major_order) { bc = t / tr; br = t - bc * tr; } else { br = t / tcn; bc = t - br * tcn; }
+    const int64_t rb = br * kPT, cb = bc * kPT;
+    const bool full = (rb + kPT <= nloc) && (cb + kPT <= n2);
+#pragma unroll 4
+    for (int k = 0; k < kPT; k += 4) {
+      const int64_t r = rb + ty + k, c = cb + tx;
+      T v = T(0);
+      if (full || (r < nloc && c < n2)) {
+        v = __ldcs(D + r * ldd + c);
+        const double av = fabs((double)v);
+        if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
+      }
+      tile[ty + k][tx] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < kPT; k += 4) {
+      const int64_t c = cb + ty + k, r = rb + tx;
+      if (full || (r < nloc && c < n2)) __stcs(Dt + c * ldt + r, tile[tx][ty + k]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mx > 0.0) atomicMax(maxbits, dbits(mx));
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
 template <typename T>
 cudaError_t launch_prep(const T* D, int64_t ldd, int64_t nloc, int64_t n2, T* Dt, int64_t ldt,
                         unsigned long long* maxbits, int* nonfinite, int num_sms, cudaStream_t st) {
   if (nloc == 0 || n2 == 0) return cudaSuccess;
   if (Dt) {
-    dim3 grid((unsigned)((n2 + kTT - 1) / kTT), (unsigned)((nloc + kTT - 1) / kTT));
-    prep_transpose_kernel<T><<<grid, 256, 0, st>>>(D, ldd, nloc, n2, Dt, ldt, maxbits, nonfinite);
+    static int mode = -1;
+    if (mode < 0) {
+      const char* m = std::getenv("IRCUR_TRANSPOSE");
+      mode = m ? std::atoi(m) : 1;
+    }
+    if (mode == 0) {
+      dim3 grid((unsigned)((n2 + kTT - 1) / kTT), (unsigned)((nloc + kTT - 1) / kTT));
+      prep_transpose_kernel<T><<<grid, 256, 0, st>>>(D, ldd, nloc, n2, Dt, ldt, maxbits, nonfinite);
+    } else {
+      const int64_t ntiles = ((nloc + kPT - 1) / kPT) * ((n2 + kPT - 1) / kPT);
+      const int64_t cap = (int64_t)num_sms * 8;
+      const unsigned blocks = (unsigned)(ntiles < cap ? ntiles : cap);
+      prep_transpose64_kernel<T><<<blocks, 256, 0, st>>>(D, ldd, nloc, n2, Dt, ldt, maxbits, nonfinite,
+                                                         mode == 2 ? 0 : 1);
+    }
   } else {
     const int64_t total = nloc * n2;
     int64_t want = (total + 256 * 8 - 1) / (256 * 8);
