@@ -90,19 +90,40 @@ __global__ void __launch_bounds__(256) prep_scan_vec_kernel(const T* __restrict_
                                                             unsigned long long* maxbits, int* nonfinite) {
   constexpr int VW = 16 / sizeof(T);
   using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
-  double mx = 0.0;
+  T mx = T(0);
   int bad = 0;
   const int64_t vpr = n2 / VW;  // full vectors per row
   const int64_t total = nloc * vpr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+  constexpr int UN = 4;  // independent 16-byte loads in flight per thread
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ldd == n2) {  // dense rows: treat D as one flat vector array
+    const V4* Dv = reinterpret_cast<const V4*>(D);
+    for (; e + (UN - 1) * stride < total; e += UN * stride) {
+      V4 v[UN];
+#pragma unroll
+      for (int u = 0; u < UN; ++u) v[u] = __ldcs(Dv + e + u * stride);
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {
+        const T* pv = reinterpret_cast<const T*>(&v[u]);
+#pragma unroll
+        for (int w = 0; w < VW; ++w) {
+          const T av = fabs(pv[w]);
+          bad |= !isfinite(av);
+          mx = fmax(mx, av);
+        }
+      }
+    }
+  }
+  for (; e < total; e += stride) {
     const int64_t r = e / vpr, cv = e - r * vpr;
     const V4 v = __ldcs(reinterpret_cast<const V4*>(D + r * ldd) + cv);
     const T* pv = reinterpret_cast<const T*>(&v);
 #pragma unroll
     for (int u = 0; u < VW; ++u) {
-      const double av = fabs((double)pv[u]);
-      if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
+      const T av = fabs(pv[u]);
+      bad |= !isfinite(av);
+      mx = fmax(mx, av);
     }
   }
   // row tails
@@ -137,31 +158,67 @@ __global__ void __launch_bounds__(256) prep_transpose64_kernel(const T* __restri
                                                                int* nonfinite, int col_major_order) {
   __shared__ T tile[kPT][kPT + 1];
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  constexpr int VW = 16 / sizeof(T);                      // elements per 16-byte vector
+  constexpr int TPR = kPT / VW;                            // threads per 64-element row segment
+  constexpr int RPI = 256 / TPR;                           // rows per vector pass
+  const int vx = threadIdx.x % TPR, vy = threadIdx.x / TPR;
+  using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  const bool vec_ok = ((ldd * (int64_t)sizeof(T)) % 16 == 0) && ((ldt * (int64_t)sizeof(T)) % 16 == 0) &&
+                      ((uintptr_t)D % 16 == 0) && ((uintptr_t)Dt % 16 == 0);
   const int64_t tr = (nloc + kPT - 1) / kPT, tcn = (n2 + kPT - 1) / kPT;
   const int64_t ntiles = tr * tcn;
-  double mx = 0.0;
+  T mx = T(0);
   int bad = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int64_t br, bc;
     if (col_major_order) { bc = t / tr; br = t - bc * tr; } else { br = t / tcn; bc = t - br * tcn; }
     const int64_t rb = br * kPT, cb = bc * kPT;
     const bool full = (rb + kPT <= nloc) && (cb + kPT <= n2);
-#pragma unroll 4
-    for (int k = 0; k < kPT; k += 4) {
-      const int64_t r = rb + ty + k, c = cb + tx;
-      T v = T(0);
-      if (full || (r < nloc && c < n2)) {
-        v = __ldcs(D + r * ldd + c);
-        const double av = fabs((double)v);
-        if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
+    if (full && vec_ok) {
+      V4 v[kPT / RPI];
+#pragma unroll
+      for (int k = 0; k < kPT / RPI; ++k)
+        v[k] = __ldcs(reinterpret_cast<const V4*>(D + (rb + vy + k * RPI) * ldd + cb) + vx);
+#pragma unroll
+      for (int k = 0; k < kPT / RPI; ++k) {
+        const T* pv = reinterpret_cast<const T*>(&v[k]);
+#pragma unroll
+        for (int u = 0; u < VW; ++u) {
+          const T av = fabs(pv[u]);
+          bad |= !isfinite(av);
+          mx = fmax(mx, av);
+          tile[vy + k * RPI][vx * VW + u] = pv[u];
+        }
       }
-      tile[ty + k][tx] = v;
-    }
-    __syncthreads();
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kPT / RPI; ++k) {
+        const int c = vy + k * RPI;  // Dt row (= D column) within the tile
+        V4 o;
+        T* po = reinterpret_cast<T*>(&o);
+#pragma unroll
+        for (int u = 0; u < VW; ++u) po[u] = tile[vx * VW + u][c];
+        __stcs(reinterpret_cast<V4*>(Dt + (cb + c) * ldt + rb) + vx, o);
+      }
+    } else {
 #pragma unroll 4
-    for (int k = 0; k < kPT; k += 4) {
-      const int64_t c = cb + ty + k, r = rb + tx;
-      if (full || (r < nloc && c < n2)) __stcs(Dt + c * ldt + r, tile[tx][ty + k]);
+      for (int k = 0; k < kPT; k += 4) {
+        const int64_t r = rb + ty + k, c = cb + tx;
+        T v = T(0);
+        if (r < nloc && c < n2) {
+          v = __ldcs(D + r * ldd + c);
+          const T av = fabs(v);
+          bad |= !isfinite(av);
+          mx = fmax(mx, av);
+        }
+        tile[ty + k][tx] = v;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int k = 0; k < kPT; k += 4) {
+        const int64_t c = cb + ty + k, r = rb + tx;
+        if (r < nloc && c < n2) __stcs(Dt + c * ldt + r, tile[tx][ty + k]);
+      }
     }
     __syncthreads();
   }
