@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(256) prep_scan_vec_kernel(const T* __restrict_
   if (tail > 0) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * tail; e += stride) {
       const int64_t r = e / tail, c = vpr * VW + (e - r * tail);
-      const double av = fabs((double)D[r * ldd + c]);
-      if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
+      const T av = fabs(D[r * ldd + c]);
+      bad |= !isfinite(av);
+      mx = fmax(mx, av);
     }
   }
 #pragma unroll
