@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostics: skip the nvidia-smi sampler")
+    ap.add_argument("--no-profile", action="store_true", help="diagnostics: no per-kernel events")
     return ap.parse_args()
 
 
@@ -83,6 +85,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if self.index < 0:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -150,18 +154,23 @@ def run_ours(args):
                           max_iter=MAX_ITER, seed=ir.RngSeed(SOLVER_SEED))
     cm = args.colmajor if args.colmajor == "auto" else args.colmajor in ("1", "true", "True")
     stream = torch.cuda.current_stream()
+    prof = not args.no_profile
     for _ in range(args.warmup):
-        res = ir.solve_device(D, cfg, colmajor=cm, profile=True)
+        res = ir.solve_device(D, cfg, colmajor=cm, profile=prof)
     torch.cuda.synchronize()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     results = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(-1 if args.no_clocks else local) as clk:
         start.record(stream)
-        for _ in range(args.steps):
-            results.append(ir.solve_device(D, cfg, colmajor=cm, profile=True))
+        marks[0].record(stream)
+        for i in range(args.steps):
+            results.append(ir.solve_device(D, cfg, colmajor=cm, profile=prof))
+            marks[i + 1].record(stream)
         stop.record(stream)
         torch.cuda.synchronize()
     total_ms = start.elapsed_time(stop)
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     ms_per_step = total_ms / args.steps
     res = results[-1]
     iters = res.trace.iterations
@@ -170,6 +179,10 @@ def run_ours(args):
     svd_ms = core_ms = 0.0
     for rr in results:
         p = rr.profile
+        if p is None:
+            p = {"strips_ms": np.full(rr.trace.iterations, np.nan), "svd_ms": np.zeros(rr.trace.iterations),
+                 "core_ms": np.zeros(rr.trace.iterations), "kernel_launches": 5 * rr.trace.iterations}
+            rr.profile = p
         for k in range(rr.trace.iterations):
             strip_ms += float(p["strips_ms"][k])
             svd_ms += float(p["svd_ms"][k])
@@ -196,6 +209,8 @@ def run_ours(args):
                    "final_e": res.trace.errors[-1], "colmajor_copy": bool(res.colmajor),
                    "l2": "inputs larger than L2 (D >= 400 MB), no flush",
                    "parallelism": "single GPU"},
+        "step_ms": step_ms,
+        "host_ms_last_step": (res.profile or {}).get("host_ms"),
         "breakdown_ms_per_solve": {
             "strips": strip_ms / len(results), "svd": svd_ms / len(results),
             "core": core_ms / len(results),

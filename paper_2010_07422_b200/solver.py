@@ -245,6 +245,22 @@ def _want_colmajor(colmajor, n1, n2, m_cols, dtype_size, mode) -> bool:
     return n2 < 600 * m_cols
 
 
+class _Ticker:
+    """Host wall-clock marks between the phases of solve_device (profiling)."""
+
+    def __init__(self, on: bool):
+        import time
+        self.on, self.clock = on, time.perf_counter
+        self.t = self.clock() if on else 0.0
+        self.marks: dict = {}
+
+    def __call__(self, name: str) -> None:
+        if self.on:
+            t = self.clock()
+            self.marks[name] = (t - self.t) * 1e3
+            self.t = t
+
+
 @dataclass
 class DeviceHandle:
     """Final rank-r factors on the device: L = P Q with P^T (r x n1) and Q (r x n2)."""
@@ -272,6 +288,7 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
                  colmajor="auto", fetch_factors=True, profile=False) -> DeviceResult:
     """Run the loop on the device; results stay on the device (see solve)."""
     cfg = config
+    tick = _Ticker(profile)
     Dd = _device_matrix(D, device, compute_dtype)
     if Dd.numel() == 0:
         raise ValueError("D must be nonempty")
@@ -283,13 +300,17 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     resampled = cfg.mode == "resampled"
     n_sets = cfg.max_iter if resampled else 1
     sets = draw_index_sets(n1, n2, m_rows, m_cols, cfg.seed, n_sets)
+    tick("draw")
     stream = torch.cuda.current_stream(dev).cuda_stream
     ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
     cm = _want_colmajor(colmajor, n1, n2, m_cols, Dd.element_size(), cfg.mode)
     max_abs = ctx.prepare(Dd, cm)  # ValueError on NaN/Inf (matcore.py:75-76)
+    tick("prepare")
     ctx.set_indices(sets)
+    tick("set_indices")
     rows0, cols0 = sets[0]
     a, b = ctx.slab_sqnorms(0)
+    tick("slab")
     trace = SolverTrace()
     if np.sqrt(a) + np.sqrt(b) == 0.0:
         # solver.py:335-341: sampled slabs identically zero
@@ -304,8 +325,10 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     prof = None
     if observer is None:
         iters, conv, errors, ms = ctx.run(zetas, cfg.eps, mode, cfg.max_iter)
+        tick("run")
         if profile:
             prof = ctx.profile(iters)
+            tick("profile")
         trace.errors = [float(e) for e in errors]
         trace.seconds = [float(t) / 1e3 for t in ms]
     else:
@@ -338,7 +361,10 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     if fetch_factors:
         Pt, Qt = ctx.factors()
         handle = DeviceHandle(Pt, Qt, dtype)
+        tick("factors")
     res = DeviceResult(trace, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), handle)
+    if prof is not None:
+        prof["host_ms"] = tick.marks
     res.profile = prof
     res.colmajor = cm
     res.sets = sets
