@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: skip the nvidia-smi sampler")
     ap.add_argument("--no-profile", action="store_true", help="diagnostics: no per-kernel events")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded NCCL path even at N=1 (tests the multi-GPU code on one GPU)")
     return ap.parse_args()
 
 
@@ -141,10 +143,16 @@ def run_ours(args):
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        from paper_2010_07422_b200 import dist as irdist
-        return irdist.bench_sharded(args, CONFIGS, rank, world, local)
+        if rank == 0:
+            _build.build()
+        dist.barrier()
+        return run_sharded(args, rank, world, local)
     _build.build()
     n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
     tdt = torch.float32 if dts == "f32" else torch.float64
@@ -210,7 +218,8 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (D >= 400 MB), no flush",
                    "parallelism": "single GPU"},
         "step_ms": step_ms,
-        "host_ms_last_step": (res.profile or {}).get("host_ms"),
+        "host_ms_steps": [{k: round(v, 2) for k, v in (rr.profile or {}).get("host_ms", {}).items()}
+                          for rr in results],
         "breakdown_ms_per_solve": {
             "strips": strip_ms / len(results), "svd": svd_ms / len(results),
             "core": core_ms / len(results),
@@ -245,6 +254,113 @@ def run_ours(args):
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(Dh.numpy(), args.config, cfg, iters, args.cpu_budget)
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------- row-sharded (N > 1)
+def run_sharded(args, rank, world, local):
+    """D row-sharded over the ranks; the same total problem
+    at every N (strong scaling).  Each rank generates its own rows on its GPU
+    (bitwise the rows numpy would generate), solves with three NCCL
+    all-reduces per iteration, and the step time is the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_07422_b200 as ir
+    from paper_2010_07422_b200 import dist as irdist
+    from paper_2010_07422_b200 import gen
+
+    dev = torch.device("cuda", local)
+    n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
+    tdt = torch.float32 if dts == "f32" else torch.float64
+    s = 4 if dts == "f32" else 8
+    r0, nl = irdist.shard_rows(n1, world, rank)
+
+    def stats_reduce(mx, q):
+        t = torch.tensor([mx], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        qq = torch.tensor([q], dtype=torch.int64, device=dev)
+        dist.all_reduce(qq)
+        return float(t.item()), int(qq.item())
+
+    D, linf, a = gen.baseline_problem_device(n1, n2, r, alpha, DATA_SEED, dtype=tdt, row0=r0, nrows=nl,
+                                             stats_reduce=stats_reduce)
+    cfg = ir.SolverConfig(rank=r, eps=EPS, zeta0=linf, gamma=GAMMA, mode=args.mode,
+                          max_iter=MAX_ITER, seed=ir.RngSeed(SOLVER_SEED))
+    cm = args.colmajor if args.colmajor == "auto" else args.colmajor in ("1", "true", "True")
+
+    def one(Din):
+        return irdist.run_collective(irdist.solve_shard_program(Din, cfg, n1=n1, row0=r0, colmajor=cm))
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        res = one(D)
+    dist.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(-1 if (args.no_clocks or rank != 0) else local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            results.append(one(D))
+        stop.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    mine = torch.tensor([start.elapsed_time(stop) / args.steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+    ms_per_step = float(mine.item())
+    res = results[-1]
+    launches = sum(2 + rr.engine.profile(0)["kernel_launches"] for rr in results)
+    lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+    dist.all_reduce(lt)
+    # e2e: pinned host shard -> sharded solve -> local strips back to the host
+    e2e = None
+    if args.e2e_steps > 0:
+        Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
+        Dh.copy_(D)
+        del D
+        torch.cuda.synchronize()
+        one(Dh)
+        times, d2h = [], 0
+        for _ in range(args.e2e_steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rr = one(Dh)
+            last = rr.trace.iterations - 1 if args.mode == "resampled" else 0
+            outs = rr.engine.strips(last)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            d2h = sum(o.nbytes for o in outs)
+        tt = torch.tensor([float(np.mean(times)), float(d2h), float(Dh.numel() * s)], dtype=torch.float64,
+                          device=dev)
+        tmax = tt[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = tt[1:].clone()
+        dist.all_reduce(tsum)
+        e2e = {"value": float(tmax.item()), "unit": "s", "h2d_bytes_per_step": int(tsum[1].item()),
+               "d2h_bytes_per_step": int(tsum[0].item()),
+               "api": "paper_2010_07422_b200.dist.solve_shard_program (pinned host shard per rank)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if dts == "f32" else "f64",
+            "data": "synthetic (BASELINE.json generator on device, numpy-PCG64-exact, row-sharded)",
+            "config": {"workload": args.config, "n1": n1, "n2": n2, "rank": r, "alpha": alpha,
+                       "mode": args.mode, "gamma": GAMMA, "eps": EPS, "zeta0": "max|L|",
+                       "iterations": res.trace.iterations, "converged": res.trace.converged,
+                       "final_e": res.trace.errors[-1], "launched_iterations": res.launched,
+                       "l2": "inputs larger than L2 (D >= 400 MB), no flush",
+                       "parallelism": f"row-sharded x{world} (NCCL all-reduce of U, Q partials, 4 sums)"},
+            "roofline": None,
+            "gpu_launches": int(lt.item()),
+            "clocks": clk.summary(),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 # ------------------------------------------------------------- CPU oracle

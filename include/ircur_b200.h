@@ -97,6 +97,48 @@ int ircur_run(ircur_ctx_t ctx, const double* zetas, double eps, int mode, int ma
  * observer path, solver.py:410-411).  Returns e_k.  Host-blocking. */
 int ircur_iterate(ircur_ctx_t ctx, int k, int set, double zeta, double* e);
 
+/* ---- Row-sharded loop (multi-GPU, one process per GPU) -------------------
+ * Each rank's context owns rows [row0, row0+local_rows) of D; index sets and
+ * zetas are identical on all ranks.  The caller owns the collectives (NCCL
+ * through torch.distributed in paper_2010_07422_b200/dist.py): after each
+ * phase it all-reduces (SUM, in place, on the context stream) the exchange
+ * buffer named below.  Iteration k:
+ *   IRCUR_SHARD_CORE    zero U, write this shard's rows of the thresholded
+ *                       core U = (D - T(D - L))(I, J)         -> allreduce U
+ *   IRCUR_SHARD_FACTOR  core SVD/pinv of the full U (replicated, bitwise
+ *                       identical on every rank); column strip complete
+ *                       (local rows); row strip: local partial sums of
+ *                       Q_{k+1} = W_r^T R                     -> allreduce Qpart
+ *   IRCUR_SHARD_RESID   row strip again: Q_{k+1} = Qpart with Q(:,J) = W^T U,
+ *                       residual; local {den_I, res_I, den_J, res_J} sums
+ *                                                             -> allreduce scal[0:4]
+ *   IRCUR_SHARD_STOP    e_k from scal, stop flag (device + mapped host)
+ * Kernels of an iteration after the stop are no-ops, so a rank may run ahead
+ * of the stop decision as long as every rank issues the same phases. */
+typedef enum {
+  IRCUR_SHARD_CORE = 0,
+  IRCUR_SHARD_FACTOR = 1,
+  IRCUR_SHARD_RESID = 2,
+  IRCUR_SHARD_STOP = 3
+} ircur_shard_phase_t;
+
+/* Device pointers of the exchange buffers: U (fp64, u_elems), Qpart (context
+ * dtype, q_elems), scal (fp64, 4 used). */
+int ircur_shard_buffers(ircur_ctx_t ctx, void** U, int64_t* u_elems, void** Qpart,
+                        int64_t* q_elems, void** scal);
+/* Start a sharded loop (L_0 = 0, flags cleared); like the prologue of ircur_run. */
+int ircur_shard_reset(ircur_ctx_t ctx);
+/* Enqueue one phase of iteration k (index set `set`, threshold zeta). */
+int ircur_shard_phase(ircur_ctx_t ctx, int phase, int k, int set, double zeta, double eps,
+                      int max_iter);
+/* Non-blocking: device stop flag and completed-iteration count (mapped host
+ * memory written by the STOP phase / the single-device loop). */
+int ircur_poll(ircur_ctx_t ctx, int* done, int* iterations);
+/* Host-blocking end of a sharded loop: iterations, converged, e_k and
+ * per-iteration milliseconds (as ircur_run returns them). */
+int ircur_shard_finish(ircur_ctx_t ctx, const double* zetas, int mode, int* iterations,
+                       int* converged, double* errors, float* iter_ms);
+
 /* Final CUR/sparse strips of the last completed iteration, fp64, written to
  * device or host pointers (cudaMemcpyDefault):  C  local_rows x |J|,
  * R |I_loc| x n2, S_rows |I_loc| x n2, S_cols local_rows x |J| (row-major).
@@ -113,6 +155,11 @@ int ircur_get_core(ircur_ctx_t ctx, double* W, double* sigma, double* V,
 /* Rank-r factors of L = P Q of the last iteration: P = C V diag(inv_sigma)
  * (local_rows x rank), Q = W^T R (rank x n2), in the context dtype. */
 int ircur_get_factors(ircur_ctx_t ctx, void* P, void* Q);
+
+/* Zero-copy access to the same factors: device pointers of P^T (rank x
+ * local_rows, leading dimension *ldp) and Q (rank x n2, *ldq) inside the
+ * context.  Valid until the next ircur_run / ircur_shard_reset. */
+int ircur_factor_buffers(ircur_ctx_t ctx, void** Pt, int64_t* ldp, void** Qt, int64_t* ldq);
 
 /* Stream L = P Q for the local rows into L (device, row-major, ldl),
  * out_dtype IRCUR_F32/F64.  Replaces solver.materialize (solver.py:211-213)

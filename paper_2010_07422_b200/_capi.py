@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_PKG, "libircur_b200.so")
 OK, EINVAL, ENONFINITE, ECUDA, ENCCL, ENOMEM, EEMPTY = 0, -1, -2, -3, -4, -5, -6
 F32, F64 = 0, 1
 FIXED, RESAMPLED = 0, 1
+SHARD_CORE, SHARD_FACTOR, SHARD_RESID, SHARD_STOP = 0, 1, 2, 3
 
 # (name, restype, argtypes) — mirrors include/ircur_b200.h one to one.
 _vp, _i, _i64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
@@ -35,9 +36,15 @@ PROTOTYPES = [
     ("ircur_slab_sqnorms", _i, [_vp, _i, _pd, _pd]),
     ("ircur_run", _i, [_vp, _pd, _d, _i, _i, _pi, _pi, _pd, _pf]),
     ("ircur_iterate", _i, [_vp, _i, _i, _d, _pd]),
+    ("ircur_shard_buffers", _i, [_vp, C.POINTER(_vp), _pi64, C.POINTER(_vp), _pi64, C.POINTER(_vp)]),
+    ("ircur_shard_reset", _i, [_vp]),
+    ("ircur_shard_phase", _i, [_vp, _i, _i, _i, _d, _d, _i]),
+    ("ircur_poll", _i, [_vp, _pi, _pi]),
+    ("ircur_shard_finish", _i, [_vp, _pd, _i, _pi, _pi, _pd, _pf]),
     ("ircur_get_strips", _i, [_vp, _vp, _vp, _vp, _vp]),
     ("ircur_get_core", _i, [_vp, _vp, _vp, _vp, _vp, _pi, _pi, _pi]),
     ("ircur_get_factors", _i, [_vp, _vp, _vp]),
+    ("ircur_factor_buffers", _i, [_vp, C.POINTER(_vp), _pi64, C.POINTER(_vp), _pi64]),
     ("ircur_materialize", _i, [_vp, _vp, _i64, _i]),
     ("ircur_set_profiling", _i, [_vp, _i]),
     ("ircur_get_profile", _i, [_vp, _i, _pi, C.POINTER(C.c_longlong), _pf, _pf, _pf, _pf]),

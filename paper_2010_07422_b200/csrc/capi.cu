@@ -89,6 +89,10 @@ struct ircur_ctx {
   int launched_iters = 0;
   long long kernel_launches = 0;
   int strips_cs = 1;
+  // row sharding: exchange buffers (all-reduced by the caller between phases)
+  void* Qpart = nullptr;     // R x ldq: local partial sums of Q_{k+1} = W^T R
+  double* scal = nullptr;    // 8: {den_rows, res_rows, den_cols, res_cols} local sums
+  int ncta_a = 0;            // CTAs of the last kStripPartial launch (partials offset)
   // last completed iteration
   int last_k = -1, last_set = 0;
   double last_zeta = 0.0;
@@ -114,43 +118,48 @@ int64_t pad4(int64_t n) { return (n + 3) & ~int64_t(3); }
 
 int svd_cluster_size(int n, int m, int kk) { return svd_pick_cluster(n, m, kk); }
 
-template <typename T>
-int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int max_iter,
-                     bool host_flags) {
-  cudaStream_t st = c->stream;
-  const int old = k & 1, nw = old ^ 1;
-  const int* I = c->d_rows + (size_t)set * c->max_rows;
-  const int* J = c->d_cols + (size_t)set * c->max_cols;
-  const int mI_all = c->h_row_cnt[set];
-  const int i_lo = c->h_row_lo[set];
-  const int mI = c->h_row_loc_cnt[set];  // local rows of I (single GPU: all)
-  const int nJ = c->h_col_cnt[set];
-  (void)mI_all;
-  const T zt = storage_zeta<T>(zeta);
-  const int R = c->r;
-  const int* done = c->flags;
+struct IterSets {
+  const int* I;  // local sampled rows (global ids), |I_loc| = mI
+  const int* J;
+  int mI_all, i_lo, mI, nJ;
+};
 
-  CoreArgs<T> ca;
+IterSets iter_sets(const ircur_ctx* c, int set) {
+  IterSets q;
+  q.I = c->d_rows + (size_t)set * c->max_rows + c->h_row_lo[set];
+  q.J = c->d_cols + (size_t)set * c->max_cols;
+  q.mI_all = c->h_row_cnt[set];
+  q.i_lo = c->h_row_lo[set];
+  q.mI = c->h_row_loc_cnt[set];
+  q.nJ = c->h_col_cnt[set];
+  return q;
+}
+
+template <typename T>
+CoreArgs<T> core_args(const ircur_ctx* c, int k, const IterSets& q, double zeta) {
+  const int old = k & 1;
+  CoreArgs<T> ca{};
   ca.D = (const T*)c->D; ca.ldd = c->ldd; ca.row0 = c->row0;
-  ca.I = I + i_lo; ca.mI = mI; ca.J = J; ca.nJ = nJ;
+  ca.I = q.I; ca.mI = q.mI; ca.J = q.J; ca.nJ = q.nJ;
   ca.Pt = (const T*)c->Pt[old]; ca.ldp = c->ldp;
   ca.Qt = (const T*)c->Qt[old]; ca.ldq = c->ldq;
-  ca.zt = zt; ca.U = c->U; ca.ldu = c->max_cols;
-  ca.PoldI = (T*)c->PoldI; ca.QoldJ = (T*)c->QoldJ; ca.done = done;
+  ca.zt = storage_zeta<T>(zeta); ca.U = c->U; ca.ldu = c->max_cols; ca.upos0 = q.i_lo;
+  ca.PoldI = (T*)c->PoldI; ca.QoldJ = (T*)c->QoldJ; ca.done = c->flags;
   ca.rowmap = c->rowmap; ca.colmap = c->colmap;
-  cudaEvent_t* pe = c->profiling ? &c->evp[(size_t)k * 5] : nullptr;
-  if (pe) IR_CUDA(cudaEventRecord(pe[0], st));
-  IR_CUDA(launch_core<T>(ca, R, st));
-  if (pe) IR_CUDA(cudaEventRecord(pe[1], st));
+  return ca;
+}
 
-  SvdArgs sa;
+template <typename T>
+SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
+  const int R = c->r;
+  SvdArgs sa{};
   sa.U = c->U; sa.ldu = c->max_cols; sa.G = c->G; sa.ldg = c->max_cols;
-  sa.m = mI; sa.n = nJ; sa.r = R;
-  sa.kk = std::min(std::min(2 * R, 32), std::min(mI, nJ));
+  sa.m = q.mI_all; sa.n = q.nJ; sa.r = R;  // the full core (all-reduced when row-sharded)
+  sa.kk = std::min(std::min(2 * R, 32), std::min(q.mI_all, q.nJ));
   sa.warm = k > 0 ? c->QoldJ : nullptr; sa.warm_ld = R; sa.warm_cols = k > 0 ? R : 0;
   sa.W = c->W; sa.sigma = c->sigma; sa.V = c->V; sa.inv = c->inv;
   sa.Wr = c->Wr; sa.PI = c->PI; sa.VS = c->VS; sa.QJ = c->QJ;
-  sa.scratch = c->svd_scratch; sa.done = done; sa.steps_out = c->svd_steps + k;
+  sa.scratch = c->svd_scratch; sa.done = c->flags; sa.steps_out = c->svd_steps + k;
   // Ritz-residual target relative to lambda_1: round-off floor, relaxed in
   // early iterations in proportion to e_{k-1} (an SVD perturbation delta
   // moves e_k by ~delta/e_k relative)
@@ -160,21 +169,27 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   sa.dbg = c->profiling ? c->svd_dbg : nullptr;
   sa.maxsteps = 100;
   sa.salt = 0x1234567ull + (uint64_t)k * 7919ull;
-  const int svd_cs = svd_cluster_size(nJ, mI, sa.kk);
-  IR_CUDA(launch_svd<T>(sa, svd_cs, st));
-  if (pe) IR_CUDA(cudaEventRecord(pe[2], st));
+  return sa;
+}
 
-  StripsArgs<T> pa;
+// Both strips in kStripFull mode; the row-sharded phases adjust modes/targets.
+template <typename T>
+StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double zeta) {
+  const int old = k & 1, nw = old ^ 1;
+  const int R = c->r;
   const int TX = strips_tx();
+  StripsArgs<T> pa{};
   StripDesc<T>& rs = pa.s[0];
-  const size_t a16 = 16;
   rs.src = (const T*)c->D; rs.line_stride = c->ldd; rs.pos_stride = 1;
-  rs.bulk_ok = ((c->ldd * (int64_t)sizeof(T)) % 16 == 0) && ((uintptr_t)c->D % a16 == 0);
-  rs.lines = I + i_lo; rs.line_off = (int)c->row0; rs.nk = mI; rs.npos = (int)c->n2;
-  rs.lineA = (const T*)c->PoldI; rs.lineW = (const T*)c->Wr; rs.lineRes = (const T*)c->PI;
+  rs.bulk_ok = ((c->ldd * (int64_t)sizeof(T)) % 16 == 0) && ((uintptr_t)c->D % 16 == 0);
+  rs.lines = q.I; rs.line_off = (int)c->row0; rs.nk = q.mI; rs.npos = (int)c->n2;
+  rs.lineA = (const T*)c->PoldI;
+  rs.lineW = (const T*)c->Wr + (size_t)q.i_lo * R;
+  rs.lineRes = (const T*)c->PI + (size_t)q.i_lo * R;
   rs.Bold = (const T*)c->Qt[old]; rs.ldb = c->ldq; rs.Fnew = (T*)c->Qt[nw]; rs.ldf = c->ldq;
   rs.omap = c->colmap; rs.otherF = (const T*)c->QJ;
   rs.tiles = (int)((c->n2 + TX - 1) / TX);
+  rs.mode = kStripFull;
   StripDesc<T>& cs = pa.s[1];
   if (c->Dt) {
     cs.src = (const T*)c->Dt; cs.line_stride = c->ldt; cs.pos_stride = 1;
@@ -182,31 +197,99 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   } else {
     cs.src = (const T*)c->D; cs.line_stride = 1; cs.pos_stride = c->ldd; cs.bulk_ok = 0;
   }
-  cs.lines = J; cs.line_off = 0; cs.nk = nJ; cs.npos = (int)c->nloc;
+  cs.lines = q.J; cs.line_off = 0; cs.nk = q.nJ; cs.npos = (int)c->nloc;
   cs.lineA = (const T*)c->QoldJ; cs.lineW = (const T*)c->VS; cs.lineRes = (const T*)c->QJ;
   cs.Bold = (const T*)c->Pt[old]; cs.ldb = c->ldp; cs.Fnew = (T*)c->Pt[nw]; cs.ldf = c->ldp;
   cs.omap = c->rowmap; cs.otherF = (const T*)c->PI;
   cs.tiles = (int)((c->nloc + TX - 1) / TX);
-  pa.zt = zt; pa.partials = c->partials; pa.done = done;
+  cs.mode = kStripFull;
+  pa.zt = storage_zeta<T>(zeta); pa.partials = c->partials; pa.done = c->flags;
   pa.maxl = (std::max(c->max_rows, c->max_cols) + c->strips_cs - 1) / c->strips_cs;
-  int ncta = 0;
-  IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, c->num_sms, &ncta, st));
-  if (pe) IR_CUDA(cudaEventRecord(pe[3], st));
+  return pa;
+}
 
-  FinalizeArgs fa;
+FinalizeArgs finalize_args(ircur_ctx* c, int k, const IterSets& q, double eps, int max_iter, bool host_flags) {
+  FinalizeArgs fa{};
   fa.partials = c->partials;
-  fa.ncta_rows = ncta;
-  fa.ncta_cols = 0;
-  fa.I = I + i_lo; fa.mI = mI; fa.J = J; fa.nJ = nJ; fa.row0 = c->row0;
+  fa.I = q.I; fa.mI = q.mI; fa.J = q.J; fa.nJ = q.nJ; fa.row0 = c->row0;
   fa.rowmap = c->rowmap; fa.colmap = c->colmap;
   fa.k = k; fa.eps = eps; fa.max_iter = max_iter;
   fa.errors = c->errors; fa.done = c->flags; fa.iters = c->flags + 1; fa.converged = c->flags + 2;
   fa.host_done = host_flags ? c->h_flags_dev : nullptr;
   fa.host_iters = host_flags ? c->h_flags_dev + 1 : nullptr;
+  return fa;
+}
+
+// One single-device iteration: core -> gram+svd -> fused strips -> finalize.
+template <typename T>
+int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int max_iter,
+                     bool host_flags) {
+  cudaStream_t st = c->stream;
+  const IterSets q = iter_sets(c, set);
+  const int R = c->r;
+  cudaEvent_t* pe = c->profiling ? &c->evp[(size_t)k * 5] : nullptr;
+  if (pe) IR_CUDA(cudaEventRecord(pe[0], st));
+  IR_CUDA(launch_core<T>(core_args<T>(c, k, q, zeta), R, st));
+  if (pe) IR_CUDA(cudaEventRecord(pe[1], st));
+  const SvdArgs sa = svd_args<T>(c, k, q);
+  IR_CUDA(launch_svd<T>(sa, svd_cluster_size(q.nJ, q.mI_all, sa.kk), st));
+  if (pe) IR_CUDA(cudaEventRecord(pe[2], st));
+  int ncta = 0;
+  IR_CUDA(launch_strips<T>(strips_args<T>(c, k, q, zeta), R, c->strips_cs, c->num_sms, &ncta, st));
+  if (pe) IR_CUDA(cudaEventRecord(pe[3], st));
+  FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, host_flags);
+  fa.ncta_rows = ncta;
   IR_CUDA(launch_finalize(fa, st));
   if (pe) IR_CUDA(cudaEventRecord(pe[4], st));
   c->kernel_launches += 5;  // core, gram, svd, strips, finalize
   ++c->launched_iters;
+  return IRCUR_OK;
+}
+
+// Row-sharded iteration, one phase at a time; the caller all-reduces the
+// exchange buffer named in include/ircur_b200.h between phases.
+template <typename T>
+int launch_shard_phase(ircur_ctx* c, int phase, int k, int set, double zeta, double eps, int max_iter) {
+  cudaStream_t st = c->stream;
+  const IterSets q = iter_sets(c, set);
+  const int R = c->r;
+  if (phase == IRCUR_SHARD_CORE) {
+    // rows of U owned by other shards must be zero for the summing all-reduce
+    IR_CUDA(cudaMemsetAsync(c->U, 0, (size_t)c->max_rows * c->max_cols * sizeof(double), st));
+    IR_CUDA(launch_core<T>(core_args<T>(c, k, q, zeta), R, st));
+    c->kernel_launches += 1;
+  } else if (phase == IRCUR_SHARD_FACTOR) {
+    const SvdArgs sa = svd_args<T>(c, k, q);
+    IR_CUDA(launch_svd<T>(sa, svd_cluster_size(q.nJ, q.mI_all, sa.kk), st));
+    StripsArgs<T> pa = strips_args<T>(c, k, q, zeta);
+    pa.s[0].mode = kStripPartial;
+    pa.s[0].Fnew = (T*)c->Qpart;
+    IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, c->num_sms, &c->ncta_a, st));
+    c->kernel_launches += 3;  // gram, svd, strips
+  } else if (phase == IRCUR_SHARD_RESID) {
+    StripsArgs<T> pa = strips_args<T>(c, k, q, zeta);
+    pa.s[0].mode = kStripFinish;
+    pa.s[0].Fsrc = (const T*)c->Qpart;
+    pa.s[0].ldfs = c->ldq;
+    pa.s[1].tiles = 0;
+    pa.partials = c->partials + 4 * (size_t)c->ncta_a;
+    int ncta_b = 0;
+    IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, c->num_sms, &ncta_b, st));
+    FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, false);
+    fa.ncta_rows = c->ncta_a + ncta_b;
+    fa.sums_out = c->scal;
+    IR_CUDA(launch_finalize(fa, st));
+    c->kernel_launches += 2;
+  } else if (phase == IRCUR_SHARD_STOP) {
+    FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, true);
+    fa.partials = c->scal;
+    fa.ncta_rows = 1;
+    IR_CUDA(launch_finalize(fa, st));
+    c->kernel_launches += 1;
+    ++c->launched_iters;
+  } else {
+    return fail(IRCUR_EINVAL, "unknown shard phase");
+  }
   return IRCUR_OK;
 }
 
@@ -286,6 +369,9 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->inv, (size_t)rank * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->G, (size_t)max_cols * max_cols * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->svd_scratch, 2 * (size_t)max_cols * 32 * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->Qpart, (size_t)rank * c->ldq * c->esz));
+  IR_CUDA_C(cudaMalloc(&c->scal, 8 * sizeof(double)));
+  IR_CUDA_C(cudaMemsetAsync(c->scal, 0, 8 * sizeof(double), c->stream));
   c->max_partials = 4 * 2 * c->num_sms + 8192;  // strips: 4 sums per persistent CTA (<= 2/SM)
   IR_CUDA_C(cudaMalloc(&c->partials, (size_t)c->max_partials * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->rowmap, (size_t)local_rows * sizeof(int)));
@@ -315,7 +401,7 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U,
                   c->PoldI, c->QoldJ, c->Wr, c->PI, c->VS, c->QJ, c->W, c->sigma, c->V, c->inv,
                   c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps,
-                  c->rowmap, c->colmap, c->svd_dbg};
+                  c->rowmap, c->colmap, c->svd_dbg, c->Qpart, c->scal};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -442,16 +528,13 @@ int ircur_slab_sqnorms(ircur_ctx_t c, int set, double* rows_sq, double* cols_sq)
   return IRCUR_OK;
 }
 
-int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_iter, int* iterations,
-              int* converged, double* errors, float* iter_ms) {
-  if (!c || !c->D || !zetas) return fail(IRCUR_EINVAL, "null context, D or zetas");
-  if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
-  if (mode == IRCUR_RESAMPLED && c->n_sets < max_iter)
-    return fail(IRCUR_EINVAL, "resampled mode needs max_iter index sets");
-  if (c->n_sets < 1) return fail(IRCUR_EINVAL, "no index sets uploaded");
-  IR_CUDA(cudaSetDevice(c->device));
+}  // extern "C"
+
+namespace {
+
+// L_0 = 0: P_0 = Q_0 = 0 (solver.py:352-353); fresh flags and position maps.
+int reset_loop(ircur_ctx* c) {
   cudaStream_t st = c->stream;
-  // L_0 = 0: P_0 = Q_0 = 0 (solver.py:352-353)
   IR_CUDA(cudaMemsetAsync(c->Pt[0], 0, (size_t)c->r * c->ldp * c->esz, st));
   IR_CUDA(cudaMemsetAsync(c->Qt[0], 0, (size_t)c->r * c->ldq * c->esz, st));
   IR_CUDA(cudaMemsetAsync(c->flags, 0, 16 * sizeof(int), st));
@@ -463,28 +546,13 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   IR_CUDA(cudaEventRecord(c->ev[0], st));
   c->launched_iters = 0;
   c->kernel_launches = 0;
-  constexpr int kAhead = 3;
-  int launched = 0;
-  while (true) {
-    const int seen = hf[1];
-    const bool fin = hf[0] != 0;
-    while (!fin && launched < max_iter && launched < seen + kAhead) {
-      const int set = mode == IRCUR_FIXED ? 0 : launched;
-      int rc = iteration(c, launched, set, zetas[launched], eps, max_iter, true);
-      if (rc) return rc;
-      IR_CUDA(cudaEventRecord(c->ev[launched + 1], st));
-      ++launched;
-    }
-    if (fin || launched == max_iter) break;
-    // spin until the device reports progress (mapped memory, no API sync)
-    const int before = seen;
-    while (hf[0] == 0 && hf[1] == before) {
-      cudaError_t q = cudaStreamQuery(st);
-      if (q == cudaSuccess) break;  // everything queued has finished
-      if (q != cudaErrorNotReady) return fail(IRCUR_ECUDA, std::string("stream: ") + cudaGetErrorString(q));
-    }
-  }
-  IR_CUDA(cudaStreamSynchronize(st));
+  return IRCUR_OK;
+}
+
+// Wait for the stream, read the device trace, remember the final state.
+int read_trace(ircur_ctx* c, const double* zetas, int mode, int* iterations, int* converged,
+               double* errors, float* iter_ms) {
+  IR_CUDA(cudaStreamSynchronize(c->stream));
   int hflags[3] = {0, 0, 0};
   IR_CUDA(cudaMemcpy(hflags, c->flags, 3 * sizeof(int), cudaMemcpyDeviceToHost));
   const int iters = hflags[1];
@@ -507,9 +575,97 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   return IRCUR_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_iter, int* iterations,
+              int* converged, double* errors, float* iter_ms) {
+  if (!c || !c->D || !zetas) return fail(IRCUR_EINVAL, "null context, D or zetas");
+  if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
+  if (mode == IRCUR_RESAMPLED && c->n_sets < max_iter)
+    return fail(IRCUR_EINVAL, "resampled mode needs max_iter index sets");
+  if (c->n_sets < 1) return fail(IRCUR_EINVAL, "no index sets uploaded");
+  if (c->nloc != c->n1) return fail(IRCUR_EINVAL, "row-sharded context: use ircur_shard_phase");
+  IR_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  if (int rc = reset_loop(c)) return rc;
+  volatile int* hf = c->h_flags;
+  constexpr int kAhead = 3;
+  int launched = 0;
+  while (true) {
+    const int seen = hf[1];
+    const bool fin = hf[0] != 0;
+    while (!fin && launched < max_iter && launched < seen + kAhead) {
+      const int set = mode == IRCUR_FIXED ? 0 : launched;
+      int rc = iteration(c, launched, set, zetas[launched], eps, max_iter, true);
+      if (rc) return rc;
+      IR_CUDA(cudaEventRecord(c->ev[launched + 1], st));
+      ++launched;
+    }
+    if (fin || launched == max_iter) break;
+    // spin until the device reports progress (mapped memory, no API sync)
+    const int before = seen;
+    while (hf[0] == 0 && hf[1] == before) {
+      cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) break;  // everything queued has finished
+      if (q != cudaErrorNotReady) return fail(IRCUR_ECUDA, std::string("stream: ") + cudaGetErrorString(q));
+    }
+  }
+  return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
+}
+
+int ircur_shard_buffers(ircur_ctx_t c, void** U, int64_t* u_elems, void** Qpart, int64_t* q_elems,
+                        void** scal) {
+  if (!c) return fail(IRCUR_EINVAL, "null context");
+  if (U) *U = c->U;
+  if (u_elems) *u_elems = (int64_t)c->max_rows * c->max_cols;
+  if (Qpart) *Qpart = c->Qpart;
+  if (q_elems) *q_elems = (int64_t)c->r * c->ldq;
+  if (scal) *scal = c->scal;
+  return IRCUR_OK;
+}
+
+int ircur_shard_reset(ircur_ctx_t c) {
+  if (!c || !c->D) return fail(IRCUR_EINVAL, "null context or D");
+  if (c->n_sets < 1) return fail(IRCUR_EINVAL, "no index sets uploaded");
+  IR_CUDA(cudaSetDevice(c->device));
+  return reset_loop(c);
+}
+
+int ircur_shard_phase(ircur_ctx_t c, int phase, int k, int set, double zeta, double eps, int max_iter) {
+  if (!c || !c->D) return fail(IRCUR_EINVAL, "null context or D");
+  if (k < 0 || k >= c->max_iter || set < 0 || set >= c->n_sets || max_iter < 1 || max_iter > c->max_iter)
+    return fail(IRCUR_EINVAL, "bad k/set/max_iter");
+  IR_CUDA(cudaSetDevice(c->device));
+  int rc = c->dtype == IRCUR_F32 ? launch_shard_phase<float>(c, phase, k, set, zeta, eps, max_iter)
+                                 : launch_shard_phase<double>(c, phase, k, set, zeta, eps, max_iter);
+  if (rc == IRCUR_OK && phase == IRCUR_SHARD_STOP) IR_CUDA(cudaEventRecord(c->ev[k + 1], c->stream));
+  return rc;
+}
+
+int ircur_poll(ircur_ctx_t c, int* done, int* iterations) {
+  if (!c) return fail(IRCUR_EINVAL, "null context");
+  volatile int* hf = c->h_flags;
+  if (done) *done = hf[0];
+  if (iterations) *iterations = hf[1];
+  const cudaError_t q = cudaStreamQuery(c->stream);
+  if (q != cudaSuccess && q != cudaErrorNotReady)
+    return fail(IRCUR_ECUDA, std::string("stream: ") + cudaGetErrorString(q));
+  return IRCUR_OK;
+}
+
+int ircur_shard_finish(ircur_ctx_t c, const double* zetas, int mode, int* iterations, int* converged,
+                       double* errors, float* iter_ms) {
+  if (!c || !zetas) return fail(IRCUR_EINVAL, "null context or zetas");
+  IR_CUDA(cudaSetDevice(c->device));
+  return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
+}
+
 int ircur_iterate(ircur_ctx_t c, int k, int set, double zeta, double* e) {
   if (!c || !c->D) return fail(IRCUR_EINVAL, "null context or D");
   if (k < 0 || k >= c->max_iter || set < 0 || set >= c->n_sets) return fail(IRCUR_EINVAL, "bad k/set");
+  if (c->nloc != c->n1) return fail(IRCUR_EINVAL, "row-sharded context: use ircur_shard_phase");
   IR_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   if (k == 0) {
@@ -587,7 +743,7 @@ int ircur_get_core(ircur_ctx_t c, double* W, double* sigma, double* V, double* i
   if (!c || !c->has_state) return fail(IRCUR_EINVAL, "no completed iteration");
   IR_CUDA(cudaSetDevice(c->device));
   const int set = c->last_set;
-  const int mI = c->h_row_loc_cnt[set], nJ = c->h_col_cnt[set];
+  const int mI = c->h_row_cnt[set], nJ = c->h_col_cnt[set];  // the full (replicated) core
   const int kk = std::min(c->r, std::min(mI, nJ));
   if (k) *k = kk;
   if (n_rows) *n_rows = mI;
@@ -617,6 +773,16 @@ int ircur_get_factors(ircur_ctx_t c, void* P, void* Q) {
     IR_CUDA(cudaMemcpy2DAsync(Q, c->n2 * c->esz, c->Qt[nw], c->ldq * c->esz, c->n2 * c->esz, c->r,
                               cudaMemcpyDefault, c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));
+  return IRCUR_OK;
+}
+
+int ircur_factor_buffers(ircur_ctx_t c, void** Pt, int64_t* ldp, void** Qt, int64_t* ldq) {
+  if (!c || !c->has_state) return fail(IRCUR_EINVAL, "no completed iteration");
+  const int nw = (c->last_k & 1) ^ 1;
+  if (Pt) *Pt = c->Pt[nw];
+  if (ldp) *ldp = c->ldp;
+  if (Qt) *Qt = c->Qt[nw];
+  if (ldq) *ldq = c->ldq;
   return IRCUR_OK;
 }
 

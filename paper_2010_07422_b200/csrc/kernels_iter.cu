@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs<T> a) {
   if (k2 == 0) {
 #pragma unroll
     for (int t = 0; t < R; ++t) a.PoldI[(int64_t)k1 * R + t] = pa[t];
-    a.rowmap[il] = k1;
+    a.rowmap[il] = a.upos0 + k1;
   }
   if (k1 == 0) {
 #pragma unroll
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs<T> a) {
   const T d = a.D[il * a.ldd + j];
   T s;
   const T c = keep_value(d, l, a.zt, s);
-  a.U[(int64_t)k1 * a.ldu + k2] = (double)c;
+  a.U[(int64_t)(a.upos0 + k1) * a.ldu + k2] = (double)c;
 }
 
 // ------------------------------------------------------------- finalize
@@ -58,8 +58,10 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(FinalizeArgs a) {
   __shared__ double sh[4][kFinNT / 32];
   const int tid = threadIdx.x;
   // the strips of this iteration are finished: reset the position maps
-  for (int e = tid; e < a.mI; e += kFinNT) a.rowmap[a.I[e] - a.row0] = -1;
-  for (int e = tid; e < a.nJ; e += kFinNT) a.colmap[a.J[e]] = -1;
+  if (!a.sums_out) {
+    for (int e = tid; e < a.mI; e += kFinNT) a.rowmap[a.I[e] - a.row0] = -1;
+    for (int e = tid; e < a.nJ; e += kFinNT) a.colmap[a.J[e]] = -1;
+  }
   // deterministic: each thread sums a fixed strided subset (loads unrolled,
   // adds in order), then a fixed butterfly per warp and a fixed warp order.
   double v[4] = {0, 0, 0, 0};
@@ -81,6 +83,10 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(FinalizeArgs a) {
     double s[4] = {0, 0, 0, 0};
     for (int q = 0; q < 4; ++q)
       for (int i = 0; i < kFinNT / 32; ++i) s[q] += sh[q][i];
+    if (a.sums_out) {  // row-sharded: local sums, all-reduced by the caller
+      for (int q = 0; q < 4; ++q) a.sums_out[q] = s[q];
+      return;
+    }
     const double den = sqrt(s[0]) + sqrt(s[2]);
     const double e = (sqrt(s[1]) + sqrt(s[3])) / den;
     a.errors[a.k] = e;
@@ -93,10 +99,13 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(FinalizeArgs a) {
       fin = 1;
     }
     if (fin) *a.done = 1;
-    if (a.host_iters) {
+    if (a.host_iters) {  // iteration count visible before the stop flag (ircur_poll reads done first)
       *a.host_iters = a.k + 1;
-      if (fin) *a.host_done = 1;
       __threadfence_system();
+      if (fin) {
+        *a.host_done = 1;
+        __threadfence_system();
+      }
     }
   }
 }

@@ -16,7 +16,8 @@ struct CoreArgs {
   const T* Pt; int64_t ldp;                    // P_k^T  (R x nloc)
   const T* Qt; int64_t ldq;                    // Q_k^T  (R x n2)
   T zt;
-  double* U; int ldu;                          // mI x nJ
+  double* U; int ldu;                          // mI x nJ (rows start at upos0)
+  int upos0;                                   // position of the first local row inside I (row sharding)
   T* PoldI; T* QoldJ;                          // mI x R, nJ x R
   int* rowmap; int* colmap;                    // position -> index maps (set here, cleared by finalize)
   const int* done;
@@ -41,7 +42,16 @@ struct StripDesc {
   const int* omap;                             // npos: index into otherF, or -1
   const T* otherF;                             // (other set size) x R
   int tiles;                                   // ceil(npos / TX)
+  // kStripFull: Phase I/II + factor + override + residual in one pass.
+  // Row sharding splits the row strip in two launches around the all-reduce
+  // of Q: kStripPartial writes the un-overridden local partial sums
+  // (Fnew = sum over the local lines), kStripFinish re-thresholds the tile,
+  // takes Fnew from Fsrc (the all-reduced sums), applies the override and
+  // accumulates the residual.
+  int mode;
+  const T* Fsrc; int64_t ldfs;                 // kStripFinish only: R x npos
 };
+constexpr int kStripFull = 0, kStripPartial = 1, kStripFinish = 2;
 
 template <typename T>
 struct StripsArgs {
@@ -60,6 +70,7 @@ struct FinalizeArgs {
   volatile int* host_done; volatile int* host_iters;   // mapped pinned memory (may be null)
   const int* I; int mI; const int* J; int nJ; int64_t row0;
   int* rowmap; int* colmap;                    // cleared back to -1 for this iteration's sets
+  double* sums_out;                            // non-null: only reduce the partials into 4 sums here
 };
 
 // --------------------------------------------------------------- writeout

@@ -242,6 +242,8 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     __syncthreads();   // ... and everybody else's
 
     // ---- pass 1: Phase I/II in place + factor partials
+    const int mode = s.mode;  // uniform per tile (and per cluster)
+    const bool accum = mode != kStripFinish;
     Pair<T> b[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) b[t] = lds_pair(bsg + t * kSTX + 2 * lane);
@@ -276,10 +278,12 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
         den = fma_rn(d[g].v.y, d[g].v.y, den);
         sts_pair(stg + (size_t)(kl + g * kSNW) * kSTX + pe, c[g]);
       }
+      if (accum) {
 #pragma unroll
-      for (int t = 0; t < R; ++t)
+        for (int t = 0; t < R; ++t)
 #pragma unroll
-        for (int g = 0; g < kG; ++g) acc[t] = pfma(Pair<T>::splat(av[g][RP + t]), c[g], acc[t]);
+          for (int g = 0; g < kG; ++g) acc[t] = pfma(Pair<T>::splat(av[g][RP + t]), c[g], acc[t]);
+      }
     }
     for (; kl < nl; kl += kSNW) {
       T* cell = stg + (size_t)kl * kSTX + pe;
@@ -295,34 +299,43 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
       den = fma_rn(d.v.x, d.v.x, den);
       den = fma_rn(d.v.y, d.v.y, den);
       sts_pair(cell, c);
-      const T* wv = av + RP;
+      if (accum) {
+        const T* wv = av + RP;
 #pragma unroll
-      for (int t = 0; t < R; ++t) acc[t] = pfma(Pair<T>::splat(wv[t]), c, acc[t]);
+        for (int t = 0; t < R; ++t) acc[t] = pfma(Pair<T>::splat(wv[t]), c, acc[t]);
+      }
     }
-    if (q == 0) den_acc0 += (double)den; else den_acc1 += (double)den;
+    if (accum) {
+      if (q == 0) den_acc0 += (double)den; else den_acc1 += (double)den;
 #pragma unroll
-    for (int t = 0; t < R; ++t) sts_pair(red + ((size_t)w * R + t) * kSTX + pe, acc[t]);
-    __syncthreads();
-    T* pbuf = part + (size_t)(i & 1) * R * kSTX;
-    T* fsum = CS > 1 ? pbuf : fnew;
-    for (int o = tid; o < R * kSTX; o += kSNT) {
-      T sum = red[o];
-#pragma unroll
-      for (int ww = 1; ww < kSNW; ++ww) sum += red[(size_t)ww * R * kSTX + o];
-      fsum[o] = sum;
-    }
-    if (CS > 1) {
-      cl.sync();
+      for (int t = 0; t < R; ++t) sts_pair(red + ((size_t)w * R + t) * kSTX + pe, acc[t]);
+      __syncthreads();
+      T* pbuf = part + (size_t)(i & 1) * R * kSTX;
+      T* fsum = CS > 1 ? pbuf : fnew;
       for (int o = tid; o < R * kSTX; o += kSNT) {
-        T sum = *cl.map_shared_rank(pbuf + o, 0);
-        for (int qq = 1; qq < CS; ++qq) sum += *cl.map_shared_rank(pbuf + o, qq);
-        fnew[o] = sum;
+        T sum = red[o];
+#pragma unroll
+        for (int ww = 1; ww < kSNW; ++ww) sum += red[(size_t)ww * R * kSTX + o];
+        fsum[o] = sum;
+      }
+      if (CS > 1) {
+        cl.sync();
+        for (int o = tid; o < R * kSTX; o += kSNT) {
+          T sum = *cl.map_shared_rank(pbuf + o, 0);
+          for (int qq = 1; qq < CS; ++qq) sum += *cl.map_shared_rank(pbuf + o, qq);
+          fnew[o] = sum;
+        }
+      }
+    } else {  // kStripFinish: the factor sums were all-reduced across the row shards
+      for (int o = tid; o < R * kSTX; o += kSNT) {
+        const int t = o / kSTX, x = o - t * kSTX;
+        fnew[o] = x0 + x < s.npos ? s.Fsrc[(int64_t)t * s.ldfs + x0 + x] : T(0);
       }
     }
     __syncthreads();
     // positions of the other index set take the factor computed from the core
     // (Q(:,J) = W^T U, P(I,:) = U V Sigma^+): one value for the I x J block.
-    for (int x = tid; x < kSTX; x += kSNT) {
+    for (int x = tid; x < kSTX && mode != kStripPartial; x += kSNT) {
       const int pos = x0 + x;
       if (pos < s.npos) {
         const int e = s.omap[pos];
@@ -336,6 +349,11 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     for (int o = tid; o < R * kSTX; o += kSNT) {
       const int t = o / kSTX, x = o - t * kSTX;
       if ((t % CS) == rank && x0 + x < s.npos) s.Fnew[(int64_t)t * s.ldf + x0 + x] = fnew[o];
+    }
+    if (mode == kStripPartial) {  // residual after the all-reduce (kStripFinish launch)
+      __syncthreads();
+      issue(i + 2, st);
+      continue;
     }
     // ---- pass 2: stopping residual on the thresholded tile
     Pair<T> f[R];
@@ -443,6 +461,7 @@ template <typename T>
 cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, int* ncta_out,
                           cudaStream_t st) {
   const int tiles = a.s[0].tiles + a.s[1].tiles;
+  if (ncta_out) *ncta_out = 0;
   if (tiles == 0) return cudaSuccess;
   cudaError_t e = cudaErrorInvalidValue;
   IRCUR_DISPATCH_RANK(R, RR, e = launch_strips_r<T, RR>(a, cs, num_sms, st));

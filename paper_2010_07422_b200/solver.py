@@ -166,6 +166,58 @@ class Context:
                     core_ms=arrs[0][:n_iters], svd_ms=arrs[1][:n_iters],
                     strips_ms=arrs[2][:n_iters], finalize_ms=arrs[3][:n_iters])
 
+    # ---- row-sharded loop (include/ircur_b200.h, "Row-sharded loop")
+    def shard_buffers(self):
+        """(U fp64, Qpart, scal[:4]) as zero-copy torch views of the context's
+        exchange buffers, for the caller's all-reduce."""
+        u, q, sc = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        nu, nq = C.c_int64(), C.c_int64()
+        _capi.check(self.lib.ircur_shard_buffers(self.h, C.byref(u), C.byref(nu), C.byref(q), C.byref(nq),
+                                                 C.byref(sc)))
+        qdt = "<f4" if self.dtype == _capi.F32 else "<f8"
+        return (_device_view(u.value, nu.value, "<f8", self.device),
+                _device_view(q.value, nq.value, qdt, self.device),
+                _device_view(sc.value, 4, "<f8", self.device))
+
+    def host_tensor(self, vals) -> torch.Tensor:
+        """A small fp64 tensor on this context's device (scalar all-reduces)."""
+        return torch.tensor(vals, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def shard_reset(self) -> None:
+        _capi.check(self.lib.ircur_shard_reset(self.h))
+
+    def shard_phase(self, phase: int, k: int, s: int, zeta: float, eps: float, max_iter: int) -> None:
+        _capi.check(self.lib.ircur_shard_phase(self.h, phase, k, s, zeta, eps, max_iter))
+
+    def poll(self) -> tuple[bool, int]:
+        d, it = C.c_int(), C.c_int()
+        _capi.check(self.lib.ircur_poll(self.h, C.byref(d), C.byref(it)))
+        return bool(d.value), it.value
+
+    def shard_finish(self, zetas, mode: int):
+        z = np.ascontiguousarray(zetas, dtype=np.float64)
+        n = len(z)
+        errors = np.zeros(n, dtype=np.float64)
+        ms = np.zeros(n, dtype=np.float32)
+        it, conv = C.c_int(0), C.c_int(0)
+        pd = C.POINTER(C.c_double)
+        _capi.check(self.lib.ircur_shard_finish(self.h, z.ctypes.data_as(pd), mode, C.byref(it), C.byref(conv),
+                                                errors.ctypes.data_as(pd), ms.ctypes.data_as(C.POINTER(C.c_float))))
+        n = it.value
+        return n, bool(conv.value), errors[:n], ms[:n]
+
+    def factor_views(self):
+        """(P^T, Q) as zero-copy views of the context's final factor buffers
+        (valid until the next solve on this context)."""
+        pp, qq = C.c_void_p(), C.c_void_p()
+        lp, lq = C.c_int64(), C.c_int64()
+        _capi.check(self.lib.ircur_factor_buffers(self.h, C.byref(pp), C.byref(lp), C.byref(qq), C.byref(lq)))
+        ts = "<f4" if self.dtype == _capi.F32 else "<f8"
+        r = self.rank
+        Pt = _device_view(pp.value, r * lp.value, ts, self.device).view(r, lp.value)[:, :self.local_rows]
+        Qt = _device_view(qq.value, r * lq.value, ts, self.device).view(r, lq.value)[:, :self.n2]
+        return Pt, Qt
+
     def factors(self):
         tdt = torch.float32 if self.dtype == _capi.F32 else torch.float64
         dev = f"cuda:{self.device}"
@@ -175,12 +227,26 @@ class Context:
         return Pt, Qt
 
 
+class _CudaArray:
+    """__cuda_array_interface__ wrapper so torch can view a library buffer."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                         "strides": None, "version": 3}
+
+
+def _device_view(ptr: int, n: int, typestr: str, device: int) -> torch.Tensor:
+    return torch.as_tensor(_CudaArray(ptr, n, typestr), device=f"cuda:{device}")
+
+
 _CACHE: "OrderedDict[tuple, Context]" = OrderedDict()
 _CACHE_MAX = 4
 
 
-def _context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream) -> Context:
-    key = (device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream)
+def _context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0=0,
+             local_rows=None) -> Context:
+    local_rows = n1 if local_rows is None else local_rows
+    key = (device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0, local_rows)
     ctx = _CACHE.get(key)
     if ctx is not None:
         _CACHE.move_to_end(key)
@@ -189,13 +255,13 @@ def _context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream) -> C
         _, old = _CACHE.popitem(last=False)
         old.close()
     try:
-        ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream=stream)
+        ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, row0, local_rows, stream=stream)
     except MemoryError:
         for _, old in _CACHE.items():
             old.close()
         _CACHE.clear()
         torch.cuda.empty_cache()
-        ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream=stream)
+        ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, row0, local_rows, stream=stream)
     _CACHE[key] = ctx
     return ctx
 
@@ -286,7 +352,14 @@ class DeviceResult:
 
 def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
                  colmajor="auto", fetch_factors=True, profile=False) -> DeviceResult:
-    """Run the loop on the device; results stay on the device (see solve)."""
+    """Run the loop on the device; results stay on the device (see solve).
+
+    The returned DeviceResult reads its strips/core from the cached library
+    context, and with fetch_factors=True its `handle` holds zero-copy views
+    of the context's final factors: both stay valid until the next solve on
+    the same context (same device, shape, dtype and stream).  Pass
+    fetch_factors="copy" for private factor tensors.
+    """
     cfg = config
     tick = _Ticker(profile)
     Dd = _device_matrix(D, device, compute_dtype)
@@ -359,7 +432,9 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     I, J = sets[last]
     handle = None
     if fetch_factors:
-        Pt, Qt = ctx.factors()
+        # zero-copy views into the context (valid until its next solve);
+        # fetch_factors="copy" returns private tensors instead
+        Pt, Qt = ctx.factors() if fetch_factors == "copy" else ctx.factor_views()
         handle = DeviceHandle(Pt, Qt, dtype)
         tick("factors")
     res = DeviceResult(trace, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), handle)
@@ -404,7 +479,7 @@ def solve(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=
     copy of D used by the column-strip kernel: True/False/"auto").
     """
     res = solve_device(D, config, observer, device=device, compute_dtype=compute_dtype,
-                       colmajor=colmajor)
+                       colmajor=colmajor, fetch_factors="copy")
     n1, n2 = res.rows.bound, res.cols.bound
     if res.zero_state:
         cur, sparse = _zero_results(n1, n2, res.rows, res.cols, config.rank)

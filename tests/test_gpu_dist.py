@@ -1,0 +1,106 @@
+"""Row-sharded device path (ircur_shard_* C-ABI) on one GPU.
+
+Ranks are emulated in one process by the lockstep driver of
+paper_2010_07422_b200/dist.py: each rank has its own library context over
+its rows of D, and the all-reduces are done between phases by torch ops on
+the same stream, so no kernel ever waits on another rank's kernel.
+  * one shard: the split row-strip launches (partial sums, then finish)
+    reproduce the single-GPU fused kernel bit for bit;
+  * 2 and 3 shards: the oracle within the north-star tolerances (the Q sums
+    are reassociated across shards, so not bitwise).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ircur_oracle as orc
+import paper_2010_07422_b200 as ir
+from paper_2010_07422_b200.dist import gather_program, run_lockstep, shard_rows, solve_shard_program
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(n1, n2, rank, seed=11, alpha=0.1):
+    D, _, _, linf = orc.baseline_problem(n1, n2, rank, alpha, seed)
+    return D, linf
+
+
+def _cfg(rank, linf, mode="resampled", eps=1e-9, max_iter=80):
+    return ir.SolverConfig(rank=rank, eps=eps, zeta0=linf, gamma=0.7, mode=mode, max_iter=max_iter,
+                           seed=ir.RngSeed(2))
+
+
+def _sharded(Dd, cfg, world):
+    n1 = Dd.shape[0]
+    progs = []
+    for g in range(world):
+        r0, nl = shard_rows(n1, world, g)
+        progs.append(solve_shard_program(Dd[r0:r0 + nl], cfg, n1=n1, row0=r0))
+    res = run_lockstep(progs)
+    assert len({r.launched for r in res}) == 1
+    return res, run_lockstep([gather_program(r) for r in res])
+
+
+def _rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+def test_one_shard_bitwise_equals_single_gpu(mode):
+    D, linf = _problem(240, 200, 4)
+    cfg = _cfg(4, linf, mode)
+    Dd = torch.from_numpy(D).cuda()
+    cur1, sp1, tr1 = ir.solve(Dd, cfg)
+    _, out = _sharded(Dd, cfg, 1)
+    cur, sp, tr = out[0]
+    assert tr.iterations == tr1.iterations and tr.converged == tr1.converged
+    assert tr.errors == tr1.errors
+    for a, b in ((cur.C, cur1.C), (cur.R, cur1.R), (sp.row_values, sp1.row_values),
+                 (sp.col_values, sp1.col_values), (cur.core_pinv.sigma, cur1.core_pinv.sigma)):
+        np.testing.assert_array_equal(a, b)
+    ir.clear_cache()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+def test_sharded_fp64_matches_oracle(world, mode):
+    D, linf = _problem(301, 257, 4)
+    cfg = _cfg(4, linf, mode)
+    ref = orc.solve(D, rank=4, eps=cfg.eps, zeta0=linf, gamma=0.7, mode=mode, max_iter=cfg.max_iter, seed=2)
+    _, out = _sharded(torch.from_numpy(D).cuda(), cfg, world)
+    for cur, sp, tr in out:
+        assert tr.iterations == ref.iterations and tr.converged == ref.converged
+        np.testing.assert_allclose(tr.errors, ref.errors, rtol=1e-9, atol=1e-15)
+        np.testing.assert_array_equal(cur.rows.indices, ref.rows)
+        np.testing.assert_array_equal(cur.cols.indices, ref.cols)
+        for a, b in ((cur.C, ref.C), (cur.R, ref.R), (sp.row_values, ref.S_rows), (sp.col_values, ref.S_cols)):
+            assert _rel(a, b) < 1e-9
+        np.testing.assert_allclose(cur.core_pinv.sigma, ref.sigma, rtol=1e-9)
+    ir.clear_cache()
+
+
+def test_sharded_fp32_matches_oracle():
+    D, linf = _problem(400, 380, 5, alpha=0.2)
+    D32 = D.astype(np.float32)
+    cfg = _cfg(5, linf, eps=1e-5)
+    ref = orc.solve(D32.astype(np.float64), rank=5, eps=1e-5, zeta0=linf, gamma=0.7, mode="resampled",
+                    max_iter=cfg.max_iter, seed=2)
+    _, out = _sharded(torch.from_numpy(D32).cuda(), cfg, 2)
+    cur, sp, tr = out[0]
+    assert abs(tr.iterations - ref.iterations) <= 1 and tr.converged
+    n = min(tr.iterations, ref.iterations)
+    np.testing.assert_allclose(tr.errors[:n], ref.errors[:n], rtol=1e-4 if n < 3 else 1e-2)
+    if tr.iterations == ref.iterations:
+        for a, b in ((cur.C, ref.C), (cur.R, ref.R), (sp.row_values, ref.S_rows)):
+            assert _rel(a, b) < 1e-4
+    ir.clear_cache()
+
+
+def test_sharded_nonfinite_raises():
+    D, linf = _problem(120, 100, 3)
+    D[-1, 5] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        _sharded(torch.from_numpy(D).cuda(), _cfg(3, linf), 2)
+    ir.clear_cache()

@@ -1,0 +1,82 @@
+"""Host-side logic of the drop-in (no GPU): index draws, config validation,
+threshold schedule, colmajor rule, generator restatements."""
+
+import numpy as np
+import pytest
+
+from oracle import ircur_oracle as orc
+import paper_2010_07422_b200 as ir
+from paper_2010_07422_b200 import sampling
+from paper_2010_07422_b200.solver import _want_colmajor
+
+
+def test_sorted_unique_equals_np_unique():
+    rng = np.random.default_rng(0)
+    for n, m in ((10, 50), (1000, 139), (100000, 461), (1, 3)):
+        x = rng.integers(0, n, size=m)
+        np.testing.assert_array_equal(sampling.sorted_unique(x), np.unique(x))
+    np.testing.assert_array_equal(sampling.sorted_unique(np.array([], dtype=np.int64)), np.array([], dtype=np.int64))
+
+
+@pytest.mark.parametrize("mode", ["fixed", "resampled"])
+@pytest.mark.parametrize("shape", [(1000, 1000), (90, 60), (25344, 1000), (1, 1)])
+def test_draw_order_equals_oracle_index_stream(mode, shape):
+    n1, n2 = shape
+    r, seed, max_iter = 3, 7, 6
+    m1 = ir.sample_count(n1, r, 4.0)
+    m2 = ir.sample_count(n2, r, 4.0)
+    sets = ir.draw_index_sets(n1, n2, m1, m2, ir.RngSeed(seed), max_iter if mode == "resampled" else 1)
+    ref = orc.index_stream(n1, n2, r, 4.0, 4.0, mode, max_iter, seed)
+    for k in range(max_iter):
+        I, J = sets[k if mode == "resampled" else 0]
+        np.testing.assert_array_equal(I, ref[k][0])
+        np.testing.assert_array_equal(J, ref[k][1])
+
+
+def test_sample_count_matches_oracle():
+    for n in (1, 2, 10, 1000, 10000, 25344, 100000):
+        for r in (1, 2, 5, 10):
+            for c in (0.5, 4.0):
+                assert ir.sample_count(n, r, c) == orc.sample_count(n, r, c)
+
+
+def test_solver_config_validation_messages():
+    with pytest.raises(ValueError, match="rank"):
+        ir.SolverConfig(rank=0)
+    with pytest.raises(ValueError, match="eps"):
+        ir.SolverConfig(rank=1, eps=0.0)
+    with pytest.raises(ValueError, match="zeta0"):
+        ir.SolverConfig(rank=1, zeta0=-1.0)
+    with pytest.raises(ValueError, match="gamma"):
+        ir.SolverConfig(rank=1, gamma=1.0)
+    with pytest.raises(ValueError, match="mode"):
+        ir.SolverConfig(rank=1, mode="other")
+    with pytest.raises(ValueError, match="max_iter"):
+        ir.SolverConfig(rank=1, max_iter=0)
+
+
+def test_threshold_schedule_bits():
+    cfg = ir.SolverConfig(rank=2, zeta0=3.7, gamma=0.7)
+    for k in range(30):
+        assert ir.threshold_at(cfg, k) == 0.7**k * 3.7  # the reference's expression, same bits
+    with pytest.raises(ValueError):
+        ir.threshold_at(cfg, -1)
+    with pytest.raises(ValueError):
+        ir.threshold_at(ir.SolverConfig(rank=2), 0)
+
+
+def test_colmajor_rule(monkeypatch):
+    monkeypatch.delenv("IRCUR_COLMAJOR", raising=False)
+    assert _want_colmajor("auto", 100000, 100000, 461, 4, "resampled")
+    assert _want_colmajor("auto", 10000, 10000, 185, 4, "resampled")
+    assert not _want_colmajor("auto", 1000, 10**6, 10, 4, "resampled")
+    assert _want_colmajor(True, 10, 10**6, 1, 4, "fixed") and not _want_colmajor(False, 10, 10, 5, 4, "fixed")
+    monkeypatch.setenv("IRCUR_COLMAJOR", "0")
+    assert not _want_colmajor(True, 10, 10, 5, 4, "fixed")
+
+
+def test_blocked_generator_equals_reference_generator():
+    D, L, S, linf = orc.baseline_problem(300, 170, 4, 0.2, 5)
+    Db, linf_b, a = orc.baseline_problem_blocked(300, 170, 4, 0.2, 5, block_rows=64)
+    np.testing.assert_array_equal(Db, D)
+    assert linf_b == linf
