@@ -43,6 +43,8 @@ SOLVER_SEED = 1
 GAMMA = 0.7
 EPS = 1e-5
 MAX_ITER = 100
+COLMAJOR = {"auto": "auto", "0": False, "none": False, "1": "full", "full": "full", "2": "sampled",
+            "sampled": "sampled"}
 METRIC = "IRCUR time-to-tol=1e-5 (n=1e4..1e5) & strip-kernel HBM GB/s vs B200 peak"
 
 
@@ -63,7 +65,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
     ap.add_argument("--mode", default="resampled", choices=["fixed", "resampled"])
-    ap.add_argument("--colmajor", default="auto")
+    ap.add_argument("--colmajor", default="auto", choices=sorted(COLMAJOR))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
@@ -160,7 +162,7 @@ def run_ours(args):
     D, linf, a = gen.baseline_problem_device(n1, n2, r, alpha, DATA_SEED, dtype=tdt)
     cfg = ir.SolverConfig(rank=r, eps=EPS, zeta0=linf, gamma=GAMMA, mode=args.mode,
                           max_iter=MAX_ITER, seed=ir.RngSeed(SOLVER_SEED))
-    cm = args.colmajor if args.colmajor == "auto" else args.colmajor in ("1", "true", "True")
+    cm = COLMAJOR[args.colmajor]
     stream = torch.cuda.current_stream()
     prof = not args.no_profile
     for _ in range(args.warmup):
@@ -214,7 +216,7 @@ def run_ours(args):
         "config": {"workload": args.config, "n1": n1, "n2": n2, "rank": r, "alpha": alpha,
                    "mode": args.mode, "gamma": GAMMA, "eps": EPS, "zeta0": "max|L|",
                    "iterations": iters, "converged": res.trace.converged,
-                   "final_e": res.trace.errors[-1], "colmajor_copy": bool(res.colmajor),
+                   "final_e": res.trace.errors[-1], "colmajor_copy": ["none", "full", "sampled"][int(res.colmajor)],
                    "l2": "inputs larger than L2 (D >= 400 MB), no flush",
                    "parallelism": "single GPU"},
         "step_ms": step_ms,
@@ -286,7 +288,7 @@ def run_sharded(args, rank, world, local):
                                              stats_reduce=stats_reduce)
     cfg = ir.SolverConfig(rank=r, eps=EPS, zeta0=linf, gamma=GAMMA, mode=args.mode,
                           max_iter=MAX_ITER, seed=ir.RngSeed(SOLVER_SEED))
-    cm = args.colmajor if args.colmajor == "auto" else args.colmajor in ("1", "true", "True")
+    cm = COLMAJOR[args.colmajor]
 
     def one(Din):
         return irdist.run_collective(irdist.solve_shard_program(Din, cfg, n1=n1, row0=r0, colmajor=cm))

@@ -69,6 +69,14 @@ int ircur_ctx_destroy(ircur_ctx_t ctx);
 int ircur_prepare(ircur_ctx_t ctx, const void* D, int64_t ldd, int make_colmajor,
                   int* all_finite, double* max_abs);
 
+/* Like ircur_prepare, but the column-major copy holds only the columns of
+ * the J sets [0, cover_sets) (their union; ~20% of D for 40 iterations at
+ * n = 1e5), so the pass writes a fraction of D instead of all of it.  Needs
+ * the index sets uploaded first.  Iterations past the covered sets extend
+ * the copy automatically (one more pass over D).  Host-blocking. */
+int ircur_prepare_sampled(ircur_ctx_t ctx, const void* D, int64_t ldd, int cover_sets,
+                          int* all_finite, double* max_abs);
+
 /* Upload the pre-generated index sets (host int64, strictly increasing),
  * n_sets consecutive (I_k, J_k) pairs packed with strides max_rows/max_cols.
  * The host draws them with the reference's numpy call sequence

@@ -50,6 +50,14 @@ struct ircur_ctx {
   // owned
   void* Dt = nullptr;
   int64_t ldt = 0;
+  // column-major copy: 0 none, 1 full (line j = column j), 2 sampled (line
+  // colsel[j] for the union of the J sets [0, covered))
+  int dt_mode = 0;
+  int64_t dt_cap = 0;        // lines allocated in Dt
+  int covered = 0;           // sets whose columns are in Dt (mode 2)
+  int* d_colsel = nullptr;   // n2: column -> line of Dt or -1 (mode 2)
+  int* d_cols_c = nullptr;   // per set: Dt line of each J entry (mode 2)
+  std::vector<int> h_cols;   // host copy of the J sets (n_sets x max_cols)
   int* d_rows = nullptr;
   int* d_cols = nullptr;
   int n_sets = 0;
@@ -121,6 +129,7 @@ int svd_cluster_size(int n, int m, int kk) { return svd_pick_cluster(n, m, kk); 
 struct IterSets {
   const int* I;  // local sampled rows (global ids), |I_loc| = mI
   const int* J;
+  const int* Jline;  // line of each J entry in the column-major copy
   int mI_all, i_lo, mI, nJ;
 };
 
@@ -128,6 +137,7 @@ IterSets iter_sets(const ircur_ctx* c, int set) {
   IterSets q;
   q.I = c->d_rows + (size_t)set * c->max_rows + c->h_row_lo[set];
   q.J = c->d_cols + (size_t)set * c->max_cols;
+  q.Jline = c->dt_mode == 2 ? c->d_cols_c + (size_t)set * c->max_cols : q.J;
   q.mI_all = c->h_row_cnt[set];
   q.i_lo = c->h_row_lo[set];
   q.mI = c->h_row_loc_cnt[set];
@@ -165,6 +175,8 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   // moves e_k by ~delta/e_k relative)
   sa.tol = sizeof(T) == 8 ? 2e-14 : 1e-11;
   sa.tol_scale = sizeof(T) == 8 ? 1e-11 : 1e-8;
+  if (const char* ev = std::getenv(sizeof(T) == 8 ? "IRCUR_SVD_TOL64" : "IRCUR_SVD_TOL32"))  // tuning
+    sa.tol = std::atof(ev);
   sa.prev_err = k > 0 ? c->errors + (k - 1) : nullptr;
   sa.dbg = c->profiling ? c->svd_dbg : nullptr;
   sa.maxsteps = 100;
@@ -197,7 +209,7 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
   } else {
     cs.src = (const T*)c->D; cs.line_stride = 1; cs.pos_stride = c->ldd; cs.bulk_ok = 0;
   }
-  cs.lines = q.J; cs.line_off = 0; cs.nk = q.nJ; cs.npos = (int)c->nloc;
+  cs.lines = c->Dt ? q.Jline : q.J; cs.line_off = 0; cs.nk = q.nJ; cs.npos = (int)c->nloc;
   cs.lineA = (const T*)c->QoldJ; cs.lineW = (const T*)c->VS; cs.lineRes = (const T*)c->QJ;
   cs.Bold = (const T*)c->Pt[old]; cs.ldb = c->ldp; cs.Fnew = (T*)c->Pt[nw]; cs.ldf = c->ldp;
   cs.omap = c->rowmap; cs.otherF = (const T*)c->PI;
@@ -218,6 +230,56 @@ FinalizeArgs finalize_args(ircur_ctx* c, int k, const IterSets& q, double eps, i
   fa.host_done = host_flags ? c->h_flags_dev : nullptr;
   fa.host_iters = host_flags ? c->h_flags_dev + 1 : nullptr;
   return fa;
+}
+
+// Sampled column-major copy covering the J sets [0, cover): column map,
+// per-set line indices, capacity, then one prep_select pass over D.
+int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfinite) {
+  cover = std::max(1, std::min(cover, c->n_sets));
+  std::vector<int> sel((size_t)c->n2, -1);
+  for (int s = 0; s < cover; ++s)
+    for (int j = 0; j < c->h_col_cnt[s]; ++j) sel[c->h_cols[(size_t)s * c->max_cols + j]] = 0;
+  int64_t nl = 0;
+  for (int64_t j = 0; j < c->n2; ++j)
+    if (sel[j] >= 0) sel[j] = (int)nl++;
+  std::vector<int> lines((size_t)c->n_sets * c->max_cols, -1);
+  for (int s = 0; s < c->n_sets; ++s)
+    for (int j = 0; j < c->h_col_cnt[s]; ++j) lines[(size_t)s * c->max_cols + j] = sel[c->h_cols[(size_t)s * c->max_cols + j]];
+  cudaStream_t st = c->stream;
+  if (nl > c->dt_cap) {
+    IR_CUDA(cudaStreamSynchronize(st));  // in-flight iterations may still read the old copy
+    if (c->Dt) cudaFree(c->Dt);
+    c->Dt = nullptr;
+    c->dt_cap = 0;
+    c->ldt = pad4(c->nloc);
+    const int64_t cap = std::min<int64_t>(c->n2, nl + nl / 4 + 64);
+    IR_CUDA(cudaMalloc(&c->Dt, (size_t)cap * c->ldt * c->esz));
+    c->dt_cap = cap;
+  }
+  if (!c->d_colsel) IR_CUDA(cudaMalloc(&c->d_colsel, (size_t)c->n2 * sizeof(int)));
+  if (c->d_cols_c) cudaFree(c->d_cols_c);
+  c->d_cols_c = nullptr;
+  IR_CUDA(cudaMalloc(&c->d_cols_c, lines.size() * sizeof(int)));
+  IR_CUDA(cudaMemcpyAsync(c->d_colsel, sel.data(), sel.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  IR_CUDA(cudaMemcpyAsync(c->d_cols_c, lines.data(), lines.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  if (c->dtype == IRCUR_F32)
+    IR_CUDA(launch_prep_select<float>((const float*)c->D, c->ldd, c->nloc, c->n2, c->d_colsel, (float*)c->Dt,
+                                      c->ldt, maxbits, nonfinite, c->num_sms, st));
+  else
+    IR_CUDA(launch_prep_select<double>((const double*)c->D, c->ldd, c->nloc, c->n2, c->d_colsel,
+                                       (double*)c->Dt, c->ldt, maxbits, nonfinite, c->num_sms, st));
+  IR_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+  c->dt_mode = 2;
+  c->covered = cover;
+  return IRCUR_OK;
+}
+
+// Before iteration on `set`: extend the sampled copy when the loop has run
+// past the sets it covers (the finite/max results of the re-read are unused).
+int ensure_cover(ircur_ctx* c, int set) {
+  if (c->dt_mode != 2 || set < c->covered) return IRCUR_OK;
+  const int grow = std::max(8, c->covered / 2);
+  return build_cover(c, set + grow, c->maxbits, c->flags + 4);
 }
 
 // One single-device iteration: core -> gram+svd -> fused strips -> finalize.
@@ -401,7 +463,7 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U,
                   c->PoldI, c->QoldJ, c->Wr, c->PI, c->VS, c->QJ, c->W, c->sigma, c->V, c->inv,
                   c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps,
-                  c->rowmap, c->colmap, c->svd_dbg, c->Qpart, c->scal};
+                  c->rowmap, c->colmap, c->svd_dbg, c->Qpart, c->scal, c->d_colsel, c->d_cols_c};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -421,14 +483,21 @@ int ircur_prepare(ircur_ctx_t c, const void* D, int64_t ldd, int make_colmajor, 
   c->D = D;
   c->ldd = ldd;
   c->has_state = false;
-  if (make_colmajor && !c->Dt) {
+  if (make_colmajor && (!c->Dt || c->dt_cap < c->n2)) {
+    if (c->Dt) cudaFree(c->Dt);
     c->ldt = pad4(c->nloc);
+    c->Dt = nullptr;
+    c->dt_cap = 0;
     IR_CUDA(cudaMalloc(&c->Dt, (size_t)c->n2 * c->ldt * c->esz));
+    c->dt_cap = c->n2;
   }
   if (!make_colmajor && c->Dt) {
     cudaFree(c->Dt);
     c->Dt = nullptr;
+    c->dt_cap = 0;
   }
+  c->dt_mode = make_colmajor ? 1 : 0;
+  c->covered = 0;
   IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), c->stream));
   IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), c->stream));
   if (c->dtype == IRCUR_F32)
@@ -442,6 +511,32 @@ int ircur_prepare(ircur_ctx_t c, const void* D, int64_t ldd, int make_colmajor, 
   IR_CUDA(cudaMemcpyAsync(&mb, c->maxbits, sizeof(mb), cudaMemcpyDeviceToHost, c->stream));
   IR_CUDA(cudaMemcpyAsync(&nf, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));
+  double mx;
+  std::memcpy(&mx, &mb, sizeof(mx));
+  if (all_finite) *all_finite = nf ? 0 : 1;
+  if (max_abs) *max_abs = mx;
+  if (nf) return fail(IRCUR_ENONFINITE, "matrix contains non-finite entries");
+  return IRCUR_OK;
+}
+
+int ircur_prepare_sampled(ircur_ctx_t c, const void* D, int64_t ldd, int cover_sets, int* all_finite,
+                          double* max_abs) {
+  if (!c || !D) return fail(IRCUR_EINVAL, "null context or D");
+  if (ldd < c->n2) return fail(IRCUR_EINVAL, "ldd < n2");
+  if (c->n_sets < 1) return fail(IRCUR_EINVAL, "upload the index sets before ircur_prepare_sampled");
+  if (cover_sets < 1) return fail(IRCUR_EINVAL, "cover_sets must be >= 1");
+  IR_CUDA(cudaSetDevice(c->device));
+  c->D = D;
+  c->ldd = ldd;
+  c->has_state = false;
+  c->dt_mode = 0;  // (an allocation from an earlier solve is reused when large enough)
+  IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), c->stream));
+  IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), c->stream));
+  if (int rc = build_cover(c, cover_sets, c->maxbits, c->flags + 3)) return rc;
+  unsigned long long mb = 0;
+  int nf = 0;
+  IR_CUDA(cudaMemcpy(&mb, c->maxbits, sizeof(mb), cudaMemcpyDeviceToHost));
+  IR_CUDA(cudaMemcpy(&nf, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost));
   double mx;
   std::memcpy(&mx, &mb, sizeof(mx));
   if (all_finite) *all_finite = nf ? 0 : 1;
@@ -495,6 +590,11 @@ int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int3
     IR_CUDA(cudaMalloc(&c->d_cols, hc.size() * sizeof(int)));
   }
   c->n_sets = n_sets;
+  c->h_cols = hc;
+  if (c->dt_mode == 2) {  // the sampled copy belongs to the previous sets
+    c->dt_mode = 0;
+    c->covered = 0;
+  }
   IR_CUDA(cudaMemcpyAsync(c->d_rows, hr.data(), hr.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
   IR_CUDA(cudaMemcpyAsync(c->d_cols, hc.data(), hc.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
@@ -598,6 +698,7 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
     const bool fin = hf[0] != 0;
     while (!fin && launched < max_iter && launched < seen + kAhead) {
       const int set = mode == IRCUR_FIXED ? 0 : launched;
+      if (int rc = ensure_cover(c, set)) return rc;
       int rc = iteration(c, launched, set, zetas[launched], eps, max_iter, true);
       if (rc) return rc;
       IR_CUDA(cudaEventRecord(c->ev[launched + 1], st));
@@ -638,6 +739,8 @@ int ircur_shard_phase(ircur_ctx_t c, int phase, int k, int set, double zeta, dou
   if (k < 0 || k >= c->max_iter || set < 0 || set >= c->n_sets || max_iter < 1 || max_iter > c->max_iter)
     return fail(IRCUR_EINVAL, "bad k/set/max_iter");
   IR_CUDA(cudaSetDevice(c->device));
+  if (phase == IRCUR_SHARD_CORE)
+    if (int rc = ensure_cover(c, set)) return rc;
   int rc = c->dtype == IRCUR_F32 ? launch_shard_phase<float>(c, phase, k, set, zeta, eps, max_iter)
                                  : launch_shard_phase<double>(c, phase, k, set, zeta, eps, max_iter);
   if (rc == IRCUR_OK && phase == IRCUR_SHARD_STOP) IR_CUDA(cudaEventRecord(c->ev[k + 1], c->stream));
@@ -673,6 +776,7 @@ int ircur_iterate(ircur_ctx_t c, int k, int set, double zeta, double* e) {
     IR_CUDA(cudaMemsetAsync(c->Qt[0], 0, (size_t)c->r * c->ldq * c->esz, st));
   }
   IR_CUDA(cudaMemsetAsync(c->flags, 0, 3 * sizeof(int), st));
+  if (int rc = ensure_cover(c, set)) return rc;
   int rc = iteration(c, k, set, zeta, 0.0, c->max_iter + 1, false);
   if (rc) return rc;
   double ek = 0.0;

@@ -52,6 +52,10 @@ template <typename T>
 cudaError_t launch_prep(const T* D, int64_t ldd, int64_t nloc, int64_t n2, T* Dt, int64_t ldt,
                         unsigned long long* maxbits, int* nonfinite, int num_sms, cudaStream_t st);
 template <typename T>
+cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2, const int* colsel, T* Dt,
+                               int64_t ldt, unsigned long long* maxbits, int* nonfinite, int num_sms,
+                               cudaStream_t st);
+template <typename T>
 cudaError_t launch_slab_sq(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2,
                            const int* I, int mI, const int* J, int nJ, int nb_rows, int nb_cols,
                            double* partials, cudaStream_t st);

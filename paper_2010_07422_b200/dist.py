@@ -107,13 +107,14 @@ def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, co
     sets = draw_index_sets(n1, n2, m_rows, m_cols, cfg.seed, cfg.max_iter if resampled else 1)
     make = engine_factory or _gpu_engine
     eng, Dd = make(D_local, n1, row0, cfg, m_rows, m_cols, device=device, compute_dtype=compute_dtype)
-    from .solver import _want_colmajor
+    from .solver import _copy_plan
 
-    cm = _want_colmajor(colmajor, n1, n2, m_cols, getattr(Dd, "element_size", lambda: 8)(), cfg.mode)
+    cm, cover = _copy_plan(colmajor, n2, m_cols, sets, cfg)
+    eng.set_indices(sets)
     # matcore.require_finite / inf_norm over all shards: every rank raises together
     bad, max_abs = 0.0, 0.0
     try:
-        max_abs = eng.prepare(Dd, cm)
+        max_abs = eng.prepare(Dd, cm, cover)
     except ValueError as e:
         if "non-finite" not in str(e):
             raise
@@ -123,7 +124,6 @@ def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, co
     if float(flag[0]) != 0.0:
         raise ValueError("matrix contains non-finite entries")
     max_abs = float(flag[1])
-    eng.set_indices(sets)
     a, b = eng.slab_sqnorms(0)
     den = eng.host_tensor([a, b])
     yield ("sum", den)

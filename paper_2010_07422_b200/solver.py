@@ -81,13 +81,21 @@ class Context:
         except Exception:
             pass
 
-    def prepare(self, D: torch.Tensor, colmajor: bool) -> float:
+    def prepare(self, D: torch.Tensor, colmajor, cover: int = 0) -> float:
+        """Finite check + max|D| (+ column-major copy): colmajor 0/False none,
+        1/True full copy, 2 only the columns of the J sets [0, cover)
+        (index sets must be uploaded first)."""
         self._D = D
-        self.colmajor = bool(colmajor)
+        mode = int(colmajor)
+        self.colmajor = mode
         ok = C.c_int(0)
         mx = C.c_double(0.0)
-        _capi.check(self.lib.ircur_prepare(self.h, C.c_void_p(_ptr(D)), D.stride(0), int(colmajor),
-                                           C.byref(ok), C.byref(mx)))
+        if mode == 2:
+            _capi.check(self.lib.ircur_prepare_sampled(self.h, C.c_void_p(_ptr(D)), D.stride(0), int(cover),
+                                                       C.byref(ok), C.byref(mx)))
+        else:
+            _capi.check(self.lib.ircur_prepare(self.h, C.c_void_p(_ptr(D)), D.stride(0), mode,
+                                               C.byref(ok), C.byref(mx)))
         return float(mx.value)
 
     def set_indices(self, sets) -> None:
@@ -327,6 +335,36 @@ class _Ticker:
             self.t = t
 
 
+def _copy_plan(colmajor, n2: int, m_cols: int, sets, cfg: SolverConfig) -> tuple[int, int]:
+    """Which column-major copy the prep pass builds: (mode, cover) with mode
+    0 = none, 1 = full copy of D, 2 = only the columns of the J sets
+    [0, cover) (extended automatically if the loop runs longer).  cover is
+    the iteration count the threshold schedule needs to reach eps
+    (log eps / log gamma) plus slack."""
+    env = os.environ.get("IRCUR_COLMAJOR")
+    if env is not None:
+        colmajor = {"0": False, "1": "full", "2": "sampled"}.get(env, env)
+    if colmajor in (False, 0, "0", "false", "False", "none", ""):
+        return 0, 0
+    if colmajor == "auto" and not _want_colmajor("auto", 0, n2, m_cols, 0, cfg.mode):
+        return 0, 0
+    if colmajor in ("full", 1) and colmajor is not True:
+        return 1, 0
+    if cfg.mode == "fixed":
+        cover = 1
+    else:
+        est = int(np.ceil(np.log(cfg.eps) / np.log(cfg.gamma))) + 8
+        cover = max(1, min(len(sets), est))
+    if isinstance(colmajor, str) and colmajor.startswith("sampled"):
+        if ":" in colmajor:  # "sampled:K" covers the first K sets (tests of the extension path)
+            cover = max(1, min(len(sets), int(colmajor.split(":")[1])))
+        return 2, cover
+    mark = np.zeros(n2, dtype=bool)
+    for k in range(cover):
+        mark[sets[k][1]] = True
+    return (1, 0) if mark.sum() > 0.7 * n2 else (2, cover)
+
+
 @dataclass
 class DeviceHandle:
     """Final rank-r factors on the device: L = P Q with P^T (r x n1) and Q (r x n2)."""
@@ -376,11 +414,11 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     tick("draw")
     stream = torch.cuda.current_stream(dev).cuda_stream
     ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
-    cm = _want_colmajor(colmajor, n1, n2, m_cols, Dd.element_size(), cfg.mode)
-    max_abs = ctx.prepare(Dd, cm)  # ValueError on NaN/Inf (matcore.py:75-76)
-    tick("prepare")
     ctx.set_indices(sets)
     tick("set_indices")
+    cm, cover = _copy_plan(colmajor, n2, m_cols, sets, cfg)
+    max_abs = ctx.prepare(Dd, cm, cover)  # ValueError on NaN/Inf (matcore.py:75-76)
+    tick("prepare")
     rows0, cols0 = sets[0]
     a, b = ctx.slab_sqnorms(0)
     tick("slab")

@@ -37,7 +37,7 @@ class NumpyShardEngine:
         self.sets = []
 
     # ---- setup
-    def prepare(self, D, colmajor):
+    def prepare(self, D, colmajor, cover=0):
         if not np.isfinite(self.D).all():
             raise ValueError("matrix contains non-finite entries")
         return float(np.abs(self.D).max())

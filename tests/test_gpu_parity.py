@@ -113,14 +113,21 @@ def test_nonfinite_rejected(ir):
         ir.solve(D.astype(np.float32), ir.SolverConfig(rank=2), device=0)
 
 
-def test_colmajor_copy_and_strided_paths_agree(ir):
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+def test_colmajor_copy_and_strided_paths_agree(ir, dtype, mode):
+    """Full copy, sampled copy (incl. on-demand extension past the covered
+    sets) and the strided gather from row-major D give identical bits."""
     from oracle.ircur_oracle import baseline_problem
-    D = baseline_problem(150, 130, 3, 0.1, 8)[0]
-    cfg = ir.SolverConfig(rank=3, gamma=0.7, mode="resampled", seed=ir.RngSeed(9))
-    a = ir.solve(D, cfg, device=0, colmajor=True)
-    b = ir.solve(D, cfg, device=0, colmajor=False)
-    assert a[2].errors == b[2].errors
-    np.testing.assert_array_equal(a[0].C, b[0].C)
+    D = baseline_problem(150, 130, 3, 0.1, 8)[0].astype(dtype)
+    cfg = ir.SolverConfig(rank=3, gamma=0.7, eps=1e-9, mode=mode, seed=ir.RngSeed(9))
+    ref = ir.solve(D, cfg, device=0, colmajor="full")
+    assert ref[2].iterations > 6
+    for cm in (False, "sampled", "sampled:1", "sampled:3"):
+        b = ir.solve(D, cfg, device=0, colmajor=cm)
+        assert b[2].errors == ref[2].errors, cm
+        for x, y in ((b[0].C, ref[0].C), (b[0].R, ref[0].R), (b[1].col_values, ref[1].col_values)):
+            np.testing.assert_array_equal(x, y)
 
 
 def test_materialize_matches_oracle(ir):

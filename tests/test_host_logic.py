@@ -7,7 +7,7 @@ import pytest
 from oracle import ircur_oracle as orc
 import paper_2010_07422_b200 as ir
 from paper_2010_07422_b200 import sampling
-from paper_2010_07422_b200.solver import _want_colmajor
+from paper_2010_07422_b200.solver import _copy_plan, _want_colmajor
 
 
 def test_sorted_unique_equals_np_unique():
@@ -80,3 +80,23 @@ def test_blocked_generator_equals_reference_generator():
     Db, linf_b, a = orc.baseline_problem_blocked(300, 170, 4, 0.2, 5, block_rows=64)
     np.testing.assert_array_equal(Db, D)
     assert linf_b == linf
+
+
+def test_copy_plan(monkeypatch):
+    monkeypatch.delenv("IRCUR_COLMAJOR", raising=False)
+    cfg = ir.SolverConfig(rank=10, eps=1e-5, gamma=0.7, mode="resampled", max_iter=100)
+    n = 100000
+    m = ir.sample_count(n, 10, 4.0)
+    sets = ir.draw_index_sets(n, n, m, m, ir.RngSeed(1), 100)
+    mode, cover = _copy_plan("auto", n, m, sets, cfg)
+    assert mode == 2 and cover == int(np.ceil(np.log(1e-5) / np.log(0.7))) + 8
+    assert _copy_plan("full", n, m, sets, cfg) == (1, 0)
+    assert _copy_plan(False, n, m, sets, cfg) == (0, 0)
+    assert _copy_plan("sampled:3", n, m, sets, cfg) == (2, 3)
+    fixed = ir.SolverConfig(rank=10, mode="fixed")
+    assert _copy_plan(True, n, m, sets[:1], fixed) == (2, 1)
+    # small n: the union of the sets covers most columns -> full copy
+    sets2 = ir.draw_index_sets(200, 200, 60, 60, ir.RngSeed(1), 100)
+    assert _copy_plan(True, 200, 60, sets2, cfg) == (1, 0)
+    monkeypatch.setenv("IRCUR_COLMAJOR", "0")
+    assert _copy_plan(True, n, m, sets, cfg) == (0, 0)
