@@ -165,7 +165,17 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   SvdArgs sa{};
   sa.U = c->U; sa.ldu = c->max_cols; sa.G = c->G; sa.ldg = c->max_cols;
   sa.m = q.mI_all; sa.n = q.nJ; sa.r = R;  // the full core (all-reduced when row-sharded)
-  sa.kk = std::min(std::min(2 * R, 32), std::min(q.mI_all, q.nJ));
+  // block = r + 2 columns: the top-r Ritz pairs converge at rate
+  // lambda_{r+3}/lambda_r per step; the small dense Rayleigh-Ritz (latency
+  // bound, ~kk^2 per Jacobi round) dominates the step cost, so a larger
+  // block costs more than the steps it saves (measured: kk = 2r is 1.9x
+  // slower at r = 10 for the same step count).  IRCUR_SVD_EXTRA overrides.
+  static const int kk_extra = [] {
+    const char* e = std::getenv("IRCUR_SVD_EXTRA");
+    return e ? std::max(0, std::atoi(e)) : 2;
+  }();
+  const int kk_want = R + kk_extra;
+  sa.kk = std::min(std::min(kk_want, 32), std::min(q.mI_all, q.nJ));
   sa.warm = k > 0 ? c->QoldJ : nullptr; sa.warm_ld = R; sa.warm_cols = k > 0 ? R : 0;
   sa.W = c->W; sa.sigma = c->sigma; sa.V = c->V; sa.inv = c->inv;
   sa.Wr = c->Wr; sa.PI = c->PI; sa.VS = c->VS; sa.QJ = c->QJ;
@@ -180,6 +190,11 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   sa.prev_err = k > 0 ? c->errors + (k - 1) : nullptr;
   sa.dbg = c->profiling ? c->svd_dbg : nullptr;
   sa.maxsteps = 100;
+  static const int sweeps = [] {
+    const char* e = std::getenv("IRCUR_SVD_SWEEPS");
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  sa.sweeps = sweeps;
   sa.salt = 0x1234567ull + (uint64_t)k * 7919ull;
   return sa;
 }
@@ -430,7 +445,7 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->V, (size_t)max_cols * rank * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->inv, (size_t)rank * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->G, (size_t)max_cols * max_cols * sizeof(double)));
-  IR_CUDA_C(cudaMalloc(&c->svd_scratch, 2 * (size_t)max_cols * 32 * sizeof(double)));
+  IR_CUDA_C(cudaMalloc(&c->svd_scratch, 3 * (size_t)max_cols * 32 * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->Qpart, (size_t)rank * c->ldq * c->esz));
   IR_CUDA_C(cudaMalloc(&c->scal, 8 * sizeof(double)));
   IR_CUDA_C(cudaMemsetAsync(c->scal, 0, 8 * sizeof(double), c->stream));

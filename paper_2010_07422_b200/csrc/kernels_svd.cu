@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U,
 // Shared-memory layout in doubles; identical on host (size) and device.
 struct SvdLayout {
   int n, m, kk, KP, HL, per, mper, rowsmax, ldgq, S, gq_smem, RL;
-  int oVq, oGq, oP, oBq, oXq, oH, oH2, oZ, oLc, oT, oRed, oRout, oRes, oLam, oCs, oW, oPt, total;
+  int oVq, oGq, oP, oBq, oXq, oH, oH2, oZ, oLc, oT, oRed, oRout, oRes, oResq, oLam, oCs, oW, oPt, total;
 };
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -107,6 +107,7 @@ __host__ __device__ inline SvdLayout svd_layout(int n, int m, int kk, int cs) {
   L.oRed = off; off += 2 * L.RL;
   L.oRout = off; off += L.RL;
   L.oRes = off; off += kk;
+  L.oResq = off; off += 2 * kKMax;
   L.oLam = off; off += kk;
   L.oCs = off; off += 4 * kKMax;
   L.oW = off; off += 2 * kKMax + 8;
@@ -128,7 +129,7 @@ __device__ __forceinline__ double hash_uniform(uint64_t a, uint64_t b) {
 
 struct Sm {
   SvdLayout L;
-  double *Vq, *Gq, *P, *Bq, *Xq, *H, *H2, *Z, *Lc, *T, *red, *rout, *res, *lam, *cs, *ws;
+  double *Vq, *Gq, *P, *Bq, *Xq, *H, *H2, *Z, *Lc, *T, *red, *rout, *res, *resq, *lam, *cs, *ws;
   int* flags;
   int* ptab;
 };
@@ -143,8 +144,13 @@ __device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, Sm& S, int bu
   cl.sync();
   const int CS = (int)cl.num_blocks();
   for (int e = threadIdx.x; e < len; e += kSvdNT) {
-    double s = *cl.map_shared_rank(src + e, 0);
-    for (int q = 1; q < CS; ++q) s += *cl.map_shared_rank(src + e, q);
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = q < CS ? *cl.map_shared_rank(src + e, q) : 0.0;
+    double s = v[0];
+#pragma unroll
+    for (int q = 1; q < 16; ++q)
+      if (q < CS) s += v[q];
     S.rout[e] = s;
   }
   __syncthreads();
@@ -203,15 +209,34 @@ __device__ void tiled_product(const double* A, int lda, int nr, int n, const dou
 }
 
 // Cyclic Jacobi eigen-decomposition of the symmetric kk x kk S.H on the first
-// kEigNT threads (round-robin parallel ordering from a partner table; J^T H J
-// for all disjoint pairs of a round in one pass; named barrier).  On exit
-// S.lam holds the eigenvalues in decreasing order and S.Z the matching
-// eigenvectors.  `thr_rel` is the stopping threshold relative to the largest
-// diagonal entry, `max_sweeps` caps the work (an inexact Z only costs the
-// subspace iteration an extra step; the final extraction runs to
+// kEigNT threads.  Parallel (round-robin, circle method) ordering: in every
+// round one thread per disjoint pair (p, q) computes the rotation and
+// publishes (c, s) and the partner of p and q; then every thread applies
+// J^T H J and Z J to its fixed set of <= 8 matrix entries (kept in
+// registers as indices).  Two named barriers per round; the off-diagonal
+// maximum that decides the next sweep is reduced inside the last round.
+// On exit S.lam holds the eigenvalues in decreasing order and S.Z the
+// matching eigenvectors.  `thr_rel` is the stopping threshold relative to the
+// largest diagonal entry, `max_sweeps` caps the work (an inexact Z only costs
+// the subspace iteration an extra step; the final extraction runs to
 // convergence).  Caller: the first kEigNT threads.
+constexpr int kEigCPT = 8;  // columns per thread (kk <= 32, 128 threads: >= 4 row groups)
+
+__device__ __forceinline__ int circle_player(int pos, int rd, int nrd) {
+  if (pos == 0) return 0;
+  int x = pos - 1 + rd;
+  x -= (x >= nrd) ? nrd : 0;
+  return x + 1;
+}
+
+__device__ __forceinline__ double approx_sqrtf_d(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long long* dbg = nullptr) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
   const int HL = S.L.HL;
   double* H = S.H;
   double* Hn = S.H2;
@@ -219,89 +244,107 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long l
   double* Zn = S.T;  // free while the eigenproblem is solved
   const int nply = kk + (kk & 1);
   const int nrd = nply - 1;
-  int* ptab = S.ptab;  // ptab[rd * nply + x] = partner of x in round rd (circle method)
-  for (int e = tid; e < nrd * nply; e += kEigNT) {
-    const int rd = e / nply, pos = e - rd * nply;
-    const int x = pos == 0 ? 0 : ((pos - 1 + rd) % nrd) + 1;
-    const int pp = nply - 1 - pos;
-    const int y = pp == 0 ? 0 : ((pp - 1 + rd) % nrd) + 1;
-    ptab[rd * nply + x] = y;
-  }
-  unsigned short* etab = reinterpret_cast<unsigned short*>(ptab + kKMax * kKMax);  // (a << 8 | b)
-  for (int e = tid; e < kk * kk; e += kEigNT) {
-    const int a = e / kk, b = e - a * kk;
-    etab[e] = (unsigned short)((a << 8) | b);
-    Z[a * HL + b] = (a == b) ? 1.0 : 0.0;
-  }
+  int* prt = S.ptab;  // partner of each index in the current round (itself when idle)
+  // entry mapping: thread -> row a, columns b = g, g + ng, g + 2 ng, ...
+  const int ng = kEigNT / kk;  // row groups (>= 4)
+  const int a = tid % kk, g = tid / kk;
+  const bool act = g < ng;
+  const int ncol = act ? (kk - g + ng - 1) / ng : 0;  // <= kEigCPT
+#pragma unroll
+  for (int v = 0; v < kEigCPT; ++v)
+    if (v < ncol) {
+      const int b = g + v * ng;
+      Z[a * HL + b] = (a == b) ? 1.0 : 0.0;
+    }
   double scale = 0.0;
   for (int i = 0; i < kk; ++i) scale = fmax(scale, fabs(H[i * HL + i]));
   const double thr = thr_rel * scale;
   const double isc = scale > 0.0 ? 1.0 / scale : 1.0;  // keeps the fp32 tangent in range
-  eig_sync();
-  const int nent = kk * kk;
-  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    int any = 0;
-    for (int e = tid; e < nent; e += kEigNT) {
-      const int ab = etab[e];
-      const int a = ab >> 8, b = ab & 255;
-      any |= (a < b && fabs(H[a * HL + b]) > thr);
+  double off = 0.0;
+#pragma unroll
+  for (int v = 0; v < kEigCPT; ++v)
+    if (v < ncol) {
+      const int b = g + v * ng;
+      if (a != b) off = fmax(off, fabs(H[a * HL + b]));
     }
-    any = __any_sync(0xffffffffu, any);
-    if ((tid & 31) == 0) S.flags[2 + (tid >> 5)] = any;
-    eig_sync();
-    const int go = S.flags[2] | S.flags[3] | S.flags[4] | S.flags[5];
-    eig_sync();
-    if (!go) break;
+  double* offw = S.ws + 16;  // 2 x 4 warp maxima (double-buffered by sweep)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) off = fmax(off, __shfl_xor_sync(0xffffffffu, off, o));
+  if (lane == 0) offw[wq] = off;
+  eig_sync();
+  off = fmax(fmax(offw[0], offw[1]), fmax(offw[2], offw[3]));
+  for (int sweep = 0; sweep < max_sweeps && off > thr; ++sweep) {
     if (dbg && blockIdx.x == 0 && tid == 0) dbg[13] += 1;
+    double offl = 0.0;
+    const bool rec = dbg && blockIdx.x == 0 && tid == 0;
     for (int rd = 0; rd < nrd; ++rd) {
-      const int* pt = ptab + rd * nply;
-      int rot = 0;
-      if (tid < kk) {
-        const int p = tid, q = pt[p];
-        if (q < kk && p < q) {
+      long long tr0 = rec ? clock64() : 0;
+      if (tid < nply / 2) {
+        int p = circle_player(tid, rd, nrd), q = circle_player(nply - 1 - tid, rd, nrd);
+        if (p > q) { const int t = p; p = q; q = t; }
+        if (q < kk) {
+          const double hpq = H[p * HL + q], hpp = H[p * HL + p], hqq = H[q * HL + q];
           double c = 1.0, s = 0.0;
-          const double hpq = H[p * HL + q];
           if (fabs(hpq) > 1e-300 && fabs(hpq) > thr) {
             // tan(theta) in fp32 (only the convergence rate depends on it);
             // c = (1 + t^2)^{-1/2}, s = t c in fp64 from that t keep the
             // transform orthogonal to fp64 round-off.
-            const double hpp = H[p * HL + p], hqq = H[q * HL + q];
             const float d = (float)((hqq - hpp) * isc), h2 = (float)(2.0 * hpq * isc);
-            const float rt = sqrtf(fmaf(d, d, h2 * h2));
+            const float rt = (float)approx_sqrtf_d(fmaf(d, d, h2 * h2));
             const float tf = __fdividef(h2, fabsf(d) + rt) * (d >= 0.f ? 1.f : -1.f);
             const double t = (double)tf;
             c = rsqrt(fma(t, t, 1.0));
             s = t * c;
-            rot = 1;
           }
           S.cs[2 * p] = c;  S.cs[2 * p + 1] = s;     // first of the pair
           S.cs[2 * q] = c;  S.cs[2 * q + 1] = -s;    // second (sign flip)
-        } else if (q >= kk) {
+          prt[p] = q;
+          prt[q] = p;
+        } else {  // p pairs with the padding index of an odd kk
           S.cs[2 * p] = 1.0; S.cs[2 * p + 1] = 0.0;
+          prt[p] = p;
         }
       }
-      rot = __any_sync(0xffffffffu, rot);  // rotating threads all live in warp 0 (kk <= 32)
-      int* rflag = S.flags + 8 + (rd & 1);  // alternate slots: no barrier needed when skipping
-      if (tid == 0) *rflag = rot;
+      long long tr1 = rec ? clock64() : 0;
       eig_sync();
-      if (!*rflag) continue;  // nothing rotates this round: H, Z unchanged
-#pragma unroll 4
-      for (int e = tid; e < nent; e += kEigNT) {
-        const int ab = etab[e];
-        const int a = ab >> 8, b = ab & 255;
-        const int x = pt[a], y = pt[b];
-        const int pa = x < kk ? x : a, pb = y < kk ? y : b;
+      long long tr2 = rec ? clock64() : 0;
+      const bool lastrd = rd == nrd - 1;
+      if (act) {
+        // row a:  H' = J^T H J  restricted to (a, b):  rows a, pa then columns b, pb
+        const int pa = prt[a];
         const double ca = S.cs[2 * a], sa = S.cs[2 * a + 1];
-        const double cb = S.cs[2 * b], sb = S.cs[2 * b + 1];
-        const double r_b = ca * H[a * HL + b] - sa * H[pa * HL + b];
-        const double r_pb = ca * H[a * HL + pb] - sa * H[pa * HL + pb];
-        Hn[a * HL + b] = cb * r_b - sb * r_pb;
-        Zn[a * HL + b] = cb * Z[a * HL + b] - sb * Z[a * HL + pb];  // Z <- Z J
+        const double* Ha = H + a * HL;
+        const double* Hpa = H + pa * HL;
+        const double* Za = Z + a * HL;
+#pragma unroll 4
+        for (int v = 0; v < ncol; ++v) {
+          const int b = g + v * ng;
+          const int pb = prt[b];
+          const double cb = S.cs[2 * b], sb = S.cs[2 * b + 1];
+          const double r_b = ca * Ha[b] - sa * Hpa[b];
+          const double r_pb = ca * Ha[pb] - sa * Hpa[pb];
+          const double hn = cb * r_b - sb * r_pb;
+          Hn[a * HL + b] = hn;
+          Zn[a * HL + b] = cb * Za[b] - sb * Za[pb];  // Z <- Z J
+          if (lastrd && a != b) offl = fmax(offl, fabs(hn));
+        }
       }
+      if (lastrd) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) offl = fmax(offl, __shfl_xor_sync(0xffffffffu, offl, o));
+        if (lane == 0) offw[4 * (sweep & 1) + wq] = offl;
+      }
+      long long tr3 = rec ? clock64() : 0;
       eig_sync();
+      if (rec) {
+        const long long tr4 = clock64();
+        dbg[11] += tr1 - tr0; dbg[12] += tr2 - tr1; dbg[15] += tr3 - tr2; dbg[6] += tr4 - tr3;
+      }
       double* t = H; H = Hn; Hn = t;
       t = Z; Z = Zn; Zn = t;
     }
+    const double* ow = offw + 4 * (sweep & 1);
+    off = fmax(fmax(ow[0], ow[1]), fmax(ow[2], ow[3]));
   }
   if (Z != S.Z) {
     for (int e = tid; e < kk * kk; e += kEigNT) {
@@ -334,42 +377,72 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long l
   eig_sync();
 }
 
-// Cholesky M = Lc Lc^T of the kk x kk Gram M (ld kk) by warp 0 of the eig
-// threads (reciprocal diagonal kept in column kk); returns 0 on breakdown.
-// Caller: first kEigNT threads.
+// Cholesky M = Lc Lc^T of the kk x kk Gram M (ld kk), right-looking, by warp
+// 0 of the eig threads with lane i owning row i (column values broadcast by
+// shuffles); the reciprocal diagonal is kept in column kk.  Returns 0 on
+// breakdown.  Caller: first kEigNT threads.
 __device__ int cholesky_warp(const double* M, double* Lc, int HL, int kk, int* flag) {
-  // right-looking: Lc starts as the lower triangle of M; column j is scaled,
-  // then the trailing lower triangle is updated by all eig threads.
   const int tid = threadIdx.x;
-  for (int e = tid; e < kk * kk; e += kEigNT) {
-    const int i = e / kk, j = e - i * kk;
-    if (j <= i) Lc[i * HL + j] = M[i * kk + j];
-  }
-  if (tid == 0) *flag = 1;
-  eig_sync();
-  for (int j = 0; j < kk; ++j) {
-    double d = Lc[j * HL + j];
-    const bool bad = !(d > 1e-300);
-    if (bad) d = 1.0;
-    const double ir = rsqrt(d);  // 1 / L_jj (division-free)
-    if (tid == 0) {
-      if (bad) *flag = 0;
-      Lc[j * HL + j] = d * ir;
-      Lc[j * HL + kk] = ir;
-    }
-    for (int i = j + 1 + tid; i < kk; i += kEigNT) Lc[i * HL + j] *= ir;
-    eig_sync();
-    const int nt = kk - j - 1;  // trailing block rows j+1..kk-1
-    for (int e = tid; e < nt * nt; e += kEigNT) {
-      const int ii = e / nt, kq = e - ii * nt;
-      if (kq <= ii) {
-        const int i = j + 1 + ii, k2 = j + 1 + kq;
-        Lc[i * HL + k2] = fma(-Lc[i * HL + j], Lc[k2 * HL + j], Lc[i * HL + k2]);
+  if (tid < 32) {
+    const int i = tid;
+    const bool row = i < kk;
+    if (row)
+      for (int k = 0; k <= i; ++k) Lc[i * HL + k] = M[i * kk + k];
+    __syncwarp();
+    int ok = 1;
+    for (int j = 0; j < kk; ++j) {
+      double d = Lc[j * HL + j];
+      const bool bad = !(d > 1e-300);
+      if (bad) { d = 1.0; ok = 0; }
+      const double ir = rsqrt(d);  // 1 / L_jj (division-free)
+      double lij = 0.0;
+      if (row && i > j) {
+        lij = Lc[i * HL + j] * ir;
+        Lc[i * HL + j] = lij;
       }
+      if (i == j) {
+        Lc[j * HL + j] = d * ir;
+        Lc[j * HL + kk] = ir;
+      }
+      for (int k0 = j + 1; k0 < kk; k0 += 4) {
+        double lk[4], lv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u;
+          lk[u] = __shfl_sync(0xffffffffu, lij, k & 31);
+          lv[u] = (row && k < kk && k <= i) ? Lc[i * HL + k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u;
+          if (row && k < kk && k <= i) Lc[i * HL + k] = fma(-lij, lk[u], lv[u]);
+        }
+      }
+      __syncwarp();
     }
-    eig_sync();
+    if (tid == 0) *flag = ok;
   }
+  eig_sync();
   return *flag;
+}
+
+// x_i = (b_i - sum_{k<i} L_ik x_k) * Linv_i for i = 0..kk-1 (forward) with the
+// inner products split over four independent partial sums.
+__device__ __forceinline__ void tri_forward(const double* Lc, int HL, int kk, const double* b, int bstride,
+                                            double* x, int xstride) {
+  for (int i = 0; i < kk; ++i) {
+    double s0 = b[i * bstride], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const double* Li = Lc + i * HL;
+    int k2 = 0;
+    for (; k2 + 3 < i; k2 += 4) {
+      s0 = fma(-Li[k2], x[k2 * xstride], s0);
+      s1 = fma(-Li[k2 + 1], x[(k2 + 1) * xstride], s1);
+      s2 = fma(-Li[k2 + 2], x[(k2 + 2) * xstride], s2);
+      s3 = fma(-Li[k2 + 3], x[(k2 + 3) * xstride], s3);
+    }
+    for (; k2 < i; ++k2) s0 = fma(-Li[k2], x[k2 * xstride], s0);
+    x[i * xstride] = ((s0 + s1) + (s2 + s3)) * Li[kk];
+  }
 }
 
 // Rayleigh-Ritz on (H', M): H = Lc^{-1} H' Lc^{-T}, eig(H) = Z Lambda Z^T,
@@ -382,21 +455,10 @@ __device__ int ritz_small(Sm& S, int kk, const double* Hp, const double* M, doub
   long long t0 = clock64();
   if (!cholesky_warp(M, S.Lc, HL, kk, S.flags + 1)) return 0;
   if (rec) { const long long t1 = clock64(); dbg[8] += t1 - t0; t0 = t1; }
-  for (int c = tid; c < kk; c += kEigNT) {  // K = Lc^{-1} H' (forward substitution)
-    for (int i = 0; i < kk; ++i) {
-      double s = Hp[i * kk + c];
-      for (int k2 = 0; k2 < i; ++k2) s = fma(-S.Lc[i * HL + k2], S.H2[k2 * HL + c], s);
-      S.H2[i * HL + c] = s * S.Lc[i * HL + kk];
-    }
-  }
+  // K = Lc^{-1} H' (column c: stride HL down the rows), then H^T = Lc^{-1} K^T
+  if (tid < kk) tri_forward(S.Lc, HL, kk, Hp + tid, kk, S.H2 + tid, HL);
   eig_sync();
-  for (int c = tid; c < kk; c += kEigNT) {  // H^T = Lc^{-1} K^T
-    for (int i = 0; i < kk; ++i) {
-      double s = S.H2[c * HL + i];
-      for (int k2 = 0; k2 < i; ++k2) s = fma(-S.Lc[i * HL + k2], S.T[c * HL + k2], s);
-      S.T[c * HL + i] = s * S.Lc[i * HL + kk];
-    }
-  }
+  if (tid < kk) tri_forward(S.Lc, HL, kk, S.H2 + tid * HL, 1, S.T + tid * HL, 1);
   eig_sync();
   for (int e = tid; e < kk * kk; e += kEigNT) {
     const int i = e / kk, j = e - i * kk;
@@ -406,11 +468,19 @@ __device__ int ritz_small(Sm& S, int kk, const double* Hp, const double* M, doub
   if (rec) { const long long t1 = clock64(); dbg[9] += t1 - t0; t0 = t1; }
   jacobi_eig(S, kk, thr_rel, max_sweeps, dbg);
   if (rec) { const long long t1 = clock64(); dbg[10] += t1 - t0; t0 = t1; dbg[14] += 1; }
-  for (int c = tid; c < kk; c += kEigNT) {  // T = Lc^{-T} Z (back substitution)
+  if (tid < kk) {  // T = Lc^{-T} Z (back substitution, column c = tid)
+    const int c = tid;
     for (int i = kk - 1; i >= 0; --i) {
-      double s = S.Z[i * HL + c];
-      for (int k2 = i + 1; k2 < kk; ++k2) s = fma(-S.Lc[k2 * HL + i], S.T[k2 * HL + c], s);
-      S.T[i * HL + c] = s * S.Lc[i * HL + kk];
+      double s0 = S.Z[i * HL + c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int k2 = i + 1;
+      for (; k2 + 3 < kk; k2 += 4) {
+        s0 = fma(-S.Lc[k2 * HL + i], S.T[k2 * HL + c], s0);
+        s1 = fma(-S.Lc[(k2 + 1) * HL + i], S.T[(k2 + 1) * HL + c], s1);
+        s2 = fma(-S.Lc[(k2 + 2) * HL + i], S.T[(k2 + 2) * HL + c], s2);
+        s3 = fma(-S.Lc[(k2 + 3) * HL + i], S.T[(k2 + 3) * HL + c], s3);
+      }
+      for (; k2 < kk; ++k2) s0 = fma(-S.Lc[k2 * HL + i], S.T[k2 * HL + c], s0);
+      S.T[i * HL + c] = ((s0 + s1) + (s2 + s3)) * S.Lc[i * HL + kk];
     }
   }
   eig_sync();
@@ -500,6 +570,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   S.Vq = svsm + L.oVq; S.P = svsm + L.oP; S.Bq = svsm + L.oBq; S.Xq = svsm + L.oXq;
   S.H = svsm + L.oH; S.H2 = svsm + L.oH2; S.Z = svsm + L.oZ; S.Lc = svsm + L.oLc; S.T = svsm + L.oT;
   S.red = svsm + L.oRed; S.rout = svsm + L.oRout; S.res = svsm + L.oRes; S.lam = svsm + L.oLam;
+  S.resq = svsm + L.oResq;
   S.cs = svsm + L.oCs; S.ws = svsm + L.oW;
   S.flags = reinterpret_cast<int*>(svsm + L.oW + kKMax);
   S.ptab = reinterpret_cast<int*>(svsm + L.oPt);
@@ -539,9 +610,9 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   cl.sync();
 
   int step = 0, buf = 0, redo = 0;
-  bool prev_conv = false, have_prev = false;
   double prev_res = 1e300;
   int stall = 0;
+  double* scrX = a.scratch + 2 * (size_t)n * kLdV;  // Ritz block X of the latest step
   long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tc = clock64();
 #define PH(i) do { if (a.dbg) { const long long _t = clock64(); tph[i] += _t - tc; tc = _t; } } while (0)
@@ -550,7 +621,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     // ---- 1. B_q = G(lo:hi, :) V   (V through L1 from the L2 scratch)
     tiled_product(Gq, ldgq, nr, n, scr[gbuf], kLdV, KP, kk, S.Bq, S.P, L.S);
     PH(0);
-    // ---- 2. one reduction: [V^T B | V^T V | previous Ritz residuals]
+    // ---- 2. one reduction: [V^T B | V^T V]
     double* rb = S.red + buf * RL;
     for (int e = tid; e < 2 * kk * kk; e += kSvdNT) {
       const int which = e / (kk * kk);
@@ -561,22 +632,12 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       for (int i = 0; i < nr; ++i) s = fma(S.Vq[i * KP + c1], Y[i * KP + c2], s);
       rb[e] = s;
     }
-    for (int c = tid; c < kk; c += kSvdNT) rb[2 * kk * kk + c] = S.res[c];
-    cluster_sum(cl, S, buf, RL);
+    cluster_sum(cl, S, buf, 2 * kk * kk);
     buf ^= 1;
-    if (have_prev) {
-      double resmax = 0.0;
-      for (int c = 0; c < reff; ++c) resmax = fmax(resmax, sqrt(S.rout[2 * kk * kk + c]));
-      const double l0 = S.lam[0];  // Ritz values of the previous step
-      prev_conv = !(l0 > 0.0) || resmax <= tol * l0;
-      if (resmax > 0.5 * prev_res) ++stall; else stall = 0;
-      prev_res = resmax;
-      if (stall >= 3 && resmax <= 1e-11 * l0) prev_conv = true;
-    }
     PH(1);
     // ---- 3. Rayleigh-Ritz (generalised through chol(V^T V))
     if (eigt) {
-      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, 4e-16, 2, a.dbg);
+      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, 4e-16, a.sweeps, a.dbg);
       if (tid == 0) S.flags[7] = ok;
     }
     __syncthreads();
@@ -590,7 +651,13 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
         S.Vq[i * KP + c] = scr[gbuf][(int64_t)(lo + i) * kLdV + c];
       }
       __syncthreads();
-      if (++redo > 3) break;
+      if (++redo > 3) {
+        for (int e = tid; e < nr * kk; e += kSvdNT) {
+          const int i = e / kk, c = e - i * kk;
+          scrX[(int64_t)(lo + i) * kLdV + c] = S.Vq[i * KP + c];
+        }
+        break;
+      }
       continue;
     }
     PH(2);
@@ -605,20 +672,12 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       }
       S.Xq[i * KP + c] = sx;
       S.P[i * KP + c] = sy;
+      scrX[(int64_t)(lo + i) * kLdV + c] = sx;
     }
     __syncthreads();
     PH(3);
-    const bool last = prev_conv || step + 1 >= a.maxsteps;
-    double* sc = scr[gbuf ^ 1];
-    if (last) {
-      for (int e = tid; e < nr * kk; e += kSvdNT) {
-        const int i = e / kk, c = e - i * kk;
-        sc[(int64_t)(lo + i) * kLdV + c] = S.Xq[i * KP + c];
-      }
-      gbuf ^= 1;
-      break;
-    }
-    // ---- 5. this step's residuals (reduced with the next step) and next block
+    // ---- 5. this step's Ritz residuals (my rows) and the next block
+    double* rq = S.resq + (step & 1) * kKMax;
     const double lam0 = S.lam[0];
     const double sig_thr = 1e-10 * fabs(lam0);
     for (int c = tid; c < kk; c += kSvdNT) {
@@ -628,8 +687,9 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
         const double d = S.P[i * KP + c] - lc * S.Xq[i * KP + c];
         rs = fma(d, d, rs);
       }
-      S.res[c] = rs;
+      rq[c] = rs;
     }
+    double* sc = scr[gbuf ^ 1];
     for (int e = tid; e < nr * kk; e += kSvdNT) {
       const int i = e / kk, c = e - i * kk;
       const double lc = S.lam[c];
@@ -638,24 +698,40 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       sc[(int64_t)(lo + i) * kLdV + c] = v;
     }
     PH(4);
-    // ---- 6. publish the next block (double-buffered L2 scratch)
+    // ---- 6. publish X and the next block; residuals of THIS step from every
+    // CTA's shared memory (fixed rank order: identical on all CTAs)
     __threadfence();
     cl.sync();
+    if (tid < reff) {
+      double v[16];
+#pragma unroll
+      for (int qq = 0; qq < 16; ++qq) v[qq] = qq < CS ? *cl.map_shared_rank(rq + tid, qq) : 0.0;
+      double rs = v[0];
+#pragma unroll
+      for (int qq = 1; qq < 16; ++qq)
+        if (qq < CS) rs += v[qq];
+      S.res[tid] = sqrt(rs);
+    }
+    __syncthreads();
+    double resmax = 0.0;
+    for (int c = 0; c < reff; ++c) resmax = fmax(resmax, S.res[c]);
+    bool conv = !(lam0 > 0.0) || resmax <= tol * lam0;
+    if (resmax > 0.5 * prev_res) ++stall; else stall = 0;
+    prev_res = resmax;
+    if (stall >= 3 && resmax <= 1e-11 * lam0) conv = true;
     gbuf ^= 1;
-    have_prev = true;
     ++step;
     PH(5);
+    if (conv || step >= a.maxsteps) break;
   }
-  __threadfence();
-  cl.sync();
-  if (q == 0 && tid == 0 && a.steps_out) *a.steps_out = step + 1;
+  if (q == 0 && tid == 0 && a.steps_out) *a.steps_out = step;
   PH(6);
   if (a.dbg && q == 0 && tid == 0)
     for (int i = 0; i < 8; ++i) a.dbg[i] += tph[i];
 #undef PH
 
   // ---- 7. Rayleigh-Ritz on U itself: Y = U V (my m-rows), H2 = Y^T Y
-  const double* Vf = scr[gbuf];
+  const double* Vf = scrX;  // published before the loop's last cluster sync
   tiled_product(a.U + (int64_t)mlo * a.ldu, a.ldu, mr, n, Vf, kLdV, KP, kk, S.Xq, S.P, L.S);
   {
     double* rb = S.red + buf * RL;
@@ -679,7 +755,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   __syncthreads();
   rotate_rows(S.Xq, mr, KP, kk, S.Z, HL, S.P);
   // rotated V: my rows into Vq and into the other scratch buffer (for QJ)
-  double* Vr = scr[gbuf ^ 1];
+  double* Vr = scr[0];  // free: both block buffers are dead after the loop
   for (int e = tid; e < nr * kk; e += kSvdNT) {
     const int i = e / kk, c = e - i * kk;
     double s = 0.0;

@@ -19,10 +19,11 @@ struct SvdArgs {
   const void* warm; int warm_ld; int warm_cols;  // n x warm_cols start block (storage type) or null
   double* W; double* sigma; double* V; double* inv;  // fp64 outputs: m x r, r, n x r, r
   void* Wr; void* PI; void* VS; void* QJ;            // storage-type strip inputs: m x r, m x r, n x r, n x r
-  double* scratch;                // 2 x n x 32 doubles (double-buffered all-gather)
+  double* scratch;                // 3 x n x 32 doubles (double-buffered block + Ritz block X)
   const int* done;
   int* steps_out;
   double tol; int maxsteps;       // Ritz residual target: max(tol, tol_scale * e_{k-1}) * lambda_1
+  int sweeps;                     // Jacobi sweeps per intermediate Rayleigh-Ritz step
   double tol_scale; const double* prev_err;  // e_{k-1} on the device (null at k = 0)
   uint64_t salt;
   long long* dbg;                 // optional per-phase clock64 totals (8)

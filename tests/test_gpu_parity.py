@@ -136,3 +136,31 @@ def test_materialize_matches_oracle(ir):
     cur, _, _ = ir.solve(D, _cfg(ir, meta), device=0)
     L_ref = orc.materialize(g["C"], g["V"], g["inv_sigma"], g["W"], g["R"])
     assert rel(ir.materialize(cur), L_ref) <= TOL64
+
+
+@pytest.mark.parametrize("decay", [0.9, 0.99, 1.0])
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+def test_no_spectral_gap_matches_oracle(ir, decay, mode):
+    """Cores whose singular values have no gap at r (rank-8 data, r = 4,
+    geometric decay or exactly equal): the block subspace SVD must still
+    reproduce LAPACK's top-r triplets through the whole trace."""
+    from oracle import ircur_oracle as orc
+    rng = np.random.default_rng(17)
+    n1, n2, k = 260, 230, 8
+    A = np.linalg.qr(rng.standard_normal((n1, k)))[0]
+    B = np.linalg.qr(rng.standard_normal((n2, k)))[0]
+    s = 50.0 * decay ** np.arange(k)
+    D = (A * s) @ B.T
+    mask = rng.random((n1, n2)) < 0.05
+    D = D + np.where(mask, rng.uniform(-5, 5, (n1, n2)), 0.0)
+    zeta0 = float(np.abs((A * s) @ B.T).max())
+    kw = dict(rank=4, eps=1e-12, zeta0=zeta0, gamma=0.7, mode=mode, max_iter=12, seed=3)
+    ref = orc.solve(D, **kw)
+    cfg = ir.SolverConfig(rank=4, eps=1e-12, zeta0=zeta0, gamma=0.7, mode=mode, max_iter=12,
+                          seed=ir.RngSeed(3))
+    cur, sp, tr = ir.solve(D, cfg, device=0)
+    assert tr.iterations == ref.iterations
+    np.testing.assert_allclose(tr.errors, ref.errors, rtol=1e-8)
+    np.testing.assert_allclose(cur.core_pinv.sigma, ref.sigma, rtol=1e-9)
+    assert rel(cur.C, ref.C) <= TOL64 and rel(cur.R, ref.R) <= TOL64
+    assert rel(sp.row_values, ref.S_rows) <= TOL64
