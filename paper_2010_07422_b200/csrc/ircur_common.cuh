@@ -46,6 +46,15 @@ __device__ __forceinline__ Pair<double> pfma(Pair<double> a, Pair<double> b, Pai
   return {make_double2(__fma_rn(a.v.x, b.v.x, c.v.x), __fma_rn(a.v.y, b.v.y, c.v.y))};
 }
 
+// d - x per lane with one rounding (fma(x, -1, d) == d - x exactly rounded,
+// i.e. bitwise the scalar sub_rn of each lane).
+__device__ __forceinline__ Pair<float> psub(Pair<float> d, Pair<float> x) {
+  return {__ffma2_rn(x.v, make_float2(-1.f, -1.f), d.v)};
+}
+__device__ __forceinline__ Pair<double> psub(Pair<double> d, Pair<double> x) {
+  return {make_double2(__dsub_rn(d.v.x, x.v.x), __dsub_rn(d.v.y, x.v.y))};
+}
+
 // Threshold value in storage precision such that, for every value x of type
 // T, (|x| > zt) <=> ((double)|x| > zeta).  For float this is zeta rounded
 // toward -inf (computed on the host); for double it is zeta itself.
@@ -59,6 +68,16 @@ __device__ __forceinline__ T keep_value(T d, T l, T zt, T& s_out) {
   T s = (fabs(x) > zt) ? x : T(0);
   s_out = s;
   return sub_rn(d, s);
+}
+
+// keep_value for two adjacent entries (same per-lane operations).
+template <typename T>
+__device__ __forceinline__ Pair<T> keep_pair(Pair<T> d, Pair<T> l, T zt) {
+  const Pair<T> x = psub(d, l);
+  Pair<T> sv;
+  sv.v.x = (fabs(x.v.x) > zt) ? x.v.x : T(0);
+  sv.v.y = (fabs(x.v.y) > zt) ? x.v.y : T(0);
+  return psub(d, sv);
 }
 
 // L_k(i,j) as the shared chain.  a: R values of the row factor, b: R values

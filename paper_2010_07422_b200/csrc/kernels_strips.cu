@@ -33,7 +33,7 @@ __host__ __device__ constexpr int group_lines() { return (sizeof(T) == 8 && R > 
 
 struct StripsLayout {
   int RP;
-  size_t seg, bars, stage, bst, lvec, lidx, red, part, fnew, dred, total;
+  size_t seg, bars, stage, lptr, lvec, lidx, red, part, fnew, dred, total;
 };
 
 __host__ __device__ inline size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
@@ -44,8 +44,9 @@ __host__ __device__ inline StripsLayout strips_layout(int maxl, int R, int esz) 
   L.seg = (size_t)kSTX * esz;
   size_t off = 0;
   L.bars = off; off += 128;
-  L.stage = off; off = align128(off + 2 * (size_t)maxl * L.seg);
-  L.bst = off; off = align128(off + 2 * (size_t)R * L.seg);
+  // per buffer: maxl line segments, then the R rows of the old factor
+  L.stage = off; off = align128(off + 2 * (size_t)(maxl + R) * L.seg);
+  L.lptr = off; off = align128(off + 2 * (size_t)(maxl + R) * sizeof(void*));
   L.lvec = off; off = align128(off + (size_t)maxl * 3 * L.RP * esz);
   L.lidx = off; off = align128(off + 2 * (size_t)maxl * sizeof(int));
   L.red = off; off = align128(off + (size_t)kSNW * R * L.seg);
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
   T* stage = reinterpret_cast<T*>(sm + L.stage);
-  T* bst = reinterpret_cast<T*>(sm + L.bst);
+  const T** lptr = reinterpret_cast<const T**>(sm + L.lptr);  // [2][maxl + R] segment sources
   T* lvec = reinterpret_cast<T*>(sm + L.lvec);
   int* lidx = reinterpret_cast<int*>(sm + L.lidx);
   T* red = reinterpret_cast<T*>(sm + L.red);
@@ -158,6 +159,14 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
   }
   for (int e = tid; e < nmy[0]; e += kSNT) lidx[e] = a.s[0].lines[kb[0] + e] - a.s[0].line_off;
   for (int e = tid; e < nmy[1]; e += kSNT) lidx[maxl + e] = a.s[1].lines[kb[1] + e] - a.s[1].line_off;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {  // line sources of the bulk path: my lines, then the factor rows
+    const StripDesc<T>& s = a.s[q];
+    if (!s.bulk_ok) continue;
+    for (int e = tid; e < nmy[q] + R; e += kSNT)
+      lptr[q * (maxl + R) + e] = e < nmy[q] ? s.src + (int64_t)(s.lines[kb[q] + e] - s.line_off) * s.line_stride
+                                            : s.Bold + (int64_t)(e - nmy[q]) * s.ldb;
+  }
   (void)bars; (void)seg;
   __syncthreads();
 
@@ -176,23 +185,37 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     if (tile_of(i, q, x0)) {
       const StripDesc<T>& s = a.s[q];
       const int* li = lidx + q * maxl;
-      T* stg = stage + (size_t)st * maxl * kSTX;
-      T* bsg = bst + (size_t)st * R * kSTX;
+      T* stg = stage + (size_t)st * (maxl + R) * kSTX;
+      T* bsg = stg + (size_t)maxl * kSTX;
       const int nl = nmy[q];
       if (s.bulk_ok) {
+        // lane -> fixed 16-byte chunk of a segment, LPP segments per pass;
+        // segment v < nl is line v, v >= nl the factor row v - nl
         constexpr int EPC = 16 / (int)sizeof(T);  // elements per 16-byte chunk
         constexpr int CPL = kSTX / EPC;           // chunks per line segment
-        const int nch = (nl + R) * CPL;
-        for (int c = tid; c < nch; c += kSNT) {
-          const int ln = c / CPL, ch = c - ln * CPL;
+        constexpr int LPP = kSNT / CPL;           // segments per pass
+        const int ch = tid % CPL;
+        const T* const* lp = lptr + q * (maxl + R);
+        const uint32_t sb = smem_u32(stg) + ch * 16;
+        const int nv = nl + R;
+        if (x0 + kSTX <= s.npos) {
+          for (int v = tid / CPL; v < nv; v += LPP) {
+            const int dl = v < nl ? v : maxl + (v - nl);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + dl * kSTX * (int)sizeof(T)),
+                         "l"(lp[v] + x0 + ch * EPC)
+                         : "memory");
+          }
+        } else {
           const int pos = x0 + ch * EPC;
           const int rem = s.npos - pos;
           const int bytes = rem >= EPC ? 16 : (rem > 0 ? rem * (int)sizeof(T) : 0);
           const int sp = bytes ? pos : x0;
-          if (ln < nl)
-            cp_async16(stg + (size_t)ln * kSTX + ch * EPC, s.src + (int64_t)li[ln] * s.line_stride + sp, bytes);
-          else
-            cp_async16(bsg + (size_t)(ln - nl) * kSTX + ch * EPC, s.Bold + (int64_t)(ln - nl) * s.ldb + sp, bytes);
+          for (int v = tid / CPL; v < nv; v += LPP) {
+            const int dl = v < nl ? v : maxl + (v - nl);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sb + dl * kSTX * (int)sizeof(T)),
+                         "l"(lp[v] + sp), "r"(bytes)
+                         : "memory");
+          }
         }
       } else {
         const int nel = (nl + R) * kSTX;
@@ -223,8 +246,8 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     const int st = i & 1;
     const StripDesc<T>& s = a.s[q];
     const int nl = nmy[q];
-    T* stg = stage + (size_t)st * maxl * kSTX;
-    T* bsg = bst + (size_t)st * R * kSTX;
+    T* stg = stage + (size_t)st * (maxl + R) * kSTX;
+    T* bsg = stg + (size_t)maxl * kSTX;
     if (q != cur_strip) {
       // per-line vectors of this strip (my lines): A | W | Res, padded to RP
       for (int e = tid; e < nl * 3 * R; e += kSNT) {
@@ -250,7 +273,7 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     Pair<T> acc[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) acc[t] = Pair<T>::splat(T(0));
-    T den = T(0);
+    Pair<T> den = Pair<T>::splat(T(0));
     const int pe = 2 * lane;
     // lines in groups of kG with interleaved (independent) rank-r chains
     constexpr int kG = group_lines<T, R>();
@@ -271,11 +294,8 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
         for (int g = 0; g < kG; ++g) l[g] = pfma(Pair<T>::splat(av[g][t]), b[t], l[g]);
 #pragma unroll
       for (int g = 0; g < kG; ++g) {
-        T s0, s1;
-        c[g].v.x = keep_value(d[g].v.x, l[g].v.x, zt, s0);
-        c[g].v.y = keep_value(d[g].v.y, l[g].v.y, zt, s1);
-        den = fma_rn(d[g].v.x, d[g].v.x, den);
-        den = fma_rn(d[g].v.y, d[g].v.y, den);
+        c[g] = keep_pair(d[g], l[g], zt);
+        den = pfma(d[g], d[g], den);
         sts_pair(stg + (size_t)(kl + g * kSNW) * kSTX + pe, c[g]);
       }
       if (accum) {
@@ -292,12 +312,8 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
       Pair<T> l = pmul(Pair<T>::splat(av[0]), b[0]);
 #pragma unroll
       for (int t = 1; t < R; ++t) l = pfma(Pair<T>::splat(av[t]), b[t], l);
-      T s0, s1;
-      Pair<T> c;
-      c.v.x = keep_value(d.v.x, l.v.x, zt, s0);
-      c.v.y = keep_value(d.v.y, l.v.y, zt, s1);
-      den = fma_rn(d.v.x, d.v.x, den);
-      den = fma_rn(d.v.y, d.v.y, den);
+      const Pair<T> c = keep_pair(d, l, zt);
+      den = pfma(d, d, den);
       sts_pair(cell, c);
       if (accum) {
         const T* wv = av + RP;
@@ -306,7 +322,8 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
       }
     }
     if (accum) {
-      if (q == 0) den_acc0 += (double)den; else den_acc1 += (double)den;
+      const double dsum = (double)den.v.x + (double)den.v.y;
+      if (q == 0) den_acc0 += dsum; else den_acc1 += dsum;
 #pragma unroll
       for (int t = 0; t < R; ++t) sts_pair(red + ((size_t)w * R + t) * kSTX + pe, acc[t]);
       __syncthreads();
@@ -359,7 +376,7 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     Pair<T> f[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) f[t] = lds_pair(fnew + t * kSTX + pe);
-    T res = T(0);
+    Pair<T> res = Pair<T>::splat(T(0));
     kl = w;
     for (; kl + (kG - 1) * kSNW < nl; kl += kG * kSNW) {
       Pair<T> c[kG], l[kG];
@@ -377,10 +394,8 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
         for (int g = 0; g < kG; ++g) l[g] = pfma(Pair<T>::splat(rv[g][t]), f[t], l[g]);
 #pragma unroll
       for (int g = 0; g < kG; ++g) {
-        const T r0 = sub_rn(c[g].v.x, l[g].v.x);
-        const T r1 = sub_rn(c[g].v.y, l[g].v.y);
-        res = fma_rn(r0, r0, res);
-        res = fma_rn(r1, r1, res);
+        const Pair<T> rr = psub(c[g], l[g]);
+        res = pfma(rr, rr, res);
       }
     }
     for (; kl < nl; kl += kSNW) {
@@ -389,12 +404,11 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
       Pair<T> l = pmul(Pair<T>::splat(rv[0]), f[0]);
 #pragma unroll
       for (int t = 1; t < R; ++t) l = pfma(Pair<T>::splat(rv[t]), f[t], l);
-      const T r0 = sub_rn(c.v.x, l.v.x);
-      const T r1 = sub_rn(c.v.y, l.v.y);
-      res = fma_rn(r0, r0, res);
-      res = fma_rn(r1, r1, res);
+      const Pair<T> rr = psub(c, l);
+      res = pfma(rr, rr, res);
     }
-    if (q == 0) res_acc0 += (double)res; else res_acc1 += (double)res;
+    const double rsum = (double)res.v.x + (double)res.v.y;
+    if (q == 0) res_acc0 += rsum; else res_acc1 += rsum;
     __syncthreads();  // stage st, fnew, red are free again
     issue(i + 2, st);
   }
