@@ -190,7 +190,7 @@ int ircur_get_svd_steps(ircur_ctx_t ctx, int n_iters, int* steps);
 /* Accumulated clock64 cycles per phase of the core-SVD kernel while
  * profiling is on: [product | reduction | Rayleigh-Ritz | rotation |
  * next block | all-gather | final stage | loop overhead] (diagnostics). */
-int ircur_get_svd_phase_cycles(ircur_ctx_t ctx, long long* cycles8, int reset);
+int ircur_get_svd_phase_cycles(ircur_ctx_t ctx, long long* cycles32, int reset);
 
 /* Stateless variant: stream L = P Q from caller-held factors Pt (rank x
  * nrows, row stride ldp) and Q (rank x n2, row stride ldq), dtype

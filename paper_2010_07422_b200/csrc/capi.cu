@@ -231,6 +231,7 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
   cs.tiles = (int)((c->nloc + TX - 1) / TX);
   cs.mode = kStripFull;
   pa.zt = storage_zeta<T>(zeta); pa.partials = c->partials; pa.done = c->flags;
+  pa.dbg = c->profiling ? c->svd_dbg + 16 : nullptr;
   pa.maxl = (std::max(c->max_rows, c->max_cols) + c->strips_cs - 1) / c->strips_cs;
   return pa;
 }
@@ -458,8 +459,8 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->errors, (size_t)max_iter * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->flags, 16 * sizeof(int)));
   IR_CUDA_C(cudaMalloc(&c->svd_steps, (size_t)max_iter * sizeof(int)));
-  IR_CUDA_C(cudaMalloc(&c->svd_dbg, 16 * sizeof(long long)));
-  IR_CUDA_C(cudaMemsetAsync(c->svd_dbg, 0, 16 * sizeof(long long), c->stream));
+  IR_CUDA_C(cudaMalloc(&c->svd_dbg, 32 * sizeof(long long)));  // [0,16) SVD, [16,32) strips
+  IR_CUDA_C(cudaMemsetAsync(c->svd_dbg, 0, 32 * sizeof(long long), c->stream));
   IR_CUDA_C(cudaMalloc(&c->maxbits, sizeof(unsigned long long)));
   IR_CUDA_C(cudaHostAlloc(&c->h_flags, 16 * sizeof(int), cudaHostAllocMapped));
   IR_CUDA_C(cudaHostGetDevicePointer((void**)&c->h_flags_dev, c->h_flags, 0));
@@ -968,11 +969,11 @@ int ircur_get_svd_steps(ircur_ctx_t c, int n_iters, int* steps) {
   return IRCUR_OK;
 }
 
-int ircur_get_svd_phase_cycles(ircur_ctx_t c, long long* cycles16, int reset) {
-  if (!c || !cycles16) return fail(IRCUR_EINVAL, "bad arguments");
+int ircur_get_svd_phase_cycles(ircur_ctx_t c, long long* cycles32, int reset) {
+  if (!c || !cycles32) return fail(IRCUR_EINVAL, "bad arguments");
   IR_CUDA(cudaSetDevice(c->device));
-  IR_CUDA(cudaMemcpyAsync(cycles16, c->svd_dbg, 16 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  if (reset) IR_CUDA(cudaMemsetAsync(c->svd_dbg, 0, 16 * sizeof(long long), c->stream));
+  IR_CUDA(cudaMemcpyAsync(cycles32, c->svd_dbg, 32 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  if (reset) IR_CUDA(cudaMemsetAsync(c->svd_dbg, 0, 32 * sizeof(long long), c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));
   return IRCUR_OK;
 }

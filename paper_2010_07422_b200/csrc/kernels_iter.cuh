@@ -60,6 +60,7 @@ struct StripsArgs {
   int maxl;                                    // max lines per CTA (smem sizing)
   double* partials;                            // per CTA: {den, res}
   const int* done;
+  long long* dbg;                              // optional per-phase clock64 totals (CTA 0, thread 0)
 };
 
 // ------------------------------------------------------------- finalize

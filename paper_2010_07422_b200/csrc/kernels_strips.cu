@@ -44,8 +44,9 @@ __host__ __device__ inline StripsLayout strips_layout(int maxl, int R, int esz) 
   L.seg = (size_t)kSTX * esz;
   size_t off = 0;
   L.bars = off; off += 128;
-  // per buffer: maxl line segments, then the R rows of the old factor
-  L.stage = off; off = align128(off + 2 * (size_t)(maxl + R) * L.seg);
+  // per buffer: maxl line segments, the R rows of the old factor, then the
+  // tile's 64 entries of the override map (ints)
+  L.stage = off; off = align128(off + 2 * (size_t)(maxl + R + 1) * L.seg);
   L.lptr = off; off = align128(off + 2 * (size_t)(maxl + R) * sizeof(void*));
   L.lvec = off; off = align128(off + (size_t)maxl * 3 * L.RP * esz);
   L.lidx = off; off = align128(off + 2 * (size_t)maxl * sizeof(int));
@@ -185,9 +186,18 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     if (tile_of(i, q, x0)) {
       const StripDesc<T>& s = a.s[q];
       const int* li = lidx + q * maxl;
-      T* stg = stage + (size_t)st * (maxl + R) * kSTX;
+      T* stg = stage + (size_t)st * (maxl + R + 1) * kSTX;
       T* bsg = stg + (size_t)maxl * kSTX;
       const int nl = nmy[q];
+      if (tid < kSTX / 4) {  // override map of the tile: 16 x 16-byte chunks of ints
+        const int pos = x0 + 4 * tid;
+        const int rem = s.npos - pos;
+        const int bytes = rem >= 4 ? 16 : (rem > 0 ? 4 * rem : 0);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         smem_u32(reinterpret_cast<int*>(stg + (size_t)(maxl + R) * kSTX) + 4 * tid)),
+                     "l"(s.omap + (bytes ? pos : x0)), "r"(bytes)
+                     : "memory");
+      }
       if (s.bulk_ok) {
         // lane -> fixed 16-byte chunk of a segment, LPP segments per pass;
         // segment v < nl is line v, v >= nl the factor row v - nl
@@ -240,14 +250,19 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
   int cur_strip = -1;
   double den_acc0 = 0.0, res_acc0 = 0.0, den_acc1 = 0.0, res_acc1 = 0.0;
   const T zt = a.zt;
+  const bool rec = a.dbg && blockIdx.x == 0 && tid == 0;
+  long long tpc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tq = clock64();
+#define SPH(k) do { if (rec) { const long long _t = clock64(); tpc[k] += _t - tq; tq = _t; } } while (0)
   for (int i = 0;; ++i) {
     int q, x0;
     if (!tile_of(i, q, x0)) break;
     const int st = i & 1;
     const StripDesc<T>& s = a.s[q];
     const int nl = nmy[q];
-    T* stg = stage + (size_t)st * (maxl + R) * kSTX;
+    T* stg = stage + (size_t)st * (maxl + R + 1) * kSTX;
     T* bsg = stg + (size_t)maxl * kSTX;
+    const int* omt = reinterpret_cast<const int*>(stg + (size_t)(maxl + R) * kSTX);  // override map of the tile
     if (q != cur_strip) {
       // per-line vectors of this strip (my lines): A | W | Res, padded to RP
       for (int e = tid; e < nl * 3 * R; e += kSNT) {
@@ -261,8 +276,10 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
       cur_strip = q;
       __syncthreads();
     }
+    SPH(6);
     cp_async_wait1();  // this thread's copies of tile i have landed
     __syncthreads();   // ... and everybody else's
+    SPH(0);
 
     // ---- pass 1: Phase I/II in place + factor partials
     const int mode = s.mode;  // uniform per tile (and per cluster)
@@ -321,48 +338,50 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
         for (int t = 0; t < R; ++t) acc[t] = pfma(Pair<T>::splat(wv[t]), c, acc[t]);
       }
     }
+    SPH(1);
     if (accum) {
       const double dsum = (double)den.v.x + (double)den.v.y;
       if (q == 0) den_acc0 += dsum; else den_acc1 += dsum;
 #pragma unroll
       for (int t = 0; t < R; ++t) sts_pair(red + ((size_t)w * R + t) * kSTX + pe, acc[t]);
       __syncthreads();
+      // Positions of the other index set take the factor computed from the
+      // core (Q(:,J) = W^T U, P(I,:) = U V Sigma^+): one value for the I x J
+      // block.  Applied where each output is produced (not in kStripPartial).
+      const bool ovr = mode != kStripPartial;
       T* pbuf = part + (size_t)(i & 1) * R * kSTX;
-      T* fsum = CS > 1 ? pbuf : fnew;
       for (int o = tid; o < R * kSTX; o += kSNT) {
         T sum = red[o];
 #pragma unroll
         for (int ww = 1; ww < kSNW; ++ww) sum += red[(size_t)ww * R * kSTX + o];
-        fsum[o] = sum;
+        if (CS > 1) {
+          pbuf[o] = sum;
+        } else {
+          const int t = o / kSTX, x = o - t * kSTX;
+          const int e = (ovr && x0 + x < s.npos) ? omt[x] : -1;
+          fnew[o] = e >= 0 ? s.otherF[(int64_t)e * R + t] : sum;
+        }
       }
       if (CS > 1) {
         cl.sync();
         for (int o = tid; o < R * kSTX; o += kSNT) {
           T sum = *cl.map_shared_rank(pbuf + o, 0);
           for (int qq = 1; qq < CS; ++qq) sum += *cl.map_shared_rank(pbuf + o, qq);
-          fnew[o] = sum;
+          const int t = o / kSTX, x = o - t * kSTX;
+          const int e = (ovr && x0 + x < s.npos) ? omt[x] : -1;
+          fnew[o] = e >= 0 ? s.otherF[(int64_t)e * R + t] : sum;
         }
       }
     } else {  // kStripFinish: the factor sums were all-reduced across the row shards
       for (int o = tid; o < R * kSTX; o += kSNT) {
         const int t = o / kSTX, x = o - t * kSTX;
-        fnew[o] = x0 + x < s.npos ? s.Fsrc[(int64_t)t * s.ldfs + x0 + x] : T(0);
+        const int e = x0 + x < s.npos ? omt[x] : -1;
+        fnew[o] = e >= 0 ? s.otherF[(int64_t)e * R + t]
+                         : (x0 + x < s.npos ? s.Fsrc[(int64_t)t * s.ldfs + x0 + x] : T(0));
       }
     }
     __syncthreads();
-    // positions of the other index set take the factor computed from the core
-    // (Q(:,J) = W^T U, P(I,:) = U V Sigma^+): one value for the I x J block.
-    for (int x = tid; x < kSTX && mode != kStripPartial; x += kSNT) {
-      const int pos = x0 + x;
-      if (pos < s.npos) {
-        const int e = s.omap[pos];
-        if (e >= 0) {
-#pragma unroll
-          for (int t = 0; t < R; ++t) fnew[t * kSTX + x] = s.otherF[(int64_t)e * R + t];
-        }
-      }
-    }
-    __syncthreads();
+    SPH(2);
     for (int o = tid; o < R * kSTX; o += kSNT) {
       const int t = o / kSTX, x = o - t * kSTX;
       if ((t % CS) == rank && x0 + x < s.npos) s.Fnew[(int64_t)t * s.ldf + x0 + x] = fnew[o];
@@ -372,6 +391,7 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
       issue(i + 2, st);
       continue;
     }
+    SPH(3);
     // ---- pass 2: stopping residual on the thresholded tile
     Pair<T> f[R];
 #pragma unroll
@@ -409,9 +429,14 @@ __global__ void __launch_bounds__(kSNT, 1) strips_kernel(const __grid_constant__
     }
     const double rsum = (double)res.v.x + (double)res.v.y;
     if (q == 0) res_acc0 += rsum; else res_acc1 += rsum;
+    SPH(4);
     __syncthreads();  // stage st, fnew, red are free again
     issue(i + 2, st);
+    SPH(5);
   }
+  if (rec)
+    for (int k = 0; k < 8; ++k) a.dbg[k] += tpc[k];
+#undef SPH
   cp_async_wait0();
   const double d0 = block_sum<kSNT>(den_acc0, dred);
   const double r0 = block_sum<kSNT>(res_acc0, dred + kSNW);

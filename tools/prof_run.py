@@ -29,13 +29,17 @@ for i in range(a.solves):
           f"strips {p['strips_ms'].sum():.2f} svd {p['svd_ms'].sum():.2f} core {p['core_ms'].sum():.2f} "
           f"fin {p['finalize_ms'].sum():.2f} ms", flush=True)
     import ctypes as C
-    cyc = (C.c_longlong * 16)()
+    cyc = (C.c_longlong * 32)()
     res.ctx.lib.ircur_get_svd_phase_cycles(res.ctx.h, cyc, 1)
     names = ["product", "reduce", "ritz", "rotate", "nextblk", "gather", "final", "loop"]
     tot = sum(cyc[:8]) or 1
     print("  svd phases (Mcycles, CTA0/thread0): " + " ".join(f"{n}={c/1e6:.2f}({c/tot*100:.0f}%)" for n, c in zip(names, cyc[:8])))
     print(f"  ritz: chol={cyc[8]/1e6:.2f} solves={cyc[9]/1e6:.2f} jacobi={cyc[10]/1e6:.2f} Mcyc, "
           f"eig calls={cyc[14]} sweeps={cyc[13]}")
+    sn = ["stage_wait", "pass1", "reduce", "override+write", "pass2", "sync+issue", "lvec+loop"]
+    stot = sum(cyc[16:23]) or 1
+    print("  strips phases (Mcycles, CTA0/thread0): " + " ".join(
+        f"{n}={c/1e6:.2f}({c/stot*100:.0f}%)" for n, c in zip(sn, [cyc[16 + k] for k in (0, 1, 2, 3, 4, 5, 6)])))
     if a.detail and i == a.solves - 1:
         for k in range(res.trace.iterations):
             print(f"  k={k:2d} e={res.trace.errors[k]:.3e} svd_steps={p['svd_steps'][k]:3d} svd={p['svd_ms'][k]:.3f} "
