@@ -278,90 +278,115 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
                                                           int64_t n2, const int* __restrict__ colsel,
                                                           T* __restrict__ Dt, int64_t ldt,
                                                           unsigned long long* maxbits, int* nonfinite) {
-  __shared__ T tile[kPT][kPT + 1];
-  __shared__ int sel_col[kPT], sel_dst[kPT];
-  __shared__ int nsel;
-  constexpr int VW = 16 / sizeof(T);
-  constexpr int TPR = kPT / VW;
-  constexpr int RPI = 256 / TPR;
+  // Each thread owns one 16-byte column group of a 64 x 64 tile in KR rows.
+  // The next tile's vectors and column map are loaded before the current
+  // tile is processed (register double buffering).  Selected columns are
+  // staged in a compact, double-buffered shared buffer (slot = rank of the
+  // column among the tile's selected columns, from a 16-lane shuffle scan
+  // that every warp computes identically) and written out as 16-byte
+  // vectors: one barrier per tile.
+  constexpr int VW = 16 / sizeof(T);   // elements per vector
+  constexpr int TPR = kPT / VW;        // threads per 64-element row segment
+  constexpr int RPI = 256 / TPR;       // rows per pass
+  constexpr int KR = kPT / RPI;        // rows per thread
+  constexpr int SL = kPT + VW;         // staged column length (16-byte aligned rows)
+  constexpr int NB = sizeof(T) == 4 ? 2 : 1;  // staging buffers (fp64: one, fits 48 KB static)
+  __shared__ __align__(16) T sbuf[NB][kPT][SL];
+  __shared__ int sdst[NB][kPT];
+  using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  using I4 = typename std::conditional<sizeof(T) == 4, int4, int2>::type;
   const int vx = threadIdx.x % TPR, vy = threadIdx.x / TPR;
   const int lane = threadIdx.x & 31;
-  using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   const bool vec_ok = ((ldd * (int64_t)sizeof(T)) % 16 == 0) && ((ldt * (int64_t)sizeof(T)) % 16 == 0) &&
-                      ((uintptr_t)D % 16 == 0) && ((uintptr_t)Dt % 16 == 0);
+                      ((uintptr_t)D % 16 == 0) && ((uintptr_t)Dt % 16 == 0) && (n2 % VW == 0);
   const int64_t tr = (nloc + kPT - 1) / kPT, tcn = (n2 + kPT - 1) / kPT;
   const int64_t ntiles = tr * tcn;
   T mx = T(0);
   int bad = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  auto full_tile = [&](int64_t t) {
+    const int64_t br = t / tcn, bc = t - br * tcn;
+    return vec_ok && (br * kPT + kPT <= nloc) && (bc * kPT + kPT <= n2);
+  };
+  V4 nv[KR];
+  I4 ncs;
+  auto load = [&](int64_t t) {
     const int64_t br = t / tcn, bc = t - br * tcn;
     const int64_t rb = br * kPT, cb = bc * kPT;
-    const bool full = (rb + kPT <= nloc) && (cb + kPT <= n2);
-    if (threadIdx.x < 32) {  // compact list of the selected columns of this tile
-      int base = 0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t c = cb + h * 32 + lane;
-        const int d = c < n2 ? colsel[c] : -1;
-        const unsigned m = __ballot_sync(0xffffffffu, d >= 0);
-        if (d >= 0) {
-          const int pos = base + __popc(m & ((1u << lane) - 1u));
-          sel_col[pos] = h * 32 + lane;
-          sel_dst[pos] = d;
-        }
-        base += __popc(m);
+    for (int k = 0; k < KR; ++k) nv[k] = __ldcs(reinterpret_cast<const V4*>(D + (rb + vy + k * RPI) * ldd + cb) + vx);
+    ncs = __ldg(reinterpret_cast<const I4*>(colsel + cb) + vx);
+  };
+  int64_t t = blockIdx.x;
+  if (t < ntiles && full_tile(t)) load(t);
+  int b = 0;
+  for (; t < ntiles; t += gridDim.x, b = (b + 1) % NB) {
+    const int64_t br = t / tcn, bc = t - br * tcn;
+    const int64_t rb = br * kPT, cb = bc * kPT;
+    if (full_tile(t)) {
+      V4 v[KR];
+#pragma unroll
+      for (int k = 0; k < KR; ++k) v[k] = nv[k];
+      const I4 cs = ncs;
+      const int64_t tn = t + gridDim.x;
+      if (tn < ntiles && full_tile(tn)) load(tn);
+      const int* csp = reinterpret_cast<const int*>(&cs);
+      int mine = 0;
+#pragma unroll
+      for (int u = 0; u < VW; ++u) mine += csp[u] >= 0;
+      // exclusive scan of `mine` over the TPR lanes of this row segment
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < TPR; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o, TPR);
+        if ((lane % TPR) >= o) incl += y;
       }
-      if (lane == 0) nsel = base;
-    }
-    if (full && vec_ok) {
-      V4 v[kPT / RPI];
+      const int total = __shfl_sync(0xffffffffu, incl, TPR - 1, TPR);
+      int slot = incl - mine;
 #pragma unroll
-      for (int k = 0; k < kPT / RPI; ++k)
-        v[k] = __ldcs(reinterpret_cast<const V4*>(D + (rb + vy + k * RPI) * ldd + cb) + vx);
-#pragma unroll
-      for (int k = 0; k < kPT / RPI; ++k) {
+      for (int k = 0; k < KR; ++k) {
         const T* pv = reinterpret_cast<const T*>(&v[k]);
 #pragma unroll
         for (int u = 0; u < VW; ++u) {
           const T av = fabs(pv[u]);
           bad |= !isfinite(av);
           mx = fmax(mx, av);
-          tile[vy + k * RPI][vx * VW + u] = pv[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < VW; ++u) {
+        if (csp[u] >= 0) {
+#pragma unroll
+          for (int k = 0; k < KR; ++k) sbuf[b][slot][vy + k * RPI] = reinterpret_cast<const T*>(&v[k])[u];
+          if (vy == 0) sdst[b][slot] = csp[u];
+          ++slot;
         }
       }
       __syncthreads();
-      const int ns = nsel;
-      for (int w = threadIdx.x; w < ns * TPR; w += 256) {
+      for (int w = threadIdx.x; w < total * TPR; w += 256) {
         const int k = w / TPR, x = w - k * TPR;
-        const int lc = sel_col[k];
-        V4 o;
-        T* po = reinterpret_cast<T*>(&o);
-#pragma unroll
-        for (int u = 0; u < VW; ++u) po[u] = tile[x * VW + u][lc];
-        __stcs(reinterpret_cast<V4*>(Dt + (int64_t)sel_dst[k] * ldt + rb) + x, o);
+        __stcs(reinterpret_cast<V4*>(Dt + (int64_t)sdst[b][k] * ldt + rb) + x,
+               *reinterpret_cast<const V4*>(&sbuf[b][k][x * VW]));
       }
+      if (NB == 1) __syncthreads();
     } else {
+      // edge or unaligned tile: element-wise (each thread: one column, 64/4 rows)
       const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-#pragma unroll 4
-      for (int k = 0; k < kPT; k += 4) {
-        const int64_t r = rb + ty + k, c = cb + tx;
-        T v = T(0);
+      const int64_t c = cb + tx;
+      const int d = c < n2 ? colsel[c] : -1;
+      for (int k = ty; k < kPT; k += 4) {
+        const int64_t r = rb + k;
         if (r < nloc && c < n2) {
-          v = __ldcs(D + r * ldd + c);
-          const T av = fabs(v);
+          const T val = __ldcs(D + r * ldd + c);
+          const T av = fabs(val);
           bad |= !isfinite(av);
           mx = fmax(mx, av);
+          if (d >= 0) Dt[(int64_t)d * ldt + r] = val;
         }
-        tile[ty + k][tx] = v;
       }
-      __syncthreads();
-      const int ns = nsel;
-      for (int w = threadIdx.x; w < ns * kPT; w += 256) {
-        const int k = w / kPT, x = w - k * kPT;
-        if (rb + x < nloc) __stcs(Dt + (int64_t)sel_dst[k] * ldt + rb + x, tile[x][sel_col[k]]);
-      }
+      const int64_t tn = t + gridDim.x;
+      if (tn < ntiles && full_tile(tn)) load(tn);
+      __syncthreads();  // keeps the staging-buffer reuse distance of two barriers
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
