@@ -57,7 +57,9 @@ struct ircur_ctx {
   int covered = 0;           // sets whose columns are in Dt (mode 2)
   int* d_colsel = nullptr;   // n2: column -> line of Dt or -1 (mode 2)
   int* d_cols_c = nullptr;   // per set: Dt line of each J entry (mode 2)
+  int64_t cols_c_cap = 0;
   std::vector<int> h_cols;   // host copy of the J sets (n_sets x max_cols)
+
   int* d_rows = nullptr;
   int* d_cols = nullptr;
   int n_sets = 0;
@@ -273,9 +275,13 @@ int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfi
     c->dt_cap = cap;
   }
   if (!c->d_colsel) IR_CUDA(cudaMalloc(&c->d_colsel, (size_t)c->n2 * sizeof(int)));
-  if (c->d_cols_c) cudaFree(c->d_cols_c);
-  c->d_cols_c = nullptr;
-  IR_CUDA(cudaMalloc(&c->d_cols_c, lines.size() * sizeof(int)));
+  if ((int64_t)lines.size() > c->cols_c_cap) {
+    IR_CUDA(cudaStreamSynchronize(st));
+    if (c->d_cols_c) cudaFree(c->d_cols_c);
+    c->d_cols_c = nullptr;
+    IR_CUDA(cudaMalloc(&c->d_cols_c, lines.size() * sizeof(int)));
+    c->cols_c_cap = (int64_t)lines.size();
+  }
   IR_CUDA(cudaMemcpyAsync(c->d_colsel, sel.data(), sel.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   IR_CUDA(cudaMemcpyAsync(c->d_cols_c, lines.data(), lines.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   if (c->dtype == IRCUR_F32)
@@ -607,6 +613,7 @@ int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int3
   }
   c->n_sets = n_sets;
   c->h_cols = hc;
+
   if (c->dt_mode == 2) {  // the sampled copy belongs to the previous sets
     c->dt_mode = 0;
     c->covered = 0;
@@ -619,20 +626,25 @@ int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int3
 
 int ircur_slab_sqnorms(ircur_ctx_t c, int set, double* rows_sq, double* cols_sq) {
   if (!c || !c->D || set < 0 || set >= c->n_sets) return fail(IRCUR_EINVAL, "bad context/set");
+
   IR_CUDA(cudaSetDevice(c->device));
   const int nb_rows = std::max(1, std::min(c->num_sms * 2, (int)((int64_t)c->h_row_loc_cnt[set] * c->n2 / 4096 + 1)));
   const int nb_cols = std::max(1, std::min(c->num_sms * 2, (int)(c->nloc * c->h_col_cnt[set] / 4096 + 1)));
   if (nb_rows + nb_cols > c->max_partials) return fail(IRCUR_EINVAL, "partials buffer too small");
   const int* I = c->d_rows + (size_t)set * c->max_rows + c->h_row_lo[set];
   const int* J = c->d_cols + (size_t)set * c->max_cols;
+  // D(:,J) from the column-major copy when it holds set `set` (coalesced lines)
+  const bool use_dt = c->Dt && (c->dt_mode == 1 || (c->dt_mode == 2 && set < c->covered));
+  const int* Jl = c->dt_mode == 2 ? c->d_cols_c + (size_t)set * c->max_cols : J;
   if (c->dtype == IRCUR_F32)
     IR_CUDA(launch_slab_sq<float>((const float*)c->D, c->ldd, c->row0, c->nloc, c->n2, I,
                                   c->h_row_loc_cnt[set], J, c->h_col_cnt[set], nb_rows, nb_cols,
-                                  c->partials, c->stream));
+                                  c->partials, use_dt ? (const float*)c->Dt : nullptr, c->ldt, Jl, c->stream));
   else
     IR_CUDA(launch_slab_sq<double>((const double*)c->D, c->ldd, c->row0, c->nloc, c->n2, I,
                                    c->h_row_loc_cnt[set], J, c->h_col_cnt[set], nb_rows, nb_cols,
-                                   c->partials, c->stream));
+                                   c->partials, use_dt ? (const double*)c->Dt : nullptr, c->ldt, Jl,
+                                   c->stream));
   std::vector<double> h(nb_rows + nb_cols);
   IR_CUDA(cudaMemcpyAsync(h.data(), c->partials, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));

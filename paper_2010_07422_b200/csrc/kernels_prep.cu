@@ -417,7 +417,8 @@ cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2
 template <typename T>
 __global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, int64_t row0, int64_t nloc,
                                                       int64_t n2, const int* I, int mI, const int* J,
-                                                      int nJ, int nb_rows, double* partials) {
+                                                      int nJ, int nb_rows, double* partials, const T* Dt,
+                                                      int64_t ldt, const int* Jline) {
   __shared__ double sh[8];
   double acc = 0.0;
   if ((int)blockIdx.x < nb_rows) {
@@ -430,11 +431,20 @@ __global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, i
   } else {
     const int nb_cols = gridDim.x - nb_rows;
     const int64_t total = nloc * nJ;
-    for (int64_t e = (int64_t)(blockIdx.x - nb_rows) * 256 + threadIdx.x; e < total;
-         e += (int64_t)nb_cols * 256) {
-      const int64_t x = e / nJ, k = e - x * nJ;
-      const double v = (double)D[x * ldd + J[k]];
-      acc = fma(v, v, acc);
+    if (Dt) {  // the column-major copy holds D(:,J): contiguous lines
+      for (int64_t e = (int64_t)(blockIdx.x - nb_rows) * 256 + threadIdx.x; e < total;
+           e += (int64_t)nb_cols * 256) {
+        const int64_t k = e / nloc, x = e - k * nloc;
+        const double v = (double)Dt[(int64_t)Jline[k] * ldt + x];
+        acc = fma(v, v, acc);
+      }
+    } else {
+      for (int64_t e = (int64_t)(blockIdx.x - nb_rows) * 256 + threadIdx.x; e < total;
+           e += (int64_t)nb_cols * 256) {
+        const int64_t x = e / nJ, k = e - x * nJ;
+        const double v = (double)D[x * ldd + J[k]];
+        acc = fma(v, v, acc);
+      }
     }
   }
   const double s = block_sum<256>(acc, sh);
@@ -444,9 +454,9 @@ __global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, i
 template <typename T>
 cudaError_t launch_slab_sq(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2,
                            const int* I, int mI, const int* J, int nJ, int nb_rows, int nb_cols,
-                           double* partials, cudaStream_t st) {
+                           double* partials, const T* Dt, int64_t ldt, const int* Jline, cudaStream_t st) {
   slab_sq_kernel<T><<<nb_rows + nb_cols, 256, 0, st>>>(D, ldd, row0, nloc, n2, I, mI, J, nJ, nb_rows,
-                                                       partials);
+                                                       partials, Dt, ldt, Jline);
   return cudaGetLastError();
 }
 
@@ -582,7 +592,8 @@ int64_t gen_blocks(int64_t nrows, int64_t n2) {
   template cudaError_t launch_prep_select<T>(const T*, int64_t, int64_t, int64_t, const int*, T*,  \
                                              int64_t, unsigned long long*, int*, int, cudaStream_t); \
   template cudaError_t launch_slab_sq<T>(const T*, int64_t, int64_t, int64_t, int64_t, const int*, \
-                                         int, const int*, int, int, int, double*, cudaStream_t);
+                                         int, const int*, int, int, int, double*, const T*, int64_t, \
+                                         const int*, cudaStream_t);
 IRCUR_PREP_INST(float)
 IRCUR_PREP_INST(double)
 

@@ -59,7 +59,7 @@ cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2
 template <typename T>
 cudaError_t launch_slab_sq(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2,
                            const int* I, int mI, const int* J, int nJ, int nb_rows, int nb_cols,
-                           double* partials, cudaStream_t st);
+                           double* partials, const T* Dt, int64_t ldt, const int* Jline, cudaStream_t st);
 size_t svd_smem_bytes(int n, int m, int kk, int cs);
 int svd_pick_cluster(int n, int m, int kk);
 template <typename T> cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st);

@@ -164,3 +164,28 @@ def test_no_spectral_gap_matches_oracle(ir, decay, mode):
     np.testing.assert_allclose(cur.core_pinv.sigma, ref.sigma, rtol=1e-9)
     assert rel(cur.C, ref.C) <= TOL64 and rel(cur.R, ref.R) <= TOL64
     assert rel(sp.row_values, ref.S_rows) <= TOL64
+
+
+@pytest.mark.parametrize("colmajor", ["sampled", "full", False])
+def test_zero_slabs_early_exit(ir, colmajor):
+    """solver.py:335-341: when D(I_0,:) and D(:,J_0) are identically zero the
+    solve returns the zero state, even if D is nonzero elsewhere.  The
+    sampled prep pass computes these norms itself; every copy mode must
+    agree with the reference's oracle."""
+    from oracle import ircur_oracle as orc
+    n1, n2, r = 300, 280, 3
+    cfg = ir.SolverConfig(rank=r, zeta0=1.0, mode="resampled", max_iter=20, seed=ir.RngSeed(4))
+    m1, m2 = ir.sample_count(n1, r, 4.0), ir.sample_count(n2, r, 4.0)
+    I0, J0 = ir.draw_index_sets(n1, n2, m1, m2, cfg.seed, 1)[0]
+    D = np.random.default_rng(0).standard_normal((n1, n2))
+    D[I0, :] = 0.0
+    D[:, J0] = 0.0
+    ref = orc.solve(D, rank=r, zeta0=1.0, mode="resampled", max_iter=20, seed=4)
+    cur, sp, tr = ir.solve(D, cfg, device=0, colmajor=colmajor)
+    assert ref.iterations == 0 or ref.errors == [0.0]
+    assert tr.errors == [0.0] and tr.converged and not cur.C.any()
+    D[I0[0], 5] = 1e-30  # one tiny nonzero entry in the row slab: no early exit
+    ref = orc.solve(D, rank=r, zeta0=1.0, mode="resampled", max_iter=20, seed=4)
+    cur, sp, tr = ir.solve(D, cfg, device=0, colmajor=colmajor)
+    assert tr.iterations == ref.iterations == 1 and tr.thresholds == [1.0]
+    assert tr.errors == ref.errors
