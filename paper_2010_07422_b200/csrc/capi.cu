@@ -832,11 +832,14 @@ int ircur_get_strips(ircur_ctx_t c, double* C, double* R, double* S_rows, double
   for (int q = 0; q < 4; ++q) {
     if (!out[q] || cnt[q] == 0) continue;
     cudaPointerAttributes at;
-    const bool is_dev = cudaPointerGetAttributes(&at, out[q]) == cudaSuccess &&
-                        (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    const bool known = cudaPointerGetAttributes(&at, out[q]) == cudaSuccess;
     cudaGetLastError();
-    if (is_dev) {
+    if (known && (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged)) {
       dev[q] = out[q];
+    } else if (known && at.type == cudaMemoryTypeHost && at.devicePointer) {
+      // page-locked host memory: the write-out kernel stores straight into it
+      // over PCIe (coalesced fp64 rows), no device staging buffer
+      dev[q] = static_cast<double*>(at.devicePointer);
     } else {
       IR_CUDA(cudaMalloc(&dev[q], cnt[q] * sizeof(double)));
       tmp[q] = true;

@@ -145,7 +145,10 @@ class Context:
             outs = [torch.empty(s, dtype=torch.float64, device=f"cuda:{self.device}") for s in shapes]
             ptrs = [C.c_void_p(_ptr(t)) for t in outs]
         else:
-            outs = [np.empty(s, dtype=np.float64) for s in shapes]
+            # page-locked host arrays (torch's caching host allocator): the
+            # write-out kernels store into them directly at PCIe speed, where
+            # first-touch pageable memory runs at a few GB/s
+            outs = [torch.empty(s, dtype=torch.float64, pin_memory=True).numpy() for s in shapes]
             ptrs = [C.c_void_p(o.ctypes.data) for o in outs]
         _capi.check(self.lib.ircur_get_strips(self.h, *ptrs))
         return outs  # C, R, S_rows, S_cols
