@@ -77,6 +77,17 @@ int ircur_prepare(ircur_ctx_t ctx, const void* D, int64_t ldd, int make_colmajor
 int ircur_prepare_sampled(ircur_ctx_t ctx, const void* D, int64_t ldd, int cover_sets,
                           int* all_finite, double* max_abs);
 
+/* The reference's index draws on the host, bit for bit: n_sets pairs
+ * I_s = unique(integers(0, n1, m_rows)), J_s = unique(integers(0, n2, m_cols))
+ * from a numpy PCG64 Generator whose state is pcg = {state lo, state hi,
+ * inc lo, inc hi, has_uint32, uinteger} (rng.bit_generator.state).  Sets are
+ * written sorted with strides m_rows / m_cols; counts per set.  pcg_out
+ * (optional) receives the state after the draws.  Host only (no device).
+ * Replaces sampling.py:93-104 in the order of solver.py:325-329, 362-364. */
+int ircur_draw_index_sets(const uint64_t* pcg, int64_t n1, int64_t n2, int m_rows, int m_cols,
+                          int n_sets, int64_t* rows, int32_t* row_counts, int64_t* cols,
+                          int32_t* col_counts, uint64_t* pcg_out);
+
 /* Upload the pre-generated index sets (host int64, strictly increasing),
  * n_sets consecutive (I_k, J_k) pairs packed with strides max_rows/max_cols.
  * The host draws them with the reference's numpy call sequence

@@ -100,14 +100,18 @@ class Context:
 
     def set_indices(self, sets) -> None:
         n = len(sets)
-        rows = np.zeros((n, self.max_rows), dtype=np.int64)
-        cols = np.zeros((n, self.max_cols), dtype=np.int64)
-        rc = np.zeros(n, dtype=np.int32)
-        cc = np.zeros(n, dtype=np.int32)
-        for s, (I, J) in enumerate(sets):
-            rows[s, :I.size] = I
-            cols[s, :J.size] = J
-            rc[s], cc[s] = I.size, J.size
+        pre = getattr(sets, "rows", None)
+        if pre is not None and pre.shape == (n, self.max_rows) and sets.cols.shape == (n, self.max_cols):
+            rows, cols, rc, cc = sets.rows, sets.cols, sets.row_counts, sets.col_counts
+        else:
+            rows = np.zeros((n, self.max_rows), dtype=np.int64)
+            cols = np.zeros((n, self.max_cols), dtype=np.int64)
+            rc = np.zeros(n, dtype=np.int32)
+            cc = np.zeros(n, dtype=np.int32)
+            for s, (I, J) in enumerate(sets):
+                rows[s, :I.size] = I
+                cols[s, :J.size] = J
+                rc[s], cc[s] = I.size, J.size
         p64 = C.POINTER(C.c_int64)
         p32 = C.POINTER(C.c_int32)
         _capi.check(self.lib.ircur_set_indices(self.h, n, rows.ctypes.data_as(p64), rc.ctypes.data_as(p32),

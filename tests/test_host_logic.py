@@ -100,3 +100,21 @@ def test_copy_plan(monkeypatch):
     assert _copy_plan(True, 200, 60, sets2, cfg) == (1, 0)
     monkeypatch.setenv("IRCUR_COLMAJOR", "0")
     assert _copy_plan(True, n, m, sets, cfg) == (0, 0)
+
+
+@pytest.mark.parametrize("shape,r,seed,stream", [((100000, 100000), 10, 1, 0), ((10000, 10000), 5, 7, 3),
+                                                 ((1, 1), 1, 0, 0), ((2, 3), 2, 5, 1), ((1000, 97), 4, 11, 0),
+                                                 ((25344, 1000), 2, 2, 0)])
+def test_c_draws_equal_numpy(shape, r, seed, stream):
+    """ircur_draw_index_sets (PCG64 + bounded Lemire + bitmap unique in C)
+    reproduces numpy's integers()/unique sequence exactly."""
+    from paper_2010_07422_b200.sampling import draw_index_sets_numpy
+    n1, n2 = shape
+    m1, m2 = ir.sample_count(n1, r, 4.0), ir.sample_count(n2, r, 4.0)
+    s = ir.RngSeed(seed, stream)
+    fast = ir.draw_index_sets(n1, n2, m1, m2, s, 60)
+    ref = draw_index_sets_numpy(n1, n2, m1, m2, s, 60)
+    for (a, b), (c, d) in zip(fast, ref):
+        np.testing.assert_array_equal(a, c)
+        np.testing.assert_array_equal(b, d)
+        assert a.dtype == np.int64 and b.dtype == np.int64
