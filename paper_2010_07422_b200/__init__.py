@@ -14,6 +14,7 @@ from .solver import (
     materialize,
     materialize_device,
     solve,
+    solve_batch,
     solve_device,
     threshold_at,
 )
@@ -22,7 +23,7 @@ from .types import CurFactors, PinvFactor, SolverConfig, SolverTrace, SparseEsti
 __all__ = [
     "Context", "CurFactors", "DeviceResult", "IndexSet", "PinvFactor", "RngSeed", "SolverConfig",
     "SolverTrace", "SparseEstimate", "SvdFactors", "clear_cache", "draw_index_sets", "materialize",
-    "materialize_device", "sample_count", "sample_indices", "solve", "solve_device", "threshold_at",
+    "materialize_device", "sample_count", "sample_indices", "solve", "solve_batch", "solve_device", "threshold_at",
 ]
 
 __version__ = "0.1.0"

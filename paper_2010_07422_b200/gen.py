@@ -70,3 +70,41 @@ def baseline_problem_device(n1: int, n2: int, rank: int, alpha: float, seed: int
     D = torch.empty((nrows, n2), dtype=dtype, device=dev)
     _call(D.data_ptr(), dt, n2, n1, n2, row0, nrows, rank, Wd, Vd, alpha, amp * a, pcg, stream)
     return D, mx, a
+
+
+def video_problem(frames: int = 1000, height: int = 144, width: int = 176, rank: int = 2, n_blocks: int = 12,
+                  block: int = 16, seed: int = 0, dtype=np.float32):
+    """BASELINE.json cfg3: a video-like matrix, one frame per
+    column, pixel (x, y) at row y + x * height (the reference's frame
+    layout, mio.py:162-174).  Low-rank background = `rank` Gaussian-blurred
+    (sigma = 8 px) N(0,1) fields times per-frame weights following random
+    walks (step 0.01); sparse foreground = `n_blocks` moving block x block
+    squares of U[0.5, 1] intensity with constant velocities |v| <= 3
+    px/frame, wrapping at the borders.  Host numpy (a data source for
+    parity tests and the cfg3 bench line, not part of the hot path).
+    Returns (D, L, S)."""
+    from scipy.ndimage import gaussian_filter
+
+    rng = np.random.default_rng(seed)
+    fields = np.stack([gaussian_filter(rng.standard_normal((width, height)), sigma=8.0, mode="wrap")
+                       for _ in range(rank)])
+    fields /= np.abs(fields).max(axis=(1, 2), keepdims=True)
+    F = fields.reshape(rank, width * height).T          # row = y + x * height
+    w = 1.0 + np.cumsum(0.01 * rng.standard_normal((rank, frames)), axis=1)
+    L = F @ w
+    S = np.zeros((width * height, frames))
+    pos = rng.uniform(0, [width, height], size=(n_blocks, 2))
+    ang = rng.uniform(0, 2 * np.pi, n_blocks)
+    spd = rng.uniform(0.5, 3.0, n_blocks)
+    vel = np.stack([spd * np.cos(ang), spd * np.sin(ang)], axis=1)
+    inten = rng.uniform(0.5, 1.0, n_blocks)
+    xs = np.arange(block)
+    for t in range(frames):
+        p = (pos + t * vel)
+        for b in range(n_blocks):
+            x = (int(p[b, 0]) + xs) % width
+            y = (int(p[b, 1]) + xs) % height
+            rows = (y[None, :] + x[:, None] * height).ravel()
+            S[rows, t] = inten[b]
+    D = (L + S).astype(dtype)
+    return D, L, S

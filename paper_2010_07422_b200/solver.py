@@ -31,7 +31,7 @@ from . import _capi
 from .sampling import IndexSet, draw_index_sets, sample_count
 from .types import CurFactors, PinvFactor, SolverConfig, SolverTrace, SparseEstimate
 
-__all__ = ["solve", "solve_device", "materialize", "materialize_device", "threshold_at",
+__all__ = ["solve", "solve_device", "solve_batch", "materialize", "materialize_device", "threshold_at",
            "Context", "DeviceResult"]
 
 
@@ -256,12 +256,20 @@ def _device_view(ptr: int, n: int, typestr: str, device: int) -> torch.Tensor:
 
 _CACHE: "OrderedDict[tuple, Context]" = OrderedDict()
 _CACHE_MAX = 4
+_CACHE_LOCK = __import__("threading").RLock()
 
 
 def _context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0=0,
              local_rows=None) -> Context:
     local_rows = n1 if local_rows is None else local_rows
     key = (device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0, local_rows)
+    with _CACHE_LOCK:
+        return _context_locked(key, device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0,
+                               local_rows)
+
+
+def _context_locked(key, device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0,
+                    local_rows) -> Context:
     ctx = _CACHE.get(key)
     if ctx is not None:
         _CACHE.move_to_end(key)
@@ -282,9 +290,10 @@ def _context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0
 
 
 def clear_cache() -> None:
-    for _, ctx in _CACHE.items():
-        ctx.close()
-    _CACHE.clear()
+    with _CACHE_LOCK:
+        for _, ctx in _CACHE.items():
+            ctx.close()
+        _CACHE.clear()
 
 
 # ------------------------------------------------------------ device input
@@ -532,6 +541,39 @@ def solve(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=
     last = (res.trace.iterations - 1) if res.cfg.mode == "resampled" else 0
     cur, sparse = _host_results(res.ctx, last, n1, n2, res.handle)
     return cur, sparse, res.trace
+
+
+def solve_batch(Ds, configs, *, device=None, streams: int = 4, compute_dtype=None, colmajor="auto"):
+    """Independent problems (BASELINE.json cfg4: 512 x 2000^2) solved
+    concurrently: `streams` host threads each drive their own CUDA stream and
+    library context (ctypes releases the GIL inside the library), so the
+    small per-problem kernels of several problems share the GPU.  Returns
+    the list of (CurFactors, SparseEstimate, SolverTrace) in input order,
+    bitwise equal to sequential solves."""
+    import concurrent.futures as cf
+
+    global _CACHE_MAX
+    Ds = list(Ds)
+    configs = list(configs) if isinstance(configs, (list, tuple)) else [configs] * len(Ds)
+    if len(configs) != len(Ds):
+        raise ValueError("need one config per problem")
+    dev = device if device is not None else torch.cuda.current_device()
+    nstreams = max(1, min(streams, len(Ds)))
+    pool_streams = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
+    with _CACHE_LOCK:
+        _CACHE_MAX = max(_CACHE_MAX, nstreams + 2)
+    out = [None] * len(Ds)
+
+    def worker(w):
+        st = pool_streams[w]
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            for i in range(w, len(Ds), nstreams):
+                out[i] = solve(Ds[i], configs[i], device=dev, compute_dtype=compute_dtype, colmajor=colmajor)
+            st.synchronize()
+
+    with cf.ThreadPoolExecutor(nstreams) as ex:
+        list(ex.map(worker, range(nstreams)))
+    return out
 
 
 # ------------------------------------------------------------ materialise
