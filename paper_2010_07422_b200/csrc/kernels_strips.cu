@@ -16,6 +16,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels_iter.cuh"
 #include "launchers.cuh"
 
@@ -502,6 +504,17 @@ cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, in
   const int tiles = a.s[0].tiles + a.s[1].tiles;
   if (ncta_out) *ncta_out = 0;
   if (tiles == 0) return cudaSuccess;
+  if constexpr (sizeof(T) == 4) {
+    static const bool v1 = [] {
+      const char* e = std::getenv("IRCUR_STRIPS_V1");  // A/B switch: force the cluster kernel
+      return e && e[0] == '1';
+    }();
+    const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
+    if (!v1 && aligned) {
+      const cudaError_t e = launch_strips2(a, R, num_sms, ncta_out, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
   cudaError_t e = cudaErrorInvalidValue;
   IRCUR_DISPATCH_RANK(R, RR, e = launch_strips_r<T, RR>(a, cs, num_sms, st));
   if (ncta_out) {

@@ -44,6 +44,10 @@ template <typename T> int strips_pick_cluster(int nk_max, int R);
 template <typename T>
 cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, int* ncta_out, cudaStream_t st);
 int strips_tx();
+// fp32 two-group kernel (kernels_strips2.cu); cudaErrorNotSupported when the
+// sampled lines do not fit its shared-memory stage
+cudaError_t launch_strips2(const StripsArgs<float>& a, int R, int num_sms, int* ncta_out, cudaStream_t st);
+size_t strips2_smem_bytes(int maxl, int R);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
 template <typename T, typename O>
