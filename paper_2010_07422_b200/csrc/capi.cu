@@ -185,7 +185,10 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   // Ritz-residual target relative to lambda_1: round-off floor, relaxed in
   // early iterations in proportion to e_{k-1} (an SVD perturbation delta
   // moves e_k by ~delta/e_k relative)
-  sa.tol = sizeof(T) == 8 ? 2e-14 : 1e-11;
+  // fp32 data: the strips carry ~6e-8 relative round-off, and a 1e-6
+  // lambda_1 floor leaves L within that noise of the 1e-11 result (measured
+  // at cfg2/cfg5: 8e-8 relative, same iterations) for 20% fewer steps
+  sa.tol = sizeof(T) == 8 ? 2e-14 : 1e-6;
   sa.tol_scale = sizeof(T) == 8 ? 1e-11 : 1e-8;
   if (const char* ev = std::getenv(sizeof(T) == 8 ? "IRCUR_SVD_TOL64" : "IRCUR_SVD_TOL32"))  // tuning
     sa.tol = std::atof(ev);
