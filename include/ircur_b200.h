@@ -96,6 +96,14 @@ int ircur_set_indices(ircur_ctx_t ctx, int n_sets, const int64_t* rows,
                       const int32_t* row_counts, const int64_t* cols,
                       const int32_t* col_counts);
 
+/* Append n_more index sets after the uploaded ones (same layout as
+ * ircur_set_indices); the sampled column-major copy is left as is (later
+ * sets extend it on demand).  Lets the host draw the tail of the sequence
+ * while the prep pass runs. */
+int ircur_append_indices(ircur_ctx_t ctx, int n_more, const int64_t* rows,
+                         const int32_t* row_counts, const int64_t* cols,
+                         const int32_t* col_counts);
+
 /* den = ||D(I_s,:)||_F^2, ||D(:,J_s)||_F^2 partial sums of the LOCAL rows
  * for index set s (fp64; host-blocking).  Replaces the pre-loop frob_norm
  * pair of solver.py:331-333 used by the den == 0 early exit (:335-341). */

@@ -36,6 +36,7 @@ PROTOTYPES = [
     ("ircur_draw_index_sets", _i, [_pu64, _i64, _i64, _i, _i, _i, _pi64, C.POINTER(C.c_int32), _pi64,
                                    C.POINTER(C.c_int32), _pu64]),
     ("ircur_set_indices", _i, [_vp, _i, _pi64, C.POINTER(C.c_int32), _pi64, C.POINTER(C.c_int32)]),
+    ("ircur_append_indices", _i, [_vp, _i, _pi64, C.POINTER(C.c_int32), _pi64, C.POINTER(C.c_int32)]),
     ("ircur_slab_sqnorms", _i, [_vp, _i, _pd, _pd]),
     ("ircur_run", _i, [_vp, _pd, _d, _i, _i, _pi, _pi, _pd, _pf]),
     ("ircur_iterate", _i, [_vp, _i, _i, _d, _pd]),

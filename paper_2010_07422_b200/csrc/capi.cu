@@ -63,6 +63,7 @@ struct ircur_ctx {
   int* d_rows = nullptr;
   int* d_cols = nullptr;
   int n_sets = 0;
+  int sets_cap = 0;          // index sets the device arrays hold
   std::vector<int> h_row_cnt, h_col_cnt, h_row_lo;  // h_row_lo: first local entry in set
   std::vector<int> h_row_loc_cnt;
   void* Pt[2] = {nullptr, nullptr};
@@ -570,17 +571,21 @@ int ircur_prepare_sampled(ircur_ctx_t c, const void* D, int64_t ldd, int cover_s
   return IRCUR_OK;
 }
 
-int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int32_t* row_counts,
-                      const int64_t* cols, const int32_t* col_counts) {
-  if (!c || n_sets < 1 || !rows || !cols || !row_counts || !col_counts)
-    return fail(IRCUR_EINVAL, "bad index-set arguments");
-  IR_CUDA(cudaSetDevice(c->device));
-  std::vector<int> hr((size_t)n_sets * c->max_rows, 0), hc((size_t)n_sets * c->max_cols, 0);
-  c->h_row_cnt.assign(n_sets, 0);
-  c->h_col_cnt.assign(n_sets, 0);
-  c->h_row_lo.assign(n_sets, 0);
-  c->h_row_loc_cnt.assign(n_sets, 0);
-  for (int s = 0; s < n_sets; ++s) {
+}  // extern "C"
+
+namespace {
+
+// Validate and upload index sets [first, first + n) (host int64, strictly
+// increasing, strides max_rows / max_cols); device arrays grow as needed.
+int upload_sets(ircur_ctx* c, int first, int n, const int64_t* rows, const int32_t* row_counts,
+                const int64_t* cols, const int32_t* col_counts) {
+  std::vector<int> hr((size_t)n * c->max_rows, 0), hc((size_t)n * c->max_cols, 0);
+  const int total = first + n;
+  c->h_row_cnt.resize(total, 0);
+  c->h_col_cnt.resize(total, 0);
+  c->h_row_lo.resize(total, 0);
+  c->h_row_loc_cnt.resize(total, 0);
+  for (int s = 0; s < n; ++s) {
     const int mr = row_counts[s], mc = col_counts[s];
     if (mr < 1 || mr > c->max_rows || mc < 1 || mc > c->max_cols)
       return fail(IRCUR_EINVAL, "index set size out of range");
@@ -601,30 +606,62 @@ int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int3
         return fail(IRCUR_EINVAL, "column indices must be strictly increasing and in range");
       hc[(size_t)s * c->max_cols + j] = (int)v;
     }
-    c->h_row_cnt[s] = mr;
-    c->h_col_cnt[s] = mc;
-    c->h_row_lo[s] = lo < 0 ? 0 : lo;
-    c->h_row_loc_cnt[s] = cnt;
+    c->h_row_cnt[first + s] = mr;
+    c->h_col_cnt[first + s] = mc;
+    c->h_row_lo[first + s] = lo < 0 ? 0 : lo;
+    c->h_row_loc_cnt[first + s] = cnt;
   }
-  if (n_sets > c->n_sets) {
+  cudaStream_t st = c->stream;
+  if (total > c->sets_cap) {
+    const int cap = std::max(total, c->max_iter);
+    int *nr = nullptr, *nc = nullptr;
+    IR_CUDA(cudaMalloc(&nr, (size_t)cap * c->max_rows * sizeof(int)));
+    IR_CUDA(cudaMalloc(&nc, (size_t)cap * c->max_cols * sizeof(int)));
+    if (first > 0 && c->d_rows) {
+      IR_CUDA(cudaMemcpyAsync(nr, c->d_rows, (size_t)first * c->max_rows * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      IR_CUDA(cudaMemcpyAsync(nc, c->d_cols, (size_t)first * c->max_cols * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    }
+    IR_CUDA(cudaStreamSynchronize(st));
     if (c->d_rows) cudaFree(c->d_rows);
     if (c->d_cols) cudaFree(c->d_cols);
-    c->d_rows = nullptr;
-    c->d_cols = nullptr;
-    IR_CUDA(cudaMalloc(&c->d_rows, hr.size() * sizeof(int)));
-    IR_CUDA(cudaMalloc(&c->d_cols, hc.size() * sizeof(int)));
+    c->d_rows = nr;
+    c->d_cols = nc;
+    c->sets_cap = cap;
   }
-  c->n_sets = n_sets;
-  c->h_cols = hc;
+  c->h_cols.resize((size_t)total * c->max_cols, 0);
+  std::memcpy(c->h_cols.data() + (size_t)first * c->max_cols, hc.data(), hc.size() * sizeof(int));
+  c->n_sets = total;
+  IR_CUDA(cudaMemcpyAsync(c->d_rows + (size_t)first * c->max_rows, hr.data(), hr.size() * sizeof(int),
+                          cudaMemcpyHostToDevice, st));
+  IR_CUDA(cudaMemcpyAsync(c->d_cols + (size_t)first * c->max_cols, hc.data(), hc.size() * sizeof(int),
+                          cudaMemcpyHostToDevice, st));
+  IR_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+  return IRCUR_OK;
+}
 
+}  // namespace
+
+extern "C" {
+
+int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int32_t* row_counts,
+                      const int64_t* cols, const int32_t* col_counts) {
+  if (!c || n_sets < 1 || !rows || !cols || !row_counts || !col_counts)
+    return fail(IRCUR_EINVAL, "bad index-set arguments");
+  IR_CUDA(cudaSetDevice(c->device));
   if (c->dt_mode == 2) {  // the sampled copy belongs to the previous sets
     c->dt_mode = 0;
     c->covered = 0;
   }
-  IR_CUDA(cudaMemcpyAsync(c->d_rows, hr.data(), hr.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-  IR_CUDA(cudaMemcpyAsync(c->d_cols, hc.data(), hc.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-  IR_CUDA(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
-  return IRCUR_OK;
+  c->n_sets = 0;
+  return upload_sets(c, 0, n_sets, rows, row_counts, cols, col_counts);
+}
+
+int ircur_append_indices(ircur_ctx_t c, int n_more, const int64_t* rows, const int32_t* row_counts,
+                         const int64_t* cols, const int32_t* col_counts) {
+  if (!c || n_more < 1 || !rows || !cols || !row_counts || !col_counts || c->n_sets < 1)
+    return fail(IRCUR_EINVAL, "bad index-set arguments (append needs uploaded sets)");
+  IR_CUDA(cudaSetDevice(c->device));
+  return upload_sets(c, c->n_sets, n_more, rows, row_counts, cols, col_counts);
 }
 
 int ircur_slab_sqnorms(ircur_ctx_t c, int set, double* rows_sq, double* cols_sq) {

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _capi
-from .sampling import IndexSet, draw_index_sets, sample_count
+from .sampling import IndexSet, draw_index_sets, draw_index_sets_from, pcg_words, sample_count
 from .types import CurFactors, PinvFactor, SolverConfig, SolverTrace, SparseEstimate
 
 __all__ = ["solve", "solve_device", "solve_batch", "materialize", "materialize_device", "threshold_at",
@@ -117,6 +117,15 @@ class Context:
         _capi.check(self.lib.ircur_set_indices(self.h, n, rows.ctypes.data_as(p64), rc.ctypes.data_as(p32),
                                                cols.ctypes.data_as(p64), cc.ctypes.data_as(p32)))
         self.sets = sets
+
+    def append_indices(self, sets) -> None:
+        """Upload more sets after the current ones (a DrawnSets)."""
+        p64, p32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+        _capi.check(self.lib.ircur_append_indices(self.h, len(sets), sets.rows.ctypes.data_as(p64),
+                                                  sets.row_counts.ctypes.data_as(p32),
+                                                  sets.cols.ctypes.data_as(p64),
+                                                  sets.col_counts.ctypes.data_as(p32)))
+        self.sets = list(self.sets) + list(sets)
 
     def slab_sqnorms(self, s: int) -> tuple[float, float]:
         a, b = C.c_double(), C.c_double()
@@ -351,6 +360,11 @@ class _Ticker:
             self.t = t
 
 
+def _cover_estimate(cfg: SolverConfig) -> int:
+    """Iterations the threshold schedule needs to reach eps: ceil(log eps / log gamma)."""
+    return int(np.ceil(np.log(cfg.eps) / np.log(cfg.gamma)))
+
+
 def _copy_plan(colmajor, n2: int, m_cols: int, sets, cfg: SolverConfig) -> tuple[int, int]:
     """Which column-major copy the prep pass builds: (mode, cover) with mode
     0 = none, 1 = full copy of D, 2 = only the columns of the J sets
@@ -369,8 +383,7 @@ def _copy_plan(colmajor, n2: int, m_cols: int, sets, cfg: SolverConfig) -> tuple
     if cfg.mode == "fixed":
         cover = 1
     else:
-        est = int(np.ceil(np.log(cfg.eps) / np.log(cfg.gamma))) + 8
-        cover = max(1, min(len(sets), est))
+        cover = max(1, min(len(sets), _cover_estimate(cfg) + 8))
     if isinstance(colmajor, str) and colmajor.startswith("sampled"):
         if ":" in colmajor:  # "sampled:K" covers the first K sets (tests of the extension path)
             cover = max(1, min(len(sets), int(colmajor.split(":")[1])))
@@ -426,15 +439,40 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     m_cols = sample_count(n2, cfg.rank, cfg.c_cols)
     resampled = cfg.mode == "resampled"
     n_sets = cfg.max_iter if resampled else 1
-    sets = draw_index_sets(n1, n2, m_rows, m_cols, cfg.seed, n_sets)
+    # Draw the sets the prep pass needs first; the rest of the sequence is
+    # drawn by a worker thread while the (host-blocking) prep pass runs.
+    n_first = min(n_sets, _cover_estimate(cfg) + 8) if resampled else n_sets
+    pcg = pcg_words(cfg.seed) if max(n1, n2) <= 2**32 else None
+    if pcg is None:
+        sets, pcg_next = draw_index_sets(n1, n2, m_rows, m_cols, cfg.seed, n_sets), None
+        n_first = n_sets
+    else:
+        sets, pcg_next = draw_index_sets_from(pcg, n1, n2, m_rows, m_cols, n_first)
     tick("draw")
     stream = torch.cuda.current_stream(dev).cuda_stream
     ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
     ctx.set_indices(sets)
     tick("set_indices")
     cm, cover = _copy_plan(colmajor, n2, m_cols, sets, cfg)
-    max_abs = ctx.prepare(Dd, cm, cover)  # ValueError on NaN/Inf (matcore.py:75-76)
+    rest = None
+    if n_first < n_sets:
+        import threading
+
+        box = {}
+        worker = threading.Thread(target=lambda: box.update(
+            r=draw_index_sets_from(pcg_next, n1, n2, m_rows, m_cols, n_sets - n_first)[0]))
+        worker.start()
+    try:
+        max_abs = ctx.prepare(Dd, cm, cover)  # ValueError on NaN/Inf (matcore.py:75-76)
+    finally:
+        if n_first < n_sets:
+            worker.join()
+            rest = box["r"]
     tick("prepare")
+    if rest is not None:
+        ctx.append_indices(rest)
+        sets.extend_drawn(rest)
+        tick("append")
     rows0, cols0 = sets[0]
     a, b = ctx.slab_sqnorms(0)
     tick("slab")

@@ -118,3 +118,20 @@ def test_c_draws_equal_numpy(shape, r, seed, stream):
         np.testing.assert_array_equal(a, c)
         np.testing.assert_array_equal(b, d)
         assert a.dtype == np.int64 and b.dtype == np.int64
+
+
+def test_c_draws_continue_from_state():
+    """Drawing n0 sets and then the rest from the returned PCG64 state gives
+    the sequence of one call (the overlapped draws of solve_device)."""
+    from paper_2010_07422_b200.sampling import draw_index_sets_from, pcg_words
+    n, r = 50000, 7
+    m = ir.sample_count(n, r, 4.0)
+    s = ir.RngSeed(3, 2)
+    whole = ir.draw_index_sets(n, n, m, m, s, 40)
+    first, st = draw_index_sets_from(pcg_words(s), n, n, m, m, 17)
+    rest, _ = draw_index_sets_from(st, n, n, m, m, 23)
+    first.extend_drawn(rest)
+    assert len(first) == 40 and first.rows.shape == (40, m)
+    for (a, b), (c, d) in zip(first, whole):
+        np.testing.assert_array_equal(a, c)
+        np.testing.assert_array_equal(b, d)
