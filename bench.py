@@ -228,7 +228,7 @@ def run_ours(args):
             "other": ms_per_step - (strip_ms + svd_ms + core_ms) / len(results)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "strips_kernel", "avg_launch_us": strip_ms / n_strip * 1e3,
+                     "kernel": "strips2_kernel", "avg_launch_us": strip_ms / n_strip * 1e3,
                      "bytes_per_launch": strip_bytes / n_strip},
         "gpu_launches": launches,
         "clocks": clk.summary(),
