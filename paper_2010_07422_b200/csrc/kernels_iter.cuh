@@ -61,6 +61,8 @@ struct StripsArgs {
   double* partials;                            // per CTA: {den, res}
   const int* done;
   long long* dbg;                              // optional per-phase clock64 totals (CTA 0, thread 0)
+  int prefetch_dist;                           // strips3: tiles ahead prefetched into L2
+  int desync_ns;                               // strips3: start delay of odd CTAs
 };
 
 // ------------------------------------------------------------- finalize

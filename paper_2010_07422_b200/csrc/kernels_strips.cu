@@ -505,12 +505,20 @@ cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, in
   if (ncta_out) *ncta_out = 0;
   if (tiles == 0) return cudaSuccess;
   if constexpr (sizeof(T) == 4) {
-    static const bool v1 = [] {
-      const char* e = std::getenv("IRCUR_STRIPS_V1");  // A/B switch: force the cluster kernel
-      return e && e[0] == '1';
+    // fp32: the 64-position single-stage kernel, else the two-group
+    // 32-position kernel, else this cluster kernel.  IRCUR_STRIPS_VER=1|2|3
+    // caps the choice (A/B measurements).
+    static const int ver = [] {
+      const char* e = std::getenv("IRCUR_STRIPS_VER");
+      if (!e) e = std::getenv("IRCUR_STRIPS_V1") ? "1" : nullptr;
+      return e ? std::atoi(e) : 3;
     }();
     const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
-    if (!v1 && aligned) {
+    if (ver >= 3 && aligned) {
+      const cudaError_t e = launch_strips3(a, R, num_sms, ncta_out, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
+    if (ver >= 2 && aligned) {
       const cudaError_t e = launch_strips2(a, R, num_sms, ncta_out, st);
       if (e != cudaErrorNotSupported) return e;
     }

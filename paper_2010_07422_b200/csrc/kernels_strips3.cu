@@ -1,0 +1,306 @@
+// Fused row + column strip kernel, fp32, 64-position tiles (sm_100a).
+//
+// Same per-entry semantics as kernels_strips.cu / kernels_strips2.cu
+// (Phase I/II, factor sums with the core overrides, stopping residual;
+// solver.py:375-400).  What bounds those kernels is shared-memory wavefronts,
+// dominated by the per-line vectors A | W | Res that every warp broadcasts
+// for each line it processes (LDS.128 broadcast = 2 wavefronts, 8 bytes
+// each).  Here each lane owns TWO positions (x and x + 32 of a 64-position
+// tile, packed in FFMA2 pairs), so every line-vector load feeds 2x the
+// entries of kernels_strips2.cu.  The price is shared memory: all sampled
+// lines of a 64-position tile are resident in ONE single-buffered stage per
+// CTA (16 warps on the same tile), so the next tile is prefetched into L2
+// (cp.async.bulk.prefetch) while the current one is computed.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "kernels_iter.cuh"
+#include "launchers.cuh"
+
+namespace ircur {
+
+constexpr int kS3NT = 512;
+constexpr int kS3NW = kS3NT / 32;
+constexpr int kS3TX = 64;  // positions per tile (x and x + 32 per lane)
+
+struct Strips3Layout {
+  int RP, maxp;
+  size_t lvec, stage, bst, omt, lptr, red, fnew, dred, total;
+};
+
+__host__ __device__ inline size_t al3(size_t x) { return (x + 127) & ~size_t(127); }
+
+__host__ __device__ inline Strips3Layout strips3_layout(int maxl, int R) {
+  Strips3Layout L;
+  L.RP = R + (R & 1);
+  L.maxp = (maxl + 1) / 2;
+  size_t off = 0;
+  L.lvec = off; off = al3(off + (size_t)L.maxp * 3 * L.RP * sizeof(float2));
+  L.stage = off; off = al3(off + (size_t)2 * L.maxp * kS3TX * sizeof(float));
+  L.bst = off; off = al3(off + (size_t)R * kS3TX * sizeof(float));
+  L.omt = off; off = al3(off + (size_t)kS3TX * sizeof(int));
+  L.lptr = off; off = al3(off + (size_t)2 * (2 * L.maxp + R) * sizeof(void*));
+  L.red = off; off = al3(off + (size_t)kS3NW * R * kS3TX * sizeof(float));
+  L.fnew = off; off = al3(off + (size_t)R * kS3TX * sizeof(float));
+  L.dred = off; off = al3(off + 4 * kS3NW * sizeof(double));
+  L.total = off;
+  return L;
+}
+
+__device__ __forceinline__ uint32_t s3_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int R>
+__global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant__ StripsArgs<float> a) {
+  if (*a.done) return;
+  const Strips3Layout L = strips3_layout(a.maxl, R);
+  constexpr int RPc = R + (R & 1);
+  extern __shared__ __align__(128) unsigned char sm[];
+  float2* lvec = reinterpret_cast<float2*>(sm + L.lvec);
+  float* stage = reinterpret_cast<float*>(sm + L.stage);
+  float* bst = reinterpret_cast<float*>(sm + L.bst);
+  int* omt = reinterpret_cast<int*>(sm + L.omt);
+  const float** lptr = reinterpret_cast<const float**>(sm + L.lptr);
+  float* red = reinterpret_cast<float*>(sm + L.red);
+  float* fnew = reinterpret_cast<float*>(sm + L.fnew);
+  double* dred = reinterpret_cast<double*>(sm + L.dred);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const float zt = a.zt;
+  const bool rec = a.dbg && blockIdx.x == 0 && tid == 0;
+  long long tpc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tq = clock64();
+#define SPH(k) do { if (rec) { const long long _t = clock64(); tpc[k] += _t - tq; tq = _t; } } while (0)
+
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {  // segment sources: lines, then the R rows of the old factor
+    const StripDesc<float>& s = a.s[q];
+    float const** lp = lptr + q * (2 * L.maxp + R);
+    for (int e = tid; e < s.nk + R; e += kS3NT)
+      lp[e] = e < s.nk ? s.src + (int64_t)(s.lines[e] - s.line_off) * s.line_stride : s.Bold + (int64_t)(e - s.nk) * s.ldb;
+  }
+  double den_acc[2] = {0.0, 0.0}, res_acc[2] = {0.0, 0.0};
+  const int tiles0 = a.s[0].tiles;
+  const int total = tiles0 + a.s[1].tiles;
+  // L2 prefetch of a whole tile (its line segments and factor rows)
+  auto prefetch = [&](int t) {
+    if (t >= total) return;
+    const int q = t < tiles0 ? 0 : 1;
+    const StripDesc<float>& s = a.s[q];
+    const int x0 = (t - (q ? tiles0 : 0)) * kS3TX;
+    const int n = s.npos - x0 < kS3TX ? s.npos - x0 : kS3TX;
+    const uint32_t bytes = (uint32_t)((n * 4 + 15) & ~15);
+    const float* const* lp = lptr + q * (2 * L.maxp + R);
+    for (int v = tid; v < s.nk + R; v += kS3NT)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lp[v] + x0), "r"(bytes) : "memory");
+  };
+  __syncthreads();
+  for (int d = 1; d < a.prefetch_dist; ++d) prefetch((int)blockIdx.x + d * (int)gridDim.x);
+  if (a.desync_ns > 0 && (blockIdx.x & 1)) __nanosleep(a.desync_ns);  // stagger the tile phases
+  int cur = -1;
+  for (int t = (int)blockIdx.x; t < total; t += (int)gridDim.x) {
+    const int q = t < tiles0 ? 0 : 1;
+    const StripDesc<float>& s = a.s[q];
+    const int nl = s.nk, np = (nl + 1) / 2, nl2 = 2 * np;
+    const int mode = s.mode;
+    const int x0 = (t - (q ? tiles0 : 0)) * kS3TX;
+    const float* const* lp = lptr + q * (2 * L.maxp + R);
+    if (q != cur) {  // per-pair line vectors of this strip: (A | W | Res)[t] for lines 2kp, 2kp+1
+      for (int e = tid; e < np * 3 * RPc; e += kS3NT) {
+        const int kp = e / (3 * RPc), rem = e - kp * 3 * RPc, v = rem / RPc, tt = rem - v * RPc;
+        const float* sv = v == 0 ? s.lineA : (v == 1 ? s.lineW : s.lineRes);
+        const int k0 = 2 * kp, k1 = k0 + 1;
+        float2 val = make_float2(0.f, 0.f);
+        if (tt < R) {
+          val.x = sv[(int64_t)k0 * R + tt];
+          if (k1 < nl) val.y = sv[(int64_t)k1 * R + tt];
+        }
+        lvec[e] = val;
+      }
+      cur = q;
+    }
+    SPH(6);
+    // ---- stage the tile: 16 x 16-byte chunks per 256-byte line segment
+    {
+      const int ch = tid & 15;
+      const int pos = x0 + ch * 4;
+      const int rem = s.npos - pos;
+      const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
+      const int sp = bytes ? pos : x0;
+      for (int v = tid >> 4; v < nl2 + R; v += kS3NT / 16) {
+        float* dst = v < nl2 ? stage + (size_t)v * kS3TX : bst + (size_t)(v - nl2) * kS3TX;
+        const float* src = v < nl ? lp[v] : (v < nl2 ? lp[0] : lp[nl + (v - nl2)]);
+        const int b = v < nl || v >= nl2 ? bytes : 0;  // the padding line of an odd count reads zeros
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s3_smem(dst + ch * 4)),
+                     "l"(src + sp), "r"(b)
+                     : "memory");
+      }
+      if (tid < 16) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s3_smem(omt + ch * 4)),
+                     "l"(s.omap + sp), "r"(bytes)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    if (a.prefetch_dist > 0) prefetch(t + a.prefetch_dist * (int)gridDim.x);
+    SPH(0);
+    Pair<float> b[R];
+#pragma unroll
+    for (int tt = 0; tt < R; ++tt) b[tt].v = make_float2(bst[tt * kS3TX + lane], bst[tt * kS3TX + lane + 32]);
+    // ---- pass 1: Phase I/II in place + factor partials (positions x, x + 32 per FFMA2)
+    Pair<float> acc[R];
+#pragma unroll
+    for (int tt = 0; tt < R; ++tt) acc[tt] = Pair<float>::splat(0.f);
+    Pair<float> den = Pair<float>::splat(0.f);
+    const bool accum = mode != kStripFinish;
+    for (int kp = w; kp < np; kp += kS3NW) {
+      const float2* va = lvec + (size_t)kp * 3 * RPc;
+      float* c0 = stage + (size_t)(2 * kp) * kS3TX + lane;
+      float* c1 = c0 + kS3TX;
+      Pair<float> d0, d1;
+      d0.v = make_float2(c0[0], c0[32]);
+      d1.v = make_float2(c1[0], c1[32]);
+      float2 av = va[0];
+      Pair<float> l0, l1;
+      l0.v = __fmul2_rn(make_float2(av.x, av.x), b[0].v);
+      l1.v = __fmul2_rn(make_float2(av.y, av.y), b[0].v);
+#pragma unroll
+      for (int tt = 1; tt < R; ++tt) {
+        av = va[tt];
+        l0.v = __ffma2_rn(make_float2(av.x, av.x), b[tt].v, l0.v);
+        l1.v = __ffma2_rn(make_float2(av.y, av.y), b[tt].v, l1.v);
+      }
+      const Pair<float> e0 = keep_pair(d0, l0, zt);
+      const Pair<float> e1 = keep_pair(d1, l1, zt);
+      den = pfma(d0, d0, den);
+      den = pfma(d1, d1, den);
+      c0[0] = e0.v.x;
+      c0[32] = e0.v.y;
+      c1[0] = e1.v.x;
+      c1[32] = e1.v.y;
+      if (accum) {
+        const float2* vw = va + RPc;
+#pragma unroll
+        for (int tt = 0; tt < R; ++tt) {
+          const float2 wv = vw[tt];
+          acc[tt].v = __ffma2_rn(make_float2(wv.x, wv.x), e0.v, acc[tt].v);
+          acc[tt].v = __ffma2_rn(make_float2(wv.y, wv.y), e1.v, acc[tt].v);
+        }
+      }
+    }
+    SPH(1);
+    if (accum) {
+      den_acc[q] += (double)den.v.x + (double)den.v.y;
+#pragma unroll
+      for (int tt = 0; tt < R; ++tt) {
+        red[(w * R + tt) * kS3TX + lane] = acc[tt].v.x;
+        red[(w * R + tt) * kS3TX + lane + 32] = acc[tt].v.y;
+      }
+    }
+    __syncthreads();
+    SPH(2);
+    // ---- factor sums over the 16 warps (fixed order) + overrides
+    const bool ovr = mode != kStripPartial;
+    for (int o = tid; o < R * kS3TX; o += kS3NT) {
+      const int tt = o / kS3TX, x = o - tt * kS3TX;
+      const int e = (ovr && x0 + x < s.npos) ? omt[x] : -1;
+      float v;
+      if (e >= 0) {
+        v = s.otherF[(int64_t)e * R + tt];
+      } else if (accum) {
+        v = red[tt * kS3TX + x];
+#pragma unroll
+        for (int ww = 1; ww < kS3NW; ++ww) v += red[(ww * R + tt) * kS3TX + x];
+      } else {
+        v = x0 + x < s.npos ? s.Fsrc[(int64_t)tt * s.ldfs + x0 + x] : 0.f;
+      }
+      fnew[o] = v;
+      if (x0 + x < s.npos) s.Fnew[(int64_t)tt * s.ldf + x0 + x] = v;
+    }
+    __syncthreads();
+    SPH(3);
+    if (mode != kStripPartial) {
+      // ---- pass 2: stopping residual on the thresholded tile
+      Pair<float> f[R];
+#pragma unroll
+      for (int tt = 0; tt < R; ++tt) f[tt].v = make_float2(fnew[tt * kS3TX + lane], fnew[tt * kS3TX + lane + 32]);
+      Pair<float> res = Pair<float>::splat(0.f);
+      for (int kp = w; kp < np; kp += kS3NW) {
+        const float2* vr = lvec + (size_t)kp * 3 * RPc + 2 * RPc;
+        const float* c0 = stage + (size_t)(2 * kp) * kS3TX + lane;
+        const float* c1 = c0 + kS3TX;
+        Pair<float> e0, e1;
+        e0.v = make_float2(c0[0], c0[32]);
+        e1.v = make_float2(c1[0], c1[32]);
+        float2 rv = vr[0];
+        Pair<float> l0, l1;
+        l0.v = __fmul2_rn(make_float2(rv.x, rv.x), f[0].v);
+        l1.v = __fmul2_rn(make_float2(rv.y, rv.y), f[0].v);
+#pragma unroll
+        for (int tt = 1; tt < R; ++tt) {
+          rv = vr[tt];
+          l0.v = __ffma2_rn(make_float2(rv.x, rv.x), f[tt].v, l0.v);
+          l1.v = __ffma2_rn(make_float2(rv.y, rv.y), f[tt].v, l1.v);
+        }
+        const Pair<float> r0 = psub(e0, l0);
+        const Pair<float> r1 = psub(e1, l1);
+        res = pfma(r0, r0, res);
+        res = pfma(r1, r1, res);
+      }
+      res_acc[q] += (double)res.v.x + (double)res.v.y;
+    }
+    SPH(4);
+    __syncthreads();  // stage, fnew, red free for the next tile
+    SPH(5);
+  }
+  if (rec)
+    for (int k = 0; k < 8; ++k) a.dbg[k] += tpc[k];
+#undef SPH
+  const double d0 = block_sum<kS3NT>(den_acc[0], dred);
+  const double r0 = block_sum<kS3NT>(res_acc[0], dred + kS3NW);
+  const double d1 = block_sum<kS3NT>(den_acc[1], dred + 2 * kS3NW);
+  const double r1 = block_sum<kS3NT>(res_acc[1], dred + 3 * kS3NW);
+  if (tid == 0) {
+    double4 p;
+    p.x = d0; p.y = r0; p.z = d1; p.w = r1;
+    *reinterpret_cast<double4*>(a.partials + 4 * blockIdx.x) = p;
+  }
+}
+
+// cudaErrorNotSupported when the sampled lines do not fit the stage
+cudaError_t launch_strips3(const StripsArgs<float>& a0, int R, int num_sms, int* ncta_out, cudaStream_t st) {
+  StripsArgs<float> a = a0;
+  a.maxl = a.s[0].nk > a.s[1].nk ? a.s[0].nk : a.s[1].nk;
+  static const int pdist = [] {  // tiles ahead prefetched into L2 (tuning knob)
+    const char* e = std::getenv("IRCUR_STRIPS_PREFETCH");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.prefetch_dist = pdist;
+  static const int desync = [] {  // odd CTAs start later: fills interleave with compute (tuning knob)
+    const char* e = std::getenv("IRCUR_STRIPS_DESYNC_NS");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.desync_ns = desync;
+  for (int q = 0; q < 2; ++q)  // the caller counts tiles of the 64-position cluster kernel (same width)
+    if (a.s[q].tiles > 0) a.s[q].tiles = (a.s[q].npos + kS3TX - 1) / kS3TX;
+  const size_t smem = strips3_layout(a.maxl, R).total;
+  if (smem > (size_t)227 * 1024) return cudaErrorNotSupported;
+  if (ncta_out) *ncta_out = 0;
+  const int tiles = a.s[0].tiles + a.s[1].tiles;
+  if (tiles == 0) return cudaSuccess;
+  cudaError_t e = cudaErrorInvalidValue;
+  IRCUR_DISPATCH_RANK(R, RR, {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(strips3_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    strips3_kernel<RR><<<num_sms, kS3NT, smem, st>>>(a);
+    e = cudaGetLastError();
+  });
+  if (ncta_out) *ncta_out = num_sms;
+  return e;
+}
+
+}  // namespace ircur

@@ -37,7 +37,7 @@ for i in range(a.solves):
     print(f"  ritz: chol={cyc[8]/1e6:.2f} solves={cyc[9]/1e6:.2f} jacobi={cyc[10]/1e6:.2f} Mcyc, "
           f"eig calls={cyc[14]} sweeps={cyc[13]}")
     sn = ["stage_wait", "pass1", "reduce", "override+write", "pass2", "sync+issue", "lvec+loop"]
-    if os.environ.get("IRCUR_STRIPS_V1") != "1":
+    if os.environ.get("IRCUR_STRIPS_VER", "3") != "1":
         sn = ["stage(issue+wait)", "pass1", "sync_after_pass1", "reduce+write+sync", "pass2", "final_sync", "loop"]
     stot = sum(cyc[16:23]) or 1
     print("  strips phases (Mcycles, CTA0/thread0): " + " ".join(
