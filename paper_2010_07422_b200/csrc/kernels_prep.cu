@@ -303,32 +303,42 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
   const int64_t ntiles = tr * tcn;
   T mx = T(0);
   int bad = 0;
-  auto full_tile = [&](int64_t t) {
-    const int64_t br = t / tcn, bc = t - br * tcn;
+  // fp32: max of |x| over the bit patterns (|x| >= +inf's pattern flags NaN/Inf)
+  uint32_t mbits = 0u;
+  // tile coordinates advanced incrementally (no 64-bit divisions in the loop)
+  const int64_t grid = gridDim.x;
+  const int64_t gbr = grid / tcn, gbc = grid - gbr * tcn;
+  auto advance = [&](int64_t& br, int64_t& bc) {
+    br += gbr;
+    bc += gbc;
+    if (bc >= tcn) { bc -= tcn; ++br; }
+  };
+  auto full_tile = [&](int64_t br, int64_t bc) {
     return vec_ok && (br * kPT + kPT <= nloc) && (bc * kPT + kPT <= n2);
   };
   V4 nv[KR];
   I4 ncs;
-  auto load = [&](int64_t t) {
-    const int64_t br = t / tcn, bc = t - br * tcn;
+  auto load = [&](int64_t br, int64_t bc) {
     const int64_t rb = br * kPT, cb = bc * kPT;
 #pragma unroll
     for (int k = 0; k < KR; ++k) nv[k] = __ldcs(reinterpret_cast<const V4*>(D + (rb + vy + k * RPI) * ldd + cb) + vx);
     ncs = __ldg(reinterpret_cast<const I4*>(colsel + cb) + vx);
   };
   int64_t t = blockIdx.x;
-  if (t < ntiles && full_tile(t)) load(t);
+  int64_t br = t / tcn, bc = t - br * tcn;
+  if (t < ntiles && full_tile(br, bc)) load(br, bc);
   int b = 0;
-  for (; t < ntiles; t += gridDim.x, b = (b + 1) % NB) {
-    const int64_t br = t / tcn, bc = t - br * tcn;
+  for (; t < ntiles; t += grid, b = (b + 1) % NB) {
     const int64_t rb = br * kPT, cb = bc * kPT;
-    if (full_tile(t)) {
+    int64_t nbr = br, nbc = bc;
+    advance(nbr, nbc);
+    const bool next_full = t + grid < ntiles && full_tile(nbr, nbc);
+    if (full_tile(br, bc)) {
       V4 v[KR];
 #pragma unroll
       for (int k = 0; k < KR; ++k) v[k] = nv[k];
       const I4 cs = ncs;
-      const int64_t tn = t + gridDim.x;
-      if (tn < ntiles && full_tile(tn)) load(tn);
+      if (next_full) load(nbr, nbc);
       const int* csp = reinterpret_cast<const int*>(&cs);
       int mine = 0;
 #pragma unroll
@@ -345,11 +355,16 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
 #pragma unroll
       for (int k = 0; k < KR; ++k) {
         const T* pv = reinterpret_cast<const T*>(&v[k]);
+        if constexpr (sizeof(T) == 4) {
 #pragma unroll
-        for (int u = 0; u < VW; ++u) {
-          const T av = fabs(pv[u]);
-          bad |= !isfinite(av);
-          mx = fmax(mx, av);
+          for (int u = 0; u < VW; ++u) mbits = max(mbits, __float_as_uint(pv[u]) & 0x7fffffffu);
+        } else {
+#pragma unroll
+          for (int u = 0; u < VW; ++u) {
+            const T av = fabs(pv[u]);
+            bad |= !isfinite(av);
+            mx = fmax(mx, av);
+          }
         }
       }
 #pragma unroll
@@ -383,10 +398,15 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
           if (d >= 0) Dt[(int64_t)d * ldt + r] = val;
         }
       }
-      const int64_t tn = t + gridDim.x;
-      if (tn < ntiles && full_tile(tn)) load(tn);
+      if (next_full) load(nbr, nbc);
       __syncthreads();  // keeps the staging-buffer reuse distance of two barriers
     }
+    br = nbr;
+    bc = nbc;
+  }
+  if constexpr (sizeof(T) == 4) {
+    bad |= mbits >= 0x7f800000u;
+    mx = fmax(mx, __uint_as_float(mbits < 0x7f800000u ? mbits : 0u));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

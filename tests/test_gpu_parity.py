@@ -189,3 +189,28 @@ def test_zero_slabs_early_exit(ir, colmajor):
     cur, sp, tr = ir.solve(D, cfg, device=0, colmajor=colmajor)
     assert tr.iterations == ref.iterations == 1 and tr.thresholds == [1.0]
     assert tr.errors == ref.errors
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+@pytest.mark.parametrize("colmajor", ["sampled", "full", False])
+def test_nonfinite_rejected_in_full_tiles(ir, bad, colmajor):
+    """NaN/Inf inside a full 64 x 64 prep tile (the vectorised scan paths)."""
+    D = np.random.default_rng(1).standard_normal((256, 320)).astype(np.float32)
+    D[130, 200] = bad
+    with pytest.raises(ValueError, match="non-finite"):
+        ir.solve(D, ir.SolverConfig(rank=2, zeta0=1.0), device=0, colmajor=colmajor)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("colmajor", ["sampled", "full", False])
+def test_zeta0_none_uses_exact_max_abs(ir, dtype, colmajor):
+    """zeta0=None takes max|D| (solver.py:342-344) from the prep pass: the
+    first threshold must equal numpy's max|D| exactly, for a maximum that
+    is negative, inside a full tile or in an edge tile."""
+    rng = np.random.default_rng(2)
+    for where in ((70, 80), (255, 319), (3, 317)):
+        D = rng.standard_normal((256, 320)).astype(dtype)
+        D[where] = -7.25
+        cfg = ir.SolverConfig(rank=2, mode="fixed", max_iter=2)
+        tr = ir.solve(D, cfg, device=0, colmajor=colmajor)[2]
+        assert tr.thresholds[0] == float(np.abs(D).max()) == 7.25
