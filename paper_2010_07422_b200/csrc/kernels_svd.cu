@@ -610,6 +610,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   cl.sync();
 
   int step = 0, buf = 0, redo = 0;
+  bool gx_valid = false;  // S.P holds G X for the final Ritz block X (my rows)
   double prev_res = 1e300;
   int stall = 0;
   double* scrX = a.scratch + 2 * (size_t)n * kLdV;  // Ritz block X of the latest step
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
         S.Vq[i * KP + c] = scr[gbuf][(int64_t)(lo + i) * kLdV + c];
       }
       __syncthreads();
+      gx_valid = false;
       if (++redo > 3) {
         for (int e = tid; e < nr * kk; e += kSvdNT) {
           const int i = e / kk, c = e - i * kk;
@@ -674,6 +676,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       S.P[i * KP + c] = sy;
       scrX[(int64_t)(lo + i) * kLdV + c] = sx;
     }
+    gx_valid = true;
     __syncthreads();
     PH(3);
     // ---- 5. this step's Ritz residuals (my rows) and the next block
@@ -731,7 +734,16 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
 #undef PH
 
   // ---- 7. Rayleigh-Ritz on U itself: Y = U V (my m-rows), H2 = Y^T Y
+  const long long tfin0 = clock64();
   const double* Vf = scrX;  // published before the loop's last cluster sync
+  // keep G X of the last step (my n-rows): QJ = G (X Z) Sigma^-1 = (G X) Z Sigma^-1
+  if (gx_valid) {
+    for (int e = tid; e < nr * kk; e += kSvdNT) {
+      const int i = e / kk, c = e - i * kk;
+      S.Bq[i * KP + c] = S.P[i * KP + c];
+    }
+    __syncthreads();
+  }
   tiled_product(a.U + (int64_t)mlo * a.ldu, a.ldu, mr, n, Vf, kLdV, KP, kk, S.Xq, S.P, L.S);
   {
     double* rb = S.red + buf * RL;
@@ -750,7 +762,9 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
       S.H[c1 * HL + c2] = 0.5 * (S.rout[c1 * kk + c2] + S.rout[c2 * kk + c1]);
     }
     eig_sync();
+    const long long tj0 = clock64();
     jacobi_eig(S, kk, 4e-16, 30);
+    if (a.dbg && q == 0 && tid == 0) a.dbg[12] += clock64() - tj0;
   }
   __syncthreads();
   rotate_rows(S.Xq, mr, KP, kk, S.Z, HL, S.P);
@@ -820,7 +834,8 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     VS[(int64_t)(lo + i) * r + c] = (T)vs;
   }
   // QJ = U^T W = G V Sigma^{-1} for my n-rows (zero for deficient columns)
-  tiled_product(Gq, ldgq, nr, n, Vr, kLdV, KP, kk, S.Bq, S.P, L.S);
+  if (gx_valid) rotate_rows(S.Bq, nr, KP, kk, S.Z, HL, S.P);
+  else tiled_product(Gq, ldgq, nr, n, Vr, kLdV, KP, kk, S.Bq, S.P, L.S);
   for (int e = tid; e < nr * r; e += kSvdNT) {
     const int i = e / r, c = e - i * r;
     double v = 0.0;
@@ -883,6 +898,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     const int i = e / r, c = e - i * r;
     Wr[(int64_t)(mlo + i) * r + c] = (T)a.W[(int64_t)(mlo + i) * r + c];
   }
+  if (a.dbg && q == 0 && tid == 0) a.dbg[11] += clock64() - tfin0;
 }
 
 size_t svd_smem_bytes(int n, int m, int kk, int cs) {
