@@ -39,35 +39,62 @@ constexpr int kEigNT = 128;  // threads running the small dense kernels
 constexpr int kLdV = kKMax;  // leading dimension of V in the L2 scratch
 
 // ------------------------------------------------------------------ gram
-// G = U^T U (n x n), 32x32 output tile per CTA, K = m in 32-row chunks.
+// G = U^T U (n x n).  One CTA per 32 x 32 tile of the upper triangle (the
+// mirrored tile is written from the same sums: fma(a, b, c) == fma(b, a, c),
+// so G is exactly symmetric); K = m in 32-row chunks, register-prefetched
+// one chunk ahead into a double-buffered shared tile (one barrier per chunk).
 __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U, int ldu, int m, int n,
                                                    double* __restrict__ G, int ldg, const int* done) {
   if (done && *done) return;
-  __shared__ double A[32][33];
-  __shared__ double B[32][33];
+  __shared__ double A[2][32][33];
+  __shared__ double B[2][32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty 0..7
-  const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
+  // blockIdx.x -> (ta <= tb) in row-major order of the upper triangle
+  const int nt = (n + 31) / 32;
+  int ta = 0, rem = (int)blockIdx.x;
+  while (rem >= nt - ta) { rem -= nt - ta; ++ta; }
+  const int tb = ta + rem;
+  const int a0 = ta * 32, b0 = tb * 32;
   double acc[4] = {0, 0, 0, 0};
-  for (int i0 = 0; i0 < m; i0 += 32) {
+  double ra[4], rb[4];
+  auto fetch = [&](int i0) {
 #pragma unroll
-    for (int k = 0; k < 32; k += 8) {
-      const int i = i0 + ty + k;
-      A[ty + k][tx] = (i < m && a0 + tx < n) ? U[(int64_t)i * ldu + a0 + tx] : 0.0;
-      B[ty + k][tx] = (i < m && b0 + tx < n) ? U[(int64_t)i * ldu + b0 + tx] : 0.0;
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + ty + 8 * k;
+      ra[k] = (i < m && a0 + tx < n) ? U[(int64_t)i * ldu + a0 + tx] : 0.0;
+      rb[k] = (i < m && b0 + tx < n) ? U[(int64_t)i * ldu + b0 + tx] : 0.0;
     }
-    __syncthreads();
+  };
+  auto put = [&](int bf) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      A[bf][ty + 8 * k][tx] = ra[k];
+      B[bf][ty + 8 * k][tx] = rb[k];
+    }
+  };
+  fetch(0);
+  put(0);
+  __syncthreads();
+  int bf = 0;
+  for (int i0 = 0; i0 < m; i0 += 32, bf ^= 1) {
+    const bool more = i0 + 32 < m;
+    if (more) fetch(i0 + 32);
 #pragma unroll 8
     for (int i = 0; i < 32; ++i) {
-      const double bv = B[i][tx];
+      const double bv = B[bf][i][tx];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(A[i][ty + 8 * u], bv, acc[u]);
+      for (int u = 0; u < 4; ++u) acc[u] = fma(A[bf][i][ty + 8 * u], bv, acc[u]);
     }
+    if (more) put(bf ^ 1);
     __syncthreads();
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int ra = a0 + ty + 8 * u, cb = b0 + tx;
-    if (ra < n && cb < n) G[(int64_t)ra * ldg + cb] = acc[u];
+    const int r = a0 + ty + 8 * u, c = b0 + tx;
+    if (r < n && c < n) {
+      G[(int64_t)r * ldg + c] = acc[u];
+      if (ta != tb) G[(int64_t)c * ldg + r] = acc[u];
+    }
   }
 }
 
@@ -919,8 +946,9 @@ int svd_pick_cluster(int n, int m, int kk) {
 
 template <typename T>
 cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st) {
-  dim3 gg((unsigned)((a.n + 31) / 32), (unsigned)((a.n + 31) / 32));
-  gram_kernel<<<gg, 256, 0, st>>>(a.U, a.ldu, a.m, a.n, const_cast<double*>(a.G), a.ldg, a.done);
+  const int nt = (a.n + 31) / 32;
+  gram_kernel<<<(unsigned)(nt * (nt + 1) / 2), 256, 0, st>>>(a.U, a.ldu, a.m, a.n, const_cast<double*>(a.G),
+                                                             a.ldg, a.done);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = svd_smem_bytes(a.n, a.m, a.kk, cs);
