@@ -201,6 +201,11 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
     return e ? std::max(1, std::atoi(e)) : 2;
   }();
   sa.sweeps = sweeps;
+  static const double jthr_scale = [] {  // in-loop Jacobi threshold as a fraction of tol (tuning knob)
+    const char* e = std::getenv("IRCUR_SVD_JTHR");
+    return e ? std::atof(e) : 0.0;
+  }();
+  sa.jac_thr = std::max(4e-16, jthr_scale * sa.tol);
   sa.salt = 0x1234567ull + (uint64_t)k * 7919ull;
   return sa;
 }

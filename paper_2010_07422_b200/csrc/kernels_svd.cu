@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     PH(1);
     // ---- 3. Rayleigh-Ritz (generalised through chol(V^T V))
     if (eigt) {
-      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, 4e-16, a.sweeps, a.dbg);
+      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, a.jac_thr, a.sweeps, a.dbg);
       if (tid == 0) S.flags[7] = ok;
     }
     __syncthreads();

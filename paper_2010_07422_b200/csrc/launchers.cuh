@@ -24,6 +24,7 @@ struct SvdArgs {
   int* steps_out;
   double tol; int maxsteps;       // Ritz residual target: max(tol, tol_scale * e_{k-1}) * lambda_1
   int sweeps;                     // Jacobi sweeps per intermediate Rayleigh-Ritz step
+  double jac_thr;                 // Jacobi off-diagonal threshold (relative) of those steps
   double tol_scale; const double* prev_err;  // e_{k-1} on the device (null at k = 0)
   uint64_t salt;
   long long* dbg;                 // optional per-phase clock64 totals (8)
