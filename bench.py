@@ -336,6 +336,7 @@ def run_sharded(args, rank, world, local):
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
             d2h = sum(o.nbytes for o in outs)
+            del outs, rr  # page-locked result blocks return to torch's host cache
         tt = torch.tensor([float(np.mean(times)), float(d2h), float(Dh.numel() * s)], dtype=torch.float64,
                           device=dev)
         tmax = tt[:1].clone()
