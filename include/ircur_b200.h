@@ -228,6 +228,16 @@ int ircur_materialize_factors(const void* Pt, int64_t ldp, const void* Q, int64_
  * the statistics are computed: max|L| and the quantised sum
  * sum(rint(|L| * 2^24)) from which a = mean|L| is derived order-free.
  * Host-blocking. */
+/* Compact SVD of L = P Q from the device factors (Pt: rank x n1 with leading
+ * dimension ldp, Q: rank x n2, ldq; dtype F32/F64): W (n1 x rank, row-major
+ * fp64, device), sigma (rank), V (n2 x rank); *k_out = columns kept after
+ * dropping sigma < 1e-14 sigma_max.  Replaces convert.cur_to_svd
+ * (convert.py:21-48) with r-wide work: Cholesky-QR of P and Q^T and a
+ * one-sided Jacobi SVD of the r x r middle factor.  rank <= 16. */
+int ircur_factors_to_svd(const void* Pt, int64_t ldp, const void* Q, int64_t ldq, int64_t n1,
+                         int64_t n2, int rank, int dtype, double* W, double* sigma, double* V,
+                         int* k_out, void* stream);
+
 int ircur_gen_baseline(void* D, int dtype, int64_t ldd, int64_t n1, int64_t n2,
                        int64_t row0, int64_t nrows, int rank, const double* W,
                        const double* V, double alpha, double amp_a, const uint64_t* pcg,

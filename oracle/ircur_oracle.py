@@ -300,3 +300,21 @@ def mean_abs_quantised(L: np.ndarray) -> float:
     """mean|L| from an exact int64 sum of rint(|L| * 2^24) (order-free)."""
     q = np.rint(np.abs(L) * 16777216.0).astype(np.int64).sum()
     return float(q) / 16777216.0 / L.size
+
+
+# ------------------------------------------------------------ CUR -> SVD
+def cur_to_svd(C, W, sigma, V, inv_sigma, R, compact_drop=1e-14):
+    """Compact SVD of C U^+ R as convert.py:21-48 computes it: thin QRs of C
+    and R^T, SVD of the middle factor r_c U^+ r_r^T (U^+ applied through
+    the factored pinv, matcore.py:185-189), singular values below
+    compact_drop * sigma_max dropped.  Returns (W, sigma, V)."""
+    q_c, r_c = np.linalg.qr(np.asarray(C, dtype=np.float64), mode="reduced")
+    q_r, r_r = np.linalg.qr(np.asarray(R, dtype=np.float64).T, mode="reduced")
+    middle = ((r_c @ V) * inv_sigma) @ W.T @ r_r.T
+    w_u, s, v_u_t = np.linalg.svd(middle, full_matrices=False)
+    Wc, Vc = q_c @ w_u, q_r @ v_u_t.T
+    smax = s[0] if s.size else 0.0
+    if smax > 0.0:
+        keep = s >= compact_drop * smax
+        Wc, s, Vc = Wc[:, keep], s[keep], Vc[:, keep]
+    return Wc, s, Vc

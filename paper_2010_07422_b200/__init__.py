@@ -6,6 +6,7 @@ of the iteration in hand-written sm_100a CUDA kernels behind a C-ABI
 (include/ircur_b200.h, built into libircur_b200.so).
 """
 
+from .convert import cur_to_svd, factors_to_svd
 from .sampling import IndexSet, RngSeed, draw_index_sets, sample_count, sample_indices
 from .solver import (
     Context,
@@ -22,6 +23,7 @@ from .types import CurFactors, PinvFactor, SolverConfig, SolverTrace, SparseEsti
 
 __all__ = [
     "Context", "CurFactors", "DeviceResult", "IndexSet", "PinvFactor", "RngSeed", "SolverConfig",
+    "cur_to_svd", "factors_to_svd",
     "SolverTrace", "SparseEstimate", "SvdFactors", "clear_cache", "draw_index_sets", "materialize",
     "materialize_device", "sample_count", "sample_indices", "solve", "solve_batch", "solve_device", "threshold_at",
 ]
