@@ -234,6 +234,20 @@ int ircur_materialize_factors(const void* Pt, int64_t ldp, const void* Q, int64_
  * dropping sigma < 1e-14 sigma_max.  Replaces convert.cur_to_svd
  * (convert.py:21-48) with r-wide work: Cholesky-QR of P and Q^T and a
  * one-sided Jacobi SVD of the r x r middle factor.  rank <= 16. */
+/* BIN matrix files (mio.py:66-121: "IRCM", int32 rows/cols, column-major
+ * float64).  ircur_bin_block_to_rowmajor transposes a staged column block
+ * (device, nr x nc, column-major fp64, leading dimension ldsrc) into
+ * row-major dst (dst_dtype F32/F64, leading dimension ldd) and atomically
+ * keeps in *first_bad (device, init ~0) the smallest flat file index
+ * (col * file_rows + row, with the block at file rows row0.., cols col0..)
+ * of a non-finite value.  ircur_rowmajor_to_bin_block is the inverse for
+ * writers (dst: column-major fp64, leading dimension nr). */
+int ircur_bin_block_to_rowmajor(const double* src, int64_t ldsrc, int64_t nr, int64_t nc, void* dst,
+                                int64_t ldd, int dst_dtype, int64_t file_rows, int64_t row0,
+                                int64_t col0, unsigned long long* first_bad, void* stream);
+int ircur_rowmajor_to_bin_block(const void* src, int64_t lds, int src_dtype, int64_t nr, int64_t nc,
+                                double* dst, void* stream);
+
 int ircur_factors_to_svd(const void* Pt, int64_t ldp, const void* Q, int64_t ldq, int64_t n1,
                          int64_t n2, int rank, int dtype, double* W, double* sigma, double* V,
                          int* k_out, void* stream);
