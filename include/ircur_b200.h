@@ -248,6 +248,16 @@ int ircur_bin_block_to_rowmajor(const double* src, int64_t ldsrc, int64_t nr, in
 int ircur_rowmajor_to_bin_block(const void* src, int64_t lds, int src_dtype, int64_t nr, int64_t nc,
                                 double* dst, void* stream);
 
+/* Background / foreground frames of the video pipeline (cli.py:217-230,
+ * mio.py:177-187) for frames [t0, t0 + nt) of D (pixels x frames, row-major,
+ * device, same dtype as the factors): bg = clamp(rint(L)), fg =
+ * clamp(rint(|D - L| * 255 / peak_t)) as uint8 frames (t, y, x) with pixel
+ * (x, y) at row y + x * height.  peaks: nt u64 of device scratch. */
+int ircur_video_frames(const void* Pt, int64_t ldp, const void* Q, int64_t ldq, const void* D,
+                       int64_t ldd, int dtype, int64_t n1, int height, int width, int64_t t0,
+                       int nt, int rank, unsigned long long* peaks, uint8_t* bg, uint8_t* fg,
+                       void* stream);
+
 int ircur_factors_to_svd(const void* Pt, int64_t ldp, const void* Q, int64_t ldq, int64_t n1,
                          int64_t n2, int rank, int dtype, double* W, double* sigma, double* V,
                          int* k_out, void* stream);
