@@ -127,7 +127,14 @@ double storage_zeta<double>(double z) {
 
 int64_t pad4(int64_t n) { return (n + 3) & ~int64_t(3); }
 
-int svd_cluster_size(int n, int m, int kk) { return svd_pick_cluster(n, m, kk); }
+int svd_cluster_size(int n, int m, int kk) {
+  static const int forced = [] {  // tuning knob
+    const char* e = std::getenv("IRCUR_SVD_CS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0 && svd_smem_bytes(n, m, kk, forced) <= (size_t)227 * 1024) return forced;
+  return svd_pick_cluster(n, m, kk);
+}
 
 struct IterSets {
   const int* I;  // local sampled rows (global ids), |I_loc| = mI
