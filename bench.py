@@ -164,7 +164,9 @@ def run_ours(args):
                           max_iter=MAX_ITER, seed=ir.RngSeed(SOLVER_SEED))
     cm = COLMAJOR[args.colmajor]
     stream = torch.cuda.current_stream()
-    prof = not args.no_profile
+    # per-kernel events are recorded inside the timed region; their read-back
+    # (a host sync) happens after it, for the last solve
+    prof = "deferred" if not args.no_profile else False
     for _ in range(args.warmup):
         res = ir.solve_device(D, cfg, colmajor=cm, profile=prof)
     torch.cuda.synchronize()
@@ -184,23 +186,20 @@ def run_ours(args):
     ms_per_step = total_ms / args.steps
     res = results[-1]
     iters = res.trace.iterations
-    # roofline of the dominant kernel (fused strips), from the live events
-    strip_ms, strip_bytes, launches = 0.0, 0, 0
-    svd_ms = core_ms = 0.0
-    for rr in results:
-        p = rr.profile
-        if p is None:
-            p = {"strips_ms": np.full(rr.trace.iterations, np.nan), "svd_ms": np.zeros(rr.trace.iterations),
-                 "core_ms": np.zeros(rr.trace.iterations), "kernel_launches": 5 * rr.trace.iterations}
-            rr.profile = p
-        for k in range(rr.trace.iterations):
-            strip_ms += float(p["strips_ms"][k])
-            svd_ms += float(p["svd_ms"][k])
-            core_ms += float(p["core_ms"][k])
-            strip_bytes += algorithmic_strip_bytes(s, n1, n2, r, rr.trace.sampled_rows[k],
-                                                   rr.trace.sampled_cols[k])
-        launches += 2 + p["kernel_launches"]  # prep + slab norm + 5 per launched iteration
-    n_strip = sum(rr.trace.iterations for rr in results)
+    assert all(rr.trace.iterations == iters for rr in results), "solves differ in iteration count"
+    # roofline of the dominant kernel (fused strips), from the live events of
+    # the last timed solve (every solve runs the same launches)
+    p = res.read_profile() if prof else None
+    if p is None:
+        p = {"strips_ms": np.full(iters, np.nan), "svd_ms": np.zeros(iters),
+             "core_ms": np.zeros(iters), "kernel_launches": 5 * iters}
+    strip_ms = float(np.sum(p["strips_ms"][:iters]))
+    svd_ms = float(np.sum(p["svd_ms"][:iters]))
+    core_ms = float(np.sum(p["core_ms"][:iters]))
+    strip_bytes = sum(algorithmic_strip_bytes(s, n1, n2, r, res.trace.sampled_rows[k], res.trace.sampled_cols[k])
+                      for k in range(iters))
+    launches = len(results) * (2 + p["kernel_launches"])  # prep + slab norm + 5 per launched iteration
+    n_strip = iters
     peak, peak_kind = peaks()
     achieved = strip_bytes / (strip_ms / 1e3) / 1e9
     traffic = None
@@ -220,15 +219,14 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (D >= 400 MB), no flush",
                    "parallelism": "single GPU"},
         "step_ms": step_ms,
-        "host_ms_steps": [{k: round(v, 2) for k, v in (rr.profile or {}).get("host_ms", {}).items()}
+        "host_ms_steps": [{k: round(v, 2) for k, v in (getattr(rr, "_host_ms", None) or {}).items()}
                           for rr in results],
         "breakdown_ms_per_solve": {
-            "strips": strip_ms / len(results), "svd": svd_ms / len(results),
-            "core": core_ms / len(results),
-            "other": ms_per_step - (strip_ms + svd_ms + core_ms) / len(results)},
+            "strips": strip_ms, "svd": svd_ms, "core": core_ms,
+            "other": ms_per_step - (strip_ms + svd_ms + core_ms)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "strips2_kernel", "avg_launch_us": strip_ms / n_strip * 1e3,
+                     "kernel": "strips3_kernel" if dts == "f32" else "strips_kernel", "avg_launch_us": strip_ms / n_strip * 1e3,
                      "bytes_per_launch": strip_bytes / n_strip},
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -104,10 +104,22 @@ int ircur_append_indices(ircur_ctx_t ctx, int n_more, const int64_t* rows,
                          const int32_t* row_counts, const int64_t* cols,
                          const int32_t* col_counts);
 
+/* Asynchronous prep: ircur_prepare_async launches the pass of ircur_prepare
+ * (mode 0/1: make_colmajor) or ircur_prepare_sampled (mode 2, cover_sets)
+ * and returns without waiting; ircur_prepare_wait blocks until it is done
+ * and reports all_finite / max_abs (ENONFINITE like the blocking calls).
+ * Between the two the host may append index sets and queue
+ * ircur_slab_sqnorms_async, so its work overlaps the pass over D. */
+int ircur_prepare_async(ircur_ctx_t ctx, const void* D, int64_t ldd, int mode, int cover_sets);
+int ircur_prepare_wait(ircur_ctx_t ctx, int* all_finite, double* max_abs);
+
 /* den = ||D(I_s,:)||_F^2, ||D(:,J_s)||_F^2 partial sums of the LOCAL rows
  * for index set s (fp64; host-blocking).  Replaces the pre-loop frob_norm
  * pair of solver.py:331-333 used by the den == 0 early exit (:335-341). */
 int ircur_slab_sqnorms(ircur_ctx_t ctx, int set, double* rows_sq, double* cols_sq);
+/* Queue the slab norms of set s on the context stream; the next
+ * ircur_slab_sqnorms(ctx, s, ...) waits for and returns them. */
+int ircur_slab_sqnorms_async(ircur_ctx_t ctx, int set);
 
 /* The device-resident loop, single device (solver.py:358-414): for
  * k = 0..max_iter-1 runs core -> SVD/pinv -> fused strips -> stop check.

@@ -33,11 +33,14 @@ PROTOTYPES = [
     ("ircur_ctx_destroy", _i, [_vp]),
     ("ircur_prepare", _i, [_vp, _vp, _i64, _i, _pi, _pd]),
     ("ircur_prepare_sampled", _i, [_vp, _vp, _i64, _i, _pi, _pd]),
+    ("ircur_prepare_async", _i, [_vp, _vp, _i64, _i, _i]),
+    ("ircur_prepare_wait", _i, [_vp, _pi, _pd]),
     ("ircur_draw_index_sets", _i, [_pu64, _i64, _i64, _i, _i, _i, _pi64, C.POINTER(C.c_int32), _pi64,
                                    C.POINTER(C.c_int32), _pu64]),
     ("ircur_set_indices", _i, [_vp, _i, _pi64, C.POINTER(C.c_int32), _pi64, C.POINTER(C.c_int32)]),
     ("ircur_append_indices", _i, [_vp, _i, _pi64, C.POINTER(C.c_int32), _pi64, C.POINTER(C.c_int32)]),
     ("ircur_slab_sqnorms", _i, [_vp, _i, _pd, _pd]),
+    ("ircur_slab_sqnorms_async", _i, [_vp, _i]),
     ("ircur_run", _i, [_vp, _pd, _d, _i, _i, _pi, _pi, _pd, _pf]),
     ("ircur_iterate", _i, [_vp, _i, _i, _d, _pd]),
     ("ircur_shard_buffers", _i, [_vp, C.POINTER(_vp), _pi64, C.POINTER(_vp), _pi64, C.POINTER(_vp)]),

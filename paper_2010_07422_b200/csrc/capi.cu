@@ -37,6 +37,28 @@ int fail(int code, const std::string& msg) {
 
 }  // namespace
 
+// Page-locked host buffer that grows on demand (contents not preserved).
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <typename T>
+  T* as() { return static_cast<T*>(p); }
+};
+
 struct ircur_ctx {
   int device = 0, dtype = 0;
   int64_t n1 = 0, n2 = 0, row0 = 0, nloc = 0;
@@ -93,6 +115,16 @@ struct ircur_ctx {
   unsigned long long* maxbits = nullptr;
   int* h_flags = nullptr;  // mapped pinned: [0]=done [1]=iters
   int* h_flags_dev = nullptr;
+  // page-locked staging of host->device uploads (index sets, copy plan) so
+  // the uploads are asynchronous; ev_stage follows the last one queued and
+  // is waited on before the staging is rewritten
+  PinnedBuf st_rows, st_cols, st_colsel, st_lines;
+  cudaEvent_t ev_stage = nullptr;
+  // page-locked results of queued reads: [0] max|D| bits, [1] nonfinite,
+  // [2..) slab norm partials
+  unsigned long long* h_res = nullptr;
+  bool prep_pending = false;
+  int slab_pending = -1, slab_nb_rows = 0, slab_nb_cols = 0;
   std::vector<cudaEvent_t> ev;
   // optional per-phase profiling: events [k][0..4] around core | svd | strips | finalize
   bool profiling = false;
@@ -270,16 +302,22 @@ FinalizeArgs finalize_args(ircur_ctx* c, int k, const IterSets& q, double eps, i
 // per-set line indices, capacity, then one prep_select pass over D.
 int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfinite) {
   cover = std::max(1, std::min(cover, c->n_sets));
-  std::vector<int> sel((size_t)c->n2, -1);
+  cudaStream_t st = c->stream;
+  IR_CUDA(cudaEventSynchronize(c->ev_stage));  // staging free to rewrite
+  const size_t nlines = (size_t)c->n_sets * c->max_cols;
+  IR_CUDA(c->st_colsel.reserve((size_t)c->n2 * sizeof(int)));
+  IR_CUDA(c->st_lines.reserve(nlines * sizeof(int)));
+  int* sel = c->st_colsel.as<int>();
+  int* lines = c->st_lines.as<int>();
+  std::fill(sel, sel + c->n2, -1);
   for (int s = 0; s < cover; ++s)
     for (int j = 0; j < c->h_col_cnt[s]; ++j) sel[c->h_cols[(size_t)s * c->max_cols + j]] = 0;
   int64_t nl = 0;
   for (int64_t j = 0; j < c->n2; ++j)
     if (sel[j] >= 0) sel[j] = (int)nl++;
-  std::vector<int> lines((size_t)c->n_sets * c->max_cols, -1);
+  std::fill(lines, lines + nlines, -1);
   for (int s = 0; s < c->n_sets; ++s)
     for (int j = 0; j < c->h_col_cnt[s]; ++j) lines[(size_t)s * c->max_cols + j] = sel[c->h_cols[(size_t)s * c->max_cols + j]];
-  cudaStream_t st = c->stream;
   if (nl > c->dt_cap) {
     IR_CUDA(cudaStreamSynchronize(st));  // in-flight iterations may still read the old copy
     if (c->Dt) cudaFree(c->Dt);
@@ -291,22 +329,22 @@ int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfi
     c->dt_cap = cap;
   }
   if (!c->d_colsel) IR_CUDA(cudaMalloc(&c->d_colsel, (size_t)c->n2 * sizeof(int)));
-  if ((int64_t)lines.size() > c->cols_c_cap) {
+  if ((int64_t)nlines > c->cols_c_cap) {
     IR_CUDA(cudaStreamSynchronize(st));
     if (c->d_cols_c) cudaFree(c->d_cols_c);
     c->d_cols_c = nullptr;
-    IR_CUDA(cudaMalloc(&c->d_cols_c, lines.size() * sizeof(int)));
-    c->cols_c_cap = (int64_t)lines.size();
+    IR_CUDA(cudaMalloc(&c->d_cols_c, nlines * sizeof(int)));
+    c->cols_c_cap = (int64_t)nlines;
   }
-  IR_CUDA(cudaMemcpyAsync(c->d_colsel, sel.data(), sel.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  IR_CUDA(cudaMemcpyAsync(c->d_cols_c, lines.data(), lines.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  IR_CUDA(cudaMemcpyAsync(c->d_colsel, sel, (size_t)c->n2 * sizeof(int), cudaMemcpyHostToDevice, st));
+  IR_CUDA(cudaMemcpyAsync(c->d_cols_c, lines, nlines * sizeof(int), cudaMemcpyHostToDevice, st));
+  IR_CUDA(cudaEventRecord(c->ev_stage, st));
   if (c->dtype == IRCUR_F32)
     IR_CUDA(launch_prep_select<float>((const float*)c->D, c->ldd, c->nloc, c->n2, c->d_colsel, (float*)c->Dt,
                                       c->ldt, maxbits, nonfinite, c->num_sms, st));
   else
     IR_CUDA(launch_prep_select<double>((const double*)c->D, c->ldd, c->nloc, c->n2, c->d_colsel,
                                        (double*)c->Dt, c->ldt, maxbits, nonfinite, c->num_sms, st));
-  IR_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
   c->dt_mode = 2;
   c->covered = cover;
   return IRCUR_OK;
@@ -486,6 +524,9 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->maxbits, sizeof(unsigned long long)));
   IR_CUDA_C(cudaHostAlloc(&c->h_flags, 16 * sizeof(int), cudaHostAllocMapped));
   IR_CUDA_C(cudaHostGetDevicePointer((void**)&c->h_flags_dev, c->h_flags, 0));
+  IR_CUDA_C(cudaHostAlloc(&c->h_res, (2 + (size_t)c->max_partials) * sizeof(unsigned long long), cudaHostAllocDefault));
+  IR_CUDA_C(cudaEventCreateWithFlags(&c->ev_stage, cudaEventDisableTiming));
+  IR_CUDA_C(cudaEventRecord(c->ev_stage, c->stream));
   c->ev.resize(max_iter + 1);
   for (auto& e : c->ev) IR_CUDA_C(cudaEventCreate(&e));
   IR_CUDA_C(cudaMemsetAsync(c->flags, 0, 16 * sizeof(int), c->stream));
@@ -505,6 +546,9 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
+  if (c->h_res) cudaFreeHost(c->h_res);
+  if (c->ev_stage) cudaEventDestroy(c->ev_stage);
+  for (PinnedBuf* b : {&c->st_rows, &c->st_cols, &c->st_colsel, &c->st_lines}) b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evp)
@@ -513,74 +557,81 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   return IRCUR_OK;
 }
 
-int ircur_prepare(ircur_ctx_t c, const void* D, int64_t ldd, int make_colmajor, int* all_finite,
-                  double* max_abs) {
+int ircur_prepare_async(ircur_ctx_t c, const void* D, int64_t ldd, int mode, int cover_sets) {
   if (!c || !D) return fail(IRCUR_EINVAL, "null context or D");
   if (ldd < c->n2) return fail(IRCUR_EINVAL, "ldd < n2");
+  if (mode < 0 || mode > 2) return fail(IRCUR_EINVAL, "mode must be 0 (no copy), 1 (full) or 2 (sampled)");
+  if (mode == 2 && c->n_sets < 1) return fail(IRCUR_EINVAL, "upload the index sets before a sampled prep");
+  if (mode == 2 && cover_sets < 1) return fail(IRCUR_EINVAL, "cover_sets must be >= 1");
   IR_CUDA(cudaSetDevice(c->device));
   c->D = D;
   c->ldd = ldd;
   c->has_state = false;
-  if (make_colmajor && (!c->Dt || c->dt_cap < c->n2)) {
-    if (c->Dt) cudaFree(c->Dt);
-    c->ldt = pad4(c->nloc);
-    c->Dt = nullptr;
-    c->dt_cap = 0;
-    IR_CUDA(cudaMalloc(&c->Dt, (size_t)c->n2 * c->ldt * c->esz));
-    c->dt_cap = c->n2;
-  }
-  if (!make_colmajor && c->Dt) {
-    cudaFree(c->Dt);
-    c->Dt = nullptr;
-    c->dt_cap = 0;
-  }
-  c->dt_mode = make_colmajor ? 1 : 0;
   c->covered = 0;
-  IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), c->stream));
-  IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), c->stream));
-  if (c->dtype == IRCUR_F32)
-    IR_CUDA(launch_prep<float>((const float*)D, ldd, c->nloc, c->n2, (float*)c->Dt, c->ldt, c->maxbits,
-                               c->flags + 3, c->num_sms, c->stream));
-  else
-    IR_CUDA(launch_prep<double>((const double*)D, ldd, c->nloc, c->n2, (double*)c->Dt, c->ldt,
-                                c->maxbits, c->flags + 3, c->num_sms, c->stream));
-  unsigned long long mb = 0;
-  int nf = 0;
-  IR_CUDA(cudaMemcpyAsync(&mb, c->maxbits, sizeof(mb), cudaMemcpyDeviceToHost, c->stream));
-  IR_CUDA(cudaMemcpyAsync(&nf, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  c->slab_pending = -1;
+  cudaStream_t st = c->stream;
+  IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), st));
+  IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), st));
+  if (mode == 2) {
+    c->dt_mode = 0;  // (an allocation from an earlier solve is reused when large enough)
+    if (int rc = build_cover(c, cover_sets, c->maxbits, c->flags + 3)) return rc;
+  } else {
+    if (mode == 1 && (!c->Dt || c->dt_cap < c->n2)) {
+      if (c->Dt) {
+        IR_CUDA(cudaStreamSynchronize(st));
+        cudaFree(c->Dt);
+      }
+      c->ldt = pad4(c->nloc);
+      c->Dt = nullptr;
+      c->dt_cap = 0;
+      IR_CUDA(cudaMalloc(&c->Dt, (size_t)c->n2 * c->ldt * c->esz));
+      c->dt_cap = c->n2;
+    }
+    if (mode == 0 && c->Dt) {
+      IR_CUDA(cudaStreamSynchronize(st));
+      cudaFree(c->Dt);
+      c->Dt = nullptr;
+      c->dt_cap = 0;
+    }
+    c->dt_mode = mode;
+    if (c->dtype == IRCUR_F32)
+      IR_CUDA(launch_prep<float>((const float*)D, ldd, c->nloc, c->n2, (float*)c->Dt, c->ldt, c->maxbits,
+                                 c->flags + 3, c->num_sms, st));
+    else
+      IR_CUDA(launch_prep<double>((const double*)D, ldd, c->nloc, c->n2, (double*)c->Dt, c->ldt,
+                                  c->maxbits, c->flags + 3, c->num_sms, st));
+  }
+  IR_CUDA(cudaMemcpyAsync(c->h_res, c->maxbits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  IR_CUDA(cudaMemcpyAsync(c->h_res + 1, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
+  c->prep_pending = true;
+  return IRCUR_OK;
+}
+
+int ircur_prepare_wait(ircur_ctx_t c, int* all_finite, double* max_abs) {
+  if (!c || !c->prep_pending) return fail(IRCUR_EINVAL, "no prep pass queued");
+  IR_CUDA(cudaSetDevice(c->device));
   IR_CUDA(cudaStreamSynchronize(c->stream));
+  c->prep_pending = false;
   double mx;
-  std::memcpy(&mx, &mb, sizeof(mx));
+  std::memcpy(&mx, c->h_res, sizeof(mx));
+  int nf;
+  std::memcpy(&nf, c->h_res + 1, sizeof(nf));
   if (all_finite) *all_finite = nf ? 0 : 1;
   if (max_abs) *max_abs = mx;
   if (nf) return fail(IRCUR_ENONFINITE, "matrix contains non-finite entries");
   return IRCUR_OK;
 }
 
+int ircur_prepare(ircur_ctx_t c, const void* D, int64_t ldd, int make_colmajor, int* all_finite,
+                  double* max_abs) {
+  if (int rc = ircur_prepare_async(c, D, ldd, make_colmajor ? 1 : 0, 0)) return rc;
+  return ircur_prepare_wait(c, all_finite, max_abs);
+}
+
 int ircur_prepare_sampled(ircur_ctx_t c, const void* D, int64_t ldd, int cover_sets, int* all_finite,
                           double* max_abs) {
-  if (!c || !D) return fail(IRCUR_EINVAL, "null context or D");
-  if (ldd < c->n2) return fail(IRCUR_EINVAL, "ldd < n2");
-  if (c->n_sets < 1) return fail(IRCUR_EINVAL, "upload the index sets before ircur_prepare_sampled");
-  if (cover_sets < 1) return fail(IRCUR_EINVAL, "cover_sets must be >= 1");
-  IR_CUDA(cudaSetDevice(c->device));
-  c->D = D;
-  c->ldd = ldd;
-  c->has_state = false;
-  c->dt_mode = 0;  // (an allocation from an earlier solve is reused when large enough)
-  IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), c->stream));
-  IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), c->stream));
-  if (int rc = build_cover(c, cover_sets, c->maxbits, c->flags + 3)) return rc;
-  unsigned long long mb = 0;
-  int nf = 0;
-  IR_CUDA(cudaMemcpy(&mb, c->maxbits, sizeof(mb), cudaMemcpyDeviceToHost));
-  IR_CUDA(cudaMemcpy(&nf, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost));
-  double mx;
-  std::memcpy(&mx, &mb, sizeof(mx));
-  if (all_finite) *all_finite = nf ? 0 : 1;
-  if (max_abs) *max_abs = mx;
-  if (nf) return fail(IRCUR_ENONFINITE, "matrix contains non-finite entries");
-  return IRCUR_OK;
+  if (int rc = ircur_prepare_async(c, D, ldd, 2, cover_sets)) return rc;
+  return ircur_prepare_wait(c, all_finite, max_abs);
 }
 
 }  // extern "C"
@@ -591,7 +642,13 @@ namespace {
 // increasing, strides max_rows / max_cols); device arrays grow as needed.
 int upload_sets(ircur_ctx* c, int first, int n, const int64_t* rows, const int32_t* row_counts,
                 const int64_t* cols, const int32_t* col_counts) {
-  std::vector<int> hr((size_t)n * c->max_rows, 0), hc((size_t)n * c->max_cols, 0);
+  IR_CUDA(cudaEventSynchronize(c->ev_stage));  // staging free to rewrite
+  IR_CUDA(c->st_rows.reserve((size_t)n * c->max_rows * sizeof(int)));
+  IR_CUDA(c->st_cols.reserve((size_t)n * c->max_cols * sizeof(int)));
+  int* hr = c->st_rows.as<int>();
+  int* hc = c->st_cols.as<int>();
+  std::memset(hr, 0, (size_t)n * c->max_rows * sizeof(int));
+  std::memset(hc, 0, (size_t)n * c->max_cols * sizeof(int));
   const int total = first + n;
   c->h_row_cnt.resize(total, 0);
   c->h_col_cnt.resize(total, 0);
@@ -641,13 +698,13 @@ int upload_sets(ircur_ctx* c, int first, int n, const int64_t* rows, const int32
     c->sets_cap = cap;
   }
   c->h_cols.resize((size_t)total * c->max_cols, 0);
-  std::memcpy(c->h_cols.data() + (size_t)first * c->max_cols, hc.data(), hc.size() * sizeof(int));
+  std::memcpy(c->h_cols.data() + (size_t)first * c->max_cols, hc, (size_t)n * c->max_cols * sizeof(int));
   c->n_sets = total;
-  IR_CUDA(cudaMemcpyAsync(c->d_rows + (size_t)first * c->max_rows, hr.data(), hr.size() * sizeof(int),
+  IR_CUDA(cudaMemcpyAsync(c->d_rows + (size_t)first * c->max_rows, hr, (size_t)n * c->max_rows * sizeof(int),
                           cudaMemcpyHostToDevice, st));
-  IR_CUDA(cudaMemcpyAsync(c->d_cols + (size_t)first * c->max_cols, hc.data(), hc.size() * sizeof(int),
+  IR_CUDA(cudaMemcpyAsync(c->d_cols + (size_t)first * c->max_cols, hc, (size_t)n * c->max_cols * sizeof(int),
                           cudaMemcpyHostToDevice, st));
-  IR_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+  IR_CUDA(cudaEventRecord(c->ev_stage, st));
   return IRCUR_OK;
 }
 
@@ -676,9 +733,8 @@ int ircur_append_indices(ircur_ctx_t c, int n_more, const int64_t* rows, const i
   return upload_sets(c, c->n_sets, n_more, rows, row_counts, cols, col_counts);
 }
 
-int ircur_slab_sqnorms(ircur_ctx_t c, int set, double* rows_sq, double* cols_sq) {
+int ircur_slab_sqnorms_async(ircur_ctx_t c, int set) {
   if (!c || !c->D || set < 0 || set >= c->n_sets) return fail(IRCUR_EINVAL, "bad context/set");
-
   IR_CUDA(cudaSetDevice(c->device));
   const int nb_rows = std::max(1, std::min(c->num_sms * 2, (int)((int64_t)c->h_row_loc_cnt[set] * c->n2 / 4096 + 1)));
   const int nb_cols = std::max(1, std::min(c->num_sms * 2, (int)(c->nloc * c->h_col_cnt[set] / 4096 + 1)));
@@ -697,12 +753,25 @@ int ircur_slab_sqnorms(ircur_ctx_t c, int set, double* rows_sq, double* cols_sq)
                                    c->h_row_loc_cnt[set], J, c->h_col_cnt[set], nb_rows, nb_cols,
                                    c->partials, use_dt ? (const double*)c->Dt : nullptr, c->ldt, Jl,
                                    c->stream));
-  std::vector<double> h(nb_rows + nb_cols);
-  IR_CUDA(cudaMemcpyAsync(h.data(), c->partials, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  IR_CUDA(cudaMemcpyAsync(c->h_res + 2, c->partials, (size_t)(nb_rows + nb_cols) * sizeof(double),
+                          cudaMemcpyDeviceToHost, c->stream));
+  c->slab_pending = set;
+  c->slab_nb_rows = nb_rows;
+  c->slab_nb_cols = nb_cols;
+  return IRCUR_OK;
+}
+
+int ircur_slab_sqnorms(ircur_ctx_t c, int set, double* rows_sq, double* cols_sq) {
+  if (!c || !c->D || set < 0 || set >= c->n_sets) return fail(IRCUR_EINVAL, "bad context/set");
+  if (c->slab_pending != set)
+    if (int rc = ircur_slab_sqnorms_async(c, set)) return rc;
+  IR_CUDA(cudaSetDevice(c->device));
   IR_CUDA(cudaStreamSynchronize(c->stream));
+  c->slab_pending = -1;
+  const double* h = reinterpret_cast<const double*>(c->h_res + 2);
   double a = 0.0, b = 0.0;
-  for (int i = 0; i < nb_rows; ++i) a += h[i];
-  for (int i = 0; i < nb_cols; ++i) b += h[nb_rows + i];
+  for (int i = 0; i < c->slab_nb_rows; ++i) a += h[i];
+  for (int i = 0; i < c->slab_nb_cols; ++i) b += h[c->slab_nb_rows + i];
   if (rows_sq) *rows_sq = a;
   if (cols_sq) *cols_sq = b;
   return IRCUR_OK;

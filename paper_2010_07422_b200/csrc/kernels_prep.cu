@@ -434,6 +434,54 @@ cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2
 // -------------------------------------------------------------- slab norms
 // partials[blockIdx.x] = sum of squares of this CTA's share; rows part uses
 // blocks [0, nb_rows), cols part blocks [nb_rows, nb_rows + nb_cols).
+// Sum of squares of the line segment p[0, len) (contiguous), this thread's share.
+// 16-byte vector loads on the aligned body, four in flight per thread.
+template <typename T>
+__device__ __forceinline__ double seg_sq(const T* __restrict__ p, int64_t len) {
+  constexpr int V = 16 / sizeof(T);
+  using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  double acc = 0.0;
+  int64_t head = (int64_t)((16 - ((uintptr_t)p & 15)) & 15) / sizeof(T);
+  if (((uintptr_t)p % sizeof(T)) != 0) head = len;  // unaligned element type: scalar only
+  head = head < len ? head : len;
+  if ((int64_t)threadIdx.x < head) {
+    const double v = (double)p[threadIdx.x];
+    acc = fma(v, v, acc);
+  }
+  const VT* q = reinterpret_cast<const VT*>(p + head);
+  const int64_t nv = (len - head) / V;
+  int64_t i = threadIdx.x;
+  for (; i + 3 * 256 < nv; i += 4 * 256) {
+    VT a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = __ldg(q + i + u * 256);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const T* e = reinterpret_cast<const T*>(&a[u]);
+#pragma unroll
+      for (int w = 0; w < V; ++w) acc = fma((double)e[w], (double)e[w], acc);
+    }
+  }
+  for (; i < nv; i += 256) {
+    const VT a = __ldg(q + i);
+    const T* e = reinterpret_cast<const T*>(&a);
+#pragma unroll
+    for (int w = 0; w < V; ++w) acc = fma((double)e[w], (double)e[w], acc);
+  }
+  const int64_t t0 = head + nv * V;
+  if (t0 + (int64_t)threadIdx.x < len) {
+    const double v = (double)p[t0 + threadIdx.x];
+    acc = fma(v, v, acc);
+  }
+  return acc;
+}
+
+// ||D(I,:)||_F^2 (blocks [0, nb_rows)) and ||D(:,J)||_F^2 (the rest), one
+// partial per block (fixed work split: deterministic).  Work unit = one line
+// segment of kSlabSeg elements: a sampled row of D, or a column line of the
+// column-major copy Dt when it holds D(:,J).
+constexpr int64_t kSlabSeg = 8192;
+
 template <typename T>
 __global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, int64_t row0, int64_t nloc,
                                                       int64_t n2, const int* I, int mI, const int* J,
@@ -442,28 +490,29 @@ __global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, i
   __shared__ double sh[8];
   double acc = 0.0;
   if ((int)blockIdx.x < nb_rows) {
-    const int64_t total = (int64_t)mI * n2;
-    for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)nb_rows * 256) {
-      const int64_t k = e / n2, x = e - k * n2;
-      const double v = (double)D[((int64_t)I[k] - row0) * ldd + x];
-      acc = fma(v, v, acc);
+    const int64_t segs = (n2 + kSlabSeg - 1) / kSlabSeg, units = (int64_t)mI * segs;
+    for (int64_t u = blockIdx.x; u < units; u += nb_rows) {
+      const int64_t k = u / segs, s = (u - k * segs) * kSlabSeg;
+      const int64_t len = n2 - s < kSlabSeg ? n2 - s : kSlabSeg;
+      acc += seg_sq(D + ((int64_t)I[k] - row0) * ldd + s, len);
     }
   } else {
     const int nb_cols = gridDim.x - nb_rows;
-    const int64_t total = nloc * nJ;
+    const int cb = blockIdx.x - nb_rows;
     if (Dt) {  // the column-major copy holds D(:,J): contiguous lines
-      for (int64_t e = (int64_t)(blockIdx.x - nb_rows) * 256 + threadIdx.x; e < total;
-           e += (int64_t)nb_cols * 256) {
-        const int64_t k = e / nloc, x = e - k * nloc;
-        const double v = (double)Dt[(int64_t)Jline[k] * ldt + x];
-        acc = fma(v, v, acc);
+      const int64_t segs = (nloc + kSlabSeg - 1) / kSlabSeg, units = (int64_t)nJ * segs;
+      for (int64_t u = cb; u < units; u += nb_cols) {
+        const int64_t k = u / segs, s = (u - k * segs) * kSlabSeg;
+        const int64_t len = nloc - s < kSlabSeg ? nloc - s : kSlabSeg;
+        acc += seg_sq(Dt + (int64_t)Jline[k] * ldt + s, len);
       }
-    } else {
-      for (int64_t e = (int64_t)(blockIdx.x - nb_rows) * 256 + threadIdx.x; e < total;
-           e += (int64_t)nb_cols * 256) {
-        const int64_t x = e / nJ, k = e - x * nJ;
-        const double v = (double)D[x * ldd + J[k]];
-        acc = fma(v, v, acc);
+    } else {  // strided gather D(x, J[k]): one row x per step, threads along J
+      for (int64_t x = cb; x < nloc; x += nb_cols) {
+        const T* row = D + x * ldd;
+        for (int k = threadIdx.x; k < nJ; k += 256) {
+          const double v = (double)row[J[k]];
+          acc = fma(v, v, acc);
+        }
       }
     }
   }

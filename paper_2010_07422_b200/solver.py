@@ -98,6 +98,23 @@ class Context:
                                                C.byref(ok), C.byref(mx)))
         return float(mx.value)
 
+    def prepare_async(self, D: torch.Tensor, colmajor, cover: int = 0) -> None:
+        """Queue the prep pass (see prepare) without waiting; prepare_wait
+        returns its max|D| (ValueError on NaN/Inf)."""
+        self._D = D
+        mode = int(colmajor)
+        self.colmajor = mode
+        _capi.check(self.lib.ircur_prepare_async(self.h, C.c_void_p(_ptr(D)), D.stride(0), mode, int(cover)))
+
+    def prepare_wait(self) -> float:
+        ok = C.c_int(0)
+        mx = C.c_double(0.0)
+        _capi.check(self.lib.ircur_prepare_wait(self.h, C.byref(ok), C.byref(mx)))
+        return float(mx.value)
+
+    def slab_sqnorms_async(self, s: int) -> None:
+        _capi.check(self.lib.ircur_slab_sqnorms_async(self.h, s))
+
     def set_indices(self, sets) -> None:
         n = len(sets)
         pre = getattr(sets, "rows", None)
@@ -389,9 +406,16 @@ def _copy_plan(colmajor, n2: int, m_cols: int, sets, cfg: SolverConfig) -> tuple
             cover = max(1, min(len(sets), int(colmajor.split(":")[1])))
         return 2, cover
     mark = np.zeros(n2, dtype=bool)
-    for k in range(cover):
-        mark[sets[k][1]] = True
-    return (1, 0) if mark.sum() > 0.7 * n2 else (2, cover)
+    padded = getattr(sets, "cols", None)
+    if padded is not None:
+        # rows of sets.cols are padded with zeros past their counts; column
+        # 0 can only be a set's first (smallest) entry
+        mark[padded[:cover].ravel()] = True
+        mark[0] = bool((padded[:cover, 0] == 0).any())
+    else:
+        for k in range(cover):
+            mark[sets[k][1]] = True
+    return (1, 0) if np.count_nonzero(mark) > 0.7 * n2 else (2, cover)
 
 
 @dataclass
@@ -416,6 +440,16 @@ class DeviceResult:
     colmajor: bool = False
     sets: list | None = None
 
+    def read_profile(self) -> dict | None:
+        """Per-kernel event times of a solve run with profile="deferred"
+        (valid until the next solve on the same context)."""
+        if self.profile is None and self.ctx is not None:
+            host = getattr(self, "_host_ms", None)
+            self.profile = self.ctx.profile(self.trace.iterations)
+            if host is not None:
+                self.profile["host_ms"] = host
+        return self.profile
+
 
 def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
                  colmajor="auto", fetch_factors=True, profile=False) -> DeviceResult:
@@ -425,7 +459,10 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     context, and with fetch_factors=True its `handle` holds zero-copy views
     of the context's final factors: both stay valid until the next solve on
     the same context (same device, shape, dtype and stream).  Pass
-    fetch_factors="copy" for private factor tensors.
+    fetch_factors="copy" for private factor tensors.  profile=True reads the
+    per-kernel event times into result.profile; profile="deferred" records
+    the events but leaves the read-back to result.read_profile(), keeping
+    it out of the caller's timed region.
     """
     cfg = config
     tick = _Ticker(profile)
@@ -463,17 +500,20 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
             r=draw_index_sets_from(pcg_next, n1, n2, m_rows, m_cols, n_sets - n_first)[0]))
         worker.start()
     try:
-        max_abs = ctx.prepare(Dd, cm, cover)  # ValueError on NaN/Inf (matcore.py:75-76)
+        # the pass over D runs while the host draws and uploads the tail of
+        # the index sequence and queues the den == 0 check
+        ctx.prepare_async(Dd, cm, cover)
     finally:
         if n_first < n_sets:
             worker.join()
             rest = box["r"]
-    tick("prepare")
     if rest is not None:
         ctx.append_indices(rest)
         sets.extend_drawn(rest)
-        tick("append")
-    rows0, cols0 = sets[0]
+    ctx.slab_sqnorms_async(0)
+    tick("queue")
+    max_abs = ctx.prepare_wait()  # ValueError on NaN/Inf (matcore.py:75-76)
+    tick("prepare")
     a, b = ctx.slab_sqnorms(0)
     tick("slab")
     trace = SolverTrace()
@@ -491,7 +531,7 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     if observer is None:
         iters, conv, errors, ms = ctx.run(zetas, cfg.eps, mode, cfg.max_iter)
         tick("run")
-        if profile:
+        if profile and profile != "deferred":
             prof = ctx.profile(iters)
             tick("profile")
         trace.errors = [float(e) for e in errors]
@@ -533,6 +573,7 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     if prof is not None:
         prof["host_ms"] = tick.marks
     res.profile = prof
+    res._host_ms = tick.marks if profile else None
     res.colmajor = cm
     res.sets = sets
     return res

@@ -214,3 +214,29 @@ def test_zeta0_none_uses_exact_max_abs(ir, dtype, colmajor):
         cfg = ir.SolverConfig(rank=2, mode="fixed", max_iter=2)
         tr = ir.solve(D, cfg, device=0, colmajor=colmajor)[2]
         assert tr.thresholds[0] == float(np.abs(D).max()) == 7.25
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("colmajor", [0, 1, 2])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_slab_sqnorms_match_numpy(ir, dtype, colmajor, offset):
+    """ircur_slab_sqnorms (the den of solver.py:331-341) against numpy, for
+    every copy mode, on an unaligned strided view of D (odd leading
+    dimension, start off the 16-byte grid) and lines longer than one
+    8192-element work unit."""
+    from paper_2010_07422_b200 import _capi
+    from paper_2010_07422_b200.solver import Context
+    n1, n2, r = 700, 9000, 3
+    rng = np.random.default_rng(5)
+    base = torch.from_numpy(rng.standard_normal((n1, n2 + 3)).astype(dtype)).cuda()
+    D = base[:, offset:offset + n2]
+    sets = ir.draw_index_sets(n1, n2, 40, 300, ir.RngSeed(9), 2)
+    ctx = Context(0, _capi.F32 if dtype == np.float32 else _capi.F64, n1, n2, r, 40, 300, 2)
+    ctx.set_indices(sets)
+    ctx.prepare(D, colmajor, cover=1)
+    Dn = D.double().cpu().numpy()
+    for s, (I, J) in enumerate(sets):
+        a, b = ctx.slab_sqnorms(s)
+        assert a == pytest.approx(float((Dn[I, :] ** 2).sum()), rel=1e-12)
+        assert b == pytest.approx(float((Dn[:, J] ** 2).sum()), rel=1e-12)
+    ctx.close()

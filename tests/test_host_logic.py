@@ -135,3 +135,27 @@ def test_c_draws_continue_from_state():
     for (a, b), (c, d) in zip(first, whole):
         np.testing.assert_array_equal(a, c)
         np.testing.assert_array_equal(b, d)
+
+
+@pytest.mark.parametrize("n1,n2,m1,m2,n_sets", [(2**31 + 12345, 3 * 2**30 + 7, 40, 30, 37),
+                                                (100000, 100000, 461, 461, 49), (1, 5000, 3, 60, 25)])
+def test_c_draws_chunked_with_rejections_equal_numpy(n1, n2, m1, m2, n_sets):
+    """The threaded draws (chunks started at their rejection-free stream
+    positions, redrawn where Lemire rejections shifted them) equal numpy's
+    sequential integers()/unique stream, and the returned PCG64 state is
+    numpy's state after the same draws.  At n ~ 2^31 about every second
+    draw is rejected, so nearly every chunk is redrawn."""
+    from paper_2010_07422_b200.sampling import draw_index_sets_from, pcg_words
+    s = ir.RngSeed(13, 1)
+    fast, st = draw_index_sets_from(pcg_words(s), n1, n2, m1, m2, n_sets)
+    g = s.generator()
+    for a, b in fast:
+        np.testing.assert_array_equal(a, np.unique(g.integers(0, n1, m1)))
+        np.testing.assert_array_equal(b, np.unique(g.integers(0, n2, m2)))
+    ref = g.bit_generator.state
+    m64 = (1 << 64) - 1
+    want = [ref["state"]["state"] & m64, ref["state"]["state"] >> 64, ref["state"]["inc"] & m64,
+            ref["state"]["inc"] >> 64, int(ref["has_uint32"])]
+    assert [int(x) for x in st[:5]] == want
+    if ref["has_uint32"]:
+        assert int(st[5]) == int(ref["uinteger"])
