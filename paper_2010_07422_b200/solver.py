@@ -516,6 +516,7 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     tick("prepare")
     a, b = ctx.slab_sqnorms(0)
     tick("slab")
+    rows0, cols0 = sets[0]
     trace = SolverTrace()
     if np.sqrt(a) + np.sqrt(b) == 0.0:
         # solver.py:335-341: sampled slabs identically zero
@@ -526,7 +527,7 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
         cfg = replace(cfg, zeta0=max_abs)  # solver.py:342-344
     zetas = [cfg.gamma**k * cfg.zeta0 for k in range(cfg.max_iter)]
     mode = _capi.RESAMPLED if resampled else _capi.FIXED
-    ctx.set_profiling(profile)
+    ctx.set_profiling(bool(profile))
     prof = None
     if observer is None:
         iters, conv, errors, ms = ctx.run(zetas, cfg.eps, mode, cfg.max_iter)
