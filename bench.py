@@ -223,7 +223,8 @@ def run_ours(args):
                           for rr in results],
         "breakdown_ms_per_solve": {
             "strips": strip_ms, "svd": svd_ms, "core": core_ms,
-            "other": ms_per_step - (strip_ms + svd_ms + core_ms)},
+            "other": ms_per_step - (strip_ms + svd_ms + core_ms),
+            "device_gaps_ms": p.get("gaps_ms")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "strips3_kernel" if dts == "f32" else "strips_kernel", "avg_launch_us": strip_ms / n_strip * 1e3,

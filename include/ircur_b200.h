@@ -210,6 +210,10 @@ int ircur_materialize(ircur_ctx_t ctx, void* L, int64_t ldl, int out_dtype);
  * (ircur_set_profiling), read back as per-iteration milliseconds, plus the
  * number of iterations launched and kernels launched by the last ircur_run. */
 int ircur_set_profiling(ircur_ctx_t ctx, int on);
+/* Device-side gaps of the last solve while profiling (ms): upload of the
+ * index sets -> prep begin, prep pass, prep end -> slab norms queued, slab
+ * end -> ircur_run, ircur_run -> first loop kernel; -1 when not recorded. */
+int ircur_get_marks(ircur_ctx_t ctx, float* ms);
 int ircur_get_profile(ircur_ctx_t ctx, int n_iters, int* launched_iters,
                       long long* kernel_launches, float* core_ms, float* svd_ms,
                       float* strips_ms, float* finalize_ms);

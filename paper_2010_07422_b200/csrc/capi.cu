@@ -129,6 +129,8 @@ struct ircur_ctx {
   // optional per-phase profiling: events [k][0..4] around core | svd | strips | finalize
   bool profiling = false;
   std::vector<cudaEvent_t> evp;
+  // host-gap marks (profiling): set_indices | prep begin | prep end | slab end | run begin
+  cudaEvent_t evm[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   int launched_iters = 0;
   long long kernel_launches = 0;
   int strips_cs = 1;
@@ -158,6 +160,10 @@ double storage_zeta<double>(double z) {
 }
 
 int64_t pad4(int64_t n) { return (n + 3) & ~int64_t(3); }
+
+void mark(ircur_ctx* c, int i) {
+  if (c->profiling && c->evm[i]) cudaEventRecord(c->evm[i], c->stream);
+}
 
 int svd_cluster_size(int n, int m, int kk) {
   static const int forced = [] {  // tuning knob
@@ -553,6 +559,8 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evp)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->evm)
+    if (e) cudaEventDestroy(e);
   delete c;
   return IRCUR_OK;
 }
@@ -570,6 +578,7 @@ int ircur_prepare_async(ircur_ctx_t c, const void* D, int64_t ldd, int mode, int
   c->covered = 0;
   c->slab_pending = -1;
   cudaStream_t st = c->stream;
+  mark(c, 1);
   IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), st));
   IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), st));
   if (mode == 2) {
@@ -603,6 +612,7 @@ int ircur_prepare_async(ircur_ctx_t c, const void* D, int64_t ldd, int mode, int
   }
   IR_CUDA(cudaMemcpyAsync(c->h_res, c->maxbits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   IR_CUDA(cudaMemcpyAsync(c->h_res + 1, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
+  mark(c, 2);
   c->prep_pending = true;
   return IRCUR_OK;
 }
@@ -717,6 +727,7 @@ int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int3
   if (!c || n_sets < 1 || !rows || !cols || !row_counts || !col_counts)
     return fail(IRCUR_EINVAL, "bad index-set arguments");
   IR_CUDA(cudaSetDevice(c->device));
+  mark(c, 0);
   if (c->dt_mode == 2) {  // the sampled copy belongs to the previous sets
     c->dt_mode = 0;
     c->covered = 0;
@@ -755,6 +766,7 @@ int ircur_slab_sqnorms_async(ircur_ctx_t c, int set) {
                                    c->stream));
   IR_CUDA(cudaMemcpyAsync(c->h_res + 2, c->partials, (size_t)(nb_rows + nb_cols) * sizeof(double),
                           cudaMemcpyDeviceToHost, c->stream));
+  mark(c, 3);
   c->slab_pending = set;
   c->slab_nb_rows = nb_rows;
   c->slab_nb_cols = nb_cols;
@@ -838,6 +850,7 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   if (c->nloc != c->n1) return fail(IRCUR_EINVAL, "row-sharded context: use ircur_shard_phase");
   IR_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
+  mark(c, 4);
   if (int rc = reset_loop(c)) return rc;
   volatile int* hf = c->h_flags;
   constexpr int kAhead = 3;
@@ -1073,8 +1086,23 @@ int ircur_set_profiling(ircur_ctx_t c, int on) {
   if (on && c->evp.empty()) {
     c->evp.resize((size_t)c->max_iter * 5);
     for (auto& e : c->evp) IR_CUDA(cudaEventCreate(&e));
+    for (auto& e : c->evm) IR_CUDA(cudaEventCreate(&e));
   }
   c->profiling = on != 0;
+  return IRCUR_OK;
+}
+
+int ircur_get_marks(ircur_ctx_t c, float* ms) {
+  if (!c || !ms) return fail(IRCUR_EINVAL, "null context or output");
+  for (int i = 0; i < 5; ++i) ms[i] = -1.f;
+  if (!c->profiling || !c->evm[0] || c->evp.empty()) return IRCUR_OK;
+  IR_CUDA(cudaSetDevice(c->device));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < 5; ++i) {
+    cudaEvent_t b = i < 4 ? c->evm[i + 1] : c->evp[0];
+    if (cudaEventElapsedTime(&ms[i], c->evm[i], b) != cudaSuccess) ms[i] = -1.f;
+  }
+  cudaGetLastError();
   return IRCUR_OK;
 }
 

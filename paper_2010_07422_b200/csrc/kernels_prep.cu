@@ -273,7 +273,7 @@ cudaError_t launch_prep(const T* D, int64_t ldd, int64_t nloc, int64_t n2, T* Dt
 // Dt.  The host selects the union of the column index sets the iterations
 // will use (about 20% of D at n = 1e5), so the per-solve pass moves ~1.2x
 // |D| instead of the 2x |D| of a full transpose.
-template <typename T>
+template <typename T, int TR, int TC>
 __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ D, int64_t ldd, int64_t nloc,
                                                           int64_t n2, const int* __restrict__ colsel,
                                                           T* __restrict__ Dt, int64_t ldt,
@@ -286,20 +286,22 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
   // that every warp computes identically) and written out as 16-byte
   // vectors: one barrier per tile.
   constexpr int VW = 16 / sizeof(T);   // elements per vector
-  constexpr int TPR = kPT / VW;        // threads per 64-element row segment
+  constexpr int TPR = TC / VW;         // threads per TC-element row segment (one warp at most)
   constexpr int RPI = 256 / TPR;       // rows per pass
-  constexpr int KR = kPT / RPI;        // rows per thread
-  constexpr int SL = kPT + VW;         // staged column length (16-byte aligned rows)
+  constexpr int KR = TR / RPI;         // rows per thread
+  constexpr int SL = TR + VW;          // staged column length (16-byte aligned rows)
+  constexpr int CPW = TR / VW;         // vectors per staged column
   constexpr int NB = sizeof(T) == 4 ? 2 : 1;  // staging buffers (fp64: one, fits 48 KB static)
-  __shared__ __align__(16) T sbuf[NB][kPT][SL];
-  __shared__ int sdst[NB][kPT];
+  static_assert(TPR <= 32 && KR >= 1 && RPI * KR == TR, "tile shape");
+  __shared__ __align__(16) T sbuf[NB][TC][SL];
+  __shared__ int sdst[NB][TC];
   using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   using I4 = typename std::conditional<sizeof(T) == 4, int4, int2>::type;
   const int vx = threadIdx.x % TPR, vy = threadIdx.x / TPR;
   const int lane = threadIdx.x & 31;
   const bool vec_ok = ((ldd * (int64_t)sizeof(T)) % 16 == 0) && ((ldt * (int64_t)sizeof(T)) % 16 == 0) &&
                       ((uintptr_t)D % 16 == 0) && ((uintptr_t)Dt % 16 == 0) && (n2 % VW == 0);
-  const int64_t tr = (nloc + kPT - 1) / kPT, tcn = (n2 + kPT - 1) / kPT;
+  const int64_t tr = (nloc + TR - 1) / TR, tcn = (n2 + TC - 1) / TC;
   const int64_t ntiles = tr * tcn;
   T mx = T(0);
   int bad = 0;
@@ -314,12 +316,12 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
     if (bc >= tcn) { bc -= tcn; ++br; }
   };
   auto full_tile = [&](int64_t br, int64_t bc) {
-    return vec_ok && (br * kPT + kPT <= nloc) && (bc * kPT + kPT <= n2);
+    return vec_ok && (br * TR + TR <= nloc) && (bc * TC + TC <= n2);
   };
   V4 nv[KR];
   I4 ncs;
   auto load = [&](int64_t br, int64_t bc) {
-    const int64_t rb = br * kPT, cb = bc * kPT;
+    const int64_t rb = br * TR, cb = bc * TC;
 #pragma unroll
     for (int k = 0; k < KR; ++k) nv[k] = __ldcs(reinterpret_cast<const V4*>(D + (rb + vy + k * RPI) * ldd + cb) + vx);
     ncs = __ldg(reinterpret_cast<const I4*>(colsel + cb) + vx);
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
   if (t < ntiles && full_tile(br, bc)) load(br, bc);
   int b = 0;
   for (; t < ntiles; t += grid, b = (b + 1) % NB) {
-    const int64_t rb = br * kPT, cb = bc * kPT;
+    const int64_t rb = br * TR, cb = bc * TC;
     int64_t nbr = br, nbc = bc;
     advance(nbr, nbc);
     const bool next_full = t + grid < ntiles && full_tile(nbr, nbc);
@@ -377,20 +379,19 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
         }
       }
       __syncthreads();
-      for (int w = threadIdx.x; w < total * TPR; w += 256) {
-        const int k = w / TPR, x = w - k * TPR;
+      for (int w = threadIdx.x; w < total * CPW; w += 256) {
+        const int k = w / CPW, x = w - k * CPW;
         __stcs(reinterpret_cast<V4*>(Dt + (int64_t)sdst[b][k] * ldt + rb) + x,
                *reinterpret_cast<const V4*>(&sbuf[b][k][x * VW]));
       }
       if (NB == 1) __syncthreads();
     } else {
-      // edge or unaligned tile: element-wise (each thread: one column, 64/4 rows)
-      const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-      const int64_t c = cb + tx;
-      const int d = c < n2 ? colsel[c] : -1;
-      for (int k = ty; k < kPT; k += 4) {
-        const int64_t r = rb + k;
+      // edge or unaligned tile: element-wise (each thread: one column, TR/(256/TC) rows)
+      for (int e = threadIdx.x; e < TR * TC; e += 256) {
+        const int kk = e / TC, tx = e - kk * TC;
+        const int64_t c = cb + tx, r = rb + kk;
         if (r < nloc && c < n2) {
+          const int d = colsel[c];
           const T val = __ldcs(D + r * ldd + c);
           const T av = fabs(val);
           bad |= !isfinite(av);
@@ -424,10 +425,30 @@ cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2
                                int64_t ldt, unsigned long long* maxbits, int* nonfinite, int num_sms,
                                cudaStream_t st) {
   if (nloc == 0 || n2 == 0) return cudaSuccess;
-  const int64_t ntiles = ((nloc + kPT - 1) / kPT) * ((n2 + kPT - 1) / kPT);
-  const int64_t cap = (int64_t)num_sms * 8;
-  const unsigned blocks = (unsigned)(ntiles < cap ? ntiles : cap);
-  prep_select_kernel<T><<<blocks, 256, 0, st>>>(D, ldd, nloc, n2, colsel, Dt, ldt, maxbits, nonfinite);
+  static const int shape = [] {  // tile shape (tuning knob): 0 = 64 x 64, 1 = 32 x 128 rows x columns
+    const char* e = std::getenv("IRCUR_PREP_SHAPE");
+    return e ? std::atoi(e) : 1;   // fp32 at cfg5: 8.22 ms (32 x 128, 512-byte row runs) vs 8.47 ms (64 x 64)
+  }();
+  const bool wide = sizeof(T) == 4 && shape == 1;
+  const int tr = wide ? 32 : kPT, tc = wide ? 128 : kPT;
+  const int64_t ntiles = ((nloc + tr - 1) / tr) * ((n2 + tc - 1) / tc);
+  // persistent grid: every CTA resident (the loop strides over the tiles)
+  auto grid_for = [&](auto kern) {
+    static int per_sm = 0;
+    if (per_sm == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess)
+      per_sm = 4;
+    const int64_t cap = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
+    return (unsigned)(ntiles < cap ? ntiles : cap);
+  };
+  if constexpr (sizeof(T) == 4) {
+    if (wide) {
+      auto kern = prep_select_kernel<T, 32, 128>;
+      kern<<<grid_for(kern), 256, 0, st>>>(D, ldd, nloc, n2, colsel, Dt, ldt, maxbits, nonfinite);
+      return cudaGetLastError();
+    }
+  }
+  auto kern = prep_select_kernel<T, kPT, kPT>;
+  kern<<<grid_for(kern), 256, 0, st>>>(D, ldd, nloc, n2, colsel, Dt, ldt, maxbits, nonfinite);
   return cudaGetLastError();
 }
 

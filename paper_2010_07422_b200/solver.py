@@ -203,7 +203,11 @@ class Context:
                                                *[a.ctypes.data_as(pf) for a in arrs]))
         steps = np.zeros(max(n_iters, 1), dtype=np.int32)
         _capi.check(self.lib.ircur_get_svd_steps(self.h, n_iters, steps.ctypes.data_as(C.POINTER(C.c_int))))
+        marks = np.full(5, -1.0, dtype=np.float32)
+        _capi.check(self.lib.ircur_get_marks(self.h, marks.ctypes.data_as(pf)))
         return dict(launched_iters=li.value, kernel_launches=kl.value, svd_steps=steps[:n_iters],
+                    gaps_ms=dict(zip(("upload_to_prep", "prep", "prep_to_slab_end", "slab_to_run",
+                                      "run_to_first_kernel"), [float(x) for x in marks])),
                     core_ms=arrs[0][:n_iters], svd_ms=arrs[1][:n_iters],
                     strips_ms=arrs[2][:n_iters], finalize_ms=arrs[3][:n_iters])
 
@@ -488,6 +492,7 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     tick("draw")
     stream = torch.cuda.current_stream(dev).cuda_stream
     ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
+    ctx.set_profiling(bool(profile))
     ctx.set_indices(sets)
     tick("set_indices")
     cm, cover = _copy_plan(colmajor, n2, m_cols, sets, cfg)
@@ -527,7 +532,6 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
         cfg = replace(cfg, zeta0=max_abs)  # solver.py:342-344
     zetas = [cfg.gamma**k * cfg.zeta0 for k in range(cfg.max_iter)]
     mode = _capi.RESAMPLED if resampled else _capi.FIXED
-    ctx.set_profiling(bool(profile))
     prof = None
     if observer is None:
         iters, conv, errors, ms = ctx.run(zetas, cfg.eps, mode, cfg.max_iter)
