@@ -111,6 +111,14 @@ int ircur_append_indices(ircur_ctx_t ctx, int n_more, const int64_t* rows,
  * Between the two the host may append index sets and queue
  * ircur_slab_sqnorms_async, so its work overlaps the pass over D. */
 int ircur_prepare_async(ircur_ctx_t ctx, const void* D, int64_t ldd, int mode, int cover_sets);
+/* The same pass in row chunks [row_begin, row_end) of the local rows, in
+ * order, starting at 0 (row_begin % 4 == 0): lets the pass over rows already
+ * on the device run while the host streams in the rest of D (the caller
+ * orders each chunk after its copy, e.g. with an event on the context
+ * stream).  The chunk ending at the last row completes the pass like
+ * ircur_prepare_async. */
+int ircur_prepare_rows_async(ircur_ctx_t ctx, const void* D, int64_t ldd, int mode, int cover_sets,
+                             int64_t row_begin, int64_t row_end);
 int ircur_prepare_wait(ircur_ctx_t ctx, int* all_finite, double* max_abs);
 
 /* den = ||D(I_s,:)||_F^2, ||D(:,J_s)||_F^2 partial sums of the LOCAL rows

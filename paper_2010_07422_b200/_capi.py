@@ -34,6 +34,7 @@ PROTOTYPES = [
     ("ircur_prepare", _i, [_vp, _vp, _i64, _i, _pi, _pd]),
     ("ircur_prepare_sampled", _i, [_vp, _vp, _i64, _i, _pi, _pd]),
     ("ircur_prepare_async", _i, [_vp, _vp, _i64, _i, _i]),
+    ("ircur_prepare_rows_async", _i, [_vp, _vp, _i64, _i, _i, _i64, _i64]),
     ("ircur_prepare_wait", _i, [_vp, _pi, _pd]),
     ("ircur_draw_index_sets", _i, [_pu64, _i64, _i64, _i, _i, _i, _pi64, C.POINTER(C.c_int32), _pi64,
                                    C.POINTER(C.c_int32), _pu64]),

@@ -124,6 +124,7 @@ struct ircur_ctx {
   // [2..) slab norm partials
   unsigned long long* h_res = nullptr;
   bool prep_pending = false;
+  int64_t prep_next_row = 0;  // chunked prep: first row of the next chunk
   int slab_pending = -1, slab_nb_rows = 0, slab_nb_cols = 0;
   std::vector<cudaEvent_t> ev;
   // optional per-phase profiling: events [k][0..4] around core | svd | strips | finalize
@@ -306,7 +307,7 @@ FinalizeArgs finalize_args(ircur_ctx* c, int k, const IterSets& q, double eps, i
 
 // Sampled column-major copy covering the J sets [0, cover): column map,
 // per-set line indices, capacity, then one prep_select pass over D.
-int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfinite) {
+int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfinite, bool launch = true) {
   cover = std::max(1, std::min(cover, c->n_sets));
   cudaStream_t st = c->stream;
   IR_CUDA(cudaEventSynchronize(c->ev_stage));  // staging free to rewrite
@@ -345,14 +346,43 @@ int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfi
   IR_CUDA(cudaMemcpyAsync(c->d_colsel, sel, (size_t)c->n2 * sizeof(int), cudaMemcpyHostToDevice, st));
   IR_CUDA(cudaMemcpyAsync(c->d_cols_c, lines, nlines * sizeof(int), cudaMemcpyHostToDevice, st));
   IR_CUDA(cudaEventRecord(c->ev_stage, st));
-  if (c->dtype == IRCUR_F32)
-    IR_CUDA(launch_prep_select<float>((const float*)c->D, c->ldd, c->nloc, c->n2, c->d_colsel, (float*)c->Dt,
-                                      c->ldt, maxbits, nonfinite, c->num_sms, st));
-  else
-    IR_CUDA(launch_prep_select<double>((const double*)c->D, c->ldd, c->nloc, c->n2, c->d_colsel,
-                                       (double*)c->Dt, c->ldt, maxbits, nonfinite, c->num_sms, st));
+  if (launch) {
+    if (c->dtype == IRCUR_F32)
+      IR_CUDA(launch_prep_select<float>((const float*)c->D, c->ldd, c->nloc, c->n2, c->d_colsel, (float*)c->Dt,
+                                        c->ldt, maxbits, nonfinite, c->num_sms, st));
+    else
+      IR_CUDA(launch_prep_select<double>((const double*)c->D, c->ldd, c->nloc, c->n2, c->d_colsel,
+                                         (double*)c->Dt, c->ldt, maxbits, nonfinite, c->num_sms, st));
+  }
   c->dt_mode = 2;
   c->covered = cover;
+  return IRCUR_OK;
+}
+
+// The prep pass over local rows [r0, r1) of D (the copy plan of dt_mode is
+// in place): finite flag / max|D| into maxbits / flags[3], rows into Dt.
+int prep_rows(ircur_ctx* c, int64_t r0, int64_t r1) {
+  cudaStream_t st = c->stream;
+  const int64_t nr = r1 - r0;
+  if (c->dtype == IRCUR_F32) {
+    const float* D = (const float*)c->D + r0 * c->ldd;
+    float* Dt = c->Dt ? (float*)c->Dt + r0 : nullptr;
+    if (c->dt_mode == 2)
+      IR_CUDA(launch_prep_select<float>(D, c->ldd, nr, c->n2, c->d_colsel, Dt, c->ldt, c->maxbits, c->flags + 3,
+                                        c->num_sms, st));
+    else
+      IR_CUDA(launch_prep<float>(D, c->ldd, nr, c->n2, c->dt_mode == 1 ? Dt : nullptr, c->ldt, c->maxbits,
+                                 c->flags + 3, c->num_sms, st));
+  } else {
+    const double* D = (const double*)c->D + r0 * c->ldd;
+    double* Dt = c->Dt ? (double*)c->Dt + r0 : nullptr;
+    if (c->dt_mode == 2)
+      IR_CUDA(launch_prep_select<double>(D, c->ldd, nr, c->n2, c->d_colsel, Dt, c->ldt, c->maxbits,
+                                         c->flags + 3, c->num_sms, st));
+    else
+      IR_CUDA(launch_prep<double>(D, c->ldd, nr, c->n2, c->dt_mode == 1 ? Dt : nullptr, c->ldt, c->maxbits,
+                                  c->flags + 3, c->num_sms, st));
+  }
   return IRCUR_OK;
 }
 
@@ -565,56 +595,67 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   return IRCUR_OK;
 }
 
-int ircur_prepare_async(ircur_ctx_t c, const void* D, int64_t ldd, int mode, int cover_sets) {
+int ircur_prepare_rows_async(ircur_ctx_t c, const void* D, int64_t ldd, int mode, int cover_sets, int64_t row_begin,
+                             int64_t row_end) {
   if (!c || !D) return fail(IRCUR_EINVAL, "null context or D");
   if (ldd < c->n2) return fail(IRCUR_EINVAL, "ldd < n2");
   if (mode < 0 || mode > 2) return fail(IRCUR_EINVAL, "mode must be 0 (no copy), 1 (full) or 2 (sampled)");
-  if (mode == 2 && c->n_sets < 1) return fail(IRCUR_EINVAL, "upload the index sets before a sampled prep");
-  if (mode == 2 && cover_sets < 1) return fail(IRCUR_EINVAL, "cover_sets must be >= 1");
+  if (row_begin < 0 || row_end <= row_begin || row_end > c->nloc || (row_begin % 4) != 0)
+    return fail(IRCUR_EINVAL, "row range must satisfy 0 <= begin < end <= local rows, begin % 4 == 0");
   IR_CUDA(cudaSetDevice(c->device));
-  c->D = D;
-  c->ldd = ldd;
-  c->has_state = false;
-  c->covered = 0;
-  c->slab_pending = -1;
   cudaStream_t st = c->stream;
-  mark(c, 1);
-  IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), st));
-  IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), st));
-  if (mode == 2) {
-    c->dt_mode = 0;  // (an allocation from an earlier solve is reused when large enough)
-    if (int rc = build_cover(c, cover_sets, c->maxbits, c->flags + 3)) return rc;
-  } else {
-    if (mode == 1 && (!c->Dt || c->dt_cap < c->n2)) {
-      if (c->Dt) {
+  if (row_begin == 0) {  // first chunk: plan the pass
+    if (mode == 2 && c->n_sets < 1) return fail(IRCUR_EINVAL, "upload the index sets before a sampled prep");
+    if (mode == 2 && cover_sets < 1) return fail(IRCUR_EINVAL, "cover_sets must be >= 1");
+    c->D = D;
+    c->ldd = ldd;
+    c->has_state = false;
+    c->covered = 0;
+    c->slab_pending = -1;
+    c->prep_next_row = 0;
+    mark(c, 1);
+    IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), st));
+    IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), st));
+    if (mode == 2) {
+      c->dt_mode = 0;  // (an allocation from an earlier solve is reused when large enough)
+      if (int rc = build_cover(c, cover_sets, c->maxbits, c->flags + 3, false)) return rc;
+    } else {
+      if (mode == 1 && (!c->Dt || c->dt_cap < c->n2)) {
+        if (c->Dt) {
+          IR_CUDA(cudaStreamSynchronize(st));
+          cudaFree(c->Dt);
+        }
+        c->ldt = pad4(c->nloc);
+        c->Dt = nullptr;
+        c->dt_cap = 0;
+        IR_CUDA(cudaMalloc(&c->Dt, (size_t)c->n2 * c->ldt * c->esz));
+        c->dt_cap = c->n2;
+      }
+      if (mode == 0 && c->Dt) {
         IR_CUDA(cudaStreamSynchronize(st));
         cudaFree(c->Dt);
+        c->Dt = nullptr;
+        c->dt_cap = 0;
       }
-      c->ldt = pad4(c->nloc);
-      c->Dt = nullptr;
-      c->dt_cap = 0;
-      IR_CUDA(cudaMalloc(&c->Dt, (size_t)c->n2 * c->ldt * c->esz));
-      c->dt_cap = c->n2;
+      c->dt_mode = mode;
     }
-    if (mode == 0 && c->Dt) {
-      IR_CUDA(cudaStreamSynchronize(st));
-      cudaFree(c->Dt);
-      c->Dt = nullptr;
-      c->dt_cap = 0;
-    }
-    c->dt_mode = mode;
-    if (c->dtype == IRCUR_F32)
-      IR_CUDA(launch_prep<float>((const float*)D, ldd, c->nloc, c->n2, (float*)c->Dt, c->ldt, c->maxbits,
-                                 c->flags + 3, c->num_sms, st));
-    else
-      IR_CUDA(launch_prep<double>((const double*)D, ldd, c->nloc, c->n2, (double*)c->Dt, c->ldt,
-                                  c->maxbits, c->flags + 3, c->num_sms, st));
+  } else if (D != c->D || ldd != c->ldd || mode != c->dt_mode || row_begin != c->prep_next_row) {
+    return fail(IRCUR_EINVAL, "row chunks must continue the pass started at row 0 (same D, ldd, mode, in order)");
   }
-  IR_CUDA(cudaMemcpyAsync(c->h_res, c->maxbits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  IR_CUDA(cudaMemcpyAsync(c->h_res + 1, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
-  mark(c, 2);
-  c->prep_pending = true;
+  if (int rc = prep_rows(c, row_begin, row_end)) return rc;
+  c->prep_next_row = row_end;
+  if (row_end == c->nloc) {
+    IR_CUDA(cudaMemcpyAsync(c->h_res, c->maxbits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    IR_CUDA(cudaMemcpyAsync(c->h_res + 1, c->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
+    mark(c, 2);
+    c->prep_pending = true;
+  }
   return IRCUR_OK;
+}
+
+int ircur_prepare_async(ircur_ctx_t c, const void* D, int64_t ldd, int mode, int cover_sets) {
+  if (!c) return fail(IRCUR_EINVAL, "null context");
+  return ircur_prepare_rows_async(c, D, ldd, mode, cover_sets, 0, c->nloc);
 }
 
 int ircur_prepare_wait(ircur_ctx_t c, int* all_finite, double* max_abs) {

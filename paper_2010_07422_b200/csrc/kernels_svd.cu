@@ -305,7 +305,6 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long l
     double offl = 0.0;
     const bool rec = dbg && blockIdx.x == 0 && tid == 0;
     for (int rd = 0; rd < nrd; ++rd) {
-      long long tr0 = rec ? clock64() : 0;
       if (tid < nply / 2) {
         int p = circle_player(tid, rd, nrd), q = circle_player(nply - 1 - tid, rd, nrd);
         if (p > q) { const int t = p; p = q; q = t; }
@@ -332,9 +331,7 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long l
           prt[p] = p;
         }
       }
-      long long tr1 = rec ? clock64() : 0;
       eig_sync();
-      long long tr2 = rec ? clock64() : 0;
       const bool lastrd = rd == nrd - 1;
       if (act) {
         // row a:  H' = J^T H J  restricted to (a, b):  rows a, pa then columns b, pb
@@ -361,12 +358,7 @@ __device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long l
         for (int o = 16; o > 0; o >>= 1) offl = fmax(offl, __shfl_xor_sync(0xffffffffu, offl, o));
         if (lane == 0) offw[4 * (sweep & 1) + wq] = offl;
       }
-      long long tr3 = rec ? clock64() : 0;
       eig_sync();
-      if (rec) {
-        const long long tr4 = clock64();
-        dbg[11] += tr1 - tr0; dbg[12] += tr2 - tr1; dbg[15] += tr3 - tr2; dbg[6] += tr4 - tr3;
-      }
       double* t = H; H = Hn; Hn = t;
       t = Z; Z = Zn; Zn = t;
     }
@@ -762,6 +754,8 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
 
   // ---- 7. Rayleigh-Ritz on U itself: Y = U V (my m-rows), H2 = Y^T Y
   const long long tfin0 = clock64();
+  long long tf = tfin0;
+#define FPH(i) do { if (a.dbg && q == 0 && tid == 0) { const long long _t = clock64(); a.dbg[24 + (i)] += _t - tf; tf = _t; } } while (0)
   const double* Vf = scrX;  // published before the loop's last cluster sync
   // keep G X of the last step (my n-rows): QJ = G (X Z) Sigma^-1 = (G X) Z Sigma^-1
   if (gx_valid) {
@@ -772,6 +766,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     __syncthreads();
   }
   tiled_product(a.U + (int64_t)mlo * a.ldu, a.ldu, mr, n, Vf, kLdV, KP, kk, S.Xq, S.P, L.S);
+  FPH(0);
   {
     double* rb = S.red + buf * RL;
     for (int e = tid; e < kk * kk; e += kSvdNT) {
@@ -783,6 +778,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     cluster_sum(cl, S, buf, kk * kk);
     buf ^= 1;
   }
+  FPH(1);
   if (eigt) {
     for (int e = tid; e < kk * kk; e += kEigNT) {
       const int c1 = e / kk, c2 = e - c1 * kk;
@@ -794,6 +790,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     if (a.dbg && q == 0 && tid == 0) a.dbg[12] += clock64() - tj0;
   }
   __syncthreads();
+  FPH(2);
   rotate_rows(S.Xq, mr, KP, kk, S.Z, HL, S.P);
   // rotated V: my rows into Vq and into the other scratch buffer (for QJ)
   double* Vr = scr[0];  // free: both block buffers are dead after the loop
@@ -817,6 +814,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   }
   if (tid < kk) S.lam[tid] = sqrt(S.rout[tid]);  // sigma
   __syncthreads();
+  FPH(3);
   const double smax = S.lam[0];
   // ---- 8. outputs
   T* Wr = reinterpret_cast<T*>(a.Wr);
@@ -860,6 +858,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     a.V[(int64_t)(lo + i) * r + c] = vv;
     VS[(int64_t)(lo + i) * r + c] = (T)vs;
   }
+  FPH(4);
   // QJ = U^T W = G V Sigma^{-1} for my n-rows (zero for deficient columns)
   if (gx_valid) rotate_rows(S.Bq, nr, KP, kk, S.Z, HL, S.P);
   else tiled_product(Gq, ldgq, nr, n, Vr, kLdV, KP, kk, S.Bq, S.P, L.S);
@@ -873,7 +872,9 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     QJ[(int64_t)(lo + i) * r + c] = (T)v;
   }
   __threadfence();
+  FPH(5);
   cl.sync();
+  FPH(6);
   if (ndef > 0 && q == 0) {
     // CGS2 completion of W's deficient columns with unit-vector candidates
     double* dots = S.rout;
@@ -925,6 +926,8 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     const int i = e / r, c = e - i * r;
     Wr[(int64_t)(mlo + i) * r + c] = (T)a.W[(int64_t)(mlo + i) * r + c];
   }
+  FPH(7);
+#undef FPH
   if (a.dbg && q == 0 && tid == 0) a.dbg[11] += clock64() - tfin0;
 }
 

@@ -106,6 +106,14 @@ class Context:
         self.colmajor = mode
         _capi.check(self.lib.ircur_prepare_async(self.h, C.c_void_p(_ptr(D)), D.stride(0), mode, int(cover)))
 
+    def prepare_rows_async(self, D: torch.Tensor, colmajor, cover: int, r0: int, r1: int) -> None:
+        """One row chunk [r0, r1) of the prep pass (chunks in order from 0)."""
+        self._D = D
+        mode = int(colmajor)
+        self.colmajor = mode
+        _capi.check(self.lib.ircur_prepare_rows_async(self.h, C.c_void_p(_ptr(D)), D.stride(0), mode, int(cover),
+                                                      int(r0), int(r1)))
+
     def prepare_wait(self) -> float:
         ok = C.c_int(0)
         mx = C.c_double(0.0)
@@ -351,6 +359,53 @@ def _device_matrix(D, device, compute_dtype) -> torch.Tensor:
     return t
 
 
+_STREAM_CHUNKS = 16          # row chunks of a host D streamed in under the prep pass
+_STREAM_MIN_BYTES = 256 << 20
+_copy_streams: dict = {}
+
+
+def _host_source(D, device, compute_dtype):
+    """(host tensor, device dtype) when D is a contiguous host matrix worth
+    streaming in chunks (the prep pass then runs under the copy), else None."""
+    if isinstance(D, torch.Tensor):
+        if D.is_cuda:
+            return None
+        t = D
+    elif isinstance(D, np.ndarray) and D.dtype in (np.float32, np.float64):
+        t = torch.from_numpy(D)
+    else:
+        return None
+    if t.ndim != 2 or not t.is_contiguous() or t.numel() * t.element_size() < _STREAM_MIN_BYTES:
+        return None
+    want = compute_dtype or (torch.float32 if t.dtype == torch.float32 else torch.float64)
+    if t.dtype != want:
+        return None
+    return t, want
+
+
+def _stream_in(Dh: torch.Tensor, Dd: torch.Tensor, ctx: "Context", cm: int, cover: int) -> None:
+    """Copy host rows into Dd chunk by chunk on a side stream and queue each
+    chunk's prep pass on the context stream behind its copy."""
+    dev = Dd.device
+    cs = _copy_streams.get(dev.index)
+    if cs is None:
+        cs = _copy_streams[dev.index] = torch.cuda.Stream(device=dev)
+    cur = torch.cuda.current_stream(dev)
+    cs.wait_stream(cur)  # Dd's allocation / earlier users
+    Dd.record_stream(cs)
+    n1 = Dd.shape[0]
+    step = max(64, -(-n1 // _STREAM_CHUNKS))
+    step = -(-step // 64) * 64
+    for r0 in range(0, n1, step):
+        r1 = min(n1, r0 + step)
+        with torch.cuda.stream(cs):
+            Dd[r0:r1].copy_(Dh[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        cur.wait_event(ev)
+        ctx.prepare_rows_async(Dd, cm, cover, r0, r1)
+
+
 def _want_colmajor(colmajor, n1, n2, m_cols, dtype_size, mode) -> bool:
     env = os.environ.get("IRCUR_COLMAJOR")
     if env is not None:
@@ -470,7 +525,14 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     """
     cfg = config
     tick = _Ticker(profile)
-    Dd = _device_matrix(D, device, compute_dtype)
+    src = _host_source(D, device, compute_dtype) if torch.cuda.is_available() else None
+    if src is not None:  # host D: allocate here, stream the rows in under the prep pass
+        Dh, want = src
+        Dd = torch.empty(tuple(Dh.shape), dtype=want,
+                         device=torch.device("cuda", device if device is not None else torch.cuda.current_device()))
+    else:
+        Dh = None
+        Dd = _device_matrix(D, device, compute_dtype)
     if Dd.numel() == 0:
         raise ValueError("D must be nonempty")
     n1, n2 = int(Dd.shape[0]), int(Dd.shape[1])
@@ -507,7 +569,10 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     try:
         # the pass over D runs while the host draws and uploads the tail of
         # the index sequence and queues the den == 0 check
-        ctx.prepare_async(Dd, cm, cover)
+        if Dh is not None:
+            _stream_in(Dh, Dd, ctx, cm, cover)
+        else:
+            ctx.prepare_async(Dd, cm, cover)
     finally:
         if n_first < n_sets:
             worker.join()

@@ -240,3 +240,49 @@ def test_slab_sqnorms_match_numpy(ir, dtype, colmajor, offset):
         assert a == pytest.approx(float((Dn[I, :] ** 2).sum()), rel=1e-12)
         assert b == pytest.approx(float((Dn[:, J] ** 2).sum()), rel=1e-12)
     ctx.close()
+
+
+@pytest.mark.parametrize("colmajor", ["sampled", "full", False])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_streamed_host_input_matches_device_input(ir, monkeypatch, colmajor, dtype):
+    """A host D is copied in row chunks with the prep pass queued behind each
+    chunk (solver._stream_in); the results must be bitwise those of the same
+    D passed as a device tensor, and NaN in the last chunk is still
+    rejected.  Streaming is forced on a small matrix (several chunks,
+    a ragged last chunk)."""
+    from paper_2010_07422_b200 import solver
+    monkeypatch.setattr(solver, "_STREAM_MIN_BYTES", 0)
+    monkeypatch.setattr(solver, "_STREAM_CHUNKS", 5)
+    n1, n2, r = 700, 520, 3
+    rng = np.random.default_rng(11)
+    L = rng.standard_normal((n1, r)) @ rng.standard_normal((r, n2))
+    S = np.where(rng.random((n1, n2)) < 0.05, 10.0 * rng.standard_normal((n1, n2)), 0.0)
+    D = (L + S).astype(dtype)
+    cfg = ir.SolverConfig(rank=r, mode="resampled", max_iter=30, seed=ir.RngSeed(5))
+    a = ir.solve(D, cfg, device=0, colmajor=colmajor)
+    b = ir.solve(torch.from_numpy(D).cuda(), cfg, device=0, colmajor=colmajor)
+    assert a[2].iterations == b[2].iterations and a[2].errors == b[2].errors
+    np.testing.assert_array_equal(a[0].C, b[0].C)
+    np.testing.assert_array_equal(a[0].R, b[0].R)
+    np.testing.assert_array_equal(a[1].row_values, b[1].row_values)
+    D[n1 - 3, 7] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        ir.solve(D, cfg, device=0, colmajor=colmajor)
+
+
+def test_prepare_rows_rejects_out_of_order_chunks(ir):
+    """ircur_prepare_rows_async chunks must start at row 0 and continue in
+    order (include/ircur_b200.h)."""
+    from paper_2010_07422_b200 import _capi
+    from paper_2010_07422_b200.solver import Context
+    D = torch.randn(256, 64, device="cuda")
+    ctx = Context(0, _capi.F32, 256, 64, 2, 16, 16, 4)
+    ctx.set_indices(ir.draw_index_sets(256, 64, 16, 16, ir.RngSeed(1), 1))
+    with pytest.raises(Exception):
+        ctx.prepare_rows_async(D, 0, 1, 64, 128)  # no pass started at row 0
+    ctx.prepare_rows_async(D, 0, 1, 0, 64)
+    with pytest.raises(Exception):
+        ctx.prepare_rows_async(D, 0, 1, 128, 256)  # gap
+    ctx.prepare_rows_async(D, 0, 1, 64, 256)
+    assert ctx.prepare_wait() == float(D.abs().max())
+    ctx.close()

@@ -37,6 +37,8 @@ for i in range(a.solves):
     print(f"  ritz: chol={cyc[8]/1e6:.2f} solves={cyc[9]/1e6:.2f} jacobi={cyc[10]/1e6:.2f} Mcyc, "
           f"eig calls={cyc[14]} sweeps={cyc[13]}; final extraction={cyc[11]/1e6:.2f} Mcyc "
           f"(its jacobi {cyc[12]/1e6:.2f})")
+    fn = ["UV", "H2sum", "jacobi", "rotate+norms", "outputs", "QJ", "sync", "W+Wr"]
+    print("  final extraction (Mcycles): " + " ".join(f"{n}={c/1e6:.2f}" for n, c in zip(fn, cyc[24:32])))
     sn = ["stage_wait", "pass1", "reduce", "override+write", "pass2", "sync+issue", "lvec+loop"]
     if os.environ.get("IRCUR_STRIPS_VER", "3") != "1":
         sn = ["stage(issue+wait)", "pass1", "sync_after_pass1", "reduce+write+sync", "pass2", "final_sync", "loop"]
