@@ -36,8 +36,10 @@ CONFIGS = {
     "cfg1": (1000, 1000, 5, 0.1, "f64", 0),
     "cfg2": (10000, 10000, 5, 0.2, "f32", 1),
     "cfg2f64": (10000, 10000, 5, 0.2, "f64", 1),
+    "cfg4": (2000, 2000, 5, 0.2, "f32", 3),     # x BATCH["cfg4"] independent problems
     "cfg5": (100000, 100000, 10, 0.2, "f32", 4),
 }
+BATCH = {"cfg4": 512}  # problem-parallel configs: problems per batch (data/solver seeds 1000 + p)
 DATA_SEED = 0
 SOLVER_SEED = 1
 GAMMA = 0.7
@@ -71,6 +73,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: skip the nvidia-smi sampler")
     ap.add_argument("--no-profile", action="store_true", help="diagnostics: no per-kernel events")
+    ap.add_argument("--batch-streams", type=int, default=16,
+                    help="cfg4: host threads / CUDA streams driving independent problems")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded NCCL path even at N=1 (tests the multi-GPU code on one GPU)")
     return ap.parse_args()
@@ -369,6 +373,151 @@ def run_sharded(args, rank, world, local):
 
 
 # ------------------------------------------------------------- CPU oracle
+def run_batch(args):
+    """Problem-parallel workload (BASELINE.json cfg4: 512 independent 2000^2
+    fp32 problems, seeds 1000 + p).  One step = solving the whole batch:
+    `--batch-streams` host threads, each with its own CUDA stream and library
+    context, drive solve_device over their share of the problems (ctypes
+    releases the GIL, so the small per-problem kernels of several problems
+    overlap on the GPU).  On N GPUs each rank takes 1/N of the problems (no
+    traffic); timed with CUDA events fenced across the worker streams."""
+    import threading
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_07422_b200 as ir
+    from paper_2010_07422_b200 import _build, gen
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+    n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
+    nb = BATCH[args.config]
+    mine = list(range(rank, nb, world))
+    cm = COLMAJOR[args.colmajor]
+    probs, cfgs = [], []
+    for p in mine:
+        D, linf, _ = gen.baseline_problem_device(n1, n2, r, alpha, 1000 + p, dtype=torch.float32)
+        probs.append(D)
+        cfgs.append(ir.SolverConfig(rank=r, eps=EPS, zeta0=linf, gamma=GAMMA, mode=args.mode, max_iter=MAX_ITER,
+                                    seed=ir.RngSeed(1000 + p)))
+    ns = max(1, min(args.batch_streams, len(probs)))
+    streams = [torch.cuda.Stream() for _ in range(ns)]
+    stats = [dict(strip_ms=0.0, strip_bytes=0, iters=0, launches=0, solves=0) for _ in range(ns)]
+    s = 4
+
+    def batch_once(record):
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        main = torch.cuda.current_stream()
+        start.record(main)
+        done = [torch.cuda.Event() for _ in range(ns)]
+
+        def worker(w):
+            st = streams[w]
+            st.wait_event(start)
+            with torch.cuda.stream(st):
+                for i in range(w, len(probs), ns):
+                    res = ir.solve_device(probs[i], cfgs[i], colmajor=cm, fetch_factors=False,
+                                          profile="deferred" if record else False)
+                    if record:
+                        p = res.read_profile()
+                        it = res.trace.iterations
+                        d = stats[w]
+                        d["strip_ms"] += float(np.sum(p["strips_ms"][:it]))
+                        d["strip_bytes"] += sum(algorithmic_strip_bytes(s, n1, n2, r, res.trace.sampled_rows[k],
+                                                                         res.trace.sampled_cols[k])
+                                                for k in range(it))
+                        d["iters"] += it
+                        d["launches"] += 2 + p["kernel_launches"]
+                        d["solves"] += 1
+                done[w].record(st)
+
+        th = [threading.Thread(target=worker, args=(w,)) for w in range(ns)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for e in done:
+            main.wait_event(e)
+        stop.record(main)
+        torch.cuda.synchronize()
+        return start.elapsed_time(stop)
+
+    for _ in range(args.warmup):
+        batch_once(False)
+    for d in stats:
+        d.update(strip_ms=0.0, strip_bytes=0, iters=0, launches=0, solves=0)
+    with ClockSampler(-1 if args.no_clocks else local) as clk:
+        if world > 1:
+            dist.barrier()
+        step_ms = [batch_once(True) for _ in range(args.steps)]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    tot = {k: sum(d[k] for d in stats) for k in stats[0]}
+    peak, peak_kind = peaks()
+    n_strip = max(1, tot["iters"])
+    achieved = tot["strip_bytes"] / (tot["strip_ms"] / 1e3) / 1e9 if tot["strip_ms"] > 0 else None
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (BASELINE.json generator on device, numpy-PCG64-exact), seeds 1000 + p",
+        "config": {"workload": args.config, "problems": nb, "n1": n1, "n2": n2, "rank": r, "alpha": alpha,
+                   "mode": args.mode, "gamma": GAMMA, "eps": EPS, "zeta0": "max|L|",
+                   "streams_per_gpu": ns, "mean_iterations": tot["iters"] / max(1, tot["solves"]),
+                   "l2": "8 GB of problems cycled per batch (> L2), no flush",
+                   "parallelism": f"problem-parallel over {world} GPU(s), no communication"},
+        "step_ms": step_ms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "strips3_kernel", "avg_launch_us": tot["strip_ms"] / n_strip * 1e3,
+                     "bytes_per_launch": tot["strip_bytes"] / n_strip,
+                     "note": "strip launches overlap across streams: per-launch times include the sharing"},
+        "gpu_launches": tot["launches"] // max(1, args.steps),
+        "clocks": clk.summary(),
+    }
+    if args.e2e_steps > 0:
+        hosts = [torch.empty((n1, n2), dtype=torch.float32, pin_memory=True) for _ in probs]
+        for h, d in zip(hosts, probs):
+            h.copy_(d)
+        out = ir.solve_batch(hosts, cfgs, streams=ns, colmajor=cm)  # warm (contexts, page-locked result blocks)
+        del out
+        times = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = ir.solve_batch(hosts, cfgs, streams=ns, colmajor=cm)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            d2h = sum(8 * (c.C.size + c.R.size + sp.row_values.size + sp.col_values.size) for c, sp, _ in out)
+            del out
+        line["e2e"] = {"value": float(np.mean(times)), "unit": "s",
+                       "h2d_bytes_per_step": int(len(hosts) * n1 * n2 * 4), "d2h_bytes_per_step": int(d2h),
+                       "api": "paper_2010_07422_b200.solve_batch(pinned host problems)"}
+        if not args.no_cpu_baseline and rank == 0:
+            D0 = probs[0].double().cpu().numpy()
+            cb = cpu_baseline(D0, args.config, cfgs[0], 0, args.cpu_budget)
+            cb["value"] *= nb
+            cb["sample"] = f"problem 0 of {nb}: " + cb["sample"] + f", x{nb} problems"
+            line["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def cpu_baseline(Dh, config, cfg, gpu_iters, budget):
     """Reference algorithm (oracle port, fp64 arithmetic like the reference)
     on this host's cores.  Small problems: full solves.  n = 1e5: a bounded
@@ -431,6 +580,10 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(cb["value"])
     v = float(np.mean(vals))
+    nb = BATCH.get(args.config, 1)
+    if nb > 1:  # problem-parallel config: one problem timed, the batch is nb of them
+        v *= nb
+        cb["sample"] = f"one problem of {nb}: " + cb["sample"] + f", x{nb} problems"
     cb["value"] = v
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
@@ -448,6 +601,9 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config in BATCH:
+        run_batch(args)
         return
     run_ours(args)
 

@@ -218,6 +218,23 @@ int ircur_materialize(ircur_ctx_t ctx, void* L, int64_t ldl, int out_dtype);
  * (ircur_set_profiling), read back as per-iteration milliseconds, plus the
  * number of iterations launched and kernels launched by the last ircur_run. */
 int ircur_set_profiling(ircur_ctx_t ctx, int on);
+/* One whole single-GPU solve, natively (the host sequence of
+ * paper_2010_07422_b200.solve_device, solver.py:304-416): the index draws
+ * from the PCG64 state `pcg` (6 words, see ircur_draw_index_sets; the first
+ * sets before the prep pass, the rest while it runs), the column-major copy
+ * plan (colmajor 0 none, 1 full, 2 sampled, 3 full when the covered columns
+ * exceed 70% of D, else sampled), the prep pass, the den == 0 check, the
+ * threshold schedule zeta_k = gamma^k zeta0 (zeta0 <= 0: max|D|) and the loop.
+ * rows/cols receive the drawn sets (max_iter x max_rows / max_cols, zero
+ * padded; one set in fixed mode), errors / iter_ms max_iter entries.  Results
+ * are then read with ircur_get_strips etc. like after ircur_run.  The whole
+ * call runs without the caller's interpreter (batched problems from several
+ * host threads). */
+int ircur_solve(ircur_ctx_t ctx, const void* D, int64_t ldd, const uint64_t* pcg, double zeta0, double gamma,
+                double eps, int mode, int max_iter, int colmajor, int64_t* rows, int32_t* row_counts,
+                int64_t* cols, int32_t* col_counts, int* iterations, int* converged, double* errors,
+                float* iter_ms, double* zeta0_used, int* copy_mode, int* zero_state);
+
 /* Device-side gaps of the last solve while profiling (ms): upload of the
  * index sets -> prep begin, prep pass, prep end -> slab norms queued, slab
  * end -> ircur_run, ircur_run -> first loop kernel; -1 when not recorded. */

@@ -43,6 +43,8 @@ PROTOTYPES = [
     ("ircur_slab_sqnorms", _i, [_vp, _i, _pd, _pd]),
     ("ircur_slab_sqnorms_async", _i, [_vp, _i]),
     ("ircur_run", _i, [_vp, _pd, _d, _i, _i, _pi, _pi, _pd, _pf]),
+    ("ircur_solve", _i, [_vp, _vp, _i64, _pu64, _d, _d, _d, _i, _i, _i, _pi64, C.POINTER(C.c_int32), _pi64,
+                         C.POINTER(C.c_int32), _pi, _pi, _pd, _pf, _pd, _pi, _pi]),
     ("ircur_iterate", _i, [_vp, _i, _i, _d, _pd]),
     ("ircur_shard_buffers", _i, [_vp, C.POINTER(_vp), _pi64, C.POINTER(_vp), _pi64, C.POINTER(_vp)]),
     ("ircur_shard_reset", _i, [_vp]),

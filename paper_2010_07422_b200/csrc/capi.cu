@@ -854,13 +854,16 @@ int reset_loop(ircur_ctx* c) {
 // Wait for the stream, read the device trace, remember the final state.
 int read_trace(ircur_ctx* c, const double* zetas, int mode, int* iterations, int* converged,
                double* errors, float* iter_ms) {
-  IR_CUDA(cudaStreamSynchronize(c->stream));
   int hflags[3] = {0, 0, 0};
-  IR_CUDA(cudaMemcpy(hflags, c->flags, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  IR_CUDA(cudaMemcpyAsync(hflags, c->flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
   const int iters = hflags[1];
   if (iterations) *iterations = iters;
   if (converged) *converged = hflags[2];
-  if (errors && iters > 0) IR_CUDA(cudaMemcpy(errors, c->errors, iters * sizeof(double), cudaMemcpyDeviceToHost));
+  if (errors && iters > 0) {
+    IR_CUDA(cudaMemcpyAsync(errors, c->errors, iters * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    IR_CUDA(cudaStreamSynchronize(c->stream));
+  }
   if (iter_ms) {
     for (int k = 0; k < iters; ++k) {
       float ms = 0.f;
@@ -917,6 +920,79 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
     }
   }
   return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
+}
+
+int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, double zeta0, double gamma,
+                double eps, int mode, int max_iter, int colmajor, int64_t* rows, int32_t* row_counts, int64_t* cols,
+                int32_t* col_counts, int* iterations, int* converged, double* errors, float* iter_ms,
+                double* zeta0_used, int* copy_mode, int* zero_state) {
+  if (!c || !D || !pcg || !rows || !row_counts || !cols || !col_counts)
+    return fail(IRCUR_EINVAL, "null context, D, generator state or index buffers");
+  if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
+  if (c->nloc != c->n1) return fail(IRCUR_EINVAL, "row-sharded context: use the shard phases");
+  if (!(gamma > 0.0 && gamma < 1.0) || !(eps > 0.0)) return fail(IRCUR_EINVAL, "need 0 < gamma < 1 and eps > 0");
+  if (colmajor < 0 || colmajor > 3) return fail(IRCUR_EINVAL, "colmajor must be 0..3");
+  if (c->n1 > 0x100000000ll || c->n2 > 0x100000000ll) return fail(IRCUR_EINVAL, "dimension above 2^32");
+  const bool resampled = mode == IRCUR_RESAMPLED;
+  const int n_sets = resampled ? max_iter : 1;
+  const int est = (int)std::ceil(std::log(eps) / std::log(gamma));
+  const int n_first = resampled ? std::min(n_sets, est + 8) : n_sets;
+  const int mr = c->max_rows, mc = c->max_cols;
+  std::memset(rows, 0, (size_t)n_sets * mr * sizeof(int64_t));
+  std::memset(cols, 0, (size_t)n_sets * mc * sizeof(int64_t));
+  uint64_t st1[6];
+  // draws the prep pass needs first (sampling.py:93-104, solver.py:325-329)
+  if (int rc = ircur_draw_index_sets(pcg, c->n1, c->n2, mr, mc, n_first, rows, row_counts, cols, col_counts, st1))
+    return fail(rc, "index draws failed");
+  if (int rc = ircur_set_indices(c, n_first, rows, row_counts, cols, col_counts)) return rc;
+  // copy plan (solver._copy_plan): 3 = full copy when the covered columns exceed 70% of D
+  int cm = colmajor, cover = 0;
+  if (cm >= 2) {
+    cover = resampled ? std::max(1, std::min(n_first, est + 8)) : 1;
+    if (cm == 3) {
+      std::vector<unsigned char> mark((size_t)c->n2, 0);
+      int64_t u = 0;
+      for (int s = 0; s < cover; ++s)
+        for (int j = 0; j < col_counts[s]; ++j) {
+          unsigned char& m = mark[(size_t)cols[(size_t)s * mc + j]];
+          u += !m;
+          m = 1;
+        }
+      cm = u > 0.7 * (double)c->n2 ? 1 : 2;
+      if (cm == 1) cover = 0;
+    }
+  }
+  if (copy_mode) *copy_mode = cm;
+  if (int rc = ircur_prepare_async(c, D, ldd, cm, cover)) return rc;
+  // the rest of the sequence is drawn and uploaded while the pass runs
+  if (n_first < n_sets) {
+    const int nm = n_sets - n_first;
+    if (int rc = ircur_draw_index_sets(st1, c->n1, c->n2, mr, mc, nm, rows + (size_t)n_first * mr,
+                                       row_counts + n_first, cols + (size_t)n_first * mc, col_counts + n_first,
+                                       nullptr))
+      return fail(rc, "index draws failed");
+    if (int rc = ircur_append_indices(c, nm, rows + (size_t)n_first * mr, row_counts + n_first,
+                                      cols + (size_t)n_first * mc, col_counts + n_first))
+      return rc;
+  }
+  if (int rc = ircur_slab_sqnorms_async(c, 0)) return rc;
+  double mx = 0.0;
+  if (int rc = ircur_prepare_wait(c, nullptr, &mx)) return rc;
+  double a = 0.0, b = 0.0;
+  if (int rc = ircur_slab_sqnorms(c, 0, &a, &b)) return rc;
+  if (zero_state) *zero_state = 0;
+  if (std::sqrt(a) + std::sqrt(b) == 0.0) {  // solver.py:335-341
+    if (zero_state) *zero_state = 1;
+    if (iterations) *iterations = 0;
+    if (converged) *converged = 1;
+    if (errors) errors[0] = 0.0;
+    return IRCUR_OK;
+  }
+  const double z0 = zeta0 > 0.0 ? zeta0 : mx;  // solver.py:342-344 (zeta0 None -> max|D|)
+  if (zeta0_used) *zeta0_used = z0;
+  std::vector<double> zetas((size_t)max_iter);
+  for (int k = 0; k < max_iter; ++k) zetas[k] = std::pow(gamma, (double)k) * z0;  // solver.py:372
+  return ircur_run(c, zetas.data(), eps, mode, max_iter, iterations, converged, errors, iter_ms);
 }
 
 int ircur_shard_buffers(ircur_ctx_t c, void** U, int64_t* u_elems, void** Qpart, int64_t* q_elems,

@@ -77,7 +77,7 @@ def _gpu_engine(D_local, n1: int, row0: int, config: SolverConfig, m_rows: int, 
     import torch
 
     from . import _capi
-    from .solver import _context, _device_matrix
+    from .solver import _context, _device_matrix, _release
 
     Dd = _device_matrix(D_local, device, compute_dtype)
     nloc, n2 = int(Dd.shape[0]), int(Dd.shape[1])
@@ -85,6 +85,7 @@ def _gpu_engine(D_local, n1: int, row0: int, config: SolverConfig, m_rows: int, 
     dtype = _capi.F32 if Dd.dtype == torch.float32 else _capi.F64
     stream = torch.cuda.current_stream(dev).cuda_stream
     ctx = _context(dev, dtype, n1, n2, config.rank, m_rows, m_cols, config.max_iter, stream, row0, nloc)
+    _release(ctx)  # one driving thread per rank: no lease needed against concurrent eviction
     return ctx, Dd
 
 

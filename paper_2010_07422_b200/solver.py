@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _capi
-from .sampling import IndexSet, draw_index_sets, draw_index_sets_from, pcg_words, sample_count
+from .sampling import DrawnSets, IndexSet, draw_index_sets, draw_index_sets_from, pcg_words, sample_count
 from .types import CurFactors, PinvFactor, SolverConfig, SolverTrace, SparseEstimate
 
 __all__ = ["solve", "solve_device", "solve_batch", "materialize", "materialize_device", "threshold_at",
@@ -66,6 +66,7 @@ class Context:
                                               max_cols, max_iter, row0, self.local_rows,
                                               C.c_void_p(self.stream)))
         self.h = h
+        self._busy = 0  # solves currently running on this context (solver._context leases)
         self._D = None
         self.sets: list = []
         self.colmajor = False
@@ -302,8 +303,25 @@ def _context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0
     local_rows = n1 if local_rows is None else local_rows
     key = (device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0, local_rows)
     with _CACHE_LOCK:
-        return _context_locked(key, device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0,
-                               local_rows)
+        ctx = _context_locked(key, device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0,
+                              local_rows)
+        ctx._busy += 1  # leased until _release: never evicted while a solve runs on it
+        return ctx
+
+
+def _release(ctx: Context) -> None:
+    with _CACHE_LOCK:
+        ctx._busy -= 1
+
+
+def _evict_idle(keep: int) -> None:
+    """Close least-recently-used contexts that no solve is running on until
+    at most `keep` remain (contexts in use stay; the cache then grows)."""
+    while len(_CACHE) > keep:
+        victim = next((k for k, c in _CACHE.items() if c._busy == 0), None)
+        if victim is None:
+            return
+        _CACHE.pop(victim).close()
 
 
 def _context_locked(key, device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0,
@@ -312,15 +330,11 @@ def _context_locked(key, device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, 
     if ctx is not None:
         _CACHE.move_to_end(key)
         return ctx
-    while len(_CACHE) >= _CACHE_MAX:
-        _, old = _CACHE.popitem(last=False)
-        old.close()
+    _evict_idle(_CACHE_MAX - 1)
     try:
         ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, row0, local_rows, stream=stream)
     except MemoryError:
-        for _, old in _CACHE.items():
-            old.close()
-        _CACHE.clear()
+        _evict_idle(0)  # out of memory: drop every idle context, then retry once
         torch.cuda.empty_cache()
         ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, row0, local_rows, stream=stream)
     _CACHE[key] = ctx
@@ -328,10 +342,9 @@ def _context_locked(key, device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, 
 
 
 def clear_cache() -> None:
+    """Close every cached context no solve is currently running on."""
     with _CACHE_LOCK:
-        for _, ctx in _CACHE.items():
-            ctx.close()
-        _CACHE.clear()
+        _evict_idle(0)
 
 
 # ------------------------------------------------------------ device input
@@ -523,6 +536,18 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     the events but leaves the read-back to result.read_profile(), keeping
     it out of the caller's timed region.
     """
+    leases: list = []
+    try:
+        return _solve_device(D, config, observer, device=device, compute_dtype=compute_dtype, colmajor=colmajor,
+                             fetch_factors=fetch_factors, profile=profile, _leases=leases)
+    finally:
+        for c in leases:
+            _release(c)
+
+
+def _solve_device(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
+                  colmajor="auto", fetch_factors=True, profile=False, _leases=None) -> DeviceResult:
+    """See solve_device."""
     cfg = config
     tick = _Ticker(profile)
     src = _host_source(D, device, compute_dtype) if torch.cuda.is_available() else None
@@ -542,10 +567,18 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     m_cols = sample_count(n2, cfg.rank, cfg.c_cols)
     resampled = cfg.mode == "resampled"
     n_sets = cfg.max_iter if resampled else 1
+    pcg = pcg_words(cfg.seed) if max(n1, n2) <= 2**32 else None
+    code = _native_copy_code(colmajor, n2, m_cols, cfg) if (Dh is None and observer is None and pcg is not None
+                                                           and profile in (False, "deferred")) else None
+    if code is not None:  # the whole host sequence in one library call (ircur_solve)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
+        _leases.append(ctx)
+        ctx.set_profiling(bool(profile))
+        return _solve_native(ctx, Dd, cfg, pcg, code, fetch_factors, dtype, n1, n2, m_rows, m_cols, profile)
     # Draw the sets the prep pass needs first; the rest of the sequence is
     # drawn by a worker thread while the (host-blocking) prep pass runs.
     n_first = min(n_sets, _cover_estimate(cfg) + 8) if resampled else n_sets
-    pcg = pcg_words(cfg.seed) if max(n1, n2) <= 2**32 else None
     if pcg is None:
         sets, pcg_next = draw_index_sets(n1, n2, m_rows, m_cols, cfg.seed, n_sets), None
         n_first = n_sets
@@ -554,6 +587,7 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     tick("draw")
     stream = torch.cuda.current_stream(dev).cuda_stream
     ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
+    _leases.append(ctx)
     ctx.set_profiling(bool(profile))
     ctx.set_indices(sets)
     tick("set_indices")
@@ -649,6 +683,87 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     return res
 
 
+def _native_copy_code(colmajor, n2: int, m_cols: int, cfg: SolverConfig):
+    """_copy_plan's rule as an ircur_solve code (0 none, 1 full, 2 sampled,
+    3 by the covered-column share), or None for the forms only the Python
+    sequence handles (IRCUR_COLMAJOR / IRCUR_NATIVE=0 overrides, "sampled:K")."""
+    if os.environ.get("IRCUR_COLMAJOR") is not None or os.environ.get("IRCUR_NATIVE", "1") == "0":
+        return None
+    if colmajor in (False, 0, "0", "false", "False", "none", ""):
+        return 0
+    if colmajor == "auto" and not _want_colmajor("auto", 0, n2, m_cols, 0, cfg.mode):
+        return 0
+    if colmajor in ("full", 1) and colmajor is not True:
+        return 1
+    if cfg.mode == "fixed" and colmajor in ("sampled", True, "auto"):
+        return 2 if colmajor == "sampled" else 3
+    if colmajor == "sampled":
+        return 2
+    if colmajor is True or colmajor == "auto":
+        return 3
+    return None
+
+
+def _solve_native(ctx: Context, Dd: torch.Tensor, cfg: SolverConfig, pcg, code: int, fetch_factors, dtype: int,
+                  n1: int, n2: int, m_rows: int, m_cols: int, profile) -> DeviceResult:
+    """solve_device through ircur_solve: draws, copy plan, prep pass, den
+    check, schedule and loop run in the library (no interpreter work per
+    phase, so several host threads can drive independent problems)."""
+    resampled = cfg.mode == "resampled"
+    n_sets = cfg.max_iter if resampled else 1
+    rows = np.empty((n_sets, m_rows), dtype=np.int64)
+    cols = np.empty((n_sets, m_cols), dtype=np.int64)
+    rc = np.zeros(n_sets, dtype=np.int32)
+    cc = np.zeros(n_sets, dtype=np.int32)
+    errors = np.zeros(max(cfg.max_iter, 1), dtype=np.float64)
+    ms = np.zeros(max(cfg.max_iter, 1), dtype=np.float32)
+    it, conv, cm, zs = C.c_int(0), C.c_int(0), C.c_int(0), C.c_int(0)
+    z0 = C.c_double(0.0)
+    p64, p32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+    ctx._D = Dd
+    _capi.check(ctx.lib.ircur_solve(
+        ctx.h, C.c_void_p(_ptr(Dd)), Dd.stride(0), pcg.ctypes.data_as(C.POINTER(C.c_uint64)),
+        float(cfg.zeta0) if cfg.zeta0 is not None else -1.0, float(cfg.gamma), float(cfg.eps),
+        _capi.RESAMPLED if resampled else _capi.FIXED, cfg.max_iter, code, rows.ctypes.data_as(p64),
+        rc.ctypes.data_as(p32), cols.ctypes.data_as(p64), cc.ctypes.data_as(p32), C.byref(it), C.byref(conv),
+        errors.ctypes.data_as(C.POINTER(C.c_double)), ms.ctypes.data_as(C.POINTER(C.c_float)), C.byref(z0),
+        C.byref(cm), C.byref(zs)))
+    sets = DrawnSets([(rows[k, :rc[k]], cols[k, :cc[k]]) for k in range(n_sets)], rows, rc, cols, cc)
+    ctx.sets = sets
+    ctx.colmajor = cm.value
+    trace = SolverTrace()
+    if zs.value:  # solver.py:335-341: sampled slabs identically zero
+        trace.errors.append(0.0)
+        trace.converged = True
+        r0, c0 = sets[0]
+        return DeviceResult(trace, cfg, None, IndexSet(r0, n1), IndexSet(c0, n2), None, True)
+    if cfg.zeta0 is None:
+        cfg = replace(cfg, zeta0=z0.value)  # solver.py:342-344
+    iters = it.value
+    zetas = [cfg.gamma**k * cfg.zeta0 for k in range(iters)]
+    trace.errors = [float(e) for e in errors[:iters]]
+    trace.seconds = [float(t) / 1e3 for t in ms[:iters]]
+    trace.iterations = iters
+    trace.converged = bool(conv.value)
+    trace.thresholds = zetas
+    trace.allocated = [0] * iters
+    trace.sampled_rows = [int(rc[k if resampled else 0]) for k in range(iters)]
+    trace.sampled_cols = [int(cc[k if resampled else 0]) for k in range(iters)]
+    I, J = sets[(iters - 1) if resampled else 0]
+    handle = None
+    if fetch_factors:
+        Pt, Qt = ctx.factors() if fetch_factors == "copy" else ctx.factor_views()
+        handle = DeviceHandle(Pt, Qt, dtype)
+    res = DeviceResult(trace, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), handle)
+    res.profile = None
+    res._host_ms = None
+    res.colmajor = cm.value
+    res.sets = sets
+    if profile and profile != "deferred":
+        res.read_profile()
+    return res
+
+
 def _host_results(ctx: Context, set_idx: int, n1: int, n2: int, handle):
     I, J = ctx.sets[set_idx]
     Cm, Rm, Sr, Sc = ctx.strips(set_idx)
@@ -681,15 +796,20 @@ def solve(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=
     and runs everything else in fp64) and `colmajor` (build the column-major
     copy of D used by the column-strip kernel: True/False/"auto").
     """
-    res = solve_device(D, config, observer, device=device, compute_dtype=compute_dtype,
-                       colmajor=colmajor, fetch_factors="copy")
-    n1, n2 = res.rows.bound, res.cols.bound
-    if res.zero_state:
-        cur, sparse = _zero_results(n1, n2, res.rows, res.cols, config.rank)
+    leases: list = []  # the context stays leased until its results are read back
+    try:
+        res = _solve_device(D, config, observer, device=device, compute_dtype=compute_dtype,
+                            colmajor=colmajor, fetch_factors="copy", _leases=leases)
+        n1, n2 = res.rows.bound, res.cols.bound
+        if res.zero_state:
+            cur, sparse = _zero_results(n1, n2, res.rows, res.cols, config.rank)
+            return cur, sparse, res.trace
+        last = (res.trace.iterations - 1) if res.cfg.mode == "resampled" else 0
+        cur, sparse = _host_results(res.ctx, last, n1, n2, res.handle)
         return cur, sparse, res.trace
-    last = (res.trace.iterations - 1) if res.cfg.mode == "resampled" else 0
-    cur, sparse = _host_results(res.ctx, last, n1, n2, res.handle)
-    return cur, sparse, res.trace
+    finally:
+        for c in leases:
+            _release(c)
 
 
 def solve_batch(Ds, configs, *, device=None, streams: int = 4, compute_dtype=None, colmajor="auto"):

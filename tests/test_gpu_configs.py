@@ -138,3 +138,34 @@ def test_cfg5_full_size_properties(ir):
     del D, res, res2
     ir.clear_cache()
     torch.cuda.empty_cache()
+
+
+def test_concurrent_streams_beyond_cache_limit(ir):
+    """More host threads/streams than the context cache holds
+    (solver._CACHE_MAX): contexts a solve is running on are leased and never
+    evicted under it; every result equals the sequential solve."""
+    import threading
+    from paper_2010_07422_b200 import solver
+    probs, cfgs = [], []
+    for p in range(12):
+        D, _, _, linf = orc.baseline_problem(600, 500, 3, 0.2, 2000 + p)
+        probs.append(torch.from_numpy(D.astype(np.float32)).cuda())
+        cfgs.append(ir.SolverConfig(rank=3, eps=1e-5, zeta0=linf, gamma=0.7, mode="resampled", max_iter=60,
+                                    seed=ir.RngSeed(2000 + p)))
+    seq = [ir.solve_device(D, c, fetch_factors="copy").trace.errors for D, c in zip(probs, cfgs)]
+    nthreads = solver._CACHE_MAX + 4
+    streams = [torch.cuda.Stream() for _ in range(nthreads)]
+    out = [None] * len(probs)
+
+    def worker(w):
+        with torch.cuda.stream(streams[w]):
+            for i in range(w, len(probs), nthreads):
+                out[i] = ir.solve(probs[i].cpu().numpy(), cfgs[i], device=0)[2].errors
+            streams[w].synchronize()
+
+    th = [threading.Thread(target=worker, args=(w,)) for w in range(nthreads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert out == seq

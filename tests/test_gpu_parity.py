@@ -286,3 +286,43 @@ def test_prepare_rows_rejects_out_of_order_chunks(ir):
     ctx.prepare_rows_async(D, 0, 1, 64, 256)
     assert ctx.prepare_wait() == float(D.abs().max())
     ctx.close()
+
+
+@pytest.mark.parametrize("colmajor", ["auto", "sampled", "full", False, True])
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_native_solve_matches_python_sequence(ir, monkeypatch, colmajor, mode, dtype):
+    """ircur_solve (the host sequence in the library) against the Python
+    sequence of solve_device (IRCUR_NATIVE=0): same draws, copy plan,
+    thresholds, iterations and bitwise results."""
+    n1, n2, r = 400, 350, 3
+    rng = np.random.default_rng(21)
+    D = (rng.standard_normal((n1, r)) @ rng.standard_normal((r, n2))
+         + np.where(rng.random((n1, n2)) < 0.05, 8.0, 0.0)).astype(dtype)
+    for zeta0 in (None, 9.0):
+        cfg = ir.SolverConfig(rank=r, mode=mode, max_iter=25, zeta0=zeta0, seed=ir.RngSeed(8))
+        monkeypatch.setenv("IRCUR_NATIVE", "0")
+        a = ir.solve(D, cfg, device=0, colmajor=colmajor)
+        monkeypatch.delenv("IRCUR_NATIVE")
+        b = ir.solve(D, cfg, device=0, colmajor=colmajor)
+        assert a[2].iterations == b[2].iterations and a[2].errors == b[2].errors
+        assert a[2].thresholds == b[2].thresholds and a[2].converged == b[2].converged
+        assert a[2].sampled_rows == b[2].sampled_rows and a[2].sampled_cols == b[2].sampled_cols
+        np.testing.assert_array_equal(a[0].rows.indices, b[0].rows.indices)
+        np.testing.assert_array_equal(a[0].C, b[0].C)
+        np.testing.assert_array_equal(a[0].R, b[0].R)
+        np.testing.assert_array_equal(a[1].col_values, b[1].col_values)
+        np.testing.assert_array_equal(a[0].core_pinv.sigma, b[0].core_pinv.sigma)
+
+
+def test_native_solve_zero_slabs(ir):
+    """The den == 0 early exit through ircur_solve (solver.py:335-341)."""
+    n1, n2, r = 300, 280, 3
+    cfg = ir.SolverConfig(rank=r, zeta0=1.0, mode="resampled", max_iter=20, seed=ir.RngSeed(4))
+    m1, m2 = ir.sample_count(n1, r, 4.0), ir.sample_count(n2, r, 4.0)
+    I0, J0 = ir.draw_index_sets(n1, n2, m1, m2, cfg.seed, 1)[0]
+    D = np.random.default_rng(0).standard_normal((n1, n2))
+    D[I0, :] = 0.0
+    D[:, J0] = 0.0
+    cur, sp, tr = ir.solve(D, cfg, device=0)
+    assert tr.errors == [0.0] and tr.converged and tr.iterations == 0 and not cur.C.any()
