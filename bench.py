@@ -31,6 +31,10 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+# NCCL writes its log lines (the version banner at NCCL_DEBUG=VERSION or INFO)
+# to stdout by default; keep stdout to the one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
 CONFIGS = {
     # name: (n1, n2, rank, alpha, dtype, BASELINE.json configs index)
     "cfg1": (1000, 1000, 5, 0.1, "f64", 0),
@@ -297,7 +301,8 @@ def run_sharded(args, rank, world, local):
     cm = COLMAJOR[args.colmajor]
 
     def one(Din):
-        return irdist.run_collective(irdist.solve_shard_program(Din, cfg, n1=n1, row0=r0, colmajor=cm))
+        return irdist.run_collective(irdist.solve_shard_program(Din, cfg, n1=n1, row0=r0, colmajor=cm,
+                                                                profile=not args.no_profile))
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -318,6 +323,24 @@ def run_sharded(args, rank, world, local):
     ms_per_step = float(mine.item())
     res = results[-1]
     launches = sum(2 + rr.engine.profile(0)["kernel_launches"] for rr in results)
+    # roofline of this rank's strip launches (row strip in two launches around
+    # the all-reduce), from the last timed solve's events
+    roofline = None
+    it = res.trace.iterations
+    if not args.no_profile and it > 0:
+        p = res.engine.profile(it)
+        strip_ms = float(np.sum(p["strips_ms"][:it]))
+        sb = 0
+        for k in range(it):
+            I, J = res.sets[k if args.mode == "resampled" else 0]
+            mi = int(np.count_nonzero((I >= r0) & (I < r0 + nl)))
+            sb += algorithmic_strip_bytes(s, nl, n2, r, mi, int(J.size))
+        if strip_ms > 0:
+            peak, peak_kind = peaks()
+            ach = sb / (strip_ms / 1e3) / 1e9
+            roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                        "traffic": None, "peak_kind": peak_kind, "kernel": "strips3_kernel (partial + finish)",
+                        "avg_launch_us": strip_ms / it * 1e3, "bytes_per_launch": sb / it, "rank": rank}
     lt = torch.tensor([launches], dtype=torch.int64, device=dev)
     dist.all_reduce(lt)
     # e2e: pinned host shard -> sharded solve -> local strips back to the host
@@ -361,7 +384,7 @@ def run_sharded(args, rank, world, local):
                        "final_e": res.trace.errors[-1], "launched_iterations": res.launched,
                        "l2": "inputs larger than L2 (D >= 400 MB), no flush",
                        "parallelism": f"row-sharded x{world} (NCCL all-reduce of U, Q partials, 4 sums)"},
-            "roofline": None,
+            "roofline": roofline,
             "gpu_launches": int(lt.item()),
             "clocks": clk.summary(),
         }

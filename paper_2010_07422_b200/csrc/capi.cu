@@ -130,6 +130,9 @@ struct ircur_ctx {
   // optional per-phase profiling: events [k][0..4] around core | svd | strips | finalize
   bool profiling = false;
   std::vector<cudaEvent_t> evp;
+  // row-sharded runs: events around the FINISH-mode strip launch, per iteration
+  std::vector<cudaEvent_t> evq;
+  bool shard_prof = false;
   // host-gap marks (profiling): set_indices | prep begin | prep end | slab end | run begin
   cudaEvent_t evm[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   int launched_iters = 0;
@@ -438,7 +441,10 @@ int launch_shard_phase(ircur_ctx* c, int phase, int k, int set, double zeta, dou
     StripsArgs<T> pa = strips_args<T>(c, k, q, zeta);
     pa.s[0].mode = kStripPartial;
     pa.s[0].Fnew = (T*)c->Qpart;
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 2], st));
     IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, c->num_sms, &c->ncta_a, st));
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 3], st));
+    c->shard_prof = c->profiling;
     c->kernel_launches += 3;  // gram, svd, strips
   } else if (phase == IRCUR_SHARD_RESID) {
     StripsArgs<T> pa = strips_args<T>(c, k, q, zeta);
@@ -448,7 +454,9 @@ int launch_shard_phase(ircur_ctx* c, int phase, int k, int set, double zeta, dou
     pa.s[1].tiles = 0;
     pa.partials = c->partials + 4 * (size_t)c->ncta_a;
     int ncta_b = 0;
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evq[(size_t)k * 2], st));
     IR_CUDA(launch_strips<T>(pa, R, c->strips_cs, c->num_sms, &ncta_b, st));
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evq[(size_t)k * 2 + 1], st));
     FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, false);
     fa.ncta_rows = c->ncta_a + ncta_b;
     fa.sums_out = c->scal;
@@ -590,6 +598,8 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   for (auto& e : c->evp)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evm)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->evq)
     if (e) cudaEventDestroy(e);
   delete c;
   return IRCUR_OK;
@@ -895,6 +905,7 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   IR_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   mark(c, 4);
+  c->shard_prof = false;
   if (int rc = reset_loop(c)) return rc;
   volatile int* hf = c->h_flags;
   constexpr int kAhead = 3;
@@ -1204,6 +1215,8 @@ int ircur_set_profiling(ircur_ctx_t c, int on) {
     c->evp.resize((size_t)c->max_iter * 5);
     for (auto& e : c->evp) IR_CUDA(cudaEventCreate(&e));
     for (auto& e : c->evm) IR_CUDA(cudaEventCreate(&e));
+    c->evq.resize((size_t)c->max_iter * 2);
+    for (auto& e : c->evq) IR_CUDA(cudaEventCreate(&e));
   }
   c->profiling = on != 0;
   return IRCUR_OK;
@@ -1233,7 +1246,15 @@ int ircur_get_profile(ircur_ctx_t c, int n_iters, int* launched_iters, long long
   IR_CUDA(cudaStreamSynchronize(c->stream));
   for (int k = 0; k < n_iters && k < c->max_iter; ++k) {
     float t[4] = {0, 0, 0, 0};
-    for (int q = 0; q < 4; ++q) IR_CUDA(cudaEventElapsedTime(&t[q], c->evp[(size_t)k * 5 + q], c->evp[(size_t)k * 5 + q + 1]));
+    if (c->shard_prof) {  // row-sharded run: only the two strip launches are timed
+      float a = 0.f, b = 0.f;
+      IR_CUDA(cudaEventElapsedTime(&a, c->evp[(size_t)k * 5 + 2], c->evp[(size_t)k * 5 + 3]));
+      IR_CUDA(cudaEventElapsedTime(&b, c->evq[(size_t)k * 2], c->evq[(size_t)k * 2 + 1]));
+      t[2] = a + b;
+    } else {
+      for (int q = 0; q < 4; ++q)
+        IR_CUDA(cudaEventElapsedTime(&t[q], c->evp[(size_t)k * 5 + q], c->evp[(size_t)k * 5 + q + 1]));
+    }
     if (core_ms) core_ms[k] = t[0];
     if (svd_ms) svd_ms[k] = t[1];
     if (strips_ms) strips_ms[k] = t[2];

@@ -90,11 +90,12 @@ def _gpu_engine(D_local, n1: int, row0: int, config: SolverConfig, m_rows: int, 
 
 
 def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, colmajor="auto",
-                        ahead: int = 3, engine_factory=None, device=None, compute_dtype=None):
+                        ahead: int = 3, engine_factory=None, device=None, compute_dtype=None, profile=False):
     """Generator: this rank's share of a row-sharded `solve` (solver.py:304-416).
 
     D_local holds rows [row0, row0 + D_local.shape[0]) of the n1 x n2 matrix.
-    Returns (via StopIteration.value) a ShardResult.
+    Returns (via StopIteration.value) a ShardResult.  profile=True records
+    the strip launches' events (engine.profile(iterations)["strips_ms"]).
     """
     cfg = config
     if len(getattr(D_local, "shape", ())) != 2:
@@ -108,6 +109,8 @@ def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, co
     sets = draw_index_sets(n1, n2, m_rows, m_cols, cfg.seed, cfg.max_iter if resampled else 1)
     make = engine_factory or _gpu_engine
     eng, Dd = make(D_local, n1, row0, cfg, m_rows, m_cols, device=device, compute_dtype=compute_dtype)
+    if hasattr(eng, "set_profiling"):  # strip-kernel events (engine.profile) for the bench roofline
+        eng.set_profiling(bool(profile))
     from .solver import _copy_plan
 
     cm, cover = _copy_plan(colmajor, n2, m_cols, sets, cfg)
