@@ -31,9 +31,18 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-# NCCL writes its log lines (the version banner at NCCL_DEBUG=VERSION or INFO)
-# to stdout by default; keep stdout to the one JSON line
+# NCCL writes its log lines to stdout by default; keep stdout to the one JSON line
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
+
+def _json_out():
+    """A stream on the original stdout; fd 1 itself is pointed at stderr so
+    that library banners (e.g. "NCCL version ..." at communicator creation)
+    cannot interleave with the bench line."""
+    saved = os.dup(1)
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    return os.fdopen(saved, "w")
 
 CONFIGS = {
     # name: (n1, n2, rank, alpha, dtype, BASELINE.json configs index)
@@ -281,6 +290,7 @@ def run_sharded(args, rank, world, local):
     from paper_2010_07422_b200 import dist as irdist
     from paper_2010_07422_b200 import gen
 
+    out = _json_out()
     dev = torch.device("cuda", local)
     n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
     tdt = torch.float32 if dts == "f32" else torch.float64
@@ -390,7 +400,8 @@ def run_sharded(args, rank, world, local):
         }
         if e2e:
             line["e2e"] = e2e
-        print(json.dumps(line), flush=True)
+        out.write(json.dumps(line) + "\n")
+        out.flush()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -415,6 +426,7 @@ def run_batch(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    out = _json_out()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -536,7 +548,8 @@ def run_batch(args):
             cb["sample"] = f"problem 0 of {nb}: " + cb["sample"] + f", x{nb} problems"
             line["cpu_baseline"] = cb
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        out.write(json.dumps(line) + "\n")
+        out.flush()
     if world > 1:
         dist.destroy_process_group()
 
