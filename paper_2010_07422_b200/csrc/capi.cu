@@ -256,6 +256,11 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   }();
   sa.jac_thr = std::max(4e-16, jthr_scale * sa.tol);
   sa.salt = 0x1234567ull + (uint64_t)k * 7919ull;
+  static const int small_reg = [] {  // register-resident small eigensolvers for kk <= 8 (A/B knob)
+    const char* e = std::getenv("IRCUR_SVD_REG");
+    return e ? std::atoi(e) : 1;
+  }();
+  sa.small_reg = small_reg;
   return sa;
 }
 

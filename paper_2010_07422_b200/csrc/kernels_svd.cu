@@ -27,6 +27,7 @@
 
 #include "ircur_common.cuh"
 #include "launchers.cuh"
+#include "svd_small_reg.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -262,7 +263,16 @@ __device__ __forceinline__ double approx_sqrtf_d(float x) {
   return r;
 }
 
-__device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long long* dbg = nullptr) {
+__device__ void jacobi_eig(Sm& S, int kk, double thr_rel, int max_sweeps, long long* dbg = nullptr,
+                           bool reg = false) {
+  if (reg && sreg_supported(kk)) {  // one warp, registers (svd_small_reg.cuh)
+    if (threadIdx.x < 32) {
+      const int sw = eig_reg(kk, S.H, S.L.HL, S.Z, S.lam, thr_rel, max_sweeps);
+      if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[13] += sw;
+    }
+    eig_sync();
+    return;
+  }
   const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
   const int HL = S.L.HL;
   double* H = S.H;
@@ -468,10 +478,26 @@ __device__ __forceinline__ void tri_forward(const double* Lc, int HL, int kk, co
 // T = Lc^{-T} Z so that V T has orthonormal columns and diagonalises V^T G V.
 // Caller: first kEigNT threads.  Returns 0 if chol(M) broke down.
 __device__ int ritz_small(Sm& S, int kk, const double* Hp, const double* M, double thr_rel, int max_sweeps,
-                          long long* dbg = nullptr) {
+                          long long* dbg = nullptr, bool reg = false) {
   const int tid = threadIdx.x, HL = S.L.HL;
   const bool rec = dbg && blockIdx.x == 0 && tid == 0;
   long long t0 = clock64();
+  if (reg && sreg_supported(kk)) {  // one warp, registers (svd_small_reg.cuh)
+    if (tid < 32) {
+      int sw = 0;
+      const int ok = ritz_reg(kk, Hp, M, S.T, S.lam, S.H2, S.Z, HL, thr_rel, max_sweeps, &sw);
+      if (tid == 0) {
+        S.flags[1] = ok;
+        if (rec) {
+          dbg[10] += clock64() - t0;
+          dbg[13] += sw;
+          dbg[14] += 1;
+        }
+      }
+    }
+    eig_sync();
+    return S.flags[1];
+  }
   if (!cholesky_warp(M, S.Lc, HL, kk, S.flags + 1)) return 0;
   if (rec) { const long long t1 = clock64(); dbg[8] += t1 - t0; t0 = t1; }
   // K = Lc^{-1} H' (column c: stride HL down the rows), then H^T = Lc^{-1} K^T
@@ -573,7 +599,7 @@ __device__ void cgs2_global(Sm& S, double* V, int n, int kk, uint64_t salt) {
   }
 }
 
-template <typename T>
+template <typename T, bool REG>
 __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ SvdArgs a) {
   if (a.done && *a.done) return;
   cg::cluster_group cl = cg::this_cluster();
@@ -657,7 +683,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     PH(1);
     // ---- 3. Rayleigh-Ritz (generalised through chol(V^T V))
     if (eigt) {
-      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, a.jac_thr, a.sweeps, a.dbg);
+      const int ok = ritz_small(S, kk, S.rout, S.rout + kk * kk, a.jac_thr, a.sweeps, a.dbg, REG);
       if (tid == 0) S.flags[7] = ok;
     }
     __syncthreads();
@@ -786,7 +812,7 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
     }
     eig_sync();
     const long long tj0 = clock64();
-    jacobi_eig(S, kk, 4e-16, 30);
+    jacobi_eig(S, kk, 4e-16, 30, nullptr, REG);
     if (a.dbg && q == 0 && tid == 0) a.dbg[12] += clock64() - tj0;
   }
   __syncthreads();
@@ -955,13 +981,18 @@ cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t smem = svd_smem_bytes(a.n, a.m, a.kk, cs);
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(svd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  // kk <= 8 (r <= 6): the kernel with the register-resident small solvers;
+  // larger blocks: the shared-memory solvers only (its registers and code
+  // are not shared with the small-kk paths)
+  const bool reg = a.small_reg && sreg_supported(a.kk);
+  static bool attr[2] = {false, false};
+  auto kern = reg ? svd_kernel<T, true> : svd_kernel<T, false>;
+  if (!attr[reg]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(svd_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[reg] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cs, 1, 1);
@@ -975,7 +1006,7 @@ cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st) {
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, svd_kernel<T>, a);
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template cudaError_t launch_svd<float>(const SvdArgs&, int, cudaStream_t);

@@ -28,6 +28,7 @@ struct SvdArgs {
   double tol_scale; const double* prev_err;  // e_{k-1} on the device (null at k = 0)
   uint64_t salt;
   long long* dbg;                 // optional per-phase clock64 totals (8)
+  int small_reg;                  // register-resident kk x kk kernels (svd_small_reg.cuh) when kk allows
 };
 
 struct GenArgs {
