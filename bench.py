@@ -58,10 +58,16 @@ CONFIGS = {
     "cfg1": (1000, 1000, 5, 0.1, "f64", 0),
     "cfg2": (10000, 10000, 5, 0.2, "f32", 1),
     "cfg2f64": (10000, 10000, 5, 0.2, "f64", 1),
+    "cfg3": (25344, 1000, 2, None, "f32", 2),   # video-like (gen.video_problem), VIDEO["cfg3"]
+    "video_mall": (81920, 1000, 2, None, "f32", 2),        # paper Table 1 shape (shoppingmall), synthetic
+    "video_restaurant": (19200, 3055, 2, None, "f32", 2),  # paper Table 1 shape (restaurant), synthetic
     "cfg4": (2000, 2000, 5, 0.2, "f32", 3),     # x BATCH["cfg4"] independent problems
     "cfg5": (100000, 100000, 10, 0.2, "f32", 4),
 }
-BATCH = {"cfg4": 512}  # problem-parallel configs: problems per batch (data/solver seeds 1000 + p)
+BATCH = {"cfg4": 512}
+# video-like configs: (frames, height, width) of gen.video_problem; rows = pixels,
+# columns = frames; zeta0 = max|D| (solver.py:342-344) like a video run
+VIDEO = {"cfg3": (1000, 144, 176), "video_mall": (1000, 256, 320), "video_restaurant": (3055, 120, 160)}  # problem-parallel configs: problems per batch (data/solver seeds 1000 + p)
 DATA_SEED = 0
 SOLVER_SEED = 1
 GAMMA = 0.7
@@ -185,7 +191,13 @@ def run_ours(args):
     n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
     tdt = torch.float32 if dts == "f32" else torch.float64
     s = 4 if dts == "f32" else 8
-    D, linf, a = gen.baseline_problem_device(n1, n2, r, alpha, DATA_SEED, dtype=tdt)
+    if args.config in VIDEO:
+        frames, hgt, wid = VIDEO[args.config]
+        Dv, _, _ = gen.video_problem(frames=frames, height=hgt, width=wid, rank=r, seed=DATA_SEED)
+        D = torch.from_numpy(np.ascontiguousarray(Dv, dtype=np.float32)).cuda()
+        linf = None  # zeta0 = max|D|
+    else:
+        D, linf, a = gen.baseline_problem_device(n1, n2, r, alpha, DATA_SEED, dtype=tdt)
     cfg = ir.SolverConfig(rank=r, eps=EPS, zeta0=linf, gamma=GAMMA, mode=args.mode,
                           max_iter=MAX_ITER, seed=ir.RngSeed(SOLVER_SEED))
     cm = COLMAJOR[args.colmajor]
@@ -239,7 +251,8 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if dts == "f32" else "f64",
         "data": "synthetic (BASELINE.json generator on device, numpy-PCG64-exact)",
         "config": {"workload": args.config, "n1": n1, "n2": n2, "rank": r, "alpha": alpha,
-                   "mode": args.mode, "gamma": GAMMA, "eps": EPS, "zeta0": "max|L|",
+                   "mode": args.mode, "gamma": GAMMA, "eps": EPS,
+                   "zeta0": "max|D|" if args.config in VIDEO else "max|L|",
                    "iterations": iters, "converged": res.trace.converged,
                    "final_e": res.trace.errors[-1], "colmajor_copy": ["none", "full", "sampled"][int(res.colmajor)],
                    "l2": "inputs larger than L2 (D >= 400 MB), no flush",
@@ -301,6 +314,8 @@ def run_sharded(args, rank, world, local):
 
     dev = torch.device("cuda", local)
     n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
+    if args.config in VIDEO:
+        raise SystemExit("video-like configs run on one GPU (no sharded generator)")
     tdt = torch.float32 if dts == "f32" else torch.float64
     s = 4 if dts == "f32" else 8
     r0, nl = irdist.shard_rows(n1, world, rank)
@@ -611,7 +626,13 @@ def run_reference(args):
 
     n1, n2, r, alpha, dts, _ = CONFIGS[args.config]
     dt = np.float32 if dts == "f32" else np.float64
-    D, linf, a = orc.baseline_problem_blocked(n1, n2, r, alpha, DATA_SEED, dtype=dt)
+    if args.config in VIDEO:
+        from paper_2010_07422_b200 import gen
+        frames, hgt, wid = VIDEO[args.config]
+        D, _, _ = gen.video_problem(frames=frames, height=hgt, width=wid, rank=r, seed=DATA_SEED)
+        linf = None
+    else:
+        D, linf, a = orc.baseline_problem_blocked(n1, n2, r, alpha, DATA_SEED, dtype=dt)
 
     class Cfg:  # the solver settings of our arm
         rank, eps, zeta0, gamma, mode, max_iter = r, EPS, linf, GAMMA, args.mode, MAX_ITER
