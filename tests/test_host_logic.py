@@ -159,3 +159,31 @@ def test_c_draws_chunked_with_rejections_equal_numpy(n1, n2, m1, m2, n_sets):
     assert [int(x) for x in st[:5]] == want
     if ref["has_uint32"]:
         assert int(st[5]) == int(ref["uinteger"])
+
+
+def test_native_copy_code_matches_copy_plan(monkeypatch):
+    """solver._native_copy_code (the code ircur_solve receives) makes the
+    same copy-plan decision as solver._copy_plan for every colmajor form;
+    code 3 is the covered-column rule, evaluated here like ircur_solve does."""
+    from paper_2010_07422_b200.solver import _copy_plan, _cover_estimate, _native_copy_code
+    monkeypatch.delenv("IRCUR_COLMAJOR", raising=False)
+    monkeypatch.delenv("IRCUR_NATIVE", raising=False)
+    for (n, m, ns) in ((100000, 461, 49), (200, 60, 100), (10000, 185, 49)):
+        sets = ir.draw_index_sets(n, n, m, m, ir.RngSeed(1), ns)
+        for mode in ("resampled", "fixed"):
+            cfg = ir.SolverConfig(rank=10, mode=mode, eps=1e-5, gamma=0.7)
+            for cm in ("auto", "sampled", "full", False, True, 0, 1):
+                want = _copy_plan(cm, n, m, sets, cfg)
+                code = _native_copy_code(cm, n, m, cfg)
+                assert code is not None
+                cover = 1 if mode == "fixed" else max(1, min(len(sets), _cover_estimate(cfg) + 8))
+                if code == 3:
+                    u = len(set(np.concatenate([sets[k][1] for k in range(cover)]).tolist()))
+                    got = (1, 0) if u > 0.7 * n else (2, cover)
+                else:
+                    got = (code, cover if code == 2 else 0)
+                assert got == want, (n, mode, cm, got, want)
+    monkeypatch.setenv("IRCUR_NATIVE", "0")
+    assert _native_copy_code("auto", 1000, 10, ir.SolverConfig(rank=2)) is None
+    monkeypatch.delenv("IRCUR_NATIVE")
+    assert _native_copy_code("sampled:3", 1000, 10, ir.SolverConfig(rank=2)) is None
