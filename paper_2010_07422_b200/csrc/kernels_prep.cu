@@ -239,11 +239,10 @@ cudaError_t launch_prep(const T* D, int64_t ldd, int64_t nloc, int64_t n2, T* Dt
                         unsigned long long* maxbits, int* nonfinite, int num_sms, cudaStream_t st) {
   if (nloc == 0 || n2 == 0) return cudaSuccess;
   if (Dt) {
-    static int mode = -1;
-    if (mode < 0) {
+    static const int mode = [] {
       const char* m = std::getenv("IRCUR_TRANSPOSE");
-      mode = m ? std::atoi(m) : 1;
-    }
+      return m ? std::atoi(m) : 1;
+    }();
     if (mode == 0) {
       dim3 grid((unsigned)((n2 + kTT - 1) / kTT), (unsigned)((nloc + kTT - 1) / kTT));
       prep_transpose_kernel<T><<<grid, 256, 0, st>>>(D, ldd, nloc, n2, Dt, ldt, maxbits, nonfinite);
@@ -448,10 +447,12 @@ cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2
   const int64_t ntiles = ((nloc + tr - 1) / tr) * ((n2 + tc - 1) / tc);
   // persistent grid: every CTA resident (the loop strides over the tiles)
   auto grid_for = [&](auto kern) {
-    static int per_sm = 0;
-    if (per_sm == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess)
-      per_sm = 4;
-    const int64_t cap = (int64_t)num_sms * (per_sm > 0 ? per_sm : 1);
+    static const int per_sm = [&] {  // once per kernel, thread-safe
+      int v = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 256, 0) != cudaSuccess || v < 1) v = 4;
+      return v;
+    }();
+    const int64_t cap = (int64_t)num_sms * per_sm;
     return (unsigned)(ntiles < cap ? ntiles : cap);
   };
   static const int nanmax = [] {  // NaN-propagating float max (one FMNMX per element) vs the bit-pattern max

@@ -471,15 +471,13 @@ int strips_pick_cluster(int nk_max, int R) {
 template <typename T, int R>
 static cudaError_t launch_strips_r(const StripsArgs<T>& a, int cs, int num_sms, cudaStream_t st) {
   const size_t smem = strips_smem_bytes<T>(a.maxl, R);
-  static bool attr_done = false;
-  if (!attr_done) {
+  static const cudaError_t fattr = [] {  // once, thread-safe (several host threads may launch)
     cudaError_t e = cudaFuncSetAttribute(strips_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(strips_kernel<T, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+    return cudaFuncSetAttribute(strips_kernel<T, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }();
+  if (fattr != cudaSuccess) return fattr;
   const int tiles = a.s[0].tiles + a.s[1].tiles;
   const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (size_t)(227 * 1024) / (smem + 1024)));
   int ncl = std::max(1, std::min(tiles, num_sms * per_sm / cs));

@@ -306,12 +306,9 @@ cudaError_t launch_strips2(const StripsArgs<float>& a0, int R, int num_sms, int*
   if (tiles == 0) return cudaSuccess;
   cudaError_t e = cudaErrorInvalidValue;
   IRCUR_DISPATCH_RANK(R, RR, {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(strips2_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    static const cudaError_t attr =  // once, thread-safe
+        cudaFuncSetAttribute(strips2_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (attr != cudaSuccess) return attr;
     strips2_kernel<RR><<<num_sms, kS2NT, smem, st>>>(a);
     e = cudaGetLastError();
   });

@@ -290,12 +290,9 @@ cudaError_t launch_strips3(const StripsArgs<float>& a0, int R, int num_sms, int*
   if (tiles == 0) return cudaSuccess;
   cudaError_t e = cudaErrorInvalidValue;
   IRCUR_DISPATCH_RANK(R, RR, {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(strips3_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    static const cudaError_t attr =  // once, thread-safe
+        cudaFuncSetAttribute(strips3_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (attr != cudaSuccess) return attr;
     strips3_kernel<RR><<<num_sms, kS3NT, smem, st>>>(a);
     e = cudaGetLastError();
   });

@@ -985,15 +985,16 @@ cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st) {
   // larger blocks: the shared-memory solvers only (its registers and code
   // are not shared with the small-kk paths)
   const bool reg = a.small_reg && sreg_supported(a.kk);
-  static bool attr[2] = {false, false};
   auto kern = reg ? svd_kernel<T, true> : svd_kernel<T, false>;
-  if (!attr[reg]) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    attr[reg] = true;
-  }
+  auto set_attrs = [](auto k) {
+    cudaError_t r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (r != cudaSuccess) return r;
+    return cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  };
+  static const cudaError_t attr_reg = set_attrs(svd_kernel<T, true>);  // once, thread-safe
+  static const cudaError_t attr_std = set_attrs(svd_kernel<T, false>);
+  e = reg ? attr_reg : attr_std;
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cs, 1, 1);
   cfg.blockDim = dim3(kSvdNT, 1, 1);
