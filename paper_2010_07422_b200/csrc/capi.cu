@@ -92,16 +92,19 @@ struct ircur_ctx {
   void* Qt[2] = {nullptr, nullptr};
   int64_t ldp = 0, ldq = 0;
   double* U = nullptr;
-  void* PoldI = nullptr;
-  void* QoldJ = nullptr;
-  void* Wr = nullptr;
-  void* PI = nullptr;
-  void* VS = nullptr;
-  void* QJ = nullptr;
-  double* W = nullptr;
-  double* sigma = nullptr;
-  double* V = nullptr;
-  double* inv = nullptr;
+  // per-iteration buffers, two copies by iteration parity (k & 1): iteration
+  // k + 1's core, gathers and SVD can then be produced while iteration k's
+  // strips still read theirs
+  void* PoldI[2] = {nullptr, nullptr};
+  void* QoldJ[2] = {nullptr, nullptr};
+  void* Wr[2] = {nullptr, nullptr};
+  void* PI[2] = {nullptr, nullptr};
+  void* VS[2] = {nullptr, nullptr};
+  void* QJ[2] = {nullptr, nullptr};
+  double* W[2] = {nullptr, nullptr};
+  double* sigma[2] = {nullptr, nullptr};
+  double* V[2] = {nullptr, nullptr};
+  double* inv[2] = {nullptr, nullptr};
   double* G = nullptr;
   double* svd_scratch = nullptr;
   double* partials = nullptr;
@@ -110,8 +113,8 @@ struct ircur_ctx {
   int* flags = nullptr;  // [0]=done [1]=iters [2]=converged [3]=nonfinite
   int* svd_steps = nullptr;  // subspace steps taken by the core SVD, per iteration
   long long* svd_dbg = nullptr;  // per-phase clock64 totals of the SVD kernel (profiling)
-  int* rowmap = nullptr;     // local row -> position in I (or -1), per iteration
-  int* colmap = nullptr;     // column -> position in J (or -1), per iteration
+  int* rowmap[2] = {nullptr, nullptr};  // local row -> position in I (or -1), by iteration parity
+  int* colmap[2] = {nullptr, nullptr};  // column -> position in J (or -1), by iteration parity
   unsigned long long* maxbits = nullptr;
   int* h_flags = nullptr;  // mapped pinned: [0]=done [1]=iters
   int* h_flags_dev = nullptr;
@@ -206,8 +209,9 @@ CoreArgs<T> core_args(const ircur_ctx* c, int k, const IterSets& q, double zeta)
   ca.Pt = (const T*)c->Pt[old]; ca.ldp = c->ldp;
   ca.Qt = (const T*)c->Qt[old]; ca.ldq = c->ldq;
   ca.zt = storage_zeta<T>(zeta); ca.U = c->U; ca.ldu = c->max_cols; ca.upos0 = q.i_lo;
-  ca.PoldI = (T*)c->PoldI; ca.QoldJ = (T*)c->QoldJ; ca.done = c->flags;
-  ca.rowmap = c->rowmap; ca.colmap = c->colmap;
+  const int p = k & 1;
+  ca.PoldI = (T*)c->PoldI[p]; ca.QoldJ = (T*)c->QoldJ[p]; ca.done = c->flags;
+  ca.rowmap = c->rowmap[p]; ca.colmap = c->colmap[p];
   return ca;
 }
 
@@ -228,9 +232,10 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   }();
   const int kk_want = R + kk_extra;
   sa.kk = std::min(std::min(kk_want, 32), std::min(q.mI_all, q.nJ));
-  sa.warm = k > 0 ? c->QoldJ : nullptr; sa.warm_ld = R; sa.warm_cols = k > 0 ? R : 0;
-  sa.W = c->W; sa.sigma = c->sigma; sa.V = c->V; sa.inv = c->inv;
-  sa.Wr = c->Wr; sa.PI = c->PI; sa.VS = c->VS; sa.QJ = c->QJ;
+  const int p = k & 1;
+  sa.warm = k > 0 ? c->QoldJ[p] : nullptr; sa.warm_ld = R; sa.warm_cols = k > 0 ? R : 0;
+  sa.W = c->W[p]; sa.sigma = c->sigma[p]; sa.V = c->V[p]; sa.inv = c->inv[p];
+  sa.Wr = c->Wr[p]; sa.PI = c->PI[p]; sa.VS = c->VS[p]; sa.QJ = c->QJ[p];
   sa.scratch = c->svd_scratch; sa.done = c->flags; sa.steps_out = c->svd_steps + k;
   // Ritz-residual target relative to lambda_1: round-off floor, relaxed in
   // early iterations in proportion to e_{k-1} (an SVD perturbation delta
@@ -275,11 +280,12 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
   rs.src = (const T*)c->D; rs.line_stride = c->ldd; rs.pos_stride = 1;
   rs.bulk_ok = ((c->ldd * (int64_t)sizeof(T)) % 16 == 0) && ((uintptr_t)c->D % 16 == 0);
   rs.lines = q.I; rs.line_off = (int)c->row0; rs.nk = q.mI; rs.npos = (int)c->n2;
-  rs.lineA = (const T*)c->PoldI;
-  rs.lineW = (const T*)c->Wr + (size_t)q.i_lo * R;
-  rs.lineRes = (const T*)c->PI + (size_t)q.i_lo * R;
+  const int p = k & 1;
+  rs.lineA = (const T*)c->PoldI[p];
+  rs.lineW = (const T*)c->Wr[p] + (size_t)q.i_lo * R;
+  rs.lineRes = (const T*)c->PI[p] + (size_t)q.i_lo * R;
   rs.Bold = (const T*)c->Qt[old]; rs.ldb = c->ldq; rs.Fnew = (T*)c->Qt[nw]; rs.ldf = c->ldq;
-  rs.omap = c->colmap; rs.otherF = (const T*)c->QJ;
+  rs.omap = c->colmap[p]; rs.otherF = (const T*)c->QJ[p];
   rs.tiles = (int)((c->n2 + TX - 1) / TX);
   rs.mode = kStripFull;
   StripDesc<T>& cs = pa.s[1];
@@ -290,9 +296,9 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
     cs.src = (const T*)c->D; cs.line_stride = 1; cs.pos_stride = c->ldd; cs.bulk_ok = 0;
   }
   cs.lines = c->Dt ? q.Jline : q.J; cs.line_off = 0; cs.nk = q.nJ; cs.npos = (int)c->nloc;
-  cs.lineA = (const T*)c->QoldJ; cs.lineW = (const T*)c->VS; cs.lineRes = (const T*)c->QJ;
+  cs.lineA = (const T*)c->QoldJ[p]; cs.lineW = (const T*)c->VS[p]; cs.lineRes = (const T*)c->QJ[p];
   cs.Bold = (const T*)c->Pt[old]; cs.ldb = c->ldp; cs.Fnew = (T*)c->Pt[nw]; cs.ldf = c->ldp;
-  cs.omap = c->rowmap; cs.otherF = (const T*)c->PI;
+  cs.omap = c->rowmap[p]; cs.otherF = (const T*)c->PI[p];
   cs.tiles = (int)((c->nloc + TX - 1) / TX);
   cs.mode = kStripFull;
   pa.zt = storage_zeta<T>(zeta); pa.partials = c->partials; pa.done = c->flags;
@@ -305,7 +311,7 @@ FinalizeArgs finalize_args(ircur_ctx* c, int k, const IterSets& q, double eps, i
   FinalizeArgs fa{};
   fa.partials = c->partials;
   fa.I = q.I; fa.mI = q.mI; fa.J = q.J; fa.nJ = q.nJ; fa.row0 = c->row0;
-  fa.rowmap = c->rowmap; fa.colmap = c->colmap;
+  fa.rowmap = c->rowmap[k & 1]; fa.colmap = c->colmap[k & 1];
   fa.k = k; fa.eps = eps; fa.max_iter = max_iter;
   fa.errors = c->errors; fa.done = c->flags; fa.iters = c->flags + 1; fa.converged = c->flags + 2;
   fa.host_done = host_flags ? c->h_flags_dev : nullptr;
@@ -544,16 +550,18 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
     IR_CUDA_C(cudaMalloc(&c->Qt[b], (size_t)rank * c->ldq * c->esz));
   }
   IR_CUDA_C(cudaMalloc(&c->U, (size_t)max_rows * max_cols * sizeof(double)));
-  IR_CUDA_C(cudaMalloc(&c->PoldI, (size_t)max_rows * rank * c->esz));
-  IR_CUDA_C(cudaMalloc(&c->QoldJ, (size_t)max_cols * rank * c->esz));
-  IR_CUDA_C(cudaMalloc(&c->Wr, (size_t)max_rows * rank * c->esz));
-  IR_CUDA_C(cudaMalloc(&c->PI, (size_t)max_rows * rank * c->esz));
-  IR_CUDA_C(cudaMalloc(&c->VS, (size_t)max_cols * rank * c->esz));
-  IR_CUDA_C(cudaMalloc(&c->QJ, (size_t)max_cols * rank * c->esz));
-  IR_CUDA_C(cudaMalloc(&c->W, (size_t)max_rows * rank * sizeof(double)));
-  IR_CUDA_C(cudaMalloc(&c->sigma, (size_t)rank * sizeof(double)));
-  IR_CUDA_C(cudaMalloc(&c->V, (size_t)max_cols * rank * sizeof(double)));
-  IR_CUDA_C(cudaMalloc(&c->inv, (size_t)rank * sizeof(double)));
+  for (int b = 0; b < 2; ++b) {
+    IR_CUDA_C(cudaMalloc(&c->PoldI[b], (size_t)max_rows * rank * c->esz));
+    IR_CUDA_C(cudaMalloc(&c->QoldJ[b], (size_t)max_cols * rank * c->esz));
+    IR_CUDA_C(cudaMalloc(&c->Wr[b], (size_t)max_rows * rank * c->esz));
+    IR_CUDA_C(cudaMalloc(&c->PI[b], (size_t)max_rows * rank * c->esz));
+    IR_CUDA_C(cudaMalloc(&c->VS[b], (size_t)max_cols * rank * c->esz));
+    IR_CUDA_C(cudaMalloc(&c->QJ[b], (size_t)max_cols * rank * c->esz));
+    IR_CUDA_C(cudaMalloc(&c->W[b], (size_t)max_rows * rank * sizeof(double)));
+    IR_CUDA_C(cudaMalloc(&c->sigma[b], (size_t)rank * sizeof(double)));
+    IR_CUDA_C(cudaMalloc(&c->V[b], (size_t)max_cols * rank * sizeof(double)));
+    IR_CUDA_C(cudaMalloc(&c->inv[b], (size_t)rank * sizeof(double)));
+  }
   IR_CUDA_C(cudaMalloc(&c->G, (size_t)max_cols * max_cols * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->svd_scratch, 3 * (size_t)max_cols * 32 * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->Qpart, (size_t)rank * c->ldq * c->esz));
@@ -561,10 +569,12 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMemsetAsync(c->scal, 0, 8 * sizeof(double), c->stream));
   c->max_partials = 4 * 2 * c->num_sms + 8192;  // strips: 4 sums per persistent CTA (<= 2/SM)
   IR_CUDA_C(cudaMalloc(&c->partials, (size_t)c->max_partials * sizeof(double)));
-  IR_CUDA_C(cudaMalloc(&c->rowmap, (size_t)local_rows * sizeof(int)));
-  IR_CUDA_C(cudaMalloc(&c->colmap, (size_t)n2 * sizeof(int)));
-  IR_CUDA_C(cudaMemsetAsync(c->rowmap, 0xFF, (size_t)local_rows * sizeof(int), c->stream));
-  IR_CUDA_C(cudaMemsetAsync(c->colmap, 0xFF, (size_t)n2 * sizeof(int), c->stream));
+  for (int b = 0; b < 2; ++b) {
+    IR_CUDA_C(cudaMalloc(&c->rowmap[b], (size_t)local_rows * sizeof(int)));
+    IR_CUDA_C(cudaMalloc(&c->colmap[b], (size_t)n2 * sizeof(int)));
+    IR_CUDA_C(cudaMemsetAsync(c->rowmap[b], 0xFF, (size_t)local_rows * sizeof(int), c->stream));
+    IR_CUDA_C(cudaMemsetAsync(c->colmap[b], 0xFF, (size_t)n2 * sizeof(int), c->stream));
+  }
   IR_CUDA_C(cudaMalloc(&c->errors, (size_t)max_iter * sizeof(double)));
   IR_CUDA_C(cudaMalloc(&c->flags, 16 * sizeof(int)));
   IR_CUDA_C(cudaMalloc(&c->svd_steps, (size_t)max_iter * sizeof(int)));
@@ -589,9 +599,12 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U,
-                  c->PoldI, c->QoldJ, c->Wr, c->PI, c->VS, c->QJ, c->W, c->sigma, c->V, c->inv,
+                  c->PoldI[0], c->QoldJ[0], c->Wr[0], c->PI[0], c->VS[0], c->QJ[0], c->W[0], c->sigma[0],
+                  c->V[0], c->inv[0], c->PoldI[1], c->QoldJ[1], c->Wr[1], c->PI[1], c->VS[1], c->QJ[1],
+                  c->W[1], c->sigma[1], c->V[1], c->inv[1],
                   c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps,
-                  c->rowmap, c->colmap, c->svd_dbg, c->Qpart, c->scal, c->d_colsel, c->d_cols_c};
+                  c->rowmap[0], c->colmap[0], c->rowmap[1], c->colmap[1], c->svd_dbg, c->Qpart, c->scal,
+                  c->d_colsel, c->d_cols_c};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -855,8 +868,10 @@ int reset_loop(ircur_ctx* c) {
   IR_CUDA(cudaMemsetAsync(c->Pt[0], 0, (size_t)c->r * c->ldp * c->esz, st));
   IR_CUDA(cudaMemsetAsync(c->Qt[0], 0, (size_t)c->r * c->ldq * c->esz, st));
   IR_CUDA(cudaMemsetAsync(c->flags, 0, 16 * sizeof(int), st));
-  IR_CUDA(cudaMemsetAsync(c->rowmap, 0xFF, (size_t)c->nloc * sizeof(int), st));
-  IR_CUDA(cudaMemsetAsync(c->colmap, 0xFF, (size_t)c->n2 * sizeof(int), st));
+  for (int b = 0; b < 2; ++b) {
+    IR_CUDA(cudaMemsetAsync(c->rowmap[b], 0xFF, (size_t)c->nloc * sizeof(int), st));
+    IR_CUDA(cudaMemsetAsync(c->colmap[b], 0xFF, (size_t)c->n2 * sizeof(int), st));
+  }
   volatile int* hf = c->h_flags;
   hf[0] = 0;
   hf[1] = 0;
@@ -1152,14 +1167,15 @@ int ircur_get_core(ircur_ctx_t c, double* W, double* sigma, double* V, double* i
   if (n_cols) *n_cols = nJ;
   const size_t R = (size_t)c->r;
   if (W && kk > 0)
-    IR_CUDA(cudaMemcpy2DAsync(W, kk * sizeof(double), c->W, R * sizeof(double), kk * sizeof(double), mI,
+    IR_CUDA(cudaMemcpy2DAsync(W, kk * sizeof(double), c->W[c->last_k & 1], R * sizeof(double), kk * sizeof(double), mI,
                               cudaMemcpyDefault, c->stream));
   if (V && kk > 0)
-    IR_CUDA(cudaMemcpy2DAsync(V, kk * sizeof(double), c->V, R * sizeof(double), kk * sizeof(double), nJ,
+    IR_CUDA(cudaMemcpy2DAsync(V, kk * sizeof(double), c->V[c->last_k & 1], R * sizeof(double), kk * sizeof(double), nJ,
                               cudaMemcpyDefault, c->stream));
-  if (sigma && kk > 0) IR_CUDA(cudaMemcpyAsync(sigma, c->sigma, kk * sizeof(double), cudaMemcpyDefault, c->stream));
+  if (sigma && kk > 0)
+    IR_CUDA(cudaMemcpyAsync(sigma, c->sigma[c->last_k & 1], kk * sizeof(double), cudaMemcpyDefault, c->stream));
   if (inv_sigma && kk > 0)
-    IR_CUDA(cudaMemcpyAsync(inv_sigma, c->inv, kk * sizeof(double), cudaMemcpyDefault, c->stream));
+    IR_CUDA(cudaMemcpyAsync(inv_sigma, c->inv[c->last_k & 1], kk * sizeof(double), cudaMemcpyDefault, c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));
   return IRCUR_OK;
 }
