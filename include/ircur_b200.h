@@ -239,6 +239,10 @@ int ircur_solve(ircur_ctx_t ctx, const void* D, int64_t ldd, const uint64_t* pcg
  * index sets -> prep begin, prep pass, prep end -> slab norms queued, slab
  * end -> ircur_run, ircur_run -> first loop kernel; -1 when not recorded. */
 int ircur_get_marks(ircur_ctx_t ctx, float* ms);
+/* Diagnostic counters of the last ircur_run: 0 = entries of the next
+ * iteration's gathers that differ from the sampled-factor kernel's
+ * (IRCUR_SAMPLED_CHECK=1; 0 means it reproduces the strips bitwise). */
+int ircur_debug_counter(ircur_ctx_t ctx, int which, long long* value);
 int ircur_get_profile(ircur_ctx_t ctx, int n_iters, int* launched_iters,
                       long long* kernel_launches, float* core_ms, float* svd_ms,
                       float* strips_ms, float* finalize_ms);

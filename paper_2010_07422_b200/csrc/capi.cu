@@ -127,6 +127,10 @@ struct ircur_ctx {
   // [2..) slab norm partials
   unsigned long long* h_res = nullptr;
   bool prep_pending = false;
+  // sampled-factor kernel (kernels_sampled.cu): verification in the sequential loop
+  int sampled_check = 0;        // IRCUR_SAMPLED_CHECK: run it after the strips, compare in the next core
+  int run_fixed = 0;            // mode of the current loop (the next iteration's index set)
+  unsigned* dbg_counter = nullptr;  // [0] sampled-factor mismatches
   int64_t prep_next_row = 0;  // chunked prep: first row of the next chunk
   int slab_pending = -1, slab_nb_rows = 0, slab_nb_cols = 0;
   std::vector<cudaEvent_t> ev;
@@ -212,6 +216,8 @@ CoreArgs<T> core_args(const ircur_ctx* c, int k, const IterSets& q, double zeta)
   const int p = k & 1;
   ca.PoldI = (T*)c->PoldI[p]; ca.QoldJ = (T*)c->QoldJ[p]; ca.done = c->flags;
   ca.rowmap = c->rowmap[p]; ca.colmap = c->colmap[p];
+  ca.verify = (c->sampled_check && k > 0 && sizeof(T) == 4) ? 1 : 0;
+  ca.mismatches = c->dbg_counter;
   return ca;
 }
 
@@ -305,6 +311,37 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
   pa.dbg = c->profiling ? c->svd_dbg + 16 : nullptr;
   pa.maxl = (std::max(c->max_rows, c->max_cols) + c->strips_cs - 1) / c->strips_cs;
   return pa;
+}
+
+// Sampled-factor kernel for the step k -> k + 1: the entries strips_args'
+// launch would produce at the positions of set `set_next` (fp32 only).
+SampledArgs sampled_args(const ircur_ctx* c, int k, const IterSets& q, int set_next, double zeta) {
+  const IterSets qn = iter_sets(c, set_next);
+  const int p = k & 1, pn = p ^ 1, old = k & 1;
+  const int R = c->r;
+  SampledArgs sa{};
+  SampledStrip& rs = sa.s[0];  // Q_k(:, J_{k+1}): the row strip at the next columns
+  rs.src = (const float*)c->D; rs.line_stride = c->ldd; rs.pos_stride = 1;
+  rs.lines = q.I; rs.line_off = (int)c->row0; rs.nk = q.mI;
+  rs.lineA = (const float*)c->PoldI[p]; rs.lineW = (const float*)c->Wr[p] + (size_t)q.i_lo * R;
+  rs.B = (const float*)c->Qt[old]; rs.ldb = c->ldq;
+  rs.pos = qn.J; rs.pos_off = 0; rs.npos = qn.nJ;
+  rs.omap = c->colmap[p]; rs.otherF = (const float*)c->QJ[p];
+  rs.out = (float*)c->QoldJ[pn];
+  SampledStrip& cs = sa.s[1];  // P_k(I_{k+1}, :): the column strip at the next rows
+  if (c->Dt) {
+    cs.src = (const float*)c->Dt; cs.line_stride = c->ldt; cs.pos_stride = 1; cs.lines = q.Jline;
+  } else {
+    cs.src = (const float*)c->D; cs.line_stride = 1; cs.pos_stride = c->ldd; cs.lines = q.J;
+  }
+  cs.line_off = 0; cs.nk = q.nJ;
+  cs.lineA = (const float*)c->QoldJ[p]; cs.lineW = (const float*)c->VS[p];
+  cs.B = (const float*)c->Pt[old]; cs.ldb = c->ldp;
+  cs.pos = qn.I; cs.pos_off = (int)c->row0; cs.npos = qn.mI;
+  cs.omap = c->rowmap[p]; cs.otherF = (const float*)c->PI[p];
+  cs.out = (float*)c->PoldI[pn];
+  sa.zt = storage_zeta<float>(zeta); sa.done = c->flags;
+  return sa;
 }
 
 FinalizeArgs finalize_args(ircur_ctx* c, int k, const IterSets& q, double eps, int max_iter, bool host_flags) {
@@ -425,6 +462,12 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   int ncta = 0;
   IR_CUDA(launch_strips<T>(strips_args<T>(c, k, q, zeta), R, c->strips_cs, c->num_sms, &ncta, st));
   if (pe) IR_CUDA(cudaEventRecord(pe[3], st));
+  if constexpr (sizeof(T) == 4) {
+    // verification: the next iteration's gathers must equal the sampled entries
+    const int set_next = c->run_fixed ? 0 : set + 1;
+    if (c->sampled_check && set_next < c->n_sets)
+      IR_CUDA(launch_sampled_factors(sampled_args(c, k, q, set_next, zeta), R, st));
+  }
   FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, host_flags);
   fa.ncta_rows = ncta;
   IR_CUDA(launch_finalize(fa, st));
@@ -581,6 +624,12 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->svd_dbg, 32 * sizeof(long long)));  // [0,16) SVD, [16,32) strips
   IR_CUDA_C(cudaMemsetAsync(c->svd_dbg, 0, 32 * sizeof(long long), c->stream));
   IR_CUDA_C(cudaMalloc(&c->maxbits, sizeof(unsigned long long)));
+  IR_CUDA_C(cudaMalloc(&c->dbg_counter, 4 * sizeof(unsigned)));
+  IR_CUDA_C(cudaMemsetAsync(c->dbg_counter, 0, 4 * sizeof(unsigned), c->stream));
+  {
+    const char* e = std::getenv("IRCUR_SAMPLED_CHECK");
+    c->sampled_check = e ? std::atoi(e) : 0;
+  }
   IR_CUDA_C(cudaHostAlloc(&c->h_flags, 16 * sizeof(int), cudaHostAllocMapped));
   IR_CUDA_C(cudaHostGetDevicePointer((void**)&c->h_flags_dev, c->h_flags, 0));
   IR_CUDA_C(cudaHostAlloc(&c->h_res, (2 + (size_t)c->max_partials) * sizeof(unsigned long long), cudaHostAllocDefault));
@@ -604,7 +653,7 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
                   c->W[1], c->sigma[1], c->V[1], c->inv[1],
                   c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps,
                   c->rowmap[0], c->colmap[0], c->rowmap[1], c->colmap[1], c->svd_dbg, c->Qpart, c->scal,
-                  c->d_colsel, c->d_cols_c};
+                  c->d_colsel, c->d_cols_c, c->dbg_counter};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -926,7 +975,9 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   cudaStream_t st = c->stream;
   mark(c, 4);
   c->shard_prof = false;
+  c->run_fixed = mode == IRCUR_FIXED;
   if (int rc = reset_loop(c)) return rc;
+  IR_CUDA(cudaMemsetAsync(c->dbg_counter, 0, 4 * sizeof(unsigned), st));
   volatile int* hf = c->h_flags;
   constexpr int kAhead = 3;
   int launched = 0;
@@ -1240,6 +1291,16 @@ int ircur_set_profiling(ircur_ctx_t c, int on) {
     for (auto& e : c->evq) IR_CUDA(cudaEventCreate(&e));
   }
   c->profiling = on != 0;
+  return IRCUR_OK;
+}
+
+int ircur_debug_counter(ircur_ctx_t c, int which, long long* value) {
+  if (!c || !value || which < 0 || which > 3) return fail(IRCUR_EINVAL, "bad context/counter");
+  IR_CUDA(cudaSetDevice(c->device));
+  unsigned v = 0;
+  IR_CUDA(cudaMemcpyAsync(&v, c->dbg_counter + which, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  *value = v;
   return IRCUR_OK;
 }
 

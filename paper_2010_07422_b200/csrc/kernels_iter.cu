@@ -28,19 +28,37 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs<T> a) {
   const int64_t il = (int64_t)a.I[k1] - a.row0;
   const int j = a.J[k2];
   T pa[R], qb[R];
+  if (a.presampled) {
 #pragma unroll
-  for (int t = 0; t < R; ++t) {
-    pa[t] = a.Pt[t * a.ldp + il];
-    qb[t] = a.Qt[t * a.ldq + j];
+    for (int t = 0; t < R; ++t) {
+      pa[t] = a.PoldI[(int64_t)k1 * R + t];
+      qb[t] = a.QoldJ[(int64_t)k2 * R + t];
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      pa[t] = a.Pt[t * a.ldp + il];
+      qb[t] = a.Qt[t * a.ldq + j];
+    }
   }
   if (k2 == 0) {
+    if (!a.presampled) {
 #pragma unroll
-    for (int t = 0; t < R; ++t) a.PoldI[(int64_t)k1 * R + t] = pa[t];
+      for (int t = 0; t < R; ++t) {
+        if (a.verify && a.PoldI[(int64_t)k1 * R + t] != pa[t]) atomicAdd(a.mismatches, 1u);
+        a.PoldI[(int64_t)k1 * R + t] = pa[t];
+      }
+    }
     a.rowmap[il] = a.upos0 + k1;
   }
   if (k1 == 0) {
+    if (!a.presampled) {
 #pragma unroll
-    for (int t = 0; t < R; ++t) a.QoldJ[(int64_t)k2 * R + t] = qb[t];
+      for (int t = 0; t < R; ++t) {
+        if (a.verify && a.QoldJ[(int64_t)k2 * R + t] != qb[t]) atomicAdd(a.mismatches, 1u);
+        a.QoldJ[(int64_t)k2 * R + t] = qb[t];
+      }
+    }
     a.colmap[j] = k2;
   }
   const T l = lowrank_entry<T, R>(pa, qb);

@@ -21,6 +21,11 @@ struct CoreArgs {
   T* PoldI; T* QoldJ;                          // mI x R, nJ x R
   int* rowmap; int* colmap;                    // position -> index maps (set here, cleared by finalize)
   const int* done;
+  // presampled: PoldI / QoldJ already hold P(I,:), Q(:,J) (sampled_factors_kernel
+  // of the previous iteration), read instead of gathering from Pt / Qt.
+  // verify: gather from Pt / Qt as usual but count entries that differ from
+  // what PoldI / QoldJ already hold (a check of the sampled kernel).
+  int presampled; int verify; unsigned* mismatches;
 };
 
 // ---------------------------------------------------------------- strips
@@ -63,6 +68,25 @@ struct StripsArgs {
   long long* dbg;                              // optional per-phase clock64 totals (CTA 0, thread 0)
   int prefetch_dist;                           // strips3: tiles ahead prefetched into L2
   int desync_ns;                               // strips3: start delay of odd CTAs
+};
+
+// ------------------------------------------------------- sampled factors
+// One strip restricted to a list of positions (kernels_sampled.cu): element
+// (line k, position x = pos[p] - pos_off) = src[(lines[k] - line_off) *
+// line_stride + x * pos_stride]; B(:, x) = B[t * ldb + x]; out: npos x R.
+struct SampledStrip {
+  const float* src; int64_t line_stride; int64_t pos_stride;
+  const int* lines; int line_off; int nk;
+  const float* lineA; const float* lineW;      // nk x R
+  const float* B; int64_t ldb;
+  const int* pos; int pos_off; int npos;
+  const int* omap; const float* otherF;         // override: position -> index of the other set
+  float* out;
+};
+struct SampledArgs {
+  SampledStrip s[2];                            // [0] Q(:, J_{k+1}), [1] P(I_{k+1}, :)
+  float zt;
+  const int* done;
 };
 
 // ------------------------------------------------------------- finalize

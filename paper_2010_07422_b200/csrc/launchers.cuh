@@ -52,6 +52,7 @@ cudaError_t launch_strips2(const StripsArgs<float>& a, int R, int num_sms, int* 
 size_t strips2_smem_bytes(int maxl, int R);
 // fp32 64-position single-stage kernel (kernels_strips3.cu); NotSupported when the lines do not fit
 cudaError_t launch_strips3(const StripsArgs<float>& a, int R, int num_sms, int* ncta_out, cudaStream_t st);
+cudaError_t launch_sampled_factors(const SampledArgs& a, int R, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
 template <typename T, typename O>
