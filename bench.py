@@ -260,10 +260,14 @@ def run_ours(args):
         "step_ms": step_ms,
         "host_ms_steps": [{k: round(v, 2) for k, v in (getattr(rr, "_host_ms", None) or {}).items()}
                           for rr in results],
-        "breakdown_ms_per_solve": {
+        "breakdown_ms_per_solve": ({
+            "loop": "overlapped: chain (core, Gram, SVD of k + 1) beside the strips of k",
+            "strips": strip_ms, "chain": svd_ms,
+            "device_gaps_ms": p.get("gaps_ms")} if p.get("overlapped") else {
+            "loop": "sequential",
             "strips": strip_ms, "svd": svd_ms, "core": core_ms,
             "other": ms_per_step - (strip_ms + svd_ms + core_ms),
-            "device_gaps_ms": p.get("gaps_ms")},
+            "device_gaps_ms": p.get("gaps_ms")}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "strips3_kernel" if dts == "f32" else "strips_kernel", "avg_launch_us": strip_ms / n_strip * 1e3,

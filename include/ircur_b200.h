@@ -241,8 +241,13 @@ int ircur_solve(ircur_ctx_t ctx, const void* D, int64_t ldd, const uint64_t* pcg
 int ircur_get_marks(ircur_ctx_t ctx, float* ms);
 /* Diagnostic counters of the last ircur_run: 0 = entries of the next
  * iteration's gathers that differ from the sampled-factor kernel's
- * (IRCUR_SAMPLED_CHECK=1; 0 means it reproduces the strips bitwise). */
+ * (IRCUR_SAMPLED_CHECK=1; 0 means it reproduces the strips bitwise);
+ * 1 = whether the run took the overlapped two-stream loop (IRCUR_OVERLAP). */
 int ircur_debug_counter(ircur_ctx_t ctx, int which, long long* value);
+/* Overlapped, profiled run: per iteration k, ms[4k..4k+3] = start and end
+ * of the chain (core .. SVD) and start and end of the strips, relative to
+ * the first chain's start (diagnostics of the two-stream schedule). */
+int ircur_get_timeline(ircur_ctx_t ctx, int n_iters, float* ms);
 int ircur_get_profile(ircur_ctx_t ctx, int n_iters, int* launched_iters,
                       long long* kernel_launches, float* core_ms, float* svd_ms,
                       float* strips_ms, float* finalize_ms);

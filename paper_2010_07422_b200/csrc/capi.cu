@@ -131,6 +131,15 @@ struct ircur_ctx {
   int sampled_check = 0;        // IRCUR_SAMPLED_CHECK: run it after the strips, compare in the next core
   int run_fixed = 0;            // mode of the current loop (the next iteration's index set)
   unsigned* dbg_counter = nullptr;  // [0] sampled-factor mismatches
+  int err_lag = 1;                  // SVD tolerance from e_{k - err_lag} (set per run)
+  int err_lag_env = 0;              // IRCUR_SVD_ERRLAG, 0 = unset
+  // overlapped loop (run_overlap): chain stream (high priority) and strips stream
+  int overlap = 0;                  // IRCUR_OVERLAP
+  cudaStream_t sA = nullptr, sB = nullptr;
+  std::vector<cudaEvent_t> ovev;    // 5 per iteration: gate, svd, strips, sampled, finalize
+  cudaEvent_t ov_start = nullptr, ov_endA = nullptr, ov_endB = nullptr, ov_cover = nullptr;
+  bool overlap_prof = false;
+  int last_run_overlapped = 0;
   int64_t prep_next_row = 0;  // chunked prep: first row of the next chunk
   int slab_pending = -1, slab_nb_rows = 0, slab_nb_cols = 0;
   std::vector<cudaEvent_t> ev;
@@ -205,7 +214,7 @@ IterSets iter_sets(const ircur_ctx* c, int set) {
 }
 
 template <typename T>
-CoreArgs<T> core_args(const ircur_ctx* c, int k, const IterSets& q, double zeta) {
+CoreArgs<T> core_args(const ircur_ctx* c, int k, const IterSets& q, double zeta, bool presampled = false) {
   const int old = k & 1;
   CoreArgs<T> ca{};
   ca.D = (const T*)c->D; ca.ldd = c->ldd; ca.row0 = c->row0;
@@ -216,7 +225,8 @@ CoreArgs<T> core_args(const ircur_ctx* c, int k, const IterSets& q, double zeta)
   const int p = k & 1;
   ca.PoldI = (T*)c->PoldI[p]; ca.QoldJ = (T*)c->QoldJ[p]; ca.done = c->flags;
   ca.rowmap = c->rowmap[p]; ca.colmap = c->colmap[p];
-  ca.verify = (c->sampled_check && k > 0 && sizeof(T) == 4) ? 1 : 0;
+  ca.presampled = presampled ? 1 : 0;
+  ca.verify = (!presampled && c->sampled_check && k > 0 && sizeof(T) == 4) ? 1 : 0;
   ca.mismatches = c->dbg_counter;
   return ca;
 }
@@ -253,7 +263,9 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   sa.tol_scale = sizeof(T) == 8 ? 1e-11 : 1e-8;
   if (const char* ev = std::getenv(sizeof(T) == 8 ? "IRCUR_SVD_TOL64" : "IRCUR_SVD_TOL32"))  // tuning
     sa.tol = std::atof(ev);
-  sa.prev_err = k > 0 ? c->errors + (k - 1) : nullptr;
+  // e_{k - lag}: lag 1 in the sequential loop; the overlapped loop runs the
+  // SVD of k + 1 next to the stop test of k, so it uses lag 2 (IRCUR_SVD_ERRLAG)
+  sa.prev_err = k >= c->err_lag ? c->errors + (k - c->err_lag) : nullptr;
   sa.dbg = c->profiling ? c->svd_dbg : nullptr;
   sa.maxsteps = 100;
   static const int sweeps = [] {
@@ -534,6 +546,143 @@ int iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int max_ite
                                : launch_iteration<double>(c, k, set, zeta, eps, max_iter, hf);
 }
 
+// ---- overlapped loop ------------------------------------------------------
+// Iteration k + 1's core, Gram matrix and SVD need only P_k(I_{k+1},:) and
+// Q_k(:,J_{k+1}), which the sampled-factor kernel produces right after the
+// SVD of k (bitwise the strips' values).  So the chain stream (high priority)
+// runs  sampled(k) -> core(k+1) -> gram(k+1) -> SVD(k+1)  while the strips
+// stream runs  strips(k) -> finalize(k).  strips(k) is released by the event
+// after gram(k+1), together with SVD(k+1): the SVD's thread-block cluster is
+// placed first (priority) and the strip kernel's grid leaves its SMs free
+// (a persistent grid placed first would leave no GPC with room for the
+// cluster: tools/micro/cluster_coschedule.cu).  Cross-stream order:
+//   sampled(k) after strips(k-1)   (the full P_{k-1}, Q_{k-1}; buffers of parity k-1)
+//   core(k+1)  after finalize(k-1) (position maps of parity k+1 cleared)
+//   finalize(k) after sampled(k)   (it clears the maps sampled(k) reads)
+// The SVD tolerance uses e_{k-1} for iteration k + 1 (err_lag 2).
+
+int read_trace(ircur_ctx* c, const double* zetas, int mode, int* iterations, int* converged, double* errors,
+               float* iter_ms);
+
+int overlap_setup(ircur_ctx* c) {
+  if (!c->sA) {
+    int lo = 0, hi = 0;
+    IR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    IR_CUDA(cudaStreamCreateWithPriority(&c->sA, cudaStreamNonBlocking, hi));
+    IR_CUDA(cudaStreamCreateWithPriority(&c->sB, cudaStreamNonBlocking, lo));
+    for (cudaEvent_t* e : {&c->ov_start, &c->ov_endA, &c->ov_endB, &c->ov_cover})
+      IR_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  if ((int)c->ovev.size() < 5 * c->max_iter) {
+    for (auto& e : c->ovev) cudaEventDestroy(e);
+    c->ovev.assign((size_t)5 * c->max_iter, nullptr);
+    for (auto& e : c->ovev) IR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return IRCUR_OK;
+}
+
+// fp32, one GPU, rank <= 16, strips3_kernel for every set of the loop
+bool overlap_eligible(ircur_ctx* c, int mode, int max_iter) {
+  if (!c->overlap || c->dtype != IRCUR_F32 || c->nloc != c->n1 || c->r > 16 || !c->Dt) return false;
+  if (c->err_lag_env != 0 && c->err_lag_env != 2) return false;
+  const int nsets = mode == IRCUR_FIXED ? 1 : std::min(max_iter, c->n_sets);
+  for (int s = 0; s < nsets; ++s) {
+    const IterSets q = iter_sets(c, s);
+    if (!strips3_selected(strips_args<float>(c, s, q, 1.0), c->r)) return false;
+  }
+  return true;
+}
+
+int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max_iter, int* iterations,
+                int* converged, double* errors, float* iter_ms) {
+  if (int rc = overlap_setup(c)) return rc;
+  cudaStream_t us = c->stream, sA = c->sA, sB = c->sB;
+  const int R = c->r;
+  auto ev = [&](int k, int which) { return c->ovev[(size_t)k * 5 + which]; };  // 0 gate 1 svd 2 strips 3 sampled 4 fin
+  auto set_of = [&](int k) { return mode == IRCUR_FIXED ? 0 : k; };
+  IR_CUDA(cudaEventRecord(c->ov_start, us));
+  IR_CUDA(cudaStreamWaitEvent(sA, c->ov_start, 0));
+  IR_CUDA(cudaStreamWaitEvent(sB, c->ov_start, 0));
+  c->overlap_prof = c->profiling;
+  // the chain part of iteration k: core (gathered at k = 0, else presampled), Gram, SVD
+  auto chain = [&](int k, cudaEvent_t gate) -> int {
+    const IterSets q = iter_sets(c, set_of(k));
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 0], sA));
+    IR_CUDA(launch_core<float>(core_args<float>(c, k, q, zetas[k], k > 0), R, sA));
+    const SvdArgs sa = svd_args<float>(c, k, q);
+    IR_CUDA(launch_svd<float>(sa, svd_cluster_size(q.nJ, q.mI_all, sa.kk), sA, gate));
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 1], sA));
+    IR_CUDA(cudaEventRecord(ev(k, 1), sA));
+    c->kernel_launches += 3;
+    return IRCUR_OK;
+  };
+  // column copy must cover the set before any stream reads it; a rebuild
+  // (rare: the loop ran past the covered sets) drains both streams first
+  auto cover = [&](int set) -> int {
+    if (c->dt_mode != 2 || set < c->covered) return IRCUR_OK;
+    IR_CUDA(cudaStreamSynchronize(sA));
+    IR_CUDA(cudaStreamSynchronize(sB));
+    if (int rc = ensure_cover(c, set)) return rc;
+    IR_CUDA(cudaEventRecord(c->ov_cover, us));
+    IR_CUDA(cudaStreamWaitEvent(sA, c->ov_cover, 0));
+    IR_CUDA(cudaStreamWaitEvent(sB, c->ov_cover, 0));
+    return IRCUR_OK;
+  };
+  if (int rc = cover(set_of(0))) return rc;
+  if (int rc = chain(0, nullptr)) return rc;
+  volatile int* hf = c->h_flags;
+  constexpr int kAhead = 3;
+  int launched = 0;
+  while (launched < max_iter) {
+    const int k = launched;
+    const int set = set_of(k);
+    const bool next = k + 1 < max_iter && set_of(k + 1) < c->n_sets;
+    const IterSets q = iter_sets(c, set);
+    int cs_next = 0;
+    if (next) {
+      if (int rc = cover(set_of(k + 1))) return rc;
+      if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 2), 0));
+      IR_CUDA(launch_sampled_factors(sampled_args(c, k, q, set_of(k + 1), zetas[k]), R, sA));
+      IR_CUDA(cudaEventRecord(ev(k, 3), sA));
+      if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 4), 0));
+      const IterSets qn = iter_sets(c, set_of(k + 1));
+      const SvdArgs san = svd_args<float>(c, k + 1, qn);
+      cs_next = svd_cluster_size(qn.nJ, qn.mI_all, san.kk);
+      if (int rc = chain(k + 1, ev(k, 0))) return rc;
+      c->kernel_launches += 1;
+    }
+    // strips(k) with the SVD(k + 1) cluster's SMs left free, then the stop test
+    IR_CUDA(cudaStreamWaitEvent(sB, next ? ev(k, 0) : ev(k, 1), 0));
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 2], sB));
+    int ncta = 0;
+    IR_CUDA(launch_strips<float>(strips_args<float>(c, k, q, zetas[k]), R, c->strips_cs,
+                                 std::max(1, c->num_sms - cs_next), &ncta, sB));
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 3], sB));
+    IR_CUDA(cudaEventRecord(ev(k, 2), sB));
+    if (next) IR_CUDA(cudaStreamWaitEvent(sB, ev(k, 3), 0));
+    FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, true);
+    fa.ncta_rows = ncta;
+    IR_CUDA(launch_finalize(fa, sB));
+    IR_CUDA(cudaEventRecord(ev(k, 4), sB));
+    IR_CUDA(cudaEventRecord(c->ev[k + 1], sB));
+    c->kernel_launches += 2;
+    ++c->launched_iters;
+    ++launched;
+    // run ahead of the device by at most kAhead iterations; stop when it converged
+    while (hf[0] == 0 && launched >= hf[1] + kAhead) {
+      cudaError_t qr = cudaStreamQuery(sB);
+      if (qr == cudaSuccess) break;
+      if (qr != cudaErrorNotReady) return fail(IRCUR_ECUDA, std::string("stream: ") + cudaGetErrorString(qr));
+    }
+    if (hf[0] != 0) break;
+  }
+  IR_CUDA(cudaEventRecord(c->ov_endA, sA));
+  IR_CUDA(cudaEventRecord(c->ov_endB, sB));
+  IR_CUDA(cudaStreamWaitEvent(us, c->ov_endA, 0));
+  IR_CUDA(cudaStreamWaitEvent(us, c->ov_endB, 0));
+  return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
+}
+
 }  // namespace
 
 extern "C" {
@@ -629,6 +778,10 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   {
     const char* e = std::getenv("IRCUR_SAMPLED_CHECK");
     c->sampled_check = e ? std::atoi(e) : 0;
+    const char* o = std::getenv("IRCUR_OVERLAP");
+    c->overlap = o ? std::atoi(o) : 1;  // the overlapped loop wherever eligible (IRCUR_OVERLAP=0: sequential)
+    const char* l = std::getenv("IRCUR_SVD_ERRLAG");
+    c->err_lag_env = l ? std::max(1, std::atoi(l)) : 0;
   }
   IR_CUDA_C(cudaHostAlloc(&c->h_flags, 16 * sizeof(int), cudaHostAllocMapped));
   IR_CUDA_C(cudaHostGetDevicePointer((void**)&c->h_flags_dev, c->h_flags, 0));
@@ -668,6 +821,18 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evq)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->ovev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ov_start, c->ov_endA, c->ov_endB, c->ov_cover})
+    if (e) cudaEventDestroy(e);
+  if (c->sA) {
+    cudaStreamSynchronize(c->sA);
+    cudaStreamDestroy(c->sA);
+  }
+  if (c->sB) {
+    cudaStreamSynchronize(c->sB);
+    cudaStreamDestroy(c->sB);
+  }
   delete c;
   return IRCUR_OK;
 }
@@ -976,8 +1141,14 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   mark(c, 4);
   c->shard_prof = false;
   c->run_fixed = mode == IRCUR_FIXED;
+  c->overlap_prof = false;
   if (int rc = reset_loop(c)) return rc;
   IR_CUDA(cudaMemsetAsync(c->dbg_counter, 0, 4 * sizeof(unsigned), st));
+  c->last_run_overlapped = overlap_eligible(c, mode, max_iter) ? 1 : 0;
+  // the overlapped loop's SVD(k + 1) starts before e_k exists: it uses e_{k-1}
+  c->err_lag = c->last_run_overlapped ? 2 : (c->err_lag_env ? c->err_lag_env : 1);
+  if (c->last_run_overlapped)
+    return run_overlap(c, zetas, eps, mode, max_iter, iterations, converged, errors, iter_ms);
   volatile int* hf = c->h_flags;
   constexpr int kAhead = 3;
   int launched = 0;
@@ -1297,10 +1468,26 @@ int ircur_set_profiling(ircur_ctx_t c, int on) {
 int ircur_debug_counter(ircur_ctx_t c, int which, long long* value) {
   if (!c || !value || which < 0 || which > 3) return fail(IRCUR_EINVAL, "bad context/counter");
   IR_CUDA(cudaSetDevice(c->device));
+  if (which == 1) {  // the last ircur_run took the overlapped loop
+    *value = c->last_run_overlapped;
+    return IRCUR_OK;
+  }
   unsigned v = 0;
   IR_CUDA(cudaMemcpyAsync(&v, c->dbg_counter + which, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));
   *value = v;
+  return IRCUR_OK;
+}
+
+int ircur_get_timeline(ircur_ctx_t c, int n_iters, float* ms) {
+  if (!c || !ms || n_iters < 1) return fail(IRCUR_EINVAL, "bad arguments");
+  if (!c->overlap_prof || c->evp.empty()) return fail(IRCUR_EINVAL, "no overlapped, profiled run");
+  IR_CUDA(cudaSetDevice(c->device));
+  IR_CUDA(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < n_iters && k < c->max_iter; ++k)
+    for (int j = 0; j < 4; ++j)
+      if (cudaEventElapsedTime(&ms[k * 4 + j], c->evp[0], c->evp[(size_t)k * 5 + j]) != cudaSuccess) ms[k * 4 + j] = -1.f;
+  cudaGetLastError();
   return IRCUR_OK;
 }
 
@@ -1328,11 +1515,13 @@ int ircur_get_profile(ircur_ctx_t c, int n_iters, int* launched_iters, long long
   IR_CUDA(cudaStreamSynchronize(c->stream));
   for (int k = 0; k < n_iters && k < c->max_iter; ++k) {
     float t[4] = {0, 0, 0, 0};
-    if (c->shard_prof) {  // row-sharded run: only the two strip launches are timed
+    if (c->shard_prof || c->overlap_prof) {  // row-sharded / overlapped run: only the strips are timed
       float a = 0.f, b = 0.f;
       IR_CUDA(cudaEventElapsedTime(&a, c->evp[(size_t)k * 5 + 2], c->evp[(size_t)k * 5 + 3]));
-      IR_CUDA(cudaEventElapsedTime(&b, c->evq[(size_t)k * 2], c->evq[(size_t)k * 2 + 1]));
+      if (c->shard_prof) IR_CUDA(cudaEventElapsedTime(&b, c->evq[(size_t)k * 2], c->evq[(size_t)k * 2 + 1]));
       t[2] = a + b;
+      // overlapped: the "svd" slot holds the chain (core, Gram, SVD), which runs beside the strips
+      if (c->overlap_prof) IR_CUDA(cudaEventElapsedTime(&t[1], c->evp[(size_t)k * 5], c->evp[(size_t)k * 5 + 1]));
     } else {
       for (int q = 0; q < 4; ++q)
         IR_CUDA(cudaEventElapsedTime(&t[q], c->evp[(size_t)k * 5 + q], c->evp[(size_t)k * 5 + q + 1]));

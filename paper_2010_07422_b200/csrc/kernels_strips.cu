@@ -496,6 +496,21 @@ static cudaError_t launch_strips_r(const StripsArgs<T>& a, int cs, int num_sms, 
   return cudaLaunchKernelEx(&cfg, strips_kernel<T, R>, a);
 }
 
+static int strips_version() {
+  static const int ver = [] {
+    const char* e = std::getenv("IRCUR_STRIPS_VER");
+    if (!e) e = std::getenv("IRCUR_STRIPS_V1") ? "1" : nullptr;
+    return e ? std::atoi(e) : 3;
+  }();
+  return ver;
+}
+
+bool strips3_selected(const StripsArgs<float>& a, int R) {
+  const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
+  const int maxl = a.s[0].nk > a.s[1].nk ? a.s[0].nk : a.s[1].nk;
+  return strips_version() >= 3 && aligned && strips3_smem_bytes(maxl, R) <= (size_t)227 * 1024;
+}
+
 template <typename T>
 cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, int* ncta_out,
                           cudaStream_t st) {
@@ -506,11 +521,7 @@ cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, in
     // fp32: the 64-position single-stage kernel, else the two-group
     // 32-position kernel, else this cluster kernel.  IRCUR_STRIPS_VER=1|2|3
     // caps the choice (A/B measurements).
-    static const int ver = [] {
-      const char* e = std::getenv("IRCUR_STRIPS_VER");
-      if (!e) e = std::getenv("IRCUR_STRIPS_V1") ? "1" : nullptr;
-      return e ? std::atoi(e) : 3;
-    }();
+    const int ver = strips_version();
     const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
     if (ver >= 3 && aligned) {
       const cudaError_t e = launch_strips3(a, R, num_sms, ncta_out, st);

@@ -267,6 +267,8 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
   }
 }
 
+size_t strips3_smem_bytes(int maxl, int R) { return strips3_layout(maxl, R).total; }
+
 // cudaErrorNotSupported when the sampled lines do not fit the stage
 cudaError_t launch_strips3(const StripsArgs<float>& a0, int R, int num_sms, int* ncta_out, cudaStream_t st) {
   StripsArgs<float> a = a0;

@@ -974,12 +974,16 @@ int svd_pick_cluster(int n, int m, int kk) {
 }
 
 template <typename T>
-cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st) {
+cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st, cudaEvent_t after_gram) {
   const int nt = (a.n + 31) / 32;
   gram_kernel<<<(unsigned)(nt * (nt + 1) / 2), 256, 0, st>>>(a.U, a.ldu, a.m, a.n, const_cast<double*>(a.G),
                                                              a.ldg, a.done);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (after_gram) {  // (overlapped loop: gates the previous iteration's strips)
+    e = cudaEventRecord(after_gram, st);
+    if (e != cudaSuccess) return e;
+  }
   const size_t smem = svd_smem_bytes(a.n, a.m, a.kk, cs);
   // kk <= 8 (r <= 6): the kernel with the register-resident small solvers;
   // larger blocks: the shared-memory solvers only (its registers and code
@@ -1010,7 +1014,7 @@ cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template cudaError_t launch_svd<float>(const SvdArgs&, int, cudaStream_t);
-template cudaError_t launch_svd<double>(const SvdArgs&, int, cudaStream_t);
+template cudaError_t launch_svd<float>(const SvdArgs&, int, cudaStream_t, cudaEvent_t);
+template cudaError_t launch_svd<double>(const SvdArgs&, int, cudaStream_t, cudaEvent_t);
 
 }  // namespace ircur

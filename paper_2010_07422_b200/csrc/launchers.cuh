@@ -53,6 +53,10 @@ size_t strips2_smem_bytes(int maxl, int R);
 // fp32 64-position single-stage kernel (kernels_strips3.cu); NotSupported when the lines do not fit
 cudaError_t launch_strips3(const StripsArgs<float>& a, int R, int num_sms, int* ncta_out, cudaStream_t st);
 cudaError_t launch_sampled_factors(const SampledArgs& a, int R, cudaStream_t st);
+size_t strips3_smem_bytes(int maxl, int R);
+// the fp32 strip launch of `a` runs strips3_kernel (what the sampled-factor
+// kernel reproduces bitwise)
+bool strips3_selected(const StripsArgs<float>& a, int R);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
 template <typename T, typename O>
@@ -71,7 +75,8 @@ cudaError_t launch_slab_sq(const T* D, int64_t ldd, int64_t row0, int64_t nloc, 
                            double* partials, const T* Dt, int64_t ldt, const int* Jline, cudaStream_t st);
 size_t svd_smem_bytes(int n, int m, int kk, int cs);
 int svd_pick_cluster(int n, int m, int kk);
-template <typename T> cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st);
+template <typename T> cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st,
+                                             cudaEvent_t after_gram = nullptr);
 cudaError_t launch_gen(const GenArgs& a, int64_t* nblocks_out, cudaStream_t st);
 int64_t gen_blocks(int64_t nrows, int64_t n2);
 

@@ -214,7 +214,11 @@ class Context:
         _capi.check(self.lib.ircur_get_svd_steps(self.h, n_iters, steps.ctypes.data_as(C.POINTER(C.c_int))))
         marks = np.full(5, -1.0, dtype=np.float32)
         _capi.check(self.lib.ircur_get_marks(self.h, marks.ctypes.data_as(pf)))
+        ov = C.c_longlong(0)
+        _capi.check(self.lib.ircur_debug_counter(self.h, 1, C.byref(ov)))
+        # overlapped loop: svd_ms is the chain (core, Gram, SVD) beside the strips; core_ms is 0
         return dict(launched_iters=li.value, kernel_launches=kl.value, svd_steps=steps[:n_iters],
+                    overlapped=bool(ov.value),
                     gaps_ms=dict(zip(("upload_to_prep", "prep", "prep_to_slab_end", "slab_to_run",
                                       "run_to_first_kernel"), [float(x) for x in marks])),
                     core_ms=arrs[0][:n_iters], svd_ms=arrs[1][:n_iters],

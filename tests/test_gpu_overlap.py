@@ -38,6 +38,7 @@ def _mismatches(res) -> int:
 @pytest.mark.parametrize("colmajor", ["sampled", "full"])
 def test_sampled_factors_equal_strip_factors(ir, monkeypatch, r, mode, colmajor):
     monkeypatch.setenv("IRCUR_SAMPLED_CHECK", "1")
+    monkeypatch.setenv("IRCUR_OVERLAP", "0")  # the check runs in the sequential loop
     ir.clear_cache()  # the flag is read when a context is created
     try:
         D, L, S, linf = orc.baseline_problem(900, 700, r, 0.1, seed=40 + r)
@@ -48,6 +49,7 @@ def test_sampled_factors_equal_strip_factors(ir, monkeypatch, r, mode, colmajor)
         assert _mismatches(res) == 0
     finally:
         monkeypatch.delenv("IRCUR_SAMPLED_CHECK")
+        monkeypatch.delenv("IRCUR_OVERLAP")
         ir.clear_cache()
 
 
@@ -57,6 +59,7 @@ def test_check_detects_a_different_summation_order(ir, monkeypatch):
     differ from the sampled kernel's in the last bits, and the counter sees it."""
     import torch
     monkeypatch.setenv("IRCUR_SAMPLED_CHECK", "1")
+    monkeypatch.setenv("IRCUR_OVERLAP", "0")  # the check runs in the sequential loop
     ir.clear_cache()
     try:
         D, L, S, linf = orc.baseline_problem(900, 700, 5, 0.1, seed=45)
@@ -65,4 +68,76 @@ def test_check_detects_a_different_summation_order(ir, monkeypatch):
         assert _mismatches(res) > 0
     finally:
         monkeypatch.delenv("IRCUR_SAMPLED_CHECK")
+        monkeypatch.delenv("IRCUR_OVERLAP")
         ir.clear_cache()
+
+
+def _flag(res, which):
+    v = C.c_longlong(-1)
+    assert res.ctx.lib.ircur_debug_counter(res.ctx.h, which, C.byref(v)) == 0
+    return int(v.value)
+
+
+@pytest.mark.parametrize("r", [2, 5, 10])
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+@pytest.mark.parametrize("colmajor", ["sampled", "full"])
+def test_overlapped_loop_equals_sequential(ir, monkeypatch, r, mode, colmajor):
+    """The two-stream loop (SVD of k + 1 next to the strips of k, IRCUR_OVERLAP)
+    gives bitwise the sequential loop's results with the same SVD tolerance
+    lag (IRCUR_SVD_ERRLAG=2): trace, strips, core."""
+    import torch
+    D, L, S, linf = orc.baseline_problem(1500, 1300, r, 0.1, seed=60 + r)
+    Dd = torch.from_numpy(D.astype(np.float32)).cuda()
+    cfg = ir.SolverConfig(rank=r, zeta0=linf, gamma=0.7, mode=mode, max_iter=60, seed=ir.RngSeed(4))
+    out = []
+    try:
+        for env in ({"IRCUR_SVD_ERRLAG": "2", "IRCUR_OVERLAP": "0"}, {"IRCUR_OVERLAP": "1"}):
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            ir.clear_cache()
+            res = ir.solve_device(Dd, cfg, colmajor=colmajor)
+            assert _flag(res, 1) == int(env["IRCUR_OVERLAP"])
+            cur, sp, tr = ir.solve(Dd, cfg, colmajor=colmajor)
+            out.append((cur, sp, tr))
+            for k in env:
+                monkeypatch.delenv(k)
+    finally:
+        ir.clear_cache()
+    (c1, s1, t1), (c2, s2, t2) = out
+    assert t1.iterations == t2.iterations and t1.errors == t2.errors and t1.converged == t2.converged
+    assert t1.iterations > 3
+    np.testing.assert_array_equal(c1.C, c2.C)
+    np.testing.assert_array_equal(c1.R, c2.R)
+    np.testing.assert_array_equal(s1.row_values, s2.row_values)
+    np.testing.assert_array_equal(s1.col_values, s2.col_values)
+    np.testing.assert_array_equal(c1.core_pinv.sigma, c2.core_pinv.sigma)
+
+
+@pytest.mark.parametrize("dtype,colmajor,want", [("f32", "sampled", 1), ("f32", "full", 1),
+                                                 ("f32", False, 0), ("f64", "sampled", 0)])
+def test_default_loop_selection(ir, monkeypatch, dtype, colmajor, want):
+    """With no environment override the overlapped loop runs wherever it is
+    eligible (fp32, one GPU, strips3_kernel on every set: needs the column
+    copy), and the sequential loop elsewhere; both match the oracle."""
+    import torch
+    monkeypatch.delenv("IRCUR_OVERLAP", raising=False)
+    monkeypatch.delenv("IRCUR_SVD_ERRLAG", raising=False)
+    ir.clear_cache()
+    D, L, S, linf = orc.baseline_problem(800, 600, 4, 0.1, seed=77)
+    Dm = D.astype(np.float32) if dtype == "f32" else D
+    cfg = ir.SolverConfig(rank=4, zeta0=linf, gamma=0.7, mode="resampled", max_iter=60, seed=ir.RngSeed(5))
+    try:
+        res = ir.solve_device(torch.from_numpy(Dm).cuda(), cfg, colmajor=colmajor)
+        assert _flag(res, 1) == want
+        cur, sp, tr = ir.solve(Dm, cfg, device=0, colmajor=colmajor)
+    finally:
+        ir.clear_cache()
+    ref = orc.solve(np.asarray(Dm, dtype=np.float64), rank=4, zeta0=linf, gamma=0.7, mode="resampled",
+                    max_iter=60, seed=5)
+    np.testing.assert_array_equal(cur.rows.indices, ref.rows)
+    np.testing.assert_array_equal(cur.cols.indices, ref.cols)
+    tol = 1e-4 if dtype == "f32" else 1e-9
+    assert abs(tr.iterations - ref.iterations) <= (1 if dtype == "f32" else 0)
+    if tr.iterations == ref.iterations:
+        assert np.linalg.norm(cur.C - ref.C) <= tol * np.linalg.norm(ref.C)
+        assert np.linalg.norm(sp.row_values - ref.S_rows) <= tol * max(np.linalg.norm(ref.S_rows), 1.0)
