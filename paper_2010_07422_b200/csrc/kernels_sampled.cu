@@ -18,6 +18,9 @@
 // mode, tests/test_gpu_overlap.py).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <mutex>
+
 #include "kernels_iter.cuh"
 #include "launchers.cuh"
 
@@ -84,12 +87,117 @@ __global__ void __launch_bounds__(256) sampled_factors_kernel(const __grid_const
   }
 }
 
+// Staged variant: a block takes kSmpP positions of one strip.  Phase 1
+// computes every thresholded element e(line, position) in parallel into
+// shared memory (the element gathers and line loads are independent, so
+// they overlap), phase 2 forms the 16 ordered partial sums per (position, t)
+// from shared memory, phase 3 adds them in warp order.  Same operations in
+// the same order as sampled_factors_kernel, so the same bits; several times
+// more parallel memory traffic in flight.
+constexpr int kSmpP = 4;
+
+__host__ __device__ inline size_t sampled_staged_smem(int nk, int R) {
+  const int nk2 = nk + (nk & 1);
+  return ((size_t)nk2 * kSmpP + (size_t)nk2 * R + (size_t)kSmpP * R + (size_t)kSmpP * kSmpW * R) * sizeof(float);
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) sampled_staged_kernel(const __grid_constant__ SampledArgs a) {
+  if (*a.done) return;
+  const SampledStrip& s = a.s[blockIdx.y];
+  const int p0 = blockIdx.x * kSmpP;
+  if (p0 >= s.npos) return;
+  const int nk = s.nk, nk2 = nk + (nk & 1);
+  extern __shared__ float smp_sm[];
+  float* sE = smp_sm;               // [nk2][kSmpP] thresholded elements
+  float* sW = sE + nk2 * kSmpP;     // [nk2][R] line weights (row nk zero)
+  float* sB = sW + nk2 * R;         // [kSmpP][R] old factor at the positions
+  float* red = sB + kSmpP * R;      // [kSmpP][kSmpW][R] partial sums
+  __shared__ int64_t xs[kSmpP];
+  const int tid = threadIdx.x;
+  if (tid < kSmpP) xs[tid] = p0 + tid < s.npos ? (int64_t)s.pos[p0 + tid] - s.pos_off : -1;
+  for (int i = tid; i < nk * R; i += blockDim.x) sW[i] = s.lineW[i];
+  if (nk & 1) {
+    for (int i = tid; i < R; i += blockDim.x) sW[nk * R + i] = 0.f;
+    for (int i = tid; i < kSmpP; i += blockDim.x) sE[nk * kSmpP + i] = 0.f;
+  }
+  __syncthreads();
+  for (int i = tid; i < kSmpP * R; i += blockDim.x) {
+    const int p = i / R, t = i - p * R;
+    sB[i] = xs[p] >= 0 ? s.B[t * s.ldb + xs[p]] : 0.f;
+  }
+  __syncthreads();
+  // phase 1: e(k, p) = d - T_zeta(d - <A_k, B(:, x_p)>), as strips3_kernel
+#pragma unroll 4
+  for (int i = tid; i < nk * kSmpP; i += blockDim.x) {
+    const int k = i / kSmpP, p = i - k * kSmpP;
+    const int64_t x = xs[p];
+    float e = 0.f;
+    if (x >= 0) {
+      const float d = s.src[(int64_t)(s.lines[k] - s.line_off) * s.line_stride + x * s.pos_stride];
+      const float* A = s.lineA + (int64_t)k * R;
+      const float* b = sB + p * R;
+      float l = __fmul_rn(A[0], b[0]);
+#pragma unroll
+      for (int t = 1; t < R; ++t) l = __fmaf_rn(A[t], b[t], l);
+      const float xd = __fmaf_rn(l, -1.f, d);
+      const float sv = fabsf(xd) > a.zt ? xd : 0.f;
+      e = __fmaf_rn(sv, -1.f, d);
+    }
+    sE[i] = e;
+  }
+  __syncthreads();
+  // phase 2: partial w sums line pairs kp = w, w + 16, ...; 2kp before 2kp + 1
+  const int npair = nk2 / 2;
+  for (int i = tid; i < kSmpP * R * kSmpW; i += blockDim.x) {
+    const int w = i % kSmpW, t = (i / kSmpW) % R, p = i / (kSmpW * R);
+    float acc = 0.f;
+    for (int kp = w; kp < npair; kp += kSmpW) {
+      const int k0 = 2 * kp, k1 = k0 + 1;
+      acc = __fmaf_rn(sW[k0 * R + t], sE[k0 * kSmpP + p], acc);
+      acc = __fmaf_rn(sW[k1 * R + t], sE[k1 * kSmpP + p], acc);
+    }
+    red[(p * kSmpW + w) * R + t] = acc;
+  }
+  __syncthreads();
+  // phase 3: fixed warp order, then the override of the other index set
+  for (int i = tid; i < kSmpP * R; i += blockDim.x) {
+    const int p = i / R, t = i - p * R;
+    if (xs[p] < 0) continue;
+    const int o = s.omap[xs[p]];
+    float v;
+    if (o >= 0) {
+      v = s.otherF[(int64_t)o * R + t];
+    } else {
+      v = red[(p * kSmpW) * R + t];
+#pragma unroll
+      for (int ww = 1; ww < kSmpW; ++ww) v += red[(p * kSmpW + ww) * R + t];
+    }
+    s.out[(int64_t)(p0 + p) * R + t] = v;
+  }
+}
+
 cudaError_t launch_sampled_factors(const SampledArgs& a, int R, cudaStream_t st) {
   const int n = a.s[0].npos > a.s[1].npos ? a.s[0].npos : a.s[1].npos;
   if (n == 0) return cudaSuccess;
   if (R > kSmpW) return cudaErrorNotSupported;  // one thread per factor entry in the final sum
-  dim3 grid((unsigned)((n + kSmpPos - 1) / kSmpPos), 2);
+  const int nk = a.s[0].nk > a.s[1].nk ? a.s[0].nk : a.s[1].nk;
+  const size_t smem = sampled_staged_smem(nk, R);
+  static const bool legacy = std::getenv("IRCUR_SAMPLED_LEGACY") != nullptr;  // A/B knob
   cudaError_t e = cudaErrorInvalidValue;
+  if (!legacy && smem <= 200 * 1024) {
+    dim3 grid((unsigned)((n + kSmpP - 1) / kSmpP), 2);
+    IRCUR_DISPATCH_RANK(R, RR, {
+      static std::once_flag once;
+      std::call_once(once, [] {
+        cudaFuncSetAttribute(sampled_staged_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      });
+      sampled_staged_kernel<RR><<<grid, 256, smem, st>>>(a);
+      e = cudaGetLastError();
+    });
+    return e;
+  }
+  dim3 grid((unsigned)((n + kSmpPos - 1) / kSmpPos), 2);
   IRCUR_DISPATCH_RANK(R, RR, {
     sampled_factors_kernel<RR><<<grid, kSmpPos * kSmpW, 0, st>>>(a);
     e = cudaGetLastError();
