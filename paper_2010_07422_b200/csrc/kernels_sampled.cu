@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(256) sampled_factors_kernel(const __grid_const
 // the same order as sampled_factors_kernel, so the same bits; several times
 // more parallel memory traffic in flight.
 constexpr int kSmpP = 4;
+constexpr int kSmpB = 4;     // element gathers in flight per thread
+constexpr int kSmpThreads = 512;
 
 __host__ __device__ inline size_t sampled_staged_smem(int nk, int R) {
   const int nk2 = nk + (nk & 1);
@@ -102,7 +104,7 @@ __host__ __device__ inline size_t sampled_staged_smem(int nk, int R) {
 }
 
 template <int R>
-__global__ void __launch_bounds__(256) sampled_staged_kernel(const __grid_constant__ SampledArgs a) {
+__global__ void __launch_bounds__(kSmpThreads) sampled_staged_kernel(const __grid_constant__ SampledArgs a) {
   if (*a.done) return;
   const SampledStrip& s = a.s[blockIdx.y];
   const int p0 = blockIdx.x * kSmpP;
@@ -127,24 +129,36 @@ __global__ void __launch_bounds__(256) sampled_staged_kernel(const __grid_consta
     sB[i] = xs[p] >= 0 ? s.B[t * s.ldb + xs[p]] : 0.f;
   }
   __syncthreads();
-  // phase 1: e(k, p) = d - T_zeta(d - <A_k, B(:, x_p)>), as strips3_kernel
-#pragma unroll 4
-  for (int i = tid; i < nk * kSmpP; i += blockDim.x) {
-    const int k = i / kSmpP, p = i - k * kSmpP;
-    const int64_t x = xs[p];
-    float e = 0.f;
-    if (x >= 0) {
-      const float d = s.src[(int64_t)(s.lines[k] - s.line_off) * s.line_stride + x * s.pos_stride];
-      const float* A = s.lineA + (int64_t)k * R;
-      const float* b = sB + p * R;
-      float l = __fmul_rn(A[0], b[0]);
+  // phase 1: e(k, p) = d - T_zeta(d - <A_k, B(:, x_p)>), as strips3_kernel;
+  // each thread issues kSmpB independent element gathers before using them
+  const int ne = nk * kSmpP;
+  for (int base = tid; base < ne; base += kSmpB * blockDim.x) {
+    float d[kSmpB];
 #pragma unroll
-      for (int t = 1; t < R; ++t) l = __fmaf_rn(A[t], b[t], l);
-      const float xd = __fmaf_rn(l, -1.f, d);
-      const float sv = fabsf(xd) > a.zt ? xd : 0.f;
-      e = __fmaf_rn(sv, -1.f, d);
+    for (int u = 0; u < kSmpB; ++u) {
+      const int i = base + u * blockDim.x;
+      const int k = i / kSmpP, p = i - k * kSmpP;
+      d[u] = i < ne && xs[p] >= 0 ? s.src[(int64_t)(s.lines[k] - s.line_off) * s.line_stride + xs[p] * s.pos_stride]
+                                  : 0.f;
     }
-    sE[i] = e;
+#pragma unroll
+    for (int u = 0; u < kSmpB; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i >= ne) break;
+      const int k = i / kSmpP, p = i - k * kSmpP;
+      float e = 0.f;
+      if (xs[p] >= 0) {
+        const float* A = s.lineA + (int64_t)k * R;
+        const float* b = sB + p * R;
+        float l = __fmul_rn(A[0], b[0]);
+#pragma unroll
+        for (int t = 1; t < R; ++t) l = __fmaf_rn(A[t], b[t], l);
+        const float xd = __fmaf_rn(l, -1.f, d[u]);
+        const float sv = fabsf(xd) > a.zt ? xd : 0.f;
+        e = __fmaf_rn(sv, -1.f, d[u]);
+      }
+      sE[i] = e;
+    }
   }
   __syncthreads();
   // phase 2: partial w sums line pairs kp = w, w + 16, ...; 2kp before 2kp + 1
@@ -192,7 +206,7 @@ cudaError_t launch_sampled_factors(const SampledArgs& a, int R, cudaStream_t st)
       std::call_once(once, [] {
         cudaFuncSetAttribute(sampled_staged_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       });
-      sampled_staged_kernel<RR><<<grid, 256, smem, st>>>(a);
+      sampled_staged_kernel<RR><<<grid, kSmpThreads, smem, st>>>(a);
       e = cudaGetLastError();
     });
     return e;
