@@ -488,7 +488,7 @@ def run_batch(args):
             st.wait_event(start)
             with torch.cuda.stream(st):
                 for i in range(w, len(probs), ns):
-                    res = ir.solve_device(probs[i], cfgs[i], colmajor=cm, fetch_factors=False,
+                    res = ir.solve_device(probs[i], cfgs[i], colmajor=cm, fetch_factors=False, overlap=False,
                                           profile="deferred" if record else False)
                     if record:
                         p = res.read_profile()

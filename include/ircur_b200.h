@@ -244,6 +244,12 @@ int ircur_get_marks(ircur_ctx_t ctx, float* ms);
  * (IRCUR_SAMPLED_CHECK=1; 0 means it reproduces the strips bitwise);
  * 1 = whether the run took the overlapped two-stream loop (IRCUR_OVERLAP). */
 int ircur_debug_counter(ircur_ctx_t ctx, int which, long long* value);
+/* Loop selection for the following runs on ctx: 1 = the overlapped loop
+ * (SVD of k + 1 beside the strips of k on two streams) where eligible, 0 =
+ * the sequential loop, -1 = the default (IRCUR_OVERLAP at creation, else 1).
+ * Callers that run several solves concurrently on one GPU pass 0: the
+ * overlapped loop sizes its strip grid for a GPU of its own. */
+int ircur_set_overlap(ircur_ctx_t ctx, int mode);
 /* Overlapped, profiled run: per iteration k, ms[4k..4k+3] = start and end
  * of the chain (core .. SVD) and start and end of the strips, relative to
  * the first chain's start (diagnostics of the two-stream schedule). */

@@ -133,6 +133,7 @@ struct ircur_ctx {
   unsigned* dbg_counter = nullptr;  // [0] sampled-factor mismatches
   int err_lag = 1;                  // SVD tolerance from e_{k - err_lag} (set per run)
   int err_lag_env = 0;              // IRCUR_SVD_ERRLAG, 0 = unset
+  int overlap_default = 1;          // IRCUR_OVERLAP at creation (ircur_set_overlap(ctx, -1) restores it)
   // overlapped loop (run_overlap): chain stream (high priority) and strips stream
   int overlap = 0;                  // IRCUR_OVERLAP
   cudaStream_t sA = nullptr, sB = nullptr;
@@ -780,6 +781,7 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
     c->sampled_check = e ? std::atoi(e) : 0;
     const char* o = std::getenv("IRCUR_OVERLAP");
     c->overlap = o ? std::atoi(o) : 1;  // the overlapped loop wherever eligible (IRCUR_OVERLAP=0: sequential)
+    c->overlap_default = c->overlap;
     const char* l = std::getenv("IRCUR_SVD_ERRLAG");
     c->err_lag_env = l ? std::max(1, std::atoi(l)) : 0;
   }
@@ -1145,8 +1147,11 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   if (int rc = reset_loop(c)) return rc;
   IR_CUDA(cudaMemsetAsync(c->dbg_counter, 0, 4 * sizeof(unsigned), st));
   c->last_run_overlapped = overlap_eligible(c, mode, max_iter) ? 1 : 0;
-  // the overlapped loop's SVD(k + 1) starts before e_k exists: it uses e_{k-1}
-  c->err_lag = c->last_run_overlapped ? 2 : (c->err_lag_env ? c->err_lag_env : 1);
+  // the overlapped loop's SVD(k + 1) starts before e_k exists: it uses e_{k-1}.
+  // fp32 runs use the same lag in the sequential loop, so the loop choice
+  // (ircur_set_overlap, eligibility) never changes an fp32 result.
+  const int lag_default = c->dtype == IRCUR_F32 ? 2 : 1;
+  c->err_lag = c->last_run_overlapped ? 2 : (c->err_lag_env ? c->err_lag_env : lag_default);
   if (c->last_run_overlapped)
     return run_overlap(c, zetas, eps, mode, max_iter, iterations, converged, errors, iter_ms);
   volatile int* hf = c->h_flags;
@@ -1476,6 +1481,12 @@ int ircur_debug_counter(ircur_ctx_t c, int which, long long* value) {
   IR_CUDA(cudaMemcpyAsync(&v, c->dbg_counter + which, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));
   *value = v;
+  return IRCUR_OK;
+}
+
+int ircur_set_overlap(ircur_ctx_t c, int mode) {
+  if (!c || mode < -1 || mode > 1) return fail(IRCUR_EINVAL, "mode must be -1, 0 or 1");
+  c->overlap = mode < 0 ? c->overlap_default : mode;
   return IRCUR_OK;
 }
 

@@ -27,6 +27,8 @@
 
 #include "ircur_common.cuh"
 #include "launchers.cuh"
+#include <mutex>
+
 #include "svd_small_reg.cuh"
 
 namespace cg = cooperative_groups;
@@ -42,53 +44,73 @@ constexpr int kLdV = kKMax;  // leading dimension of V in the L2 scratch
 // ------------------------------------------------------------------ gram
 // G = U^T U (n x n).  One CTA per 32 x 32 tile of the upper triangle (the
 // mirrored tile is written from the same sums: fma(a, b, c) == fma(b, a, c),
-// so G is exactly symmetric); K = m in 32-row chunks, register-prefetched
-// one chunk ahead into a double-buffered shared tile (one barrier per chunk).
-__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U, int ldu, int m, int n,
+// so G is exactly symmetric); K = m in 32-row chunks streamed through a
+// kGramNS-stage cp.async pipeline.  The kernel is bound by shared-load ->
+// DFMA latency (ncu: short-scoreboard stalls, FP64 pipe 19% busy), so each
+// chunk's rows 0..15 and 16..31 go to the two 256-thread halves of the CTA
+// (twice the warps per scheduler); the halves' sums, each in row order, are
+// added in a fixed order at the end.
+constexpr int kGramNS = 4;
+constexpr int kGramSmem = kGramNS * 2 * 32 * 33 * (int)sizeof(double);
+
+__global__ void __launch_bounds__(512) gram_kernel(const double* __restrict__ U, int ldu, int m, int n,
                                                    double* __restrict__ G, int ldg, const int* done) {
   if (done && *done) return;
-  __shared__ double A[2][32][33];
-  __shared__ double B[2][32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty 0..7
+  extern __shared__ double gram_sm[];
+  auto As = [&](int st, int r, int c) -> double& { return gram_sm[((st * 2) * 32 + r) * 33 + c]; };
+  auto Bs = [&](int st, int r, int c) -> double& { return gram_sm[((st * 2 + 1) * 32 + r) * 33 + c]; };
+  const int tx = threadIdx.x & 31, ty = (threadIdx.x >> 5) & 7;  // ty 0..7
+  const int half = threadIdx.x >> 8;
   // blockIdx.x -> (ta <= tb) in row-major order of the upper triangle
   const int nt = (n + 31) / 32;
   int ta = 0, rem = (int)blockIdx.x;
   while (rem >= nt - ta) { rem -= nt - ta; ++ta; }
   const int tb = ta + rem;
   const int a0 = ta * 32, b0 = tb * 32;
+  const int nch = (m + 31) / 32;
+  auto issue = [&](int ch) {
+    if (ch < nch) {
+      const int st = ch % kGramNS;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int r = ty + 8 * (2 * half + k), i = ch * 32 + r;
+        const bool va = i < m && a0 + tx < n, vb = i < m && b0 + tx < n;
+        const double* pa = va ? U + (int64_t)i * ldu + a0 + tx : U;
+        const double* pb = vb ? U + (int64_t)i * ldu + b0 + tx : U;
+        const unsigned da = (unsigned)__cvta_generic_to_shared(&As(st, r, tx));
+        const unsigned db = (unsigned)__cvta_generic_to_shared(&Bs(st, r, tx));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(da), "l"(pa), "r"(va ? 8 : 0));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(db), "l"(pb), "r"(vb ? 8 : 0));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
   double acc[4] = {0, 0, 0, 0};
-  double ra[4], rb[4];
-  auto fetch = [&](int i0) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = i0 + ty + 8 * k;
-      ra[k] = (i < m && a0 + tx < n) ? U[(int64_t)i * ldu + a0 + tx] : 0.0;
-      rb[k] = (i < m && b0 + tx < n) ? U[(int64_t)i * ldu + b0 + tx] : 0.0;
-    }
-  };
-  auto put = [&](int bf) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      A[bf][ty + 8 * k][tx] = ra[k];
-      B[bf][ty + 8 * k][tx] = rb[k];
-    }
-  };
-  fetch(0);
-  put(0);
-  __syncthreads();
-  int bf = 0;
-  for (int i0 = 0; i0 < m; i0 += 32, bf ^= 1) {
-    const bool more = i0 + 32 < m;
-    if (more) fetch(i0 + 32);
+  for (int c = 0; c < kGramNS - 1; ++c) issue(c);
+  for (int c = 0; c < nch; ++c) {
+    issue(c + kGramNS - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kGramNS - 1));
+    __syncthreads();
+    const int st = c % kGramNS;
 #pragma unroll 8
-    for (int i = 0; i < 32; ++i) {
-      const double bv = B[bf][i][tx];
+    for (int i = 16 * half; i < 16 * half + 16; ++i) {
+      const double bv = Bs(st, i, tx);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(A[bf][i][ty + 8 * u], bv, acc[u]);
+      for (int u = 0; u < 4; ++u) acc[u] = fma(As(st, i, ty + 8 * u), bv, acc[u]);
     }
-    if (more) put(bf ^ 1);
     __syncthreads();
   }
+  // second half's sums through shared memory (the pipeline buffers are idle)
+  double* part = gram_sm;
+  if (half == 1) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) part[(ty + 8 * u) * 33 + tx] = acc[u];
+  }
+  __syncthreads();
+  if (half == 1) return;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) acc[u] += part[(ty + 8 * u) * 33 + tx];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int r = a0 + ty + 8 * u, c = b0 + tx;
@@ -976,8 +998,12 @@ int svd_pick_cluster(int n, int m, int kk) {
 template <typename T>
 cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st, cudaEvent_t after_gram) {
   const int nt = (a.n + 31) / 32;
-  gram_kernel<<<(unsigned)(nt * (nt + 1) / 2), 256, 0, st>>>(a.U, a.ldu, a.m, a.n, const_cast<double*>(a.G),
-                                                             a.ldg, a.done);
+  static std::once_flag gram_once;
+  std::call_once(gram_once, [] {
+    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGramSmem);
+  });
+  gram_kernel<<<(unsigned)(nt * (nt + 1) / 2), 512, kGramSmem, st>>>(a.U, a.ldu, a.m, a.n,
+                                                                     const_cast<double*>(a.G), a.ldg, a.done);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (after_gram) {  // (overlapped loop: gates the previous iteration's strips)

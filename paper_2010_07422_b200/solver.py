@@ -204,6 +204,10 @@ class Context:
     def set_profiling(self, on: bool) -> None:
         _capi.check(self.lib.ircur_set_profiling(self.h, int(on)))
 
+    def set_overlap(self, overlap) -> None:
+        """None: library default; True / False: overlapped (where eligible) / sequential loop."""
+        _capi.check(self.lib.ircur_set_overlap(self.h, -1 if overlap is None else int(bool(overlap))))
+
     def profile(self, n_iters: int) -> dict:
         li, kl = C.c_int(), C.c_longlong()
         arrs = [np.zeros(max(n_iters, 1), dtype=np.float32) for _ in range(4)]
@@ -528,7 +532,7 @@ class DeviceResult:
 
 
 def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
-                 colmajor="auto", fetch_factors=True, profile=False) -> DeviceResult:
+                 colmajor="auto", fetch_factors=True, profile=False, overlap=None) -> DeviceResult:
     """Run the loop on the device; results stay on the device (see solve).
 
     The returned DeviceResult reads its strips/core from the cached library
@@ -538,19 +542,22 @@ def solve_device(D, config: SolverConfig, observer=None, *, device=None, compute
     fetch_factors="copy" for private factor tensors.  profile=True reads the
     per-kernel event times into result.profile; profile="deferred" records
     the events but leaves the read-back to result.read_profile(), keeping
-    it out of the caller's timed region.
+    it out of the caller's timed region.  overlap: None = the library
+    default (the overlapped loop where eligible), False = the sequential loop
+    (concurrent solves sharing one GPU), True = overlapped where eligible.
     """
     leases: list = []
     try:
         return _solve_device(D, config, observer, device=device, compute_dtype=compute_dtype, colmajor=colmajor,
-                             fetch_factors=fetch_factors, profile=profile, _leases=leases)
+                             fetch_factors=fetch_factors, profile=profile, overlap=overlap, _leases=leases)
     finally:
         for c in leases:
             _release(c)
 
 
 def _solve_device(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
-                  colmajor="auto", fetch_factors=True, profile=False, _leases=None) -> DeviceResult:
+                  colmajor="auto", fetch_factors=True, profile=False, overlap=None,
+                  _leases=None) -> DeviceResult:
     """See solve_device."""
     cfg = config
     tick = _Ticker(profile)
@@ -579,6 +586,7 @@ def _solve_device(D, config: SolverConfig, observer=None, *, device=None, comput
         ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
         _leases.append(ctx)
         ctx.set_profiling(bool(profile))
+        ctx.set_overlap(overlap)
         return _solve_native(ctx, Dd, cfg, pcg, code, fetch_factors, dtype, n1, n2, m_rows, m_cols, profile)
     # Draw the sets the prep pass needs first; the rest of the sequence is
     # drawn by a worker thread while the (host-blocking) prep pass runs.
@@ -593,6 +601,7 @@ def _solve_device(D, config: SolverConfig, observer=None, *, device=None, comput
     ctx = _context(dev, dtype, n1, n2, cfg.rank, m_rows, m_cols, cfg.max_iter, stream)
     _leases.append(ctx)
     ctx.set_profiling(bool(profile))
+    ctx.set_overlap(overlap)
     ctx.set_indices(sets)
     tick("set_indices")
     cm, cover = _copy_plan(colmajor, n2, m_cols, sets, cfg)
@@ -791,19 +800,20 @@ def _zero_results(n1, n2, rows: IndexSet, cols: IndexSet, rank: int):
 
 
 def solve(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=None,
-          colmajor="auto"):
+          colmajor="auto", overlap=None):
     """Drop-in for ircur.solver.solve (solver.py:304-416).
 
     Returns (CurFactors, SparseEstimate, SolverTrace) with float64 host
     arrays.  Extra keyword arguments (not in the reference): `device` (CUDA
     ordinal), `compute_dtype` (torch dtype; default keeps fp32 input in fp32
     and runs everything else in fp64) and `colmajor` (build the column-major
-    copy of D used by the column-strip kernel: True/False/"auto").
+    copy of D used by the column-strip kernel: True/False/"auto") and
+    `overlap` (loop selection, see solve_device).
     """
     leases: list = []  # the context stays leased until its results are read back
     try:
         res = _solve_device(D, config, observer, device=device, compute_dtype=compute_dtype,
-                            colmajor=colmajor, fetch_factors="copy", _leases=leases)
+                            colmajor=colmajor, fetch_factors="copy", overlap=overlap, _leases=leases)
         n1, n2 = res.rows.bound, res.cols.bound
         if res.zero_state:
             cur, sparse = _zero_results(n1, n2, res.rows, res.cols, config.rank)
@@ -841,7 +851,9 @@ def solve_batch(Ds, configs, *, device=None, streams: int = 4, compute_dtype=Non
         st = pool_streams[w]
         with torch.cuda.device(dev), torch.cuda.stream(st):
             for i in range(w, len(Ds), nstreams):
-                out[i] = solve(Ds[i], configs[i], device=dev, compute_dtype=compute_dtype, colmajor=colmajor)
+                # the sequential loop: the overlapped one sizes its strip grid for a GPU of its own
+                out[i] = solve(Ds[i], configs[i], device=dev, compute_dtype=compute_dtype, colmajor=colmajor,
+                               overlap=False)
             st.synchronize()
 
     with cf.ThreadPoolExecutor(nstreams) as ex:

@@ -141,3 +141,20 @@ def test_default_loop_selection(ir, monkeypatch, dtype, colmajor, want):
     if tr.iterations == ref.iterations:
         assert np.linalg.norm(cur.C - ref.C) <= tol * np.linalg.norm(ref.C)
         assert np.linalg.norm(sp.row_values - ref.S_rows) <= tol * max(np.linalg.norm(ref.S_rows), 1.0)
+
+
+def test_loop_choice_does_not_change_fp32_results(ir):
+    """overlap=False (solve_batch's choice) and the default overlapped loop
+    give bitwise the same fp32 results: both use the SVD tolerance lag 2."""
+    D, L, S, linf = orc.baseline_problem(1200, 1000, 5, 0.2, seed=91)
+    Dm = D.astype(np.float32)
+    cfg = ir.SolverConfig(rank=5, zeta0=linf, gamma=0.7, mode="resampled", max_iter=60, seed=ir.RngSeed(8))
+    out = []
+    for ov in (None, False, True):
+        res = ir.solve_device(Dm, cfg, device=0, overlap=ov)
+        assert _flag(res, 1) == (0 if ov is False else 1)
+        out.append(ir.solve(Dm, cfg, device=0, overlap=ov))
+    for cur, sp, tr in out[1:]:
+        assert tr.errors == out[0][2].errors and tr.iterations == out[0][2].iterations
+        np.testing.assert_array_equal(cur.C, out[0][0].C)
+        np.testing.assert_array_equal(sp.col_values, out[0][1].col_values)
