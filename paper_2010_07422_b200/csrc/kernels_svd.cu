@@ -42,25 +42,31 @@ constexpr int kEigNT = 128;  // threads running the small dense kernels
 constexpr int kLdV = kKMax;  // leading dimension of V in the L2 scratch
 
 // ------------------------------------------------------------------ gram
-// G = U^T U (n x n).  One CTA per 32 x 32 tile of the upper triangle (the
-// mirrored tile is written from the same sums: fma(a, b, c) == fma(b, a, c),
-// so G is exactly symmetric); K = m in 32-row chunks streamed through a
-// kGramNS-stage cp.async pipeline.  The kernel is bound by shared-load ->
-// DFMA latency (ncu: short-scoreboard stalls, FP64 pipe 19% busy), so each
-// chunk's rows 0..15 and 16..31 go to the two 256-thread halves of the CTA
-// (twice the warps per scheduler); the halves' sums, each in row order, are
-// added in a fixed order at the end.
+// G = U^T U (n x n) on the FP64 tensor cores (mma.sync m8n8k4 f64).  One CTA
+// per 32 x 32 tile of the upper triangle; warp w owns the 8 x 8 blocks
+// (w / 2, 2 (w % 2) + {0, 1}) and runs K = m in steps of 4 rows.  K streams in
+// 32-row chunks through a kGramNS-stage cp.async pipeline.  Exact symmetry:
+// below-diagonal blocks of a diagonal tile are not computed, and a diagonal
+// 8 x 8 block writes its upper triangle and the mirror of it.  (The CUDA-core
+// version — one DFMA per shared load, latency-bound at 23 us for 460^2 — is
+// what this replaces.)
 constexpr int kGramNS = 4;
-constexpr int kGramSmem = kGramNS * 2 * 32 * 33 * (int)sizeof(double);
+constexpr int kGramLd = 33;
+constexpr int kGramSmem = kGramNS * 2 * 32 * kGramLd * (int)sizeof(double);
 
-__global__ void __launch_bounds__(512) gram_kernel(const double* __restrict__ U, int ldu, int m, int n,
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U, int ldu, int m, int n,
                                                    double* __restrict__ G, int ldg, const int* done) {
   if (done && *done) return;
   extern __shared__ double gram_sm[];
-  auto As = [&](int st, int r, int c) -> double& { return gram_sm[((st * 2) * 32 + r) * 33 + c]; };
-  auto Bs = [&](int st, int r, int c) -> double& { return gram_sm[((st * 2 + 1) * 32 + r) * 33 + c]; };
-  const int tx = threadIdx.x & 31, ty = (threadIdx.x >> 5) & 7;  // ty 0..7
-  const int half = threadIdx.x >> 8;
+  auto As = [&](int st, int r, int c) -> double& { return gram_sm[((st * 2) * 32 + r) * kGramLd + c]; };
+  auto Bs = [&](int st, int r, int c) -> double& { return gram_sm[((st * 2 + 1) * 32 + r) * kGramLd + c]; };
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // blockIdx.x -> (ta <= tb) in row-major order of the upper triangle
   const int nt = (n + 31) / 32;
   int ta = 0, rem = (int)blockIdx.x;
@@ -71,21 +77,26 @@ __global__ void __launch_bounds__(512) gram_kernel(const double* __restrict__ U,
   auto issue = [&](int ch) {
     if (ch < nch) {
       const int st = ch % kGramNS;
+      const int c = tid & 31;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int r = ty + 8 * (2 * half + k), i = ch * 32 + r;
-        const bool va = i < m && a0 + tx < n, vb = i < m && b0 + tx < n;
-        const double* pa = va ? U + (int64_t)i * ldu + a0 + tx : U;
-        const double* pb = vb ? U + (int64_t)i * ldu + b0 + tx : U;
-        const unsigned da = (unsigned)__cvta_generic_to_shared(&As(st, r, tx));
-        const unsigned db = (unsigned)__cvta_generic_to_shared(&Bs(st, r, tx));
+      for (int k = 0; k < 4; ++k) {
+        const int r = (tid >> 5) + 8 * k, i = ch * 32 + r;
+        const bool va = i < m && a0 + c < n, vb = i < m && b0 + c < n;
+        const double* pa = va ? U + (int64_t)i * ldu + a0 + c : U;
+        const double* pb = vb ? U + (int64_t)i * ldu + b0 + c : U;
+        const unsigned da = (unsigned)__cvta_generic_to_shared(&As(st, r, c));
+        const unsigned db = (unsigned)__cvta_generic_to_shared(&Bs(st, r, c));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(da), "l"(pa), "r"(va ? 8 : 0));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(db), "l"(pb), "r"(vb ? 8 : 0));
       }
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
-  double acc[4] = {0, 0, 0, 0};
+  const int br = warp >> 1, bc0 = (warp & 1) * 2;  // block row, first block column (8 x 8 blocks)
+  const bool diag = ta == tb;
+  const bool on0 = !diag || bc0 >= br, on1 = !diag || bc0 + 1 >= br;
+  const int g = lane >> 2, q = lane & 3;  // fragment row / column group
+  double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
 #pragma unroll
   for (int c = 0; c < kGramNS - 1; ++c) issue(c);
   for (int c = 0; c < nch; ++c) {
@@ -93,32 +104,35 @@ __global__ void __launch_bounds__(512) gram_kernel(const double* __restrict__ U,
     asm volatile("cp.async.wait_group %0;\n" ::"n"(kGramNS - 1));
     __syncthreads();
     const int st = c % kGramNS;
-#pragma unroll 8
-    for (int i = 16 * half; i < 16 * half + 16; ++i) {
-      const double bv = Bs(st, i, tx);
+    if (on0 || on1) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fma(As(st, i, ty + 8 * u), bv, acc[u]);
+      for (int k0 = 0; k0 < 32; k0 += 4) {
+        const double av = As(st, k0 + q, br * 8 + g);
+        const double bv0 = Bs(st, k0 + q, bc0 * 8 + g);
+        const double bv1 = Bs(st, k0 + q, bc0 * 8 + 8 + g);
+        if (on0) dmma_8x8x4(acc0, av, bv0);
+        if (on1) dmma_8x8x4(acc1, av, bv1);
+      }
     }
     __syncthreads();
   }
-  // second half's sums through shared memory (the pipeline buffers are idle)
-  double* part = gram_sm;
-  if (half == 1) {
+  auto store = [&](const double (&acc)[2], int bc) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) part[(ty + 8 * u) * 33 + tx] = acc[u];
-  }
-  __syncthreads();
-  if (half == 1) return;
-#pragma unroll
-  for (int u = 0; u < 4; ++u) acc[u] += part[(ty + 8 * u) * 33 + tx];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int r = a0 + ty + 8 * u, c = b0 + tx;
-    if (r < n && c < n) {
-      G[(int64_t)r * ldg + c] = acc[u];
-      if (ta != tb) G[(int64_t)c * ldg + r] = acc[u];
+    for (int h = 0; h < 2; ++h) {
+      const int r = a0 + br * 8 + g, cc = b0 + bc * 8 + 2 * q + h;
+      if (r >= n || cc >= n) continue;
+      if (diag && bc == br) {  // diagonal block: upper triangle and its mirror
+        if (cc < r) continue;
+        G[(int64_t)r * ldg + cc] = acc[h];
+        G[(int64_t)cc * ldg + r] = acc[h];
+      } else {
+        G[(int64_t)r * ldg + cc] = acc[h];
+        G[(int64_t)cc * ldg + r] = acc[h];
+      }
     }
-  }
+  };
+  if (on0) store(acc0, bc0);
+  if (on1) store(acc1, bc0 + 1);
 }
 
 // ------------------------------------------------------------ layout
@@ -1002,7 +1016,7 @@ cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st, cudaEvent_t af
   std::call_once(gram_once, [] {
     cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGramSmem);
   });
-  gram_kernel<<<(unsigned)(nt * (nt + 1) / 2), 512, kGramSmem, st>>>(a.U, a.ldu, a.m, a.n,
+  gram_kernel<<<(unsigned)(nt * (nt + 1) / 2), 256, kGramSmem, st>>>(a.U, a.ldu, a.m, a.n,
                                                                      const_cast<double*>(a.G), a.ldg, a.done);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
