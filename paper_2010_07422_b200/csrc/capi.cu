@@ -264,6 +264,8 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   sa.tol_scale = sizeof(T) == 8 ? 1e-11 : 1e-8;
   if (const char* ev = std::getenv(sizeof(T) == 8 ? "IRCUR_SVD_TOL64" : "IRCUR_SVD_TOL32"))  // tuning
     sa.tol = std::atof(ev);
+  if (const char* ev = std::getenv(sizeof(T) == 8 ? "IRCUR_SVD_TOLSCALE64" : "IRCUR_SVD_TOLSCALE32"))  // tuning
+    sa.tol_scale = std::atof(ev);
   // e_{k - lag}: lag 1 in the sequential loop; the overlapped loop runs the
   // SVD of k + 1 next to the stop test of k, so it uses lag 2 (IRCUR_SVD_ERRLAG)
   sa.prev_err = k >= c->err_lag ? c->errors + (k - c->err_lag) : nullptr;

@@ -1,6 +1,7 @@
-"""Core-SVD tolerance floor sweep (diagnostics): steps, time and result drift.
+"""Core-SVD tolerance sweep (diagnostics): steps, time and result drift.
 
-    IRCUR_SVD_TOL32=1e-9 python tools/tol_sweep.py cfg5
+    python tools/tol_sweep.py cfg5 1e-6 1e-7 ...          (the floor, IRCUR_SVD_TOL32/64)
+    TOL_VAR=SCALE python tools/tol_sweep.py cfg5 1e-8 1e-5  (the e_{k-lag} scale, IRCUR_SVD_TOLSCALE32/64)
 """
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -18,8 +19,9 @@ cfg = ir.SolverConfig(rank=r, eps=bench.EPS, zeta0=linf, gamma=bench.GAMMA, mode
                       max_iter=bench.MAX_ITER, seed=ir.RngSeed(bench.SOLVER_SEED))
 out = {}
 for tol in sys.argv[2:]:
-    os.environ["IRCUR_SVD_TOL32"] = tol
-    os.environ["IRCUR_SVD_TOL64"] = tol
+    var = "TOLSCALE" if os.environ.get("TOL_VAR") == "SCALE" else "TOL"
+    os.environ[f"IRCUR_SVD_{var}32"] = tol
+    os.environ[f"IRCUR_SVD_{var}64"] = tol
     ir.solve_device(D, cfg, profile=True)
     ts = []
     for _ in range(3):
