@@ -134,6 +134,12 @@ struct ircur_ctx {
   int err_lag = 1;                  // SVD tolerance from e_{k - err_lag} (set per run)
   int err_lag_env = 0;              // IRCUR_SVD_ERRLAG, 0 = unset
   int overlap_default = 1;          // IRCUR_OVERLAP at creation (ircur_set_overlap(ctx, -1) restores it)
+  // ircur_solve with zeta0 given: chain(0) of the overlapped loop launched
+  // before the prep pass (pre_chain0), the pass gated behind its SVD cluster
+  bool chain0_pre = false;
+  bool prep_gate_pending = false;
+  int prep_sms = 0;                 // SMs the prep pass's persistent grid may use (0 = all)
+  cudaEvent_t ov_gate0 = nullptr;
   // overlapped loop (run_overlap): chain stream (high priority) and strips stream
   int overlap = 0;                  // IRCUR_OVERLAP
   cudaStream_t sA = nullptr, sB = nullptr;
@@ -430,24 +436,30 @@ int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfi
 int prep_rows(ircur_ctx* c, int64_t r0, int64_t r1) {
   cudaStream_t st = c->stream;
   const int64_t nr = r1 - r0;
+  if (c->prep_gate_pending) {  // placed after chain(0)'s SVD cluster (pre_chain0)
+    IR_CUDA(cudaStreamWaitEvent(st, c->ov_gate0, 0));
+    c->prep_gate_pending = false;
+  }
+  const int sms = c->prep_sms > 0 ? c->prep_sms : c->num_sms;
+  if (r1 == c->nloc) c->prep_sms = 0;
   if (c->dtype == IRCUR_F32) {
     const float* D = (const float*)c->D + r0 * c->ldd;
     float* Dt = c->Dt ? (float*)c->Dt + r0 : nullptr;
     if (c->dt_mode == 2)
       IR_CUDA(launch_prep_select<float>(D, c->ldd, nr, c->n2, c->d_colsel, Dt, c->ldt, c->maxbits, c->flags + 3,
-                                        c->num_sms, st));
+                                        sms, st));
     else
       IR_CUDA(launch_prep<float>(D, c->ldd, nr, c->n2, c->dt_mode == 1 ? Dt : nullptr, c->ldt, c->maxbits,
-                                 c->flags + 3, c->num_sms, st));
+                                 c->flags + 3, sms, st));
   } else {
     const double* D = (const double*)c->D + r0 * c->ldd;
     double* Dt = c->Dt ? (double*)c->Dt + r0 : nullptr;
     if (c->dt_mode == 2)
       IR_CUDA(launch_prep_select<double>(D, c->ldd, nr, c->n2, c->d_colsel, Dt, c->ldt, c->maxbits,
-                                         c->flags + 3, c->num_sms, st));
+                                         c->flags + 3, sms, st));
     else
       IR_CUDA(launch_prep<double>(D, c->ldd, nr, c->n2, c->dt_mode == 1 ? Dt : nullptr, c->ldt, c->maxbits,
-                                  c->flags + 3, c->num_sms, st));
+                                  c->flags + 3, sms, st));
   }
   return IRCUR_OK;
 }
@@ -573,7 +585,7 @@ int overlap_setup(ircur_ctx* c) {
     IR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     IR_CUDA(cudaStreamCreateWithPriority(&c->sA, cudaStreamNonBlocking, hi));
     IR_CUDA(cudaStreamCreateWithPriority(&c->sB, cudaStreamNonBlocking, lo));
-    for (cudaEvent_t* e : {&c->ov_start, &c->ov_endA, &c->ov_endB, &c->ov_cover})
+    for (cudaEvent_t* e : {&c->ov_start, &c->ov_endA, &c->ov_endB, &c->ov_cover, &c->ov_gate0})
       IR_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   if ((int)c->ovev.size() < 5 * c->max_iter) {
@@ -632,7 +644,10 @@ int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max
     return IRCUR_OK;
   };
   if (int rc = cover(set_of(0))) return rc;
-  if (int rc = chain(0, nullptr)) return rc;
+  if (c->chain0_pre)
+    c->chain0_pre = false;  // chain(0) is already queued on sA (pre_chain0), ahead of the prep pass
+  else if (int rc = chain(0, nullptr))
+    return rc;
   volatile int* hf = c->h_flags;
   constexpr int kAhead = 3;
   int launched = 0;
@@ -684,6 +699,67 @@ int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max
   IR_CUDA(cudaStreamWaitEvent(us, c->ov_endA, 0));
   IR_CUDA(cudaStreamWaitEvent(us, c->ov_endB, 0));
   return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
+}
+
+// ircur_solve with zeta0 given: iteration 0's core reads D itself and its
+// threshold is known, so chain(0) (core, Gram, SVD) needs nothing from the
+// prep pass.  It is queued on the chain stream first; the pass waits for the
+// same gate as the SVD cluster and leaves the cluster's SMs free (the pass is
+// HBM-bound).  ircur_run then continues the overlapped loop at sampled(0).
+// Eligibility is decided for any set size up to max_rows x max_cols, as
+// overlap_eligible decides it once the column copy exists.
+int reset_loop(ircur_ctx* c);
+
+int pre_chain0(ircur_ctx* c, const void* D, int64_t ldd, double zeta0, int mode, int cm) {
+  c->chain0_pre = false;
+  c->prep_gate_pending = false;
+  c->prep_sms = 0;
+  const char* knob = std::getenv("IRCUR_PRE_CHAIN0");  // A/B knob, read per solve
+  const bool off = knob && std::atoi(knob) == 0;
+  if (off || !(zeta0 > 0.0) || cm == 0 || !c->overlap || c->dtype != IRCUR_F32 || c->nloc != c->n1 || c->r > 16 ||
+      !D || ldd < c->n2)  // (a bad ldd is reported by the prep call that follows)
+    return IRCUR_OK;
+  if (c->err_lag_env != 0 && c->err_lag_env != 2) return IRCUR_OK;
+  c->D = D;  // (ircur_prepare_async sets the same; the core and the strip plan read it)
+  c->ldd = ldd;
+  const IterSets q = iter_sets(c, 0);
+  {
+    StripsArgs<float> a = strips_args<float>(c, 0, q, 1.0);
+    a.s[0].nk = c->max_rows;
+    a.s[1].nk = c->max_cols;
+    a.s[1].bulk_ok = 1;  // the column copy's ldt is padded to 16 bytes
+    if (!strips3_selected(a, c->r)) return IRCUR_OK;
+  }
+  if (int rc = overlap_setup(c)) return rc;
+  cudaStream_t us = c->stream;
+  c->run_fixed = mode == IRCUR_FIXED;
+  if (int rc = reset_loop(c)) return rc;
+  IR_CUDA(cudaMemsetAsync(c->dbg_counter, 0, 4 * sizeof(unsigned), us));
+  c->err_lag = 2;
+  IR_CUDA(cudaEventRecord(c->ov_start, us));
+  IR_CUDA(cudaStreamWaitEvent(c->sA, c->ov_start, 0));
+  if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[0], c->sA));
+  IR_CUDA(launch_core<float>(core_args<float>(c, 0, q, zeta0, false), c->r, c->sA));
+  const SvdArgs sa = svd_args<float>(c, 0, q);
+  const int cs = svd_cluster_size(q.nJ, q.mI_all, sa.kk);
+  IR_CUDA(launch_svd<float>(sa, cs, c->sA, c->ov_gate0));
+  if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[1], c->sA));
+  IR_CUDA(cudaEventRecord(c->ovev[1], c->sA));  // ev(0, 1): SVD(0) done
+  c->kernel_launches += 3;
+  c->chain0_pre = true;
+  c->prep_gate_pending = true;
+  c->prep_sms = std::max(1, c->num_sms - cs);
+  return IRCUR_OK;
+}
+
+// An ircur_solve that returns before ircur_run: the pre-launched chain(0)
+// is joined into the solver stream and forgotten.
+void drop_pre(ircur_ctx* c) {
+  if (!c->chain0_pre && !c->prep_gate_pending) return;
+  if (c->sA && cudaEventRecord(c->ov_endA, c->sA) == cudaSuccess) cudaStreamWaitEvent(c->stream, c->ov_endA, 0);
+  c->chain0_pre = false;
+  c->prep_gate_pending = false;
+  c->prep_sms = 0;
 }
 
 }  // namespace
@@ -1146,8 +1222,12 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   c->shard_prof = false;
   c->run_fixed = mode == IRCUR_FIXED;
   c->overlap_prof = false;
-  if (int rc = reset_loop(c)) return rc;
-  IR_CUDA(cudaMemsetAsync(c->dbg_counter, 0, 4 * sizeof(unsigned), st));
+  if (c->chain0_pre && !(overlap_eligible(c, mode, max_iter) && c->run_fixed == (mode == IRCUR_FIXED)))
+    drop_pre(c);  // (not expected: pre_chain0 checks the same conditions)
+  if (!c->chain0_pre) {
+    if (int rc = reset_loop(c)) return rc;
+    IR_CUDA(cudaMemsetAsync(c->dbg_counter, 0, 4 * sizeof(unsigned), st));
+  }
   c->last_run_overlapped = overlap_eligible(c, mode, max_iter) ? 1 : 0;
   // the overlapped loop's SVD(k + 1) starts before e_k exists: it uses e_{k-1}.
   // fp32 runs use the same lag in the sequential loop, so the loop choice
@@ -1223,6 +1303,12 @@ int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, 
     }
   }
   if (copy_mode) *copy_mode = cm;
+  struct PreGuard {
+    ircur_ctx* c;
+    bool armed = true;
+    ~PreGuard() { if (armed) drop_pre(c); }
+  } guard{c};
+  if (int rc = pre_chain0(c, D, ldd, zeta0, mode, cm)) return rc;
   if (int rc = ircur_prepare_async(c, D, ldd, cm, cover)) return rc;
   // the rest of the sequence is drawn and uploaded while the pass runs
   if (n_first < n_sets) {
@@ -1252,6 +1338,7 @@ int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, 
   if (zeta0_used) *zeta0_used = z0;
   std::vector<double> zetas((size_t)max_iter);
   for (int k = 0; k < max_iter; ++k) zetas[k] = std::pow(gamma, (double)k) * z0;  // solver.py:372
+  guard.armed = false;  // ircur_run continues the pre-launched chain (or drops it)
   return ircur_run(c, zetas.data(), eps, mode, max_iter, iterations, converged, errors, iter_ms);
 }
 

@@ -158,3 +158,34 @@ def test_loop_choice_does_not_change_fp32_results(ir):
         assert tr.errors == out[0][2].errors and tr.iterations == out[0][2].iterations
         np.testing.assert_array_equal(cur.C, out[0][0].C)
         np.testing.assert_array_equal(sp.col_values, out[0][1].col_values)
+
+
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+def test_chain0_beside_prep_pass_is_bitwise_neutral(ir, monkeypatch, mode):
+    """With zeta0 given, ircur_solve queues iteration 0's core, Gram and SVD
+    ahead of the prep pass (which runs beside the SVD cluster).  Results are
+    bitwise those of the plain order (IRCUR_PRE_CHAIN0=0); a NaN in D still
+    raises, and zeta0 = None (max|D| needed first) takes the plain order."""
+    import torch
+    D, L, S, linf = orc.baseline_problem(1500, 1300, 6, 0.1, seed=93)
+    Dd = torch.from_numpy(D.astype(np.float32)).cuda()
+    cfg = ir.SolverConfig(rank=6, zeta0=linf, gamma=0.7, mode=mode, max_iter=60, seed=ir.RngSeed(6))
+    out = []
+    for knob in ("0", "1"):
+        monkeypatch.setenv("IRCUR_PRE_CHAIN0", knob)
+        res = ir.solve_device(Dd, cfg)
+        assert _flag(res, 1) == 1
+        out.append(ir.solve(Dd, cfg))
+    (c1, s1, t1), (c2, s2, t2) = out
+    assert t1.errors == t2.errors and t1.iterations == t2.iterations and t1.iterations > 3
+    np.testing.assert_array_equal(c1.C, c2.C)
+    np.testing.assert_array_equal(c1.R, c2.R)
+    np.testing.assert_array_equal(s1.row_values, s2.row_values)
+    np.testing.assert_array_equal(c1.core_pinv.sigma, c2.core_pinv.sigma)
+    Dn = Dd.clone()
+    Dn[700, 11] = float("nan")
+    with pytest.raises(ValueError):
+        ir.solve(Dn, cfg)
+    cur, sp, tr = ir.solve(Dd, cfg)  # the context is still usable after the error
+    assert tr.errors == t1.errors
+    monkeypatch.delenv("IRCUR_PRE_CHAIN0")
