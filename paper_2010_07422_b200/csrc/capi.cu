@@ -137,6 +137,7 @@ struct ircur_ctx {
   // ircur_solve with zeta0 given: chain(0) of the overlapped loop launched
   // before the prep pass (pre_chain0), the pass gated behind its SVD cluster
   bool chain0_pre = false;
+  bool chain1_pre = false;          // sampled(0) and chain(1) queued as well
   bool prep_gate_pending = false;
   int prep_sms = 0;                 // SMs the prep pass's persistent grid may use (0 = all)
   cudaEvent_t ov_gate0 = nullptr;
@@ -336,7 +337,8 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
 
 // Sampled-factor kernel for the step k -> k + 1: the entries strips_args'
 // launch would produce at the positions of set `set_next` (fp32 only).
-SampledArgs sampled_args(const ircur_ctx* c, int k, const IterSets& q, int set_next, double zeta) {
+SampledArgs sampled_args(const ircur_ctx* c, int k, const IterSets& q, int set_next, double zeta,
+                         bool from_D = false) {
   const IterSets qn = iter_sets(c, set_next);
   const int p = k & 1, pn = p ^ 1, old = k & 1;
   const int R = c->r;
@@ -350,9 +352,9 @@ SampledArgs sampled_args(const ircur_ctx* c, int k, const IterSets& q, int set_n
   rs.omap = c->colmap[p]; rs.otherF = (const float*)c->QJ[p];
   rs.out = (float*)c->QoldJ[pn];
   SampledStrip& cs = sa.s[1];  // P_k(I_{k+1}, :): the column strip at the next rows
-  if (c->Dt) {
+  if (c->Dt && !from_D) {
     cs.src = (const float*)c->Dt; cs.line_stride = c->ldt; cs.pos_stride = 1; cs.lines = q.Jline;
-  } else {
+  } else {  // (from_D: the same elements, read from D before the column copy exists)
     cs.src = (const float*)c->D; cs.line_stride = 1; cs.pos_stride = c->ldd; cs.lines = q.J;
   }
   cs.line_off = 0; cs.nk = q.nJ;
@@ -644,8 +646,9 @@ int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max
     return IRCUR_OK;
   };
   if (int rc = cover(set_of(0))) return rc;
+  const bool pre1 = c->chain0_pre && c->chain1_pre;
   if (c->chain0_pre)
-    c->chain0_pre = false;  // chain(0) is already queued on sA (pre_chain0), ahead of the prep pass
+    c->chain0_pre = c->chain1_pre = false;  // chain(0) (and chain(1)) already queued on sA by pre_chain0
   else if (int rc = chain(0, nullptr))
     return rc;
   volatile int* hf = c->h_flags;
@@ -657,7 +660,11 @@ int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max
     const bool next = k + 1 < max_iter && set_of(k + 1) < c->n_sets;
     const IterSets q = iter_sets(c, set);
     int cs_next = 0;
-    if (next) {
+    if (next && k == 0 && pre1) {  // sampled(0) -> chain(1) ran beside the prep pass
+      if (int rc = cover(set_of(1))) return rc;
+      const IterSets qn = iter_sets(c, set_of(1));
+      cs_next = svd_cluster_size(qn.nJ, qn.mI_all, svd_args<float>(c, 1, qn).kk);
+    } else if (next) {
       if (int rc = cover(set_of(k + 1))) return rc;
       if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 2), 0));
       IR_CUDA(launch_sampled_factors(sampled_args(c, k, q, set_of(k + 1), zetas[k]), R, sA));
@@ -710,8 +717,10 @@ int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max
 // overlap_eligible decides it once the column copy exists.
 int reset_loop(ircur_ctx* c);
 
-int pre_chain0(ircur_ctx* c, const void* D, int64_t ldd, double zeta0, int mode, int cm) {
+int pre_chain0(ircur_ctx* c, const void* D, int64_t ldd, double zeta0, double gamma, int mode, int max_iter,
+               int cm) {
   c->chain0_pre = false;
+  c->chain1_pre = false;
   c->prep_gate_pending = false;
   c->prep_sms = 0;
   const char* knob = std::getenv("IRCUR_PRE_CHAIN0");  // A/B knob, read per solve
@@ -747,6 +756,25 @@ int pre_chain0(ircur_ctx* c, const void* D, int64_t ldd, double zeta0, int mode,
   IR_CUDA(cudaEventRecord(c->ovev[1], c->sA));  // ev(0, 1): SVD(0) done
   c->kernel_launches += 3;
   c->chain0_pre = true;
+  // sampled(0) -> core(1) -> Gram(1) -> SVD(1): the old factors are zero and
+  // the column strip's elements come from D itself, so these need nothing
+  // from the pass either (zeta_1 as ircur_solve computes it, solver.py:372)
+  const int set1 = mode == IRCUR_FIXED ? 0 : 1;
+  const bool chain1 = !(knob && std::atoi(knob) == 1);  // IRCUR_PRE_CHAIN0=1: chain(0) only (A/B)
+  if (chain1 && max_iter > 1 && set1 < c->n_sets) {
+    IR_CUDA(launch_sampled_factors(sampled_args(c, 0, q, set1, zeta0, true), c->r, c->sA));
+    IR_CUDA(cudaEventRecord(c->ovev[3], c->sA));  // ev(0, 3): finalize(0) clears maps it reads
+    const IterSets q1 = iter_sets(c, set1);
+    const double zeta1 = std::pow(gamma, 1.0) * zeta0;
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[5], c->sA));
+    IR_CUDA(launch_core<float>(core_args<float>(c, 1, q1, zeta1, true), c->r, c->sA));
+    const SvdArgs sa1 = svd_args<float>(c, 1, q1);
+    IR_CUDA(launch_svd<float>(sa1, svd_cluster_size(q1.nJ, q1.mI_all, sa1.kk), c->sA, c->ovev[0]));  // gate ev(0, 0)
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[6], c->sA));
+    IR_CUDA(cudaEventRecord(c->ovev[5 + 1], c->sA));  // ev(1, 1)
+    c->kernel_launches += 4;
+    c->chain1_pre = true;
+  }
   c->prep_gate_pending = true;
   c->prep_sms = std::max(1, c->num_sms - cs);
   return IRCUR_OK;
@@ -758,6 +786,7 @@ void drop_pre(ircur_ctx* c) {
   if (!c->chain0_pre && !c->prep_gate_pending) return;
   if (c->sA && cudaEventRecord(c->ov_endA, c->sA) == cudaSuccess) cudaStreamWaitEvent(c->stream, c->ov_endA, 0);
   c->chain0_pre = false;
+  c->chain1_pre = false;
   c->prep_gate_pending = false;
   c->prep_sms = 0;
 }
@@ -1308,7 +1337,7 @@ int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, 
     bool armed = true;
     ~PreGuard() { if (armed) drop_pre(c); }
   } guard{c};
-  if (int rc = pre_chain0(c, D, ldd, zeta0, mode, cm)) return rc;
+  if (int rc = pre_chain0(c, D, ldd, zeta0, gamma, mode, max_iter, cm)) return rc;
   if (int rc = ircur_prepare_async(c, D, ldd, cm, cover)) return rc;
   // the rest of the sequence is drawn and uploaded while the pass runs
   if (n_first < n_sets) {
