@@ -250,9 +250,10 @@ int ircur_debug_counter(ircur_ctx_t ctx, int which, long long* value);
  * Callers that run several solves concurrently on one GPU pass 0: the
  * overlapped loop sizes its strip grid for a GPU of its own. */
 int ircur_set_overlap(ircur_ctx_t ctx, int mode);
-/* Overlapped, profiled run: per iteration k, ms[4k..4k+3] = start and end
- * of the chain (core .. SVD) and start and end of the strips, relative to
- * the first chain's start (diagnostics of the two-stream schedule). */
+/* Overlapped, profiled run: per iteration k, ms[5k..5k+4] = start and end
+ * of the chain (core .. SVD), start and end of the strips, and the end of
+ * the sampled-factor kernel of k, relative to the first chain's start
+ * (diagnostics of the two-stream schedule; -1 where not recorded). */
 int ircur_get_timeline(ircur_ctx_t ctx, int n_iters, float* ms);
 int ircur_get_profile(ircur_ctx_t ctx, int n_iters, int* launched_iters,
                       long long* kernel_launches, float* core_ms, float* svd_ms,

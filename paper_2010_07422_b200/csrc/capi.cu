@@ -668,6 +668,7 @@ int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max
       if (int rc = cover(set_of(k + 1))) return rc;
       if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 2), 0));
       IR_CUDA(launch_sampled_factors(sampled_args(c, k, q, set_of(k + 1), zetas[k]), R, sA));
+      if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 4], sA));
       IR_CUDA(cudaEventRecord(ev(k, 3), sA));
       if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 4), 0));
       const IterSets qn = iter_sets(c, set_of(k + 1));
@@ -1614,8 +1615,8 @@ int ircur_get_timeline(ircur_ctx_t c, int n_iters, float* ms) {
   IR_CUDA(cudaSetDevice(c->device));
   IR_CUDA(cudaStreamSynchronize(c->stream));
   for (int k = 0; k < n_iters && k < c->max_iter; ++k)
-    for (int j = 0; j < 4; ++j)
-      if (cudaEventElapsedTime(&ms[k * 4 + j], c->evp[0], c->evp[(size_t)k * 5 + j]) != cudaSuccess) ms[k * 4 + j] = -1.f;
+    for (int j = 0; j < 5; ++j)
+      if (cudaEventElapsedTime(&ms[k * 5 + j], c->evp[0], c->evp[(size_t)k * 5 + j]) != cudaSuccess) ms[k * 5 + j] = -1.f;
   cudaGetLastError();
   return IRCUR_OK;
 }

@@ -100,7 +100,21 @@ constexpr int kSmpThreads = 512;
 
 __host__ __device__ inline size_t sampled_staged_smem(int nk, int R) {
   const int nk2 = nk + (nk & 1);
-  return ((size_t)nk2 * kSmpP + (size_t)nk2 * R + (size_t)kSmpP * R + (size_t)kSmpP * kSmpW * R) * sizeof(float);
+  return ((size_t)nk2 * kSmpP + 2 * (size_t)nk2 * R + (size_t)kSmpP * R + (size_t)kSmpP * kSmpW * R) *
+             sizeof(float) + (size_t)nk2 * sizeof(int);
+}
+
+// n floats global -> shared, 16-byte vectors when both sides allow it
+__device__ __forceinline__ void smp_stage(float* dst, const float* __restrict__ src, int n, int tid, int nt) {
+  if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+    const int n4 = n >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int i = tid; i < n4; i += nt) d4[i] = __ldg(s4 + i);
+    for (int i = 4 * n4 + tid; i < n; i += nt) dst[i] = __ldg(src + i);
+  } else {
+    for (int i = tid; i < n; i += nt) dst[i] = __ldg(src + i);
+  }
 }
 
 template <int R>
@@ -110,54 +124,79 @@ __global__ void __launch_bounds__(kSmpThreads) sampled_staged_kernel(const __gri
   const int p0 = blockIdx.x * kSmpP;
   if (p0 >= s.npos) return;
   const int nk = s.nk, nk2 = nk + (nk & 1);
-  extern __shared__ float smp_sm[];
-  float* sE = smp_sm;               // [nk2][kSmpP] thresholded elements
-  float* sW = sE + nk2 * kSmpP;     // [nk2][R] line weights (row nk zero)
-  float* sB = sW + nk2 * R;         // [kSmpP][R] old factor at the positions
+  extern __shared__ __align__(16) float smp_sm[];
+  float* sW = smp_sm;               // [nk2][R] line weights (row nk zero)
+  float* sA = sW + nk2 * R;         // [nk2][R] old factor at the lines
+  float* sE = sA + nk2 * R;         // [nk2][kSmpP] thresholded elements
+  float* sB = sE + nk2 * kSmpP;     // [kSmpP][R] old factor at the positions
   float* red = sB + kSmpP * R;      // [kSmpP][kSmpW][R] partial sums
+  int* sL = reinterpret_cast<int*>(red + kSmpP * kSmpW * R);  // [nk] line indices
   __shared__ int64_t xs[kSmpP];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // round 1: positions and line indices
   if (tid < kSmpP) xs[tid] = p0 + tid < s.npos ? (int64_t)s.pos[p0 + tid] - s.pos_off : -1;
-  for (int i = tid; i < nk * R; i += blockDim.x) sW[i] = s.lineW[i];
-  if (nk & 1) {
-    for (int i = tid; i < R; i += blockDim.x) sW[nk * R + i] = 0.f;
-    for (int i = tid; i < kSmpP; i += blockDim.x) sE[nk * kSmpP + i] = 0.f;
-  }
+  for (int i = tid; i < nk; i += nt) sL[i] = s.lines[i] - s.line_off;
   __syncthreads();
-  for (int i = tid; i < kSmpP * R; i += blockDim.x) {
+  // round 2: the element gathers (kept in registers) and, while they are in
+  // flight, the line vectors and the old factor at the positions
+  const int ne = nk * kSmpP;
+  constexpr int kMaxE = 2;  // register batches of kSmpB gathers before the staging loads
+  float d[kMaxE][kSmpB];
+#pragma unroll
+  for (int b = 0; b < kMaxE; ++b)
+#pragma unroll
+    for (int u = 0; u < kSmpB; ++u) {
+      const int i = tid + (b * kSmpB + u) * nt;
+      const int k = i / kSmpP, p = i - k * kSmpP;
+      d[b][u] = i < ne && xs[p] >= 0 ? s.src[(int64_t)sL[k] * s.line_stride + xs[p] * s.pos_stride] : 0.f;
+    }
+  smp_stage(sW, s.lineW, nk * R, tid, nt);
+  smp_stage(sA, s.lineA, nk * R, tid, nt);
+  if (nk & 1) {
+    for (int i = tid; i < R; i += nt) sW[nk * R + i] = 0.f;
+    for (int i = tid; i < kSmpP; i += nt) sE[nk * kSmpP + i] = 0.f;
+  }
+  for (int i = tid; i < kSmpP * R; i += nt) {
     const int p = i / R, t = i - p * R;
     sB[i] = xs[p] >= 0 ? s.B[t * s.ldb + xs[p]] : 0.f;
   }
   __syncthreads();
-  // phase 1: e(k, p) = d - T_zeta(d - <A_k, B(:, x_p)>), as strips3_kernel;
-  // each thread issues kSmpB independent element gathers before using them
-  const int ne = nk * kSmpP;
-  for (int base = tid; base < ne; base += kSmpB * blockDim.x) {
-    float d[kSmpB];
+  // phase 1: e(k, p) = d - T_zeta(d - <A_k, B(:, x_p)>), as strips3_kernel
+  auto elem = [&](int i, float dv) {
+    const int k = i / kSmpP, p = i - k * kSmpP;
+    float e = 0.f;
+    if (xs[p] >= 0) {
+      const float* A = sA + k * R;
+      const float* bb = sB + p * R;
+      float l = __fmul_rn(A[0], bb[0]);
+#pragma unroll
+      for (int t = 1; t < R; ++t) l = __fmaf_rn(A[t], bb[t], l);
+      const float xd = __fmaf_rn(l, -1.f, dv);
+      const float sv = fabsf(xd) > a.zt ? xd : 0.f;
+      e = __fmaf_rn(sv, -1.f, dv);
+    }
+    sE[i] = e;
+  };
+#pragma unroll
+  for (int b = 0; b < kMaxE; ++b)
 #pragma unroll
     for (int u = 0; u < kSmpB; ++u) {
-      const int i = base + u * blockDim.x;
+      const int i = tid + (b * kSmpB + u) * nt;
+      if (i < ne) elem(i, d[b][u]);
+    }
+  // (sets larger than kMaxE * kSmpB * nt / kSmpP lines: the rest in batches)
+  for (int base = tid + kMaxE * kSmpB * nt; base < ne; base += kSmpB * nt) {
+    float dd[kSmpB];
+#pragma unroll
+    for (int u = 0; u < kSmpB; ++u) {
+      const int i = base + u * nt;
       const int k = i / kSmpP, p = i - k * kSmpP;
-      d[u] = i < ne && xs[p] >= 0 ? s.src[(int64_t)(s.lines[k] - s.line_off) * s.line_stride + xs[p] * s.pos_stride]
-                                  : 0.f;
+      dd[u] = i < ne && xs[p] >= 0 ? s.src[(int64_t)sL[k] * s.line_stride + xs[p] * s.pos_stride] : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < kSmpB; ++u) {
-      const int i = base + u * blockDim.x;
-      if (i >= ne) break;
-      const int k = i / kSmpP, p = i - k * kSmpP;
-      float e = 0.f;
-      if (xs[p] >= 0) {
-        const float* A = s.lineA + (int64_t)k * R;
-        const float* b = sB + p * R;
-        float l = __fmul_rn(A[0], b[0]);
-#pragma unroll
-        for (int t = 1; t < R; ++t) l = __fmaf_rn(A[t], b[t], l);
-        const float xd = __fmaf_rn(l, -1.f, d[u]);
-        const float sv = fabsf(xd) > a.zt ? xd : 0.f;
-        e = __fmaf_rn(sv, -1.f, d[u]);
-      }
-      sE[i] = e;
+      const int i = base + u * nt;
+      if (i < ne) elem(i, dd[u]);
     }
   }
   __syncthreads();

@@ -22,14 +22,16 @@ cfg = ir.SolverConfig(rank=r, eps=bench.EPS, zeta0=linf, gamma=bench.GAMMA, mode
 for _ in range(2):
     res = ir.solve_device(D, cfg, profile="deferred")
 it = res.trace.iterations
-ms = np.zeros(4 * it, dtype=np.float32)
+ms = np.zeros(5 * it, dtype=np.float32)
 rc = res.ctx.lib.ircur_get_timeline(res.ctx.h, it, ms.ctypes.data_as(C.POINTER(C.c_float)))
 assert rc == 0, res.ctx.lib.ircur_last_error()
-t = ms.reshape(it, 4) * 1e3
+t = ms.reshape(it, 5) * 1e3
 print(f"{name}: {it} iterations; us relative to the first chain start")
-print("  k  chain_start chain_end  strips_start strips_end   strips_us  chain_us  overlap_us")
+print("  k  chain_start chain_end  strips_start strips_end  sampled_end   strips_us  chain_us  "
+      "strips(k-1)->sampled(k)end  sampled(k)end->core(k+1)")
 for k in range(it):
-    cs, ce, ss, se = t[k]
-    nxt = t[k + 1] if k + 1 < it else None
-    ov = (min(se, nxt[1]) - max(ss, nxt[0])) if nxt is not None else 0.0
-    print(f"{k:3d} {cs:11.1f} {ce:9.1f} {ss:13.1f} {se:10.1f} {se - ss:11.1f} {ce - cs:9.1f} {ov:11.1f}")
+    cs, ce, ss, se, sm = t[k]
+    prev_se = t[k - 1][3] if k > 0 else float("nan")
+    nxt_cs = t[k + 1][0] if k + 1 < it else float("nan")
+    print(f"{k:3d} {cs:11.1f} {ce:9.1f} {ss:13.1f} {se:10.1f} {sm:11.1f} {se - ss:11.1f} {ce - cs:9.1f} "
+          f"{sm - prev_se:26.1f} {nxt_cs - sm:24.1f}")
