@@ -923,6 +923,8 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   if (c->h_res) cudaFreeHost(c->h_res);
   if (c->ev_stage) cudaEventDestroy(c->ev_stage);
   for (PinnedBuf* b : {&c->st_rows, &c->st_cols, &c->st_colsel, &c->st_lines}) b->release();
+  for (cudaStream_t s : {c->sA, c->sB})  // the overlapped loop's streams drain before their events go
+    if (s) cudaStreamSynchronize(s);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evp)
@@ -933,16 +935,10 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->ovev)
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ov_start, c->ov_endA, c->ov_endB, c->ov_cover})
+  for (cudaEvent_t e : {c->ov_start, c->ov_endA, c->ov_endB, c->ov_cover, c->ov_gate0})
     if (e) cudaEventDestroy(e);
-  if (c->sA) {
-    cudaStreamSynchronize(c->sA);
-    cudaStreamDestroy(c->sA);
-  }
-  if (c->sB) {
-    cudaStreamSynchronize(c->sB);
-    cudaStreamDestroy(c->sB);
-  }
+  if (c->sA) cudaStreamDestroy(c->sA);
+  if (c->sB) cudaStreamDestroy(c->sB);
   delete c;
   return IRCUR_OK;
 }
@@ -1264,8 +1260,15 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   // (ircur_set_overlap, eligibility) never changes an fp32 result.
   const int lag_default = c->dtype == IRCUR_F32 ? 2 : 1;
   c->err_lag = c->last_run_overlapped ? 2 : (c->err_lag_env ? c->err_lag_env : lag_default);
-  if (c->last_run_overlapped)
-    return run_overlap(c, zetas, eps, mode, max_iter, iterations, converged, errors, iter_ms);
+  if (c->last_run_overlapped) {
+    const int rc = run_overlap(c, zetas, eps, mode, max_iter, iterations, converged, errors, iter_ms);
+    if (rc != IRCUR_OK) {  // leave no work of the side streams unordered behind the solver stream
+      cudaStreamSynchronize(c->sA);
+      cudaStreamSynchronize(c->sB);
+      c->chain0_pre = c->chain1_pre = false;
+    }
+    return rc;
+  }
   volatile int* hf = c->h_flags;
   constexpr int kAhead = 3;
   int launched = 0;
