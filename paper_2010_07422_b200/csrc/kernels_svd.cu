@@ -50,7 +50,7 @@ constexpr int kLdV = kKMax;  // leading dimension of V in the L2 scratch
 // 8 x 8 block writes its upper triangle and the mirror of it.  (The CUDA-core
 // version — one DFMA per shared load, latency-bound at 23 us for 460^2 — is
 // what this replaces.)
-constexpr int kGramNS = 4;
+constexpr int kGramNS = 8;
 constexpr int kGramLd = 33;
 constexpr int kGramSmem = kGramNS * 2 * 32 * kGramLd * (int)sizeof(double);
 
