@@ -236,7 +236,7 @@ def run_ours(args):
     core_ms = float(np.sum(p["core_ms"][:iters]))
     strip_bytes = sum(algorithmic_strip_bytes(s, n1, n2, r, res.trace.sampled_rows[k], res.trace.sampled_cols[k])
                       for k in range(iters))
-    launches = len(results) * (2 + p["kernel_launches"])  # prep + slab norm + 5 per launched iteration
+    launches = len(results) * (2 + p["kernel_launches"])  # prep + slab norm + the loop's launches (library count)
     n_strip = iters
     peak, peak_kind = peaks()
     achieved = strip_bytes / (strip_ms / 1e3) / 1e9
