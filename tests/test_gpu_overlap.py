@@ -189,3 +189,35 @@ def test_chain0_beside_prep_pass_is_bitwise_neutral(ir, monkeypatch, mode):
     cur, sp, tr = ir.solve(Dd, cfg)  # the context is still usable after the error
     assert tr.errors == t1.errors
     monkeypatch.delenv("IRCUR_PRE_CHAIN0")
+
+
+@pytest.mark.parametrize("n1,n2,r,max_iter,eps,mode", [
+    (300, 260, 16, 30, 1e-5, "resampled"),   # the largest rank the overlapped loop takes
+    (80, 700, 3, 1, 1e-5, "resampled"),      # one iteration: no next chain, no pre-launched chain(1) run
+    (500, 400, 4, 2, 1e-5, "resampled"),     # chain(1) pre-launched and consumed, then stop
+    (600, 600, 5, 40, 0.5, "resampled"),     # converges at once: speculative chains are discarded
+    (700, 90, 2, 50, 1e-6, "fixed"),         # tall and thin, fixed sets
+    (64, 900, 6, 50, 1e-6, "resampled"),     # wide and short
+])
+def test_overlapped_edge_cases_equal_sequential(ir, n1, n2, r, max_iter, eps, mode):
+    """Edge cases of the two-stream loop and of the chains queued beside the
+    prep pass, bitwise against the sequential loop (both use the fp32 SVD
+    tolerance lag 2)."""
+    import torch
+    D, L, S, linf = orc.baseline_problem(n1, n2, r, 0.1, seed=n1 + n2 + r)
+    Dd = torch.from_numpy(D.astype(np.float32)).cuda()
+    cfg = ir.SolverConfig(rank=r, zeta0=linf, gamma=0.7, eps=eps, mode=mode, max_iter=max_iter,
+                          seed=ir.RngSeed(r + max_iter))
+    seq = ir.solve(Dd, cfg, overlap=False)
+    res = ir.solve_device(Dd, cfg)
+    ov_ran = _flag(res, 1)
+    ovl = ir.solve(Dd, cfg)
+    (c1, s1, t1), (c2, s2, t2) = seq, ovl
+    assert t1.errors == t2.errors and t1.iterations == t2.iterations and t1.converged == t2.converged
+    np.testing.assert_array_equal(c1.C, c2.C)
+    np.testing.assert_array_equal(c1.R, c2.R)
+    np.testing.assert_array_equal(s1.row_values, s2.row_values)
+    np.testing.assert_array_equal(s1.col_values, s2.col_values)
+    np.testing.assert_array_equal(c1.core_pinv.sigma, c2.core_pinv.sigma)
+    if r <= 16 and ov_ran == 0:
+        pytest.skip("strips3_kernel not selected for this shape: sequential loop both times")
