@@ -16,7 +16,12 @@ from paper_2010_07422_b200 import gen
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
 n1, n2, r, al, dts, _ = bench.CONFIGS[name]
-D, linf, _ = gen.baseline_problem_device(n1, n2, r, al, bench.DATA_SEED, dtype=torch.float32)
+if name in bench.VIDEO:  # video-like configs: zeta0 = max|D|
+    f, h, w = bench.VIDEO[name]
+    Dv, _, _ = gen.video_problem(frames=f, height=h, width=w, rank=r, seed=bench.DATA_SEED)
+    D, linf = torch.from_numpy(np.ascontiguousarray(Dv, dtype=np.float32)).cuda(), None
+else:
+    D, linf, _ = gen.baseline_problem_device(n1, n2, r, al, bench.DATA_SEED, dtype=torch.float32)
 cfg = ir.SolverConfig(rank=r, eps=bench.EPS, zeta0=linf, gamma=bench.GAMMA, mode="resampled",
                       max_iter=bench.MAX_ITER, seed=ir.RngSeed(bench.SOLVER_SEED))
 for _ in range(2):

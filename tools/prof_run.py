@@ -17,7 +17,12 @@ ap.add_argument("--mode", default="resampled")
 a = ap.parse_args()
 n1, n2, r, alpha, dts, _ = bench.CONFIGS[a.config]
 tdt = torch.float32 if dts == "f32" else torch.float64
-D, linf, amp = gen.baseline_problem_device(n1, n2, r, alpha, bench.DATA_SEED, dtype=tdt)
+if a.config in bench.VIDEO:  # video-like configs: zeta0 = max|D|
+    f, h, w = bench.VIDEO[a.config]
+    Dv, _, _ = gen.video_problem(frames=f, height=h, width=w, rank=r, seed=bench.DATA_SEED)
+    D, linf = torch.from_numpy(np.ascontiguousarray(Dv, dtype=np.float32)).cuda(), None
+else:
+    D, linf, amp = gen.baseline_problem_device(n1, n2, r, alpha, bench.DATA_SEED, dtype=tdt)
 cfg = ir.SolverConfig(rank=r, eps=bench.EPS, zeta0=linf, gamma=bench.GAMMA, mode=a.mode,
                       max_iter=bench.MAX_ITER, seed=ir.RngSeed(bench.SOLVER_SEED))
 cm = a.colmajor if a.colmajor == "auto" else a.colmajor == "1"
