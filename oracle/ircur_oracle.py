@@ -114,6 +114,10 @@ class OracleResult:
     converged: bool = False
     sampled_rows: list = field(default_factory=list)
     sampled_cols: list = field(default_factory=list)
+    # record_x=True: the pre-threshold strips D - L of the final iteration
+    # (the |x| > zeta decisions of solver.py:375-377), for support-flip checks
+    X_rows: np.ndarray | None = None
+    X_cols: np.ndarray | None = None
 
 
 def _eval_rows(C, W, V, inv, R, rows):
@@ -130,7 +134,7 @@ def _eval_cols(C, W, V, inv, R, cols):
 
 def solve(D, rank, eps=1e-5, zeta0=None, gamma=0.65, c_rows=4.0, c_cols=4.0,
           mode="fixed", max_iter=200, seed=0, stream=0, upcast=True,
-          on_iter=None) -> OracleResult:
+          on_iter=None, record_x=False) -> OracleResult:
     """Algorithm 1 exactly as the reference loop runs it (solver.py:304-416),
     in float64 regardless of D's dtype (matcore.require_finite, :70-77).
 
@@ -138,7 +142,8 @@ def solve(D, rank, eps=1e-5, zeta0=None, gamma=0.65, c_rows=4.0, c_cols=4.0,
     instead (the same fp64 values; used only to time bounded CPU samples of
     matrices whose fp64 copy would not fit in host memory).  on_iter(k,
     seconds) is called after every iteration; returning True stops the loop
-    (bounded timing samples)."""
+    (bounded timing samples).  record_x keeps the final iteration's
+    pre-threshold strips D - L (X_rows, X_cols) for support-flip checks."""
     import time as _time
     if upcast:
         D = np.asarray(D, dtype=np.float64)
@@ -184,8 +189,9 @@ def solve(D, rank, eps=1e-5, zeta0=None, gamma=0.65, c_rows=4.0, c_cols=4.0,
             l_cols = _eval_cols(C, W, V, inv, R, cols)
             l_cols[rows, :] = l_rows[:, cols]
         zeta = gamma ** k * zeta0  # solver.py:372
-        s_rows = hard_threshold(d_rows - l_rows, zeta)
-        s_cols = hard_threshold(d_cols - l_cols, zeta)
+        x_rows, x_cols = d_rows - l_rows, d_cols - l_cols
+        s_rows = hard_threshold(x_rows, zeta)
+        s_cols = hard_threshold(x_cols, zeta)
         C = d_cols - s_cols  # solver.py:380-382
         R = d_rows - s_rows
         W, s, V = truncated_svd(R[:, cols], rank)
@@ -203,6 +209,8 @@ def solve(D, rank, eps=1e-5, zeta0=None, gamma=0.65, c_rows=4.0, c_cols=4.0,
         res.C, res.R, res.S_rows, res.S_cols = C, R, s_rows, s_cols
         res.W, res.sigma, res.V, res.inv_sigma = W, s, V, inv
         res.rows, res.cols = rows, cols
+        if record_x:
+            res.X_rows, res.X_cols = x_rows, x_cols
         if e <= eps:
             res.converged = True
             break

@@ -1431,8 +1431,13 @@ int ircur_iterate(ircur_ctx_t c, int k, int set, double zeta, double* e) {
   IR_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   if (k == 0) {
-    IR_CUDA(cudaMemsetAsync(c->Pt[0], 0, (size_t)c->r * c->ldp * c->esz, st));
-    IR_CUDA(cudaMemsetAsync(c->Qt[0], 0, (size_t)c->r * c->ldq * c->esz, st));
+    // a fresh loop: nothing of an earlier run (position maps left by an
+    // overlapped run's run-ahead, flags, a pre-launched chain) carries over,
+    // and the SVD tolerance lag is the one ircur_run's sequential loop uses,
+    // so an observer trajectory equals the plain one
+    if (c->chain0_pre) drop_pre(c);
+    if (int rc = reset_loop(c)) return rc;
+    c->err_lag = c->err_lag_env ? c->err_lag_env : (c->dtype == IRCUR_F32 ? 2 : 1);
   }
   IR_CUDA(cudaMemsetAsync(c->flags, 0, 3 * sizeof(int), st));
   if (int rc = ensure_cover(c, set)) return rc;

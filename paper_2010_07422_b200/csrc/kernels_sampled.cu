@@ -241,10 +241,9 @@ cudaError_t launch_sampled_factors(const SampledArgs& a, int R, cudaStream_t st)
   if (!legacy && smem <= 200 * 1024) {
     dim3 grid((unsigned)((n + kSmpP - 1) / kSmpP), 2);
     IRCUR_DISPATCH_RANK(R, RR, {
-      static std::once_flag once;
-      std::call_once(once, [] {
-        cudaFuncSetAttribute(sampled_staged_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      });
+      static std::atomic<unsigned long long> devs{0};
+      const cudaError_t attr = smem_attr_once(devs, sampled_staged_kernel<RR>, 200 * 1024);
+      if (attr != cudaSuccess) return attr;
       sampled_staged_kernel<RR><<<grid, kSmpThreads, smem, st>>>(a);
       e = cudaGetLastError();
     });

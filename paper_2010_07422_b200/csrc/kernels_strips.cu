@@ -471,12 +471,8 @@ int strips_pick_cluster(int nk_max, int R) {
 template <typename T, int R>
 static cudaError_t launch_strips_r(const StripsArgs<T>& a, int cs, int num_sms, cudaStream_t st) {
   const size_t smem = strips_smem_bytes<T>(a.maxl, R);
-  static const cudaError_t fattr = [] {  // once, thread-safe (several host threads may launch)
-    cudaError_t e = cudaFuncSetAttribute(strips_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(strips_kernel<T, R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  }();
+  static std::atomic<unsigned long long> devs{0};  // per device (several host threads may launch)
+  const cudaError_t fattr = smem_attr_once(devs, strips_kernel<T, R>, 227 * 1024, true);
   if (fattr != cudaSuccess) return fattr;
   const int tiles = a.s[0].tiles + a.s[1].tiles;
   const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (size_t)(227 * 1024) / (smem + 1024)));

@@ -306,8 +306,8 @@ cudaError_t launch_strips2(const StripsArgs<float>& a0, int R, int num_sms, int*
   if (tiles == 0) return cudaSuccess;
   cudaError_t e = cudaErrorInvalidValue;
   IRCUR_DISPATCH_RANK(R, RR, {
-    static const cudaError_t attr =  // once, thread-safe
-        cudaFuncSetAttribute(strips2_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    static std::atomic<unsigned long long> devs{0};  // once per device
+    const cudaError_t attr = smem_attr_once(devs, strips2_kernel<RR>, 227 * 1024);
     if (attr != cudaSuccess) return attr;
     strips2_kernel<RR><<<num_sms, kS2NT, smem, st>>>(a);
     e = cudaGetLastError();

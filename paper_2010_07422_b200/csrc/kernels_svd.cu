@@ -637,8 +637,17 @@ __device__ void cgs2_global(Sm& S, double* V, int n, int kk, uint64_t salt) {
 
 template <typename T, bool REG>
 __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ SvdArgs a) {
-  if (a.done && *a.done) return;
   cg::cluster_group cl = cg::this_cluster();
+  {  // one skip decision for the whole cluster: in the overlapped loop the stop
+     // flag can be set (finalize on the other stream) while the CTAs start, and a
+     // CTA that exits alone would leave the others reading its shared memory
+    __shared__ int s_done;
+    if (threadIdx.x == 0) s_done = (a.done && *(volatile const int*)a.done) ? 1 : 0;
+    cl.sync();
+    const int d0 = *cl.map_shared_rank(&s_done, 0);
+    cl.sync();  // every CTA has read rank 0's flag before any of them exits
+    if (d0) return;
+  }
   const int CS = (int)cl.num_blocks();
   const int q = (int)cl.block_rank();
   const int n = a.n, m = a.m, r = a.r, kk = a.kk;
@@ -1012,13 +1021,12 @@ int svd_pick_cluster(int n, int m, int kk) {
 template <typename T>
 cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st, cudaEvent_t after_gram) {
   const int nt = (a.n + 31) / 32;
-  static std::once_flag gram_once;
-  std::call_once(gram_once, [] {
-    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGramSmem);
-  });
+  static std::atomic<unsigned long long> gram_devs{0};  // once per device
+  cudaError_t e = smem_attr_once(gram_devs, gram_kernel, kGramSmem);
+  if (e != cudaSuccess) return e;
   gram_kernel<<<(unsigned)(nt * (nt + 1) / 2), 256, kGramSmem, st>>>(a.U, a.ldu, a.m, a.n,
                                                                      const_cast<double*>(a.G), a.ldg, a.done);
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (after_gram) {  // (overlapped loop: gates the previous iteration's strips)
     e = cudaEventRecord(after_gram, st);
@@ -1030,14 +1038,9 @@ cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st, cudaEvent_t af
   // are not shared with the small-kk paths)
   const bool reg = a.small_reg && sreg_supported(a.kk);
   auto kern = reg ? svd_kernel<T, true> : svd_kernel<T, false>;
-  auto set_attrs = [](auto k) {
-    cudaError_t r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (r != cudaSuccess) return r;
-    return cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  };
-  static const cudaError_t attr_reg = set_attrs(svd_kernel<T, true>);  // once, thread-safe
-  static const cudaError_t attr_std = set_attrs(svd_kernel<T, false>);
-  e = reg ? attr_reg : attr_std;
+  static std::atomic<unsigned long long> devs_reg{0}, devs_std{0};  // once per device
+  e = reg ? smem_attr_once(devs_reg, svd_kernel<T, true>, 227 * 1024, true)
+          : smem_attr_once(devs_std, svd_kernel<T, false>, 227 * 1024, true);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cs, 1, 1);

@@ -3,9 +3,37 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "kernels_iter.cuh"
 
 namespace ircur {
+
+// Function attributes (dynamic shared memory above 48 KB, non-portable
+// cluster sizes) are stored per device context, so they are set once per
+// (kernel, device): `mask` is the kernel's static bitmask of devices done.
+// Two threads racing here both set the attribute, which is idempotent.
+template <typename SetFn>
+inline cudaError_t attr_once(std::atomic<unsigned long long>& mask, SetFn&& set) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = set();
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+template <typename K>
+inline cudaError_t smem_attr_once(std::atomic<unsigned long long>& mask, K* kern, int bytes,
+                                  bool nonportable_cluster = false) {
+  return attr_once(mask, [&] {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess || !nonportable_cluster) return e;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  });
+}
 
 struct u128 {
   uint64_t lo, hi;

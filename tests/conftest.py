@@ -44,3 +44,21 @@ def solver_kwargs(meta):
 @pytest.fixture(scope="session")
 def golden():
     return load_golden
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write the parity records (flip counts, worst errors) of this session
+    to gpurun_out/parity_stats.json (tests/parity.py)."""
+    try:
+        import parity
+    except Exception:
+        return
+    if not parity.STATS:
+        return
+    out = os.path.join(ROOT, "gpurun_out")
+    try:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, "parity_stats.json"), "w") as f:
+            json.dump(parity.STATS, f, indent=1, default=float)
+    except OSError:
+        pass

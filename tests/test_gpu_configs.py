@@ -16,6 +16,7 @@ import pytest
 import torch
 
 from oracle import ircur_oracle as orc
+import parity
 
 pytestmark = pytest.mark.gpu
 
@@ -37,44 +38,32 @@ def ir():
 
 def _solve_both(ir, D, rank, zeta0, seed, gamma=0.7, eps=1e-5, max_iter=100, mode="resampled"):
     ref = orc.solve(np.asarray(D, dtype=np.float64) if D.dtype == np.float32 else D, rank=rank, eps=eps,
-                    zeta0=zeta0, gamma=gamma, mode=mode, max_iter=max_iter, seed=seed)
-    cfg = ir.SolverConfig(rank=rank, eps=eps, zeta0=zeta0, gamma=gamma, mode=mode, max_iter=max_iter,
-                          seed=ir.RngSeed(seed))
-    return ref, ir.solve(D, cfg, device=0)
+                    zeta0=zeta0, gamma=gamma, mode=mode, max_iter=max_iter, seed=seed, record_x=True)
+    kw = dict(rank=rank, eps=eps, zeta0=zeta0, gamma=gamma, mode=mode, max_iter=max_iter)
+
+    def resolve(mi, e):
+        return ir.solve(D, ir.SolverConfig(**{**kw, "max_iter": mi, "eps": e}, seed=ir.RngSeed(seed)), device=0)
+
+    return ref, resolve(max_iter, eps), resolve
 
 
-def _check(ref, out, f32):
-    cur, sp, tr = out
-    if f32:
-        assert abs(tr.iterations - ref.iterations) <= 1 and tr.converged == ref.converged
-        n = min(tr.iterations, ref.iterations)
-        np.testing.assert_allclose(tr.errors[:n], ref.errors[:n], rtol=1e-3)
-        if tr.iterations == ref.iterations:
-            for a, b in ((cur.C, ref.C), (cur.R, ref.R), (sp.row_values, ref.S_rows), (sp.col_values, ref.S_cols)):
-                assert rel(a, b) <= TOL32
-    else:
-        assert tr.iterations == ref.iterations and tr.converged == ref.converged
-        np.testing.assert_allclose(tr.errors, ref.errors, rtol=TOL64, atol=1e-15)
-        for a, b in ((cur.C, ref.C), (cur.R, ref.R), (sp.row_values, ref.S_rows), (sp.col_values, ref.S_cols)):
-            assert rel(a, b) <= TOL64
-        np.testing.assert_allclose(cur.core_pinv.sigma, ref.sigma, rtol=TOL64)
-    np.testing.assert_array_equal(cur.rows.indices, ref.rows)
-    np.testing.assert_array_equal(cur.cols.indices, ref.cols)
+def _check(ref, out, f32, resolve=None, name=""):
+    parity.check(out, ref, f32, resolve=resolve, name=name)
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_cfg2_matches_oracle(ir, dtype):
     D, linf, _ = orc.baseline_problem_blocked(10000, 10000, 5, 0.2, 0, dtype=dtype)
-    ref, out = _solve_both(ir, D, 5, linf, 1)
-    _check(ref, out, dtype == np.float32)
+    ref, out, resolve = _solve_both(ir, D, 5, linf, 1)
+    _check(ref, out, dtype == np.float32, resolve, f"cfg2_{np.dtype(dtype).name}")
     ir.clear_cache()
 
 
 def test_cfg3_video_matches_oracle(ir):
     from paper_2010_07422_b200.gen import video_problem
     D, L, S = video_problem(seed=0)
-    ref, out = _solve_both(ir, D, 2, None, 1)
-    _check(ref, out, True)
+    ref, out, resolve = _solve_both(ir, D, 2, None, 1)
+    _check(ref, out, True, resolve, "cfg3_video")
     # the foreground is recovered: S on the sampled rows has the blocks' support
     cur, sp, tr = out
     assert tr.converged
@@ -85,8 +74,8 @@ def test_cfg3_video_matches_oracle(ir):
 def test_cfg4_problems_match_oracle(ir, p):
     D, _, _, linf = orc.baseline_problem(2000, 2000, 5, 0.2, 1000 + p)
     D = D.astype(np.float32)
-    ref, out = _solve_both(ir, D, 5, linf, 1000 + p)
-    _check(ref, out, True)
+    ref, out, resolve = _solve_both(ir, D, 5, linf, 1000 + p)
+    _check(ref, out, True, resolve, f"cfg4_p{p}")
 
 
 def test_cfg4_batch_equals_one_by_one(ir):

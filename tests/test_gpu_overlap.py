@@ -221,3 +221,38 @@ def test_overlapped_edge_cases_equal_sequential(ir, n1, n2, r, max_iter, eps, mo
     np.testing.assert_array_equal(c1.core_pinv.sigma, c2.core_pinv.sigma)
     if r <= 16 and ov_ran == 0:
         pytest.skip("strips3_kernel not selected for this shape: sequential loop both times")
+
+
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+def test_observer_after_overlapped_run_equals_fresh_context(ir, mode):
+    """An observer solve (ircur_iterate, one iteration per call) on a cached
+    context that just ran an overlapped fp32 solve must not inherit its
+    state: the overlapped run's run-ahead leaves position maps of the next
+    parity set and a different SVD tolerance lag.  The observer
+    trajectory must equal the same observer solve on a fresh context, and
+    the plain (non-observer) solve."""
+    from oracle.ircur_oracle import baseline_problem
+    D = baseline_problem(900, 800, 5, 0.2, 21)[0].astype(np.float32)
+    kw = dict(rank=5, gamma=0.7, eps=1e-6, mode=mode, max_iter=60)
+    seen = []
+
+    def obs(k, zeta, cur, sparse, e):
+        seen.append((k, e, cur.C.copy(), cur.R.copy()))
+
+    ir.clear_cache()
+    fresh_plain = ir.solve(D, ir.SolverConfig(seed=ir.RngSeed(11), **kw), device=0)
+    ir.clear_cache()
+    fresh = ir.solve(D, ir.SolverConfig(seed=ir.RngSeed(11), **kw), observer=obs, device=0)
+    fresh_seen, seen[:] = list(seen), []
+    ir.clear_cache()
+    ir.solve(D, ir.SolverConfig(seed=ir.RngSeed(3), **kw), device=0)  # overlapped run first
+    again = ir.solve(D, ir.SolverConfig(seed=ir.RngSeed(11), **kw), observer=obs, device=0)
+    assert again[2].errors == fresh[2].errors == fresh_plain[2].errors
+    assert len(seen) == len(fresh_seen)
+    for (k1, e1, C1, R1), (k2, e2, C2, R2) in zip(seen, fresh_seen):
+        assert k1 == k2 and e1 == e2
+        np.testing.assert_array_equal(C1, C2)
+        np.testing.assert_array_equal(R1, R2)
+    np.testing.assert_array_equal(again[0].C, fresh_plain[0].C)
+    np.testing.assert_array_equal(again[1].row_values, fresh_plain[1].row_values)
+    ir.clear_cache()

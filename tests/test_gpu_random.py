@@ -18,6 +18,7 @@ import numpy as np
 import pytest
 
 from oracle import ircur_oracle as orc
+import parity
 
 pytestmark = pytest.mark.gpu
 
@@ -58,19 +59,14 @@ def test_random_problem_matches_oracle(ir, i):
     zeta0 = linf if use_zeta else None
     kw = dict(rank=r, eps=eps, zeta0=zeta0, gamma=gamma, mode=mode, max_iter=150)
     Dm = D.astype(np.float32) if f32 else D
-    ref = orc.solve(np.asarray(Dm, dtype=np.float64), seed=9 + i, **kw)
-    cur, sp, tr = ir.solve(Dm, ir.SolverConfig(seed=ir.RngSeed(9 + i), **kw), device=0)
-    np.testing.assert_array_equal(cur.rows.indices, ref.rows)
-    np.testing.assert_array_equal(cur.cols.indices, ref.cols)
-    if f32:
-        assert abs(tr.iterations - ref.iterations) <= 1 and tr.converged == ref.converged
-        if tr.iterations == ref.iterations:
-            for a, b in ((cur.C, ref.C), (cur.R, ref.R), (sp.row_values, ref.S_rows), (sp.col_values, ref.S_cols)):
-                assert rel(a, b) <= TOL32
-        return
-    assert tr.iterations == ref.iterations and tr.converged == ref.converged
-    assert tr.thresholds == ref.thresholds
-    np.testing.assert_allclose(tr.errors, ref.errors, rtol=TOL64, atol=1e-15)
-    for a, b in ((cur.C, ref.C), (cur.R, ref.R), (sp.row_values, ref.S_rows), (sp.col_values, ref.S_cols)):
-        assert rel(a, b) <= TOL64
-    np.testing.assert_allclose(cur.core_pinv.sigma, ref.sigma, rtol=TOL64, atol=1e-12 * max(ref.sigma.max(), 1e-300))
+    ref = orc.solve(np.asarray(Dm, dtype=np.float64), seed=9 + i, record_x=True, **kw)
+
+    def resolve(mi, e):
+        return ir.solve(Dm, ir.SolverConfig(seed=ir.RngSeed(9 + i), **{**kw, "max_iter": mi, "eps": e}), device=0)
+
+    out = resolve(kw["max_iter"], eps)
+    parity.check(out, ref, f32, resolve=resolve, name=f"random_{i}")
+    cur = out[0]
+    if not f32:
+        np.testing.assert_allclose(cur.core_pinv.sigma, ref.sigma, rtol=TOL64,
+                                   atol=1e-12 * max(ref.sigma.max(), 1e-300))
