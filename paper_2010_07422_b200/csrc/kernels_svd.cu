@@ -638,13 +638,16 @@ __device__ void cgs2_global(Sm& S, double* V, int n, int kk, uint64_t salt) {
 template <typename T, bool REG>
 __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ SvdArgs a) {
   cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double svsm[];
   {  // one skip decision for the whole cluster: in the overlapped loop the stop
      // flag can be set (finalize on the other stream) while the CTAs start, and a
-     // CTA that exits alone would leave the others reading its shared memory
-    __shared__ int s_done;
-    if (threadIdx.x == 0) s_done = (a.done && *(volatile const int*)a.done) ? 1 : 0;
+     // CTA that exits alone would leave the others reading its shared memory.
+     // (The flag borrows the first word of the dynamic shared memory, which the
+     // kernel only uses after the second cluster barrier.)
+    int* s_done = reinterpret_cast<int*>(svsm);
+    if (threadIdx.x == 0) *s_done = (a.done && *(volatile const int*)a.done) ? 1 : 0;
     cl.sync();
-    const int d0 = *cl.map_shared_rank(&s_done, 0);
+    const int d0 = *cl.map_shared_rank(s_done, 0);
     cl.sync();  // every CTA has read rank 0's flag before any of them exits
     if (d0) return;
   }
@@ -652,7 +655,6 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   const int q = (int)cl.block_rank();
   const int n = a.n, m = a.m, r = a.r, kk = a.kk;
   const int reff = min(r, min(m, n));
-  extern __shared__ __align__(16) double svsm[];
   Sm S;
   S.L = svd_layout(n, m, kk, CS);
   const SvdLayout& L = S.L;
