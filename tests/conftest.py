@@ -56,9 +56,14 @@ def pytest_sessionfinish(session, exitstatus):
     if not parity.STATS:
         return
     out = os.path.join(ROOT, "gpurun_out")
+    path = os.path.join(out, "parity_stats.json")
     try:
         os.makedirs(out, exist_ok=True)
-        with open(os.path.join(out, "parity_stats.json"), "w") as f:
-            json.dump(parity.STATS, f, indent=1, default=float)
+        old = []
+        if os.path.exists(path):  # several pytest sessions in one call: append
+            with open(path) as f:
+                old = json.load(f)
+        with open(path, "w") as f:
+            json.dump(old + parity.STATS, f, indent=1, default=float)
     except OSError:
         pass
