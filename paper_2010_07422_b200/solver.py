@@ -334,10 +334,19 @@ def _evict_idle(keep: int) -> None:
 
 def _context_locked(key, device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, stream, row0,
                     local_rows) -> Context:
-    ctx = _CACHE.get(key)
-    if ctx is not None:
-        _CACHE.move_to_end(key)
-        return ctx
+    # A context serves one solve at a time: threads solving problems of the
+    # same shape on the same stream (e.g. the reference's threaded trial
+    # pool, cli.py:117-125, all on the default stream) each get their own.
+    slot = 0
+    while True:
+        ctx = _CACHE.get(key + (slot,))
+        if ctx is None:
+            break
+        if ctx._busy == 0:
+            _CACHE.move_to_end(key + (slot,))
+            return ctx
+        slot += 1
+    key = key + (slot,)
     _evict_idle(_CACHE_MAX - 1)
     try:
         ctx = Context(device, dtype, n1, n2, rank, m_rows, m_cols, max_iter, row0, local_rows, stream=stream)

@@ -158,3 +158,34 @@ def test_concurrent_streams_beyond_cache_limit(ir):
     for t in th:
         t.join()
     assert out == seq
+
+
+def test_concurrent_threads_same_stream_same_shape(ir):
+    """The reference's threaded trial pool (cli.py:117-125, _run_trial
+    cli.py:76-97) solves same-shaped problems from several threads on the
+    default stream: each solve must get its own context (a shared one
+    mixed index sets and core factors across threads)."""
+    import threading
+    probs, cfgs = [], []
+    for p in range(12):
+        D, _, _, linf = orc.baseline_problem(50, 50, 2, 0.2, 3000 + p)
+        probs.append(D)
+        cfgs.append(ir.SolverConfig(rank=2, zeta0=linf, gamma=0.7, mode="fixed", max_iter=30,
+                                    c_rows=1.0 + (p % 2), c_cols=1.0 + (p % 2), seed=ir.RngSeed(3000 + p)))
+    seq = [ir.solve(D, c, device=0) for D, c in zip(probs, cfgs)]
+    out = [None] * len(probs)
+
+    def worker(w):
+        for i in range(w, len(probs), 4):
+            out[i] = ir.solve(probs[i], cfgs[i], device=0)
+
+    th = [threading.Thread(target=worker, args=(w,)) for w in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for (c1, s1, t1), (c2, s2, t2) in zip(seq, out):
+        assert t1.errors == t2.errors
+        np.testing.assert_array_equal(c1.rows.indices, c2.rows.indices)
+        np.testing.assert_array_equal(c1.C, c2.C)
+        np.testing.assert_array_equal(c1.core_pinv.W, c2.core_pinv.W)
