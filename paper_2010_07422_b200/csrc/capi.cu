@@ -92,6 +92,7 @@ struct ircur_ctx {
   void* Qt[2] = {nullptr, nullptr};
   int64_t ldp = 0, ldq = 0;
   double* U = nullptr;
+  double* U2 = nullptr;              // second core buffer (single-GPU loops: parity of k)
   // per-iteration buffers, two copies by iteration parity (k & 1): iteration
   // k + 1's core, gathers and SVD can then be produced while iteration k's
   // strips still read theirs
@@ -129,6 +130,10 @@ struct ircur_ctx {
   bool prep_pending = false;
   // sampled-factor kernel (kernels_sampled.cu): verification in the sequential loop
   int sampled_check = 0;        // IRCUR_SAMPLED_CHECK: run it after the strips, compare in the next core
+  // sequential fp32 loop with the tensor-core strips: iteration k ran the
+  // sampled-factor kernel for k + 1, so core(k + 1) reads P_k(I_{k+1}, :) and
+  // Q_k(:, J_{k+1}) from it, exactly as the overlapped loop does
+  bool seq_presampled = false;
   int run_fixed = 0;            // mode of the current loop (the next iteration's index set)
   unsigned* dbg_counter = nullptr;  // [0] sampled-factor mismatches
   int err_lag = 1;                  // SVD tolerance from e_{k - err_lag} (set per run)
@@ -221,6 +226,11 @@ IterSets iter_sets(const ircur_ctx* c, int set) {
   return q;
 }
 
+// The core of iteration k.  Single-GPU loops alternate two buffers by
+// parity: in the overlapped loop core(k + 1) runs while strips(k) still read
+// U_k's I x J entries.  The row-sharded path all-reduces the one buffer.
+double* core_U(const ircur_ctx* c, int k) { return (c->nloc != c->n1 || !c->U2) ? c->U : ((k & 1) ? c->U2 : c->U); }
+
 template <typename T>
 CoreArgs<T> core_args(const ircur_ctx* c, int k, const IterSets& q, double zeta, bool presampled = false) {
   const int old = k & 1;
@@ -229,7 +239,7 @@ CoreArgs<T> core_args(const ircur_ctx* c, int k, const IterSets& q, double zeta,
   ca.I = q.I; ca.mI = q.mI; ca.J = q.J; ca.nJ = q.nJ;
   ca.Pt = (const T*)c->Pt[old]; ca.ldp = c->ldp;
   ca.Qt = (const T*)c->Qt[old]; ca.ldq = c->ldq;
-  ca.zt = storage_zeta<T>(zeta); ca.U = c->U; ca.ldu = c->max_cols; ca.upos0 = q.i_lo;
+  ca.zt = storage_zeta<T>(zeta); ca.U = core_U(c, k); ca.ldu = c->max_cols; ca.upos0 = q.i_lo;
   const int p = k & 1;
   ca.PoldI = (T*)c->PoldI[p]; ca.QoldJ = (T*)c->QoldJ[p]; ca.done = c->flags;
   ca.rowmap = c->rowmap[p]; ca.colmap = c->colmap[p];
@@ -243,7 +253,7 @@ template <typename T>
 SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   const int R = c->r;
   SvdArgs sa{};
-  sa.U = c->U; sa.ldu = c->max_cols; sa.G = c->G; sa.ldg = c->max_cols;
+  sa.U = core_U(c, k); sa.ldu = c->max_cols; sa.G = c->G; sa.ldg = c->max_cols;
   sa.m = q.mI_all; sa.n = q.nJ; sa.r = R;  // the full core (all-reduced when row-sharded)
   // block = r + 2 columns: the top-r Ritz pairs converge at rate
   // lambda_{r+3}/lambda_r per step; the small dense Rayleigh-Ritz (latency
@@ -314,6 +324,7 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
   rs.lineRes = (const T*)c->PI[p] + (size_t)q.i_lo * R;
   rs.Bold = (const T*)c->Qt[old]; rs.ldb = c->ldq; rs.Fnew = (T*)c->Qt[nw]; rs.ldf = c->ldq;
   rs.omap = c->colmap[p]; rs.otherF = (const T*)c->QJ[p];
+  rs.U = core_U(c, k) + (size_t)q.i_lo * c->max_cols; rs.u_ls = c->max_cols; rs.u_ps = 1;
   rs.tiles = (int)((c->n2 + TX - 1) / TX);
   rs.mode = kStripFull;
   StripDesc<T>& cs = pa.s[1];
@@ -327,6 +338,7 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
   cs.lineA = (const T*)c->QoldJ[p]; cs.lineW = (const T*)c->VS[p]; cs.lineRes = (const T*)c->QJ[p];
   cs.Bold = (const T*)c->Pt[old]; cs.ldb = c->ldp; cs.Fnew = (T*)c->Pt[nw]; cs.ldf = c->ldp;
   cs.omap = c->rowmap[p]; cs.otherF = (const T*)c->PI[p];
+  cs.U = core_U(c, k); cs.u_ls = 1; cs.u_ps = c->max_cols;
   cs.tiles = (int)((c->nloc + TX - 1) / TX);
   cs.mode = kStripFull;
   pa.zt = storage_zeta<T>(zeta); pa.partials = c->partials; pa.done = c->flags;
@@ -483,7 +495,8 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   const int R = c->r;
   cudaEvent_t* pe = c->profiling ? &c->evp[(size_t)k * 5] : nullptr;
   if (pe) IR_CUDA(cudaEventRecord(pe[0], st));
-  IR_CUDA(launch_core<T>(core_args<T>(c, k, q, zeta), R, st));
+  const bool presampled = sizeof(T) == 4 && k > 0 && c->seq_presampled;
+  IR_CUDA(launch_core<T>(core_args<T>(c, k, q, zeta, presampled), R, st));
   if (pe) IR_CUDA(cudaEventRecord(pe[1], st));
   const SvdArgs sa = svd_args<T>(c, k, q);
   IR_CUDA(launch_svd<T>(sa, svd_cluster_size(q.nJ, q.mI_all, sa.kk), st));
@@ -492,10 +505,16 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
   IR_CUDA(launch_strips<T>(strips_args<T>(c, k, q, zeta), R, c->strips_cs, c->num_sms, &ncta, st));
   if (pe) IR_CUDA(cudaEventRecord(pe[3], st));
   if constexpr (sizeof(T) == 4) {
-    // verification: the next iteration's gathers must equal the sampled entries
+    // the next iteration's sampled factors: verification (IRCUR_SAMPLED_CHECK,
+    // strips3: the next core's gathers must equal them), or the values the
+    // next core reads (tensor-core strips, as in the overlapped loop)
     const int set_next = c->run_fixed ? 0 : set + 1;
-    if (c->sampled_check && set_next < c->n_sets)
+    const bool s5 = c->nloc == c->n1 && strips5_selected(strips_args<T>(c, k, q, zeta), R);
+    c->seq_presampled = s5 && set_next < c->n_sets;
+    if ((c->sampled_check || s5) && set_next < c->n_sets)
       IR_CUDA(launch_sampled_factors(sampled_args(c, k, q, set_next, zeta), R, st));
+  } else {
+    c->seq_presampled = false;
   }
   FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, host_flags);
   fa.ncta_rows = ncta;
@@ -605,7 +624,8 @@ bool overlap_eligible(ircur_ctx* c, int mode, int max_iter) {
   const int nsets = mode == IRCUR_FIXED ? 1 : std::min(max_iter, c->n_sets);
   for (int s = 0; s < nsets; ++s) {
     const IterSets q = iter_sets(c, s);
-    if (!strips3_selected(strips_args<float>(c, s, q, 1.0), c->r)) return false;
+    const StripsArgs<float> a = strips_args<float>(c, s, q, 1.0);
+    if (!strips3_selected(a, c->r) && !strips5_selected(a, c->r)) return false;
   }
   return true;
 }
@@ -738,7 +758,7 @@ int pre_chain0(ircur_ctx* c, const void* D, int64_t ldd, double zeta0, double ga
     a.s[0].nk = c->max_rows;
     a.s[1].nk = c->max_cols;
     a.s[1].bulk_ok = 1;  // the column copy's ldt is padded to 16 bytes
-    if (!strips3_selected(a, c->r)) return IRCUR_OK;
+    if (!strips3_selected(a, c->r) && !strips5_selected(a, c->r)) return IRCUR_OK;
   }
   if (int rc = overlap_setup(c)) return rc;
   cudaStream_t us = c->stream;
@@ -851,6 +871,7 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
     IR_CUDA_C(cudaMalloc(&c->Qt[b], (size_t)rank * c->ldq * c->esz));
   }
   IR_CUDA_C(cudaMalloc(&c->U, (size_t)max_rows * max_cols * sizeof(double)));
+  if (c->nloc == c->n1) IR_CUDA_C(cudaMalloc(&c->U2, (size_t)max_rows * max_cols * sizeof(double)));
   for (int b = 0; b < 2; ++b) {
     IR_CUDA_C(cudaMalloc(&c->PoldI[b], (size_t)max_rows * rank * c->esz));
     IR_CUDA_C(cudaMalloc(&c->QoldJ[b], (size_t)max_cols * rank * c->esz));
@@ -868,7 +889,9 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
   IR_CUDA_C(cudaMalloc(&c->Qpart, (size_t)rank * c->ldq * c->esz));
   IR_CUDA_C(cudaMalloc(&c->scal, 8 * sizeof(double)));
   IR_CUDA_C(cudaMemsetAsync(c->scal, 0, 8 * sizeof(double), c->stream));
-  c->max_partials = 4 * 2 * c->num_sms + 8192;  // strips: 4 sums per persistent CTA (<= 2/SM)
+  // strips: 4 sums per persistent CTA (<= 2/SM), or per (128-position tile, rank) for strips5
+  c->max_partials = (int)std::max<int64_t>(4 * 2 * c->num_sms + 8192,
+                                           16 * ((c->n2 + 127) / 128 + (c->nloc + 127) / 128) + 64);
   IR_CUDA_C(cudaMalloc(&c->partials, (size_t)c->max_partials * sizeof(double)));
   for (int b = 0; b < 2; ++b) {
     IR_CUDA_C(cudaMalloc(&c->rowmap[b], (size_t)local_rows * sizeof(int)));
@@ -910,7 +933,7 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   if (!c) return IRCUR_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U,
+  void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U, c->U2,
                   c->PoldI[0], c->QoldJ[0], c->Wr[0], c->PI[0], c->VS[0], c->QJ[0], c->W[0], c->sigma[0],
                   c->V[0], c->inv[0], c->PoldI[1], c->QoldJ[1], c->Wr[1], c->PI[1], c->VS[1], c->QJ[1],
                   c->W[1], c->sigma[1], c->V[1], c->inv[1],
@@ -1198,6 +1221,7 @@ int reset_loop(ircur_ctx* c) {
   IR_CUDA(cudaEventRecord(c->ev[0], st));
   c->launched_iters = 0;
   c->kernel_launches = 0;
+  c->seq_presampled = false;
   return IRCUR_OK;
 }
 

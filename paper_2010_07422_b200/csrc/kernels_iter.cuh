@@ -55,6 +55,9 @@ struct StripDesc {
   // accumulates the residual.
   int mode;
   const T* Fsrc; int64_t ldfs;                 // kStripFinish only: R x npos
+  // the core U = (D - S)(I, J): entry (line k, position with omap e) at
+  // U[k * u_ls + e * u_ps] (strips5: the I x J entries of the strips)
+  const double* U; int64_t u_ls, u_ps;
 };
 constexpr int kStripFull = 0, kStripPartial = 1, kStripFinish = 2;
 

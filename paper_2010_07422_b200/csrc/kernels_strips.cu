@@ -496,15 +496,20 @@ static int strips_version() {
   static const int ver = [] {
     const char* e = std::getenv("IRCUR_STRIPS_VER");
     if (!e) e = std::getenv("IRCUR_STRIPS_V1") ? "1" : nullptr;
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 5;
   }();
   return ver;
+}
+
+bool strips5_selected(const StripsArgs<float>& a, int R) {
+  return strips_version() >= 5 && strips5_supported(a, R);
 }
 
 bool strips3_selected(const StripsArgs<float>& a, int R) {
   const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
   const int maxl = a.s[0].nk > a.s[1].nk ? a.s[0].nk : a.s[1].nk;
-  return strips_version() >= 3 && aligned && strips3_smem_bytes(maxl, R) <= (size_t)227 * 1024;
+  return strips_version() >= 3 && !strips5_selected(a, R) && aligned &&
+         strips3_smem_bytes(maxl, R) <= (size_t)227 * 1024;
 }
 
 template <typename T>
@@ -514,11 +519,15 @@ cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, in
   if (ncta_out) *ncta_out = 0;
   if (tiles == 0) return cudaSuccess;
   if constexpr (sizeof(T) == 4) {
-    // fp32: the 64-position single-stage kernel, else the two-group
-    // 32-position kernel, else this cluster kernel.  IRCUR_STRIPS_VER=1|2|3
-    // caps the choice (A/B measurements).
+    // fp32: the tensor-core kernel, else the 64-position single-stage
+    // kernel, else the two-group 32-position kernel, else this cluster
+    // kernel.  IRCUR_STRIPS_VER=1|2|3|5 caps the choice (A/B measurements).
     const int ver = strips_version();
     const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
+    if (ver >= 5) {
+      const cudaError_t e = launch_strips5(a, R, num_sms, ncta_out, st);
+      if (e != cudaErrorNotSupported) return e;
+    }
     if (ver >= 3 && aligned) {
       const cudaError_t e = launch_strips3(a, R, num_sms, ncta_out, st);
       if (e != cudaErrorNotSupported) return e;

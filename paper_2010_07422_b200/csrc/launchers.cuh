@@ -85,6 +85,13 @@ size_t strips3_smem_bytes(int maxl, int R);
 // the fp32 strip launch of `a` runs strips3_kernel (what the sampled-factor
 // kernel reproduces bitwise)
 bool strips3_selected(const StripsArgs<float>& a, int R);
+// fp32 tensor-core kernel (kernels_strips5.cu): 4-CTA clusters, 128-position
+// tiles; NotSupported outside its envelope (r <= 10, <= 512 lines, aligned
+// line segments, kStripFull)
+cudaError_t launch_strips5(const StripsArgs<float>& a, int R, int num_sms, int* ncta_out, cudaStream_t st);
+bool strips5_supported(const StripsArgs<float>& a, int R);
+// the fp32 strip launch of `a` runs strips5_kernel
+bool strips5_selected(const StripsArgs<float>& a, int R);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
 template <typename T, typename O>

@@ -28,13 +28,23 @@ __device__ __forceinline__ uint32_t mnmaj_off(int mn, int k, int lbo, int sbo) {
   return (mn / 32) * lbo + (k / 8) * sbo + (k % 8) * 128 + ((((mn % 32) / 4) ^ (k % 8)) * 16) + (mn % 4) * 4;
 }
 
+__device__ __forceinline__ uint32_t kmaj_sw128_off(int row, int k, int sbo) {
+  return (row / 8) * sbo + (row % 8) * 128 + (((k / 4) ^ (row % 8)) * 16) + (k % 4) * 4;
+}
+__device__ __forceinline__ uint32_t mnmaj_il_off(int mn, int k, int lbo, int sbo) {
+  return (mn / 4) * sbo + (k / 8) * lbo + (k % 8) * 16 + (mn % 4) * 4;
+}
+
 __global__ void __launch_bounds__(128, 1) probe_kernel(Probe p) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint32_t tbase;
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, w = tid >> 5;
-  unsigned char* sa = sm;           // 32 KB
-  unsigned char* sb = sm + 32768;   // 32 KB
+  // swizzled layouts are defined on absolute shared addresses: align the
+  // operand base to 1 KB (static shared variables precede the dynamic ones)
+  unsigned char* base = sm + ((1024 - (smem_u32(sm) & 1023)) & 1023);
+  unsigned char* sa = base;           // 32 KB
+  unsigned char* sb = base + 32768;   // 32 KB
   if (w == 0) tmem_alloc(&tbase, 256);
   if (tid == 0) { bar_init(&bar, 1); bar_init_fence(); }
   fence_before();
@@ -79,6 +89,64 @@ __global__ void __launch_bounds__(128, 1) probe_kernel(Probe p) {
       *reinterpret_cast<float*>(sb + kmaj_off(n, k, 128, 512)) = p.B[n * K + k];
     }
     idesc = idesc_tf32(M, N, 1, 0);
+  } else if (p.test == 5) {  // A in TMEM, B K-major interleave, K = 32
+    M = 128; N = 64; K = 32;
+    float v[16];
+    for (int h = 0; h < 2; ++h) {
+      for (int i = 0; i < 16; ++i) v[i] = p.A[tid * K + 16 * h + i];
+      st16(T + lane_off + 128 + 16 * h, v);
+    }
+    st_wait();
+    for (int e = tid; e < N * K; e += 128) {
+      const int n = e / K, k = e % K;
+      *reinterpret_cast<float*>(sb + kmaj_off(n, k, 128, 1024)) = p.B[n * K + k];
+    }
+    idesc = idesc_tf32(M, N, 0, 0);
+  } else if (p.test == 6) {  // A K-major interleave, B MN-major SW128, K = 32
+    M = 128; N = 64; K = 32;
+    for (int e = tid; e < M * K; e += 128) {
+      const int m = e / K, k = e % K;
+      *reinterpret_cast<float*>(sa + kmaj_off(m, k, 128, 1024)) = p.A[m * K + k];
+    }
+    for (int e = tid; e < N * K; e += 128) {
+      const int n = e / K, k = e % K;
+      *reinterpret_cast<float*>(sb + mnmaj_off(n, k, 1024, 2048)) = p.B[n * K + k];
+    }
+    idesc = idesc_tf32(M, N, 0, 1);
+  } else if (p.test == 7) {  // A K-major SW128 (K = 32 = one 128 B row), B K-major interleave
+    M = 128; N = 64; K = 32;
+    for (int e = tid; e < M * K; e += 128) {
+      const int m = e / K, k = e % K;
+      *reinterpret_cast<float*>(sa + kmaj_sw128_off(m, k, 1024)) = p.A[m * K + k];
+    }
+    for (int e = tid; e < N * K; e += 128) {
+      const int n = e / K, k = e % K;
+      *reinterpret_cast<float*>(sb + kmaj_off(n, k, 128, 1024)) = p.B[n * K + k];
+    }
+    idesc = idesc_tf32(M, N, 0, 0);
+  } else if (p.test == 8 || p.test == 10) {  // A K-major interleave, B MN-major interleave
+    M = 128; N = 64; K = 32;
+    for (int e = tid; e < M * K; e += 128) {
+      const int m = e / K, k = e % K;
+      *reinterpret_cast<float*>(sa + kmaj_off(m, k, 128, 1024)) = p.A[m * K + k];
+    }
+    for (int e = tid; e < N * K; e += 128) {
+      const int n = e / K, k = e % K;
+      // core matrices: 4 MN x 8 K (128 B); MN cores 128 B apart, K groups 2048 B apart
+      *reinterpret_cast<float*>(sb + mnmaj_il_off(n, k, 2048, 128)) = p.B[n * K + k];
+    }
+    idesc = idesc_tf32(M, N, 0, 1);
+  } else if (p.test == 9) {  // test 6 data, descriptor LBO/SBO swapped
+    M = 128; N = 64; K = 32;
+    for (int e = tid; e < M * K; e += 128) {
+      const int m = e / K, k = e % K;
+      *reinterpret_cast<float*>(sa + kmaj_off(m, k, 128, 1024)) = p.A[m * K + k];
+    }
+    for (int e = tid; e < N * K; e += 128) {
+      const int n = e / K, k = e % K;
+      *reinterpret_cast<float*>(sb + mnmaj_off(n, k, 1024, 2048)) = p.B[n * K + k];
+    }
+    idesc = idesc_tf32(M, N, 0, 1);
   } else if (p.test == 4) {  // M = 64 layout probe: SS K-major, N = 16, K = 8
     M = 64; N = 16; K = 8;
     for (int e = tid; e < M * K; e += 128) {
@@ -106,6 +174,29 @@ __global__ void __launch_bounds__(128, 1) probe_kernel(Probe p) {
     } else if (p.test == 2) {
       for (int s = 0; s < 4; ++s)
         mma_ts(T, T + 128 + 8 * s, smem_desc(b0 + s * 2048, 1024, 2048, kSwizzle128), idesc, s > 0);
+    } else if (p.test == 5) {
+      for (int s = 0; s < 4; ++s)
+        mma_ts(T, T + 128 + 8 * s, smem_desc(b0 + s * 256, 128, 1024, kSwizzleNone), idesc, s > 0);
+    } else if (p.test == 6) {
+      for (int s = 0; s < 4; ++s)
+        mma_ss(T, smem_desc(a0 + s * 256, 128, 1024, kSwizzleNone), smem_desc(b0 + s * 2048, 1024, 2048, kSwizzle128),
+               idesc, s > 0);
+    } else if (p.test == 7) {
+      for (int s = 0; s < 4; ++s)
+        mma_ss(T, smem_desc(a0 + s * 32, 16, 1024, kSwizzle128), smem_desc(b0 + s * 256, 128, 1024, kSwizzleNone),
+               idesc, s > 0);
+    } else if (p.test == 8) {  // interleave: LBO = K-group stride, SBO = MN-core stride
+      for (int s = 0; s < 4; ++s)
+        mma_ss(T, smem_desc(a0 + s * 256, 128, 1024, kSwizzleNone), smem_desc(b0 + s * 2048, 2048, 128, kSwizzleNone),
+               idesc, s > 0);
+    } else if (p.test == 10) {  // interleave, the other reading of LBO / SBO
+      for (int s = 0; s < 4; ++s)
+        mma_ss(T, smem_desc(a0 + s * 256, 128, 1024, kSwizzleNone), smem_desc(b0 + s * 2048, 128, 2048, kSwizzleNone),
+               idesc, s > 0);
+    } else if (p.test == 9) {
+      for (int s = 0; s < 4; ++s)
+        mma_ss(T, smem_desc(a0 + s * 256, 128, 1024, kSwizzleNone), smem_desc(b0 + s * 2048, 2048, 1024, kSwizzle128),
+               idesc, s > 0);
     } else if (p.test == 3) {
       for (int s = 0; s < 2; ++s)
         mma_ss(T, smem_desc(a0 + s * 4096, 1024, 4096, kSwizzle128),
@@ -151,11 +242,11 @@ int main() {
   cudaMalloc(&dA, A.size() * 4);
   cudaMalloc(&dB, B.size() * 4);
   cudaMalloc(&dD, D.size() * 4);
-  cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
   int fails = 0;
-  for (int test = 1; test <= 4; ++test) {
+  for (int test = 1; test <= 10; ++test) {
     int m = 128, n = 64, k = 8;
-    if (test == 2) k = 32;
+    if (test == 2 || test >= 5) k = 32;
     if (test == 3) { n = 32; k = 16; }
     if (test == 4) { m = 64; n = 16; k = 8; }
     std::vector<float> a(m * k), b(n * k);
@@ -165,7 +256,7 @@ int main() {
     cudaMemcpy(dB, b.data(), b.size() * 4, cudaMemcpyHostToDevice);
     cudaMemset(dD, 0, D.size() * 4);
     Probe p{dA, dB, dD, test};
-    probe_kernel<<<1, 128, 65536>>>(p);
+    probe_kernel<<<1, 128, 65536 + 1024>>>(p);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("test %d: CUDA error %s\n", test, cudaGetErrorString(e)); return 1; }
     cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
