@@ -18,19 +18,26 @@
 // against A' = [A_hi | A_lo | A_hi] (3r <= 32).  For MMA2, c (its fp32 value,
 // read as c_hi) times [W_hi | W_lo] (N = 32) plus c_lo times W_hi (N = 16).
 //
-// Per tile and CTA (TMEM lane = position, 512 columns):
-//   [0,128)   L, then c in place (Phase I/II in registers: l -> c)
-//   [128,256) c_lo, then Lnew (MMA3)
-//   [256,288) B' (MMA1 A operand), then F' (MMA3 A operand)
-//   [288,320) F^T partial sums (MMA2 accumulator: cols 0-15 hi, 16-31 lo part)
-// The four CTAs' F^T partials are summed in rank order through distributed
-// shared memory (every CTA gets the same bits), the override of the other
-// index set is applied, and rank 0 writes the new factor.  Phase B reads c and
-// Lnew from TMEM for the residual.  D tiles are double-buffered with cp.async
-// (tile t + 1 loads during tile t).  The I x J entries of c are taken from the
-// core U (the core kernel's values), so the strips agree with U bit for bit on
-// the intersection, as _sync_intersection makes them in the reference
-// (solver.py:216-221).
+// TMEM (lane = position, 512 columns), two tile slots by tile parity:
+//   TL[2] [0,256)   L, then c in place (Phase I/II in registers: l -> c), then
+//                   the residual r = c - Lnew: MMA3 accumulates -F'.Res'^T
+//                   onto c
+//   TC    [256,384) c_lo (MMA2 A operand)
+//   TB[2] [384,448) B' (MMA1 A operand), then -F' (MMA3 A operand)
+//   TF    [448,480) F^T partial sums (MMA2 accumulator: cols 0-15 hi, 16-31 lo)
+// Software pipeline (per CTA, tile t): Phase I/II of t, then the residual of
+// t - 1, then -- by the four warps of line group 0 -- B' of t + 1 (so MMA1 of
+// t + 1 runs while they finish t) and the factor epilogue of t, while the other
+// warps go on to Phase I/II of t + 1.  The epilogue sums the four CTAs' F^T
+// partials in rank order: each CTA owns 32 positions, receives the partials
+// of its positions from every rank (distributed shared memory stores +
+// cluster-scope mbarriers), applies the override of the other index set,
+// writes the new factor, and sends the final values to every rank, so all
+// four hold the same bits.  D tiles are double-buffered with cp.async (tile
+// t + 2 loads once Phase I/II of t is done).  The I x J entries of c are taken
+// from the core U (the core kernel's values), so the strips agree with U bit
+// for bit on the intersection, as _sync_intersection makes them in the
+// reference (solver.py:216-221).
 //
 // den and the residual are reduced per tile and written per (tile, rank), so
 // e_k does not depend on the grid size.
@@ -51,20 +58,23 @@ constexpr int NT = (NW + 1) * 32;
 constexpr int KC = 32;         // concatenated K of the r-products
 constexpr int RMAX = 10;       // 3 r <= KC
 // TMEM columns
-constexpr uint32_t TL = 0, TC = 128, TB = 256, TF = 288, TCOLS = 512;
+constexpr uint32_t TL0 = 0, TC = 256, TB0 = 384, TF = 448, TCOLS = 512;
 // shared memory (offsets from a 1 KB aligned base)
 constexpr size_t D_BYTES = (size_t)ML * TP * 4;             // one D tile: [line][pos]
 constexpr size_t O_D = 0;                                   // 2 D tiles
-constexpr size_t O_BST = O_D + 2 * D_BYTES;                 // 2 x Bold staging [16][TP]
-constexpr size_t BST_BYTES = (size_t)16 * TP * 4;
+constexpr size_t O_BST = O_D + 2 * D_BYTES;                 // 2 x Bold staging [RMAX][TP]
+constexpr size_t BST_BYTES = (size_t)RMAX * TP * 4;
 constexpr size_t O_OM = O_BST + 2 * BST_BYTES;              // 2 x omap [TP]
-constexpr size_t O_AOP = O_OM + 2 * TP * 4;                 // A'  [ML][KC] K-major SW128 (1 KB aligned)
+constexpr size_t O_AOP = (O_OM + 2 * TP * 4 + 1023) & ~(size_t)1023;  // A' [ML][KC] K-major SW128
 constexpr size_t O_ROP = O_AOP + (size_t)ML * KC * 4;       // Res'
 constexpr size_t O_WOP = O_ROP + (size_t)ML * KC * 4;       // W'  [32 rows][ML lines] K-major SW128
-constexpr size_t O_FP = O_WOP + (size_t)32 * ML * 4;        // 2 x F partials [TP][16]
-constexpr size_t O_WS = O_FP + 2 * (size_t)TP * 16 * 4;     // per-warp (den, res) doubles
-constexpr size_t O_BAR = O_WS + (size_t)NW * 2 * 8;
-constexpr int NBAR = 2 + 3 + 4 + 2;                         // full[2], lfull ffull bfull, cready[4], bready fready
+constexpr int XF = 12;                                      // floats per position in the exchange (R <= 10, 16 B multiple)
+constexpr size_t O_XIN = O_WOP + (size_t)32 * ML * 4;       // [2][CS src][32 own pos][XF] partials received
+constexpr size_t O_XOUT = O_XIN + (size_t)2 * CS * 32 * XF * 4;  // [2][TP][XF] final factor values
+constexpr size_t O_WS = O_XOUT + (size_t)2 * TP * XF * 4;  // per-warp (den, res) doubles
+constexpr size_t O_LOFF = O_WS + (size_t)NW * 2 * 8;        // line offsets (int64) [2 strips][ML]
+constexpr size_t O_BAR = O_LOFF + (size_t)2 * ML * 8;
+constexpr int NBAR = 2 + 3 + 4 + 2 + 4;  // full[2], lfull ffull bfull, cready[4], bready fready, xin[2] xout[2]
 constexpr size_t O_TBASE = O_BAR + NBAR * 8;
 constexpr size_t SMEM = O_TBASE + 16 + 1024;                // + alignment slack
 }  // namespace s5
@@ -108,14 +118,43 @@ __device__ __forceinline__ uint32_t n_clusters_x() {
   asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ float ld_cluster_f32(uint32_t local_saddr, uint32_t rank) {
+// 4 floats of a peer CTA's shared memory (the loads of a cluster_sync_all()
+// protected buffer need no ordering among themselves: no memory clobber)
+__device__ __forceinline__ float4 ld_cluster_v4(uint32_t local_saddr, uint32_t rank) {
   uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_saddr), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_saddr), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote));
   return v;
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ void st_cluster_v4(uint32_t local_saddr, uint32_t rank, float4 v) {
+  uint32_t remote;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_saddr), "r"(rank));
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+// arrive on a peer's (or this CTA's) mbarrier, releasing this thread's prior
+// shared::cluster stores at cluster scope
+__device__ __forceinline__ void arrive_cluster(uint64_t* local_bar, uint32_t rank) {
+  uint32_t remote;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(umma::smem_u32(local_bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(umma::smem_u32(b)), "r"(parity)
+        : "memory");
+}
 
 template <int R>
 __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constant__ StripsArgs<float> a) {
@@ -129,16 +168,20 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
   unsigned char* Aop = sm + O_AOP;
   unsigned char* Rop = sm + O_ROP;
   unsigned char* Wop = sm + O_WOP;
-  float* Fp = reinterpret_cast<float*>(sm + O_FP);
+  float* Xin = reinterpret_cast<float*>(sm + O_XIN);
+  float* Xout = reinterpret_cast<float*>(sm + O_XOUT);
   double* Ws = reinterpret_cast<double*>(sm + O_WS);
+  int64_t* loff = reinterpret_cast<int64_t*>(sm + O_LOFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + O_BAR);
-  uint64_t* full = bars;          // [2]
-  uint64_t* lfull = bars + 2;
-  uint64_t* ffull = bars + 3;
-  uint64_t* bfull = bars + 4;
-  uint64_t* cready = bars + 5;    // [4]
-  uint64_t* bready = bars + 9;
-  uint64_t* fready = bars + 10;
+  uint64_t* full = bars;          // [2] D tile landed (cp.async, 512 arrivals)
+  uint64_t* lfull = bars + 2;     // MMA1 done
+  uint64_t* ffull = bars + 3;     // MMA2 done
+  uint64_t* bfull = bars + 4;     // MMA3 done
+  uint64_t* cready = bars + 5;    // [4] c / c_lo of line group g in TMEM
+  uint64_t* bready = bars + 9;    // B' in TMEM
+  uint64_t* fready = bars + 10;   // -F' in TMEM
+  uint64_t* xin = bars + 11;      // [2] partials of my positions from all ranks
+  uint64_t* xout = bars + 13;     // [2] final values from all owners
   uint32_t* tbase = reinterpret_cast<uint32_t*>(sm + O_TBASE);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -155,14 +198,26 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
     for (int g = 0; g < 4; ++g) umma::bar_init(&cready[g], 4);
     umma::bar_init(bready, 4);
     umma::bar_init(fready, 4);
+    for (int k = 0; k < 2; ++k) {
+      umma::bar_init(&xin[k], CS * 32);
+      umma::bar_init(&xout[k], CS * 32);
+    }
     umma::bar_init_fence();
+  }
+  for (int e = tid; e < 2 * ML; e += NT) {  // element offsets of this CTA's line segments, both strips
+    const int q = e / ML, li = e - q * ML;
+    const StripDesc<float>& s = a.s[q];
+    const int nk = s.nk, h = (nk + CS - 1) / CS, l0 = (int)rank * h;
+    loff[e] = (s.tiles > 0 && li < h && l0 + li < nk) ? (int64_t)(s.lines[l0 + li] - s.line_off) * s.line_stride : 0;
   }
   umma::fence_before();
   __syncthreads();
+  cluster_sync_all();  // every CTA's barriers are initialised before any remote arrive
   umma::fence_after();
   const uint32_t T = *tbase;
 
   const int tiles0 = a.s[0].tiles, total = tiles0 + a.s[1].tiles;
+  auto strip_of = [&](int t) { return t < tiles0 ? 0 : 1; };
   // this CTA's lines of strip q: [l0, l0 + hl)
   auto line_range = [&](int q, int& l0, int& hl) {
     const int nk = a.s[q].nk;
@@ -173,7 +228,7 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
   };
   // ---- cp.async loads of tile t into buffer b (elementwise warps)
   auto issue_loads = [&](int t, int b) {
-    const int q = t < tiles0 ? 0 : 1;
+    const int q = strip_of(t);
     const StripDesc<float>& s = a.s[q];
     const int x0 = (t - (q ? tiles0 : 0)) * TP;
     int l0, hl;
@@ -185,10 +240,10 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       const int pos = x0 + ch * 4;
       const int rem = s.npos - pos;
       const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
-      const float* src = s.src + (int64_t)(s.lines[l0 + li] - s.line_off) * s.line_stride + (bytes ? pos : x0);
-      umma::cp_async16(dst + (size_t)li * TP + ch * 4, src, (uint32_t)bytes);
+      umma::cp_async16(dst + (size_t)li * TP + ch * 4, s.src + loff[q * ML + li] + (bytes ? pos : x0),
+                       (uint32_t)bytes);
     }
-    float* bdst = Bst + (size_t)b * 16 * TP;
+    float* bdst = Bst + (size_t)b * RMAX * TP;
     for (int e = tid; e < R * (TP / 4); e += NW * 32) {
       const int tt = e >> 5, ch = e & 31;
       const int pos = x0 + ch * 4;
@@ -240,71 +295,70 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
   const uint32_t idesc_f32 = umma::idesc_tf32(128, 32, 0, 0);
   const uint32_t idesc_f16 = umma::idesc_tf32(128, 16, 0, 0);
   const uint32_t a_op = umma::smem_u32(Aop), r_op = umma::smem_u32(Rop), w_op = umma::smem_u32(Wop);
+  auto TL = [&](int i) { return TL0 + 128u * (uint32_t)(i & 1); };
+  auto TB = [&](int i) { return TB0 + 32u * (uint32_t)(i & 1); };
 
-  const int q_ = w & 3, g_ = w >> 2;  // elementwise warp: position quadrant, line group
-  const int p = 32 * q_ + lane;        // position in the tile (TMEM lane)
-  const uint32_t lane_off = (uint32_t)(32 * q_) << 16;
-  int cur = -1;
-  int i = 0;
-  if (!issuer_warp && cid < total) issue_loads(cid, 0);
-  for (int t = cid; t < total; t += ncl, ++i) {
-    const int b = i & 1;
-    const uint32_t ph = (uint32_t)(i & 1);
-    const int q = t < tiles0 ? 0 : 1;
-    const StripDesc<float>& s = a.s[q];
-    const int x0 = (t - (q ? tiles0 : 0)) * TP;
-    int l0, hl;
-    line_range(q, l0, hl);
-    const int ng = (hl + 31) / 32;
-    if (q != cur) {  // all MMAs of the previous tile are complete (bfull waited)
-      if (!issuer_warp) build_strip_ops(q);
-      __syncthreads();
-      cur = q;
-    }
-    if (issuer_warp) {
-      // ================= MMA issue (one thread)
-      if (lane == 0) {
-        umma::bar_wait(bready, ph);
-        umma::fence_after();
-        for (int k = 0; k < KC / 8; ++k)
-          umma::mma_ts(T + TL, T + TB + 8 * k, umma::smem_desc(a_op + 32 * k, 16, 1024, umma::kSwizzle128), idesc_r,
-                       k > 0);
-        umma::commit(lfull);
-        for (int g = 0; g < ng; ++g) {
+  if (issuer_warp) {
+    // ================= MMA issue (one thread), in tile order
+    if (lane == 0) {
+      int i = 0;
+      for (int t = cid; t < total; t += ncl, ++i) {
+        const uint32_t ph = (uint32_t)(i & 1);
+        const int q = strip_of(t);
+        int l0, hl;
+        line_range(q, l0, hl);
+        const int ng = (hl + 31) / 32;
+        const bool fresh = i == 0 || strip_of(t - ncl) != q;
+        const bool next_same = t + ncl < total && strip_of(t + ncl) == q;
+        if (fresh) {  // MMA1 of t (otherwise issued during tile t - 1)
+          umma::bar_wait(bready, ph);
+          umma::fence_after();
+          for (int k = 0; k < KC / 8; ++k)
+            umma::mma_ts(T + TL(i), T + TB(i) + 8 * k, umma::smem_desc(a_op + 32 * k, 16, 1024, umma::kSwizzle128),
+                         idesc_r, k > 0);
+          umma::commit(lfull);
+        }
+        for (int g = 0; g < ng; ++g) {  // MMA2: F^T = c . [W_hi | W_lo] + c_lo . W_hi
           umma::bar_wait(&cready[g], ph);
           umma::fence_after();
           for (int k = 0; k < 4; ++k) {
             const uint64_t wd = umma::smem_desc(w_op + g * 4096 + 32 * k, 16, 1024, umma::kSwizzle128);
-            umma::mma_ts(T + TF, T + TL + 32 * g + 8 * k, wd, idesc_f32, (g | k) > 0);
+            umma::mma_ts(T + TF, T + TL(i) + 32 * g + 8 * k, wd, idesc_f32, (g | k) > 0);
             umma::mma_ts(T + TF, T + TC + 32 * g + 8 * k, wd, idesc_f16, true);
           }
         }
         umma::commit(ffull);
-      }
-      __syncwarp();
-      cluster_sync_all();  // F partials of all ranks written
-      if (lane == 0) {
+        if (next_same) {  // MMA1 of t + 1 into the other slot
+          umma::bar_wait(bready, ph ^ 1u);
+          umma::fence_after();
+          for (int k = 0; k < KC / 8; ++k)
+            umma::mma_ts(T + TL(i + 1), T + TB(i + 1) + 8 * k,
+                         umma::smem_desc(a_op + 32 * k, 16, 1024, umma::kSwizzle128), idesc_r, k > 0);
+          umma::commit(lfull);
+        }
+        // MMA3: r = c - F'.Res'^T accumulated onto c (F' stored negated)
         umma::bar_wait(fready, ph);
         umma::fence_after();
         for (int k = 0; k < KC / 8; ++k)
-          umma::mma_ts(T + TC, T + TB + 8 * k, umma::smem_desc(r_op + 32 * k, 16, 1024, umma::kSwizzle128), idesc_r,
-                       k > 0);
+          umma::mma_ts(T + TL(i), T + TB(i) + 8 * k, umma::smem_desc(r_op + 32 * k, 16, 1024, umma::kSwizzle128),
+                       idesc_r, true);
         umma::commit(bfull);
       }
-      __syncwarp();
-      named_bar(1, NT);  // end of tile
-      continue;
     }
+    __syncwarp();
+  } else {
     // ================= elementwise warps
-    // prefetch the next tile into the other buffer (its previous tile is done)
-    if (t + ncl < total) issue_loads(t + ncl, b ^ 1);
-    umma::bar_wait(&full[b], (uint32_t)((i >> 1) & 1));
-    const float* Db = Dt + (size_t)b * ML * TP;
-    const int* Omb = Om + b * TP;
-    const bool inpos = x0 + p < s.npos;
-    const int om = inpos ? Omb[p] : -1;
-    if (g_ == 0) {  // B' = [B | B | B_lo | 0] for this tile's positions
-      const float* Bb = Bst + (size_t)b * 16 * TP;
+    const int q_ = w & 3, g_ = w >> 2;  // position quadrant (TMEM lanes), line group (TMEM columns)
+    const int p = 32 * q_ + lane;        // position in the tile
+    const uint32_t lane_off = (uint32_t)(32 * q_) << 16;
+    // optional per-phase clock64 totals of thread 0 (ircur_set_profiling)
+    const bool rec = a.dbg && blockIdx.x == 0 && tid == 0;
+    long long tpc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
+#define S5PH(k) do { if (rec) { const long long _t = clock64(); tpc[k] += _t - tq; tq = _t; } } while (0)
+    // B' = [B | B | B_lo | 0] of tile t (buffer b) into TB(i), group-0 warps
+    auto build_bprime = [&](int i, int b) {
+      const float* Bb = Bst + (size_t)b * RMAX * TP;
       float v[KC];
 #pragma unroll
       for (int k = 0; k < KC; ++k) v[k] = 0.f;
@@ -315,135 +369,212 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
         v[R + tt] = x;
         v[2 * R + tt] = s5_lo(x);
       }
-      s5_st32(T + lane_off + TB, v);
+      s5_st32(T + lane_off + TB(i), v);
       umma::st_wait();
       umma::fence_before();
       __syncwarp();
       if (lane == 0) umma::bar_arrive(bready);
-    }
-    // ---- Phase I/II (solver.py:375-382): l -> c in TMEM, c_lo beside it
-    float den = 0.f;
-    umma::bar_wait(lfull, ph);
-    umma::fence_after();
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {  // 16 lines at a time (register pressure)
-      const int c0 = 32 * g_ + 16 * hh;
-      float l[16];
-      umma::ld16(T + lane_off + TL + c0, l);
-      umma::ld_wait();
-      float c[16], cl[16];
-#pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        const int li = c0 + j;
-        Pair<float> d, lp;
-        d.v = make_float2(li < hl ? Db[(size_t)li * TP + p] : 0.f, li + 1 < hl ? Db[(size_t)(li + 1) * TP + p] : 0.f);
-        lp.v = make_float2(l[j], l[j + 1]);
-        const Pair<float> e = keep_pair(d, lp, a.zt);
-        c[j] = li < hl ? e.v.x : 0.f;
-        c[j + 1] = li + 1 < hl ? e.v.y : 0.f;
-        den = __fmaf_rn(d.v.x, d.v.x, den);
-        den = __fmaf_rn(d.v.y, d.v.y, den);
-      }
-      if (om >= 0) {  // I x J entries: the core's values (U = (D - S)(I, J))
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int li = c0 + j;
-          if (li < hl) c[j] = (float)s.U[(int64_t)(l0 + li) * s.u_ls + (int64_t)om * s.u_ps];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) cl[j] = s5_lo(c[j]);
-      umma::st16(T + lane_off + TL + c0, c);
-      umma::st16(T + lane_off + TC + c0, cl);
-    }
-    umma::st_wait();
-    umma::fence_before();
-    __syncwarp();
-    if (lane == 0) umma::bar_arrive(&cready[g_]);
-    // ---- factor sums: rank partials -> cluster sum -> override -> F, F'
-    float* fpb = Fp + (size_t)b * TP * 16;
-    if (g_ == 0) {
-      umma::bar_wait(ffull, ph);
+    };
+    // residual of tile i (TL(i) holds r after MMA3) and its per-tile sums
+    float den_prev = 0.f;
+    int t_prev = -1, q_prev = 0;
+    auto phase_b = [&](int i, int t, int q, float den) {
+      float res = 0.f;
+      umma::bar_wait(bfull, (uint32_t)(i & 1));
       umma::fence_after();
-      float v[32];
-      s5_ld32(T + lane_off + TF, v);
-      umma::ld_wait();
 #pragma unroll
-      for (int tt = 0; tt < R; ++tt) fpb[p * 16 + tt] = ng > 0 ? __fadd_rn(v[tt], v[16 + tt]) : 0.f;
-    }
-    cluster_sync_all();
-    if (g_ == 0) {
-      float f[R];
-      const uint32_t my = umma::smem_u32(fpb + p * 16);
+      for (int hh = 0; hh < 2; ++hh) {
+        float r[16];
+        umma::ld16(T + lane_off + TL(i) + 32 * g_ + 16 * hh, r);
+        umma::ld_wait();
 #pragma unroll
-      for (int tt = 0; tt < R; ++tt) f[tt] = ld_cluster_f32(my + 4 * tt, 0);
-      for (uint32_t rr = 1; rr < CS; ++rr) {
-#pragma unroll
-        for (int tt = 0; tt < R; ++tt) f[tt] = __fadd_rn(f[tt], ld_cluster_f32(my + 4 * tt, rr));
+        for (int j = 0; j < 16; ++j) res = __fmaf_rn(r[j], r[j], res);
       }
-      if (om >= 0) {
-#pragma unroll
-        for (int tt = 0; tt < R; ++tt) f[tt] = s.otherF[(int64_t)om * R + tt];
+      umma::fence_before();
+      const double dd = warp_sum((double)den), rd = warp_sum((double)res);
+      if (lane == 0) {
+        Ws[2 * w] = dd;
+        Ws[2 * w + 1] = rd;
       }
-      if (rank == 0 && inpos) {
-#pragma unroll
-        for (int tt = 0; tt < R; ++tt) s.Fnew[(int64_t)tt * s.ldf + x0 + p] = f[tt];
+      named_bar(1, NW * 32);  // all elementwise warps: residual of tile t done
+      if (tid == 0) {
+        double sd = 0.0, sr = 0.0;
+        for (int ww = 0; ww < NW; ++ww) {
+          sd += Ws[2 * ww];
+          sr += Ws[2 * ww + 1];
+        }
+        double4 pr;
+        pr.x = q ? 0.0 : sd;
+        pr.y = q ? 0.0 : sr;
+        pr.z = q ? sd : 0.0;
+        pr.w = q ? sr : 0.0;
+        *reinterpret_cast<double4*>(a.partials + 4 * ((size_t)t * CS + rank)) = pr;
       }
-      float v[KC];
-#pragma unroll
-      for (int k = 0; k < KC; ++k) v[k] = 0.f;
-#pragma unroll
-      for (int tt = 0; tt < R; ++tt) {
-        v[tt] = f[tt];
-        v[R + tt] = f[tt];
-        v[2 * R + tt] = s5_lo(f[tt]);
+      named_bar(2, NW * 32);  // Ws read before the next tile's sums
+    };
+
+    if (cid < total) issue_loads(cid, 0);
+    if (cid + ncl < total) issue_loads(cid + ncl, 1);
+    int cur = -1;
+    int i = 0;
+    for (int t = cid; t < total; t += ncl, ++i) {
+      const int b = i & 1;
+      const uint32_t ph = (uint32_t)(i & 1);
+      const int q = strip_of(t);
+      const StripDesc<float>& s = a.s[q];
+      const int x0 = (t - (q ? tiles0 : 0)) * TP;
+      int l0, hl;
+      line_range(q, l0, hl);
+      const bool fresh = q != cur;
+      const bool next_same = t + ncl < total && strip_of(t + ncl) == q;
+      S5PH(7);
+      if (fresh) {
+        if (t_prev >= 0) {  // drain the previous strip's last tile before its operands are replaced
+          phase_b(i - 1, t_prev, q_prev, den_prev);
+          t_prev = -1;
+        }
+        build_strip_ops(q);
+        named_bar(1, NW * 32);
+        cur = q;
+        umma::bar_wait(&full[b], (uint32_t)((i >> 1) & 1));
+        if (g_ == 0) build_bprime(i, b);
+      } else {
+        umma::bar_wait(&full[b], (uint32_t)((i >> 1) & 1));
       }
-      s5_st32(T + lane_off + TB, v);
+      S5PH(0);
+      const float* Db = Dt + (size_t)b * ML * TP;
+      const bool inpos = x0 + p < s.npos;
+      const int om = inpos ? Om[b * TP + p] : -1;
+      // ---- Phase I/II (solver.py:375-382): l -> c in TMEM, c_lo beside it
+      float den = 0.f;
+      umma::bar_wait(lfull, ph);
+      umma::fence_after();
+      S5PH(1);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {  // 16 lines at a time (register pressure)
+        const int c0 = 32 * g_ + 16 * hh;
+        float l[16];
+        umma::ld16(T + lane_off + TL(i) + c0, l);
+        umma::ld_wait();
+        float c[16], cl[16];
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          const int li = c0 + j;
+          Pair<float> d, lp;
+          d.v = make_float2(li < hl ? Db[(size_t)li * TP + p] : 0.f, li + 1 < hl ? Db[(size_t)(li + 1) * TP + p] : 0.f);
+          lp.v = make_float2(l[j], l[j + 1]);
+          const Pair<float> e = keep_pair(d, lp, a.zt);
+          c[j] = li < hl ? e.v.x : 0.f;
+          c[j + 1] = li + 1 < hl ? e.v.y : 0.f;
+          den = __fmaf_rn(d.v.x, d.v.x, den);
+          den = __fmaf_rn(d.v.y, d.v.y, den);
+        }
+        if (om >= 0) {  // I x J entries: the core's values (U = (D - S)(I, J))
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int li = c0 + j;
+            if (li < hl) c[j] = (float)s.U[(int64_t)(l0 + li) * s.u_ls + (int64_t)om * s.u_ps];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cl[j] = s5_lo(c[j]);
+        umma::st16(T + lane_off + TL(i) + c0, c);
+        umma::st16(T + lane_off + TC + c0, cl);
+      }
       umma::st_wait();
       umma::fence_before();
       __syncwarp();
-      if (lane == 0) umma::bar_arrive(fready);
-    }
-    // ---- Phase B: residual c - Lnew on the same lines (solver.py:393-400)
-    float res = 0.f;
-    umma::bar_wait(bfull, ph);
-    umma::fence_after();
+      if (lane == 0) umma::bar_arrive(&cready[g_]);
+      S5PH(2);
+      // ---- residual of the previous tile (same strip)
+      if (t_prev >= 0) phase_b(i - 1, t_prev, q_prev, den_prev);
+      S5PH(3);
+      // D buffer b is free once every warp is past Phase I/II of t (the
+      // residual's barrier, or this one): tile t + 2 loads into it
+      if (t_prev < 0) named_bar(1, NW * 32);
+      if (t + 2 * ncl < total) issue_loads(t + 2 * ncl, b);
+      if (g_ == 0) {
+        // B' of the next tile (same strip): its MMA1 runs during this epilogue
+        if (next_same) {
+          umma::bar_wait(&full[b ^ 1], (uint32_t)(((i + 1) >> 1) & 1));
+          build_bprime(i + 1, b ^ 1);
+        }
+        S5PH(4);
+        // ---- factor epilogue: partials -> owner rank -> sum, override, write -> all ranks
+        umma::bar_wait(ffull, ph);
+        umma::fence_after();
+        float v[32];
+        s5_ld32(T + lane_off + TF, v);
+        umma::ld_wait();
+        float pf[XF];
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int c0 = 32 * g_ + 16 * hh;
-      float c[16], ln[16];
-      umma::ld16(T + lane_off + TL + c0, c);
-      umma::ld16(T + lane_off + TC + c0, ln);
-      umma::ld_wait();
+        for (int k = 0; k < XF; ++k) pf[k] = (k < R && hl > 0) ? __fadd_rn(v[k], v[16 + k]) : 0.f;
+        // my partial of position p -> rank q_ (the owner of positions 32 q_ ..), slot [rank]
+        float* xin_slot = Xin + (((size_t)b * CS + rank) * 32 + lane) * XF;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float r = __fsub_rn(c[j], ln[j]);
-        res = __fmaf_rn(r, r, res);
+        for (int k = 0; k < XF; k += 4)
+          st_cluster_v4(umma::smem_u32(xin_slot + k), (uint32_t)q_, make_float4(pf[k], pf[k + 1], pf[k + 2], pf[k + 3]));
+        arrive_cluster(&xin[b], (uint32_t)q_);
+        S5PH(5);
+        const uint32_t xph = (uint32_t)((i >> 1) & 1);  // xin/xout[b] complete every other tile
+        if (q_ == (int)rank) {  // owner: the four partials in rank order, override, write, broadcast
+          wait_cluster(&xin[b], xph);
+          float f[XF];
+#pragma unroll
+          for (int k = 0; k < XF; ++k) f[k] = Xin[(((size_t)b * CS + 0) * 32 + lane) * XF + k];
+#pragma unroll
+          for (int rr = 1; rr < CS; ++rr)
+#pragma unroll
+            for (int k = 0; k < XF; ++k) f[k] = __fadd_rn(f[k], Xin[(((size_t)b * CS + rr) * 32 + lane) * XF + k]);
+          if (om >= 0) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) f[k] = s.otherF[(int64_t)om * R + k];
+          }
+          if (inpos) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) s.Fnew[(int64_t)k * s.ldf + x0 + p] = f[k];
+          }
+          float* xo = Xout + ((size_t)b * TP + p) * XF;
+          for (uint32_t rr = 0; rr < CS; ++rr) {
+#pragma unroll
+            for (int k = 0; k < XF; k += 4)
+              st_cluster_v4(umma::smem_u32(xo + k), rr, make_float4(f[k], f[k + 1], f[k + 2], f[k + 3]));
+            arrive_cluster(&xout[b], rr);
+          }
+        }
+        // final values of my positions (owner rank q_) -> -F' = -[F | F | F_lo | 0]
+        wait_cluster(&xout[b], xph);
+        S5PH(6);
+        {
+          const float* xo = Xout + ((size_t)b * TP + p) * XF;
+          float nv[KC];
+#pragma unroll
+          for (int k = 0; k < KC; ++k) nv[k] = 0.f;
+#pragma unroll
+          for (int tt = 0; tt < R; ++tt) {
+            const float f = xo[tt];
+            nv[tt] = -f;
+            nv[R + tt] = -f;
+            nv[2 * R + tt] = -s5_lo(f);
+          }
+          s5_st32(T + lane_off + TB(i), nv);
+          umma::st_wait();
+          umma::fence_before();
+          __syncwarp();
+          if (lane == 0) umma::bar_arrive(fready);
+        }
       }
+      den_prev = den;
+      t_prev = t;
+      q_prev = q;
     }
-    umma::fence_before();
-    // per-tile sums: warp, then warps in order (thread 0), per (tile, rank)
-    double dd = warp_sum((double)den), rd = warp_sum((double)res);
-    if (lane == 0) {
-      Ws[2 * w] = dd;
-      Ws[2 * w + 1] = rd;
-    }
-    named_bar(1, NT);  // end of tile: TMEM, D buffer b, F partials of b free
-    if (tid == 0) {
-      double sd = 0.0, sr = 0.0;
-      for (int ww = 0; ww < NW; ++ww) {
-        sd += Ws[2 * ww];
-        sr += Ws[2 * ww + 1];
-      }
-      double4 pr;
-      pr.x = q ? 0.0 : sd;
-      pr.y = q ? 0.0 : sr;
-      pr.z = q ? sd : 0.0;
-      pr.w = q ? sr : 0.0;
-      *reinterpret_cast<double4*>(a.partials + 4 * ((size_t)t * CS + rank)) = pr;
-    }
+    if (t_prev >= 0) phase_b(i - 1, t_prev, q_prev, den_prev);
+    if (rec)
+      for (int k = 0; k < 8; ++k) a.dbg[k] += tpc[k];
+#undef S5PH
   }
-  // no CTA leaves while a peer may still read its F partials
+  __syncwarp();
+  // no CTA leaves while a peer may still store into its shared memory or arrive on its barriers
   cluster_sync_all();
   umma::fence_after();
   if (issuer_warp) umma::tmem_free(T, TCOLS);
@@ -472,26 +603,35 @@ cudaError_t launch_strips5(const StripsArgs<float>& a0, int R, int num_sms, int*
   if (tiles == 0) return cudaSuccess;
   const int ncl = std::max(1, std::min(tiles, num_sms / CS));
   cudaError_t e = cudaErrorInvalidValue;
-  IRCUR_DISPATCH_RANK(R, RR, {
-    if constexpr (RR <= RMAX) {
-      static std::atomic<unsigned long long> devs{0};  // once per device
-      const cudaError_t attr = smem_attr_once(devs, strips5_kernel<RR>, (int)SMEM);
-      if (attr != cudaSuccess) return attr;
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(ncl * CS), 1, 1);
-      cfg.blockDim = dim3(NT, 1, 1);
-      cfg.dynamicSmemBytes = SMEM;
-      cfg.stream = st;
-      cudaLaunchAttribute attrs[1];
-      attrs[0].id = cudaLaunchAttributeClusterDimension;
-      attrs[0].val.clusterDim.x = CS;
-      attrs[0].val.clusterDim.y = 1;
-      attrs[0].val.clusterDim.z = 1;
-      cfg.attrs = attrs;
-      cfg.numAttrs = 1;
-      e = cudaLaunchKernelEx(&cfg, strips5_kernel<RR>, a);
-    }
-  });
+  auto launch = [&](auto kern) {
+    static std::atomic<unsigned long long> devs{0};  // once per device (per rank instantiation)
+    (void)devs;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(ncl * CS), 1, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = CS;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+  };
+  static std::atomic<unsigned long long> devs[RMAX + 1];
+  switch (R) {
+#define S5_CASE(RR)                                                                           \
+  case RR: {                                                                                  \
+    const cudaError_t attr = smem_attr_once(devs[RR], strips5_kernel<RR>, (int)SMEM);         \
+    if (attr != cudaSuccess) return attr;                                                     \
+    e = launch(strips5_kernel<RR>);                                                           \
+  } break;
+    S5_CASE(1) S5_CASE(2) S5_CASE(3) S5_CASE(4) S5_CASE(5) S5_CASE(6) S5_CASE(7) S5_CASE(8) S5_CASE(9) S5_CASE(10)
+#undef S5_CASE
+    default: return cudaErrorNotSupported;
+  }
   if (e == cudaSuccess && ncta_out) *ncta_out = tiles * CS;  // partial slots: one per (tile, rank)
   return e;
 }

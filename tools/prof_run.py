@@ -45,11 +45,16 @@ for i in range(a.solves):
     fn = ["UV", "H2sum", "jacobi", "rotate+norms", "outputs", "QJ", "sync", "W+Wr"]
     print("  final extraction (Mcycles): " + " ".join(f"{n}={c/1e6:.2f}" for n, c in zip(fn, cyc[24:32])))
     sn = ["stage_wait", "pass1", "reduce", "override+write", "pass2", "sync+issue", "lvec+loop"]
-    if os.environ.get("IRCUR_STRIPS_VER", "3") != "1":
+    ver = os.environ.get("IRCUR_STRIPS_VER", "5")
+    if ver == "5":
+        sn = ["prefetch", "wait_full", "Bprime+MMA1", "phaseA", "MMA2_wait", "partial+cluster_bar",
+              "dsmem+Fprime+MMA3", "phaseB+end"]
+    elif ver != "1":
         sn = ["stage(issue+wait)", "pass1", "sync_after_pass1", "reduce+write+sync", "pass2", "final_sync", "loop"]
-    stot = sum(cyc[16:23]) or 1
+    nph = 8 if ver == "5" else 7
+    stot = sum(cyc[16:16 + nph]) or 1
     print("  strips phases (Mcycles, CTA0/thread0): " + " ".join(
-        f"{n}={c/1e6:.2f}({c/stot*100:.0f}%)" for n, c in zip(sn, [cyc[16 + k] for k in (0, 1, 2, 3, 4, 5, 6)])))
+        f"{n}={c/1e6:.2f}({c/stot*100:.0f}%)" for n, c in zip(sn, [cyc[16 + k] for k in range(nph)])))
     if a.detail and i == a.solves - 1:
         for k in range(res.trace.iterations):
             print(f"  k={k:2d} e={res.trace.errors[k]:.3e} svd_steps={p['svd_steps'][k]:3d} svd={p['svd_ms'][k]:.3f} "
