@@ -52,31 +52,35 @@ namespace ircur {
 namespace s5 {
 constexpr int CS = 4;          // CTAs per cluster
 constexpr int TP = 128;        // positions per tile (MMA M, TMEM lanes)
-constexpr int ML = 128;        // lines per CTA (MMA N of the K = r products)
-constexpr int NW = 16;         // elementwise warps
-constexpr int NT = (NW + 1) * 32;
+constexpr int ML = 128;        // TMEM columns / operand rows for the lines of one CTA
+constexpr int HMAX = 116;      // lines per CTA (<= 464 sampled lines per strip)
+constexpr int NEW = 16;        // elementwise warps: 4 per lane quadrant, 32 lines each
+constexpr int NEP = 4;         // epilogue warps: one per lane quadrant
+constexpr int NT = (NEW + NEP + 1) * 32;  // + the MMA-issuing warp
 constexpr int KC = 32;         // concatenated K of the r-products
 constexpr int RMAX = 10;       // 3 r <= KC
-// TMEM columns
-constexpr uint32_t TL0 = 0, TC = 256, TB0 = 384, TF = 448, TCOLS = 512;
+// TMEM columns (512): two slots by tile parity
+constexpr uint32_t TL0 = 0, TC = 256, TB0 = 384, TF0 = 448, TCOLS = 512;
 // shared memory (offsets from a 1 KB aligned base)
-constexpr size_t D_BYTES = (size_t)ML * TP * 4;             // one D tile: [line][pos]
+constexpr size_t D_BYTES = (size_t)HMAX * TP * 4;           // one D tile: [line][pos]
 constexpr size_t O_D = 0;                                   // 2 D tiles
-constexpr size_t O_BST = O_D + 2 * D_BYTES;                 // 2 x Bold staging [RMAX][TP]
-constexpr size_t BST_BYTES = (size_t)RMAX * TP * 4;
-constexpr size_t O_OM = O_BST + 2 * BST_BYTES;              // 2 x omap [TP]
-constexpr size_t O_AOP = (O_OM + 2 * TP * 4 + 1023) & ~(size_t)1023;  // A' [ML][KC] K-major SW128
+constexpr size_t O_AOP = (O_D + 2 * D_BYTES + 1023) & ~(size_t)1023;  // A' [ML][KC] K-major SW128
 constexpr size_t O_ROP = O_AOP + (size_t)ML * KC * 4;       // Res'
 constexpr size_t O_WOP = O_ROP + (size_t)ML * KC * 4;       // W'  [32 rows][ML lines] K-major SW128
-constexpr int XF = 12;                                      // floats per position in the exchange (R <= 10, 16 B multiple)
-constexpr size_t O_XIN = O_WOP + (size_t)32 * ML * 4;       // [2][CS src][32 own pos][XF] partials received
+constexpr size_t O_BP = O_WOP + (size_t)32 * ML * 4;        // 2 x B' [TP][KC] K-major SW128 (MMA1 A operand)
+constexpr size_t O_OM = O_BP + 2 * (size_t)TP * KC * 4;     // 2 x omap [TP]
+constexpr int XF = 12;                                      // floats per position in the exchange (R <= 10)
+constexpr size_t O_XIN = O_OM + 2 * TP * 4;                 // [2][CS src][32 own pos][XF] partials received
 constexpr size_t O_XOUT = O_XIN + (size_t)2 * CS * 32 * XF * 4;  // [2][TP][XF] final factor values
 constexpr size_t O_WS = O_XOUT + (size_t)2 * TP * XF * 4;  // per-warp (den, res) doubles
-constexpr size_t O_LOFF = O_WS + (size_t)NW * 2 * 8;        // line offsets (int64) [2 strips][ML]
+constexpr size_t O_LOFF = O_WS + (size_t)NEW * 2 * 8;       // line offsets (int64) [2 strips][ML]
 constexpr size_t O_BAR = O_LOFF + (size_t)2 * ML * 8;
-constexpr int NBAR = 2 + 3 + 4 + 2 + 4;  // full[2], lfull ffull bfull, cready[4], bready fready, xin[2] xout[2]
+// per tile parity: full lfull ffull bfull bready fready rdone xin xout cready[4]; + opsready
+constexpr int NB_PER = 13;
+constexpr int NBAR = 2 * NB_PER + 1;
 constexpr size_t O_TBASE = O_BAR + NBAR * 8;
 constexpr size_t SMEM = O_TBASE + 16 + 1024;                // + alignment slack
+static_assert(SMEM <= 227 * 1024, "strips5 shared memory");
 }  // namespace s5
 
 __device__ __forceinline__ float s5_lo(float x) { return __fsub_rn(x, umma::tf32_hi(x)); }
@@ -163,45 +167,42 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
   extern __shared__ unsigned char sm_raw[];
   unsigned char* sm = sm_raw + ((1024 - (umma::smem_u32(sm_raw) & 1023)) & 1023);
   float* Dt = reinterpret_cast<float*>(sm + O_D);
-  float* Bst = reinterpret_cast<float*>(sm + O_BST);
-  int* Om = reinterpret_cast<int*>(sm + O_OM);
   unsigned char* Aop = sm + O_AOP;
   unsigned char* Rop = sm + O_ROP;
   unsigned char* Wop = sm + O_WOP;
+  unsigned char* Bp = sm + O_BP;
+  int* Om = reinterpret_cast<int*>(sm + O_OM);
   float* Xin = reinterpret_cast<float*>(sm + O_XIN);
   float* Xout = reinterpret_cast<float*>(sm + O_XOUT);
   double* Ws = reinterpret_cast<double*>(sm + O_WS);
   int64_t* loff = reinterpret_cast<int64_t*>(sm + O_LOFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + O_BAR);
-  uint64_t* full = bars;          // [2] D tile landed (cp.async, 512 arrivals)
-  uint64_t* lfull = bars + 2;     // MMA1 done
-  uint64_t* ffull = bars + 3;     // MMA2 done
-  uint64_t* bfull = bars + 4;     // MMA3 done
-  uint64_t* cready = bars + 5;    // [4] c / c_lo of line group g in TMEM
-  uint64_t* bready = bars + 9;    // B' in TMEM
-  uint64_t* fready = bars + 10;   // -F' in TMEM
-  uint64_t* xin = bars + 11;      // [2] partials of my positions from all ranks
-  uint64_t* xout = bars + 13;     // [2] final values from all owners
+  // barriers of tile parity b: bar(b, k)
+  auto bar = [&](int b, int k) { return bars + b * NB_PER + k; };
+  constexpr int kFull = 0, kL = 1, kF = 2, kB = 3, kBready = 4, kFready = 5, kRdone = 6, kXin = 7, kXout = 8,
+                kC = 9;  // kC + g: cready of line group g
+  uint64_t* opsready = bars + 2 * NB_PER;
   uint32_t* tbase = reinterpret_cast<uint32_t*>(sm + O_TBASE);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t rank = cluster_rank();
   const int cid = (int)cluster_id_x(), ncl = (int)n_clusters_x();
-  const bool issuer_warp = w == NW;
+  const bool issuer_warp = w == NEW + NEP;
   if (issuer_warp) umma::tmem_alloc(tbase, TCOLS);
   if (tid == 0) {
-    umma::bar_init(&full[0], NW * 32);
-    umma::bar_init(&full[1], NW * 32);
-    umma::bar_init(lfull, 1);
-    umma::bar_init(ffull, 1);
-    umma::bar_init(bfull, 1);
-    for (int g = 0; g < 4; ++g) umma::bar_init(&cready[g], 4);
-    umma::bar_init(bready, 4);
-    umma::bar_init(fready, 4);
-    for (int k = 0; k < 2; ++k) {
-      umma::bar_init(&xin[k], CS * 32);
-      umma::bar_init(&xout[k], CS * 32);
+    for (int b = 0; b < 2; ++b) {
+      umma::bar_init(bar(b, kFull), NEW * 32);
+      umma::bar_init(bar(b, kL), 1);
+      umma::bar_init(bar(b, kF), 1);
+      umma::bar_init(bar(b, kB), 1);
+      umma::bar_init(bar(b, kBready), 4);
+      umma::bar_init(bar(b, kFready), 4);
+      umma::bar_init(bar(b, kRdone), NEW);
+      umma::bar_init(bar(b, kXin), CS * 32);
+      umma::bar_init(bar(b, kXout), CS * 32);
+      for (int g = 0; g < 4; ++g) umma::bar_init(bar(b, kC + g), 4);
     }
+    umma::bar_init(opsready, 1);
     umma::bar_init_fence();
   }
   for (int e = tid; e < 2 * ML; e += NT) {  // element offsets of this CTA's line segments, both strips
@@ -217,189 +218,175 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
   const uint32_t T = *tbase;
 
   const int tiles0 = a.s[0].tiles, total = tiles0 + a.s[1].tiles;
+  const int ntl = cid < total ? (total - 1 - cid) / ncl + 1 : 0;  // this cluster's tiles
+  auto tile_of = [&](int i) { return cid + i * ncl; };
   auto strip_of = [&](int t) { return t < tiles0 ? 0 : 1; };
-  // this CTA's lines of strip q: [l0, l0 + hl)
-  auto line_range = [&](int q, int& l0, int& hl) {
+  auto fresh_at = [&](int i) { return i == 0 || strip_of(tile_of(i)) != strip_of(tile_of(i - 1)); };
+  auto line_range = [&](int q, int& l0, int& hl) {  // this CTA's lines of strip q: [l0, l0 + hl)
     const int nk = a.s[q].nk;
     const int h = (nk + CS - 1) / CS;
     l0 = (int)rank * h;
     hl = nk - l0 < h ? nk - l0 : h;
     if (hl < 0) hl = 0;
   };
-  // ---- cp.async loads of tile t into buffer b (elementwise warps)
-  auto issue_loads = [&](int t, int b) {
-    const int q = strip_of(t);
-    const StripDesc<float>& s = a.s[q];
-    const int x0 = (t - (q ? tiles0 : 0)) * TP;
-    int l0, hl;
-    line_range(q, l0, hl);
-    float* dst = Dt + (size_t)b * ML * TP;
-    const int nch = hl * (TP / 4);
-    for (int e = tid; e < nch; e += NW * 32) {
-      const int li = e >> 5, ch = e & 31;
-      const int pos = x0 + ch * 4;
-      const int rem = s.npos - pos;
-      const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
-      umma::cp_async16(dst + (size_t)li * TP + ch * 4, s.src + loff[q * ML + li] + (bytes ? pos : x0),
-                       (uint32_t)bytes);
-    }
-    float* bdst = Bst + (size_t)b * RMAX * TP;
-    for (int e = tid; e < R * (TP / 4); e += NW * 32) {
-      const int tt = e >> 5, ch = e & 31;
-      const int pos = x0 + ch * 4;
-      const int rem = s.npos - pos;
-      const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
-      umma::cp_async16(bdst + (size_t)tt * TP + ch * 4, s.Bold + (int64_t)tt * s.ldb + (bytes ? pos : x0),
-                       (uint32_t)bytes);
-    }
-    if (tid < TP / 4) {
-      const int pos = x0 + tid * 4;
-      const int rem = s.npos - pos;
-      const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
-      umma::cp_async16(Om + b * TP + tid * 4, s.omap + (bytes ? pos : x0), (uint32_t)bytes);
-    }
-    umma::cp_async_arrive(&full[b]);
-  };
-  // ---- per-strip operands: A', Res' (K-major rows [x_hi | x_lo | x_hi | 0]) and W'
-  auto build_strip_ops = [&](int q) {
-    const StripDesc<float>& s = a.s[q];
-    int l0, hl;
-    line_range(q, l0, hl);
-    for (int e = tid; e < ML * KC; e += NW * 32) {
-      const int li = e / KC, k = e - li * KC;
-      float va = 0.f, vr = 0.f;
-      if (li < hl && k < 3 * R) {
-        const int tt = k % R, part = k / R;  // 0: hi, 1: lo, 2: hi
-        const float xa = s.lineA[(int64_t)(l0 + li) * R + tt];
-        const float xr = s.lineRes[(int64_t)(l0 + li) * R + tt];
-        va = part == 1 ? s5_lo(xa) : umma::tf32_hi(xa);
-        vr = part == 1 ? s5_lo(xr) : umma::tf32_hi(xr);
-      }
-      *reinterpret_cast<float*>(Aop + s5_kmaj(li, k)) = va;
-      *reinterpret_cast<float*>(Rop + s5_kmaj(li, k)) = vr;
-    }
-    for (int e = tid; e < 32 * ML; e += NW * 32) {
-      const int tp = e / ML, li = e - tp * ML;
-      const int tt = tp & 15;
-      float v = 0.f;
-      if (li < hl && tt < R) {
-        const float x = s.lineW[(int64_t)(l0 + li) * R + tt];
-        v = tp < 16 ? umma::tf32_hi(x) : s5_lo(x);
-      }
-      *reinterpret_cast<float*>(Wop + s5_wop(tp, li)) = v;
-    }
-    umma::fence_async_smem();
-  };
-
-  const uint32_t idesc_r = umma::idesc_tf32(128, ML, 0, 0);
-  const uint32_t idesc_f32 = umma::idesc_tf32(128, 32, 0, 0);
-  const uint32_t idesc_f16 = umma::idesc_tf32(128, 16, 0, 0);
-  const uint32_t a_op = umma::smem_u32(Aop), r_op = umma::smem_u32(Rop), w_op = umma::smem_u32(Wop);
   auto TL = [&](int i) { return TL0 + 128u * (uint32_t)(i & 1); };
   auto TB = [&](int i) { return TB0 + 32u * (uint32_t)(i & 1); };
+  auto TF = [&](int i) { return TF0 + 32u * (uint32_t)(i & 1); };
+  auto xph = [&](int i) { return (uint32_t)((i >> 1) & 1); };  // phase parity of tile i's barriers
 
   if (issuer_warp) {
-    // ================= MMA issue (one thread), in tile order
+    // ================= MMA issue (one thread): three in-order streams, polled
+    //   MMA1(n1): B' built, TL slot free (residual of n1 - 2 read), after MMA2(n1 - 1)
+    //   MMA2(n2): line groups of c / c_lo written, after MMA1(n2), TF slot read (MMA3(n2 - 2) issued)
+    //   MMA3(n3): -F' written, after MMA2(n3)
     if (lane == 0) {
-      int i = 0;
-      for (int t = cid; t < total; t += ncl, ++i) {
-        const uint32_t ph = (uint32_t)(i & 1);
-        const int q = strip_of(t);
-        int l0, hl;
-        line_range(q, l0, hl);
-        const int ng = (hl + 31) / 32;
-        const bool fresh = i == 0 || strip_of(t - ncl) != q;
-        const bool next_same = t + ncl < total && strip_of(t + ncl) == q;
-        if (fresh) {  // MMA1 of t (otherwise issued during tile t - 1)
-          umma::bar_wait(bready, ph);
+      const uint32_t idesc_r = umma::idesc_tf32(128, ML, 0, 0);
+      const uint32_t idesc_f32 = umma::idesc_tf32(128, 32, 0, 0);
+      const uint32_t idesc_f16 = umma::idesc_tf32(128, 16, 0, 0);
+      const uint32_t a_op = umma::smem_u32(Aop), r_op = umma::smem_u32(Rop), w_op = umma::smem_u32(Wop);
+      const uint32_t bp0 = umma::smem_u32(Bp);
+      int n1 = 0, n2 = 0, g2 = 0, n3 = 0, nfresh = 0;
+      while (n3 < ntl) {
+        if (n1 < ntl && n1 <= n2 && umma::bar_try(bar(n1 & 1, kBready), xph(n1)) &&
+            (n1 < 2 || umma::bar_try(bar(n1 & 1, kRdone), xph(n1 - 2))) &&
+            (!fresh_at(n1) || umma::bar_try(opsready, (uint32_t)(nfresh & 1)))) {
+          if (fresh_at(n1)) ++nfresh;
           umma::fence_after();
+          const uint32_t bpa = bp0 + (uint32_t)(n1 & 1) * (TP * KC * 4);
           for (int k = 0; k < KC / 8; ++k)
-            umma::mma_ts(T + TL(i), T + TB(i) + 8 * k, umma::smem_desc(a_op + 32 * k, 16, 1024, umma::kSwizzle128),
-                         idesc_r, k > 0);
-          umma::commit(lfull);
+            umma::mma_ss(T + TL(n1), umma::smem_desc(bpa + 32 * k, 16, 1024, umma::kSwizzle128),
+                         umma::smem_desc(a_op + 32 * k, 16, 1024, umma::kSwizzle128), idesc_r, k > 0);
+          umma::commit(bar(n1 & 1, kL));
+          ++n1;
+          continue;
         }
-        for (int g = 0; g < ng; ++g) {  // MMA2: F^T = c . [W_hi | W_lo] + c_lo . W_hi
-          umma::bar_wait(&cready[g], ph);
-          umma::fence_after();
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t wd = umma::smem_desc(w_op + g * 4096 + 32 * k, 16, 1024, umma::kSwizzle128);
-            umma::mma_ts(T + TF, T + TL(i) + 32 * g + 8 * k, wd, idesc_f32, (g | k) > 0);
-            umma::mma_ts(T + TF, T + TC + 32 * g + 8 * k, wd, idesc_f16, true);
+        if (n2 < n1 && n2 < n3 + 2) {
+          int l0, hl;
+          line_range(strip_of(tile_of(n2)), l0, hl);
+          const int ng = (hl + 31) / 32;
+          if (g2 < ng && umma::bar_try(bar(n2 & 1, kC + g2), xph(n2))) {
+            umma::fence_after();
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t wd = umma::smem_desc(w_op + g2 * 4096 + 32 * k, 16, 1024, umma::kSwizzle128);
+              umma::mma_ts(T + TF(n2), T + TL(n2) + 32 * g2 + 8 * k, wd, idesc_f32, (g2 | k) > 0);
+              umma::mma_ts(T + TF(n2), T + TC + 32 * g2 + 8 * k, wd, idesc_f16, true);
+            }
+            ++g2;
+          }
+          if (g2 >= ng) {
+            umma::commit(bar(n2 & 1, kF));
+            ++n2;
+            g2 = 0;
+            continue;
           }
         }
-        umma::commit(ffull);
-        if (next_same) {  // MMA1 of t + 1 into the other slot
-          umma::bar_wait(bready, ph ^ 1u);
+        if (n3 < n2 && umma::bar_try(bar(n3 & 1, kFready), xph(n3))) {
           umma::fence_after();
-          for (int k = 0; k < KC / 8; ++k)
-            umma::mma_ts(T + TL(i + 1), T + TB(i + 1) + 8 * k,
-                         umma::smem_desc(a_op + 32 * k, 16, 1024, umma::kSwizzle128), idesc_r, k > 0);
-          umma::commit(lfull);
+          const uint32_t r_base = r_op;
+          for (int k = 0; k < KC / 8; ++k)  // r = c - F'.Res'^T accumulated onto c (F' stored negated)
+            umma::mma_ts(T + TL(n3), T + TB(n3) + 8 * k, umma::smem_desc(r_base + 32 * k, 16, 1024, umma::kSwizzle128),
+                         idesc_r, true);
+          umma::commit(bar(n3 & 1, kB));
+          ++n3;
         }
-        // MMA3: r = c - F'.Res'^T accumulated onto c (F' stored negated)
-        umma::bar_wait(fready, ph);
-        umma::fence_after();
-        for (int k = 0; k < KC / 8; ++k)
-          umma::mma_ts(T + TL(i), T + TB(i) + 8 * k, umma::smem_desc(r_op + 32 * k, 16, 1024, umma::kSwizzle128),
-                       idesc_r, true);
-        umma::commit(bfull);
       }
     }
     __syncwarp();
-  } else {
-    // ================= elementwise warps
-    const int q_ = w & 3, g_ = w >> 2;  // position quadrant (TMEM lanes), line group (TMEM columns)
-    const int p = 32 * q_ + lane;        // position in the tile
+  } else if (w < NEW) {
+    // ================= elementwise warps: loads, Phase I/II, residual
+    const int q_ = w & 3, g_ = w >> 2;  // lane quadrant, line group (TMEM columns 32 g_ ..)
+    const int p = 32 * q_ + lane;
     const uint32_t lane_off = (uint32_t)(32 * q_) << 16;
-    // optional per-phase clock64 totals of thread 0 (ircur_set_profiling)
+    const int et = tid;  // 0 .. NEW * 32 - 1
     const bool rec = a.dbg && blockIdx.x == 0 && tid == 0;
     long long tpc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tq = clock64();
 #define S5PH(k) do { if (rec) { const long long _t = clock64(); tpc[k] += _t - tq; tq = _t; } } while (0)
-    // B' = [B | B | B_lo | 0] of tile t (buffer b) into TB(i), group-0 warps
-    auto build_bprime = [&](int i, int b) {
-      const float* Bb = Bst + (size_t)b * RMAX * TP;
-      float v[KC];
-#pragma unroll
-      for (int k = 0; k < KC; ++k) v[k] = 0.f;
-#pragma unroll
-      for (int tt = 0; tt < R; ++tt) {
-        const float x = Bb[tt * TP + p];
-        v[tt] = x;
-        v[R + tt] = x;
-        v[2 * R + tt] = s5_lo(x);
+    // tile i into buffer i & 1: 16-byte cp.async per chunk, every elementwise
+    // thread arrives on the buffer's barrier when its copies land.  (1-D bulk
+    // copies of the 512-byte line segments were measured slower: the copy
+    // engine takes ~70 cycles per copy, ~7 bytes/cycle per SM.)
+    auto issue_loads = [&](int i) {
+      const int t = tile_of(i), b = i & 1;
+      const int q = strip_of(t);
+      const StripDesc<float>& s = a.s[q];
+      const int x0 = (t - (q ? tiles0 : 0)) * TP;
+      int l0, hl;
+      line_range(q, l0, hl);
+      float* dst = Dt + (size_t)b * HMAX * TP;
+      const bool whole = x0 + TP <= s.npos;
+      const int nch = hl * (TP / 4);
+      for (int e = et; e < nch; e += NEW * 32) {
+        const int li = e >> 5, ch = e & 31;
+        const int pos = x0 + ch * 4;
+        const int rem = s.npos - pos;
+        const int bytes = whole ? 16 : (rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0));
+        umma::cp_async16(dst + (size_t)li * TP + ch * 4, s.src + loff[q * ML + li] + (bytes ? pos : x0),
+                         (uint32_t)bytes);
       }
-      s5_st32(T + lane_off + TB(i), v);
-      umma::st_wait();
-      umma::fence_before();
-      __syncwarp();
-      if (lane == 0) umma::bar_arrive(bready);
+      if (et < TP / 4) {
+        const int pos = x0 + et * 4;
+        const int rem = s.npos - pos;
+        const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
+        umma::cp_async16(Om + b * TP + et * 4, s.omap + (bytes ? pos : x0), (uint32_t)bytes);
+      }
+      umma::cp_async_arrive(bar(b, kFull));
     };
-    // residual of tile i (TL(i) holds r after MMA3) and its per-tile sums
-    float den_prev = 0.f;
-    int t_prev = -1, q_prev = 0;
-    auto phase_b = [&](int i, int t, int q, float den) {
+    auto build_strip_ops = [&](int q) {  // A', Res' rows [x_hi | x_lo | x_hi | 0]; W' [W_hi ; W_lo]
+      const StripDesc<float>& s = a.s[q];
+      int l0, hl;
+      line_range(q, l0, hl);
+      for (int e = et; e < ML * KC; e += NEW * 32) {
+        const int li = e / KC, k = e - li * KC;
+        float va = 0.f, vr = 0.f;
+        if (li < hl && k < 3 * R) {
+          const int tt = k % R, part = k / R;  // 0: hi, 1: lo, 2: hi
+          const float xa = s.lineA[(int64_t)(l0 + li) * R + tt];
+          const float xr = s.lineRes[(int64_t)(l0 + li) * R + tt];
+          va = part == 1 ? s5_lo(xa) : umma::tf32_hi(xa);
+          vr = part == 1 ? s5_lo(xr) : umma::tf32_hi(xr);
+        }
+        *reinterpret_cast<float*>(Aop + s5_kmaj(li, k)) = va;
+        *reinterpret_cast<float*>(Rop + s5_kmaj(li, k)) = vr;
+      }
+      for (int e = et; e < 32 * ML; e += NEW * 32) {
+        const int tp = e / ML, li = e - tp * ML;
+        const int tt = tp & 15;
+        float v = 0.f;
+        if (li < hl && tt < R) {
+          const float x = s.lineW[(int64_t)(l0 + li) * R + tt];
+          v = tp < 16 ? umma::tf32_hi(x) : s5_lo(x);
+        }
+        *reinterpret_cast<float*>(Wop + s5_wop(tp, li)) = v;
+      }
+      umma::fence_async_smem();
+    };
+    // residual of tile i (TL(i) holds r = c - Lnew after MMA3) and its per-tile sums
+    auto phase_b = [&](int i, float den) {
+      const int t = tile_of(i), q = strip_of(t);
       float res = 0.f;
-      umma::bar_wait(bfull, (uint32_t)(i & 1));
+      umma::bar_wait(bar(i & 1, kB), xph(i));
       umma::fence_after();
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        float r[16];
-        umma::ld16(T + lane_off + TL(i) + 32 * g_ + 16 * hh, r);
+      {
+        float r[32];
+        s5_ld32(T + lane_off + TL(i) + 32 * g_, r);
         umma::ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) res = __fmaf_rn(r[j], r[j], res);
+        for (int j = 0; j < 32; ++j) res = __fmaf_rn(r[j], r[j], res);
       }
       umma::fence_before();
+      __syncwarp();
+      if (lane == 0) umma::bar_arrive(bar(i & 1, kRdone));  // TL(i) may be overwritten (MMA1 of i + 2)
       const double dd = warp_sum((double)den), rd = warp_sum((double)res);
       if (lane == 0) {
         Ws[2 * w] = dd;
         Ws[2 * w + 1] = rd;
       }
-      named_bar(1, NW * 32);  // all elementwise warps: residual of tile t done
+      named_bar(1, NEW * 32);
       if (tid == 0) {
         double sd = 0.0, sr = 0.0;
-        for (int ww = 0; ww < NW; ++ww) {
+        for (int ww = 0; ww < NEW; ++ww) {
           sd += Ws[2 * ww];
           sr += Ws[2 * ww + 1];
         }
@@ -410,168 +397,200 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
         pr.w = q ? sr : 0.0;
         *reinterpret_cast<double4*>(a.partials + 4 * ((size_t)t * CS + rank)) = pr;
       }
-      named_bar(2, NW * 32);  // Ws read before the next tile's sums
+      named_bar(2, NEW * 32);  // Ws read before the next tile's sums
     };
 
-    if (cid < total) issue_loads(cid, 0);
-    if (cid + ncl < total) issue_loads(cid + ncl, 1);
+    if (ntl > 0) issue_loads(0);
+    if (ntl > 1) issue_loads(1);
     int cur = -1;
-    int i = 0;
-    for (int t = cid; t < total; t += ncl, ++i) {
-      const int b = i & 1;
-      const uint32_t ph = (uint32_t)(i & 1);
+    bool pending = false;
+    float den_prev = 0.f;
+    for (int i = 0; i < ntl; ++i) {
+      const int t = tile_of(i), b = i & 1;
       const int q = strip_of(t);
       const StripDesc<float>& s = a.s[q];
       const int x0 = (t - (q ? tiles0 : 0)) * TP;
       int l0, hl;
       line_range(q, l0, hl);
-      const bool fresh = q != cur;
-      const bool next_same = t + ncl < total && strip_of(t + ncl) == q;
       S5PH(7);
-      if (fresh) {
-        if (t_prev >= 0) {  // drain the previous strip's last tile before its operands are replaced
-          phase_b(i - 1, t_prev, q_prev, den_prev);
-          t_prev = -1;
+      if (q != cur) {  // new strip: drain, then its operands (no MMA reads them now)
+        if (pending) {
+          phase_b(i - 1, den_prev);
+          pending = false;
         }
         build_strip_ops(q);
-        named_bar(1, NW * 32);
+        named_bar(1, NEW * 32);
+        if (tid == 0) umma::bar_arrive(opsready);
         cur = q;
-        umma::bar_wait(&full[b], (uint32_t)((i >> 1) & 1));
-        if (g_ == 0) build_bprime(i, b);
-      } else {
-        umma::bar_wait(&full[b], (uint32_t)((i >> 1) & 1));
       }
+      umma::bar_wait(bar(b, kFull), xph(i));
       S5PH(0);
-      const float* Db = Dt + (size_t)b * ML * TP;
+      const float* Db = Dt + (size_t)b * HMAX * TP;
       const bool inpos = x0 + p < s.npos;
       const int om = inpos ? Om[b * TP + p] : -1;
       // ---- Phase I/II (solver.py:375-382): l -> c in TMEM, c_lo beside it
       float den = 0.f;
-      umma::bar_wait(lfull, ph);
+      umma::bar_wait(bar(b, kL), xph(i));
       umma::fence_after();
       S5PH(1);
+      {
+        const int g = g_;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {  // 16 lines at a time (register pressure)
-        const int c0 = 32 * g_ + 16 * hh;
-        float l[16];
-        umma::ld16(T + lane_off + TL(i) + c0, l);
-        umma::ld_wait();
-        float c[16], cl[16];
+        for (int hh = 0; hh < 2; ++hh) {  // 16 lines at a time (register pressure)
+          const int c0 = 32 * g + 16 * hh;
+          float l[16];
+          umma::ld16(T + lane_off + TL(i) + c0, l);
+          umma::ld_wait();
+          float c[16], cl[16];
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          const int li = c0 + j;
-          Pair<float> d, lp;
-          d.v = make_float2(li < hl ? Db[(size_t)li * TP + p] : 0.f, li + 1 < hl ? Db[(size_t)(li + 1) * TP + p] : 0.f);
-          lp.v = make_float2(l[j], l[j + 1]);
-          const Pair<float> e = keep_pair(d, lp, a.zt);
-          c[j] = li < hl ? e.v.x : 0.f;
-          c[j + 1] = li + 1 < hl ? e.v.y : 0.f;
-          den = __fmaf_rn(d.v.x, d.v.x, den);
-          den = __fmaf_rn(d.v.y, d.v.y, den);
-        }
-        if (om >= 0) {  // I x J entries: the core's values (U = (D - S)(I, J))
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < 16; j += 2) {
             const int li = c0 + j;
-            if (li < hl) c[j] = (float)s.U[(int64_t)(l0 + li) * s.u_ls + (int64_t)om * s.u_ps];
+            Pair<float> d, lp;
+            d.v = make_float2(li < hl ? Db[(size_t)li * TP + p] : 0.f,
+                              li + 1 < hl ? Db[(size_t)(li + 1) * TP + p] : 0.f);
+            lp.v = make_float2(l[j], l[j + 1]);
+            const Pair<float> e = keep_pair(d, lp, a.zt);
+            c[j] = li < hl ? e.v.x : 0.f;
+            c[j + 1] = li + 1 < hl ? e.v.y : 0.f;
+            den = __fmaf_rn(d.v.x, d.v.x, den);
+            den = __fmaf_rn(d.v.y, d.v.y, den);
           }
-        }
+          if (om >= 0) {  // I x J entries: the core's values (U = (D - S)(I, J))
 #pragma unroll
-        for (int j = 0; j < 16; ++j) cl[j] = s5_lo(c[j]);
-        umma::st16(T + lane_off + TL(i) + c0, c);
-        umma::st16(T + lane_off + TC + c0, cl);
+            for (int j = 0; j < 16; ++j) {
+              const int li = c0 + j;
+              if (li < hl) c[j] = (float)s.U[(int64_t)(l0 + li) * s.u_ls + (int64_t)om * s.u_ps];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) cl[j] = s5_lo(c[j]);
+          umma::st16(T + lane_off + TL(i) + c0, c);
+          umma::st16(T + lane_off + TC + c0, cl);
+        }
+        umma::st_wait();
+        umma::fence_before();
+        __syncwarp();
+        if (lane == 0) umma::bar_arrive(bar(b, kC + g));
       }
-      umma::st_wait();
-      umma::fence_before();
-      __syncwarp();
-      if (lane == 0) umma::bar_arrive(&cready[g_]);
       S5PH(2);
-      // ---- residual of the previous tile (same strip)
-      if (t_prev >= 0) phase_b(i - 1, t_prev, q_prev, den_prev);
+      if (pending) phase_b(i - 1, den_prev);  // its barrier also frees D buffer b
+      else named_bar(1, NEW * 32);
       S5PH(3);
-      // D buffer b is free once every warp is past Phase I/II of t (the
-      // residual's barrier, or this one): tile t + 2 loads into it
-      if (t_prev < 0) named_bar(1, NW * 32);
-      if (t + 2 * ncl < total) issue_loads(t + 2 * ncl, b);
-      if (g_ == 0) {
-        // B' of the next tile (same strip): its MMA1 runs during this epilogue
-        if (next_same) {
-          umma::bar_wait(&full[b ^ 1], (uint32_t)(((i + 1) >> 1) & 1));
-          build_bprime(i + 1, b ^ 1);
-        }
-        S5PH(4);
-        // ---- factor epilogue: partials -> owner rank -> sum, override, write -> all ranks
-        umma::bar_wait(ffull, ph);
-        umma::fence_after();
-        float v[32];
-        s5_ld32(T + lane_off + TF, v);
-        umma::ld_wait();
-        float pf[XF];
-#pragma unroll
-        for (int k = 0; k < XF; ++k) pf[k] = (k < R && hl > 0) ? __fadd_rn(v[k], v[16 + k]) : 0.f;
-        // my partial of position p -> rank q_ (the owner of positions 32 q_ ..), slot [rank]
-        float* xin_slot = Xin + (((size_t)b * CS + rank) * 32 + lane) * XF;
-#pragma unroll
-        for (int k = 0; k < XF; k += 4)
-          st_cluster_v4(umma::smem_u32(xin_slot + k), (uint32_t)q_, make_float4(pf[k], pf[k + 1], pf[k + 2], pf[k + 3]));
-        arrive_cluster(&xin[b], (uint32_t)q_);
-        S5PH(5);
-        const uint32_t xph = (uint32_t)((i >> 1) & 1);  // xin/xout[b] complete every other tile
-        if (q_ == (int)rank) {  // owner: the four partials in rank order, override, write, broadcast
-          wait_cluster(&xin[b], xph);
-          float f[XF];
-#pragma unroll
-          for (int k = 0; k < XF; ++k) f[k] = Xin[(((size_t)b * CS + 0) * 32 + lane) * XF + k];
-#pragma unroll
-          for (int rr = 1; rr < CS; ++rr)
-#pragma unroll
-            for (int k = 0; k < XF; ++k) f[k] = __fadd_rn(f[k], Xin[(((size_t)b * CS + rr) * 32 + lane) * XF + k]);
-          if (om >= 0) {
-#pragma unroll
-            for (int k = 0; k < R; ++k) f[k] = s.otherF[(int64_t)om * R + k];
-          }
-          if (inpos) {
-#pragma unroll
-            for (int k = 0; k < R; ++k) s.Fnew[(int64_t)k * s.ldf + x0 + p] = f[k];
-          }
-          float* xo = Xout + ((size_t)b * TP + p) * XF;
-          for (uint32_t rr = 0; rr < CS; ++rr) {
-#pragma unroll
-            for (int k = 0; k < XF; k += 4)
-              st_cluster_v4(umma::smem_u32(xo + k), rr, make_float4(f[k], f[k + 1], f[k + 2], f[k + 3]));
-            arrive_cluster(&xout[b], rr);
-          }
-        }
-        // final values of my positions (owner rank q_) -> -F' = -[F | F | F_lo | 0]
-        wait_cluster(&xout[b], xph);
-        S5PH(6);
-        {
-          const float* xo = Xout + ((size_t)b * TP + p) * XF;
-          float nv[KC];
-#pragma unroll
-          for (int k = 0; k < KC; ++k) nv[k] = 0.f;
-#pragma unroll
-          for (int tt = 0; tt < R; ++tt) {
-            const float f = xo[tt];
-            nv[tt] = -f;
-            nv[R + tt] = -f;
-            nv[2 * R + tt] = -s5_lo(f);
-          }
-          s5_st32(T + lane_off + TB(i), nv);
-          umma::st_wait();
-          umma::fence_before();
-          __syncwarp();
-          if (lane == 0) umma::bar_arrive(fready);
-        }
-      }
+      if (i + 2 < ntl) issue_loads(i + 2);
+      S5PH(4);
+      pending = true;
       den_prev = den;
-      t_prev = t;
-      q_prev = q;
     }
-    if (t_prev >= 0) phase_b(i - 1, t_prev, q_prev, den_prev);
+    if (pending) phase_b(ntl - 1, den_prev);
     if (rec)
       for (int k = 0; k < 8; ++k) a.dbg[k] += tpc[k];
 #undef S5PH
+  } else {
+    // ================= epilogue warps (one per lane quadrant): B' of the next
+    // tile, then the factor epilogue of this one
+    const int q_ = w & 3;
+    const int p = 32 * q_ + lane;
+    const uint32_t lane_off = (uint32_t)(32 * q_) << 16;
+    // B' = [B | B | B_lo | 0] of tile j at position p (K-major SW128 row p), once MMA1(j - 2) read the slot
+    auto build_bprime = [&](int j) {
+      const int tj = tile_of(j), bj = j & 1;
+      const int qj = strip_of(tj);
+      const StripDesc<float>& sj = a.s[qj];
+      const int xj = (tj - (qj ? tiles0 : 0)) * TP;
+      const bool in_j = xj + p < sj.npos;
+      if (j >= 2) umma::bar_wait(bar(bj, kL), xph(j - 2));
+      float v[KC];
+#pragma unroll
+      for (int k = 0; k < KC; ++k) v[k] = 0.f;
+#pragma unroll
+      for (int tt = 0; tt < R; ++tt) {
+        const float x = in_j ? sj.Bold[(int64_t)tt * sj.ldb + xj + p] : 0.f;
+        v[tt] = x;
+        v[R + tt] = x;
+        v[2 * R + tt] = s5_lo(x);
+      }
+      unsigned char* row = Bp + (size_t)bj * (TP * KC * 4);
+#pragma unroll
+      for (int c4 = 0; c4 < KC / 4; ++c4)
+        *reinterpret_cast<float4*>(row + s5_kmaj(p, 4 * c4)) =
+            make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+      umma::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) umma::bar_arrive(bar(bj, kBready));
+    };
+    if (ntl > 0) build_bprime(0);
+    for (int i = 0; i < ntl; ++i) {
+      const int t = tile_of(i), b = i & 1;
+      const int q = strip_of(t);
+      const StripDesc<float>& s = a.s[q];
+      const int x0 = (t - (q ? tiles0 : 0)) * TP;
+      const bool inpos = x0 + p < s.npos;
+      int l0, hl;
+      line_range(q, l0, hl);
+      if (i + 1 < ntl) build_bprime(i + 1);
+      // ---- factor epilogue: partials -> owner rank -> sum, override, write -> all ranks
+      const int om = inpos ? s.omap[x0 + p] : -1;
+      umma::bar_wait(bar(b, kF), xph(i));
+      umma::fence_after();
+      float v[32];
+      s5_ld32(T + lane_off + TF(i), v);
+      umma::ld_wait();
+      umma::fence_before();
+      float pf[XF];
+#pragma unroll
+      for (int k = 0; k < XF; ++k) pf[k] = (k < R && hl > 0) ? __fadd_rn(v[k], v[16 + k]) : 0.f;
+      float* xin_slot = Xin + (((size_t)b * CS + rank) * 32 + lane) * XF;
+#pragma unroll
+      for (int k = 0; k < XF; k += 4)
+        st_cluster_v4(umma::smem_u32(xin_slot + k), (uint32_t)q_, make_float4(pf[k], pf[k + 1], pf[k + 2], pf[k + 3]));
+      arrive_cluster(bar(b, kXin), (uint32_t)q_);
+      if (q_ == (int)rank) {  // owner of positions 32 q_ ..: the four partials in rank order
+        wait_cluster(bar(b, kXin), xph(i));
+        float f[XF];
+#pragma unroll
+        for (int k = 0; k < XF; ++k) f[k] = Xin[(((size_t)b * CS + 0) * 32 + lane) * XF + k];
+#pragma unroll
+        for (int rr = 1; rr < CS; ++rr)
+#pragma unroll
+          for (int k = 0; k < XF; ++k) f[k] = __fadd_rn(f[k], Xin[(((size_t)b * CS + rr) * 32 + lane) * XF + k]);
+        if (om >= 0) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) f[k] = s.otherF[(int64_t)om * R + k];
+        }
+        if (inpos) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) s.Fnew[(int64_t)k * s.ldf + x0 + p] = f[k];
+        }
+        float* xo = Xout + ((size_t)b * TP + p) * XF;
+        for (uint32_t rr = 0; rr < CS; ++rr) {
+#pragma unroll
+          for (int k = 0; k < XF; k += 4)
+            st_cluster_v4(umma::smem_u32(xo + k), rr, make_float4(f[k], f[k + 1], f[k + 2], f[k + 3]));
+          arrive_cluster(bar(b, kXout), rr);
+        }
+      }
+      wait_cluster(bar(b, kXout), xph(i));
+      // -F' = -[F | F | F_lo | 0] into TB(i), once MMA3(i - 2) read the slot
+      if (i >= 2) umma::bar_wait(bar(b, kB), xph(i - 2));
+      {
+        const float* xo = Xout + ((size_t)b * TP + p) * XF;
+        float nv[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) nv[k] = 0.f;
+#pragma unroll
+        for (int tt = 0; tt < R; ++tt) {
+          const float f = xo[tt];
+          nv[tt] = -f;
+          nv[R + tt] = -f;
+          nv[2 * R + tt] = -s5_lo(f);
+        }
+        s5_st32(T + lane_off + TB(i), nv);
+        umma::st_wait();
+        umma::fence_before();
+        __syncwarp();
+        if (lane == 0) umma::bar_arrive(bar(b, kFready));
+      }
+    }
   }
   __syncwarp();
   // no CTA leaves while a peer may still store into its shared memory or arrive on its barriers
@@ -586,7 +605,7 @@ bool strips5_supported(const StripsArgs<float>& a, int R) {
     const StripDesc<float>& s = a.s[q];
     if (s.tiles == 0) continue;
     if (!s.bulk_ok || s.mode != kStripFull || s.pos_stride != 1 || !s.U) return false;
-    if (s.nk > s5::CS * s5::ML) return false;
+    if (s.nk > s5::CS * s5::HMAX) return false;
     if (((uintptr_t)s.Bold & 15) || (s.ldb & 3) || ((uintptr_t)s.omap & 15)) return false;
   }
   return true;

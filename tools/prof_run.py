@@ -47,8 +47,7 @@ for i in range(a.solves):
     sn = ["stage_wait", "pass1", "reduce", "override+write", "pass2", "sync+issue", "lvec+loop"]
     ver = os.environ.get("IRCUR_STRIPS_VER", "5")
     if ver == "5":
-        sn = ["prefetch", "wait_full", "Bprime+MMA1", "phaseA", "MMA2_wait", "partial+cluster_bar",
-              "dsmem+Fprime+MMA3", "phaseB+end"]
+        sn = ["fresh+wait_full", "wait_MMA1", "phaseA", "residual(prev)", "issue_loads", "-", "-", "loop"]
     elif ver != "1":
         sn = ["stage(issue+wait)", "pass1", "sync_after_pass1", "reduce+write+sync", "pass2", "final_sync", "loop"]
     nph = 8 if ver == "5" else 7
