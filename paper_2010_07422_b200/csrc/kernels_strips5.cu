@@ -47,6 +47,10 @@
 #include "launchers.cuh"
 #include "umma.cuh"
 
+#ifndef S5_PROF_EPI
+#define S5_PROF_EPI 0  // 1: the per-phase clock totals follow epilogue warp 0 instead of elementwise thread 0
+#endif
+
 namespace ircur {
 
 namespace s5 {
@@ -67,12 +71,13 @@ constexpr size_t O_D = 0;                                   // 2 D tiles
 constexpr size_t O_AOP = (O_D + 2 * D_BYTES + 1023) & ~(size_t)1023;  // A' [ML][KC] K-major SW128
 constexpr size_t O_ROP = O_AOP + (size_t)ML * KC * 4;       // Res'
 constexpr size_t O_WOP = O_ROP + (size_t)ML * KC * 4;       // W'  [32 rows][ML lines] K-major SW128
-constexpr size_t O_BP = O_WOP + (size_t)32 * ML * 4;        // 2 x B' [TP][KC] K-major SW128 (MMA1 A operand)
-constexpr size_t O_OM = O_BP + 2 * (size_t)TP * KC * 4;     // 2 x omap [TP]
+constexpr size_t O_BP = O_WOP + (size_t)32 * ML * 4;        // B' [TP][KC] K-major SW128 (MMA1 A operand)
+constexpr size_t O_BST = O_BP + (size_t)TP * KC * 4;        // 2 x Bold staging [RMAX][TP] (cp.async)
+constexpr size_t O_OM = O_BST + 2 * (size_t)RMAX * TP * 4;  // 2 x omap [TP]
 constexpr int XF = 12;                                      // floats per position in the exchange (R <= 10)
 constexpr size_t O_XIN = O_OM + 2 * TP * 4;                 // [2][CS src][32 own pos][XF] partials received
 constexpr size_t O_XOUT = O_XIN + (size_t)2 * CS * 32 * XF * 4;  // [2][TP][XF] final factor values
-constexpr size_t O_WS = O_XOUT + (size_t)2 * TP * XF * 4;  // per-warp (den, res) doubles
+constexpr size_t O_WS = O_XOUT + (size_t)2 * TP * XF * 4;  // per-warp den (elementwise) / res (epilogue)
 constexpr size_t O_LOFF = O_WS + (size_t)NEW * 2 * 8;       // line offsets (int64) [2 strips][ML]
 constexpr size_t O_BAR = O_LOFF + (size_t)2 * ML * 8;
 // per tile parity: full lfull ffull bfull bready fready rdone xin xout cready[4]; + opsready
@@ -149,6 +154,24 @@ __device__ __forceinline__ void arrive_cluster(uint64_t* local_bar, uint32_t ran
   asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(umma::smem_u32(local_bar)), "r"(rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// arrive without release semantics: a preceding fence_cluster() orders all of
+// this thread's earlier stores (one fence for several destinations)
+__device__ __forceinline__ void arrive_cluster_relaxed(uint64_t* local_bar, uint32_t rank) {
+  uint32_t remote;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(umma::smem_u32(local_bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+// 16 bytes into a peer's (or this CTA's) shared memory; the bytes complete
+// the transaction count of the peer's mbarrier (no fence, no separate arrive)
+__device__ __forceinline__ void st_async_v4(uint32_t local_saddr, uint64_t* local_bar, uint32_t rank, float4 v) {
+  uint32_t ra, rb;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_saddr), "r"(rank));
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(umma::smem_u32(local_bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(ra),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rb)
+               : "memory");
+}
 __device__ __forceinline__ void wait_cluster(uint64_t* b, uint32_t parity) {
   uint32_t ok = 0;
   while (!ok)
@@ -171,6 +194,7 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
   unsigned char* Rop = sm + O_ROP;
   unsigned char* Wop = sm + O_WOP;
   unsigned char* Bp = sm + O_BP;
+  float* Bst = reinterpret_cast<float*>(sm + O_BST);
   int* Om = reinterpret_cast<int*>(sm + O_OM);
   float* Xin = reinterpret_cast<float*>(sm + O_XIN);
   float* Xout = reinterpret_cast<float*>(sm + O_XOUT);
@@ -197,9 +221,9 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       umma::bar_init(bar(b, kB), 1);
       umma::bar_init(bar(b, kBready), 4);
       umma::bar_init(bar(b, kFready), 4);
-      umma::bar_init(bar(b, kRdone), NEW);
-      umma::bar_init(bar(b, kXin), CS * 32);
-      umma::bar_init(bar(b, kXout), CS * 32);
+      umma::bar_init(bar(b, kRdone), NEP);
+      umma::bar_init(bar(b, kXin), 1);   // armed by the owner warp: expect 4 ranks x 32 positions
+      umma::bar_init(bar(b, kXout), 4);  // armed by each epilogue warp: its 32 positions
       for (int g = 0; g < 4; ++g) umma::bar_init(bar(b, kC + g), 4);
     }
     umma::bar_init(opsready, 1);
@@ -236,7 +260,7 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
 
   if (issuer_warp) {
     // ================= MMA issue (one thread): three in-order streams, polled
-    //   MMA1(n1): B' built, TL slot free (residual of n1 - 2 read), after MMA2(n1 - 1)
+    //   MMA1(n1): B' built, TL slot free (residual of n1 - 2 read)
     //   MMA2(n2): line groups of c / c_lo written, after MMA1(n2), TF slot read (MMA3(n2 - 2) issued)
     //   MMA3(n3): -F' written, after MMA2(n3)
     if (lane == 0) {
@@ -247,12 +271,12 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       const uint32_t bp0 = umma::smem_u32(Bp);
       int n1 = 0, n2 = 0, g2 = 0, n3 = 0, nfresh = 0;
       while (n3 < ntl) {
-        if (n1 < ntl && n1 <= n2 && umma::bar_try(bar(n1 & 1, kBready), xph(n1)) &&
+        if (n1 < ntl && umma::bar_try(bar(n1 & 1, kBready), xph(n1)) &&
             (n1 < 2 || umma::bar_try(bar(n1 & 1, kRdone), xph(n1 - 2))) &&
             (!fresh_at(n1) || umma::bar_try(opsready, (uint32_t)(nfresh & 1)))) {
           if (fresh_at(n1)) ++nfresh;
           umma::fence_after();
-          const uint32_t bpa = bp0 + (uint32_t)(n1 & 1) * (TP * KC * 4);
+          const uint32_t bpa = bp0;
           for (int k = 0; k < KC / 8; ++k)
             umma::mma_ss(T + TL(n1), umma::smem_desc(bpa + 32 * k, 16, 1024, umma::kSwizzle128),
                          umma::smem_desc(a_op + 32 * k, 16, 1024, umma::kSwizzle128), idesc_r, k > 0);
@@ -298,7 +322,7 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
     const int p = 32 * q_ + lane;
     const uint32_t lane_off = (uint32_t)(32 * q_) << 16;
     const int et = tid;  // 0 .. NEW * 32 - 1
-    const bool rec = a.dbg && blockIdx.x == 0 && tid == 0;
+    const bool rec = a.dbg && blockIdx.x == 0 && tid == 0 && !S5_PROF_EPI;
     long long tpc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tq = clock64();
 #define S5PH(k) do { if (rec) { const long long _t = clock64(); tpc[k] += _t - tq; tq = _t; } } while (0)
@@ -314,21 +338,36 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       int l0, hl;
       line_range(q, l0, hl);
       float* dst = Dt + (size_t)b * HMAX * TP;
-      const bool whole = x0 + TP <= s.npos;
-      const int nch = hl * (TP / 4);
-      for (int e = et; e < nch; e += NEW * 32) {
-        const int li = e >> 5, ch = e & 31;
+      if (x0 + TP <= s.npos) {  // whole tile: fixed chunk per thread, lines 16 apart
+        const int ch = et & 31;
+        const float* src0 = s.src + x0 + ch * 4;
+        float* dst0 = dst + ch * 4;
+        for (int li = et >> 5; li < hl; li += NEW)
+          umma::cp_async16(dst0 + (size_t)li * TP, src0 + loff[q * ML + li], 16u);
+      } else {
+        const int nch = hl * (TP / 4);
+        for (int e = et; e < nch; e += NEW * 32) {
+          const int li = e >> 5, ch = e & 31;
+          const int pos = x0 + ch * 4;
+          const int rem = s.npos - pos;
+          const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
+          umma::cp_async16(dst + (size_t)li * TP + ch * 4, s.src + loff[q * ML + li] + (bytes ? pos : x0),
+                           (uint32_t)bytes);
+        }
+      }
+      if (et < R * (TP / 4)) {  // the old factor's rows at these positions (for B')
+        const int tt = et >> 5, ch = et & 31;
         const int pos = x0 + ch * 4;
         const int rem = s.npos - pos;
-        const int bytes = whole ? 16 : (rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0));
-        umma::cp_async16(dst + (size_t)li * TP + ch * 4, s.src + loff[q * ML + li] + (bytes ? pos : x0),
+        const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
+        umma::cp_async16(Bst + ((size_t)b * RMAX + tt) * TP + ch * 4, s.Bold + (int64_t)tt * s.ldb + (bytes ? pos : x0),
                          (uint32_t)bytes);
-      }
-      if (et < TP / 4) {
-        const int pos = x0 + et * 4;
+      } else if (et >= 480 && et < 480 + TP / 4) {
+        const int c4 = et - 480;
+        const int pos = x0 + c4 * 4;
         const int rem = s.npos - pos;
         const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
-        umma::cp_async16(Om + b * TP + et * 4, s.omap + (bytes ? pos : x0), (uint32_t)bytes);
+        umma::cp_async16(Om + b * TP + c4 * 4, s.omap + (bytes ? pos : x0), (uint32_t)bytes);
       }
       umma::cp_async_arrive(bar(b, kFull));
     };
@@ -361,50 +400,35 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       }
       umma::fence_async_smem();
     };
-    // residual of tile i (TL(i) holds r = c - Lnew after MMA3) and its per-tile sums
-    auto phase_b = [&](int i, float den) {
-      const int t = tile_of(i), q = strip_of(t);
-      float res = 0.f;
-      umma::bar_wait(bar(i & 1, kB), xph(i));
-      umma::fence_after();
+    // B' = [B | B | B_lo | 0] of tile j (K-major SW128 row p), group-0 warps.
+    // The slot is free: MMA1(j - 1) completed before Phase I/II of j - 1.
+    auto build_bprime = [&](int j) {
+      const int bj = j & 1;
+      umma::bar_wait(bar(bj, kFull), xph(j));  // Bold rows of tile j landed
+      const float* Bb = Bst + (size_t)bj * RMAX * TP;
+      float v[KC];
 #pragma unroll
-      {
-        float r[32];
-        s5_ld32(T + lane_off + TL(i) + 32 * g_, r);
-        umma::ld_wait();
+      for (int k = 0; k < KC; ++k) v[k] = 0.f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) res = __fmaf_rn(r[j], r[j], res);
+      for (int tt = 0; tt < R; ++tt) {
+        const float x = Bb[tt * TP + p];
+        v[tt] = x;
+        v[R + tt] = x;
+        v[2 * R + tt] = s5_lo(x);
       }
-      umma::fence_before();
+#pragma unroll
+      for (int c4 = 0; c4 < KC / 4; ++c4)
+        *reinterpret_cast<float4*>(Bp + s5_kmaj(p, 4 * c4)) =
+            make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+      umma::fence_async_smem();
       __syncwarp();
-      if (lane == 0) umma::bar_arrive(bar(i & 1, kRdone));  // TL(i) may be overwritten (MMA1 of i + 2)
-      const double dd = warp_sum((double)den), rd = warp_sum((double)res);
-      if (lane == 0) {
-        Ws[2 * w] = dd;
-        Ws[2 * w + 1] = rd;
-      }
-      named_bar(1, NEW * 32);
-      if (tid == 0) {
-        double sd = 0.0, sr = 0.0;
-        for (int ww = 0; ww < NEW; ++ww) {
-          sd += Ws[2 * ww];
-          sr += Ws[2 * ww + 1];
-        }
-        double4 pr;
-        pr.x = q ? 0.0 : sd;
-        pr.y = q ? 0.0 : sr;
-        pr.z = q ? sd : 0.0;
-        pr.w = q ? sr : 0.0;
-        *reinterpret_cast<double4*>(a.partials + 4 * ((size_t)t * CS + rank)) = pr;
-      }
-      named_bar(2, NEW * 32);  // Ws read before the next tile's sums
+      if (lane == 0) umma::bar_arrive(bar(bj, kBready));
     };
 
     if (ntl > 0) issue_loads(0);
     if (ntl > 1) issue_loads(1);
+    if (ntl > 0 && g_ == 0) build_bprime(0);
     int cur = -1;
-    bool pending = false;
-    float den_prev = 0.f;
     for (int i = 0; i < ntl; ++i) {
       const int t = tile_of(i), b = i & 1;
       const int q = strip_of(t);
@@ -413,11 +437,8 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       int l0, hl;
       line_range(q, l0, hl);
       S5PH(7);
-      if (q != cur) {  // new strip: drain, then its operands (no MMA reads them now)
-        if (pending) {
-          phase_b(i - 1, den_prev);
-          pending = false;
-        }
+      if (q != cur) {  // new strip: once every MMA of the previous one completed, its operands
+        if (i > 0) umma::bar_wait(bar((i - 1) & 1, kB), xph(i - 1));
         build_strip_ops(q);
         named_bar(1, NEW * 32);
         if (tid == 0) umma::bar_arrive(opsready);
@@ -426,8 +447,6 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       umma::bar_wait(bar(b, kFull), xph(i));
       S5PH(0);
       const float* Db = Dt + (size_t)b * HMAX * TP;
-      const bool inpos = x0 + p < s.npos;
-      const int om = inpos ? Om[b * TP + p] : -1;
       // ---- Phase I/II (solver.py:375-382): l -> c in TMEM, c_lo beside it
       float den = 0.f;
       umma::bar_wait(bar(b, kL), xph(i));
@@ -442,6 +461,7 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
           umma::ld16(T + lane_off + TL(i) + c0, l);
           umma::ld_wait();
           float c[16], cl[16];
+          if (hh == 0 && i > 0) umma::bar_wait(bar((i - 1) & 1, kF), xph(i - 1));  // MMA2(i - 1) read c_lo
 #pragma unroll
           for (int j = 0; j < 16; j += 2) {
             const int li = c0 + j;
@@ -455,13 +475,6 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
             den = __fmaf_rn(d.v.x, d.v.x, den);
             den = __fmaf_rn(d.v.y, d.v.y, den);
           }
-          if (om >= 0) {  // I x J entries: the core's values (U = (D - S)(I, J))
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int li = c0 + j;
-              if (li < hl) c[j] = (float)s.U[(int64_t)(l0 + li) * s.u_ls + (int64_t)om * s.u_ps];
-            }
-          }
 #pragma unroll
           for (int j = 0; j < 16; ++j) cl[j] = s5_lo(c[j]);
           umma::st16(T + lane_off + TL(i) + c0, c);
@@ -473,15 +486,24 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
         if (lane == 0) umma::bar_arrive(bar(b, kC + g));
       }
       S5PH(2);
-      if (pending) phase_b(i - 1, den_prev);  // its barrier also frees D buffer b
-      else named_bar(1, NEW * 32);
+      // ---- den of tile i (per tile, warps in order); the barrier also frees D buffer b
+      {
+        const double dd = warp_sum((double)den);
+        if (lane == 0) Ws[w] = dd;
+        named_bar(1, NEW * 32);
+        if (tid == 0) {
+          double sd = 0.0;
+          for (int ww = 0; ww < NEW; ++ww) sd += Ws[ww];
+          double* pr = a.partials + 4 * ((size_t)t * CS + rank);
+          pr[q ? 2 : 0] = sd;
+          pr[q ? 0 : 2] = 0.0;
+        }
+      }
       S5PH(3);
+      if (g_ == 0 && i + 1 < ntl) build_bprime(i + 1);  // (after thread 0 read Ws: MMA1(i + 1) gates the others)
       if (i + 2 < ntl) issue_loads(i + 2);
       S5PH(4);
-      pending = true;
-      den_prev = den;
     }
-    if (pending) phase_b(ntl - 1, den_prev);
     if (rec)
       for (int k = 0; k < 8; ++k) a.dbg[k] += tpc[k];
 #undef S5PH
@@ -491,34 +513,17 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
     const int q_ = w & 3;
     const int p = 32 * q_ + lane;
     const uint32_t lane_off = (uint32_t)(32 * q_) << 16;
-    // B' = [B | B | B_lo | 0] of tile j at position p (K-major SW128 row p), once MMA1(j - 2) read the slot
-    auto build_bprime = [&](int j) {
-      const int tj = tile_of(j), bj = j & 1;
-      const int qj = strip_of(tj);
-      const StripDesc<float>& sj = a.s[qj];
-      const int xj = (tj - (qj ? tiles0 : 0)) * TP;
-      const bool in_j = xj + p < sj.npos;
-      if (j >= 2) umma::bar_wait(bar(bj, kL), xph(j - 2));
-      float v[KC];
-#pragma unroll
-      for (int k = 0; k < KC; ++k) v[k] = 0.f;
-#pragma unroll
-      for (int tt = 0; tt < R; ++tt) {
-        const float x = in_j ? sj.Bold[(int64_t)tt * sj.ldb + xj + p] : 0.f;
-        v[tt] = x;
-        v[R + tt] = x;
-        v[2 * R + tt] = s5_lo(x);
+    const bool rec = a.dbg && blockIdx.x == 0 && tid == NEW * 32 && S5_PROF_EPI;
+    long long tpc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
+#define S5PE(k) do { if (rec) { const long long _t = clock64(); tpc[k] += _t - tq; tq = _t; } } while (0)
+    constexpr uint32_t kXinBytes = CS * 32 * XF * 4, kXoutBytes = 32 * XF * 4;
+    if (lane == 0)
+      for (int bb = 0; bb < 2 && bb < ntl; ++bb) {
+        if (q_ == (int)rank) umma::arrive_expect_tx(bar(bb, kXin), kXinBytes);
+        umma::arrive_expect_tx(bar(bb, kXout), kXoutBytes);
       }
-      unsigned char* row = Bp + (size_t)bj * (TP * KC * 4);
-#pragma unroll
-      for (int c4 = 0; c4 < KC / 4; ++c4)
-        *reinterpret_cast<float4*>(row + s5_kmaj(p, 4 * c4)) =
-            make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
-      umma::fence_async_smem();
-      __syncwarp();
-      if (lane == 0) umma::bar_arrive(bar(bj, kBready));
-    };
-    if (ntl > 0) build_bprime(0);
+    double* Wse = Ws + NEW;  // epilogue warps' per-tile residual sums
     for (int i = 0; i < ntl; ++i) {
       const int t = tile_of(i), b = i & 1;
       const int q = strip_of(t);
@@ -527,11 +532,12 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       const bool inpos = x0 + p < s.npos;
       int l0, hl;
       line_range(q, l0, hl);
-      if (i + 1 < ntl) build_bprime(i + 1);
+      S5PE(7);
       // ---- factor epilogue: partials -> owner rank -> sum, override, write -> all ranks
       const int om = inpos ? s.omap[x0 + p] : -1;
       umma::bar_wait(bar(b, kF), xph(i));
       umma::fence_after();
+      S5PE(1);
       float v[32];
       s5_ld32(T + lane_off + TF(i), v);
       umma::ld_wait();
@@ -542,10 +548,12 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       float* xin_slot = Xin + (((size_t)b * CS + rank) * 32 + lane) * XF;
 #pragma unroll
       for (int k = 0; k < XF; k += 4)
-        st_cluster_v4(umma::smem_u32(xin_slot + k), (uint32_t)q_, make_float4(pf[k], pf[k + 1], pf[k + 2], pf[k + 3]));
-      arrive_cluster(bar(b, kXin), (uint32_t)q_);
+        st_async_v4(umma::smem_u32(xin_slot + k), bar(b, kXin), (uint32_t)q_,
+                    make_float4(pf[k], pf[k + 1], pf[k + 2], pf[k + 3]));
+      S5PE(2);
       if (q_ == (int)rank) {  // owner of positions 32 q_ ..: the four partials in rank order
         wait_cluster(bar(b, kXin), xph(i));
+        S5PE(3);
         float f[XF];
 #pragma unroll
         for (int k = 0; k < XF; ++k) f[k] = Xin[(((size_t)b * CS + 0) * 32 + lane) * XF + k];
@@ -553,23 +561,26 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
         for (int rr = 1; rr < CS; ++rr)
 #pragma unroll
           for (int k = 0; k < XF; ++k) f[k] = __fadd_rn(f[k], Xin[(((size_t)b * CS + rr) * 32 + lane) * XF + k]);
+        __syncwarp();
+        if (lane == 0 && i + 2 < ntl) umma::arrive_expect_tx(bar(b, kXin), kXinBytes);  // tile i + 2
         if (om >= 0) {
 #pragma unroll
           for (int k = 0; k < R; ++k) f[k] = s.otherF[(int64_t)om * R + k];
-        }
-        if (inpos) {
-#pragma unroll
-          for (int k = 0; k < R; ++k) s.Fnew[(int64_t)k * s.ldf + x0 + p] = f[k];
         }
         float* xo = Xout + ((size_t)b * TP + p) * XF;
         for (uint32_t rr = 0; rr < CS; ++rr) {
 #pragma unroll
           for (int k = 0; k < XF; k += 4)
-            st_cluster_v4(umma::smem_u32(xo + k), rr, make_float4(f[k], f[k + 1], f[k + 2], f[k + 3]));
-          arrive_cluster(bar(b, kXout), rr);
+            st_async_v4(umma::smem_u32(xo + k), bar(b, kXout), rr, make_float4(f[k], f[k + 1], f[k + 2], f[k + 3]));
+        }
+        if (inpos) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) s.Fnew[(int64_t)k * s.ldf + x0 + p] = f[k];
         }
       }
+      S5PE(4);
       wait_cluster(bar(b, kXout), xph(i));
+      S5PE(5);
       // -F' = -[F | F | F_lo | 0] into TB(i), once MMA3(i - 2) read the slot
       if (i >= 2) umma::bar_wait(bar(b, kB), xph(i - 2));
       {
@@ -584,13 +595,47 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
           nv[R + tt] = -f;
           nv[2 * R + tt] = -s5_lo(f);
         }
+        __syncwarp();
+        if (lane == 0 && i + 2 < ntl) umma::arrive_expect_tx(bar(b, kXout), kXoutBytes);  // tile i + 2
         s5_st32(T + lane_off + TB(i), nv);
         umma::st_wait();
         umma::fence_before();
         __syncwarp();
         if (lane == 0) umma::bar_arrive(bar(b, kFready));
       }
+      S5PE(6);
+      // ---- residual r = c - Lnew of position p over this CTA's lines (solver.py:393-400)
+      umma::bar_wait(bar(b, kB), xph(i));
+      umma::fence_after();
+      S5PE(0);
+      float res = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < ML; c0 += 32) {
+        if (c0 < hl) {
+          float r[32];
+          s5_ld32(T + lane_off + TL(i) + c0, r);
+          umma::ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) res = __fmaf_rn(r[j], r[j], res);
+        }
+      }
+      umma::fence_before();
+      __syncwarp();
+      if (lane == 0) umma::bar_arrive(bar(b, kRdone));  // TL(i) may be overwritten (MMA1 of i + 2)
+      const double rd = warp_sum((double)res);
+      if (lane == 0) Wse[q_] = rd;
+      named_bar(3, NEP * 32);
+      if (q_ == 0 && lane == 0) {
+        const double sr = ((Wse[0] + Wse[1]) + Wse[2]) + Wse[3];
+        double* pr = a.partials + 4 * ((size_t)t * CS + rank);
+        pr[q ? 3 : 1] = sr;
+        pr[q ? 1 : 3] = 0.0;
+      }
+      named_bar(4, NEP * 32);  // Wse read before the next tile's sums
     }
+    if (rec)
+      for (int k = 0; k < 8; ++k) a.dbg[k] += tpc[k];
+#undef S5PE
   }
   __syncwarp();
   // no CTA leaves while a peer may still store into its shared memory or arrive on its barriers
