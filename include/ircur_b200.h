@@ -250,6 +250,12 @@ int ircur_debug_counter(ircur_ctx_t ctx, int which, long long* value);
  * Callers that run several solves concurrently on one GPU pass 0: the
  * overlapped loop sizes its strip grid for a GPU of its own. */
 int ircur_set_overlap(ircur_ctx_t ctx, int mode);
+/* Stop tolerance of the following ircur_iterate calls (ircur_run and
+ * ircur_solve take it as an argument).  fp32 strips run on the tensor cores
+ * (kernels_strips5.cu) only when eps >= 1e-6 (IRCUR_S5_MIN_EPS): their
+ * 3-term tf32 products put the residual's floor near 3e-7, so tighter
+ * tolerances take the FFMA kernel, whose floor is fp32 round-off. */
+int ircur_set_target_eps(ircur_ctx_t ctx, double eps);
 /* Overlapped, profiled run: per iteration k, ms[5k..5k+4] = start and end
  * of the chain (core .. SVD), start and end of the strips, and the end of
  * the sampled-factor kernel of k, relative to the first chain's start

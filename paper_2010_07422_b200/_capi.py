@@ -61,6 +61,7 @@ PROTOTYPES = [
     ("ircur_debug_counter", _i, [_vp, _i, C.POINTER(C.c_longlong)]),
     ("ircur_get_timeline", _i, [_vp, _i, _pf]),
     ("ircur_set_overlap", _i, [_vp, _i]),
+    ("ircur_set_target_eps", _i, [_vp, _d]),
     ("ircur_get_profile", _i, [_vp, _i, _pi, C.POINTER(C.c_longlong), _pf, _pf, _pf, _pf]),
     ("ircur_get_svd_steps", _i, [_vp, _i, _pi]),
     ("ircur_get_svd_phase_cycles", _i, [_vp, C.POINTER(C.c_longlong), _i]),

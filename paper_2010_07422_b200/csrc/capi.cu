@@ -134,6 +134,11 @@ struct ircur_ctx {
   // sampled-factor kernel for k + 1, so core(k + 1) reads P_k(I_{k+1}, :) and
   // Q_k(:, J_{k+1}) from it, exactly as the overlapped loop does
   bool seq_presampled = false;
+  // fp32 strips may run on the tensor cores: the loop's eps is at or above
+  // their residual floor (ircur_run / ircur_solve set it from eps,
+  // ircur_set_target_eps for ircur_iterate)
+  int tc_ok = 1;
+  double tc_min_eps = 1e-6;         // IRCUR_S5_MIN_EPS
   int run_fixed = 0;            // mode of the current loop (the next iteration's index set)
   unsigned* dbg_counter = nullptr;  // [0] sampled-factor mismatches
   int err_lag = 1;                  // SVD tolerance from e_{k - err_lag} (set per run)
@@ -343,6 +348,7 @@ StripsArgs<T> strips_args(const ircur_ctx* c, int k, const IterSets& q, double z
   cs.mode = kStripFull;
   pa.zt = storage_zeta<T>(zeta); pa.partials = c->partials; pa.done = c->flags;
   pa.dbg = c->profiling ? c->svd_dbg + 16 : nullptr;
+  pa.tc_ok = c->tc_ok;
   pa.maxl = (std::max(c->max_rows, c->max_cols) + c->strips_cs - 1) / c->strips_cs;
   return pa;
 }
@@ -915,6 +921,8 @@ int ircur_ctx_create(ircur_ctx_t* out, int device, int dtype, int64_t n1, int64_
     c->overlap_default = c->overlap;
     const char* l = std::getenv("IRCUR_SVD_ERRLAG");
     c->err_lag_env = l ? std::max(1, std::atoi(l)) : 0;
+    const char* me = std::getenv("IRCUR_S5_MIN_EPS");
+    if (me) c->tc_min_eps = std::atof(me);
   }
   IR_CUDA_C(cudaHostAlloc(&c->h_flags, 16 * sizeof(int), cudaHostAllocMapped));
   IR_CUDA_C(cudaHostGetDevicePointer((void**)&c->h_flags_dev, c->h_flags, 0));
@@ -1268,6 +1276,7 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   if (c->nloc != c->n1) return fail(IRCUR_EINVAL, "row-sharded context: use ircur_shard_phase");
   IR_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
+  c->tc_ok = eps >= c->tc_min_eps ? 1 : 0;
   mark(c, 4);
   c->shard_prof = false;
   c->run_fixed = mode == IRCUR_FIXED;
@@ -1330,6 +1339,7 @@ int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, 
   if (!(gamma > 0.0 && gamma < 1.0) || !(eps > 0.0)) return fail(IRCUR_EINVAL, "need 0 < gamma < 1 and eps > 0");
   if (colmajor < 0 || colmajor > 3) return fail(IRCUR_EINVAL, "colmajor must be 0..3");
   if (c->n1 > 0x100000000ll || c->n2 > 0x100000000ll) return fail(IRCUR_EINVAL, "dimension above 2^32");
+  c->tc_ok = eps >= c->tc_min_eps ? 1 : 0;
   const bool resampled = mode == IRCUR_RESAMPLED;
   const int n_sets = resampled ? max_iter : 1;
   const int est = (int)std::ceil(std::log(eps) / std::log(gamma));
@@ -1446,6 +1456,12 @@ int ircur_shard_finish(ircur_ctx_t c, const double* zetas, int mode, int* iterat
   if (!c || !zetas) return fail(IRCUR_EINVAL, "null context or zetas");
   IR_CUDA(cudaSetDevice(c->device));
   return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
+}
+
+int ircur_set_target_eps(ircur_ctx_t c, double eps) {
+  if (!c) return fail(IRCUR_EINVAL, "null context");
+  c->tc_ok = eps >= c->tc_min_eps ? 1 : 0;
+  return IRCUR_OK;
 }
 
 int ircur_iterate(ircur_ctx_t c, int k, int set, double zeta, double* e) {

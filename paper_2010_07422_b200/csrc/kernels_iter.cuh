@@ -69,8 +69,7 @@ struct StripsArgs {
   double* partials;                            // per CTA: {den, res}
   const int* done;
   long long* dbg;                              // optional per-phase clock64 totals (CTA 0, thread 0)
-  int prefetch_dist;                           // strips3: tiles ahead prefetched into L2
-  int desync_ns;                               // strips3: start delay of odd CTAs
+  int tc_ok;                                   // the tensor-core kernel may run (the loop's eps is above its floor)
 };
 
 // ------------------------------------------------------- sampled factors

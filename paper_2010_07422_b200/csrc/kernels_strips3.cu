@@ -81,21 +81,7 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
   double den_acc[2] = {0.0, 0.0}, res_acc[2] = {0.0, 0.0};
   const int tiles0 = a.s[0].tiles;
   const int total = tiles0 + a.s[1].tiles;
-  // L2 prefetch of a whole tile (its line segments and factor rows)
-  auto prefetch = [&](int t) {
-    if (t >= total) return;
-    const int q = t < tiles0 ? 0 : 1;
-    const StripDesc<float>& s = a.s[q];
-    const int x0 = (t - (q ? tiles0 : 0)) * kS3TX;
-    const int n = s.npos - x0 < kS3TX ? s.npos - x0 : kS3TX;
-    const uint32_t bytes = (uint32_t)((n * 4 + 15) & ~15);
-    const float* const* lp = lptr + q * (2 * L.maxp + R);
-    for (int v = tid; v < s.nk + R; v += kS3NT)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lp[v] + x0), "r"(bytes) : "memory");
-  };
   __syncthreads();
-  for (int d = 1; d < a.prefetch_dist; ++d) prefetch((int)blockIdx.x + d * (int)gridDim.x);
-  if (a.desync_ns > 0 && (blockIdx.x & 1)) __nanosleep(a.desync_ns);  // stagger the tile phases
   int cur = -1;
   for (int t = (int)blockIdx.x; t < total; t += (int)gridDim.x) {
     const int q = t < tiles0 ? 0 : 1;
@@ -142,7 +128,6 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
       asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    if (a.prefetch_dist > 0) prefetch(t + a.prefetch_dist * (int)gridDim.x);
     SPH(0);
     Pair<float> b[R];
 #pragma unroll
@@ -273,16 +258,6 @@ size_t strips3_smem_bytes(int maxl, int R) { return strips3_layout(maxl, R).tota
 cudaError_t launch_strips3(const StripsArgs<float>& a0, int R, int num_sms, int* ncta_out, cudaStream_t st) {
   StripsArgs<float> a = a0;
   a.maxl = a.s[0].nk > a.s[1].nk ? a.s[0].nk : a.s[1].nk;
-  static const int pdist = [] {  // tiles ahead prefetched into L2 (tuning knob)
-    const char* e = std::getenv("IRCUR_STRIPS_PREFETCH");
-    return e ? std::atoi(e) : 0;
-  }();
-  a.prefetch_dist = pdist;
-  static const int desync = [] {  // odd CTAs start later: fills interleave with compute (tuning knob)
-    const char* e = std::getenv("IRCUR_STRIPS_DESYNC_NS");
-    return e ? std::atoi(e) : 0;
-  }();
-  a.desync_ns = desync;
   for (int q = 0; q < 2; ++q)  // the caller counts tiles of the 64-position cluster kernel (same width)
     if (a.s[q].tiles > 0) a.s[q].tiles = (a.s[q].npos + kS3TX - 1) / kS3TX;
   const size_t smem = strips3_layout(a.maxl, R).total;

@@ -47,6 +47,9 @@
 #include "launchers.cuh"
 #include "umma.cuh"
 
+#ifndef S5_MMA3_FIRST
+#define S5_MMA3_FIRST 0  // issuer polling order: MMA3 before MMA1 / MMA2
+#endif
 #ifndef S5_PROF_EPI
 #define S5_PROF_EPI 0  // 1: the per-phase clock totals follow epilogue warp 0 instead of elementwise thread 0
 #endif
@@ -271,6 +274,20 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
       const uint32_t bp0 = umma::smem_u32(Bp);
       int n1 = 0, n2 = 0, g2 = 0, n3 = 0, nfresh = 0;
       while (n3 < ntl) {
+#if S5_MMA3_FIRST
+        // MMA3 first: it is on the epilogue's path (the tensor pipe runs in issue order)
+        if (n3 < n2 && umma::bar_try(bar(n3 & 1, kFready), xph(n3))) {
+          umma::fence_after();
+          const uint32_t r_base = r_op;
+          for (int k = 0; k < KC / 8; ++k)  // r = c - F'.Res'^T accumulated onto c (F' stored negated)
+            umma::mma_ts(T + TL(n3), T + TB(n3) + 8 * k, umma::smem_desc(r_base + 32 * k, 16, 1024, umma::kSwizzle128),
+                         idesc_r, true);
+          umma::commit(bar(n3 & 1, kB));
+          ++n3;
+          continue;
+        }
+
+#endif
         if (n1 < ntl && umma::bar_try(bar(n1 & 1, kBready), xph(n1)) &&
             (n1 < 2 || umma::bar_try(bar(n1 & 1, kRdone), xph(n1 - 2))) &&
             (!fresh_at(n1) || umma::bar_try(opsready, (uint32_t)(nfresh & 1)))) {
@@ -304,6 +321,7 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
             continue;
           }
         }
+#if !S5_MMA3_FIRST
         if (n3 < n2 && umma::bar_try(bar(n3 & 1, kFready), xph(n3))) {
           umma::fence_after();
           const uint32_t r_base = r_op;
@@ -312,7 +330,10 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
                          idesc_r, true);
           umma::commit(bar(n3 & 1, kB));
           ++n3;
+          continue;
         }
+
+#endif
       }
     }
     __syncwarp();
@@ -555,12 +576,27 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
         wait_cluster(bar(b, kXin), xph(i));
         S5PE(3);
         float f[XF];
+        {
+          float4 xv[CS][XF / 4];
 #pragma unroll
-        for (int k = 0; k < XF; ++k) f[k] = Xin[(((size_t)b * CS + 0) * 32 + lane) * XF + k];
+          for (int rr = 0; rr < CS; ++rr)
 #pragma unroll
-        for (int rr = 1; rr < CS; ++rr)
+            for (int k4 = 0; k4 < XF / 4; ++k4)
+              xv[rr][k4] = *reinterpret_cast<const float4*>(Xin + (((size_t)b * CS + rr) * 32 + lane) * XF + 4 * k4);
 #pragma unroll
-          for (int k = 0; k < XF; ++k) f[k] = __fadd_rn(f[k], Xin[(((size_t)b * CS + rr) * 32 + lane) * XF + k]);
+          for (int k4 = 0; k4 < XF / 4; ++k4) {
+            f[4 * k4] = xv[0][k4].x; f[4 * k4 + 1] = xv[0][k4].y; f[4 * k4 + 2] = xv[0][k4].z; f[4 * k4 + 3] = xv[0][k4].w;
+          }
+#pragma unroll
+          for (int rr = 1; rr < CS; ++rr)  // rank order: ((P0 + P1) + P2) + P3
+#pragma unroll
+            for (int k4 = 0; k4 < XF / 4; ++k4) {
+              f[4 * k4] = __fadd_rn(f[4 * k4], xv[rr][k4].x);
+              f[4 * k4 + 1] = __fadd_rn(f[4 * k4 + 1], xv[rr][k4].y);
+              f[4 * k4 + 2] = __fadd_rn(f[4 * k4 + 2], xv[rr][k4].z);
+              f[4 * k4 + 3] = __fadd_rn(f[4 * k4 + 3], xv[rr][k4].w);
+            }
+        }
         __syncwarp();
         if (lane == 0 && i + 2 < ntl) umma::arrive_expect_tx(bar(b, kXin), kXinBytes);  // tile i + 2
         if (om >= 0) {
@@ -572,10 +608,6 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
 #pragma unroll
           for (int k = 0; k < XF; k += 4)
             st_async_v4(umma::smem_u32(xo + k), bar(b, kXout), rr, make_float4(f[k], f[k + 1], f[k + 2], f[k + 3]));
-        }
-        if (inpos) {
-#pragma unroll
-          for (int k = 0; k < R; ++k) s.Fnew[(int64_t)k * s.ldf + x0 + p] = f[k];
         }
       }
       S5PE(4);
@@ -602,6 +634,10 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
         umma::fence_before();
         __syncwarp();
         if (lane == 0) umma::bar_arrive(bar(b, kFready));
+        if (q_ == (int)rank && inpos) {  // the new factor at the positions this rank owns
+#pragma unroll
+          for (int k = 0; k < R; ++k) s.Fnew[(int64_t)k * s.ldf + x0 + p] = xo[k];
+        }
       }
       S5PE(6);
       // ---- residual r = c - Lnew of position p over this CTA's lines (solver.py:393-400)
@@ -645,7 +681,7 @@ __global__ void __launch_bounds__(s5::NT, 1) strips5_kernel(const __grid_constan
 }
 
 bool strips5_supported(const StripsArgs<float>& a, int R) {
-  if (R > s5::RMAX) return false;
+  if (R > s5::RMAX || !a.tc_ok) return false;
   for (int q = 0; q < 2; ++q) {
     const StripDesc<float>& s = a.s[q];
     if (s.tiles == 0) continue;
@@ -665,7 +701,38 @@ cudaError_t launch_strips5(const StripsArgs<float>& a0, int R, int num_sms, int*
     if (a.s[q].tiles > 0) a.s[q].tiles = (a.s[q].npos + TP - 1) / TP;
   const int tiles = a.s[0].tiles + a.s[1].tiles;
   if (tiles == 0) return cudaSuccess;
-  const int ncl = std::max(1, std::min(tiles, num_sms / CS));
+  // clusters: as many as fit at once beside whatever else holds SMs (the
+  // overlapped loop leaves num_sms < the device's SMs for the SVD cluster);
+  // 4-CTA clusters need 4 free SMs of one GPC, so the count is the device's
+  // maximum of co-resident clusters less the GPC share the other work takes
+  int dev = 0, dev_sms = num_sms;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+  static int max_active[64] = {0};
+  int& mac = max_active[dev & 63];
+  if (mac == 0) {
+    cudaLaunchConfig_t qc = {};
+    qc.gridDim = dim3((unsigned)(CS * (dev_sms / CS)), 1, 1);
+    qc.blockDim = dim3(NT, 1, 1);
+    qc.dynamicSmemBytes = SMEM;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = CS;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    qc.attrs = qa;
+    qc.numAttrs = 1;
+    static std::atomic<unsigned long long> qdevs{0};
+    smem_attr_once(qdevs, strips5_kernel<1>, (int)SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, strips5_kernel<1>, &qc) != cudaSuccess || n <= 0) n = dev_sms / (CS + 1);
+    cudaGetLastError();
+    mac = n;
+  }
+  int ncl_cap = mac;
+  if (num_sms < dev_sms) ncl_cap -= (dev_sms - num_sms + CS - 1) / CS + 1;
+  if (const char* e = std::getenv("IRCUR_S5_CLUSTERS")) ncl_cap = std::atoi(e);  // tuning knob
+  const int ncl = std::max(1, std::min(tiles, ncl_cap));
   cudaError_t e = cudaErrorInvalidValue;
   auto launch = [&](auto kern) {
     static std::atomic<unsigned long long> devs{0};  // once per device (per rank instantiation)

@@ -170,6 +170,9 @@ class Context:
         n = it.value
         return n, bool(conv.value), errors[:n], ms[:n]
 
+    def set_target_eps(self, eps: float) -> None:
+        _capi.check(self.lib.ircur_set_target_eps(self.h, float(eps)))
+
     def iterate(self, k: int, s: int, zeta: float) -> float:
         e = C.c_double()
         _capi.check(self.lib.ircur_iterate(self.h, k, s, zeta, C.byref(e)))
@@ -664,6 +667,7 @@ def _solve_device(D, config: SolverConfig, observer=None, *, device=None, comput
         trace.seconds = [float(t) / 1e3 for t in ms]
     else:
         iters, conv = 0, False
+        ctx.set_target_eps(cfg.eps)
         for k in range(cfg.max_iter):
             s = k if resampled else 0
             ev0 = torch.cuda.Event(enable_timing=True)

@@ -33,10 +33,12 @@ import numpy as np
 TOL64, TOL32 = 1e-9, 1e-4
 ERR_RTOL64 = 1e-9
 ERR_RTOL32 = 2e-4
-# fp32: e_k also carries the fp32 round-off of the residual itself: each
-# residual entry c - l is rounded at ~2^-24 |d|, so e cannot be resolved
-# below ~2^-24 (||D(I,:)|| + ||D(:,J)||) / den ~ 6e-8; allow 3.4 * 2^-24
-ERR_ATOL32 = 2e-7
+# fp32: e_k also carries the round-off of the residual itself.  Each residual
+# entry c - l is a difference of values ~|d|; with the tensor-core strips
+# (3-term tf32 products, ~3 * 2^-22 relative each) e cannot be resolved below
+# ~3 * 2^-22 (||D(I,:)|| + ||D(:,J)||) / den ~ 4e-7 (the FFMA kernel's floor
+# is ~2^-24 of it); allow 1e-6 absolute.
+ERR_ATOL32 = 1e-6
 TIE_BAND64 = 1e-12
 FLIP_BAND32 = 1e-5
 
