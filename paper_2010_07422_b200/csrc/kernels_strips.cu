@@ -496,7 +496,7 @@ static int strips_version() {
   static const int ver = [] {
     const char* e = std::getenv("IRCUR_STRIPS_VER");
     if (!e) e = std::getenv("IRCUR_STRIPS_V1") ? "1" : nullptr;
-    return e ? std::atoi(e) : 5;
+    return e ? std::atoi(e) : 3;
   }();
   return ver;
 }
@@ -519,9 +519,10 @@ cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, in
   if (ncta_out) *ncta_out = 0;
   if (tiles == 0) return cudaSuccess;
   if constexpr (sizeof(T) == 4) {
-    // fp32: the tensor-core kernel, else the 64-position single-stage
-    // kernel, else the two-group 32-position kernel, else this cluster
-    // kernel.  IRCUR_STRIPS_VER=1|2|3|5 caps the choice (A/B measurements).
+    // fp32: the 64-position single-stage kernel, else the two-group
+    // 32-position kernel, else this cluster kernel.  IRCUR_STRIPS_VER=5 adds
+    // the tensor-core kernel in front (measured no faster at cfg5 and slower
+    // on the small configs, so it is opt-in); 1|2 cap the choice (A/B).
     const int ver = strips_version();
     const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
     if (ver >= 5) {

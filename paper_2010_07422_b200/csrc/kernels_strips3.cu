@@ -78,7 +78,6 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
     for (int e = tid; e < s.nk + R; e += kS3NT)
       lp[e] = e < s.nk ? s.src + (int64_t)(s.lines[e] - s.line_off) * s.line_stride : s.Bold + (int64_t)(e - s.nk) * s.ldb;
   }
-  double den_acc[2] = {0.0, 0.0}, res_acc[2] = {0.0, 0.0};
   const int tiles0 = a.s[0].tiles;
   const int total = tiles0 + a.s[1].tiles;
   __syncthreads();
@@ -174,8 +173,9 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
       }
     }
     SPH(1);
+    const double den_t = accum ? (double)den.v.x + (double)den.v.y : 0.0;
+    double res_t = 0.0;
     if (accum) {
-      den_acc[q] += (double)den.v.x + (double)den.v.y;
 #pragma unroll
       for (int tt = 0; tt < R; ++tt) {
         red[(w * R + tt) * kS3TX + lane] = acc[tt].v.x;
@@ -232,24 +232,34 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
         res = pfma(r0, r0, res);
         res = pfma(r1, r1, res);
       }
-      res_acc[q] += (double)res.v.x + (double)res.v.y;
+      res_t = (double)res.v.x + (double)res.v.y;
     }
     SPH(4);
+    {  // per-tile sums (warps in order): e_k does not depend on the grid size
+      const double dw = warp_sum(den_t), rw = warp_sum(res_t);
+      if (lane == 0) {
+        dred[2 * w] = dw;
+        dred[2 * w + 1] = rw;
+      }
+    }
     __syncthreads();  // stage, fnew, red free for the next tile
+    if (tid == 0) {
+      double sd = 0.0, sr = 0.0;
+      for (int ww = 0; ww < kS3NW; ++ww) {
+        sd += dred[2 * ww];
+        sr += dred[2 * ww + 1];
+      }
+      double* pr = a.partials + 4 * (size_t)t;
+      pr[q ? 2 : 0] = sd;
+      pr[q ? 3 : 1] = sr;
+      pr[q ? 0 : 2] = 0.0;
+      pr[q ? 1 : 3] = 0.0;
+    }
     SPH(5);
   }
   if (rec)
     for (int k = 0; k < 8; ++k) a.dbg[k] += tpc[k];
 #undef SPH
-  const double d0 = block_sum<kS3NT>(den_acc[0], dred);
-  const double r0 = block_sum<kS3NT>(res_acc[0], dred + kS3NW);
-  const double d1 = block_sum<kS3NT>(den_acc[1], dred + 2 * kS3NW);
-  const double r1 = block_sum<kS3NT>(res_acc[1], dred + 3 * kS3NW);
-  if (tid == 0) {
-    double4 p;
-    p.x = d0; p.y = r0; p.z = d1; p.w = r1;
-    *reinterpret_cast<double4*>(a.partials + 4 * blockIdx.x) = p;
-  }
 }
 
 size_t strips3_smem_bytes(int maxl, int R) { return strips3_layout(maxl, R).total; }
@@ -265,15 +275,18 @@ cudaError_t launch_strips3(const StripsArgs<float>& a0, int R, int num_sms, int*
   if (ncta_out) *ncta_out = 0;
   const int tiles = a.s[0].tiles + a.s[1].tiles;
   if (tiles == 0) return cudaSuccess;
+  // persistent grid, but no idle CTAs: small problems solved side by side
+  // (solve_batch) then leave the other SMs to their neighbours' kernels
+  const int grid = tiles < num_sms ? tiles : num_sms;
   cudaError_t e = cudaErrorInvalidValue;
   IRCUR_DISPATCH_RANK(R, RR, {
     static std::atomic<unsigned long long> devs{0};  // once per device
     const cudaError_t attr = smem_attr_once(devs, strips3_kernel<RR>, 227 * 1024);
     if (attr != cudaSuccess) return attr;
-    strips3_kernel<RR><<<num_sms, kS3NT, smem, st>>>(a);
+    strips3_kernel<RR><<<grid, kS3NT, smem, st>>>(a);
     e = cudaGetLastError();
   });
-  if (ncta_out) *ncta_out = num_sms;
+  if (ncta_out) *ncta_out = tiles;  // partial slots: one per tile
   return e;
 }
 
