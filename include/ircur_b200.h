@@ -242,7 +242,9 @@ int ircur_get_marks(ircur_ctx_t ctx, float* ms);
 /* Diagnostic counters of the last ircur_run: 0 = entries of the next
  * iteration's gathers that differ from the sampled-factor kernel's
  * (IRCUR_SAMPLED_CHECK=1; 0 means it reproduces the strips bitwise);
- * 1 = whether the run took the overlapped two-stream loop (IRCUR_OVERLAP). */
+ * 1 = whether the run took the overlapped two-stream loop (IRCUR_OVERLAP),
+ * 2 = the strip kernel of the process's last strip launch (1, 2, 3 = the FFMA
+ * kernels, 5 = the tensor-core kernel). */
 int ircur_debug_counter(ircur_ctx_t ctx, int which, long long* value);
 /* Loop selection for the following runs on ctx: 1 = the overlapped loop
  * (SVD of k + 1 beside the strips of k on two streams) where eligible, 0 =

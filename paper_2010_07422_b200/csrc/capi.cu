@@ -1644,6 +1644,10 @@ int ircur_debug_counter(ircur_ctx_t c, int which, long long* value) {
     *value = c->last_run_overlapped;
     return IRCUR_OK;
   }
+  if (which == 2) {  // the strip kernel of the process's last strip launch (1, 2, 3 or 5)
+    *value = ircur::g_last_strips_kernel.load();
+    return IRCUR_OK;
+  }
   unsigned v = 0;
   IR_CUDA(cudaMemcpyAsync(&v, c->dbg_counter + which, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   IR_CUDA(cudaStreamSynchronize(c->stream));

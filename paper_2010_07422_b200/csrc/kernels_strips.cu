@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 
 #include "kernels_iter.cuh"
@@ -492,14 +493,14 @@ static cudaError_t launch_strips_r(const StripsArgs<T>& a, int cs, int num_sms, 
   return cudaLaunchKernelEx(&cfg, strips_kernel<T, R>, a);
 }
 
+// read per launch (cheap), so tests can switch kernels within one process
 static int strips_version() {
-  static const int ver = [] {
-    const char* e = std::getenv("IRCUR_STRIPS_VER");
-    if (!e) e = std::getenv("IRCUR_STRIPS_V1") ? "1" : nullptr;
-    return e ? std::atoi(e) : 3;
-  }();
-  return ver;
+  const char* e = std::getenv("IRCUR_STRIPS_VER");
+  if (!e) e = std::getenv("IRCUR_STRIPS_V1") ? "1" : nullptr;
+  return e ? std::atoi(e) : 3;
 }
+
+std::atomic<int> g_last_strips_kernel{0};  // diagnostics: 1, 2, 3 or 5 (ircur_debug_counter 2)
 
 bool strips5_selected(const StripsArgs<float>& a, int R) {
   return strips_version() >= 5 && strips5_supported(a, R);
@@ -527,18 +528,28 @@ cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, in
     const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
     if (ver >= 5) {
       const cudaError_t e = launch_strips5(a, R, num_sms, ncta_out, st);
-      if (e != cudaErrorNotSupported) return e;
+      if (e != cudaErrorNotSupported) {
+        g_last_strips_kernel = 5;
+        return e;
+      }
     }
     if (ver >= 3 && aligned) {
       const cudaError_t e = launch_strips3(a, R, num_sms, ncta_out, st);
-      if (e != cudaErrorNotSupported) return e;
+      if (e != cudaErrorNotSupported) {
+        g_last_strips_kernel = 3;
+        return e;
+      }
     }
     if (ver >= 2 && aligned) {
       const cudaError_t e = launch_strips2(a, R, num_sms, ncta_out, st);
-      if (e != cudaErrorNotSupported) return e;
+      if (e != cudaErrorNotSupported) {
+        g_last_strips_kernel = 2;
+        return e;
+      }
     }
   }
   cudaError_t e = cudaErrorInvalidValue;
+  g_last_strips_kernel = 1;
   IRCUR_DISPATCH_RANK(R, RR, e = launch_strips_r<T, RR>(a, cs, num_sms, st));
   if (ncta_out) {
     const size_t smem = strips_smem_bytes<T>(a.maxl, R);

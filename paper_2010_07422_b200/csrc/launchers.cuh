@@ -92,6 +92,7 @@ cudaError_t launch_strips5(const StripsArgs<float>& a, int R, int num_sms, int* 
 bool strips5_supported(const StripsArgs<float>& a, int R);
 // the fp32 strip launch of `a` runs strips5_kernel
 bool strips5_selected(const StripsArgs<float>& a, int R);
+extern std::atomic<int> g_last_strips_kernel;  // diagnostics (ircur_debug_counter 2)
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
 template <typename T, typename O>
