@@ -19,6 +19,7 @@ on its own stream inside the timed region (roofline.achieved).
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import subprocess
@@ -101,6 +102,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: skip the nvidia-smi sampler")
     ap.add_argument("--no-profile", action="store_true", help="diagnostics: no per-kernel events")
+    ap.add_argument("--no-materialize", action="store_true", help="skip the full-L materialisation timing")
+    ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-numpy e2e step")
     ap.add_argument("--batch-streams", type=int, default=16,
                     help="cfg4: host threads / CUDA streams driving independent problems")
     ap.add_argument("--sharded", action="store_true",
@@ -119,6 +122,7 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.at_end = False
 
     def __enter__(self):
         if self.index < 0:
@@ -129,6 +133,10 @@ class ClockSampler:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 2.0:  # the sampler is running before the region
+                time.sleep(0.01)
+            self.rows = []
         except Exception:
             self.proc = None
         return self
@@ -140,6 +148,18 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def __exit__(self, *a):
+        if self.proc is not None and not self.rows:
+            # a region shorter than the 100 ms sampling period: one sample right
+            # at its end (clocks and throttle reasons do not change that fast)
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 7:
+                    self.rows.append(parts)
+                    self.at_end = True
+            except Exception:
+                pass
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -154,8 +174,11 @@ class ClockSampler:
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": reasons, "samples": len(self.rows)}
+        if self.at_end:
+            out["sampled"] = "at the end of the timed region (shorter than the 100 ms sampling period)"
+        return out
 
 
 def algorithmic_strip_bytes(s: int, n1: int, n2: int, r: int, mI: int, nJ: int) -> int:
@@ -237,6 +260,10 @@ def run_ours(args):
     strip_bytes = sum(algorithmic_strip_bytes(s, n1, n2, r, res.trace.sampled_rows[k], res.trace.sampled_cols[k])
                       for k in range(iters))
     launches = len(results) * (2 + p["kernel_launches"])  # prep + slab norm + the loop's launches (library count)
+    kv = C.c_longlong(0)
+    res.ctx.lib.ircur_debug_counter(res.ctx.h, 2, C.byref(kv))
+    strip_kernel = {1: "strips_kernel (fp64 / cluster)", 2: "strips2_kernel", 3: "strips3_kernel",
+                    5: "strips5_kernel (tcgen05)"}.get(int(kv.value), "strips")
     n_strip = iters
     peak, peak_kind = peaks()
     achieved = strip_bytes / (strip_ms / 1e3) / 1e9
@@ -270,11 +297,35 @@ def run_ours(args):
             "device_gaps_ms": p.get("gaps_ms")}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "strips3_kernel" if dts == "f32" else "strips_kernel", "avg_launch_us": strip_ms / n_strip * 1e3,
+                     "kernel": strip_kernel, "avg_launch_us": strip_ms / n_strip * 1e3,
                      "bytes_per_launch": strip_bytes / n_strip},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    # full-L materialisation (solver.py:211-213; BASELINE cfg2 "plus full-L
+    # materialisation"): L = P Q streamed at n1 x n2 in the storage dtype,
+    # write-bound; B_mat = s n1 n2 bytes per call
+    if not args.no_materialize:
+        try:
+            Lout = torch.empty((n1, n2), dtype=tdt, device="cuda")
+            dt = 0 if dts == "f32" else 1
+            lib, h = res.ctx.lib, res.ctx.h
+            lib.ircur_materialize(h, C.c_void_p(Lout.data_ptr()), n2, dt)  # warm
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 3
+            m0.record(stream)
+            for _ in range(reps):
+                lib.ircur_materialize(h, C.c_void_p(Lout.data_ptr()), n2, dt)
+            m1.record(stream)
+            torch.cuda.synchronize()
+            mms = m0.elapsed_time(m1) / reps
+            gbs = s * n1 * n2 / (mms / 1e3) / 1e9
+            line["materialize"] = {"ms": mms, "bytes": s * n1 * n2, "GBps": gbs, "frac": gbs / peak,
+                                   "kernel": "materialize_kernel (K = r writer, 16-byte stores)"}
+            del Lout
+            torch.cuda.empty_cache()
+        except Exception as e:  # noqa: BLE001  (out of memory on a small device)
+            line["materialize"] = {"error": str(e)[:200]}
     # end to end through the public API from pinned host memory
     if args.e2e_steps > 0:
         Dh = torch.empty(D.shape, dtype=D.dtype, pin_memory=True)
@@ -298,6 +349,18 @@ def run_ours(args):
             del cur, sparse, trace
         line["e2e"] = {"value": float(np.mean(times)), "unit": "s", "h2d_bytes_per_step": int(Dh.numel() * s),
                        "d2h_bytes_per_step": int(d2h), "api": "paper_2010_07422_b200.solve(pinned host D)"}
+        if not args.no_pageable:
+            # what a reference caller passes: an ordinary (pageable) numpy array
+            Dp = np.empty(tuple(Dh.shape), dtype=Dh.numpy().dtype)
+            np.copyto(Dp, Dh.numpy())
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cur, sparse, trace = ir.solve(Dp, cfg, colmajor=cm)
+            torch.cuda.synchronize()
+            line["e2e_pageable"] = {"value": time.perf_counter() - t0, "unit": "s",
+                                    "h2d_bytes_per_step": int(Dp.nbytes), "d2h_bytes_per_step": int(d2h),
+                                    "api": "paper_2010_07422_b200.solve(pageable numpy D)", "steps": 1}
+            del cur, sparse, trace, Dp
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(Dh.numpy(), args.config, cfg, iters, args.cpu_budget)
     _emit(line)
@@ -580,17 +643,35 @@ def run_batch(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(Dh, config, cfg, gpu_iters, budget):
-    """Reference algorithm (oracle port, fp64 arithmetic like the reference)
-    on this host's cores.  Small problems: full solves.  n = 1e5: a bounded
-    sample (first iterations + a slice of the finite/upcast pass), scaled."""
-    from oracle import ircur_oracle as orc
-
+def _blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        blas = [d.get("num_threads") for d in threadpool_info()]
+        return [d.get("num_threads") for d in threadpool_info()]
     except Exception:
-        blas = []
+        return []
+
+
+def _measured_cfg5_oracle():
+    """The committed measurement of one full oracle solve at cfg5 on the B200
+    host (tests/test_gpu_cfg5_oracle.py -> profiles/r02_cfg5_oracle_parity.json)."""
+    path = os.path.join(ROOT, "profiles", "r02_cfg5_oracle_parity.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return {"seconds": d.get("oracle_seconds"), "iterations": d.get("oracle_iterations"),
+            "note": "one full solve, fp64 arithmetic on the fp32 strips (no whole-matrix upcast), "
+                    "profiles/r02_cfg5_oracle_parity.json"}
+
+
+def cpu_baseline(Dh, config, cfg, gpu_iters, budget):
+    """Reference algorithm (oracle port, fp64 arithmetic like the reference)
+    on this host's cores.  Small problems: a full solve.  n = 1e5: a bounded
+    sample (the first iterations + a slice of the finite/upcast pass) scaled
+    to the iteration count, next to the committed full measured solve."""
+    from oracle import ircur_oracle as orc
+
+    blas = _blas_threads()
     cores = os.cpu_count()
     n1, n2 = Dh.shape
     kw = dict(rank=cfg.rank, eps=cfg.eps, zeta0=cfg.zeta0, gamma=cfg.gamma, mode=cfg.mode,
@@ -601,7 +682,6 @@ def cpu_baseline(Dh, config, cfg, gpu_iters, budget):
         tt = time.perf_counter() - t0
         return {"value": tt, "unit": "s", "cores": cores, "kind": "port", "blas_threads": blas,
                 "sample": f"one full oracle solve ({res.iterations} iterations, converged={res.converged})"}
-    # bounded sample: finite+upcast pass on a row slice, first iterations
     rows = max(1, n1 // 100)
     ts = time.perf_counter()
     np.isfinite(np.asarray(Dh[:rows], dtype=np.float64)).all()
@@ -615,14 +695,25 @@ def cpu_baseline(Dh, config, cfg, gpu_iters, budget):
     orc.solve(Dh, upcast=False, on_iter=on_iter, **kw)
     per_iter = float(np.mean(times[1:] if len(times) > 1 else times))
     est = t_prep + times[0] + per_iter * (gpu_iters - 1)
-    return {"value": est, "unit": "s", "cores": cores, "kind": "port", "blas_threads": blas,
-            "sample": (f"extrapolated: fp64 finite/upcast pass timed on {rows} of {n1} rows "
-                       f"({t_prep:.1f} s scaled), {len(times)} oracle iterations timed "
-                       f"({per_iter:.2f} s/iter after the first), x{gpu_iters} iterations")}
+    out = {"value": est, "unit": "s", "cores": cores, "kind": "port", "blas_threads": blas,
+           "sample": (f"extrapolated: fp64 finite/upcast pass timed on {rows} of {n1} rows "
+                      f"({t_prep:.1f} s scaled), {len(times)} oracle iterations timed "
+                      f"({per_iter:.2f} s/iter after the first), x{gpu_iters} iterations")}
+    m = _measured_cfg5_oracle() if config == "cfg5" else None
+    if m:
+        out["measured_full_solve"] = m
+    return out
 
 
 def run_reference(args):
-    """`--impl reference`: the reference algorithm on this host's CPU cores."""
+    """`--impl reference`: the reference algorithm (oracle port, pinned to the
+    real reference's golden vectors) on this host's CPU cores, rank 0 only.
+
+    Small configs: every step is one full solve.  cfg5 (1e5 x 1e5): the value
+    is ONE measured full solve with the reference's own semantics -- the
+    whole-matrix fp64 upcast and finite check (matcore.py:70-77), then the
+    loop -- and each of the K timed steps is a bounded sample (the first
+    iteration), reported beside it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -637,22 +728,41 @@ def run_reference(args):
         linf = None
     else:
         D, linf, a = orc.baseline_problem_blocked(n1, n2, r, alpha, DATA_SEED, dtype=dt)
-
-    class Cfg:  # the solver settings of our arm
-        rank, eps, zeta0, gamma, mode, max_iter = r, EPS, linf, GAMMA, args.mode, MAX_ITER
-
-    expected_iters = 23  # this generator family converges in 22-24 iterations
-    vals = []
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(D, args.config, Cfg, expected_iters, args.cpu_budget)
-        if i >= args.warmup:
-            vals.append(cb["value"])
-    v = float(np.mean(vals))
+    kw = dict(rank=r, eps=EPS, zeta0=linf, gamma=GAMMA, mode=args.mode, max_iter=MAX_ITER, seed=SOLVER_SEED)
+    cores = os.cpu_count()
+    blas = _blas_threads()
     nb = BATCH.get(args.config, 1)
-    if nb > 1:  # problem-parallel config: one problem timed, the batch is nb of them
-        v *= nb
-        cb["sample"] = f"one problem of {nb}: " + cb["sample"] + f", x{nb} problems"
-    cb["value"] = v
+    if n1 * n2 <= 2e8:
+        vals = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = orc.solve(D, **kw)
+            if i >= args.warmup:
+                vals.append(time.perf_counter() - t0)
+        v = float(np.mean(vals)) * nb
+        cb = {"value": v, "unit": "s", "cores": cores, "kind": "port", "blas_threads": blas,
+              "sample": f"one full oracle solve per step ({res.iterations} iterations)"
+                        + (f", one problem of {nb}, x{nb} problems" if nb > 1 else "")}
+        extra = {}
+    else:
+        samples = []
+        for i in range(args.warmup + args.steps):  # bounded samples: the first iteration
+
+            def first(k, sec):
+                samples.append(sec)
+                return True
+
+            orc.solve(D, upcast=False, on_iter=first, **kw)
+        samples = samples[args.warmup:]
+        t0 = time.perf_counter()
+        res = orc.solve(D, **kw)  # the measured full solve: upcast + finite check + loop
+        v = time.perf_counter() - t0
+        cb = {"value": v, "unit": "s", "cores": cores, "kind": "port", "blas_threads": blas,
+              "sample": (f"one full measured solve ({res.iterations} iterations, converged={res.converged}) "
+                         "including the whole-matrix fp64 upcast and finite check; the K steps are its "
+                         "first iteration, timed as bounded samples")}
+        extra = {"step_samples_s": samples, "full_solves_timed": 1}
+        del res
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
@@ -662,6 +772,7 @@ def run_reference(args):
                        "mode": args.mode, "gamma": GAMMA, "eps": EPS},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    line.update(extra)
     _emit(line)
 
 

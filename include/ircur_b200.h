@@ -323,6 +323,14 @@ int ircur_video_frames(const void* Pt, int64_t ldp, const void* Q, int64_t ldq, 
                        int nt, int rank, unsigned long long* peaks, uint8_t* bg, uint8_t* fg,
                        void* stream);
 
+/* The factored form of host-given C (n1 x |J|) and R (|I| x n2), fp64 device
+ * row-major: P^T = (C VS)^T (k x n1) with VS = V diag(inv_sigma) (|J| x k,
+ * row-major) and Q = W^T R (k x n2) with W (|I| x k, row-major); what
+ * convert.py:21-48 multiplies out, as two HBM-bound skinny products
+ * (no cuBLAS).  k <= 16, |I| k <= 6144. */
+int ircur_cur_to_factors(const double* C, int64_t ldc, const double* R, int64_t ldr, const double* VS,
+                         const double* W, int64_t n1, int64_t n2, int mI, int nJ, int k, double* Pt,
+                         int64_t ldp, double* Qt, int64_t ldq, void* stream);
 int ircur_factors_to_svd(const void* Pt, int64_t ldp, const void* Q, int64_t ldq, int64_t n1,
                          int64_t n2, int rank, int dtype, double* W, double* sigma, double* V,
                          int* k_out, void* stream);

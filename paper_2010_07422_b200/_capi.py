@@ -70,6 +70,8 @@ PROTOTYPES = [
     ("ircur_rowmajor_to_bin_block", _i, [_vp, _i64, _i, _i64, _i64, _vp, _vp]),
     ("ircur_video_frames", _i, [_vp, _i64, _vp, _i64, _vp, _i64, _i, _i64, _i, _i, _i64, _i, _i, _vp, _vp, _vp,
                                 _vp]),
+    ("ircur_cur_to_factors", _i, [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _i, _i, _i, _vp, _i64, _vp, _i64,
+                              _vp]),
     ("ircur_factors_to_svd", _i, [_vp, _i64, _vp, _i64, _i64, _i64, _i, _i, _vp, _vp, _vp, _pi, _vp]),
     ("ircur_gen_baseline", _i, [_vp, _i, _i64, _i64, _i64, _i64, _i64, _i, _vp, _vp, _d, _d,
                                 _pu64, _pd, _pi64, _vp]),

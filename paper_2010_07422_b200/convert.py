@@ -63,12 +63,21 @@ def cur_to_svd(C_: np.ndarray, core_pinv: PinvFactor, R: np.ndarray, *, device=N
     Cd = torch.from_numpy(np.ascontiguousarray(C_, dtype=np.float64)).to(dev)
     Rd = torch.from_numpy(np.ascontiguousarray(R, dtype=np.float64)).to(dev)
     VS = torch.from_numpy(np.asarray(core_pinv.V, dtype=np.float64) * np.asarray(core_pinv.inv_sigma)).to(dev)
-    Wt = torch.from_numpy(np.ascontiguousarray(np.asarray(core_pinv.W, dtype=np.float64).T)).to(dev)
     if VS.shape[1] == 0:
         n1, n2 = C_.shape[0], R.shape[1]
         return SvdFactors(W=np.zeros((n1, 0)), sigma=np.zeros(0), V=np.zeros((n2, 0)))
-    Pt = (Cd @ VS).T.contiguous()   # P^T = (C V Sigma^+)^T   (cuBLAS GEMMs, fp64)
-    Qt = (Wt @ Rd).contiguous()     # Q = W^T R
+    n1, nJ = C_.shape
+    mI, n2 = R.shape
+    kk = VS.shape[1]
+    Pt = torch.empty((kk, n1), dtype=torch.float64, device=dev)
+    Qt = torch.empty((kk, n2), dtype=torch.float64, device=dev)
+    W_ = torch.from_numpy(np.ascontiguousarray(core_pinv.W, dtype=np.float64)).to(dev)
+    VS = VS.contiguous()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    # P^T = (C V Sigma^+)^T and Q = W^T R: the library's skinny products
+    _capi.check(_capi.load().ircur_cur_to_factors(vp(Cd), nJ, vp(Rd), n2, vp(VS), vp(W_), n1, n2, mI, nJ, kk,
+                                                  vp(Pt), n1, vp(Qt), n2, C.c_void_p(stream)))
     W, s, V = factors_to_svd_device(Pt, Qt)
     return SvdFactors(W=W.cpu().numpy(), sigma=s.cpu().numpy(), V=V.cpu().numpy())
 

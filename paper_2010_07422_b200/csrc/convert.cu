@@ -249,3 +249,92 @@ extern "C" int ircur_factors_to_svd(const void* Pt, int64_t ldp, const void* Q, 
   *k_out = hk;
   return IRCUR_OK;
 }
+
+// ------------------------------------------------------------------------
+// The factored form of host C / R (convert.py:21-48 multiplies them out):
+//   P^T (k x n1) = (C V diag(inv_sigma))^T,  Q (k x n2) = W^T R
+// Both are tall-skinny products with k <= 16 outputs per row / column, HBM
+// bound on reading C and R once: a block stages a 32 x 32 tile of C in
+// shared memory (coalesced rows), each thread owns one row of C and k
+// accumulators; for Q each thread owns one column of R (coalesced across
+// the warp) and walks the rows with W^T in shared memory.  Fixed summation
+// order (ascending j / i), so results are deterministic.
+namespace ircur {
+namespace {
+constexpr int kCfRows = 128;  // rows of C per block
+constexpr int kCfChunk = 32;  // columns of C per staged tile
+
+template <int K>
+__global__ void __launch_bounds__(kCfRows) cur_p_kernel(const double* C, int64_t ldc, int64_t n1, int nJ,
+                                                        const double* VS, double* Pt, int64_t ldp) {
+  __shared__ double tile[kCfRows][kCfChunk + 1];
+  __shared__ double vs[kCfChunk][K];
+  const int64_t r0 = (int64_t)blockIdx.x * kCfRows;
+  const int tid = threadIdx.x;
+  double acc[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) acc[t] = 0.0;
+  for (int j0 = 0; j0 < nJ; j0 += kCfChunk) {
+    const int jn = nJ - j0 < kCfChunk ? nJ - j0 : kCfChunk;
+    for (int e = tid; e < kCfRows * kCfChunk; e += kCfRows) {
+      const int rr = e / kCfChunk, jj = e - rr * kCfChunk;
+      tile[rr][jj] = (r0 + rr < n1 && jj < jn) ? C[(r0 + rr) * ldc + j0 + jj] : 0.0;
+    }
+    for (int e = tid; e < kCfChunk * K; e += kCfRows) {
+      const int jj = e / K, t = e - jj * K;
+      vs[jj][t] = jj < jn ? VS[(int64_t)(j0 + jj) * K + t] : 0.0;
+    }
+    __syncthreads();
+    for (int jj = 0; jj < jn; ++jj) {
+      const double c = tile[tid][jj];
+#pragma unroll
+      for (int t = 0; t < K; ++t) acc[t] = fma(c, vs[jj][t], acc[t]);
+    }
+    __syncthreads();
+  }
+  if (r0 + tid < n1) {
+#pragma unroll
+    for (int t = 0; t < K; ++t) Pt[t * ldp + r0 + tid] = acc[t];
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) cur_q_kernel(const double* R, int64_t ldr, int mI, int64_t n2,
+                                                    const double* W, double* Qt, int64_t ldq) {
+  extern __shared__ double wsm[];  // mI x K
+  for (int e = threadIdx.x; e < mI * K; e += blockDim.x) wsm[e] = W[e];
+  __syncthreads();
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n2) return;
+  double acc[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) acc[t] = 0.0;
+  for (int i = 0; i < mI; ++i) {
+    const double rv = R[(int64_t)i * ldr + x];
+#pragma unroll
+    for (int t = 0; t < K; ++t) acc[t] = fma(wsm[i * K + t], rv, acc[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < K; ++t) Qt[t * ldq + x] = acc[t];
+}
+}  // namespace
+}  // namespace ircur
+
+extern "C" int ircur_cur_to_factors(const double* C, int64_t ldc, const double* R, int64_t ldr,
+                                    const double* VS, const double* W, int64_t n1, int64_t n2, int mI,
+                                    int nJ, int k, double* Pt, int64_t ldp, double* Qt, int64_t ldq,
+                                    void* stream) {
+  using namespace ircur;
+  if (k < 1 || k > kMaxRank || n1 < 0 || n2 < 0 || mI < 0 || nJ < 0 || ldc < nJ || ldr < n2 || ldp < n1 ||
+      ldq < n2)
+    return IRCUR_EINVAL;
+  if ((size_t)mI * k * sizeof(double) > 48 * 1024) return IRCUR_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned gp = (unsigned)((n1 + kCfRows - 1) / kCfRows), gq = (unsigned)((n2 + 255) / 256);
+  const size_t qsm = (size_t)mI * k * sizeof(double);
+  IRCUR_DISPATCH_RANK(k, KK, {
+    if (n1 > 0) cur_p_kernel<KK><<<gp, kCfRows, 0, st>>>(C, ldc, n1, nJ, VS, Pt, ldp);
+    if (n2 > 0) cur_q_kernel<KK><<<gq, 256, qsm, st>>>(R, ldr, mI, n2, W, Qt, ldq);
+  });
+  return cudaGetLastError() == cudaSuccess ? IRCUR_OK : IRCUR_ECUDA;
+}

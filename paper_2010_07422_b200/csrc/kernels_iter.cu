@@ -198,11 +198,24 @@ __global__ void __launch_bounds__(kMatNT) materialize_kernel(const T* Pt, int64_
     for (int t = 0; t < R; ++t) q[u][t] = (y0 + u < n2) ? Qt[t * ldq + y0 + u] : T(0);
   __syncthreads();
   const int nrows = (int)((nloc - xr0) < (int64_t)kMatRows ? (nloc - xr0) : (int64_t)kMatRows);
+  // 16-byte stores when the row segment is whole and aligned (the common case)
+  const bool vec = y0 + 3 < n2 && (ldl & 3) == 0 && ((reinterpret_cast<uintptr_t>(L) & 15) == 0);
   for (int rr = 0; rr < nrows; ++rr) {
     O* out = L + (xr0 + rr) * ldl + y0;
+    O v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (y0 + u < n2) out[u] = (O)lowrank_entry<T, R>(ps[rr], q[u]);
+    for (int u = 0; u < 4; ++u) v[u] = (O)lowrank_entry<T, R>(ps[rr], q[u]);
+    if (vec) {
+      if constexpr (sizeof(O) == 4) {
+        *reinterpret_cast<float4*>(out) = make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
+      } else {
+        reinterpret_cast<double2*>(out)[0] = make_double2((double)v[0], (double)v[1]);
+        reinterpret_cast<double2*>(out)[1] = make_double2((double)v[2], (double)v[3]);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (y0 + u < n2) out[u] = v[u];
     }
   }
 }
