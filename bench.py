@@ -105,7 +105,10 @@ def parse():
     ap.add_argument("--no-materialize", action="store_true", help="skip the full-L materialisation timing")
     ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-numpy e2e step")
     ap.add_argument("--batch-streams", type=int, default=16,
-                    help="cfg4: host threads / CUDA streams driving independent problems")
+                    help="cfg4 --threaded: host threads / CUDA streams driving independent problems")
+    ap.add_argument("--threaded", action="store_true",
+                    help="cfg4: the round-1 path (host threads, one solve each) instead of the batched launches")
+    ap.add_argument("--svd-cs", type=int, default=0, help="cfg4 batched: SVD cluster size (0 = smallest that fits)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded NCCL path even at N=1 (tests the multi-GPU code on one GPU)")
     return ap.parse_args()
@@ -539,7 +542,30 @@ def run_batch(args):
     stats = [dict(strip_ms=0.0, strip_bytes=0, iters=0, launches=0, solves=0) for _ in range(ns)]
     s = 4
 
+    def batch_once_batched(record):
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        main = torch.cuda.current_stream()
+        st = {}
+        start.record(main)
+        res = ir.solve_batch_device(probs, cfgs, svd_cs=args.svd_cs, colmajor=cm, stats=st)
+        stop.record(main)
+        torch.cuda.synchronize()
+        if record:
+            d = stats[0]
+            d["strip_ms"] += st.get("strip_ms", 0.0)
+            for rr in res:
+                it = rr.trace.iterations
+                d["strip_bytes"] += sum(algorithmic_strip_bytes(s, n1, n2, r, rr.trace.sampled_rows[k],
+                                                                 rr.trace.sampled_cols[k]) for k in range(it))
+                d["iters"] += it
+                d["solves"] += 1
+            d["launches"] += 5 * max(rr.trace.iterations for rr in res) + 2 * len(res)
+        return start.elapsed_time(stop)
+
     def batch_once(record):
+        if not args.threaded:
+            return batch_once_batched(record)
         start = torch.cuda.Event(enable_timing=True)
         stop = torch.cuda.Event(enable_timing=True)
         main = torch.cuda.current_stream()
@@ -601,15 +627,21 @@ def run_batch(args):
         "data": "synthetic (BASELINE.json generator on device, numpy-PCG64-exact), seeds 1000 + p",
         "config": {"workload": args.config, "problems": nb, "n1": n1, "n2": n2, "rank": r, "alpha": alpha,
                    "mode": args.mode, "gamma": GAMMA, "eps": EPS, "zeta0": "max|L|",
-                   "streams_per_gpu": ns, "mean_iterations": tot["iters"] / max(1, tot["solves"]),
+                   "path": ("threaded: host threads x streams, one solve each" if args.threaded else
+                            "batched: one launch per phase per iteration over all problems (ircur_batched_run)"),
+                   "streams_per_gpu": ns if args.threaded else 1,
+                   "mean_iterations": tot["iters"] / max(1, tot["solves"]),
                    "l2": "8 GB of problems cycled per batch (> L2), no flush",
                    "parallelism": f"problem-parallel over {world} GPU(s), no communication"},
         "step_ms": step_ms,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "strips3_kernel", "avg_launch_us": tot["strip_ms"] / n_strip * 1e3,
+                     "kernel": "strips3_kernel" + ("" if args.threaded else "_batched"),
+                     "avg_launch_us": tot["strip_ms"] / n_strip * 1e3,
                      "bytes_per_launch": tot["strip_bytes"] / n_strip,
-                     "note": "strip launches overlap across streams: per-launch times include the sharing"},
+                     "note": ("strip launches overlap across streams: per-launch times include the sharing"
+                              if args.threaded else "batched: avg_launch_us and bytes are per problem-iteration; "
+                              "achieved = all problems' bytes / the batched strip launches' time")},
         "gpu_launches": tot["launches"] // max(1, args.steps),
         "clocks": clk.summary(),
     }
@@ -617,20 +649,21 @@ def run_batch(args):
         hosts = [torch.empty((n1, n2), dtype=torch.float32, pin_memory=True) for _ in probs]
         for h, d in zip(hosts, probs):
             h.copy_(d)
-        out = ir.solve_batch(hosts, cfgs, streams=ns, colmajor=cm)  # warm (contexts, page-locked result blocks)
+        out = ir.solve_batch(hosts, cfgs, streams=ns, colmajor=cm, batched=not args.threaded, svd_cs=args.svd_cs)
         del out
         times = []
         for _ in range(args.e2e_steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            out = ir.solve_batch(hosts, cfgs, streams=ns, colmajor=cm)
+            out = ir.solve_batch(hosts, cfgs, streams=ns, colmajor=cm, batched=not args.threaded, svd_cs=args.svd_cs)
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
             d2h = sum(8 * (c.C.size + c.R.size + sp.row_values.size + sp.col_values.size) for c, sp, _ in out)
             del out
         line["e2e"] = {"value": float(np.mean(times)), "unit": "s",
                        "h2d_bytes_per_step": int(len(hosts) * n1 * n2 * 4), "d2h_bytes_per_step": int(d2h),
-                       "api": "paper_2010_07422_b200.solve_batch(pinned host problems)"}
+                       "api": "paper_2010_07422_b200.solve_batch(pinned host problems)" +
+                              (" threaded" if args.threaded else " batched")}
         if not args.no_cpu_baseline and rank == 0:
             D0 = probs[0].double().cpu().numpy()
             cb = cpu_baseline(D0, args.config, cfgs[0], 0, args.cpu_budget)

@@ -323,6 +323,24 @@ int ircur_video_frames(const void* Pt, int64_t ldp, const void* Q, int64_t ldq, 
                        int nt, int rank, unsigned long long* peaks, uint8_t* bg, uint8_t* fg,
                        void* stream);
 
+/* Batched independent problems (BASELINE cfg4; the reference's trial pool,
+ * cli.py:117-125).  ircur_batch_prepare runs ircur_solve's host sequence up to
+ * the loop (draws, copy plan, prep pass, den check, schedule) on one context;
+ * *zero_state = 1 means the den == 0 exit (no loop needed).
+ * ircur_batched_run then runs the loops of n prepared fp32 contexts (same
+ * rank, mode, max_iter, device) together on `stream`: one launch per phase
+ * per iteration over all problems (core, Gram + SVD with one svd_cs-CTA
+ * cluster per problem -- 0 picks the smallest that fits -- strips, stop
+ * test).  Each problem's trace and state are those of its own sequential
+ * solve with that cluster size; iterations / converged (n) and errors
+ * (n x errors_ld) receive the traces; the factors stay on each context.
+ * strip_ms (optional): device time of the batched strip launches, summed. */
+int ircur_batch_prepare(ircur_ctx_t ctx, const void* D, int64_t ldd, const uint64_t* pcg, double zeta0,
+                        double gamma, double eps, int mode, int max_iter, int colmajor, int64_t* rows,
+                        int32_t* row_counts, int64_t* cols, int32_t* col_counts, double* zeta0_used,
+                        int* copy_mode, int* zero_state);
+int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* iterations, int* converged,
+                      double* errors, int errors_ld, float* strip_ms);
 /* The factored form of host-given C (n1 x |J|) and R (|I| x n2), fp64 device
  * row-major: P^T = (C VS)^T (k x n1) with VS = V diag(inv_sigma) (|J| x k,
  * row-major) and Q = W^T R (k x n2) with W (|I| x k, row-major); what

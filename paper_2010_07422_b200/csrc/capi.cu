@@ -139,6 +139,11 @@ struct ircur_ctx {
   // ircur_set_target_eps for ircur_iterate)
   int tc_ok = 1;
   double tc_min_eps = 1e-6;         // IRCUR_S5_MIN_EPS
+  // ircur_batch_prepare -> ircur_batched_run: the prepared loop's schedule
+  std::vector<double> bzetas;
+  double b_eps = 0.0;
+  int b_mode = 0, b_max_iter = 0;
+  bool b_ready = false;
   int run_fixed = 0;            // mode of the current loop (the next iteration's index set)
   unsigned* dbg_counter = nullptr;  // [0] sampled-factor mismatches
   int err_lag = 1;                  // SVD tolerance from e_{k - err_lag} (set per run)
@@ -204,10 +209,8 @@ void mark(ircur_ctx* c, int i) {
 }
 
 int svd_cluster_size(int n, int m, int kk) {
-  static const int forced = [] {  // tuning knob
-    const char* e = std::getenv("IRCUR_SVD_CS");
-    return e ? std::atoi(e) : 0;
-  }();
+  const char* fe = std::getenv("IRCUR_SVD_CS");  // tuning knob (read per call: tests pair it with batched runs)
+  const int forced = fe ? std::atoi(fe) : 0;
   if (forced > 0 && svd_smem_bytes(n, m, kk, forced) <= (size_t)227 * 1024) return forced;
   return svd_pick_cluster(n, m, kk);
 }
@@ -1328,10 +1331,17 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
   return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
 }
 
-int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, double zeta0, double gamma,
+}  // extern "C"
+
+namespace {
+// ircur_solve up to the loop: draws, copy plan, prep pass, den check, the
+// threshold schedule.  allow_pre: chain(0) of the overlapped loop may run
+// beside the prep pass (single solves; not for batched problems).
+int solve_setup(ircur_ctx* c, const void* D, int64_t ldd, const uint64_t* pcg, double zeta0, double gamma,
                 double eps, int mode, int max_iter, int colmajor, int64_t* rows, int32_t* row_counts, int64_t* cols,
-                int32_t* col_counts, int* iterations, int* converged, double* errors, float* iter_ms,
-                double* zeta0_used, int* copy_mode, int* zero_state) {
+                int32_t* col_counts, int* iterations, int* converged, double* errors, double* zeta0_used,
+                int* copy_mode, int* zero_state, bool allow_pre, std::vector<double>& zetas, bool& pre_armed) {
+  pre_armed = false;
   if (!c || !D || !pcg || !rows || !row_counts || !cols || !col_counts)
     return fail(IRCUR_EINVAL, "null context, D, generator state or index buffers");
   if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
@@ -1375,7 +1385,8 @@ int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, 
     bool armed = true;
     ~PreGuard() { if (armed) drop_pre(c); }
   } guard{c};
-  if (int rc = pre_chain0(c, D, ldd, zeta0, gamma, mode, max_iter, cm)) return rc;
+  if (allow_pre)
+    if (int rc = pre_chain0(c, D, ldd, zeta0, gamma, mode, max_iter, cm)) return rc;
   if (int rc = ircur_prepare_async(c, D, ldd, cm, cover)) return rc;
   // the rest of the sequence is drawn and uploaded while the pass runs
   if (n_first < n_sets) {
@@ -1403,10 +1414,233 @@ int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, 
   }
   const double z0 = zeta0 > 0.0 ? zeta0 : mx;  // solver.py:342-344 (zeta0 None -> max|D|)
   if (zeta0_used) *zeta0_used = z0;
-  std::vector<double> zetas((size_t)max_iter);
+  zetas.assign((size_t)max_iter, 0.0);
   for (int k = 0; k < max_iter; ++k) zetas[k] = std::pow(gamma, (double)k) * z0;  // solver.py:372
   guard.armed = false;  // ircur_run continues the pre-launched chain (or drops it)
+  pre_armed = c->chain0_pre;
+  return IRCUR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int ircur_solve(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, double zeta0, double gamma,
+                double eps, int mode, int max_iter, int colmajor, int64_t* rows, int32_t* row_counts, int64_t* cols,
+                int32_t* col_counts, int* iterations, int* converged, double* errors, float* iter_ms,
+                double* zeta0_used, int* copy_mode, int* zero_state) {
+  std::vector<double> zetas;
+  bool pre = false;
+  int zs = 0;
+  if (int rc = solve_setup(c, D, ldd, pcg, zeta0, gamma, eps, mode, max_iter, colmajor, rows, row_counts, cols,
+                           col_counts, iterations, converged, errors, zeta0_used, copy_mode, &zs, true, zetas, pre))
+    return rc;
+  if (zero_state) *zero_state = zs;
+  if (zs) return IRCUR_OK;
   return ircur_run(c, zetas.data(), eps, mode, max_iter, iterations, converged, errors, iter_ms);
+}
+
+int ircur_batch_prepare(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_t* pcg, double zeta0,
+                        double gamma, double eps, int mode, int max_iter, int colmajor, int64_t* rows,
+                        int32_t* row_counts, int64_t* cols, int32_t* col_counts, double* zeta0_used,
+                        int* copy_mode, int* zero_state) {
+  if (!c) return fail(IRCUR_EINVAL, "null context");
+  c->b_ready = false;
+  std::vector<double> zetas;
+  bool pre = false;
+  int zs = 0, it = 0, cv = 0;
+  double e0 = 0.0;
+  if (int rc = solve_setup(c, D, ldd, pcg, zeta0, gamma, eps, mode, max_iter, colmajor, rows, row_counts, cols,
+                           col_counts, &it, &cv, &e0, zeta0_used, copy_mode, &zs, false, zetas, pre))
+    return rc;
+  if (zero_state) *zero_state = zs;
+  if (zs) return IRCUR_OK;
+  c->bzetas = std::move(zetas);
+  c->b_eps = eps;
+  c->b_mode = mode;
+  c->b_max_iter = max_iter;
+  c->b_ready = true;
+  return IRCUR_OK;
+}
+
+// Batched problems (BASELINE cfg4; the reference's trial pool, cli.py:117-125):
+// one launch per phase per iteration over every prepared context, the
+// sequential loop of each (core -> Gram + SVD -> strips -> stop test), on
+// `stream`.  Problems that stopped skip every kernel (their device flag).
+// Each problem's results are those of its own sequential fp32 solve with the
+// same SVD cluster size (svd_cs; 0 = the smallest that fits, 1 CTA for
+// cores up to ~150 x 150).
+int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* iterations, int* converged,
+                      double* errors, int errors_ld, float* strip_ms) {
+  if (!ctxs || n < 1 || !iterations || !converged || !errors) return fail(IRCUR_EINVAL, "null arguments");
+  ircur_ctx* c0 = ctxs[0];
+  if (!c0) return fail(IRCUR_EINVAL, "null context");
+  const int R = c0->r, dev = c0->device, mode = c0->b_mode, max_iter = c0->b_max_iter;
+  if (errors_ld < max_iter) return fail(IRCUR_EINVAL, "errors_ld < max_iter");
+  for (int p = 0; p < n; ++p) {
+    ircur_ctx* c = ctxs[p];
+    if (!c || !c->b_ready) return fail(IRCUR_EINVAL, "context not prepared (ircur_batch_prepare)");
+    if (c->dtype != IRCUR_F32 || !c->Dt) return fail(IRCUR_EINVAL, "batched run: fp32 with a column copy only");
+    if (c->r != R || c->device != dev || c->b_mode != mode || c->b_max_iter != max_iter || c->nloc != c->n1)
+      return fail(IRCUR_EINVAL, "batched problems must share rank, device, mode and max_iter");
+  }
+  IR_CUDA(cudaSetDevice(dev));
+  cudaStream_t bs = (cudaStream_t)stream;
+  // per-problem loop state, ordered after each context's prep pass
+  for (int p = 0; p < n; ++p) {
+    ircur_ctx* c = ctxs[p];
+    c->shard_prof = false;
+    c->overlap_prof = false;
+    c->run_fixed = mode == IRCUR_FIXED;
+    if (int rc = reset_loop(c)) return rc;
+    c->last_run_overlapped = 0;
+    c->seq_presampled = false;
+    c->tc_ok = 0;
+    c->err_lag = c->err_lag_env ? c->err_lag_env : 2;  // fp32 sequential lag (ircur_run)
+    IR_CUDA(cudaEventRecord(c->ev[0], c->stream));
+    IR_CUDA(cudaStreamWaitEvent(bs, c->ev[0], 0));
+  }
+  // argument arrays: device, and page-locked staging (a ring of 4 iterations)
+  constexpr int kRing = 4;
+  const size_t per = sizeof(CoreArgs<float>) + sizeof(SvdArgs) + sizeof(StripsArgs<float>) + sizeof(FinalizeArgs);
+  const size_t bytes_it = per * (size_t)n;
+  unsigned char* dargs = nullptr;
+  unsigned char* hargs = nullptr;
+  IR_CUDA(cudaMallocAsync((void**)&dargs, bytes_it * kRing, bs));
+  IR_CUDA(cudaHostAlloc((void**)&hargs, bytes_it * kRing, cudaHostAllocDefault));
+  struct Free {
+    unsigned char* d;
+    unsigned char* h;
+    cudaStream_t s;
+    ~Free() {
+      cudaStreamSynchronize(s);
+      if (d) cudaFreeAsync(d, s);
+      cudaStreamSynchronize(s);
+      if (h) cudaFreeHost(h);
+    }
+  } fr{dargs, hargs, bs};
+  std::vector<cudaEvent_t> evk(kRing);
+  for (auto& e : evk) IR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct FreeEv {
+    std::vector<cudaEvent_t>& v;
+    ~FreeEv() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } fe{evk};
+  std::vector<cudaEvent_t> evs;  // optional: events around each batched strip launch
+  struct FreeEvs {
+    std::vector<cudaEvent_t>& v;
+    ~FreeEvs() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } fes{evs};
+  if (strip_ms) {
+    *strip_ms = 0.f;
+    evs.resize(2 * (size_t)max_iter);
+    for (auto& e : evs) IR_CUDA(cudaEventCreate(&e));
+  }
+  constexpr int kAhead = 3;
+  int launched = 0;
+  for (int k = 0; k < max_iter; ++k) {
+    const int slot = k % kRing;
+    if (k >= kRing) IR_CUDA(cudaEventSynchronize(evk[slot]));  // its staging copy is done
+    if (k >= kAhead) {  // stop when every problem reported its stop (mapped flags)
+      IR_CUDA(cudaEventSynchronize(evk[(k - kAhead) % kRing]));
+      bool all = true;
+      for (int p = 0; p < n && all; ++p) all = ((volatile int*)ctxs[p]->h_flags)[0] != 0;
+      if (all) break;
+    }
+    unsigned char* h = hargs + bytes_it * slot;
+    unsigned char* d = dargs + bytes_it * slot;
+    CoreArgs<float>* hc = reinterpret_cast<CoreArgs<float>*>(h);
+    SvdArgs* hsv = reinterpret_cast<SvdArgs*>(hc + n);
+    StripsArgs<float>* hst = reinterpret_cast<StripsArgs<float>*>(hsv + n);
+    FinalizeArgs* hf = reinterpret_cast<FinalizeArgs*>(hst + n);
+    int max_total = 0, max_n = 0, max_tiles = 0, maxl = 0, cs = 0, kk0 = -1;
+    size_t smem = 0;
+    for (int p = 0; p < n; ++p) {
+      ircur_ctx* c = ctxs[p];
+      const int set = mode == IRCUR_FIXED ? 0 : k;
+      if (set >= c->n_sets) return fail(IRCUR_EINVAL, "fewer index sets than iterations");
+      if (c->dt_mode == 2 && set >= c->covered) {  // (rare) extend the column copy, in stream order
+        IR_CUDA(cudaEventRecord(evk[slot], bs));
+        IR_CUDA(cudaStreamWaitEvent(c->stream, evk[slot], 0));
+        if (int rc = ensure_cover(c, set)) return rc;
+        IR_CUDA(cudaEventRecord(c->ev[0], c->stream));
+        IR_CUDA(cudaStreamWaitEvent(bs, c->ev[0], 0));
+      }
+      const IterSets q = iter_sets(c, set);
+      const double zeta = c->bzetas[k];
+      hc[p] = core_args<float>(c, k, q, zeta, false);
+      hsv[p] = svd_args<float>(c, k, q);
+      StripsArgs<float> sa = strips_args<float>(c, k, q, zeta);
+      for (int t = 0; t < 2; ++t)
+        if (sa.s[t].tiles > 0) sa.s[t].tiles = (int)((sa.s[t].npos + 63) / 64);
+      sa.maxl = std::max(sa.s[0].nk, sa.s[1].nk);
+      hst[p] = sa;
+      FinalizeArgs fa = finalize_args(c, k, q, c->b_eps, max_iter, true);
+      fa.ncta_rows = sa.s[0].tiles + sa.s[1].tiles;  // strips3: one partial slot per tile
+      hf[p] = fa;
+      max_total = std::max(max_total, q.mI * q.nJ);
+      max_n = std::max(max_n, q.nJ);
+      max_tiles = std::max(max_tiles, sa.s[0].tiles + sa.s[1].tiles);
+      maxl = std::max(maxl, sa.maxl);
+      if (kk0 < 0) kk0 = hsv[p].kk;
+      if (hsv[p].kk != kk0) return fail(IRCUR_EINVAL, "batched problems need one SVD block size");
+      if (!strips3_selected(sa, R)) return fail(IRCUR_EINVAL, "batched run: the strips do not fit strips3");
+    }
+    // SVD cluster size: given, else the smallest that fits every problem's core
+    cs = svd_cs;
+    if (cs <= 0) {
+      cs = 1;
+      while (cs < 16) {
+        bool fits = true;
+        for (int p = 0; p < n && fits; ++p)
+          fits = svd_smem_bytes(hsv[p].n, hsv[p].m, hsv[p].kk, cs) <= (size_t)227 * 1024;
+        if (fits) break;
+        ++cs;
+      }
+    }
+    for (int p = 0; p < n; ++p) smem = std::max(smem, svd_smem_bytes(hsv[p].n, hsv[p].m, hsv[p].kk, cs));
+    if (smem > (size_t)227 * 1024) return fail(IRCUR_EINVAL, "batched SVD does not fit shared memory");
+    IR_CUDA(cudaMemcpyAsync(d, h, bytes_it, cudaMemcpyHostToDevice, bs));
+    const CoreArgs<float>* dc = reinterpret_cast<const CoreArgs<float>*>(d);
+    const SvdArgs* dsv = reinterpret_cast<const SvdArgs*>(dc + n);
+    const StripsArgs<float>* dst = reinterpret_cast<const StripsArgs<float>*>(dsv + n);
+    const FinalizeArgs* df = reinterpret_cast<const FinalizeArgs*>(dst + n);
+    IR_CUDA(launch_core_batched<float>(dc, n, max_total, R, bs));
+    IR_CUDA(launch_svd_batched<float>(dsv, n, max_n, cs, smem, svd_reg_path(hsv[0]), bs));
+    if (strip_ms) IR_CUDA(cudaEventRecord(evs[2 * (size_t)k], bs));
+    IR_CUDA(launch_strips3_batched(dst, n, max_tiles, maxl, R, bs));
+    if (strip_ms) IR_CUDA(cudaEventRecord(evs[2 * (size_t)k + 1], bs));
+    IR_CUDA(launch_finalize_batched(df, n, bs));
+    IR_CUDA(cudaEventRecord(evk[slot], bs));
+    for (int p = 0; p < n; ++p) {
+      ctxs[p]->kernel_launches += 5;
+      ++ctxs[p]->launched_iters;
+    }
+    ++launched;
+  }
+  // results: each context's trace, ordered after the batch
+  IR_CUDA(cudaEventRecord(evk[0], bs));
+  if (strip_ms) {
+    IR_CUDA(cudaEventSynchronize(evk[0]));
+    float tot = 0.f;
+    for (int k = 0; k < launched; ++k) {
+      float ms = 0.f;
+      IR_CUDA(cudaEventElapsedTime(&ms, evs[2 * (size_t)k], evs[2 * (size_t)k + 1]));
+      tot += ms;
+    }
+    *strip_ms = tot;
+  }
+  for (int p = 0; p < n; ++p) {
+    ircur_ctx* c = ctxs[p];
+    IR_CUDA(cudaStreamWaitEvent(c->stream, evk[0], 0));
+    if (int rc = read_trace(c, c->bzetas.data(), mode, iterations + p, converged + p, errors + (size_t)p * errors_ld,
+                            nullptr))
+      return rc;
+    c->b_ready = false;
+  }
+  return IRCUR_OK;
 }
 
 int ircur_shard_buffers(ircur_ctx_t c, void** U, int64_t* u_elems, void** Qpart, int64_t* q_elems,

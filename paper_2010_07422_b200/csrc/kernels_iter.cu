@@ -19,9 +19,9 @@ namespace ircur {
 
 // ------------------------------------------------------------------ core
 template <typename T, int R>
-__global__ void __launch_bounds__(256) core_kernel(CoreArgs<T> a) {
+__device__ __forceinline__ void core_body(const CoreArgs<T>& a, int bx) {
   if (*a.done) return;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int idx = bx * blockDim.x + threadIdx.x;
   const int total = a.mI * a.nJ;
   if (idx >= total) return;
   const int k1 = idx / a.nJ, k2 = idx - k1 * a.nJ;
@@ -68,10 +68,19 @@ __global__ void __launch_bounds__(256) core_kernel(CoreArgs<T> a) {
   a.U[(int64_t)(a.upos0 + k1) * a.ldu + k2] = (double)c;
 }
 
+template <typename T, int R>
+__global__ void __launch_bounds__(256) core_kernel(CoreArgs<T> a) { core_body<T, R>(a, (int)blockIdx.x); }
+
+// batched problems (ircur_batched_run): problem blockIdx.y
+template <typename T, int R>
+__global__ void __launch_bounds__(256) core_kernel_batched(const CoreArgs<T>* __restrict__ as) {
+  core_body<T, R>(as[blockIdx.y], (int)blockIdx.x);
+}
+
 // ------------------------------------------------------------- finalize
 constexpr int kFinNT = 512;
 
-__global__ void __launch_bounds__(kFinNT) finalize_kernel(FinalizeArgs a) {
+__device__ __forceinline__ void finalize_body(const FinalizeArgs& a) {
   if (*a.done) return;
   __shared__ double sh[4][kFinNT / 32];
   const int tid = threadIdx.x;
@@ -126,6 +135,11 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(FinalizeArgs a) {
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(kFinNT) finalize_kernel(FinalizeArgs a) { finalize_body(a); }
+__global__ void __launch_bounds__(kFinNT) finalize_kernel_batched(const FinalizeArgs* __restrict__ as) {
+  finalize_body(as[blockIdx.x]);
 }
 
 // --------------------------------------------------------------- writeout
@@ -236,6 +250,20 @@ cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_finalize_batched(const FinalizeArgs* d_args, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  finalize_kernel_batched<<<n, kFinNT, 0, st>>>(d_args);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_core_batched(const CoreArgs<T>* d_args, int n, int max_total, int R, cudaStream_t st) {
+  if (n <= 0 || max_total <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((max_total + 255) / 256), (unsigned)n);
+  IRCUR_DISPATCH_RANK(R, RR, core_kernel_batched<T, RR><<<grid, 256, 0, st>>>(d_args));
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st) {
   const int64_t tr = (int64_t)a.mI * a.n2;
@@ -264,6 +292,7 @@ cudaError_t launch_materialize(const T* Pt, int64_t ldp, const T* Qt, int64_t ld
 
 #define IRCUR_INST(T)                                                                      \
   template cudaError_t launch_core<T>(const CoreArgs<T>&, int, cudaStream_t);              \
+  template cudaError_t launch_core_batched<T>(const CoreArgs<T>*, int, int, int, cudaStream_t); \
   template cudaError_t launch_writeout<T>(const WriteoutArgs<T>&, int, cudaStream_t);      \
   template cudaError_t launch_materialize<T, float>(const T*, int64_t, const T*, int64_t,  \
                                                     int64_t, int64_t, float*, int64_t, int, \

@@ -51,7 +51,7 @@ __host__ __device__ inline Strips3Layout strips3_layout(int maxl, int R) {
 __device__ __forceinline__ uint32_t s3_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <int R>
-__global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant__ StripsArgs<float> a) {
+__device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx, int nbx) {
   if (*a.done) return;
   const Strips3Layout L = strips3_layout(a.maxl, R);
   constexpr int RPc = R + (R & 1);
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
   double* dred = reinterpret_cast<double*>(sm + L.dred);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const float zt = a.zt;
-  const bool rec = a.dbg && blockIdx.x == 0 && tid == 0;
+  const bool rec = a.dbg && bx == 0 && tid == 0;
   long long tpc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tq = clock64();
 #define SPH(k) do { if (rec) { const long long _t = clock64(); tpc[k] += _t - tq; tq = _t; } } while (0)
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
   const int total = tiles0 + a.s[1].tiles;
   __syncthreads();
   int cur = -1;
-  for (int t = (int)blockIdx.x; t < total; t += (int)gridDim.x) {
+  for (int t = bx; t < total; t += nbx) {
     const int q = t < tiles0 ? 0 : 1;
     const StripDesc<float>& s = a.s[q];
     const int nl = s.nk, np = (nl + 1) / 2, nl2 = 2 * np;
@@ -262,7 +262,36 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
 #undef SPH
 }
 
+template <int R>
+__global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant__ StripsArgs<float> a) {
+  strips3_body<R>(a, (int)blockIdx.x, (int)gridDim.x);
+}
+// batched problems: problem blockIdx.y, its tiles over blockIdx.x
+template <int R>
+__global__ void __launch_bounds__(kS3NT, 1) strips3_kernel_batched(const StripsArgs<float>* __restrict__ as) {
+  strips3_body<R>(as[blockIdx.y], (int)blockIdx.x, (int)gridDim.x);
+}
+
 size_t strips3_smem_bytes(int maxl, int R) { return strips3_layout(maxl, R).total; }
+
+// n problems, ctas CTAs each (the tiles of a problem stride over them).  The
+// arguments' tile counts are those of strips3 (64-position tiles) and maxl
+// the largest line count over the problems (the smem layout).
+cudaError_t launch_strips3_batched(const StripsArgs<float>* d_args, int n, int ctas, int maxl, int R,
+                                   cudaStream_t st) {
+  if (n <= 0 || ctas <= 0) return cudaSuccess;
+  const size_t smem = strips3_layout(maxl, R).total;
+  if (smem > (size_t)227 * 1024) return cudaErrorNotSupported;
+  cudaError_t e = cudaErrorInvalidValue;
+  IRCUR_DISPATCH_RANK(R, RR, {
+    static std::atomic<unsigned long long> devs{0};
+    const cudaError_t attr = smem_attr_once(devs, strips3_kernel_batched<RR>, 227 * 1024);
+    if (attr != cudaSuccess) return attr;
+    strips3_kernel_batched<RR><<<dim3((unsigned)ctas, (unsigned)n), kS3NT, smem, st>>>(d_args);
+    e = cudaGetLastError();
+  });
+  return e;
+}
 
 // cudaErrorNotSupported when the sampled lines do not fit the stage
 cudaError_t launch_strips3(const StripsArgs<float>& a0, int R, int num_sms, int* ncta_out, cudaStream_t st) {

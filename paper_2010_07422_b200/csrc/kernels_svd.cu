@@ -60,8 +60,8 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U, int ldu, int m, int n,
-                                                   double* __restrict__ G, int ldg, const int* done) {
+__device__ __forceinline__ void gram_body(const double* __restrict__ U, int ldu, int m, int n,
+                                          double* __restrict__ G, int ldg, const int* done, int bx) {
   if (done && *done) return;
   extern __shared__ double gram_sm[];
   auto As = [&](int st, int r, int c) -> double& { return gram_sm[((st * 2) * 32 + r) * kGramLd + c]; };
@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // blockIdx.x -> (ta <= tb) in row-major order of the upper triangle
   const int nt = (n + 31) / 32;
-  int ta = 0, rem = (int)blockIdx.x;
+  if (bx >= nt * (nt + 1) / 2) return;
+  int ta = 0, rem = bx;
   while (rem >= nt - ta) { rem -= nt - ta; ++ta; }
   const int tb = ta + rem;
   const int a0 = ta * 32, b0 = tb * 32;
@@ -133,6 +134,16 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U,
   };
   if (on0) store(acc0, bc0);
   if (on1) store(acc1, bc0 + 1);
+}
+
+__global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ U, int ldu, int m, int n,
+                                                   double* __restrict__ G, int ldg, const int* done) {
+  gram_body(U, ldu, m, n, G, ldg, done, (int)blockIdx.x);
+}
+// batched problems (ircur_batched_run): problem blockIdx.y, its core / Gram from the SVD arguments
+__global__ void __launch_bounds__(256) gram_kernel_batched(const SvdArgs* __restrict__ as) {
+  const SvdArgs& a = as[blockIdx.y];
+  gram_body(a.U, a.ldu, a.m, a.n, const_cast<double*>(a.G), a.ldg, a.done, (int)blockIdx.x);
 }
 
 // ------------------------------------------------------------ layout
@@ -636,7 +647,7 @@ __device__ void cgs2_global(Sm& S, double* V, int n, int kk, uint64_t salt) {
 }
 
 template <typename T, bool REG>
-__global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ SvdArgs a) {
+__device__ __forceinline__ void svd_body(const SvdArgs& a) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double svsm[];
   {  // one skip decision for the whole cluster: in the overlapped loop the stop
@@ -1004,6 +1015,17 @@ __global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ 
   if (a.dbg && q == 0 && tid == 0) a.dbg[11] += clock64() - tfin0;
 }
 
+template <typename T, bool REG>
+__global__ void __launch_bounds__(kSvdNT, 1) svd_kernel(const __grid_constant__ SvdArgs a) {
+  svd_body<T, REG>(a);
+}
+// batched problems: one cluster per problem (cluster id along x)
+template <typename T, bool REG>
+__global__ void __launch_bounds__(kSvdNT, 1) svd_kernel_batched(const SvdArgs* __restrict__ as) {
+  cg::cluster_group cl = cg::this_cluster();
+  svd_body<T, REG>(as[blockIdx.x / cl.num_blocks()]);
+}
+
 size_t svd_smem_bytes(int n, int m, int kk, int cs) {
   return (size_t)svd_layout(n, m, kk, cs).total * sizeof(double);
 }
@@ -1058,6 +1080,44 @@ cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st, cudaEvent_t af
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
+
+bool svd_reg_path(const SvdArgs& a) { return a.small_reg && sreg_supported(a.kk); }
+
+// Gram + SVD of n problems, one launch each: Gram blocks (tile, problem),
+// one cs-CTA cluster per problem.  Every problem shares cs, the register
+// path choice and the dynamic shared memory size (the largest).
+template <typename T>
+cudaError_t launch_svd_batched(const SvdArgs* d_args, int n, int max_n, int cs, size_t smem, bool reg,
+                               cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int nt = (max_n + 31) / 32;
+  static std::atomic<unsigned long long> gram_devs{0};
+  cudaError_t e = smem_attr_once(gram_devs, gram_kernel_batched, kGramSmem);
+  if (e != cudaSuccess) return e;
+  gram_kernel_batched<<<dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)n), 256, kGramSmem, st>>>(d_args);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  auto kern = reg ? svd_kernel_batched<T, true> : svd_kernel_batched<T, false>;
+  static std::atomic<unsigned long long> devs_reg{0}, devs_std{0};
+  e = reg ? smem_attr_once(devs_reg, svd_kernel_batched<T, true>, 227 * 1024, true)
+          : smem_attr_once(devs_std, svd_kernel_batched<T, false>, 227 * 1024, true);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(cs * n), 1, 1);
+  cfg.blockDim = dim3(kSvdNT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = cs;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, d_args);
+}
+template cudaError_t launch_svd_batched<float>(const SvdArgs*, int, int, int, size_t, bool, cudaStream_t);
+template cudaError_t launch_svd_batched<double>(const SvdArgs*, int, int, int, size_t, bool, cudaStream_t);
 
 template cudaError_t launch_svd<float>(const SvdArgs&, int, cudaStream_t, cudaEvent_t);
 template cudaError_t launch_svd<double>(const SvdArgs&, int, cudaStream_t, cudaEvent_t);

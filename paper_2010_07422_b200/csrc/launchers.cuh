@@ -94,6 +94,16 @@ bool strips5_supported(const StripsArgs<float>& a, int R);
 bool strips5_selected(const StripsArgs<float>& a, int R);
 extern std::atomic<int> g_last_strips_kernel;  // diagnostics (ircur_debug_counter 2)
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+// ---- batched problems (ircur_batched_run): device arrays of per-problem arguments
+template <typename T>
+cudaError_t launch_core_batched(const CoreArgs<T>* d_args, int n, int max_total, int R, cudaStream_t st);
+cudaError_t launch_finalize_batched(const FinalizeArgs* d_args, int n, cudaStream_t st);
+template <typename T>
+cudaError_t launch_svd_batched(const SvdArgs* d_args, int n, int max_n, int cs, size_t smem, bool reg,
+                               cudaStream_t st);
+bool svd_reg_path(const SvdArgs& a);  // the svd_kernel<T, true> instantiation runs (kk <= 8)
+cudaError_t launch_strips3_batched(const StripsArgs<float>* d_args, int n, int ctas, int maxl, int R,
+                                   cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
 template <typename T, typename O>
 cudaError_t launch_materialize(const T* Pt, int64_t ldp, const T* Qt, int64_t ldq, int64_t nloc,

@@ -839,13 +839,131 @@ def solve(D, config: SolverConfig, observer=None, *, device=None, compute_dtype=
             _release(c)
 
 
-def solve_batch(Ds, configs, *, device=None, streams: int = 4, compute_dtype=None, colmajor="auto"):
-    """Independent problems (BASELINE.json cfg4: 512 x 2000^2) solved
-    concurrently: `streams` host threads each drive their own CUDA stream and
-    library context (ctypes releases the GIL inside the library), so the
-    small per-problem kernels of several problems share the GPU.  Returns
-    the list of (CurFactors, SparseEstimate, SolverTrace) in input order,
-    bitwise equal to sequential solves."""
+_BATCH_POOL: list = []  # contexts of the batched path, reused across calls of the same shape
+
+
+def _batchable(Ds, configs) -> bool:
+    if not Ds or os.environ.get("IRCUR_BATCHED", "1") == "0":
+        return False
+    c0 = configs[0]
+    shape = tuple(Ds[0].shape)
+    for D, c in zip(Ds, configs):
+        dt = D.dtype if isinstance(D, torch.Tensor) else np.asarray(D).dtype
+        if dt not in (np.float32, torch.float32) or tuple(D.shape) != shape or len(shape) != 2:
+            return False
+        if (c.rank, c.mode, c.max_iter, c.c_rows, c.c_cols) != (c0.rank, c0.mode, c0.max_iter, c0.c_rows, c0.c_cols):
+            return False
+        if c.rank > 16 or max(shape) > 2**32:
+            return False
+    return True
+
+
+def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="auto", stats=None):
+    """Independent fp32 problems of one shape and schedule (BASELINE.json cfg4;
+    the reference's trial pool, cli.py:117-125) solved together: every
+    problem's host sequence (draws, copy plan, prep pass, den check) runs in
+    the library, then ircur_batched_run issues ONE launch per phase per
+    iteration over all of them (core, Gram + SVD with one cluster per
+    problem, strips, stop test).  Each problem's results equal its own
+    sequential solve with the same SVD cluster size (IRCUR_SVD_CS = svd_cs;
+    0 = the smallest that fits).  Returns a DeviceResult per problem."""
+    dev = device if device is not None else torch.cuda.current_device()
+    n = len(Ds)
+    c0 = configs[0]
+    Dds = [_device_matrix(D, dev, torch.float32) for D in Ds]
+    n1, n2 = int(Dds[0].shape[0]), int(Dds[0].shape[1])
+    m_rows = sample_count(n1, c0.rank, c0.c_rows)
+    m_cols = sample_count(n2, c0.rank, c0.c_cols)
+    resampled = c0.mode == "resampled"
+    n_sets = c0.max_iter if resampled else 1
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    key = (dev, n1, n2, c0.rank, m_rows, m_cols, c0.max_iter, stream)
+    with _CACHE_LOCK:
+        pool = [c for c in _BATCH_POOL if c._key == key]
+        while len(pool) < n:
+            ctx = Context(dev, _capi.F32, n1, n2, c0.rank, m_rows, m_cols, c0.max_iter, stream=stream)
+            ctx._key = key
+            _BATCH_POOL.append(ctx)
+            pool.append(ctx)
+    ctxs = pool[:n]
+    p64, p32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+    out = [None] * n
+    live = []
+    for i, (Dd, cfg) in enumerate(zip(Dds, configs)):
+        ctx = ctxs[i]
+        rows = np.empty((n_sets, m_rows), dtype=np.int64)
+        cols = np.empty((n_sets, m_cols), dtype=np.int64)
+        rc = np.zeros(n_sets, dtype=np.int32)
+        cc = np.zeros(n_sets, dtype=np.int32)
+        cm, zs, z0 = C.c_int(0), C.c_int(0), C.c_double(0.0)
+        code = _native_copy_code(colmajor, n2, m_cols, cfg)
+        pcg = pcg_words(cfg.seed)
+        ctx._D = Dd
+        _capi.check(ctx.lib.ircur_batch_prepare(
+            ctx.h, C.c_void_p(_ptr(Dd)), Dd.stride(0), pcg.ctypes.data_as(C.POINTER(C.c_uint64)),
+            float(cfg.zeta0) if cfg.zeta0 is not None else -1.0, float(cfg.gamma), float(cfg.eps),
+            _capi.RESAMPLED if resampled else _capi.FIXED, cfg.max_iter, 3 if code is None else code,
+            rows.ctypes.data_as(p64), rc.ctypes.data_as(p32), cols.ctypes.data_as(p64), cc.ctypes.data_as(p32),
+            C.byref(z0), C.byref(cm), C.byref(zs)))
+        sets = DrawnSets([(rows[k, :rc[k]], cols[k, :cc[k]]) for k in range(n_sets)], rows, rc, cols, cc)
+        ctx.sets = sets
+        ctx.colmajor = cm.value
+        if zs.value:  # solver.py:335-341
+            tr = SolverTrace()
+            tr.errors.append(0.0)
+            tr.converged = True
+            r0, c_0 = sets[0]
+            out[i] = DeviceResult(tr, cfg, None, IndexSet(r0, n1), IndexSet(c_0, n2), None, True)
+            continue
+        if cfg.zeta0 is None:
+            cfg = replace(cfg, zeta0=z0.value)
+        live.append((i, ctx, cfg, sets, cm.value))
+    if live:
+        nl = len(live)
+        arr = (C.c_void_p * nl)(*[c.h.value for _, c, _, _, _ in live])
+        its = np.zeros(nl, dtype=np.int32)
+        cvs = np.zeros(nl, dtype=np.int32)
+        errs = np.zeros((nl, c0.max_iter), dtype=np.float64)
+        sms = C.c_float(0.0)
+        _capi.check(_capi.load().ircur_batched_run(arr, nl, C.c_void_p(stream), int(svd_cs),
+                                                   its.ctypes.data_as(C.POINTER(C.c_int)),
+                                                   cvs.ctypes.data_as(C.POINTER(C.c_int)),
+                                                   errs.ctypes.data_as(C.POINTER(C.c_double)), c0.max_iter,
+                                                   C.byref(sms) if stats is not None else None))
+        if stats is not None:
+            stats["strip_ms"] = float(sms.value)
+        for j, (i, ctx, cfg, sets, cmv) in enumerate(live):
+            iters = int(its[j])
+            tr = SolverTrace()
+            tr.errors = [float(e) for e in errs[j, :iters]]
+            tr.seconds = [0.0] * iters
+            tr.iterations = iters
+            tr.converged = bool(cvs[j])
+            tr.thresholds = [cfg.gamma**k * cfg.zeta0 for k in range(iters)]
+            tr.allocated = [0] * iters
+            rcs, ccs = sets.row_counts, sets.col_counts
+            tr.sampled_rows = [int(rcs[k if resampled else 0]) for k in range(iters)]
+            tr.sampled_cols = [int(ccs[k if resampled else 0]) for k in range(iters)]
+            I, J = sets[(iters - 1) if resampled else 0]
+            Pt, Qt = ctx.factors()
+            res = DeviceResult(tr, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), DeviceHandle(Pt, Qt, _capi.F32))
+            res.profile = None
+            res._host_ms = None
+            res.colmajor = cmv
+            res.sets = sets
+            out[i] = res
+    return out
+
+
+def solve_batch(Ds, configs, *, device=None, streams: int = 4, compute_dtype=None, colmajor="auto",
+                batched=None, svd_cs: int = 0):
+    """Independent problems (BASELINE.json cfg4: 512 x 2000^2).
+
+    fp32 problems of one shape and schedule go through the batched path
+    (solve_batch_device: one launch per phase per iteration over all of
+    them); anything else is solved concurrently by `streams` host threads,
+    each driving its own CUDA stream and library context.  Returns the list
+    of (CurFactors, SparseEstimate, SolverTrace) in input order."""
     import concurrent.futures as cf
 
     global _CACHE_MAX
@@ -854,6 +972,19 @@ def solve_batch(Ds, configs, *, device=None, streams: int = 4, compute_dtype=Non
     if len(configs) != len(Ds):
         raise ValueError("need one config per problem")
     dev = device if device is not None else torch.cuda.current_device()
+    if (batched if batched is not None else True) and compute_dtype in (None, torch.float32) and \
+            _batchable(Ds, configs):
+        res = solve_batch_device(Ds, configs, device=dev, svd_cs=svd_cs, colmajor=colmajor)
+        outs = []
+        for r_ in res:
+            n1, n2 = r_.rows.bound, r_.cols.bound
+            if r_.zero_state:
+                cur, sparse = _zero_results(n1, n2, r_.rows, r_.cols, r_.cfg.rank)
+            else:
+                last = (r_.trace.iterations - 1) if r_.cfg.mode == "resampled" else 0
+                cur, sparse = _host_results(r_.ctx, last, n1, n2, r_.handle)
+            outs.append((cur, sparse, r_.trace))
+        return outs
     nstreams = max(1, min(streams, len(Ds)))
     pool_streams = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
     with _CACHE_LOCK:

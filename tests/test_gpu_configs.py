@@ -79,8 +79,8 @@ def test_cfg4_problems_match_oracle(ir, p):
 
 
 def test_cfg4_batch_equals_one_by_one(ir):
-    """solve_batch (several problems in flight on separate streams) gives
-    bitwise the results of sequential solves."""
+    """solve_batch's threaded path (several problems in flight on separate
+    streams) gives bitwise the results of sequential solves."""
     probs, cfgs = [], []
     for p in range(6):
         D, _, _, linf = orc.baseline_problem(2000, 2000, 5, 0.2, 1000 + p)
@@ -88,7 +88,7 @@ def test_cfg4_batch_equals_one_by_one(ir):
         cfgs.append(ir.SolverConfig(rank=5, eps=1e-5, zeta0=linf, gamma=0.7, mode="resampled", max_iter=100,
                                     seed=ir.RngSeed(1000 + p)))
     seq = [ir.solve(D, c, device=0) for D, c in zip(probs, cfgs)]
-    bat = ir.solve_batch(probs, cfgs, device=0, streams=3)
+    bat = ir.solve_batch(probs, cfgs, device=0, streams=3, batched=False)
     for (c1, s1, t1), (c2, s2, t2) in zip(seq, bat):
         assert t1.errors == t2.errors and t1.iterations == t2.iterations
         np.testing.assert_array_equal(c1.C, c2.C)
