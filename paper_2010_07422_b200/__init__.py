@@ -16,6 +16,7 @@ from .solver import (
     materialize_device,
     solve,
     solve_batch,
+    solve_batch_device,
     solve_device,
     threshold_at,
 )
@@ -25,7 +26,7 @@ __all__ = [
     "Context", "CurFactors", "DeviceResult", "IndexSet", "PinvFactor", "RngSeed", "SolverConfig",
     "cur_to_svd", "factors_to_svd",
     "SolverTrace", "SparseEstimate", "SvdFactors", "clear_cache", "draw_index_sets", "materialize",
-    "materialize_device", "sample_count", "sample_indices", "solve", "solve_batch", "solve_device", "threshold_at",
+    "materialize_device", "sample_count", "sample_indices", "solve", "solve_batch", "solve_batch_device", "solve_device", "threshold_at",
 ]
 
 __version__ = "0.1.0"
