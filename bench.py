@@ -542,6 +542,8 @@ def run_batch(args):
     stats = [dict(strip_ms=0.0, strip_bytes=0, iters=0, launches=0, solves=0) for _ in range(ns)]
     s = 4
 
+    phases = []
+
     def batch_once_batched(record):
         start = torch.cuda.Event(enable_timing=True)
         stop = torch.cuda.Event(enable_timing=True)
@@ -554,6 +556,7 @@ def run_batch(args):
         if record:
             d = stats[0]
             d["strip_ms"] += st.get("strip_ms", 0.0)
+            phases.append({"prepare_s": st.get("prepare_s"), "batched_run_s": st.get("batched_run_s")})
             for rr in res:
                 it = rr.trace.iterations
                 d["strip_bytes"] += sum(algorithmic_strip_bytes(s, n1, n2, r, rr.trace.sampled_rows[k],
@@ -634,6 +637,7 @@ def run_batch(args):
                    "l2": "8 GB of problems cycled per batch (> L2), no flush",
                    "parallelism": f"problem-parallel over {world} GPU(s), no communication"},
         "step_ms": step_ms,
+        "host_phases": phases[-args.steps:] if phases else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": None, "peak_kind": peak_kind,
                      "kernel": "strips3_kernel" + ("" if args.threaded else "_batched"),

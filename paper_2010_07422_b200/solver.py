@@ -867,6 +867,10 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
     problem, strips, stop test).  Each problem's results equal its own
     sequential solve with the same SVD cluster size (IRCUR_SVD_CS = svd_cs;
     0 = the smallest that fits).  Returns a DeviceResult per problem."""
+    import concurrent.futures as cf
+    import time as _time
+
+    t_start = _time.perf_counter()
     dev = device if device is not None else torch.cuda.current_device()
     n = len(Ds)
     c0 = configs[0]
@@ -876,21 +880,39 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
     m_cols = sample_count(n2, c0.rank, c0.c_cols)
     resampled = c0.mode == "resampled"
     n_sets = c0.max_iter if resampled else 1
-    stream = torch.cuda.current_stream(dev).cuda_stream
-    key = (dev, n1, n2, c0.rank, m_rows, m_cols, c0.max_iter, stream)
+    main = torch.cuda.current_stream(dev)
+    stream = main.cuda_stream
+    # the per-problem host sequences (draws, prep pass, den check: host syncs)
+    # run on `workers` threads, each with its own stream and contexts
+    workers = max(1, min(int(os.environ.get("IRCUR_BATCH_PREP_THREADS", "16")), n))
+    key = (dev, n1, n2, c0.rank, m_rows, m_cols, c0.max_iter)
     with _CACHE_LOCK:
         pool = [c for c in _BATCH_POOL if c._key == key]
+        wstreams = []
+        for c in pool:
+            if c._wstream not in wstreams:
+                wstreams.append(c._wstream)
+        while len(wstreams) < workers:
+            wstreams.append(torch.cuda.Stream(device=dev))
         while len(pool) < n:
-            ctx = Context(dev, _capi.F32, n1, n2, c0.rank, m_rows, m_cols, c0.max_iter, stream=stream)
+            w = len(pool) % workers
+            ctx = Context(dev, _capi.F32, n1, n2, c0.rank, m_rows, m_cols, c0.max_iter,
+                          stream=wstreams[w].cuda_stream)
             ctx._key = key
+            ctx._wstream = wstreams[w]
             _BATCH_POOL.append(ctx)
             pool.append(ctx)
     ctxs = pool[:n]
+    ready = torch.cuda.Event()
+    ready.record(main)  # the problems' device copies are ordered before every prep pass
+    for ws in {id(c._wstream): c._wstream for c in ctxs}.values():
+        ws.wait_event(ready)
     p64, p32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
     out = [None] * n
-    live = []
-    for i, (Dd, cfg) in enumerate(zip(Dds, configs)):
-        ctx = ctxs[i]
+    preps = [None] * n
+
+    def prepare(i):
+        Dd, cfg, ctx = Dds[i], configs[i], ctxs[i]
         rows = np.empty((n_sets, m_rows), dtype=np.int64)
         cols = np.empty((n_sets, m_cols), dtype=np.int64)
         rc = np.zeros(n_sets, dtype=np.int32)
@@ -914,10 +936,22 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
             tr.converged = True
             r0, c_0 = sets[0]
             out[i] = DeviceResult(tr, cfg, None, IndexSet(r0, n1), IndexSet(c_0, n2), None, True)
-            continue
+            return
         if cfg.zeta0 is None:
             cfg = replace(cfg, zeta0=z0.value)
-        live.append((i, ctx, cfg, sets, cm.value))
+        preps[i] = (i, ctx, cfg, sets, cm.value)
+
+    by_worker = [[i for i in range(n) if i % workers == w] for w in range(workers)]
+
+    def run_worker(w):
+        with torch.cuda.device(dev):
+            for i in by_worker[w]:
+                prepare(i)
+
+    with cf.ThreadPoolExecutor(workers) as ex:
+        list(ex.map(run_worker, range(workers)))
+    live = [x for x in preps if x is not None]
+    t_prep = _time.perf_counter()
     if live:
         nl = len(live)
         arr = (C.c_void_p * nl)(*[c.h.value for _, c, _, _, _ in live])
@@ -932,6 +966,8 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
                                                    C.byref(sms) if stats is not None else None))
         if stats is not None:
             stats["strip_ms"] = float(sms.value)
+            stats["prepare_s"] = t_prep - t_start
+            stats["batched_run_s"] = _time.perf_counter() - t_prep
         for j, (i, ctx, cfg, sets, cmv) in enumerate(live):
             iters = int(its[j])
             tr = SolverTrace()
