@@ -74,6 +74,8 @@ PROTOTYPES = [
                               _vp]),
     ("ircur_batch_prepare", _i, [_vp, _vp, _i64, _pu64, _d, _d, _d, _i, _i, _i, _pi64, C.POINTER(C.c_int32), _pi64,
                              C.POINTER(C.c_int32), _pd, _pi, _pi]),
+    ("ircur_batch_prepare_many", _i, [_vp, _i, _vp, _i64, _pu64, _pd, _pd, _pd, _i, _i, _i, _pi64,
+                                      C.POINTER(C.c_int32), _pi64, C.POINTER(C.c_int32), _pd, _pi, _pi, _i, _pi]),
     ("ircur_batched_run", _i, [_vp, _i, _vp, _i, _pi, _pi, _pd, _i, _pf]),
     ("ircur_factors_to_svd", _i, [_vp, _i64, _vp, _i64, _i64, _i64, _i, _i, _vp, _vp, _vp, _pi, _vp]),
     ("ircur_gen_baseline", _i, [_vp, _i, _i64, _i64, _i64, _i64, _i64, _i, _vp, _vp, _d, _d,

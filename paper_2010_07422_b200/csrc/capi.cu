@@ -10,7 +10,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ircur_b200.h"
@@ -144,6 +147,8 @@ struct ircur_ctx {
   double b_eps = 0.0;
   int b_mode = 0, b_max_iter = 0;
   bool b_ready = false;
+  bool prep_prof = false;          // diagnostics (IRCUR_BATCH_PREP_PROF): host ms per setup phase
+  double prep_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int run_fixed = 0;            // mode of the current loop (the next iteration's index set)
   unsigned* dbg_counter = nullptr;  // [0] sampled-factor mismatches
   int err_lag = 1;                  // SVD tolerance from e_{k - err_lag} (set per run)
@@ -1358,10 +1363,20 @@ int solve_setup(ircur_ctx* c, const void* D, int64_t ldd, const uint64_t* pcg, d
   std::memset(rows, 0, (size_t)n_sets * mr * sizeof(int64_t));
   std::memset(cols, 0, (size_t)n_sets * mc * sizeof(int64_t));
   uint64_t st1[6];
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto tq = now();
+  auto lap = [&](int k) {
+    if (!c->prep_prof) return;
+    const auto t = now();
+    c->prep_t[k] += std::chrono::duration<double, std::milli>(t - tq).count();
+    tq = t;
+  };
   // draws the prep pass needs first (sampling.py:93-104, solver.py:325-329)
   if (int rc = ircur_draw_index_sets(pcg, c->n1, c->n2, mr, mc, n_first, rows, row_counts, cols, col_counts, st1))
     return fail(rc, "index draws failed");
+  lap(0);
   if (int rc = ircur_set_indices(c, n_first, rows, row_counts, cols, col_counts)) return rc;
+  lap(1);
   // copy plan (solver._copy_plan): 3 = full copy when the covered columns exceed 70% of D
   int cm = colmajor, cover = 0;
   if (cm >= 2) {
@@ -1387,7 +1402,9 @@ int solve_setup(ircur_ctx* c, const void* D, int64_t ldd, const uint64_t* pcg, d
   } guard{c};
   if (allow_pre)
     if (int rc = pre_chain0(c, D, ldd, zeta0, gamma, mode, max_iter, cm)) return rc;
+  lap(2);
   if (int rc = ircur_prepare_async(c, D, ldd, cm, cover)) return rc;
+  lap(3);
   // the rest of the sequence is drawn and uploaded while the pass runs
   if (n_first < n_sets) {
     const int nm = n_sets - n_first;
@@ -1399,11 +1416,15 @@ int solve_setup(ircur_ctx* c, const void* D, int64_t ldd, const uint64_t* pcg, d
                                       cols + (size_t)n_first * mc, col_counts + n_first))
       return rc;
   }
+  lap(4);
   if (int rc = ircur_slab_sqnorms_async(c, 0)) return rc;
+  lap(5);
   double mx = 0.0;
   if (int rc = ircur_prepare_wait(c, nullptr, &mx)) return rc;
+  lap(6);
   double a = 0.0, b = 0.0;
   if (int rc = ircur_slab_sqnorms(c, 0, &a, &b)) return rc;
+  lap(7);
   if (zero_state) *zero_state = 0;
   if (std::sqrt(a) + std::sqrt(b) == 0.0) {  // solver.py:335-341
     if (zero_state) *zero_state = 1;
@@ -1460,6 +1481,75 @@ int ircur_batch_prepare(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_
   c->b_max_iter = max_iter;
   c->b_ready = true;
   return IRCUR_OK;
+}
+
+// ircur_batch_prepare for n contexts at once, on `threads` host threads (each
+// context keeps its own stream): the per-problem host sequences overlap, and
+// a Python caller pays one call instead of n.  Per problem p: D[p] (device,
+// ldd), pcg + 6p, zeta0[p] (<= 0: max|D|), gamma[p], eps[p]; index buffers at
+// rows + p * n_sets * max_rows etc.; zeta0_used / copy_mode / zero_state[p].
+// Returns the first failing problem's error (its index in *failed).
+int ircur_batch_prepare_many(ircur_ctx_t* ctxs, int n, const void* const* D, int64_t ldd, const uint64_t* pcg,
+                             const double* zeta0, const double* gamma, const double* eps, int mode, int max_iter,
+                             int colmajor, int64_t* rows, int32_t* row_counts, int64_t* cols, int32_t* col_counts,
+                             double* zeta0_used, int* copy_mode, int* zero_state, int threads, int* failed) {
+  if (!ctxs || n < 1 || !D || !pcg || !zeta0 || !gamma || !eps || !rows || !row_counts || !cols || !col_counts)
+    return fail(IRCUR_EINVAL, "null arguments");
+  const int n_sets = mode == IRCUR_RESAMPLED ? max_iter : 1;
+  const int dev = ctxs[0]->device;
+  const bool prof = std::getenv("IRCUR_BATCH_PREP_PROF") != nullptr;
+  std::atomic<int> next{0}, first_bad{-1}, bad_rc{0};
+  std::string bad_msg;
+  auto work = [&]() {
+    cudaSetDevice(dev);
+    set_draw_threads_for_thread(1);  // one problem per thread already
+    struct Reset {
+      ~Reset() { set_draw_threads_for_thread(0); }
+    } reset;
+    for (;;) {
+      const int p = next.fetch_add(1);
+      if (p >= n || first_bad.load() >= 0) return;
+      ircur_ctx* c = ctxs[p];
+      const size_t mr = (size_t)c->max_rows, mc = (size_t)c->max_cols;
+      c->prep_prof = prof;
+      const int rc = ircur_batch_prepare(c, D[p], ldd, pcg + 6 * (size_t)p, zeta0[p], gamma[p], eps[p], mode,
+                                         max_iter, colmajor, rows + (size_t)p * n_sets * mr,
+                                         row_counts + (size_t)p * n_sets, cols + (size_t)p * n_sets * mc,
+                                         col_counts + (size_t)p * n_sets, zeta0_used ? zeta0_used + p : nullptr,
+                                         copy_mode ? copy_mode + p : nullptr, zero_state ? zero_state + p : nullptr);
+      if (rc != IRCUR_OK) {
+        int exp = -1;
+        if (first_bad.compare_exchange_strong(exp, p)) {
+          bad_rc = rc;
+          bad_msg = ircur_last_error();
+        }
+        return;
+      }
+    }
+  };
+  const int nt = std::max(1, std::min(threads, n));
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  if (prof) {  // diagnostics: host time of the per-problem phases, summed over problems
+    double tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < n; ++p)
+      for (int k = 0; k < 8; ++k) tot[k] += ctxs[p]->prep_t[k];
+    std::fprintf(stderr, "batch prepare (ms, summed over problems): draws %.1f upload %.1f plan %.1f prep_async %.1f "
+                 "more_draws %.1f slab_async %.1f prep_wait %.1f slab %.1f\n", tot[0], tot[1], tot[2], tot[3], tot[4],
+                 tot[5], tot[6], tot[7]);
+  }
+  if (failed) *failed = first_bad.load();
+  if (first_bad.load() >= 0) return fail(bad_rc.load(), "problem " + std::to_string(first_bad.load()) + ": " + bad_msg);
+  return IRCUR_OK;
+}
+
+// CTAs per problem of the batched strip launch (each strides over the
+// problem's tiles; IRCUR_BATCH_STRIP_CTAS)
+static int batch_strip_ctas() {
+  const char* e = std::getenv("IRCUR_BATCH_STRIP_CTAS");
+  return e ? std::max(1, std::atoi(e)) : 8;
 }
 
 // Batched problems (BASELINE cfg4; the reference's trial pool, cli.py:117-125):
@@ -1540,6 +1630,7 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
   }
   constexpr int kAhead = 3;
   int launched = 0;
+  double host_ms = 0.0;
   for (int k = 0; k < max_iter; ++k) {
     const int slot = k % kRing;
     if (k >= kRing) IR_CUDA(cudaEventSynchronize(evk[slot]));  // its staging copy is done
@@ -1557,6 +1648,7 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
     FinalizeArgs* hf = reinterpret_cast<FinalizeArgs*>(hst + n);
     int max_total = 0, max_n = 0, max_tiles = 0, maxl = 0, cs = 0, kk0 = -1;
     size_t smem = 0;
+    const auto th0 = std::chrono::steady_clock::now();
     for (int p = 0; p < n; ++p) {
       ircur_ctx* c = ctxs[p];
       const int set = mode == IRCUR_FIXED ? 0 : k;
@@ -1586,8 +1678,12 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
       maxl = std::max(maxl, sa.maxl);
       if (kk0 < 0) kk0 = hsv[p].kk;
       if (hsv[p].kk != kk0) return fail(IRCUR_EINVAL, "batched problems need one SVD block size");
-      if (!strips3_selected(sa, R)) return fail(IRCUR_EINVAL, "batched run: the strips do not fit strips3");
+      if (!sa.s[0].bulk_ok || !sa.s[1].bulk_ok)
+        return fail(IRCUR_EINVAL, "batched run: line segments must be 16-byte aligned (strips3)");
     }
+    if (strips3_smem_bytes(maxl, R) > (size_t)227 * 1024)
+      return fail(IRCUR_EINVAL, "batched run: the sampled lines do not fit strips3");
+    host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
     // SVD cluster size: given, else the smallest that fits every problem's core
     cs = svd_cs;
     if (cs <= 0) {
@@ -1610,7 +1706,7 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
     IR_CUDA(launch_core_batched<float>(dc, n, max_total, R, bs));
     IR_CUDA(launch_svd_batched<float>(dsv, n, max_n, cs, smem, svd_reg_path(hsv[0]), bs));
     if (strip_ms) IR_CUDA(cudaEventRecord(evs[2 * (size_t)k], bs));
-    IR_CUDA(launch_strips3_batched(dst, n, max_tiles, maxl, R, bs));
+    IR_CUDA(launch_strips3_batched(dst, n, std::min(max_tiles, batch_strip_ctas()), maxl, R, bs));
     if (strip_ms) IR_CUDA(cudaEventRecord(evs[2 * (size_t)k + 1], bs));
     IR_CUDA(launch_finalize_batched(df, n, bs));
     IR_CUDA(cudaEventRecord(evk[slot], bs));
@@ -1620,6 +1716,8 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
     }
     ++launched;
   }
+  if (std::getenv("IRCUR_BATCH_PREP_PROF"))
+    std::fprintf(stderr, "batched run: %d iterations, host argument building %.2f ms\n", launched, host_ms);
   // results: each context's trace, ordered after the batch
   IR_CUDA(cudaEventRecord(evk[0], bs));
   if (strip_ms) {

@@ -169,7 +169,10 @@ int draw_unique(Pcg64& g, int64_t n, int m, Scratch& sc, int64_t* out) {
 
 // Threads for n_sets draws: ~6 sets (~30 us) per thread at least; env
 // IRCUR_DRAW_THREADS overrides (1 = sequential).
+thread_local int tls_draw_threads = 0;  // ircur::set_draw_threads_for_thread
+
 int draw_threads(int n_sets) {
+  if (tls_draw_threads > 0) return std::max(1, std::min(tls_draw_threads, n_sets));
   static const int forced = [] {
     const char* e = std::getenv("IRCUR_DRAW_THREADS");
     return e ? std::atoi(e) : 0;
@@ -181,6 +184,12 @@ int draw_threads(int n_sets) {
 }
 
 }  // namespace
+
+namespace ircur {
+// callers that already run one problem per thread (ircur_batch_prepare_many)
+// draw each problem's sets on the calling thread
+void set_draw_threads_for_thread(int n) { tls_draw_threads = n; }
+}  // namespace ircur
 
 extern "C" int ircur_draw_index_sets(const uint64_t* pcg, int64_t n1, int64_t n2, int m_rows, int m_cols,
                                      int n_sets, int64_t* rows, int32_t* row_counts, int64_t* cols,

@@ -101,7 +101,8 @@ cudaError_t launch_finalize_batched(const FinalizeArgs* d_args, int n, cudaStrea
 template <typename T>
 cudaError_t launch_svd_batched(const SvdArgs* d_args, int n, int max_n, int cs, size_t smem, bool reg,
                                cudaStream_t st);
-bool svd_reg_path(const SvdArgs& a);  // the svd_kernel<T, true> instantiation runs (kk <= 8)
+bool svd_reg_path(const SvdArgs& a);
+void set_draw_threads_for_thread(int n);  // draws.cu: per-thread draw parallelism (0 = default)  // the svd_kernel<T, true> instantiation runs (kk <= 8)
 cudaError_t launch_strips3_batched(const StripsArgs<float>* d_args, int n, int ctas, int maxl, int R,
                                    cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);

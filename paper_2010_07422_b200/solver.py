@@ -858,6 +858,22 @@ def _batchable(Ds, configs) -> bool:
     return True
 
 
+_PCG_CACHE: dict = {}
+
+
+def _pcg_cached(seed):
+    """pcg_words of a RngSeed (cached: a batch reuses the same seeds)."""
+    key = (type(seed).__name__, getattr(seed, "seed", None), getattr(seed, "stream", None))
+    w = _PCG_CACHE.get(key) if key[1] is not None else None
+    if w is None:
+        w = pcg_words(seed)
+        if w is None:
+            raise ValueError("batched problems need PCG64 seeds")
+        if key[1] is not None and len(_PCG_CACHE) < 100000:
+            _PCG_CACHE[key] = w
+    return w
+
+
 def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="auto", stats=None):
     """Independent fp32 problems of one shape and schedule (BASELINE.json cfg4;
     the reference's trial pool, cli.py:117-125) solved together: every
@@ -908,48 +924,51 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
     for ws in {id(c._wstream): c._wstream for c in ctxs}.values():
         ws.wait_event(ready)
     p64, p32 = C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+    pd = C.POINTER(C.c_double)
+    pi = C.POINTER(C.c_int)
     out = [None] * n
     preps = [None] * n
-
-    def prepare(i):
-        Dd, cfg, ctx = Dds[i], configs[i], ctxs[i]
-        rows = np.empty((n_sets, m_rows), dtype=np.int64)
-        cols = np.empty((n_sets, m_cols), dtype=np.int64)
-        rc = np.zeros(n_sets, dtype=np.int32)
-        cc = np.zeros(n_sets, dtype=np.int32)
-        cm, zs, z0 = C.c_int(0), C.c_int(0), C.c_double(0.0)
-        code = _native_copy_code(colmajor, n2, m_cols, cfg)
-        pcg = pcg_words(cfg.seed)
+    # every problem's host sequence (draws, copy plan, prep pass, den check)
+    # in one library call, on `workers` library threads
+    rows = np.empty((n, n_sets, m_rows), dtype=np.int64)
+    cols = np.empty((n, n_sets, m_cols), dtype=np.int64)
+    rc = np.zeros((n, n_sets), dtype=np.int32)
+    cc = np.zeros((n, n_sets), dtype=np.int32)
+    pcg = np.stack([_pcg_cached(c.seed) for c in configs])
+    z0in = np.array([float(c.zeta0) if c.zeta0 is not None else -1.0 for c in configs])
+    gam = np.array([float(c.gamma) for c in configs])
+    eps = np.array([float(c.eps) for c in configs])
+    z0 = np.zeros(n)
+    cm = np.zeros(n, dtype=np.int32)
+    zs = np.zeros(n, dtype=np.int32)
+    dptr = (C.c_void_p * n)(*[_ptr(Dd) for Dd in Dds])
+    harr = (C.c_void_p * n)(*[c.h.value for c in ctxs])
+    for ctx, Dd in zip(ctxs, Dds):
         ctx._D = Dd
-        _capi.check(ctx.lib.ircur_batch_prepare(
-            ctx.h, C.c_void_p(_ptr(Dd)), Dd.stride(0), pcg.ctypes.data_as(C.POINTER(C.c_uint64)),
-            float(cfg.zeta0) if cfg.zeta0 is not None else -1.0, float(cfg.gamma), float(cfg.eps),
-            _capi.RESAMPLED if resampled else _capi.FIXED, cfg.max_iter, 3 if code is None else code,
-            rows.ctypes.data_as(p64), rc.ctypes.data_as(p32), cols.ctypes.data_as(p64), cc.ctypes.data_as(p32),
-            C.byref(z0), C.byref(cm), C.byref(zs)))
-        sets = DrawnSets([(rows[k, :rc[k]], cols[k, :cc[k]]) for k in range(n_sets)], rows, rc, cols, cc)
+    code = _native_copy_code(colmajor, n2, m_cols, c0)
+    failed = C.c_int(-1)
+    _capi.check(_capi.load().ircur_batch_prepare_many(
+        harr, n, dptr, Dds[0].stride(0), pcg.ctypes.data_as(C.POINTER(C.c_uint64)), z0in.ctypes.data_as(pd),
+        gam.ctypes.data_as(pd), eps.ctypes.data_as(pd), _capi.RESAMPLED if resampled else _capi.FIXED,
+        c0.max_iter, 3 if code is None else code, rows.ctypes.data_as(p64), rc.ctypes.data_as(p32),
+        cols.ctypes.data_as(p64), cc.ctypes.data_as(p32), z0.ctypes.data_as(pd), cm.ctypes.data_as(pi),
+        zs.ctypes.data_as(pi), workers, C.byref(failed)))
+    for i in range(n):
+        cfg, ctx = configs[i], ctxs[i]
+        sets = DrawnSets([(rows[i, k, :rc[i, k]], cols[i, k, :cc[i, k]]) for k in range(n_sets)],
+                         rows[i], rc[i], cols[i], cc[i])
         ctx.sets = sets
-        ctx.colmajor = cm.value
-        if zs.value:  # solver.py:335-341
+        ctx.colmajor = int(cm[i])
+        if zs[i]:  # solver.py:335-341
             tr = SolverTrace()
             tr.errors.append(0.0)
             tr.converged = True
             r0, c_0 = sets[0]
             out[i] = DeviceResult(tr, cfg, None, IndexSet(r0, n1), IndexSet(c_0, n2), None, True)
-            return
+            continue
         if cfg.zeta0 is None:
-            cfg = replace(cfg, zeta0=z0.value)
-        preps[i] = (i, ctx, cfg, sets, cm.value)
-
-    by_worker = [[i for i in range(n) if i % workers == w] for w in range(workers)]
-
-    def run_worker(w):
-        with torch.cuda.device(dev):
-            for i in by_worker[w]:
-                prepare(i)
-
-    with cf.ThreadPoolExecutor(workers) as ex:
-        list(ex.map(run_worker, range(workers)))
+            cfg = replace(cfg, zeta0=float(z0[i]))
+        preps[i] = (i, ctx, cfg, sets, int(cm[i]))
     live = [x for x in preps if x is not None]
     t_prep = _time.perf_counter()
     if live:
@@ -981,7 +1000,7 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
             tr.sampled_rows = [int(rcs[k if resampled else 0]) for k in range(iters)]
             tr.sampled_cols = [int(ccs[k if resampled else 0]) for k in range(iters)]
             I, J = sets[(iters - 1) if resampled else 0]
-            Pt, Qt = ctx.factors()
+            Pt, Qt = ctx.factor_views()  # valid until the context's next solve
             res = DeviceResult(tr, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), DeviceHandle(Pt, Qt, _capi.F32))
             res.profile = None
             res._host_ms = None
