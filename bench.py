@@ -266,7 +266,7 @@ def run_ours(args):
     kv = C.c_longlong(0)
     res.ctx.lib.ircur_debug_counter(res.ctx.h, 2, C.byref(kv))
     strip_kernel = {1: "strips_kernel (fp64 / cluster)", 2: "strips2_kernel", 3: "strips3_kernel",
-                    5: "strips5_kernel (tcgen05)"}.get(int(kv.value), "strips")
+                    5: "strips5_kernel (tcgen05)", 6: "strips6_kernel (mma.sync tf32)"}.get(int(kv.value), "strips")
     n_strip = iters
     peak, peak_kind = peaks()
     achieved = strip_bytes / (strip_ms / 1e3) / 1e9

@@ -523,7 +523,7 @@ int launch_iteration(ircur_ctx* c, int k, int set, double zeta, double eps, int 
     // strips3: the next core's gathers must equal them), or the values the
     // next core reads (tensor-core strips, as in the overlapped loop)
     const int set_next = c->run_fixed ? 0 : set + 1;
-    const bool s5 = c->nloc == c->n1 && strips5_selected(strips_args<T>(c, k, q, zeta), R);
+    const bool s5 = c->nloc == c->n1 && strips_tc_selected(strips_args<T>(c, k, q, zeta), R);
     c->seq_presampled = s5 && set_next < c->n_sets;
     if ((c->sampled_check || s5) && set_next < c->n_sets)
       IR_CUDA(launch_sampled_factors(sampled_args(c, k, q, set_next, zeta), R, st));
@@ -639,7 +639,7 @@ bool overlap_eligible(ircur_ctx* c, int mode, int max_iter) {
   for (int s = 0; s < nsets; ++s) {
     const IterSets q = iter_sets(c, s);
     const StripsArgs<float> a = strips_args<float>(c, s, q, 1.0);
-    if (!strips3_selected(a, c->r) && !strips5_selected(a, c->r)) return false;
+    if (!strips3_selected(a, c->r) && !strips_tc_selected(a, c->r)) return false;
   }
   return true;
 }
@@ -772,7 +772,7 @@ int pre_chain0(ircur_ctx* c, const void* D, int64_t ldd, double zeta0, double ga
     a.s[0].nk = c->max_rows;
     a.s[1].nk = c->max_cols;
     a.s[1].bulk_ok = 1;  // the column copy's ldt is padded to 16 bytes
-    if (!strips3_selected(a, c->r) && !strips5_selected(a, c->r)) return IRCUR_OK;
+    if (!strips3_selected(a, c->r) && !strips_tc_selected(a, c->r)) return IRCUR_OK;
   }
   if (int rc = overlap_setup(c)) return rc;
   cudaStream_t us = c->stream;

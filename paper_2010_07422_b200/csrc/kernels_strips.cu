@@ -502,14 +502,18 @@ static int strips_version() {
 
 std::atomic<int> g_last_strips_kernel{0};  // diagnostics: 1, 2, 3 or 5 (ircur_debug_counter 2)
 
+bool strips6_selected(const StripsArgs<float>& a, int R) {
+  return strips_version() >= 6 && strips6_supported(a, R);
+}
+
 bool strips5_selected(const StripsArgs<float>& a, int R) {
-  return strips_version() >= 5 && strips5_supported(a, R);
+  return strips_version() == 5 && strips5_supported(a, R);
 }
 
 bool strips3_selected(const StripsArgs<float>& a, int R) {
   const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
   const int maxl = a.s[0].nk > a.s[1].nk ? a.s[0].nk : a.s[1].nk;
-  return strips_version() >= 3 && !strips5_selected(a, R) && aligned &&
+  return strips_version() >= 3 && !strips_tc_selected(a, R) && aligned &&
          strips3_smem_bytes(maxl, R) <= (size_t)227 * 1024;
 }
 
@@ -526,7 +530,14 @@ cudaError_t launch_strips(const StripsArgs<T>& a, int R, int cs, int num_sms, in
     // on the small configs, so it is opt-in); 1|2 cap the choice (A/B).
     const int ver = strips_version();
     const bool aligned = (a.s[0].tiles == 0 || a.s[0].bulk_ok) && (a.s[1].tiles == 0 || a.s[1].bulk_ok);
-    if (ver >= 5) {
+    if (ver >= 6) {
+      const cudaError_t e = launch_strips6(a, R, num_sms, ncta_out, st);
+      if (e != cudaErrorNotSupported) {
+        g_last_strips_kernel = 6;
+        return e;
+      }
+    }
+    if (ver == 5) {
       const cudaError_t e = launch_strips5(a, R, num_sms, ncta_out, st);
       if (e != cudaErrorNotSupported) {
         g_last_strips_kernel = 5;

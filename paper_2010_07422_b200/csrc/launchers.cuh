@@ -92,6 +92,18 @@ cudaError_t launch_strips5(const StripsArgs<float>& a, int R, int num_sms, int* 
 bool strips5_supported(const StripsArgs<float>& a, int R);
 // the fp32 strip launch of `a` runs strips5_kernel
 bool strips5_selected(const StripsArgs<float>& a, int R);
+// fp32 warp-level tensor-core kernel (kernels_strips6.cu): mma.sync tf32,
+// 32-position tiles, one CTA per SM; NotSupported outside its envelope
+// (r <= 10, <= 512 lines, aligned line segments, kStripFull)
+cudaError_t launch_strips6(const StripsArgs<float>& a, int R, int num_sms, int* ncta_out, cudaStream_t st);
+bool strips6_supported(const StripsArgs<float>& a, int R);
+size_t strips6_smem_bytes(int maxl);
+bool strips6_selected(const StripsArgs<float>& a, int R);
+// a tensor-core strip kernel (strips5 or strips6) runs for `a`: its factor
+// sums are not the FFMA chains the sampled-factor kernel reproduces
+inline bool strips_tc_selected(const StripsArgs<float>& a, int R) {
+  return strips5_selected(a, R) || strips6_selected(a, R);
+}
 extern std::atomic<int> g_last_strips_kernel;  // diagnostics (ircur_debug_counter 2)
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 // ---- batched problems (ircur_batched_run): device arrays of per-problem arguments

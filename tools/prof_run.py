@@ -46,11 +46,13 @@ for i in range(a.solves):
     print("  final extraction (Mcycles): " + " ".join(f"{n}={c/1e6:.2f}" for n, c in zip(fn, cyc[24:32])))
     sn = ["stage_wait", "pass1", "reduce", "override+write", "pass2", "sync+issue", "lvec+loop"]
     ver = os.environ.get("IRCUR_STRIPS_VER", "5")
+    if ver == "6":
+        sn = ["wait+barA", "strip+issue", "pass1", "barB", "reduce+barC", "a3+barD", "pass2", "sums"]
     if ver == "5":
         sn = ["fresh+wait_full", "wait_MMA1", "phaseA", "residual(prev)", "issue_loads", "-", "-", "loop"]
     elif ver != "1":
         sn = ["stage(issue+wait)", "pass1", "sync_after_pass1", "reduce+write+sync", "pass2", "final_sync", "loop"]
-    nph = 8 if ver == "5" else 7
+    nph = 8 if ver in ("5", "6") else 7
     stot = sum(cyc[16:16 + nph]) or 1
     print("  strips phases (Mcycles, CTA0/thread0): " + " ".join(
         f"{n}={c/1e6:.2f}({c/stot*100:.0f}%)" for n, c in zip(sn, [cyc[16 + k] for k in range(nph)])))
