@@ -14,6 +14,7 @@
 #include <chrono>
 #include <string>
 #include <thread>
+#include <mutex>
 #include <vector>
 
 #include "../../include/ircur_b200.h"
@@ -1483,23 +1484,53 @@ int ircur_batch_prepare(ircur_ctx_t c, const void* D, int64_t ldd, const uint64_
   return IRCUR_OK;
 }
 
-// ircur_batch_prepare for n contexts at once, on `threads` host threads (each
-// context keeps its own stream): the per-problem host sequences overlap, and
-// a Python caller pays one call instead of n.  Per problem p: D[p] (device,
+// ircur_batch_prepare for n contexts at once.  Per problem p: D[p] (device,
 // ldd), pcg + 6p, zeta0[p] (<= 0: max|D|), gamma[p], eps[p]; index buffers at
 // rows + p * n_sets * max_rows etc.; zeta0_used / copy_mode / zero_state[p].
-// Returns the first failing problem's error (its index in *failed).
+// Two phases: on `threads` host threads, every problem's draws and copy plan,
+// then its uploads, prep pass and slab norms queued on its context's stream
+// with no host waits; then one pass over the results (the per-problem host
+// waits of ircur_batch_prepare held a thread each).
+// Each problem's results are those of its own ircur_batch_prepare.  Returns
+// the first failing problem's error (its index in *failed).
 int ircur_batch_prepare_many(ircur_ctx_t* ctxs, int n, const void* const* D, int64_t ldd, const uint64_t* pcg,
                              const double* zeta0, const double* gamma, const double* eps, int mode, int max_iter,
                              int colmajor, int64_t* rows, int32_t* row_counts, int64_t* cols, int32_t* col_counts,
                              double* zeta0_used, int* copy_mode, int* zero_state, int threads, int* failed) {
   if (!ctxs || n < 1 || !D || !pcg || !zeta0 || !gamma || !eps || !rows || !row_counts || !cols || !col_counts)
     return fail(IRCUR_EINVAL, "null arguments");
-  const int n_sets = mode == IRCUR_RESAMPLED ? max_iter : 1;
+  if (failed) *failed = -1;
+  const bool resampled = mode == IRCUR_RESAMPLED;
+  const int n_sets = resampled ? max_iter : 1;
   const int dev = ctxs[0]->device;
   const bool prof = std::getenv("IRCUR_BATCH_PREP_PROF") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
+  std::vector<int> cms(n, 0);
   std::atomic<int> next{0}, first_bad{-1}, bad_rc{0};
   std::string bad_msg;
+  std::mutex bad_mu;
+  auto bad = [&](int p, int rc, const std::string& msg) {
+    std::lock_guard<std::mutex> lk(bad_mu);
+    if (first_bad.load() < 0 || p < first_bad.load()) {
+      first_bad = p;
+      bad_rc = rc;
+      bad_msg = msg;
+    }
+  };
+  for (int p = 0; p < n; ++p) {  // argument checks (solve_setup's)
+    ircur_ctx* c = ctxs[p];
+    if (!c || !D[p]) return fail(IRCUR_EINVAL, "null context or D");
+    if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
+    if (c->nloc != c->n1) return fail(IRCUR_EINVAL, "row-sharded context: use the shard phases");
+    if (!(gamma[p] > 0.0 && gamma[p] < 1.0) || !(eps[p] > 0.0))
+      return fail(IRCUR_EINVAL, "need 0 < gamma < 1 and eps > 0");
+    if (colmajor < 0 || colmajor > 3) return fail(IRCUR_EINVAL, "colmajor must be 0..3");
+    if (c->device != dev) return fail(IRCUR_EINVAL, "batched problems must share a device");
+  }
+  // ---- phase A+B on `threads` host threads: draws (sampling.py:86-104) and
+  // copy plan, then the problem's uploads, prep pass and slab norms queued on
+  // its context's stream (no host waits)
   auto work = [&]() {
     cudaSetDevice(dev);
     set_draw_threads_for_thread(1);  // one problem per thread already
@@ -1511,37 +1542,92 @@ int ircur_batch_prepare_many(ircur_ctx_t* ctxs, int n, const void* const* D, int
       if (p >= n || first_bad.load() >= 0) return;
       ircur_ctx* c = ctxs[p];
       const size_t mr = (size_t)c->max_rows, mc = (size_t)c->max_cols;
-      c->prep_prof = prof;
-      const int rc = ircur_batch_prepare(c, D[p], ldd, pcg + 6 * (size_t)p, zeta0[p], gamma[p], eps[p], mode,
-                                         max_iter, colmajor, rows + (size_t)p * n_sets * mr,
-                                         row_counts + (size_t)p * n_sets, cols + (size_t)p * n_sets * mc,
-                                         col_counts + (size_t)p * n_sets, zeta0_used ? zeta0_used + p : nullptr,
-                                         copy_mode ? copy_mode + p : nullptr, zero_state ? zero_state + p : nullptr);
-      if (rc != IRCUR_OK) {
-        int exp = -1;
-        if (first_bad.compare_exchange_strong(exp, p)) {
-          bad_rc = rc;
-          bad_msg = ircur_last_error();
+      int64_t* rp = rows + (size_t)p * n_sets * mr;
+      int64_t* cp = cols + (size_t)p * n_sets * mc;
+      int32_t* rcp = row_counts + (size_t)p * n_sets;
+      int32_t* ccp = col_counts + (size_t)p * n_sets;
+      // (entries past each set's count are left as they are: nothing reads them)
+      if (int rc = ircur_draw_index_sets(pcg + 6 * (size_t)p, c->n1, c->n2, (int)mr, (int)mc, n_sets, rp, rcp, cp,
+                                         ccp, nullptr)) {
+        bad(p, rc, "index draws failed");
+        return;
+      }
+      const int est = (int)std::ceil(std::log(eps[p]) / std::log(gamma[p]));
+      const int n_first = resampled ? std::min(n_sets, est + 8) : n_sets;
+      int cm = colmajor, cover = 0;
+      if (cm >= 2) {  // solver._copy_plan, as solve_setup
+        cover = resampled ? std::max(1, std::min(n_first, est + 8)) : 1;
+        if (cm == 3) {
+          std::vector<unsigned char> mark((size_t)c->n2, 0);
+          int64_t u = 0;
+          for (int st = 0; st < cover; ++st)
+            for (int j = 0; j < ccp[st]; ++j) {
+              unsigned char& m = mark[(size_t)cp[(size_t)st * mc + j]];
+              u += !m;
+              m = 1;
+            }
+          cm = u > 0.7 * (double)c->n2 ? 1 : 2;
+          if (cm == 1) cover = 0;
         }
+      }
+      cms[p] = cm;
+      c->b_ready = false;
+      c->tc_ok = eps[p] >= c->tc_min_eps ? 1 : 0;
+      int rc = ircur_set_indices(c, n_sets, rp, rcp, cp, ccp);
+      if (rc == IRCUR_OK) rc = ircur_prepare_async(c, D[p], ldd, cm, cover);
+      if (rc == IRCUR_OK) rc = ircur_slab_sqnorms_async(c, 0);
+      if (rc != IRCUR_OK) {
+        bad(p, rc, ircur_last_error());
         return;
       }
     }
   };
-  const int nt = std::max(1, std::min(threads, n));
-  std::vector<std::thread> pool;
-  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
-  if (prof) {  // diagnostics: host time of the per-problem phases, summed over problems
-    double tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int p = 0; p < n; ++p)
-      for (int k = 0; k < 8; ++k) tot[k] += ctxs[p]->prep_t[k];
-    std::fprintf(stderr, "batch prepare (ms, summed over problems): draws %.1f upload %.1f plan %.1f prep_async %.1f "
-                 "more_draws %.1f slab_async %.1f prep_wait %.1f slab %.1f\n", tot[0], tot[1], tot[2], tot[3], tot[4],
-                 tot[5], tot[6], tot[7]);
+  {
+    const int nt = std::max(1, std::min(threads, n));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
   }
-  if (failed) *failed = first_bad.load();
-  if (first_bad.load() >= 0) return fail(bad_rc.load(), "problem " + std::to_string(first_bad.load()) + ": " + bad_msg);
+  if (first_bad.load() >= 0) {
+    if (failed) *failed = first_bad.load();
+    return fail(bad_rc.load(), "problem " + std::to_string(first_bad.load()) + ": " + bad_msg);
+  }
+  for (int p = 0; p < n; ++p)
+    if (copy_mode) copy_mode[p] = cms[p];
+  const auto t1 = now();
+  const auto t2 = now();
+  // ---- phase C: finite check, max|D|, den = 0 exit (solver.py:319-344)
+  for (int p = 0; p < n; ++p) {
+    ircur_ctx* c = ctxs[p];
+    double mx = 0.0;
+    if (int rc = ircur_prepare_wait(c, nullptr, &mx)) {
+      if (failed) *failed = p;
+      return fail(rc, "problem " + std::to_string(p) + ": " + ircur_last_error());
+    }
+    double a = 0.0, b = 0.0;
+    if (int rc = ircur_slab_sqnorms(c, 0, &a, &b)) {
+      if (failed) *failed = p;
+      return fail(rc, "problem " + std::to_string(p) + ": " + ircur_last_error());
+    }
+    const bool zs = std::sqrt(a) + std::sqrt(b) == 0.0;
+    if (zero_state) zero_state[p] = zs ? 1 : 0;
+    if (zs) continue;
+    const double z0 = zeta0[p] > 0.0 ? zeta0[p] : mx;  // solver.py:342-344 (zeta0 None -> max|D|)
+    if (zeta0_used) zeta0_used[p] = z0;
+    c->bzetas.assign((size_t)max_iter, 0.0);
+    for (int k = 0; k < max_iter; ++k) c->bzetas[k] = std::pow(gamma[p], (double)k) * z0;  // solver.py:372
+    c->b_eps = eps[p];
+    c->b_mode = mode;
+    c->b_max_iter = max_iter;
+    c->b_ready = true;
+  }
+  if (prof) {
+    const auto t3 = now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "batch prepare (ms): draws, plans and queued passes %.1f, results %.1f\n", ms(t0, t1),
+                 ms(t2, t3));
+  }
   return IRCUR_OK;
 }
 
@@ -1730,12 +1816,37 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
     }
     *strip_ms = tot;
   }
+  // every problem's flags and error trace into one page-locked buffer on the
+  // batch stream, then one wait (read_trace per problem would cost two host
+  // waits each)
+  const size_t per_p = 4 * sizeof(int) + (size_t)max_iter * sizeof(double);
+  unsigned char* hres = nullptr;
+  IR_CUDA(cudaHostAlloc((void**)&hres, per_p * n, cudaHostAllocDefault));
+  struct FreeH {
+    unsigned char* h;
+    ~FreeH() { cudaFreeHost(h); }
+  } fh{hres};
   for (int p = 0; p < n; ++p) {
     ircur_ctx* c = ctxs[p];
-    IR_CUDA(cudaStreamWaitEvent(c->stream, evk[0], 0));
-    if (int rc = read_trace(c, c->bzetas.data(), mode, iterations + p, converged + p, errors + (size_t)p * errors_ld,
-                            nullptr))
-      return rc;
+    IR_CUDA(cudaMemcpyAsync(hres + per_p * p, c->flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, bs));
+    IR_CUDA(cudaMemcpyAsync(hres + per_p * p + 4 * sizeof(int), c->errors, (size_t)max_iter * sizeof(double),
+                            cudaMemcpyDeviceToHost, bs));
+  }
+  IR_CUDA(cudaStreamSynchronize(bs));
+  for (int p = 0; p < n; ++p) {
+    ircur_ctx* c = ctxs[p];
+    const int* hf = reinterpret_cast<const int*>(hres + per_p * p);
+    const int iters = hf[1];
+    iterations[p] = iters;
+    converged[p] = hf[2];
+    if (iters > 0) {
+      std::memcpy(errors + (size_t)p * errors_ld, hres + per_p * p + 4 * sizeof(int), (size_t)iters * sizeof(double));
+      c->last_k = iters - 1;  // (read_trace's state)
+      c->last_set = mode == IRCUR_FIXED ? 0 : iters - 1;
+      c->last_zeta = c->bzetas[iters - 1];
+      c->has_state = true;
+    }
+    IR_CUDA(cudaStreamWaitEvent(c->stream, evk[0], 0));  // the context's next work follows the batch
     c->b_ready = false;
   }
   return IRCUR_OK;

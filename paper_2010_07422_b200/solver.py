@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _capi
-from .sampling import DrawnSets, IndexSet, draw_index_sets, draw_index_sets_from, pcg_words, sample_count
+from .sampling import DrawnSets, IndexSet, LazyDrawnSets, draw_index_sets, draw_index_sets_from, pcg_words, sample_count
 from .types import CurFactors, PinvFactor, SolverConfig, SolverTrace, SparseEstimate
 
 __all__ = ["solve", "solve_device", "solve_batch", "materialize", "materialize_device", "threshold_at",
@@ -955,8 +955,7 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
         zs.ctypes.data_as(pi), workers, C.byref(failed)))
     for i in range(n):
         cfg, ctx = configs[i], ctxs[i]
-        sets = DrawnSets([(rows[i, k, :rc[i, k]], cols[i, k, :cc[i, k]]) for k in range(n_sets)],
-                         rows[i], rc[i], cols[i], cc[i])
+        sets = LazyDrawnSets(rows[i], rc[i], cols[i], cc[i])
         ctx.sets = sets
         ctx.colmajor = int(cm[i])
         if zs[i]:  # solver.py:335-341
