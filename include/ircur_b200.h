@@ -343,8 +343,10 @@ int ircur_batch_prepare(ircur_ctx_t ctx, const void* D, int64_t ldd, const uint6
  * on its own stream).  Per problem p: D[p] (leading dimension ldd), the PCG64
  * state pcg[6p .. 6p + 5], zeta0[p] (<= 0: max|D|), gamma[p], eps[p]; index
  * buffers rows + p n_sets max_rows, row_counts + p n_sets (same for cols);
- * zeta0_used / copy_mode / zero_state [p].  *failed = the first failing
- * problem (-1 if none). */
+ * zeta0_used / copy_mode / zero_state [p].  The threads draw and queue every
+ * problem's uploads, prep pass and slab norms without host waits; one pass
+ * then reads the results.  Entries past each set's count in the index buffers
+ * are left unwritten.  *failed = the first failing problem (-1 if none). */
 int ircur_batch_prepare_many(ircur_ctx_t* ctxs, int n, const void* const* D, int64_t ldd, const uint64_t* pcg,
                              const double* zeta0, const double* gamma, const double* eps, int mode, int max_iter,
                              int colmajor, int64_t* rows, int32_t* row_counts, int64_t* cols, int32_t* col_counts,

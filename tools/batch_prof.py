@@ -10,7 +10,7 @@ for p in range(512):
     probs.append(D); cfgs.append(ir.SolverConfig(rank=5, eps=1e-5, zeta0=linf, gamma=0.7, mode="resampled", max_iter=100, seed=ir.RngSeed(1000 + p)))
 for it in range(3):
     torch.cuda.synchronize(); t0 = time.perf_counter(); st = {}
-    res = ir.solve_batch_device(probs, cfgs, stats=st)
+    res = ir.solve_batch_device(probs, cfgs, stats=st, svd_cs=int(os.environ.get("SVDCS", "0")))
     torch.cuda.synchronize(); t1 = time.perf_counter()
     print(f"total {1e3*(t1-t0):.1f} ms prepare {1e3*st['prepare_s']:.1f} run {1e3*st['batched_run_s']:.1f}", flush=True)
 pr = cProfile.Profile(); pr.enable()
