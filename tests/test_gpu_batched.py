@@ -86,3 +86,20 @@ def test_batched_zero_slab_problem(ir):
     for i in (0, 2):
         ref = ir.solve(probs[i], cfgs[i], device=0, overlap=False)
         assert ref[2].iterations == bat[i][2].iterations
+
+
+def test_batched_nonfinite_problem_raises(ir):
+    """A non-finite entry in one problem of a batch raises the reference's
+    error (matcore.require_finite, matcore.py:70-77) naming that problem; the
+    same contexts then solve a clean batch."""
+    probs, cfgs = _problems(ir, 600, 3, r=3, seed0=1300)
+    bad = [p.copy() for p in probs]
+    bad[2][5, 7] = np.nan
+    with pytest.raises(ValueError, match="non-finite") as ei:
+        ir.solve_batch(bad, cfgs, device=0)
+    assert "problem 2" in str(ei.value)
+    bat = ir.solve_batch(probs, cfgs, device=0)
+    for i in range(3):
+        ref = ir.solve(probs[i], cfgs[i], device=0, overlap=False)
+        assert ref[2].iterations == bat[i][2].iterations
+        assert ref[2].errors == bat[i][2].errors
