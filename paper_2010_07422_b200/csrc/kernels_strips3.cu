@@ -5,9 +5,10 @@
 // solver.py:375-400).  What bounds those kernels is shared-memory wavefronts,
 // dominated by the per-line vectors A | W | Res that every warp broadcasts
 // for each line it processes (LDS.128 broadcast = 2 wavefronts, 8 bytes
-// each).  Here each lane owns TWO positions (x and x + 32 of a 64-position
+// each).  Here each lane owns TWO positions (2 lane and 2 lane + 1 of a 64-position
 // tile, packed in FFMA2 pairs), so every line-vector load feeds 2x the
-// entries of kernels_strips2.cu.  The price is shared memory: all sampled
+// entries of kernels_strips2.cu (the two positions are adjacent, 2 lane and
+// 2 lane + 1, so every stage access is one 8-byte load or store).  The price is shared memory: all sampled
 // lines of a 64-position tile are resident in ONE single-buffered stage per
 // CTA (16 warps on the same tile), so the next tile is prefetched into L2
 // (cp.async.bulk.prefetch) while the current one is computed.
@@ -22,7 +23,7 @@ namespace ircur {
 
 constexpr int kS3NT = 512;
 constexpr int kS3NW = kS3NT / 32;
-constexpr int kS3TX = 64;  // positions per tile (x and x + 32 per lane)
+constexpr int kS3TX = 64;  // positions per tile (2 lane, 2 lane + 1 per lane)
 
 struct Strips3Layout {
   int RP, maxp;
@@ -130,8 +131,8 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
     SPH(0);
     Pair<float> b[R];
 #pragma unroll
-    for (int tt = 0; tt < R; ++tt) b[tt].v = make_float2(bst[tt * kS3TX + lane], bst[tt * kS3TX + lane + 32]);
-    // ---- pass 1: Phase I/II in place + factor partials (positions x, x + 32 per FFMA2)
+    for (int tt = 0; tt < R; ++tt) b[tt].v = reinterpret_cast<const float2*>(bst + tt * kS3TX)[lane];
+    // ---- pass 1: Phase I/II in place + factor partials (positions 2 lane, 2 lane + 1 per FFMA2)
     Pair<float> acc[R];
 #pragma unroll
     for (int tt = 0; tt < R; ++tt) acc[tt] = Pair<float>::splat(0.f);
@@ -139,11 +140,11 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
     const bool accum = mode != kStripFinish;
     for (int kp = w; kp < np; kp += kS3NW) {
       const float2* va = lvec + (size_t)kp * 3 * RPc;
-      float* c0 = stage + (size_t)(2 * kp) * kS3TX + lane;
-      float* c1 = c0 + kS3TX;
+      float2* c0 = reinterpret_cast<float2*>(stage + (size_t)(2 * kp) * kS3TX) + lane;
+      float2* c1 = c0 + kS3TX / 2;
       Pair<float> d0, d1;
-      d0.v = make_float2(c0[0], c0[32]);
-      d1.v = make_float2(c1[0], c1[32]);
+      d0.v = *c0;
+      d1.v = *c1;
       float2 av = va[0];
       Pair<float> l0, l1;
       l0.v = __fmul2_rn(make_float2(av.x, av.x), b[0].v);
@@ -158,10 +159,8 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
       const Pair<float> e1 = keep_pair(d1, l1, zt);
       den = pfma(d0, d0, den);
       den = pfma(d1, d1, den);
-      c0[0] = e0.v.x;
-      c0[32] = e0.v.y;
-      c1[0] = e1.v.x;
-      c1[32] = e1.v.y;
+      *c0 = e0.v;
+      *c1 = e1.v;
       if (accum) {
         const float2* vw = va + RPc;
 #pragma unroll
@@ -178,8 +177,7 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
     if (accum) {
 #pragma unroll
       for (int tt = 0; tt < R; ++tt) {
-        red[(w * R + tt) * kS3TX + lane] = acc[tt].v.x;
-        red[(w * R + tt) * kS3TX + lane + 32] = acc[tt].v.y;
+        reinterpret_cast<float2*>(red + (w * R + tt) * kS3TX)[lane] = acc[tt].v;
       }
     }
     __syncthreads();
@@ -208,15 +206,15 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
       // ---- pass 2: stopping residual on the thresholded tile
       Pair<float> f[R];
 #pragma unroll
-      for (int tt = 0; tt < R; ++tt) f[tt].v = make_float2(fnew[tt * kS3TX + lane], fnew[tt * kS3TX + lane + 32]);
+      for (int tt = 0; tt < R; ++tt) f[tt].v = reinterpret_cast<const float2*>(fnew + tt * kS3TX)[lane];
       Pair<float> res = Pair<float>::splat(0.f);
       for (int kp = w; kp < np; kp += kS3NW) {
         const float2* vr = lvec + (size_t)kp * 3 * RPc + 2 * RPc;
-        const float* c0 = stage + (size_t)(2 * kp) * kS3TX + lane;
-        const float* c1 = c0 + kS3TX;
+        const float2* c0 = reinterpret_cast<const float2*>(stage + (size_t)(2 * kp) * kS3TX) + lane;
+        const float2* c1 = c0 + kS3TX / 2;
         Pair<float> e0, e1;
-        e0.v = make_float2(c0[0], c0[32]);
-        e1.v = make_float2(c1[0], c1[32]);
+        e0.v = *c0;
+        e1.v = *c1;
         float2 rv = vr[0];
         Pair<float> l0, l1;
         l0.v = __fmul2_rn(make_float2(rv.x, rv.x), f[0].v);
