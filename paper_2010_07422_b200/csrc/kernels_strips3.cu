@@ -82,14 +82,63 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
   const int tiles0 = a.s[0].tiles;
   const int total = tiles0 + a.s[1].tiles;
   __syncthreads();
+  // The stage is filled in two halves by line pairs: A = pairs [0, npA) with
+  // the old factor's rows and the override map, B = the rest.  A of the next
+  // tile is issued once pass 2 is done with A of this one, and B once pass 2
+  // is done with B, so the fills overlap pass 2 (B) and pass 1 (A) instead of
+  // stalling the CTA.  Each warp still walks its line pairs in ascending
+  // order, so the factor and residual sums are those of a single pass.
+  auto halves = [&](int t, int& np, int& npA) {
+    const int q = t < tiles0 ? 0 : 1;
+    np = (a.s[q].nk + 1) / 2;
+    npA = (np + 1) / 2;
+  };
+  auto issue_half = [&](int t, int h) {
+    const int q = t < tiles0 ? 0 : 1;
+    const StripDesc<float>& s = a.s[q];
+    const int nl = s.nk;
+    int np, npA;
+    halves(t, np, npA);
+    const int nl2 = 2 * np;
+    const int x0 = (t - (q ? tiles0 : 0)) * kS3TX;
+    const float* const* lp = lptr + q * (2 * L.maxp + R);
+    const int ch = tid & 15;
+    const int pos = x0 + ch * 4;
+    const int rem = s.npos - pos;
+    const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
+    const int sp = bytes ? pos : x0;
+    const int v0 = h ? 2 * npA : 0, v1 = h ? nl2 : 2 * npA + R;  // (half A: + the R rows, mapped past nl2)
+    for (int u = v0 + (tid >> 4); u < v1; u += kS3NT / 16) {
+      const int v = (!h && u >= 2 * npA) ? nl2 + (u - 2 * npA) : u;
+      float* dst = v < nl2 ? stage + (size_t)v * kS3TX : bst + (size_t)(v - nl2) * kS3TX;
+      const float* src = v < nl ? lp[v] : (v < nl2 ? lp[0] : lp[nl + (v - nl2)]);
+      const int bb = v < nl || v >= nl2 ? bytes : 0;  // the padding line of an odd count reads zeros
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s3_smem(dst + ch * 4)), "l"(src + sp),
+                   "r"(bb)
+                   : "memory");
+    }
+    if (!h && tid < 16) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s3_smem(omt + ch * 4)),
+                   "l"(s.omap + sp), "r"(bytes)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (bx < total) {
+    issue_half(bx, 0);
+    issue_half(bx, 1);
+  }
   int cur = -1;
   for (int t = bx; t < total; t += nbx) {
     const int q = t < tiles0 ? 0 : 1;
     const StripDesc<float>& s = a.s[q];
-    const int nl = s.nk, np = (nl + 1) / 2, nl2 = 2 * np;
+    const int nl = s.nk, np = (nl + 1) / 2;
+    const int npA = (np + 1) / 2;
     const int mode = s.mode;
     const int x0 = (t - (q ? tiles0 : 0)) * kS3TX;
-    const float* const* lp = lptr + q * (2 * L.maxp + R);
+    const int tn = t + nbx;
+    const bool next = tn < total;
+    const bool same_next = next && ((tn < tiles0) == (t < tiles0));  // the next tile's halves line up with these
     if (q != cur) {  // per-pair line vectors of this strip: (A | W | Res)[t] for lines 2kp, 2kp+1
       for (int e = tid; e < np * 3 * RPc; e += kS3NT) {
         const int kp = e / (3 * RPc), rem = e - kp * 3 * RPc, v = rem / RPc, tt = rem - v * RPc;
@@ -105,28 +154,7 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
       cur = q;
     }
     SPH(6);
-    // ---- stage the tile: 16 x 16-byte chunks per 256-byte line segment
-    {
-      const int ch = tid & 15;
-      const int pos = x0 + ch * 4;
-      const int rem = s.npos - pos;
-      const int bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
-      const int sp = bytes ? pos : x0;
-      for (int v = tid >> 4; v < nl2 + R; v += kS3NT / 16) {
-        float* dst = v < nl2 ? stage + (size_t)v * kS3TX : bst + (size_t)(v - nl2) * kS3TX;
-        const float* src = v < nl ? lp[v] : (v < nl2 ? lp[0] : lp[nl + (v - nl2)]);
-        const int b = v < nl || v >= nl2 ? bytes : 0;  // the padding line of an odd count reads zeros
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s3_smem(dst + ch * 4)),
-                     "l"(src + sp), "r"(b)
-                     : "memory");
-      }
-      if (tid < 16) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s3_smem(omt + ch * 4)),
-                     "l"(s.omap + sp), "r"(bytes)
-                     : "memory");
-      }
-      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-    }
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // half A of this tile (B may be in flight)
     __syncthreads();
     SPH(0);
     Pair<float> b[R];
@@ -138,39 +166,45 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
     for (int tt = 0; tt < R; ++tt) acc[tt] = Pair<float>::splat(0.f);
     Pair<float> den = Pair<float>::splat(0.f);
     const bool accum = mode != kStripFinish;
-    for (int kp = w; kp < np; kp += kS3NW) {
-      const float2* va = lvec + (size_t)kp * 3 * RPc;
-      float2* c0 = reinterpret_cast<float2*>(stage + (size_t)(2 * kp) * kS3TX) + lane;
-      float2* c1 = c0 + kS3TX / 2;
-      Pair<float> d0, d1;
-      d0.v = *c0;
-      d1.v = *c1;
-      float2 av = va[0];
-      Pair<float> l0, l1;
-      l0.v = __fmul2_rn(make_float2(av.x, av.x), b[0].v);
-      l1.v = __fmul2_rn(make_float2(av.y, av.y), b[0].v);
+    auto pass1 = [&](int k_lo, int k_hi) {
+      for (int kp = w + ((k_lo > w ? k_lo - w : 0) + kS3NW - 1) / kS3NW * kS3NW; kp < k_hi; kp += kS3NW) {
+        const float2* va = lvec + (size_t)kp * 3 * RPc;
+        float2* c0 = reinterpret_cast<float2*>(stage + (size_t)(2 * kp) * kS3TX) + lane;
+        float2* c1 = c0 + kS3TX / 2;
+        Pair<float> d0, d1;
+        d0.v = *c0;
+        d1.v = *c1;
+        float2 av = va[0];
+        Pair<float> l0, l1;
+        l0.v = __fmul2_rn(make_float2(av.x, av.x), b[0].v);
+        l1.v = __fmul2_rn(make_float2(av.y, av.y), b[0].v);
 #pragma unroll
-      for (int tt = 1; tt < R; ++tt) {
-        av = va[tt];
-        l0.v = __ffma2_rn(make_float2(av.x, av.x), b[tt].v, l0.v);
-        l1.v = __ffma2_rn(make_float2(av.y, av.y), b[tt].v, l1.v);
-      }
-      const Pair<float> e0 = keep_pair(d0, l0, zt);
-      const Pair<float> e1 = keep_pair(d1, l1, zt);
-      den = pfma(d0, d0, den);
-      den = pfma(d1, d1, den);
-      *c0 = e0.v;
-      *c1 = e1.v;
-      if (accum) {
-        const float2* vw = va + RPc;
+        for (int tt = 1; tt < R; ++tt) {
+          av = va[tt];
+          l0.v = __ffma2_rn(make_float2(av.x, av.x), b[tt].v, l0.v);
+          l1.v = __ffma2_rn(make_float2(av.y, av.y), b[tt].v, l1.v);
+        }
+        const Pair<float> e0 = keep_pair(d0, l0, zt);
+        const Pair<float> e1 = keep_pair(d1, l1, zt);
+        den = pfma(d0, d0, den);
+        den = pfma(d1, d1, den);
+        *c0 = e0.v;
+        *c1 = e1.v;
+        if (accum) {
+          const float2* vw = va + RPc;
 #pragma unroll
-        for (int tt = 0; tt < R; ++tt) {
-          const float2 wv = vw[tt];
-          acc[tt].v = __ffma2_rn(make_float2(wv.x, wv.x), e0.v, acc[tt].v);
-          acc[tt].v = __ffma2_rn(make_float2(wv.y, wv.y), e1.v, acc[tt].v);
+          for (int tt = 0; tt < R; ++tt) {
+            const float2 wv = vw[tt];
+            acc[tt].v = __ffma2_rn(make_float2(wv.x, wv.x), e0.v, acc[tt].v);
+            acc[tt].v = __ffma2_rn(make_float2(wv.y, wv.y), e1.v, acc[tt].v);
+          }
         }
       }
-    }
+    };
+    pass1(0, npA);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // half B
+    __syncthreads();
+    pass1(npA, np);
     SPH(1);
     const double den_t = accum ? (double)den.v.x + (double)den.v.y : 0.0;
     double res_t = 0.0;
@@ -200,15 +234,17 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
       fnew[o] = v;
       if (x0 + x < s.npos) s.Fnew[(int64_t)tt * s.ldf + x0 + x] = v;
     }
-    __syncthreads();
+    __syncthreads();  // (bst and omt are consumed: the next tile's half A may land)
     SPH(3);
+    Pair<float> res = Pair<float>::splat(0.f);
+    Pair<float> f[R];
     if (mode != kStripPartial) {
-      // ---- pass 2: stopping residual on the thresholded tile
-      Pair<float> f[R];
 #pragma unroll
       for (int tt = 0; tt < R; ++tt) f[tt].v = reinterpret_cast<const float2*>(fnew + tt * kS3TX)[lane];
-      Pair<float> res = Pair<float>::splat(0.f);
-      for (int kp = w; kp < np; kp += kS3NW) {
+    }
+    // ---- pass 2: stopping residual on the thresholded tile
+    auto pass2 = [&](int k_lo, int k_hi) {
+      for (int kp = w + ((k_lo > w ? k_lo - w : 0) + kS3NW - 1) / kS3NW * kS3NW; kp < k_hi; kp += kS3NW) {
         const float2* vr = lvec + (size_t)kp * 3 * RPc + 2 * RPc;
         const float2* c0 = reinterpret_cast<const float2*>(stage + (size_t)(2 * kp) * kS3TX) + lane;
         const float2* c1 = c0 + kS3TX / 2;
@@ -230,6 +266,14 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
         res = pfma(r0, r0, res);
         res = pfma(r1, r1, res);
       }
+    };
+    if (mode != kStripPartial) pass2(0, npA);
+    if (same_next) {  // half A of this tile is free
+      __syncthreads();
+      issue_half(tn, 0);
+    }
+    if (mode != kStripPartial) {
+      pass2(npA, np);
       res_t = (double)res.v.x + (double)res.v.y;
     }
     SPH(4);
@@ -241,6 +285,10 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
       }
     }
     __syncthreads();  // stage, fnew, red free for the next tile
+    if (next) {
+      if (!same_next) issue_half(tn, 0);  // (the other strip: its halves split the lines elsewhere)
+      issue_half(tn, 1);
+    }
     if (tid == 0) {
       double sd = 0.0, sr = 0.0;
       for (int ww = 0; ww < kS3NW; ++ww) {
