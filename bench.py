@@ -109,6 +109,8 @@ def parse():
     ap.add_argument("--threaded", action="store_true",
                     help="cfg4: the round-1 path (host threads, one solve each) instead of the batched launches")
     ap.add_argument("--svd-cs", type=int, default=0, help="cfg4 batched: SVD cluster size (0 = smallest that fits)")
+    ap.add_argument("--python-loop", action="store_true",
+                    help="sharded path: drive the iterations from Python (dist.py) instead of ircur_shard_run")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded NCCL path even at N=1 (tests the multi-GPU code on one GPU)")
     return ap.parse_args()
@@ -405,7 +407,8 @@ def run_sharded(args, rank, world, local):
 
     def one(Din):
         return irdist.run_collective(irdist.solve_shard_program(Din, cfg, n1=n1, row0=r0, colmajor=cm,
-                                                                profile=not args.no_profile))
+                                                                profile=not args.no_profile,
+                                                                native=not args.python_loop))
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -488,7 +491,9 @@ def run_sharded(args, rank, world, local):
                        "iterations": res.trace.iterations, "converged": res.trace.converged,
                        "final_e": res.trace.errors[-1], "launched_iterations": res.launched,
                        "l2": "inputs larger than L2 (D >= 400 MB), no flush",
-                       "parallelism": f"row-sharded x{world} (NCCL all-reduce of U, Q partials, 4 sums)"},
+                       "parallelism": f"row-sharded x{world} (NCCL all-reduce of U, Q partials, 4 sums)",
+                       "loop": "python (dist.py)" if args.python_loop
+                       else "library (ircur_shard_run, NCCL from C++)"},
             "roofline": roofline,
             "gpu_launches": int(lt.item()),
             "clocks": clk.summary(),

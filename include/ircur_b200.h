@@ -186,6 +186,20 @@ int ircur_poll(ircur_ctx_t ctx, int* done, int* iterations);
 int ircur_shard_finish(ircur_ctx_t ctx, const double* zetas, int mode, int* iterations,
                        int* converged, double* errors, float* iter_ms);
 
+/* Native sharded loop.  ircur_nccl_unique_id writes an NCCL unique id (128
+ * bytes) on one rank; every rank passes it to ircur_shard_comm_init (a
+ * collective: all ranks call it together) to give its context a communicator
+ * (the process's own NCCL, found with dlopen; no link-time dependency).
+ * ircur_shard_run then runs the whole loop after ircur_prepare /
+ * ircur_slab_sqnorms: per iteration the four phases above with the three
+ * all-reduces on the context's stream, run-ahead `ahead` iterations, and the
+ * trace as ircur_shard_finish returns it; *launched = iterations issued
+ * (min(max_iter, K + ahead) on every rank). */
+int ircur_nccl_unique_id(void* id, int64_t bytes);
+int ircur_shard_comm_init(ircur_ctx_t ctx, const void* id, int nranks, int rank);
+int ircur_shard_run(ircur_ctx_t ctx, const double* zetas, double eps, int mode, int max_iter, int ahead,
+                    int* iterations, int* converged, double* errors, float* iter_ms, int* launched);
+
 /* Final CUR/sparse strips of the last completed iteration, fp64, written to
  * device or host pointers (cudaMemcpyDefault):  C  local_rows x |J|,
  * R |I_loc| x n2, S_rows |I_loc| x n2, S_cols local_rows x |J| (row-major).

@@ -4,6 +4,8 @@
 // buffers, core, SVD scratch, index sets, trace) on one device + stream and
 // drives the device-resident iteration loop of solver.py:358-414.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -185,6 +187,8 @@ struct ircur_ctx {
   int strips_cs = 1;
   // row sharding: exchange buffers (all-reduced by the caller between phases)
   void* Qpart = nullptr;     // R x ldq: local partial sums of Q_{k+1} = W^T R
+  void* nccl_comm = nullptr; // ircur_shard_comm_init: the communicator ircur_shard_run all-reduces over
+  int nccl_nranks = 0, nccl_rank = -1;
   double* scal = nullptr;    // 8: {den_rows, res_rows, den_cols, res_cols} local sums
   int ncta_a = 0;            // CTAs of the last kStripPartial launch (partials offset)
   // last completed iteration
@@ -829,6 +833,46 @@ void drop_pre(ircur_ctx* c) {
 
 }  // namespace
 
+
+// ---------------------------------------------------------------- NCCL
+// The collectives of the native sharded loop (ircur_shard_run) go through the
+// NCCL the host process already loaded (torch's), found with dlopen
+// RTLD_NOLOAD, else the first libnccl.so.2 on the search path; nccl.h
+// supplies the types only, so the library has no link-time NCCL dependency.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy && a.error_string;
+    return a;
+  }();
+  return api;
+}
+
+void drop_comm(ircur_ctx* c) {
+  if (c->nccl_comm && nccl_api().ok) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl_comm));
+  c->nccl_comm = nullptr;
+  c->nccl_nranks = 0;
+  c->nccl_rank = -1;
+}
+
 extern "C" {
 
 int ircur_abi_version(void) { return IRCUR_ABI_VERSION; }
@@ -950,6 +994,7 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   if (!c) return IRCUR_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_comm(c);
   void* bufs[] = {c->Dt, c->d_rows, c->d_cols, c->Pt[0], c->Pt[1], c->Qt[0], c->Qt[1], c->U, c->U2,
                   c->PoldI[0], c->QoldJ[0], c->Wr[0], c->PI[0], c->VS[0], c->QJ[0], c->W[0], c->sigma[0],
                   c->V[0], c->inv[0], c->PoldI[1], c->QoldJ[1], c->Wr[1], c->PI[1], c->VS[1], c->QJ[1],
@@ -2245,4 +2290,86 @@ int ircur_gen_baseline(void* D, int dtype, int64_t ldd, int64_t n1, int64_t n2, 
   return rc;
 }
 
+
+// ---- native row-sharded loop (NCCL) -------------------------------------
+int ircur_nccl_unique_id(void* id, int64_t bytes) {
+  if (!id || bytes < (int64_t)sizeof(ncclUniqueId)) return fail(IRCUR_EINVAL, "id buffer below 128 bytes");
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return fail(IRCUR_EINVAL, "NCCL (libnccl.so.2) not available in this process");
+  ncclUniqueId u;
+  const ncclResult_t r = n.get_unique_id(&u);
+  if (r != ncclSuccess) return fail(IRCUR_ECUDA, std::string("ncclGetUniqueId: ") + n.error_string(r));
+  std::memcpy(id, &u, sizeof(u));
+  return IRCUR_OK;
+}
+
+int ircur_shard_comm_init(ircur_ctx_t c, const void* id, int nranks, int rank) {
+  if (!c || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(IRCUR_EINVAL, "bad communicator arguments");
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return fail(IRCUR_EINVAL, "NCCL (libnccl.so.2) not available in this process");
+  IR_CUDA(cudaSetDevice(c->device));
+  drop_comm(c);
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = n.comm_init_rank(&comm, nranks, u, rank);  // collective across the ranks
+  if (r != ncclSuccess) return fail(IRCUR_ECUDA, std::string("ncclCommInitRank: ") + n.error_string(r));
+  c->nccl_comm = comm;
+  c->nccl_nranks = nranks;
+  c->nccl_rank = rank;
+  return IRCUR_OK;
+}
+
+// The per-iteration sequence dist.solve_shard_program drives from Python
+// (phases CORE, FACTOR, RESID, STOP with the all-reduces of U, the Q
+// partials and the 4 sums between them, solver.py:360-410), issued from here
+// on the context's stream with the context's communicator: one call per
+// solve instead of four library calls and three collectives per iteration.
+// Run-ahead as in the Python driver: at most `ahead` iterations past the
+// last one the device finished; after the device reports the stop at K every
+// rank has issued exactly min(max_iter, K + ahead) iterations (the same on
+// every rank: K comes from all-reduced sums).
+int ircur_shard_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_iter, int ahead,
+                    int* iterations, int* converged, double* errors, float* iter_ms, int* launched_out) {
+  if (!c || !c->D || !zetas) return fail(IRCUR_EINVAL, "null context, D or zetas");
+  if (!c->nccl_comm) return fail(IRCUR_EINVAL, "no communicator (ircur_shard_comm_init)");
+  if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
+  if (ahead < 1) return fail(IRCUR_EINVAL, "ahead must be >= 1");
+  const NcclApi& n = nccl_api();
+  IR_CUDA(cudaSetDevice(c->device));
+  if (int rc = ircur_shard_reset(c)) return rc;
+  ncclComm_t comm = static_cast<ncclComm_t>(c->nccl_comm);
+  const ncclDataType_t qdt = c->dtype == IRCUR_F32 ? ncclFloat32 : ncclFloat64;
+  const size_t u_elems = (size_t)c->max_rows * c->max_cols, q_elems = (size_t)c->r * c->ldq;
+  auto allreduce = [&](void* buf, size_t count, ncclDataType_t dt) -> int {
+    const ncclResult_t r = n.all_reduce(buf, buf, count, dt, ncclSum, comm, c->stream);
+    if (r != ncclSuccess) return fail(IRCUR_ECUDA, std::string("ncclAllReduce: ") + n.error_string(r));
+    return IRCUR_OK;
+  };
+  volatile int* hf = c->h_flags;
+  int launched = 0, stop_at = max_iter;
+  while (launched < stop_at) {
+    const int done = hf[0], seen = hf[1];
+    if (done) {
+      stop_at = std::min(stop_at, seen + ahead);
+      if (launched >= stop_at) break;
+    } else if (launched >= seen + ahead) {  // the device is `ahead` iterations behind
+      const cudaError_t q = cudaStreamQuery(c->stream);
+      if (q != cudaSuccess && q != cudaErrorNotReady)
+        return fail(IRCUR_ECUDA, std::string("stream: ") + cudaGetErrorString(q));
+      continue;
+    }
+    const int k = launched, set = mode == IRCUR_RESAMPLED ? k : 0;
+    if (int rc = ircur_shard_phase(c, IRCUR_SHARD_CORE, k, set, zetas[k], eps, max_iter)) return rc;
+    if (int rc = allreduce(c->U, u_elems, ncclFloat64)) return rc;
+    if (int rc = ircur_shard_phase(c, IRCUR_SHARD_FACTOR, k, set, zetas[k], eps, max_iter)) return rc;
+    if (int rc = allreduce(c->Qpart, q_elems, qdt)) return rc;
+    if (int rc = ircur_shard_phase(c, IRCUR_SHARD_RESID, k, set, zetas[k], eps, max_iter)) return rc;
+    if (int rc = allreduce(c->scal, 4, ncclFloat64)) return rc;
+    if (int rc = ircur_shard_phase(c, IRCUR_SHARD_STOP, k, set, zetas[k], eps, max_iter)) return rc;
+    ++launched;
+  }
+  if (launched_out) *launched_out = launched;
+  return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
+}
 }  // extern "C"

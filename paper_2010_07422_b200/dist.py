@@ -90,12 +90,17 @@ def _gpu_engine(D_local, n1: int, row0: int, config: SolverConfig, m_rows: int, 
 
 
 def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, colmajor="auto",
-                        ahead: int = 3, engine_factory=None, device=None, compute_dtype=None, profile=False):
+                        ahead: int = 3, engine_factory=None, device=None, compute_dtype=None, profile=False,
+                        native: bool = False):
     """Generator: this rank's share of a row-sharded `solve` (solver.py:304-416).
 
     D_local holds rows [row0, row0 + D_local.shape[0]) of the n1 x n2 matrix.
     Returns (via StopIteration.value) a ShardResult.  profile=True records
     the strip launches' events (engine.profile(iterations)["strips_ms"]).
+    native=True runs the iteration loop inside the library (ircur_shard_run:
+    the same phases, collectives and run-ahead, issued from C++ over an NCCL
+    communicator the driver sets up with a ("native_comm", engine) request);
+    the prep exchanges before the loop go through the driver as usual.
     """
     cfg = config
     if len(getattr(D_local, "shape", ())) != 2:
@@ -141,6 +146,10 @@ def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, co
         cfg = replace(cfg, zeta0=max_abs)  # solver.py:342-344
     zetas = [cfg.gamma**k * cfg.zeta0 for k in range(cfg.max_iter)]
     mode = RESAMPLED if resampled else FIXED
+    if native:
+        yield ("native_comm", eng)
+        iters, conv, errors, ms, launched = eng.shard_run(zetas, cfg.eps, mode, cfg.max_iter, ahead)
+        return _shard_result(cfg, eng, sets, row0, n1, n2, zetas, resampled, iters, conv, errors, ms, launched)
     eng.shard_reset()
     U, Qp, scal = eng.shard_buffers()
     launched, stop_at = 0, cfg.max_iter
@@ -163,6 +172,10 @@ def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, co
         eng.shard_phase(SHARD_STOP, k, s, zetas[k], cfg.eps, cfg.max_iter)
         launched += 1
     iters, conv, errors, ms = eng.shard_finish(zetas, mode)
+    return _shard_result(cfg, eng, sets, row0, n1, n2, zetas, resampled, iters, conv, errors, ms, launched)
+
+
+def _shard_result(cfg, eng, sets, row0, n1, n2, zetas, resampled, iters, conv, errors, ms, launched):
     tr = SolverTrace()
     tr.errors = [float(e) for e in errors]
     tr.seconds = [float(t) / 1e3 for t in ms]
@@ -212,6 +225,10 @@ def run_collective(program, group=None):
         req = next(program)
         while True:
             op, payload = req
+            if op == "native_comm":  # an NCCL communicator over the group for the engine's native loop
+                _native_comm(payload, group)
+                req = program.send(None)
+                continue
             if op == "gather":
                 out = [None] * dist.get_world_size(group)
                 dist.all_gather_object(out, payload, group=group)
@@ -222,6 +239,30 @@ def run_collective(program, group=None):
             req = program.send(None)
     except StopIteration as stop:
         return stop.value
+
+
+def _native_comm(eng, group) -> None:
+    """Give `eng` (a library context) a communicator over `group` unless it
+    already holds one for this group: the decision is all-reduced, so every
+    rank takes part in the (collective) initialisation or none does."""
+    import torch
+    import torch.distributed as dist
+
+    from .solver import nccl_unique_id
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    key = getattr(eng, "_comm_key", None)
+    have = key is not None and key[0] == world and key[1] == rank and getattr(eng, "_comm_group", None) is group
+    need = torch.tensor([0 if have else 1], dtype=torch.int64, device=f"cuda:{eng.device}"
+                        if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(need, op=dist.ReduceOp.MAX, group=group)
+    if int(need.item()) == 0:
+        return
+    obj = [nccl_unique_id() if rank == 0 else None]
+    src = 0 if group is None else dist.get_global_rank(group, 0)
+    dist.broadcast_object_list(obj, src=src, group=group)
+    eng.shard_comm_init(obj[0], world, rank)
+    eng._comm_group = group
 
 
 def run_lockstep(programs):
@@ -247,6 +288,8 @@ def run_lockstep(programs):
         if len(ops) != 1:
             raise RuntimeError(f"rank programs diverged: requests {sorted(ops)}")
         op = ops.pop()
+        if op == "native_comm":
+            raise NotImplementedError("the native sharded loop needs one process per GPU (run_collective)")
         sends = [None] * n
         if op == "gather":
             sends = [[r[1] for r in reqs]] * n
@@ -271,7 +314,7 @@ def run_lockstep(programs):
 
 
 def solve_sharded(D_local, config: SolverConfig, observer=None, *, n1: int, row0: int, group=None,
-                  gather: bool = True, colmajor="auto", device=None, compute_dtype=None):
+                  gather: bool = True, colmajor="auto", device=None, compute_dtype=None, native: bool = False):
     """Row-sharded drop-in for `ircur.solve` inside a torch.distributed job:
     every rank passes its row shard of D.  With gather=True every rank gets
     the reference's (CurFactors, SparseEstimate, SolverTrace) on the host;
@@ -279,7 +322,7 @@ def solve_sharded(D_local, config: SolverConfig, observer=None, *, n1: int, row0
     if observer is not None:
         raise NotImplementedError("observer callbacks are supported by the single-GPU solve only")
     res = run_collective(solve_shard_program(D_local, config, n1=n1, row0=row0, colmajor=colmajor,
-                                             device=device, compute_dtype=compute_dtype), group)
+                                             device=device, compute_dtype=compute_dtype, native=native), group)
     if not gather:
         return res
     return run_collective(gather_program(res), group)

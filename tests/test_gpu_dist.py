@@ -106,3 +106,46 @@ def test_sharded_nonfinite_raises():
     with pytest.raises(ValueError, match="non-finite"):
         _sharded(torch.from_numpy(D).cuda(), _cfg(3, linf), 2)
     ir.clear_cache()
+
+
+@pytest.fixture(scope="module")
+def gloo1():
+    """A one-rank torch.distributed group (gloo) for the driver's own
+    exchanges; the native loop brings its own NCCL communicator."""
+    import os
+
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    fresh = not dist.is_initialized()
+    if fresh:
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    yield
+    if fresh:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+def test_native_shard_loop_bitwise_equals_python_loop(gloo1, dtype, mode):
+    """ircur_shard_run (the loop in the library, NCCL all-reduces) issues the
+    same phases and collectives as the Python driver: bitwise the same trace,
+    strips and core, the same number of launched iterations; a second solve
+    reuses the communicator."""
+    from paper_2010_07422_b200.dist import run_collective
+
+    D, linf = _problem(300, 260, 4, seed=17)
+    cfg = _cfg(4, linf, mode, eps=1e-5 if dtype == np.float32 else 1e-9)
+    Dd = torch.from_numpy(D.astype(dtype)).cuda()
+    outs = []
+    for native in (False, True, True):
+        res = run_collective(solve_shard_program(Dd, cfg, n1=300, row0=0, native=native))
+        outs.append((res.launched, run_collective(gather_program(res))))
+    (l0, (c0, s0, t0)) = outs[0]
+    for li, (ci, si, ti) in outs[1:]:
+        assert li == l0
+        assert ti.iterations == t0.iterations and ti.converged == t0.converged and ti.errors == t0.errors
+        for a, b in ((ci.C, c0.C), (ci.R, c0.R), (si.row_values, s0.row_values), (si.col_values, s0.col_values),
+                     (ci.core_pinv.sigma, c0.core_pinv.sigma)):
+            np.testing.assert_array_equal(a, b)
+    ir.clear_cache()
