@@ -186,19 +186,24 @@ int ircur_poll(ircur_ctx_t ctx, int* done, int* iterations);
 int ircur_shard_finish(ircur_ctx_t ctx, const double* zetas, int mode, int* iterations,
                        int* converged, double* errors, float* iter_ms);
 
-/* Native sharded loop.  ircur_nccl_unique_id writes an NCCL unique id (128
- * bytes) on one rank; every rank passes it to ircur_shard_comm_init (a
- * collective: all ranks call it together) to give its context a communicator
- * (the process's own NCCL, found with dlopen; no link-time dependency).
- * ircur_shard_run then runs the whole loop after ircur_prepare /
- * ircur_slab_sqnorms: per iteration the four phases above with the three
- * all-reduces on the context's stream, run-ahead `ahead` iterations, and the
- * trace as ircur_shard_finish returns it; *launched = iterations issued
- * (min(max_iter, K + ahead) on every rank). */
+/* Native sharded loop.  ircur_nccl_unique_id writes one NCCL unique id per
+ * 128 bytes of `bytes` on one rank; every rank passes n_ids (1 or 2) of them
+ * to ircur_shard_comm_init (a collective: all ranks call it together) to give
+ * its context its communicators (the process's own NCCL, found with dlopen;
+ * no link-time dependency).  ircur_shard_run then runs the whole loop after
+ * ircur_prepare / ircur_slab_sqnorms: per iteration the four phases above
+ * with the three all-reduces, run-ahead `ahead` iterations, and the trace as
+ * ircur_shard_finish returns it; *launched = iterations issued (min(max_iter,
+ * K + ahead) on every rank).  overlap = 1 with two communicators (fp32,
+ * strips3 eligible): the single-GPU two-stream schedule, the SVD of k + 1
+ * (after the all-reduces of the sampled Q partials and of U) beside the
+ * strips of k (all-reduces of the Q partials and the 4 sums), one
+ * communicator per stream. */
 int ircur_nccl_unique_id(void* id, int64_t bytes);
-int ircur_shard_comm_init(ircur_ctx_t ctx, const void* id, int nranks, int rank);
+int ircur_shard_comm_init(ircur_ctx_t ctx, const void* ids, int n_ids, int nranks, int rank);
 int ircur_shard_run(ircur_ctx_t ctx, const double* zetas, double eps, int mode, int max_iter, int ahead,
-                    int* iterations, int* converged, double* errors, float* iter_ms, int* launched);
+                    int overlap, int* iterations, int* converged, double* errors, float* iter_ms,
+                    int* launched);
 
 /* Final CUR/sparse strips of the last completed iteration, fp64, written to
  * device or host pointers (cudaMemcpyDefault):  C  local_rows x |J|,

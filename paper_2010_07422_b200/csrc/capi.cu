@@ -188,6 +188,7 @@ struct ircur_ctx {
   // row sharding: exchange buffers (all-reduced by the caller between phases)
   void* Qpart = nullptr;     // R x ldq: local partial sums of Q_{k+1} = W^T R
   void* nccl_comm = nullptr; // ircur_shard_comm_init: the communicator ircur_shard_run all-reduces over
+  void* nccl_comm2 = nullptr; // (and a second one for the overlapped loop's strip stream)
   int nccl_nranks = 0, nccl_rank = -1;
   double* scal = nullptr;    // 8: {den_rows, res_rows, den_cols, res_cols} local sums
   int ncta_a = 0;            // CTAs of the last kStripPartial launch (partials offset)
@@ -868,9 +869,184 @@ const NcclApi& nccl_api() {
 
 void drop_comm(ircur_ctx* c) {
   if (c->nccl_comm && nccl_api().ok) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl_comm));
+  if (c->nccl_comm2 && nccl_api().ok) nccl_api().comm_destroy(static_cast<ncclComm_t>(c->nccl_comm2));
   c->nccl_comm = nullptr;
+  c->nccl_comm2 = nullptr;
   c->nccl_nranks = 0;
   c->nccl_rank = -1;
+}
+
+
+// Row-sharded overlapped loop (ircur_shard_run with overlap): the two-stream
+// schedule of run_overlap with the all-reduces of the sharded phases.  Chain
+// stream sA (communicator 1): sampled(k) [Q_k(:,J_{k+1}) as local partial
+// sums over this rank's rows of I_k, the override on rank 0 only, P_k at this
+// rank's rows of I_{k+1}] -> all-reduce -> core(k+1) on the local rows of
+// I_{k+1} -> all-reduce U -> Gram + SVD(k+1).  Strip stream sB (communicator
+// 2): strips(k) [column strip whole, row strip partial] -> all-reduce Q
+// partials -> row strip finish + sums -> all-reduce the 4 sums -> stop test.
+// Every rank issues the same iterations: the loop stops issuing at
+// min(max_iter, K + ahead) once the device reported the stop at K.
+bool shard_overlap_eligible(ircur_ctx* c, int mode, int max_iter) {
+  if (c->dtype != IRCUR_F32 || c->r > 16 || !c->Dt) return false;
+  const int nsets = mode == IRCUR_FIXED ? 1 : std::min(max_iter, c->n_sets);
+  for (int s = 0; s < nsets; ++s) {
+    const IterSets q = iter_sets(c, s);
+    const StripsArgs<float> a = strips_args<float>(c, s, q, 1.0);
+    if (!strips3_selected(a, c->r)) return false;  // (the sampled-factor kernel reproduces strips3)
+  }
+  return true;
+}
+
+int run_shard_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max_iter, int ahead,
+                      int* iterations, int* converged, double* errors, float* iter_ms, int* launched_out) {
+  const NcclApi& n = nccl_api();
+  if (int rc = ircur_shard_reset(c)) return rc;
+  if (int rc = overlap_setup(c)) return rc;
+  c->last_run_overlapped = 1;
+  c->shard_prof = c->overlap_prof = c->profiling;  // strips: partial + finish launches; svd slot: the chain
+  cudaStream_t us = c->stream, sA = c->sA, sB = c->sB;
+  ncclComm_t cA = static_cast<ncclComm_t>(c->nccl_comm), cB = static_cast<ncclComm_t>(c->nccl_comm2);
+  const int R = c->r;
+  const size_t u_elems = (size_t)c->max_rows * c->max_cols, q_elems = (size_t)c->r * c->ldq;
+  const char* split = std::getenv("IRCUR_SHARD_SPLIT");
+  const bool one = c->nccl_nranks == 1 && !(split && std::atoi(split) != 0);
+  auto allreduce = [&](void* buf, size_t count, ncclDataType_t dt, ncclComm_t comm, cudaStream_t st) -> int {
+    if (one) return IRCUR_OK;  // one rank: the all-reduce is the identity
+    const ncclResult_t r = n.all_reduce(buf, buf, count, dt, ncclSum, comm, st);
+    if (r != ncclSuccess) return fail(IRCUR_ECUDA, std::string("ncclAllReduce: ") + n.error_string(r));
+    return IRCUR_OK;
+  };
+  auto ev = [&](int k, int which) { return c->ovev[(size_t)k * 5 + which]; };  // 0 gate 1 svd 2 strips 3 sampled 4 fin
+  auto set_of = [&](int k) { return mode == IRCUR_FIXED ? 0 : k; };
+  c->err_lag = c->err_lag_env ? c->err_lag_env : 2;  // the fp32 sequential lag
+  c->seq_presampled = false;
+  // one rank: nothing to exchange, so no all-reduce is issued and the row
+  // strip runs fused (IRCUR_SHARD_SPLIT=1 keeps the N > 1 sequence: split
+  // strips and NCCL all-reduces, for tests and the overhead measurement)
+  const bool fused = one;
+  IR_CUDA(cudaEventRecord(c->ov_start, us));
+  IR_CUDA(cudaStreamWaitEvent(sA, c->ov_start, 0));
+  IR_CUDA(cudaStreamWaitEvent(sB, c->ov_start, 0));
+  double* Ucore = c->U;  // (sharded contexts: one core buffer, in chain-stream order)
+  auto chain = [&](int k, cudaEvent_t gate) -> int {
+    const IterSets q = iter_sets(c, set_of(k));
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 0], sA));
+    IR_CUDA(cudaMemsetAsync(core_U(c, k), 0, u_elems * sizeof(double), sA));  // other ranks' rows: 0
+    IR_CUDA(launch_core<float>(core_args<float>(c, k, q, zetas[k], k > 0), R, sA));
+    if (int rc = allreduce(core_U(c, k), u_elems, ncclFloat64, cA, sA)) return rc;
+    const SvdArgs sa = svd_args<float>(c, k, q);
+    IR_CUDA(launch_svd<float>(sa, svd_cluster_size(q.nJ, q.mI_all, sa.kk), sA, gate));
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 1], sA));
+    IR_CUDA(cudaEventRecord(ev(k, 1), sA));
+    c->kernel_launches += 3;
+    return IRCUR_OK;
+  };
+  (void)Ucore;
+  auto cover = [&](int set) -> int {
+    if (c->dt_mode != 2 || set < c->covered) return IRCUR_OK;
+    IR_CUDA(cudaStreamSynchronize(sA));
+    IR_CUDA(cudaStreamSynchronize(sB));
+    if (int rc = ensure_cover(c, set)) return rc;
+    IR_CUDA(cudaEventRecord(c->ov_cover, us));
+    IR_CUDA(cudaStreamWaitEvent(sA, c->ov_cover, 0));
+    IR_CUDA(cudaStreamWaitEvent(sB, c->ov_cover, 0));
+    return IRCUR_OK;
+  };
+  if (int rc = cover(set_of(0))) return rc;
+  if (int rc = chain(0, nullptr)) return rc;
+  volatile int* hf = c->h_flags;
+  int launched = 0, stop_at = max_iter;
+  while (launched < stop_at) {
+    const int done = hf[0], seen = hf[1];
+    if (done) {
+      stop_at = std::min(stop_at, seen + ahead);
+      if (launched >= stop_at) break;
+    } else if (launched >= seen + ahead) {  // the device is `ahead` iterations behind
+      const cudaError_t qr = cudaStreamQuery(sB);
+      if (qr != cudaSuccess && qr != cudaErrorNotReady)
+        return fail(IRCUR_ECUDA, std::string("stream: ") + cudaGetErrorString(qr));
+      continue;
+    }
+    const int k = launched;
+    const int set = set_of(k);
+    const bool next = k + 1 < max_iter && set_of(k + 1) < c->n_sets;
+    const IterSets q = iter_sets(c, set);
+    int cs_next = 0;
+    if (next) {
+      if (int rc = cover(set_of(k + 1))) return rc;
+      if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 2), 0));  // Q_{k-1} complete (the finish pass)
+      SampledArgs sm = sampled_args(c, k, q, set_of(k + 1), zetas[k]);
+      sm.s[0].zero_override = c->nccl_rank > 0;  // partial sums: the override counted once
+      IR_CUDA(launch_sampled_factors(sm, R, sA));
+      const IterSets qn = iter_sets(c, set_of(k + 1));
+      if (int rc = allreduce(sm.s[0].out, (size_t)qn.nJ * R, ncclFloat32, cA, sA)) return rc;
+      IR_CUDA(cudaEventRecord(ev(k, 3), sA));
+      if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 4), 0));
+      const SvdArgs san = svd_args<float>(c, k + 1, qn);
+      cs_next = svd_cluster_size(qn.nJ, qn.mI_all, san.kk);
+      if (int rc = chain(k + 1, ev(k, 0))) return rc;
+      c->kernel_launches += 1;
+    }
+    // strips(k) beside SVD(k + 1): row strip partial sums, column strip whole
+    IR_CUDA(cudaStreamWaitEvent(sB, next ? ev(k, 0) : ev(k, 1), 0));
+    const int nsm = std::max(1, c->num_sms - cs_next);
+    if (fused) {  // one rank: the Q partials are the sums, so the row strip runs in one launch
+      int ncta = 0;
+      if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 2], sB));
+      IR_CUDA(launch_strips<float>(strips_args<float>(c, k, q, zetas[k]), R, c->strips_cs, nsm, &ncta, sB));
+      if (c->profiling) {
+        IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 3], sB));
+        IR_CUDA(cudaEventRecord(c->evq[(size_t)k * 2], sB));
+        IR_CUDA(cudaEventRecord(c->evq[(size_t)k * 2 + 1], sB));
+      }
+      IR_CUDA(cudaEventRecord(ev(k, 2), sB));
+      if (next) IR_CUDA(cudaStreamWaitEvent(sB, ev(k, 3), 0));  // (finalize clears the maps sampled(k) reads)
+      FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, true);
+      fa.ncta_rows = ncta;
+      IR_CUDA(launch_finalize(fa, sB));
+    } else {
+      StripsArgs<float> pa = strips_args<float>(c, k, q, zetas[k]);
+      pa.s[0].mode = kStripPartial;
+      pa.s[0].Fnew = (float*)c->Qpart;
+      int ncta_a = 0, ncta_b = 0;
+      if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 2], sB));
+      IR_CUDA(launch_strips<float>(pa, R, c->strips_cs, nsm, &ncta_a, sB));
+      if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 3], sB));
+      if (int rc = allreduce(c->Qpart, q_elems, ncclFloat32, cB, sB)) return rc;
+      StripsArgs<float> pf = strips_args<float>(c, k, q, zetas[k]);
+      pf.s[0].mode = kStripFinish;
+      pf.s[0].Fsrc = (const float*)c->Qpart;
+      pf.s[0].ldfs = c->ldq;
+      pf.s[1].tiles = 0;
+      pf.partials = c->partials + 4 * (size_t)ncta_a;
+      if (c->profiling) IR_CUDA(cudaEventRecord(c->evq[(size_t)k * 2], sB));
+      IR_CUDA(launch_strips<float>(pf, R, c->strips_cs, nsm, &ncta_b, sB));
+      if (c->profiling) IR_CUDA(cudaEventRecord(c->evq[(size_t)k * 2 + 1], sB));
+      IR_CUDA(cudaEventRecord(ev(k, 2), sB));
+      FinalizeArgs fs = finalize_args(c, k, q, eps, max_iter, false);
+      fs.ncta_rows = ncta_a + ncta_b;
+      fs.sums_out = c->scal;
+      IR_CUDA(launch_finalize(fs, sB));
+      if (int rc = allreduce(c->scal, 4, ncclFloat64, cB, sB)) return rc;
+      if (next) IR_CUDA(cudaStreamWaitEvent(sB, ev(k, 3), 0));  // (finalize clears the maps sampled(k) reads)
+      FinalizeArgs fa = finalize_args(c, k, q, eps, max_iter, true);
+      fa.partials = c->scal;
+      fa.ncta_rows = 1;
+      IR_CUDA(launch_finalize(fa, sB));
+    }
+    IR_CUDA(cudaEventRecord(ev(k, 4), sB));
+    IR_CUDA(cudaEventRecord(c->ev[k + 1], sB));
+    c->kernel_launches += 5;
+    ++c->launched_iters;
+    ++launched;
+  }
+  if (launched_out) *launched_out = launched;
+  IR_CUDA(cudaEventRecord(c->ov_endA, sA));
+  IR_CUDA(cudaEventRecord(c->ov_endB, sB));
+  IR_CUDA(cudaStreamWaitEvent(us, c->ov_endA, 0));
+  IR_CUDA(cudaStreamWaitEvent(us, c->ov_endB, 0));
+  return read_trace(c, zetas, mode, iterations, converged, errors, iter_ms);
 }
 
 extern "C" {
@@ -2293,28 +2469,37 @@ int ircur_gen_baseline(void* D, int dtype, int64_t ldd, int64_t n1, int64_t n2, 
 
 // ---- native row-sharded loop (NCCL) -------------------------------------
 int ircur_nccl_unique_id(void* id, int64_t bytes) {
-  if (!id || bytes < (int64_t)sizeof(ncclUniqueId)) return fail(IRCUR_EINVAL, "id buffer below 128 bytes");
+  const int64_t one = (int64_t)sizeof(ncclUniqueId);
+  if (!id || bytes < one) return fail(IRCUR_EINVAL, "id buffer below 128 bytes");
   const NcclApi& n = nccl_api();
   if (!n.ok) return fail(IRCUR_EINVAL, "NCCL (libnccl.so.2) not available in this process");
-  ncclUniqueId u;
-  const ncclResult_t r = n.get_unique_id(&u);
-  if (r != ncclSuccess) return fail(IRCUR_ECUDA, std::string("ncclGetUniqueId: ") + n.error_string(r));
-  std::memcpy(id, &u, sizeof(u));
+  for (int64_t o = 0; o + one <= bytes; o += one) {  // one id per 128 bytes
+    ncclUniqueId u;
+    const ncclResult_t r = n.get_unique_id(&u);
+    if (r != ncclSuccess) return fail(IRCUR_ECUDA, std::string("ncclGetUniqueId: ") + n.error_string(r));
+    std::memcpy(static_cast<char*>(id) + o, &u, sizeof(u));
+  }
   return IRCUR_OK;
 }
 
-int ircur_shard_comm_init(ircur_ctx_t c, const void* id, int nranks, int rank) {
-  if (!c || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(IRCUR_EINVAL, "bad communicator arguments");
+int ircur_shard_comm_init(ircur_ctx_t c, const void* ids, int n_ids, int nranks, int rank) {
+  if (!c || !ids || n_ids < 1 || n_ids > 2 || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(IRCUR_EINVAL, "bad communicator arguments");
   const NcclApi& n = nccl_api();
   if (!n.ok) return fail(IRCUR_EINVAL, "NCCL (libnccl.so.2) not available in this process");
   IR_CUDA(cudaSetDevice(c->device));
   drop_comm(c);
-  ncclUniqueId u;
-  std::memcpy(&u, id, sizeof(u));
-  ncclComm_t comm = nullptr;
-  const ncclResult_t r = n.comm_init_rank(&comm, nranks, u, rank);  // collective across the ranks
-  if (r != ncclSuccess) return fail(IRCUR_ECUDA, std::string("ncclCommInitRank: ") + n.error_string(r));
-  c->nccl_comm = comm;
+  for (int i = 0; i < n_ids; ++i) {
+    ncclUniqueId u;
+    std::memcpy(&u, static_cast<const char*>(ids) + i * sizeof(ncclUniqueId), sizeof(u));
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = n.comm_init_rank(&comm, nranks, u, rank);  // collective across the ranks
+    if (r != ncclSuccess) {
+      drop_comm(c);
+      return fail(IRCUR_ECUDA, std::string("ncclCommInitRank: ") + n.error_string(r));
+    }
+    (i == 0 ? c->nccl_comm : c->nccl_comm2) = comm;
+  }
   c->nccl_nranks = nranks;
   c->nccl_rank = rank;
   return IRCUR_OK;
@@ -2330,13 +2515,19 @@ int ircur_shard_comm_init(ircur_ctx_t c, const void* id, int nranks, int rank) {
 // rank has issued exactly min(max_iter, K + ahead) iterations (the same on
 // every rank: K comes from all-reduced sums).
 int ircur_shard_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_iter, int ahead,
-                    int* iterations, int* converged, double* errors, float* iter_ms, int* launched_out) {
+                    int overlap, int* iterations, int* converged, double* errors, float* iter_ms,
+                    int* launched_out) {
   if (!c || !c->D || !zetas) return fail(IRCUR_EINVAL, "null context, D or zetas");
   if (!c->nccl_comm) return fail(IRCUR_EINVAL, "no communicator (ircur_shard_comm_init)");
   if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
   if (ahead < 1) return fail(IRCUR_EINVAL, "ahead must be >= 1");
+  if (mode == IRCUR_RESAMPLED && c->n_sets < max_iter) return fail(IRCUR_EINVAL, "resampled mode needs max_iter index sets");
   const NcclApi& n = nccl_api();
   IR_CUDA(cudaSetDevice(c->device));
+  if (overlap && c->nccl_comm2 && shard_overlap_eligible(c, mode, max_iter))
+    return run_shard_overlap(c, zetas, eps, mode, max_iter, ahead, iterations, converged, errors, iter_ms,
+                             launched_out);
+  c->last_run_overlapped = 0;
   if (int rc = ircur_shard_reset(c)) return rc;
   ncclComm_t comm = static_cast<ncclComm_t>(c->nccl_comm);
   const ncclDataType_t qdt = c->dtype == IRCUR_F32 ? ncclFloat32 : ncclFloat64;

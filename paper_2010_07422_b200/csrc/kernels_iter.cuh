@@ -84,6 +84,7 @@ struct SampledStrip {
   const int* pos; int pos_off; int npos;
   const int* omap; const float* otherF;         // override: position -> index of the other set
   float* out;
+  int zero_override;                           // row-sharded partial sums: overridden positions give 0 (rank > 0)
 };
 struct SampledArgs {
   SampledStrip s[2];                            // [0] Q(:, J_{k+1}), [1] P(I_{k+1}, :)

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) sampled_factors_kernel(const __grid_const
     const int o = s.omap[x];
     float v;
     if (o >= 0) {
-      v = s.otherF[(int64_t)o * R + t];
+      v = s.zero_override ? 0.f : s.otherF[(int64_t)o * R + t];
     } else {
       v = red[pl][0][t];
 #pragma unroll
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kSmpThreads) sampled_staged_kernel(const __gri
     const int o = s.omap[xs[p]];
     float v;
     if (o >= 0) {
-      v = s.otherF[(int64_t)o * R + t];
+      v = s.zero_override ? 0.f : s.otherF[(int64_t)o * R + t];
     } else {
       v = red[(p * kSmpW) * R + t];
 #pragma unroll

@@ -91,16 +91,18 @@ def _gpu_engine(D_local, n1: int, row0: int, config: SolverConfig, m_rows: int, 
 
 def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, colmajor="auto",
                         ahead: int = 3, engine_factory=None, device=None, compute_dtype=None, profile=False,
-                        native: bool = False):
+                        native: bool = False, overlap: bool = True):
     """Generator: this rank's share of a row-sharded `solve` (solver.py:304-416).
 
     D_local holds rows [row0, row0 + D_local.shape[0]) of the n1 x n2 matrix.
     Returns (via StopIteration.value) a ShardResult.  profile=True records
     the strip launches' events (engine.profile(iterations)["strips_ms"]).
     native=True runs the iteration loop inside the library (ircur_shard_run:
-    the same phases, collectives and run-ahead, issued from C++ over an NCCL
-    communicator the driver sets up with a ("native_comm", engine) request);
-    the prep exchanges before the loop go through the driver as usual.
+    the same phases, collectives and run-ahead, issued from C++ over NCCL
+    communicators the driver sets up with a ("native_comm", engine) request);
+    the prep exchanges before the loop go through the driver as usual.  With
+    overlap (fp32) the library runs the two-stream schedule: the SVD of k + 1
+    beside the strips of k, one communicator per stream.
     """
     cfg = config
     if len(getattr(D_local, "shape", ())) != 2:
@@ -148,7 +150,7 @@ def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, co
     mode = RESAMPLED if resampled else FIXED
     if native:
         yield ("native_comm", eng)
-        iters, conv, errors, ms, launched = eng.shard_run(zetas, cfg.eps, mode, cfg.max_iter, ahead)
+        iters, conv, errors, ms, launched = eng.shard_run(zetas, cfg.eps, mode, cfg.max_iter, ahead, overlap)
         return _shard_result(cfg, eng, sets, row0, n1, n2, zetas, resampled, iters, conv, errors, ms, launched)
     eng.shard_reset()
     U, Qp, scal = eng.shard_buffers()
@@ -258,7 +260,7 @@ def _native_comm(eng, group) -> None:
     dist.all_reduce(need, op=dist.ReduceOp.MAX, group=group)
     if int(need.item()) == 0:
         return
-    obj = [nccl_unique_id() if rank == 0 else None]
+    obj = [nccl_unique_id(2) if rank == 0 else None]
     src = 0 if group is None else dist.get_global_rank(group, 0)
     dist.broadcast_object_list(obj, src=src, group=group)
     eng.shard_comm_init(obj[0], world, rank)

@@ -254,14 +254,16 @@ class Context:
     def shard_phase(self, phase: int, k: int, s: int, zeta: float, eps: float, max_iter: int) -> None:
         _capi.check(self.lib.ircur_shard_phase(self.h, phase, k, s, zeta, eps, max_iter))
 
-    def shard_comm_init(self, uid: bytes, nranks: int, rank: int) -> None:
-        """Give this context an NCCL communicator (a collective: every rank
-        calls it with the same 128-byte id from nccl_unique_id())."""
-        buf = C.create_string_buffer(bytes(uid), 128)
-        _capi.check(self.lib.ircur_shard_comm_init(self.h, buf, nranks, rank))
-        self._comm_key = (nranks, rank, bytes(uid))
+    def shard_comm_init(self, uids: bytes, nranks: int, rank: int) -> None:
+        """Give this context its NCCL communicators (a collective: every rank
+        calls it with the same ids from nccl_unique_id(), 128 bytes each; two
+        ids give the overlapped loop one communicator per stream)."""
+        n = len(uids) // 128
+        buf = C.create_string_buffer(bytes(uids), 128 * n)
+        _capi.check(self.lib.ircur_shard_comm_init(self.h, buf, n, nranks, rank))
+        self._comm_key = (nranks, rank, bytes(uids))
 
-    def shard_run(self, zetas, eps: float, mode: int, max_iter: int, ahead: int):
+    def shard_run(self, zetas, eps: float, mode: int, max_iter: int, ahead: int, overlap: bool = True):
         """The whole sharded loop in the library (ircur_shard_run):
         (iterations, converged, errors, ms, launched)."""
         z = np.ascontiguousarray(zetas, dtype=np.float64)
@@ -270,8 +272,9 @@ class Context:
         it, conv, la = C.c_int(0), C.c_int(0), C.c_int(0)
         pd = C.POINTER(C.c_double)
         _capi.check(self.lib.ircur_shard_run(self.h, z.ctypes.data_as(pd), float(eps), int(mode), int(max_iter),
-                                             int(ahead), C.byref(it), C.byref(conv), errors.ctypes.data_as(pd),
-                                             ms.ctypes.data_as(C.POINTER(C.c_float)), C.byref(la)))
+                                             int(ahead), 1 if overlap else 0, C.byref(it), C.byref(conv),
+                                             errors.ctypes.data_as(pd), ms.ctypes.data_as(C.POINTER(C.c_float)),
+                                             C.byref(la)))
         n = it.value
         return n, bool(conv.value), errors[:n], ms[:n], la.value
 
@@ -1108,9 +1111,9 @@ def materialize(cur: CurFactors) -> np.ndarray:
     return materialize_device(cur, torch.float64).cpu().numpy()
 
 
-def nccl_unique_id() -> bytes:
-    """An NCCL unique id (128 bytes) for Context.shard_comm_init."""
-    buf = C.create_string_buffer(128)
-    _capi.check(_capi.load().ircur_nccl_unique_id(buf, 128))
+def nccl_unique_id(n: int = 1) -> bytes:
+    """n NCCL unique ids (128 bytes each) for Context.shard_comm_init."""
+    buf = C.create_string_buffer(128 * n)
+    _capi.check(_capi.load().ircur_nccl_unique_id(buf, 128 * n))
     return buf.raw
 

@@ -139,7 +139,7 @@ def test_native_shard_loop_bitwise_equals_python_loop(gloo1, dtype, mode):
     Dd = torch.from_numpy(D.astype(dtype)).cuda()
     outs = []
     for native in (False, True, True):
-        res = run_collective(solve_shard_program(Dd, cfg, n1=300, row0=0, native=native))
+        res = run_collective(solve_shard_program(Dd, cfg, n1=300, row0=0, native=native, overlap=False))
         outs.append((res.launched, run_collective(gather_program(res))))
     (l0, (c0, s0, t0)) = outs[0]
     for li, (ci, si, ti) in outs[1:]:
@@ -148,4 +148,37 @@ def test_native_shard_loop_bitwise_equals_python_loop(gloo1, dtype, mode):
         for a, b in ((ci.C, c0.C), (ci.R, c0.R), (si.row_values, s0.row_values), (si.col_values, s0.col_values),
                      (ci.core_pinv.sigma, c0.core_pinv.sigma)):
             np.testing.assert_array_equal(a, b)
+    ir.clear_cache()
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("mode", ["resampled", "fixed"])
+def test_native_overlapped_shard_loop_equals_single_gpu(gloo1, monkeypatch, mode, split):
+    """The library's overlapped sharded loop (chain of k + 1 beside the strips
+    of k, sampled Q partials and U all-reduced on one communicator, Q partials
+    and the 4 sums on the other) at one rank: bitwise the single-GPU solve
+    (the split strip launches and the sampled-factor kernel reproduce the
+    fused kernels; both runs use the fp32 SVD tolerance lag of 2).  At one
+    rank the row strip runs fused; IRCUR_SHARD_SPLIT=1 keeps the partial /
+    all-reduce / finish sequence the N > 1 loop runs."""
+    import ctypes as C
+
+    monkeypatch.setenv("IRCUR_SHARD_SPLIT", split)
+
+    from paper_2010_07422_b200.dist import run_collective
+
+    D, linf = _problem(2000, 1800, 5, seed=19, alpha=0.2)
+    cfg = _cfg(5, linf, mode, eps=1e-5)
+    Dd = torch.from_numpy(D.astype(np.float32)).cuda()
+    cur1, sp1, tr1 = ir.solve(Dd, cfg)
+    res = run_collective(solve_shard_program(Dd, cfg, n1=2000, row0=0, native=True, overlap=True))
+    ov = C.c_longlong(0)
+    assert res.engine.lib.ircur_debug_counter(res.engine.h, 1, C.byref(ov)) == 0
+    assert ov.value == 1, "the overlapped sharded loop did not run"
+    cur, sp, tr = run_collective(gather_program(res))
+    assert tr.iterations == tr1.iterations and tr.converged == tr1.converged
+    assert tr.errors == tr1.errors
+    for a, b in ((cur.C, cur1.C), (cur.R, cur1.R), (sp.row_values, sp1.row_values), (sp.col_values, sp1.col_values),
+                 (cur.core_pinv.sigma, cur1.core_pinv.sigma)):
+        np.testing.assert_array_equal(a, b)
     ir.clear_cache()
