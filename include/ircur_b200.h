@@ -200,6 +200,13 @@ int ircur_shard_finish(ircur_ctx_t ctx, const double* zetas, int mode, int* iter
  * strips of k (all-reduces of the Q partials and the 4 sums), one
  * communicator per stream. */
 int ircur_nccl_unique_id(void* id, int64_t bytes);
+/* Before the prep pass (zeta0 > 0, fp32, two communicators): queue the
+ * overlapped loop's chain(0) and chain(1) (core, all-reduce of U, Gram, SVD;
+ * sampled(0) from D) on the chain stream, beside the pass, which then waits
+ * for the SVD gate and leaves the cluster's SMs free; ircur_shard_run with
+ * overlap continues at strips(0).  No-op outside that envelope. */
+int ircur_shard_pre_chain(ircur_ctx_t ctx, const void* D, int64_t ldd, double zeta0, double gamma, int mode,
+                          int max_iter);
 int ircur_shard_comm_init(ircur_ctx_t ctx, const void* ids, int n_ids, int nranks, int rank);
 int ircur_shard_run(ircur_ctx_t ctx, const double* zetas, double eps, int mode, int max_iter, int ahead,
                     int overlap, int* iterations, int* converged, double* errors, float* iter_ms,

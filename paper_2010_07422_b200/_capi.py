@@ -52,6 +52,7 @@ PROTOTYPES = [
     ("ircur_poll", _i, [_vp, _pi, _pi]),
     ("ircur_nccl_unique_id", _i, [_vp, _i64]),
     ("ircur_shard_comm_init", _i, [_vp, _vp, _i, _i, _i]),
+    ("ircur_shard_pre_chain", _i, [_vp, _vp, _i64, _d, _d, _i, _i]),
     ("ircur_shard_run", _i, [_vp, _pd, _d, _i, _i, _i, _i, _pi, _pi, _pd, _pf, _pi]),
     ("ircur_shard_finish", _i, [_vp, _pd, _i, _pi, _pi, _pd, _pf]),
     ("ircur_get_strips", _i, [_vp, _vp, _vp, _vp, _vp]),

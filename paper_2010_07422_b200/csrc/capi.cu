@@ -898,10 +898,77 @@ bool shard_overlap_eligible(ircur_ctx* c, int mode, int max_iter) {
   return true;
 }
 
+// Chain(0) and chain(1) of the overlapped sharded loop, queued before the
+// prep pass (as pre_chain0 does on one GPU): with zeta0 given and L_0 = 0 they
+// read D only, so they run beside the pass, which waits for the SVD gate and
+// leaves the cluster's SMs free.  ircur_shard_run continues at strips(0).
+int shard_pre_chain(ircur_ctx* c, double zeta0, double gamma, int mode, int max_iter) {
+  c->chain0_pre = c->chain1_pre = false;
+  c->prep_gate_pending = false;
+  c->prep_sms = 0;
+  if (!(zeta0 > 0.0) || c->dtype != IRCUR_F32 || c->r > 16 || !c->nccl_comm || !c->nccl_comm2 || !c->D)
+    return IRCUR_OK;
+  const NcclApi& n = nccl_api();
+  const char* split = std::getenv("IRCUR_SHARD_SPLIT");
+  const bool one = c->nccl_nranks == 1 && !(split && std::atoi(split) != 0);
+  ncclComm_t cA = static_cast<ncclComm_t>(c->nccl_comm);
+  auto allreduce = [&](void* buf, size_t count, ncclDataType_t dt) -> int {
+    if (one) return IRCUR_OK;
+    const ncclResult_t r = n.all_reduce(buf, buf, count, dt, ncclSum, cA, c->sA);
+    if (r != ncclSuccess) return fail(IRCUR_ECUDA, std::string("ncclAllReduce: ") + n.error_string(r));
+    return IRCUR_OK;
+  };
+  if (int rc = overlap_setup(c)) return rc;
+  if (int rc = ircur_shard_reset(c)) return rc;
+  const size_t u_elems = (size_t)c->max_rows * c->max_cols;
+  c->err_lag = c->err_lag_env ? c->err_lag_env : 2;
+  IR_CUDA(cudaEventRecord(c->ov_start, c->stream));
+  IR_CUDA(cudaStreamWaitEvent(c->sA, c->ov_start, 0));
+  IR_CUDA(cudaStreamWaitEvent(c->sB, c->ov_start, 0));
+  const IterSets q = iter_sets(c, 0);
+  if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[0], c->sA));
+  IR_CUDA(cudaMemsetAsync(core_U(c, 0), 0, u_elems * sizeof(double), c->sA));
+  IR_CUDA(launch_core<float>(core_args<float>(c, 0, q, zeta0, false), c->r, c->sA));
+  if (int rc = allreduce(core_U(c, 0), u_elems, ncclFloat64)) return rc;
+  const SvdArgs sa = svd_args<float>(c, 0, q);
+  const int cs = svd_cluster_size(q.nJ, q.mI_all, sa.kk);
+  IR_CUDA(launch_svd<float>(sa, cs, c->sA, c->ov_gate0));
+  if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[1], c->sA));
+  IR_CUDA(cudaEventRecord(c->ovev[1], c->sA));  // ev(0, 1)
+  c->kernel_launches += 3;
+  c->chain0_pre = true;
+  const int set1 = mode == IRCUR_FIXED ? 0 : 1;
+  if (max_iter > 1 && set1 < c->n_sets) {  // sampled(0) (from D) -> core(1) -> SVD(1)
+    SampledArgs sm = sampled_args(c, 0, q, set1, zeta0, true);
+    sm.s[0].zero_override = c->nccl_rank > 0;
+    IR_CUDA(launch_sampled_factors(sm, c->r, c->sA));
+    const IterSets q1 = iter_sets(c, set1);
+    if (int rc = allreduce(sm.s[0].out, (size_t)q1.nJ * c->r, ncclFloat32)) return rc;
+    IR_CUDA(cudaEventRecord(c->ovev[3], c->sA));  // ev(0, 3)
+    const double zeta1 = std::pow(gamma, 1.0) * zeta0;
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[5], c->sA));
+    IR_CUDA(cudaMemsetAsync(core_U(c, 1), 0, u_elems * sizeof(double), c->sA));
+    IR_CUDA(launch_core<float>(core_args<float>(c, 1, q1, zeta1, true), c->r, c->sA));
+    if (int rc = allreduce(core_U(c, 1), u_elems, ncclFloat64)) return rc;
+    const SvdArgs sa1 = svd_args<float>(c, 1, q1);
+    IR_CUDA(launch_svd<float>(sa1, svd_cluster_size(q1.nJ, q1.mI_all, sa1.kk), c->sA, c->ovev[0]));  // gate ev(0, 0)
+    if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[6], c->sA));
+    IR_CUDA(cudaEventRecord(c->ovev[5 + 1], c->sA));  // ev(1, 1)
+    c->kernel_launches += 4;
+    c->chain1_pre = true;
+  }
+  c->prep_gate_pending = true;
+  c->prep_sms = std::max(1, c->num_sms - cs);
+  return IRCUR_OK;
+}
+
 int run_shard_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max_iter, int ahead,
                       int* iterations, int* converged, double* errors, float* iter_ms, int* launched_out) {
   const NcclApi& n = nccl_api();
-  if (int rc = ircur_shard_reset(c)) return rc;
+  const bool pre0 = c->chain0_pre, pre1 = c->chain0_pre && c->chain1_pre;
+  c->chain0_pre = c->chain1_pre = false;
+  if (!pre0)
+    if (int rc = ircur_shard_reset(c)) return rc;
   if (int rc = overlap_setup(c)) return rc;
   c->last_run_overlapped = 1;
   c->shard_prof = c->overlap_prof = c->profiling;  // strips: partial + finish launches; svd slot: the chain
@@ -921,13 +988,20 @@ int run_shard_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, i
   auto set_of = [&](int k) { return mode == IRCUR_FIXED ? 0 : k; };
   c->err_lag = c->err_lag_env ? c->err_lag_env : 2;  // the fp32 sequential lag
   c->seq_presampled = false;
+  c->prep_gate_pending = false;
   // one rank: nothing to exchange, so no all-reduce is issued and the row
   // strip runs fused (IRCUR_SHARD_SPLIT=1 keeps the N > 1 sequence: split
   // strips and NCCL all-reduces, for tests and the overhead measurement)
   const bool fused = one;
-  IR_CUDA(cudaEventRecord(c->ov_start, us));
-  IR_CUDA(cudaStreamWaitEvent(sA, c->ov_start, 0));
-  IR_CUDA(cudaStreamWaitEvent(sB, c->ov_start, 0));
+  if (!pre0) {
+    IR_CUDA(cudaEventRecord(c->ov_start, us));
+    IR_CUDA(cudaStreamWaitEvent(sA, c->ov_start, 0));
+    IR_CUDA(cudaStreamWaitEvent(sB, c->ov_start, 0));
+  } else {  // the prep pass (on the solver stream) before the strips
+    IR_CUDA(cudaEventRecord(c->ov_cover, us));
+    IR_CUDA(cudaStreamWaitEvent(sB, c->ov_cover, 0));
+    IR_CUDA(cudaStreamWaitEvent(sA, c->ov_cover, 0));
+  }
   double* Ucore = c->U;  // (sharded contexts: one core buffer, in chain-stream order)
   auto chain = [&](int k, cudaEvent_t gate) -> int {
     const IterSets q = iter_sets(c, set_of(k));
@@ -954,7 +1028,8 @@ int run_shard_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, i
     return IRCUR_OK;
   };
   if (int rc = cover(set_of(0))) return rc;
-  if (int rc = chain(0, nullptr)) return rc;
+  if (!pre0)
+    if (int rc = chain(0, nullptr)) return rc;
   volatile int* hf = c->h_flags;
   int launched = 0, stop_at = max_iter;
   while (launched < stop_at) {
@@ -973,7 +1048,11 @@ int run_shard_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, i
     const bool next = k + 1 < max_iter && set_of(k + 1) < c->n_sets;
     const IterSets q = iter_sets(c, set);
     int cs_next = 0;
-    if (next) {
+    if (next && k == 0 && pre1) {  // sampled(0) -> chain(1) ran beside the prep pass
+      if (int rc = cover(set_of(1))) return rc;
+      const IterSets qn = iter_sets(c, set_of(1));
+      cs_next = svd_cluster_size(qn.nJ, qn.mI_all, svd_args<float>(c, 1, qn).kk);
+    } else if (next) {
       if (int rc = cover(set_of(k + 1))) return rc;
       if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 2), 0));  // Q_{k-1} complete (the finish pass)
       SampledArgs sm = sampled_args(c, k, q, set_of(k + 1), zetas[k]);
@@ -1377,6 +1456,7 @@ int ircur_set_indices(ircur_ctx_t c, int n_sets, const int64_t* rows, const int3
   if (!c || n_sets < 1 || !rows || !cols || !row_counts || !col_counts)
     return fail(IRCUR_EINVAL, "bad index-set arguments");
   IR_CUDA(cudaSetDevice(c->device));
+  drop_pre(c);  // (a chain pre-launched by a solve that stopped early belongs to its sets)
   mark(c, 0);
   if (c->dt_mode == 2) {  // the sampled copy belongs to the previous sets
     c->dt_mode = 0;
@@ -2505,6 +2585,17 @@ int ircur_shard_comm_init(ircur_ctx_t c, const void* ids, int n_ids, int nranks,
   return IRCUR_OK;
 }
 
+int ircur_shard_pre_chain(ircur_ctx_t c, const void* D, int64_t ldd, double zeta0, double gamma, int mode,
+                          int max_iter) {
+  if (!c || !D || ldd < c->n2) return fail(IRCUR_EINVAL, "null context or D, or ldd < n2");
+  if (max_iter < 1 || max_iter > c->max_iter) return fail(IRCUR_EINVAL, "max_iter out of range");
+  if (c->n_sets < 1) return fail(IRCUR_EINVAL, "upload the index sets first");
+  IR_CUDA(cudaSetDevice(c->device));
+  c->D = D;  // (ircur_prepare_async, which follows, sets the same)
+  c->ldd = ldd;
+  return shard_pre_chain(c, zeta0, gamma, mode, max_iter);
+}
+
 // The per-iteration sequence dist.solve_shard_program drives from Python
 // (phases CORE, FACTOR, RESID, STOP with the all-reduces of U, the Q
 // partials and the 4 sums between them, solver.py:360-410), issued from here
@@ -2527,6 +2618,7 @@ int ircur_shard_run(ircur_ctx_t c, const double* zetas, double eps, int mode, in
   if (overlap && c->nccl_comm2 && shard_overlap_eligible(c, mode, max_iter))
     return run_shard_overlap(c, zetas, eps, mode, max_iter, ahead, iterations, converged, errors, iter_ms,
                              launched_out);
+  drop_pre(c);  // (a pre-launched chain the sequential loop does not continue)
   c->last_run_overlapped = 0;
   if (int rc = ircur_shard_reset(c)) return rc;
   ncclComm_t comm = static_cast<ncclComm_t>(c->nccl_comm);

@@ -122,6 +122,10 @@ def solve_shard_program(D_local, config: SolverConfig, *, n1: int, row0: int, co
 
     cm, cover = _copy_plan(colmajor, n2, m_cols, sets, cfg)
     eng.set_indices(sets)
+    if native and overlap and cfg.zeta0 is not None and cm != 0 and hasattr(eng, "shard_pre_chain"):
+        # chain(0) / chain(1) of the library's overlapped loop beside the prep pass
+        yield ("native_comm", eng)
+        eng.shard_pre_chain(Dd, cfg.zeta0, cfg.gamma, RESAMPLED if resampled else FIXED, cfg.max_iter)
     # matcore.require_finite / inf_norm over all shards: every rank raises together
     bad, max_abs = 0.0, 0.0
     try:

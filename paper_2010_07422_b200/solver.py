@@ -263,6 +263,12 @@ class Context:
         _capi.check(self.lib.ircur_shard_comm_init(self.h, buf, n, nranks, rank))
         self._comm_key = (nranks, rank, bytes(uids))
 
+    def shard_pre_chain(self, D, zeta0: float, gamma: float, mode: int, max_iter: int) -> None:
+        """Queue chain(0) / chain(1) of the overlapped sharded loop before the
+        prep pass (ircur_shard_pre_chain); D is this rank's device shard."""
+        _capi.check(self.lib.ircur_shard_pre_chain(self.h, C.c_void_p(D.data_ptr()), int(D.stride(0)), float(zeta0),
+                                                   float(gamma), int(mode), int(max_iter)))
+
     def shard_run(self, zetas, eps: float, mode: int, max_iter: int, ahead: int, overlap: bool = True):
         """The whole sharded loop in the library (ircur_shard_run):
         (iterations, converged, errors, ms, launched)."""
