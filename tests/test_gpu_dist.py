@@ -182,3 +182,36 @@ def test_native_overlapped_shard_loop_equals_single_gpu(gloo1, monkeypatch, mode
                  (cur.core_pinv.sigma, cur1.core_pinv.sigma)):
         np.testing.assert_array_equal(a, b)
     ir.clear_cache()
+
+
+def test_native_loop_edge_cases(gloo1):
+    """fp64 with the default overlap request takes the library's sequential
+    loop (the overlapped one is fp32); a den == 0 problem leaves the loop
+    before it starts, after its chain(0) was queued beside the prep pass, and
+    the next solve on the same context is unaffected."""
+    from paper_2010_07422_b200.dist import run_collective
+
+    D, linf = _problem(240, 220, 4, seed=23)
+    cfg = _cfg(4, linf, "resampled", eps=1e-9)
+    Dd = torch.from_numpy(D).cuda()
+    a = run_collective(gather_program(run_collective(solve_shard_program(Dd, cfg, n1=240, row0=0, native=False))))
+    b = run_collective(gather_program(run_collective(solve_shard_program(Dd, cfg, n1=240, row0=0, native=True))))
+    assert a[2].errors == b[2].errors
+    np.testing.assert_array_equal(a[0].C, b[0].C)
+    # fp32: the zero-slab exit with a pre-launched chain, then a normal solve
+    cfg32 = _cfg(4, linf, "resampled", eps=1e-5)
+    n1, n2 = D.shape
+    m1, m2 = ir.sample_count(n1, 4, 4.0), ir.sample_count(n2, 4, 4.0)
+    I0, J0 = ir.draw_index_sets(n1, n2, m1, m2, cfg32.seed, 1)[0]
+    Z = D.astype(np.float32).copy()
+    Z[I0, :] = 0.0
+    Z[:, J0] = 0.0
+    z = run_collective(gather_program(run_collective(solve_shard_program(
+        torch.from_numpy(Z).cuda(), cfg32, n1=n1, row0=0, native=True))))
+    assert z[2].errors == [0.0] and z[2].converged
+    D32 = torch.from_numpy(D.astype(np.float32)).cuda()
+    one = ir.solve(D32, cfg32)
+    sh = run_collective(gather_program(run_collective(solve_shard_program(D32, cfg32, n1=n1, row0=0, native=True))))
+    assert sh[2].errors == one[2].errors
+    np.testing.assert_array_equal(sh[0].C, one[0].C)
+    ir.clear_cache()
