@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kS3NT, 1) strips3_kernel(const __grid_constant
 }
 // batched problems: problem blockIdx.y, its tiles over blockIdx.x
 template <int R>
-__global__ void __launch_bounds__(kS3NT, 1) strips3_kernel_batched(const StripsArgs<float>* __restrict__ as) {
+__global__ void __launch_bounds__(kS3NT, R <= 6 ? 2 : 1) strips3_kernel_batched(const StripsArgs<float>* __restrict__ as) {
   strips3_body<R>(as[blockIdx.y], (int)blockIdx.x, (int)gridDim.x);
 }
 
