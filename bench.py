@@ -561,7 +561,7 @@ def run_batch(args):
         if record:
             d = stats[0]
             d["strip_ms"] += st.get("strip_ms", 0.0)
-            phases.append({"prepare_s": st.get("prepare_s"), "batched_run_s": st.get("batched_run_s")})
+            phases.append({k: st.get(k) for k in ("setup_s", "prepare_s", "batched_run_s", "results_s")})
             for rr in res:
                 it = rr.trace.iterations
                 d["strip_bytes"] += sum(algorithmic_strip_bytes(s, n1, n2, r, rr.trace.sampled_rows[k],

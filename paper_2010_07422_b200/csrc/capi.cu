@@ -150,6 +150,19 @@ struct ircur_ctx {
   double b_eps = 0.0;
   int b_mode = 0, b_max_iter = 0;
   bool b_ready = false;
+  // ircur_batched_run's staging, kept on the batch's first context across
+  // calls (grow-only): page-locked argument ring and trace gather, device
+  // argument ring, ring and strip-timing events.  Allocating and freeing
+  // these per call (cudaFreeHost synchronises the device) cost up to
+  // 200 ms on some batches.
+  PinnedBuf b_hargs, b_hres;
+  void* b_dargs = nullptr;
+  size_t b_dargs_cap = 0;
+  std::vector<cudaEvent_t> b_evk, b_evs;
+  // ircur_batch_prepare_many's batched passes (grow-only, on the first context)
+  PinnedBuf b_prep_h, b_prep_res;
+  void* b_prep_d = nullptr;
+  size_t b_prep_cap = 0;
   bool prep_prof = false;          // diagnostics (IRCUR_BATCH_PREP_PROF): host ms per setup phase
   double prep_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int run_fixed = 0;            // mode of the current loop (the next iteration's index set)
@@ -1262,7 +1275,15 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   if (c->h_flags) cudaFreeHost(c->h_flags);
   if (c->h_res) cudaFreeHost(c->h_res);
   if (c->ev_stage) cudaEventDestroy(c->ev_stage);
-  for (PinnedBuf* b : {&c->st_rows, &c->st_cols, &c->st_colsel, &c->st_lines}) b->release();
+  for (PinnedBuf* b : {&c->st_rows, &c->st_cols, &c->st_colsel, &c->st_lines, &c->b_hargs, &c->b_hres, &c->b_prep_h,
+                        &c->b_prep_res})
+    b->release();
+  if (c->b_dargs) cudaFree(c->b_dargs);
+  if (c->b_prep_d) cudaFree(c->b_prep_d);
+  for (auto& e : c->b_evk)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->b_evs)
+    if (e) cudaEventDestroy(e);
   for (cudaStream_t s : {c->sA, c->sB})  // the overlapped loop's streams drain before their events go
     if (s) cudaStreamSynchronize(s);
   for (auto& e : c->ev)
@@ -1283,6 +1304,44 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
   return IRCUR_OK;
 }
 
+// The plan of a prep pass (its first row chunk): the borrowed D, the copy
+// mode and, for mode 2, the sampled-column map and copy capacity
+// (build_cover without the launch).  Host work plus the map uploads on the
+// context stream; no kernels.
+static int plan_pass(ircur_ctx* c, const void* D, int64_t ldd, int mode, int cover_sets) {
+  cudaStream_t st = c->stream;
+  c->D = D;
+  c->ldd = ldd;
+  c->has_state = false;
+  c->covered = 0;
+  c->slab_pending = -1;
+  c->prep_next_row = 0;
+  if (mode == 2) {
+    c->dt_mode = 0;  // (an allocation from an earlier solve is reused when large enough)
+    if (int rc = build_cover(c, cover_sets, c->maxbits, c->flags + 3, false)) return rc;
+  } else {
+    if (mode == 1 && (!c->Dt || c->dt_cap < c->n2)) {
+      if (c->Dt) {
+        IR_CUDA(cudaStreamSynchronize(st));
+        cudaFree(c->Dt);
+      }
+      c->ldt = pad4(c->nloc);
+      c->Dt = nullptr;
+      c->dt_cap = 0;
+      IR_CUDA(cudaMalloc(&c->Dt, (size_t)c->n2 * c->ldt * c->esz));
+      c->dt_cap = c->n2;
+    }
+    if (mode == 0 && c->Dt) {
+      IR_CUDA(cudaStreamSynchronize(st));
+      cudaFree(c->Dt);
+      c->Dt = nullptr;
+      c->dt_cap = 0;
+    }
+    c->dt_mode = mode;
+  }
+  return IRCUR_OK;
+}
+
 int ircur_prepare_rows_async(ircur_ctx_t c, const void* D, int64_t ldd, int mode, int cover_sets, int64_t row_begin,
                              int64_t row_end) {
   if (!c || !D) return fail(IRCUR_EINVAL, "null context or D");
@@ -1295,38 +1354,10 @@ int ircur_prepare_rows_async(ircur_ctx_t c, const void* D, int64_t ldd, int mode
   if (row_begin == 0) {  // first chunk: plan the pass
     if (mode == 2 && c->n_sets < 1) return fail(IRCUR_EINVAL, "upload the index sets before a sampled prep");
     if (mode == 2 && cover_sets < 1) return fail(IRCUR_EINVAL, "cover_sets must be >= 1");
-    c->D = D;
-    c->ldd = ldd;
-    c->has_state = false;
-    c->covered = 0;
-    c->slab_pending = -1;
-    c->prep_next_row = 0;
     mark(c, 1);
     IR_CUDA(cudaMemsetAsync(c->maxbits, 0, sizeof(unsigned long long), st));
     IR_CUDA(cudaMemsetAsync(c->flags + 3, 0, sizeof(int), st));
-    if (mode == 2) {
-      c->dt_mode = 0;  // (an allocation from an earlier solve is reused when large enough)
-      if (int rc = build_cover(c, cover_sets, c->maxbits, c->flags + 3, false)) return rc;
-    } else {
-      if (mode == 1 && (!c->Dt || c->dt_cap < c->n2)) {
-        if (c->Dt) {
-          IR_CUDA(cudaStreamSynchronize(st));
-          cudaFree(c->Dt);
-        }
-        c->ldt = pad4(c->nloc);
-        c->Dt = nullptr;
-        c->dt_cap = 0;
-        IR_CUDA(cudaMalloc(&c->Dt, (size_t)c->n2 * c->ldt * c->esz));
-        c->dt_cap = c->n2;
-      }
-      if (mode == 0 && c->Dt) {
-        IR_CUDA(cudaStreamSynchronize(st));
-        cudaFree(c->Dt);
-        c->Dt = nullptr;
-        c->dt_cap = 0;
-      }
-      c->dt_mode = mode;
-    }
+    if (int rc = plan_pass(c, D, ldd, mode, cover_sets)) return rc;
   } else if (D != c->D || ldd != c->ldd || mode != c->dt_mode || row_begin != c->prep_next_row) {
     return fail(IRCUR_EINVAL, "row chunks must continue the pass started at row 0 (same D, ldd, mode, in order)");
   }
@@ -1474,17 +1505,37 @@ int ircur_append_indices(ircur_ctx_t c, int n_more, const int64_t* rows, const i
   return upload_sets(c, c->n_sets, n_more, rows, row_counts, cols, col_counts);
 }
 
+// The slab-norm pass of index set `set`: its block split and line sources
+// (ircur_slab_sqnorms_async and the batched prep share it)
+struct SlabGeom {
+  int nb_rows = 0, nb_cols = 0;
+  const int* I = nullptr;
+  const int* J = nullptr;
+  const int* Jl = nullptr;
+  bool use_dt = false;
+};
+static int slab_geom(ircur_ctx* c, int set, SlabGeom& g) {
+  g.nb_rows = std::max(1, std::min(c->num_sms * 2, (int)((int64_t)c->h_row_loc_cnt[set] * c->n2 / 4096 + 1)));
+  g.nb_cols = std::max(1, std::min(c->num_sms * 2, (int)(c->nloc * c->h_col_cnt[set] / 4096 + 1)));
+  if (g.nb_rows + g.nb_cols > c->max_partials) return fail(IRCUR_EINVAL, "partials buffer too small");
+  g.I = c->d_rows + (size_t)set * c->max_rows + c->h_row_lo[set];
+  g.J = c->d_cols + (size_t)set * c->max_cols;
+  // D(:,J) from the column-major copy when it holds set `set` (coalesced lines)
+  g.use_dt = c->Dt && (c->dt_mode == 1 || (c->dt_mode == 2 && set < c->covered));
+  g.Jl = c->dt_mode == 2 ? c->d_cols_c + (size_t)set * c->max_cols : g.J;
+  return IRCUR_OK;
+}
+
 int ircur_slab_sqnorms_async(ircur_ctx_t c, int set) {
   if (!c || !c->D || set < 0 || set >= c->n_sets) return fail(IRCUR_EINVAL, "bad context/set");
   IR_CUDA(cudaSetDevice(c->device));
-  const int nb_rows = std::max(1, std::min(c->num_sms * 2, (int)((int64_t)c->h_row_loc_cnt[set] * c->n2 / 4096 + 1)));
-  const int nb_cols = std::max(1, std::min(c->num_sms * 2, (int)(c->nloc * c->h_col_cnt[set] / 4096 + 1)));
-  if (nb_rows + nb_cols > c->max_partials) return fail(IRCUR_EINVAL, "partials buffer too small");
-  const int* I = c->d_rows + (size_t)set * c->max_rows + c->h_row_lo[set];
-  const int* J = c->d_cols + (size_t)set * c->max_cols;
-  // D(:,J) from the column-major copy when it holds set `set` (coalesced lines)
-  const bool use_dt = c->Dt && (c->dt_mode == 1 || (c->dt_mode == 2 && set < c->covered));
-  const int* Jl = c->dt_mode == 2 ? c->d_cols_c + (size_t)set * c->max_cols : J;
+  SlabGeom g;
+  if (int rc = slab_geom(c, set, g)) return rc;
+  const int nb_rows = g.nb_rows, nb_cols = g.nb_cols;
+  const int* I = g.I;
+  const int* J = g.J;
+  const bool use_dt = g.use_dt;
+  const int* Jl = g.Jl;
   if (c->dtype == IRCUR_F32)
     IR_CUDA(launch_slab_sq<float>((const float*)c->D, c->ldd, c->row0, c->nloc, c->n2, I,
                                   c->h_row_loc_cnt[set], J, c->h_col_cnt[set], nb_rows, nb_cols,
@@ -1807,6 +1858,14 @@ int ircur_batch_prepare_many(ircur_ctx_t* ctxs, int n, const void* const* D, int
   const bool prof = std::getenv("IRCUR_BATCH_PREP_PROF") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   const auto t0 = now();
+  // one launch per phase over all problems (IRCUR_BATCH_PREP=0: each
+  // problem's own prep pass and slab norms, queued by its worker thread)
+  static const bool batch_prep_env = [] {
+    const char* e = std::getenv("IRCUR_BATCH_PREP");
+    return !(e && std::atoi(e) == 0);
+  }();
+  bool batch_prep = batch_prep_env;
+  for (int p = 0; p < n && batch_prep; ++p) batch_prep = ctxs[p] && ctxs[p]->dtype == ctxs[0]->dtype;
   std::vector<int> cms(n, 0);
   std::atomic<int> next{0}, first_bad{-1}, bad_rc{0};
   std::string bad_msg;
@@ -1875,8 +1934,12 @@ int ircur_batch_prepare_many(ircur_ctx_t* ctxs, int n, const void* const* D, int
       c->b_ready = false;
       c->tc_ok = eps[p] >= c->tc_min_eps ? 1 : 0;
       int rc = ircur_set_indices(c, n_sets, rp, rcp, cp, ccp);
-      if (rc == IRCUR_OK) rc = ircur_prepare_async(c, D[p], ldd, cm, cover);
-      if (rc == IRCUR_OK) rc = ircur_slab_sqnorms_async(c, 0);
+      if (batch_prep) {  // plan only: the passes are launched for every problem at once below
+        if (rc == IRCUR_OK) rc = ldd < c->n2 ? fail(IRCUR_EINVAL, "ldd < n2") : plan_pass(c, D[p], ldd, cm, cover);
+      } else {
+        if (rc == IRCUR_OK) rc = ircur_prepare_async(c, D[p], ldd, cm, cover);
+        if (rc == IRCUR_OK) rc = ircur_slab_sqnorms_async(c, 0);
+      }
       if (rc != IRCUR_OK) {
         bad(p, rc, ircur_last_error());
         return;
@@ -1897,19 +1960,87 @@ int ircur_batch_prepare_many(ircur_ctx_t* ctxs, int n, const void* const* D, int
   for (int p = 0; p < n; ++p)
     if (copy_mode) copy_mode[p] = cms[p];
   const auto t1 = now();
+  // ---- batched passes: every problem's prep pass (finite flag, max|D|,
+  // column copy), slab norms of set 0 and one gather of the results, on the
+  // first context's stream after every worker stream's uploads
+  const double* bres = nullptr;
+  if (batch_prep) {
+    ircur_ctx* c0 = ctxs[0];
+    cudaStream_t bs = c0->stream;
+    IR_CUDA(cudaSetDevice(dev));
+    std::vector<ircur_ctx*> joins;  // one context per distinct stream other than bs
+    for (int p = 0; p < n; ++p) {
+      bool seen = ctxs[p]->stream == bs;
+      for (ircur_ctx* q : joins) seen = seen || q->stream == ctxs[p]->stream;
+      if (!seen) joins.push_back(ctxs[p]);
+    }
+    for (ircur_ctx* q : joins) {
+      IR_CUDA(cudaEventRecord(q->ev[0], q->stream));
+      IR_CUDA(cudaStreamWaitEvent(bs, q->ev[0], 0));
+    }
+    const size_t abytes = sizeof(PrepBatchArg) * (size_t)n, rbytes = 4 * sizeof(double) * (size_t)n;
+    IR_CUDA(c0->b_prep_h.reserve(abytes));
+    IR_CUDA(c0->b_prep_res.reserve(rbytes));
+    if (abytes + rbytes > c0->b_prep_cap) {
+      if (c0->b_prep_d) IR_CUDA(cudaFree(c0->b_prep_d));
+      c0->b_prep_d = nullptr;
+      c0->b_prep_cap = 0;
+      IR_CUDA(cudaMalloc(&c0->b_prep_d, abytes + rbytes));
+      c0->b_prep_cap = abytes + rbytes;
+    }
+    PrepBatchArg* ha = c0->b_prep_h.as<PrepBatchArg>();
+    for (int p = 0; p < n; ++p) {
+      ircur_ctx* c = ctxs[p];
+      SlabGeom g;
+      if (int rc = slab_geom(c, 0, g)) {
+        if (failed) *failed = p;
+        return fail(rc, "problem " + std::to_string(p) + ": " + ircur_last_error());
+      }
+      PrepBatchArg& a = ha[p];
+      a = PrepBatchArg{};
+      a.D = c->D; a.ldd = c->ldd; a.nloc = c->nloc; a.n2 = c->n2; a.row0 = c->row0;
+      a.Dt = c->dt_mode ? c->Dt : nullptr; a.ldt = c->ldt; a.colsel = c->d_colsel; a.mode = c->dt_mode;
+      a.maxbits = c->maxbits; a.nonfinite = c->flags + 3;
+      a.I = g.I; a.mI = c->h_row_loc_cnt[0]; a.J = g.J; a.nJ = c->h_col_cnt[0]; a.Jline = g.Jl;
+      a.use_dt = g.use_dt ? 1 : 0; a.nb_rows = g.nb_rows; a.nb_cols = g.nb_cols; a.partials = c->partials;
+      c->prep_next_row = c->nloc;
+      c->prep_pending = false;
+      c->slab_pending = -1;
+    }
+    PrepBatchArg* da = static_cast<PrepBatchArg*>(c0->b_prep_d);
+    double* dres = reinterpret_cast<double*>(static_cast<unsigned char*>(c0->b_prep_d) + abytes);
+    IR_CUDA(cudaMemcpyAsync(da, ha, abytes, cudaMemcpyHostToDevice, bs));
+    IR_CUDA(c0->dtype == IRCUR_F32 ? launch_prep_batched<float>(da, ha, n, dres, bs)
+                                   : launch_prep_batched<double>(da, ha, n, dres, bs));
+    IR_CUDA(cudaMemcpyAsync(c0->b_prep_res.p, dres, rbytes, cudaMemcpyDeviceToHost, bs));
+    IR_CUDA(cudaEventRecord(c0->ev[0], bs));
+    for (ircur_ctx* q : joins) IR_CUDA(cudaStreamWaitEvent(q->stream, c0->ev[0], 0));
+    IR_CUDA(cudaStreamSynchronize(bs));
+    bres = c0->b_prep_res.as<double>();
+  }
   const auto t2 = now();
   // ---- phase C: finite check, max|D|, den = 0 exit (solver.py:319-344)
   for (int p = 0; p < n; ++p) {
     ircur_ctx* c = ctxs[p];
     double mx = 0.0;
-    if (int rc = ircur_prepare_wait(c, nullptr, &mx)) {
-      if (failed) *failed = p;
-      return fail(rc, "problem " + std::to_string(p) + ": " + ircur_last_error());
-    }
     double a = 0.0, b = 0.0;
-    if (int rc = ircur_slab_sqnorms(c, 0, &a, &b)) {
-      if (failed) *failed = p;
-      return fail(rc, "problem " + std::to_string(p) + ": " + ircur_last_error());
+    if (bres) {
+      if (bres[4 * (size_t)p + 1] != 0.0) {
+        if (failed) *failed = p;
+        return fail(IRCUR_ENONFINITE, "problem " + std::to_string(p) + ": matrix contains non-finite entries");
+      }
+      mx = bres[4 * (size_t)p];
+      a = bres[4 * (size_t)p + 2];
+      b = bres[4 * (size_t)p + 3];
+    } else {
+      if (int rc = ircur_prepare_wait(c, nullptr, &mx)) {
+        if (failed) *failed = p;
+        return fail(rc, "problem " + std::to_string(p) + ": " + ircur_last_error());
+      }
+      if (int rc = ircur_slab_sqnorms(c, 0, &a, &b)) {
+        if (failed) *failed = p;
+        return fail(rc, "problem " + std::to_string(p) + ": " + ircur_last_error());
+      }
     }
     const bool zs = std::sqrt(a) + std::sqrt(b) == 0.0;
     if (zero_state) zero_state[p] = zs ? 1 : 0;
@@ -1980,40 +2111,36 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
   constexpr int kRing = 4;
   const size_t per = sizeof(CoreArgs<float>) + sizeof(SvdArgs) + sizeof(StripsArgs<float>) + sizeof(FinalizeArgs);
   const size_t bytes_it = per * (size_t)n;
-  unsigned char* dargs = nullptr;
-  unsigned char* hargs = nullptr;
-  IR_CUDA(cudaMallocAsync((void**)&dargs, bytes_it * kRing, bs));
-  IR_CUDA(cudaHostAlloc((void**)&hargs, bytes_it * kRing, cudaHostAllocDefault));
-  struct Free {
-    unsigned char* d;
-    unsigned char* h;
+  // (cached on ctxs[0]; the previous call ended with a stream sync, so the
+  // buffers are free)
+  if (bytes_it * kRing > c0->b_dargs_cap) {
+    if (c0->b_dargs) IR_CUDA(cudaFree(c0->b_dargs));
+    c0->b_dargs = nullptr;
+    c0->b_dargs_cap = 0;
+    IR_CUDA(cudaMalloc(&c0->b_dargs, bytes_it * kRing));
+    c0->b_dargs_cap = bytes_it * kRing;
+  }
+  IR_CUDA(c0->b_hargs.reserve(bytes_it * kRing));
+  unsigned char* dargs = static_cast<unsigned char*>(c0->b_dargs);
+  unsigned char* hargs = c0->b_hargs.as<unsigned char>();
+  struct Drain {  // an early error return leaves nothing in flight on the staging
     cudaStream_t s;
-    ~Free() {
-      cudaStreamSynchronize(s);
-      if (d) cudaFreeAsync(d, s);
-      cudaStreamSynchronize(s);
-      if (h) cudaFreeHost(h);
-    }
-  } fr{dargs, hargs, bs};
-  std::vector<cudaEvent_t> evk(kRing);
-  for (auto& e : evk) IR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  struct FreeEv {
-    std::vector<cudaEvent_t>& v;
-    ~FreeEv() {
-      for (auto e : v) cudaEventDestroy(e);
-    }
-  } fe{evk};
-  std::vector<cudaEvent_t> evs;  // optional: events around each batched strip launch
-  struct FreeEvs {
-    std::vector<cudaEvent_t>& v;
-    ~FreeEvs() {
-      for (auto e : v) cudaEventDestroy(e);
-    }
-  } fes{evs};
+    ~Drain() { cudaStreamSynchronize(s); }
+  } drain{bs};
+  while ((int)c0->b_evk.size() < kRing) {
+    cudaEvent_t e = nullptr;
+    IR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c0->b_evk.push_back(e);
+  }
+  std::vector<cudaEvent_t>& evk = c0->b_evk;
+  std::vector<cudaEvent_t>& evs = c0->b_evs;  // optional: events around each batched strip launch
   if (strip_ms) {
     *strip_ms = 0.f;
-    evs.resize(2 * (size_t)max_iter);
-    for (auto& e : evs) IR_CUDA(cudaEventCreate(&e));
+    while (evs.size() < 2 * (size_t)max_iter) {
+      cudaEvent_t e = nullptr;
+      IR_CUDA(cudaEventCreate(&e));
+      evs.push_back(e);
+    }
   }
   constexpr int kAhead = 3;
   int launched = 0;
@@ -2121,12 +2248,8 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
   // batch stream, then one wait (read_trace per problem would cost two host
   // waits each)
   const size_t per_p = 4 * sizeof(int) + (size_t)max_iter * sizeof(double);
-  unsigned char* hres = nullptr;
-  IR_CUDA(cudaHostAlloc((void**)&hres, per_p * n, cudaHostAllocDefault));
-  struct FreeH {
-    unsigned char* h;
-    ~FreeH() { cudaFreeHost(h); }
-  } fh{hres};
+  IR_CUDA(c0->b_hres.reserve(per_p * n));
+  unsigned char* hres = c0->b_hres.as<unsigned char>();
   for (int p = 0; p < n; ++p) {
     ircur_ctx* c = ctxs[p];
     IR_CUDA(cudaMemcpyAsync(hres + per_p * p, c->flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, bs));

@@ -14,6 +14,7 @@
 #include "ircur_common.cuh"
 #include "launchers.cuh"
 #include <cstdlib>
+#include <algorithm>
 #include <type_traits>
 
 namespace ircur {
@@ -60,14 +61,12 @@ __global__ void __launch_bounds__(256) prep_transpose_kernel(const T* __restrict
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) prep_scan_kernel(const T* __restrict__ D, int64_t ldd,
-                                                        int64_t nloc, int64_t n2,
-                                                        unsigned long long* maxbits, int* nonfinite) {
+__device__ __forceinline__ void prep_scan_kernel_body(const T* __restrict__ D, int64_t ldd, int64_t nloc, int64_t n2, unsigned long long* maxbits, int* nonfinite, int64_t bx, int64_t nbx) {
   double mx = 0.0;
   int bad = 0;
   const int64_t total = nloc * n2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+  const int64_t stride = nbx * blockDim.x;
+  for (int64_t e = bx * blockDim.x + threadIdx.x; e < total; e += stride) {
     const int64_t r = e / n2, c = e - r * n2;
     const double av = fabs((double)__ldcs(D + r * ldd + c));
     if (!isfinite(av)) bad = 1; else mx = fmax(mx, av);
@@ -83,20 +82,23 @@ __global__ void __launch_bounds__(256) prep_scan_kernel(const T* __restrict__ D,
   }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) prep_scan_kernel(const T* __restrict__ D, int64_t ldd, int64_t nloc, int64_t n2, unsigned long long* maxbits, int* nonfinite) {
+  prep_scan_kernel_body(D, ldd, nloc, n2, maxbits, nonfinite, blockIdx.x, gridDim.x);
+}
+
 // contiguous rows, 16-byte vector loads (ldd*sizeof(T) % 16 == 0, aligned base)
 template <typename T>
-__global__ void __launch_bounds__(256) prep_scan_vec_kernel(const T* __restrict__ D, int64_t ldd,
-                                                            int64_t nloc, int64_t n2,
-                                                            unsigned long long* maxbits, int* nonfinite) {
+__device__ __forceinline__ void prep_scan_vec_kernel_body(const T* __restrict__ D, int64_t ldd, int64_t nloc, int64_t n2, unsigned long long* maxbits, int* nonfinite, int64_t bx, int64_t nbx) {
   constexpr int VW = 16 / sizeof(T);
   using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   T mx = T(0);
   int bad = 0;
   const int64_t vpr = n2 / VW;  // full vectors per row
   const int64_t total = nloc * vpr;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t stride = nbx * blockDim.x;
   constexpr int UN = 4;  // independent 16-byte loads in flight per thread
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t e = bx * blockDim.x + threadIdx.x;
   if (ldd == n2) {  // dense rows: treat D as one flat vector array
     const V4* Dv = reinterpret_cast<const V4*>(D);
     for (; e + (UN - 1) * stride < total; e += UN * stride) {
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(256) prep_scan_vec_kernel(const T* __restrict_
   // row tails
   const int64_t tail = n2 - vpr * VW;
   if (tail > 0) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * tail; e += stride) {
+    for (int64_t e = bx * blockDim.x + threadIdx.x; e < nloc * tail; e += stride) {
       const int64_t r = e / tail, c = vpr * VW + (e - r * tail);
       const T av = fabs(D[r * ldd + c]);
       bad |= !isfinite(av);
@@ -147,16 +149,18 @@ __global__ void __launch_bounds__(256) prep_scan_vec_kernel(const T* __restrict_
   }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) prep_scan_vec_kernel(const T* __restrict__ D, int64_t ldd, int64_t nloc, int64_t n2, unsigned long long* maxbits, int* nonfinite) {
+  prep_scan_vec_kernel_body(D, ldd, nloc, n2, maxbits, nonfinite, blockIdx.x, gridDim.x);
+}
+
 // Persistent 64x64-tile transpose fused with the finite/max scan.  Each CTA
 // walks tiles t = blockIdx.x + i*gridDim.x; `col_major_order` chooses whether
 // consecutive tiles share a column band (writes of concurrently running CTAs
 // land in the same 64 rows of Dt) or a row band (reads share 64 rows of D).
 constexpr int kPT = 64;
 template <typename T>
-__global__ void __launch_bounds__(256) prep_transpose64_kernel(const T* __restrict__ D, int64_t ldd,
-                                                               int64_t nloc, int64_t n2, T* __restrict__ Dt,
-                                                               int64_t ldt, unsigned long long* maxbits,
-                                                               int* nonfinite, int col_major_order) {
+__device__ __forceinline__ void prep_transpose64_kernel_body(const T* __restrict__ D, int64_t ldd, int64_t nloc, int64_t n2, T* __restrict__ Dt, int64_t ldt, unsigned long long* maxbits, int* nonfinite, int col_major_order, int64_t bx, int64_t nbx) {
   __shared__ T tile[kPT][kPT + 1];
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
   constexpr int VW = 16 / sizeof(T);                      // elements per 16-byte vector
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(256) prep_transpose64_kernel(const T* __restri
   const int64_t ntiles = tr * tcn;
   T mx = T(0);
   int bad = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (int64_t t = bx; t < ntiles; t += nbx) {
     int64_t br, bc;
     if (col_major_order) { bc = t / tr; br = t - bc * tr; } else { br = t / tcn; bc = t - br * tcn; }
     const int64_t rb = br * kPT, cb = bc * kPT;
@@ -235,6 +239,11 @@ __global__ void __launch_bounds__(256) prep_transpose64_kernel(const T* __restri
 }
 
 template <typename T>
+__global__ void __launch_bounds__(256) prep_transpose64_kernel(const T* __restrict__ D, int64_t ldd, int64_t nloc, int64_t n2, T* __restrict__ Dt, int64_t ldt, unsigned long long* maxbits, int* nonfinite, int col_major_order) {
+  prep_transpose64_kernel_body(D, ldd, nloc, n2, Dt, ldt, maxbits, nonfinite, col_major_order, blockIdx.x, gridDim.x);
+}
+
+template <typename T>
 cudaError_t launch_prep(const T* D, int64_t ldd, int64_t nloc, int64_t n2, T* Dt, int64_t ldt,
                         unsigned long long* maxbits, int* nonfinite, int num_sms, cudaStream_t st) {
   if (nloc == 0 || n2 == 0) return cudaSuccess;
@@ -273,10 +282,7 @@ cudaError_t launch_prep(const T* D, int64_t ldd, int64_t nloc, int64_t n2, T* Dt
 // will use (about 20% of D at n = 1e5), so the per-solve pass moves ~1.2x
 // |D| instead of the 2x |D| of a full transpose.
 template <typename T, int TR, int TC, bool NM>
-__global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ D, int64_t ldd, int64_t nloc,
-                                                          int64_t n2, const int* __restrict__ colsel,
-                                                          T* __restrict__ Dt, int64_t ldt,
-                                                          unsigned long long* maxbits, int* nonfinite) {
+__device__ __forceinline__ void prep_select_kernel_body(const T* __restrict__ D, int64_t ldd, int64_t nloc, int64_t n2, const int* __restrict__ colsel, T* __restrict__ Dt, int64_t ldt, unsigned long long* maxbits, int* nonfinite, int64_t bx, int64_t nbx) {
   // Each thread owns one 16-byte column group of a 64 x 64 tile in KR rows.
   // The next tile's vectors and column map are loaded before the current
   // tile is processed (register double buffering).  Selected columns are
@@ -290,7 +296,7 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
   constexpr int KR = TR / RPI;         // rows per thread
   constexpr int SL = TR + VW;          // staged column length (16-byte aligned rows)
   constexpr int CPW = TR / VW;         // vectors per staged column
-  constexpr int NB = sizeof(T) == 4 ? 2 : 1;  // staging buffers (fp64: one, fits 48 KB static)
+  constexpr int NB = 2 * TC * SL * sizeof(T) <= 40 * 1024 ? 2 : 1;  // staging buffers (two when they fit 48 KB static)
   static_assert(TPR <= 32 && KR >= 1 && RPI * KR == TR, "tile shape");
   __shared__ __align__(16) T sbuf[NB][TC][SL];
   __shared__ int sdst[NB][TC];
@@ -309,7 +315,7 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
   uint32_t mbits = 0u;
   float fm = 0.f;
   // tile coordinates advanced incrementally (no 64-bit divisions in the loop)
-  const int64_t grid = gridDim.x;
+  const int64_t grid = nbx;
   const int64_t gbr = grid / tcn, gbc = grid - gbr * tcn;
   auto advance = [&](int64_t& br, int64_t& bc) {
     br += gbr;
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
     for (int k = 0; k < KR; ++k) nv[k] = __ldcs(reinterpret_cast<const V4*>(D + (rb + vy + k * RPI) * ldd + cb) + vx);
     ncs = __ldg(reinterpret_cast<const I4*>(colsel + cb) + vx);
   };
-  int64_t t = blockIdx.x;
+  int64_t t = bx;
   int64_t br = t / tcn, bc = t - br * tcn;
   if (t < ntiles && full_tile(br, bc)) load(br, bc);
   int b = 0;
@@ -433,17 +439,24 @@ __global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ 
   }
 }
 
+template <typename T, int TR, int TC, bool NM>
+__global__ void __launch_bounds__(256) prep_select_kernel(const T* __restrict__ D, int64_t ldd, int64_t nloc, int64_t n2, const int* __restrict__ colsel, T* __restrict__ Dt, int64_t ldt, unsigned long long* maxbits, int* nonfinite) {
+  prep_select_kernel_body<T, TR, TC, NM>(D, ldd, nloc, n2, colsel, Dt, ldt, maxbits, nonfinite, blockIdx.x, gridDim.x);
+}
+
 template <typename T>
 cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2, const int* colsel, T* Dt,
                                int64_t ldt, unsigned long long* maxbits, int* nonfinite, int num_sms,
                                cudaStream_t st) {
   if (nloc == 0 || n2 == 0) return cudaSuccess;
-  static const int shape = [] {  // tile shape (tuning knob): 0 = 64 x 64, 1 = 32 x 128 rows x columns
+  static const int shape = [] {  // tile shape (tuning knob): 0 = 64 x 64, 1 = 32 x 128, 2 = 64 x 128 rows x columns
     const char* e = std::getenv("IRCUR_PREP_SHAPE");
-    return e ? std::atoi(e) : 1;   // fp32 at cfg5: 8.22 ms (32 x 128, 512-byte row runs) vs 8.47 ms (64 x 64)
+    // fp32 at cfg5 (sampled copy, same box): 8.33 ms (64 x 128: 512-byte row runs read, 256-byte
+    // column runs written) vs 8.45 ms (32 x 128) vs 8.7 ms (64 x 64)
+    return e ? std::atoi(e) : 2;
   }();
-  const bool wide = sizeof(T) == 4 && shape == 1;
-  const int tr = wide ? 32 : kPT, tc = wide ? 128 : kPT;
+  const bool wide = sizeof(T) == 4 && shape >= 1;
+  const int tr = wide && shape == 1 ? 32 : kPT, tc = wide ? 128 : kPT;
   const int64_t ntiles = ((nloc + tr - 1) / tr) * ((n2 + tc - 1) / tc);
   // persistent grid: every CTA resident (the loop strides over the tiles)
   auto grid_for = [&](auto kern) {
@@ -460,6 +473,11 @@ cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2
     return e ? std::atoi(e) : 1;  // measured 8.11 vs 8.15 ms at cfg5 (same box)
   }();
   if constexpr (sizeof(T) == 4) {
+    if (wide && shape == 2) {
+      auto kern = prep_select_kernel<T, 64, 128, true>;
+      kern<<<grid_for(kern), 256, 0, st>>>(D, ldd, nloc, n2, colsel, Dt, ldt, maxbits, nonfinite);
+      return cudaGetLastError();
+    }
     if (wide) {
       auto kern = nanmax ? prep_select_kernel<T, 32, 128, true> : prep_select_kernel<T, 32, 128, false>;
       kern<<<grid_for(kern), 256, 0, st>>>(D, ldd, nloc, n2, colsel, Dt, ldt, maxbits, nonfinite);
@@ -523,22 +541,19 @@ __device__ __forceinline__ double seg_sq(const T* __restrict__ p, int64_t len) {
 constexpr int64_t kSlabSeg = 8192;
 
 template <typename T>
-__global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, int64_t row0, int64_t nloc,
-                                                      int64_t n2, const int* I, int mI, const int* J,
-                                                      int nJ, int nb_rows, double* partials, const T* Dt,
-                                                      int64_t ldt, const int* Jline) {
+__device__ __forceinline__ void slab_sq_kernel_body(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2, const int* I, int mI, const int* J, int nJ, int nb_rows, double* partials, const T* Dt, int64_t ldt, const int* Jline, int64_t bx, int64_t nbx) {
   __shared__ double sh[8];
   double acc = 0.0;
-  if ((int)blockIdx.x < nb_rows) {
+  if ((int)bx < nb_rows) {
     const int64_t segs = (n2 + kSlabSeg - 1) / kSlabSeg, units = (int64_t)mI * segs;
-    for (int64_t u = blockIdx.x; u < units; u += nb_rows) {
+    for (int64_t u = bx; u < units; u += nb_rows) {
       const int64_t k = u / segs, s = (u - k * segs) * kSlabSeg;
       const int64_t len = n2 - s < kSlabSeg ? n2 - s : kSlabSeg;
       acc += seg_sq(D + ((int64_t)I[k] - row0) * ldd + s, len);
     }
   } else {
-    const int nb_cols = gridDim.x - nb_rows;
-    const int cb = blockIdx.x - nb_rows;
+    const int nb_cols = (int)nbx - nb_rows;
+    const int cb = (int)bx - nb_rows;
     if (Dt) {  // the column-major copy holds D(:,J): contiguous lines
       const int64_t segs = (nloc + kSlabSeg - 1) / kSlabSeg, units = (int64_t)nJ * segs;
       for (int64_t u = cb; u < units; u += nb_cols) {
@@ -557,7 +572,12 @@ __global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, i
     }
   }
   const double s = block_sum<256>(acc, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  if (threadIdx.x == 0) partials[bx] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) slab_sq_kernel(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2, const int* I, int mI, const int* J, int nJ, int nb_rows, double* partials, const T* Dt, int64_t ldt, const int* Jline) {
+  slab_sq_kernel_body(D, ldd, row0, nloc, n2, I, mI, J, nJ, nb_rows, partials, Dt, ldt, Jline, blockIdx.x, gridDim.x);
 }
 
 template <typename T>
@@ -695,6 +715,100 @@ int64_t gen_blocks(int64_t nrows, int64_t n2) {
   return (cells + (int64_t)kGenNT * kGenPer - 1) / ((int64_t)kGenNT * kGenPer);
 }
 
+// ------------------------------------------------- batched prep (ircur_batch_prepare_many)
+// Every problem's prep pass, slab norms and result gather in one launch each
+// (grid.y = problem): the same per-problem bodies as the single-problem
+// launches, so max|D|, the non-finite flag, the column copy and the slab
+// partials are those of each problem's own pass (the partials use the
+// problem's own block split, and the gather adds them in the host's order).
+__global__ void prep_batch_init_kernel(const PrepBatchArg* __restrict__ as, int n) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) {
+    *as[p].maxbits = 0ull;
+    *as[p].nonfinite = 0;
+  }
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) prep_batched_kernel(const PrepBatchArg* __restrict__ as) {
+  const PrepBatchArg& a = as[blockIdx.y];
+  if (a.mode != MODE || a.nloc == 0 || a.n2 == 0) return;
+  const T* D = static_cast<const T*>(a.D);
+  if constexpr (MODE == 0) {
+    const bool vec = ((a.ldd * (int64_t)sizeof(T)) % 16 == 0) && ((uintptr_t)D % 16 == 0);
+    if (vec)
+      prep_scan_vec_kernel_body<T>(D, a.ldd, a.nloc, a.n2, a.maxbits, a.nonfinite, blockIdx.x, gridDim.x);
+    else
+      prep_scan_kernel_body<T>(D, a.ldd, a.nloc, a.n2, a.maxbits, a.nonfinite, blockIdx.x, gridDim.x);
+  } else if constexpr (MODE == 1) {
+    prep_transpose64_kernel_body<T>(D, a.ldd, a.nloc, a.n2, static_cast<T*>(a.Dt), a.ldt, a.maxbits, a.nonfinite,
+                                    1, blockIdx.x, gridDim.x);
+  } else if constexpr (sizeof(T) == 4) {
+    prep_select_kernel_body<T, 64, 128, true>(D, a.ldd, a.nloc, a.n2, a.colsel, static_cast<T*>(a.Dt), a.ldt,
+                                              a.maxbits, a.nonfinite, blockIdx.x, gridDim.x);
+  } else {
+    prep_select_kernel_body<T, kPT, kPT, false>(D, a.ldd, a.nloc, a.n2, a.colsel, static_cast<T*>(a.Dt), a.ldt,
+                                                a.maxbits, a.nonfinite, blockIdx.x, gridDim.x);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) slab_batched_kernel(const PrepBatchArg* __restrict__ as) {
+  const PrepBatchArg& a = as[blockIdx.y];
+  const int nb = a.nb_rows + a.nb_cols;
+  if ((int)blockIdx.x >= nb) return;
+  slab_sq_kernel_body<T>(static_cast<const T*>(a.D), a.ldd, a.row0, a.nloc, a.n2, a.I, a.mI, a.J, a.nJ, a.nb_rows,
+                         a.partials, a.use_dt ? static_cast<const T*>(a.Dt) : nullptr, a.ldt, a.Jline, blockIdx.x,
+                         nb);
+}
+
+// res[4 p ..]: max|D| (the maxbits pattern), non-finite flag, row-slab and
+// column-slab sums of squares (partials added in order, as ircur_slab_sqnorms)
+__global__ void prep_batch_gather_kernel(const PrepBatchArg* __restrict__ as, int n, double* __restrict__ res) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const PrepBatchArg& a = as[p];
+  res[4 * (size_t)p] = __longlong_as_double((long long)*a.maxbits);
+  res[4 * (size_t)p + 1] = (double)*a.nonfinite;
+  double x = 0.0, y = 0.0;
+  for (int i = 0; i < a.nb_rows; ++i) x += a.partials[i];
+  for (int i = 0; i < a.nb_cols; ++i) y += a.partials[a.nb_rows + i];
+  res[4 * (size_t)p + 2] = x;
+  res[4 * (size_t)p + 3] = y;
+}
+
+template <typename T>
+cudaError_t launch_prep_batched(const PrepBatchArg* d_args, const PrepBatchArg* h_args, int n, double* d_res,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n > 65535) return cudaErrorInvalidValue;
+  constexpr int kTilesPerCta = 16;  // each CTA strides over ~16 of its problem's tiles
+  int64_t want[3] = {0, 0, 0};
+  int max_slab = 0;
+  for (int p = 0; p < n; ++p) {
+    const PrepBatchArg& a = h_args[p];
+    if (a.mode < 0 || a.mode > 2) return cudaErrorInvalidValue;
+    int64_t tiles;
+    if (a.mode == 0) {
+      tiles = (a.nloc * a.n2 + 256 * (16 / (int64_t)sizeof(T)) - 1) / (256 * (16 / (int64_t)sizeof(T)));
+    } else if (a.mode == 1) {
+      tiles = ((a.nloc + kPT - 1) / kPT) * ((a.n2 + kPT - 1) / kPT);
+    } else {
+      const int64_t tr = kPT, tc = sizeof(T) == 4 ? 128 : kPT;  // (the default shapes of launch_prep_select)
+      tiles = ((a.nloc + tr - 1) / tr) * ((a.n2 + tc - 1) / tc);
+    }
+    want[a.mode] = std::max(want[a.mode], (tiles + kTilesPerCta - 1) / kTilesPerCta);
+    max_slab = std::max(max_slab, a.nb_rows + a.nb_cols);
+  }
+  prep_batch_init_kernel<<<(n + 127) / 128, 128, 0, st>>>(d_args, n);
+  if (want[0] > 0) prep_batched_kernel<T, 0><<<dim3((unsigned)std::min<int64_t>(want[0], 1 << 20), n), 256, 0, st>>>(d_args);
+  if (want[1] > 0) prep_batched_kernel<T, 1><<<dim3((unsigned)std::min<int64_t>(want[1], 1 << 20), n), 256, 0, st>>>(d_args);
+  if (want[2] > 0) prep_batched_kernel<T, 2><<<dim3((unsigned)std::min<int64_t>(want[2], 1 << 20), n), 256, 0, st>>>(d_args);
+  if (max_slab > 0) slab_batched_kernel<T><<<dim3((unsigned)max_slab, n), 256, 0, st>>>(d_args);
+  prep_batch_gather_kernel<<<(n + 127) / 128, 128, 0, st>>>(d_args, n, d_res);
+  return cudaGetLastError();
+}
+
 #define IRCUR_PREP_INST(T)                                                                       \
   template cudaError_t launch_prep<T>(const T*, int64_t, int64_t, int64_t, T*, int64_t,          \
                                       unsigned long long*, int*, int, cudaStream_t);              \
@@ -702,7 +816,8 @@ int64_t gen_blocks(int64_t nrows, int64_t n2) {
                                              int64_t, unsigned long long*, int*, int, cudaStream_t); \
   template cudaError_t launch_slab_sq<T>(const T*, int64_t, int64_t, int64_t, int64_t, const int*, \
                                          int, const int*, int, int, int, double*, const T*, int64_t, \
-                                         const int*, cudaStream_t);
+                                         const int*, cudaStream_t);                                      \
+  template cudaError_t launch_prep_batched<T>(const PrepBatchArg*, const PrepBatchArg*, int, double*, cudaStream_t);
 IRCUR_PREP_INST(float)
 IRCUR_PREP_INST(double)
 

@@ -132,6 +132,22 @@ template <typename T>
 cudaError_t launch_slab_sq(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2,
                            const int* I, int mI, const int* J, int nJ, int nb_rows, int nb_cols,
                            double* partials, const T* Dt, int64_t ldt, const int* Jline, cudaStream_t st);
+// batched prep pass + slab norms (ircur_batch_prepare_many): one entry per problem
+struct PrepBatchArg {
+  const void* D; int64_t ldd, nloc, n2, row0;
+  void* Dt; int64_t ldt;          // column-major copy (modes 1, 2)
+  const int* colsel;              // mode 2: column -> copy line (or -1)
+  int mode;                       // 0 scan only, 1 full column-major copy, 2 sampled columns
+  unsigned long long* maxbits; int* nonfinite;
+  // slab norms of set 0 (ircur_slab_sqnorms_async's geometry)
+  const int* I; int mI; const int* J; int nJ; const int* Jline; int use_dt;
+  int nb_rows, nb_cols; double* partials;
+};
+// init, prep pass per mode, slab norms and the gather of n x {max|D|,
+// non-finite, rows_sq, cols_sq} into d_res; h_args: a host copy of d_args
+template <typename T>
+cudaError_t launch_prep_batched(const PrepBatchArg* d_args, const PrepBatchArg* h_args, int n, double* d_res,
+                                cudaStream_t st);
 size_t svd_smem_bytes(int n, int m, int kk, int cs);
 int svd_pick_cluster(int n, int m, int kk);
 template <typename T> cudaError_t launch_svd(const SvdArgs& a, int cs, cudaStream_t st,

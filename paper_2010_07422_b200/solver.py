@@ -549,6 +549,32 @@ class DeviceHandle:
     dtype: int
 
 
+class _LazyDeviceHandle:
+    """DeviceHandle whose P^T / Q views of the context's factor buffers are
+    made on first use (torch.as_tensor over __cuda_array_interface__ costs
+    tens of microseconds, which adds up over the 512 results of a batch).
+    The views alias the same buffers whenever they are made: valid until the
+    context's next solve, like DeviceHandle's."""
+
+    def __init__(self, ctx: "Context", dtype: int):
+        self._ctx = ctx
+        self.dtype = dtype
+        self._views = None
+
+    def _get(self):
+        if self._views is None:
+            self._views = self._ctx.factor_views()
+        return self._views
+
+    @property
+    def Pt(self) -> torch.Tensor:
+        return self._get()[0]
+
+    @property
+    def Qt(self) -> torch.Tensor:
+        return self._get()[1]
+
+
 @dataclass
 class DeviceResult:
     trace: SolverTrace
@@ -977,6 +1003,7 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
         ctx._D = Dd
     code = _native_copy_code(colmajor, n2, m_cols, c0)
     failed = C.c_int(-1)
+    t_setup = _time.perf_counter()
     _capi.check(_capi.load().ircur_batch_prepare_many(
         harr, n, dptr, Dds[0].stride(0), pcg.ctypes.data_as(C.POINTER(C.c_uint64)), z0in.ctypes.data_as(pd),
         gam.ctypes.data_as(pd), eps.ctypes.data_as(pd), _capi.RESAMPLED if resampled else _capi.FIXED,
@@ -1029,13 +1056,16 @@ def solve_batch_device(Ds, configs, *, device=None, svd_cs: int = 0, colmajor="a
             tr.sampled_rows = [int(rcs[k if resampled else 0]) for k in range(iters)]
             tr.sampled_cols = [int(ccs[k if resampled else 0]) for k in range(iters)]
             I, J = sets[(iters - 1) if resampled else 0]
-            Pt, Qt = ctx.factor_views()  # valid until the context's next solve
-            res = DeviceResult(tr, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), DeviceHandle(Pt, Qt, _capi.F32))
+            res = DeviceResult(tr, cfg, ctx, IndexSet(I, n1), IndexSet(J, n2), _LazyDeviceHandle(ctx, _capi.F32))
             res.profile = None
             res._host_ms = None
             res.colmajor = cmv
             res.sets = sets
             out[i] = res
+        if stats is not None:
+            stats["results_s"] = _time.perf_counter() - t_prep - stats["batched_run_s"]
+    if stats is not None:
+        stats["setup_s"] = t_setup - t_start
     return out
 
 
