@@ -269,6 +269,11 @@ def run_ours(args):
     res.ctx.lib.ircur_debug_counter(res.ctx.h, 2, C.byref(kv))
     strip_kernel = {1: "strips_kernel (fp64 / cluster)", 2: "strips2_kernel", 3: "strips3_kernel",
                     5: "strips5_kernel (tcgen05)", 6: "strips6_kernel (mma.sync tf32)"}.get(int(kv.value), "strips")
+    if int(kv.value) == 3:
+        tcv = C.c_longlong(0)
+        res.ctx.lib.ircur_debug_counter(res.ctx.h, 4, C.byref(tcv))
+        if int(tcv.value):
+            strip_kernel = "strips3_kernel (FFMA2 thresholding and factor sums, tcgen05 tf32 residual)"
     n_strip = iters
     peak, peak_kind = peaks()
     achieved = strip_bytes / (strip_ms / 1e3) / 1e9

@@ -270,7 +270,9 @@ int ircur_get_marks(ircur_ctx_t ctx, float* ms);
  * (IRCUR_SAMPLED_CHECK=1; 0 means it reproduces the strips bitwise);
  * 1 = whether the run took the overlapped two-stream loop (IRCUR_OVERLAP),
  * 2 = the strip kernel of the process's last strip launch (1, 2, 3 = the FFMA
- * kernels, 5 = the tensor-core kernel). */
+ * kernels, 5 / 6 = the opt-in tensor-core kernels),
+ * 4 = whether the last strips3 launch ran its residual pass on the tensor
+ * cores (tcgen05; the default for row strips of >= 32768 positions). */
 int ircur_debug_counter(ircur_ctx_t ctx, int which, long long* value);
 /* Loop selection for the following runs on ctx: 1 = the overlapped loop
  * (SVD of k + 1 beside the strips of k on two streams) where eligible, 0 =

@@ -4,6 +4,8 @@
 // buffers, core, SVD scratch, index sets, trace) on one device + stream and
 // drives the device-resident iteration loop of solver.py:358-414.
 #include <cuda_runtime.h>
+
+#include <climits>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -2160,7 +2162,7 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
     SvdArgs* hsv = reinterpret_cast<SvdArgs*>(hc + n);
     StripsArgs<float>* hst = reinterpret_cast<StripsArgs<float>*>(hsv + n);
     FinalizeArgs* hf = reinterpret_cast<FinalizeArgs*>(hst + n);
-    int max_total = 0, max_n = 0, max_tiles = 0, maxl = 0, cs = 0, kk0 = -1;
+    int max_total = 0, max_n = 0, max_tiles = 0, maxl = 0, cs = 0, kk0 = -1, min_rowpos = INT_MAX;
     size_t smem = 0;
     const auto th0 = std::chrono::steady_clock::now();
     for (int p = 0; p < n; ++p) {
@@ -2190,6 +2192,7 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
       max_n = std::max(max_n, q.nJ);
       max_tiles = std::max(max_tiles, sa.s[0].tiles + sa.s[1].tiles);
       maxl = std::max(maxl, sa.maxl);
+      min_rowpos = std::min(min_rowpos, sa.s[0].npos);
       if (kk0 < 0) kk0 = hsv[p].kk;
       if (hsv[p].kk != kk0) return fail(IRCUR_EINVAL, "batched problems need one SVD block size");
       if (!sa.s[0].bulk_ok || !sa.s[1].bulk_ok)
@@ -2220,7 +2223,7 @@ int ircur_batched_run(ircur_ctx_t* ctxs, int n, void* stream, int svd_cs, int* i
     IR_CUDA(launch_core_batched<float>(dc, n, max_total, R, bs));
     IR_CUDA(launch_svd_batched<float>(dsv, n, max_n, cs, smem, svd_reg_path(hsv[0]), bs));
     if (strip_ms) IR_CUDA(cudaEventRecord(evs[2 * (size_t)k], bs));
-    IR_CUDA(launch_strips3_batched(dst, n, std::min(max_tiles, batch_strip_ctas()), maxl, R, bs));
+    IR_CUDA(launch_strips3_batched(dst, n, std::min(max_tiles, batch_strip_ctas()), maxl, R, min_rowpos, bs));
     if (strip_ms) IR_CUDA(cudaEventRecord(evs[2 * (size_t)k + 1], bs));
     IR_CUDA(launch_finalize_batched(df, n, bs));
     IR_CUDA(cudaEventRecord(evk[slot], bs));
@@ -2505,7 +2508,7 @@ int ircur_set_profiling(ircur_ctx_t c, int on) {
 }
 
 int ircur_debug_counter(ircur_ctx_t c, int which, long long* value) {
-  if (!c || !value || which < 0 || which > 3) return fail(IRCUR_EINVAL, "bad context/counter");
+  if (!c || !value || which < 0 || which > 4) return fail(IRCUR_EINVAL, "bad context/counter");
   IR_CUDA(cudaSetDevice(c->device));
   if (which == 1) {  // the last ircur_run took the overlapped loop
     *value = c->last_run_overlapped;
@@ -2513,6 +2516,10 @@ int ircur_debug_counter(ircur_ctx_t c, int which, long long* value) {
   }
   if (which == 2) {  // the strip kernel of the process's last strip launch (1, 2, 3 or 5)
     *value = ircur::g_last_strips_kernel.load();
+    return IRCUR_OK;
+  }
+  if (which == 4) {  // the process's last strips3 launch ran its residual on the tensor cores
+    *value = ircur::g_last_strips3_tc.load();
     return IRCUR_OK;
   }
   unsigned v = 0;

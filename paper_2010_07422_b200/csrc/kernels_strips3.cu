@@ -509,17 +509,22 @@ __global__ void __launch_bounds__(kS3NT, R <= 6 ? 2 : 1) strips3_kernel_batched(
 size_t strips3_smem_bytes(int maxl, int R) { return strips3_layout(maxl, R).total; }
 
 // The tensor-core residual is the default where it applies (R <= 10, at most
-// 512 lines per strip, the padded stage fits); IRCUR_S3_TC=0 keeps the FFMA
-// residual (A/B runs).
-static bool strips3_tc_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("IRCUR_S3_TC");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+// 512 lines per strip, the padded stage fits) and pays: its per-tile MMA
+// round trip needs several tiles per CTA to amortise, so it is taken for row
+// strips of at least 32768 positions (measured: cfg5 263 -> 244 us per launch,
+// n = 10^4 and smaller 10-15% slower).  The rule depends on the row strip's
+// width only, which row sharding and batching do not change, so a problem
+// gets the same residual arithmetic on every path.  IRCUR_S3_TC=0 keeps the
+// FFMA residual, =2 forces the tensor-core one wherever it fits (A/B runs, tests).
+constexpr int kS3TcMinPos = 32768;
+std::atomic<int> g_last_strips3_tc{0};
+static int strips3_tc_knob() {  // read per launch (tests switch it)
+  const char* e = std::getenv("IRCUR_S3_TC");
+  return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 1;
 }
-bool strips3_uses_tc(int maxl, int R) {
-  return strips3_tc_enabled() && 6 * R <= kS3K && maxl <= 512 &&
+bool strips3_uses_tc(int maxl, int R, int row_positions) {
+  const int knob = strips3_tc_knob();
+  return knob != 0 && (knob == 2 || row_positions >= kS3TcMinPos) && 6 * R <= kS3K && maxl <= 512 &&
          strips3_layout(maxl, R, true).total <= (size_t)227 * 1024;
 }
 
@@ -546,14 +551,15 @@ static cudaError_t strips3_launch_batched_one(const StripsArgs<float>* d_args, i
 }
 
 cudaError_t launch_strips3_batched(const StripsArgs<float>* d_args, int n, int ctas, int maxl, int R,
-                                   cudaStream_t st) {
+                                   int min_row_positions, cudaStream_t st) {
   if (n <= 0 || ctas <= 0) return cudaSuccess;
   if (strips3_layout(maxl, R).total > (size_t)227 * 1024) return cudaErrorNotSupported;
   // the same residual arithmetic as a problem's own solve (launch_strips3 makes the same choice)
-  const bool tc = strips3_uses_tc(maxl, R);
+  const bool tc = strips3_uses_tc(maxl, R, min_row_positions);
   const size_t smem = strips3_layout(maxl, R, tc).total;
   cudaError_t e = cudaErrorInvalidValue;
   IRCUR_DISPATCH_RANK(R, RR, { e = strips3_launch_batched_one<RR>(d_args, n, ctas, tc, smem, st); });
+  g_last_strips3_tc = tc ? 1 : 0;
   return e;
 }
 
@@ -582,7 +588,7 @@ cudaError_t launch_strips3(const StripsArgs<float>& a0, int R, int num_sms, int*
   a.maxl = a.s[0].nk > a.s[1].nk ? a.s[0].nk : a.s[1].nk;
   for (int q = 0; q < 2; ++q)  // the caller counts tiles of the 64-position cluster kernel (same width)
     if (a.s[q].tiles > 0) a.s[q].tiles = (a.s[q].npos + kS3TX - 1) / kS3TX;
-  const bool tc = strips3_uses_tc(a.maxl, R);
+  const bool tc = strips3_uses_tc(a.maxl, R, a.s[0].tiles > 0 ? a.s[0].npos : a.s[1].npos);
   const size_t smem = strips3_layout(a.maxl, R, tc).total;
   if (smem > (size_t)227 * 1024) return cudaErrorNotSupported;
   if (ncta_out) *ncta_out = 0;
@@ -593,6 +599,7 @@ cudaError_t launch_strips3(const StripsArgs<float>& a0, int R, int num_sms, int*
   const int grid = tiles < num_sms ? tiles : num_sms;
   cudaError_t e = cudaErrorInvalidValue;
   IRCUR_DISPATCH_RANK(R, RR, { e = strips3_launch_one<RR>(a, tc, grid, smem, st); });
+  g_last_strips3_tc = tc ? 1 : 0;
   if (ncta_out) *ncta_out = tiles;  // partial slots: one per tile
   return e;
 }

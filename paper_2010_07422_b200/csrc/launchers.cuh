@@ -105,6 +105,7 @@ inline bool strips_tc_selected(const StripsArgs<float>& a, int R) {
   return strips5_selected(a, R) || strips6_selected(a, R);
 }
 extern std::atomic<int> g_last_strips_kernel;  // diagnostics (ircur_debug_counter 2)
+extern std::atomic<int> g_last_strips3_tc;     // the last strips3 launch's residual ran on tcgen05 (counter 4)
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 // ---- batched problems (ircur_batched_run): device arrays of per-problem arguments
 template <typename T>
@@ -115,8 +116,10 @@ cudaError_t launch_svd_batched(const SvdArgs* d_args, int n, int max_n, int cs, 
                                cudaStream_t st);
 bool svd_reg_path(const SvdArgs& a);
 void set_draw_threads_for_thread(int n);  // draws.cu: per-thread draw parallelism (0 = default)  // the svd_kernel<T, true> instantiation runs (kk <= 8)
+// min_row_positions: the narrowest row strip of the batch (the residual
+// arithmetic is chosen as launch_strips3 chooses it for a problem of that width)
 cudaError_t launch_strips3_batched(const StripsArgs<float>* d_args, int n, int ctas, int maxl, int R,
-                                   cudaStream_t st);
+                                   int min_row_positions, cudaStream_t st);
 template <typename T> cudaError_t launch_writeout(const WriteoutArgs<T>& a, int R, cudaStream_t st);
 template <typename T, typename O>
 cudaError_t launch_materialize(const T* Pt, int64_t ldp, const T* Qt, int64_t ldq, int64_t nloc,
