@@ -311,8 +311,11 @@ SvdArgs svd_args(ircur_ctx* c, int k, const IterSets& q) {
   // fp32 data: the strips carry ~6e-8 relative round-off, and a 1e-6
   // lambda_1 floor leaves L within that noise of the 1e-11 result (measured
   // at cfg2/cfg5: 8e-8 relative, same iterations) for 20% fewer steps
+  // fp32 scale 1e-5 (round 2): the e_k of the first iterations move by
+  // < 3e-5 relative (the parity bar is 2e-4; 1e-4 measured 2.7e-4 on a cfg4
+  // problem), the final L by fp32 round-off (1e-7), for 8 of cfg5's 91 steps
   sa.tol = sizeof(T) == 8 ? 2e-14 : 1e-6;
-  sa.tol_scale = sizeof(T) == 8 ? 1e-11 : 1e-8;
+  sa.tol_scale = sizeof(T) == 8 ? 1e-11 : 1e-5;
   if (const char* ev = std::getenv(sizeof(T) == 8 ? "IRCUR_SVD_TOL64" : "IRCUR_SVD_TOL32"))  // tuning
     sa.tol = std::atof(ev);
   if (const char* ev = std::getenv(sizeof(T) == 8 ? "IRCUR_SVD_TOLSCALE64" : "IRCUR_SVD_TOLSCALE32"))  // tuning
