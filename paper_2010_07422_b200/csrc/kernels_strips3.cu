@@ -202,6 +202,7 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
     const bool next = tn < total;
     const bool same_next = next && ((tn < tiles0) == (t < tiles0));  // the next tile's halves line up with these
     if (q != cur) {  // per-pair line vectors of this strip: (A | W | Res)[t] for lines 2kp, 2kp+1
+#pragma unroll 4  // (independent global loads: batch them)
       for (int e = tid; e < np * NV * RPc; e += kS3NT) {
         const int kp = e / (NV * RPc), rem = e - kp * NV * RPc, v = rem / RPc, tt = rem - v * RPc;
         const float* sv = v == 0 ? s.lineA : (v == 1 ? s.lineW : s.lineRes);
@@ -222,6 +223,9 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
         const int line = 128 * (w >> 2) + 32 * (w & 3) + lane;
         const bool live = mode != kStripPartial && line < nl;
         const uint32_t ta = T + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)(kS3K * (w >> 2));
+        float rr[R];  // this line's Res row (loaded once)
+#pragma unroll
+        for (int tt = 0; tt < R; ++tt) rr[tt] = live ? s.lineRes[(int64_t)line * R + tt] : 0.f;
 #pragma unroll
         for (int c = 0; c < kS3K / 16; ++c) {  // 16 columns at a time (registers)
           float v[16];
@@ -229,9 +233,9 @@ __device__ __forceinline__ void strips3_body(const StripsArgs<float>& a, int bx,
           for (int j = 0; j < 16; ++j) {
             const int k = 16 * c + j, part = k / R, tt = k - part * R;  // compile-time after unrolling
             float val = 0.f;
-            if (part < 6 && live) {
+            if (part < 6) {
               float hi, mid, lo;
-              s3_split(s.lineRes[(int64_t)line * R + tt], hi, mid, lo);
+              s3_split(rr[tt], hi, mid, lo);
               val = (part == 0 || part == 1 || part == 4) ? hi : (part == 5 ? lo : mid);
             }
             v[j] = val;
