@@ -88,6 +88,10 @@ struct ircur_ctx {
   int* d_colsel = nullptr;   // n2: column -> line of Dt or -1 (mode 2)
   int* d_cols_c = nullptr;   // per set: Dt line of each J entry (mode 2)
   int64_t cols_c_cap = 0;
+  std::vector<int> h_sel;    // host copy of the column -> line map (mode 2), extended in place
+  int64_t dt_used = 0;       // lines of Dt in use (mode 2)
+  int* d_newcols = nullptr;  // columns of one extension (extend_cover)
+  int64_t newcols_cap = 0;
   std::vector<int> h_cols;   // host copy of the J sets (n_sets x max_cols)
 
   int* d_rows = nullptr;
@@ -449,13 +453,16 @@ int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfi
   std::fill(lines, lines + nlines, -1);
   for (int s = 0; s < c->n_sets; ++s)
     for (int j = 0; j < c->h_col_cnt[s]; ++j) lines[(size_t)s * c->max_cols + j] = sel[c->h_cols[(size_t)s * c->max_cols + j]];
+  c->h_sel.assign(sel, sel + c->n2);
+  c->dt_used = nl;
   if (nl > c->dt_cap) {
     IR_CUDA(cudaStreamSynchronize(st));  // in-flight iterations may still read the old copy
     if (c->Dt) cudaFree(c->Dt);
     c->Dt = nullptr;
     c->dt_cap = 0;
     c->ldt = pad4(c->nloc);
-    const int64_t cap = std::min<int64_t>(c->n2, nl + nl / 4 + 64);
+    // half again as many lines: extend_cover appends the columns of later sets
+    const int64_t cap = std::min<int64_t>(c->n2, nl + nl / 2 + 64);
     IR_CUDA(cudaMalloc(&c->Dt, (size_t)cap * c->ldt * c->esz));
     c->dt_cap = cap;
   }
@@ -464,8 +471,10 @@ int build_cover(ircur_ctx* c, int cover, unsigned long long* maxbits, int* nonfi
     IR_CUDA(cudaStreamSynchronize(st));
     if (c->d_cols_c) cudaFree(c->d_cols_c);
     c->d_cols_c = nullptr;
-    IR_CUDA(cudaMalloc(&c->d_cols_c, nlines * sizeof(int)));
-    c->cols_c_cap = (int64_t)nlines;
+    // (room for the sets appended after this pass: extend_cover fills their rows)
+    const size_t want = std::max(nlines, (size_t)std::max(c->max_iter, c->n_sets) * c->max_cols);
+    IR_CUDA(cudaMalloc(&c->d_cols_c, want * sizeof(int)));
+    c->cols_c_cap = (int64_t)want;
   }
   IR_CUDA(cudaMemcpyAsync(c->d_colsel, sel, (size_t)c->n2 * sizeof(int), cudaMemcpyHostToDevice, st));
   IR_CUDA(cudaMemcpyAsync(c->d_cols_c, lines, nlines * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -516,12 +525,79 @@ int prep_rows(ircur_ctx* c, int64_t r0, int64_t r1) {
   return IRCUR_OK;
 }
 
+// Sets the prep pass copies for a threshold schedule that needs `est` =
+// ceil(log eps / log gamma) iterations to reach eps (solver._cover_sets, the
+// same rule).  The measured counts are ~0.7 est (cfg1-cfg5: 22-24 of 33), and
+// a set past the cover costs one extend_cover gather (~0.25 ms at cfg5)
+// against ~0.06 ms for a set copied by the prep pass, so the cover is 3/4 est
+// + 2 rather than est + 8: 27 sets instead of 41 at cfg5, 2.3 GB fewer writes.
+int cover_sets_for(int est) { return (3 * est + 3) / 4 + 2; }
+
+// Extend the sampled copy to the J sets [covered, cover) without another pass
+// over D: columns not yet in Dt take its next free lines and are gathered
+// from the row-major D (one 32-byte sector per element: n1 * |J| * 32 bytes
+// per set at fp32, ~0.25 ms at cfg5, against ~7 ms for a full prep pass).
+// Falls back to build_cover when Dt or the line table is too small.
+int extend_cover(ircur_ctx* c, int cover) {
+  cover = std::max(1, std::min(cover, c->n_sets));
+  if (cover <= c->covered) return IRCUR_OK;
+  cudaStream_t st = c->stream;
+  const size_t mc = (size_t)c->max_cols;
+  std::vector<int> h_sel = c->h_sel;  // (committed below, once the extension is known to fit)
+  std::vector<int> newcols;
+  int64_t nl = c->dt_used;
+  for (int s = c->covered; s < cover; ++s)
+    for (int j = 0; j < c->h_col_cnt[s]; ++j) {
+      const int col = c->h_cols[(size_t)s * mc + j];
+      if (h_sel[col] < 0) {
+        h_sel[col] = 0;
+        newcols.push_back(col);
+      }
+    }
+  // ascending columns: the 32 columns a warp of the gather reads in one row then
+  // share DRAM pages
+  std::sort(newcols.begin(), newcols.end());
+  for (int col : newcols) h_sel[col] = (int)nl++;
+  if ((int64_t)h_sel.size() != c->n2 || nl > c->dt_cap || (int64_t)((size_t)cover * mc) > c->cols_c_cap || !c->D)
+    return build_cover(c, cover, c->maxbits, c->flags + 4);
+  IR_CUDA(cudaEventSynchronize(c->ev_stage));  // staging free to rewrite
+  IR_CUDA(c->st_lines.reserve((size_t)c->n_sets * mc * sizeof(int)));
+  int* lines = c->st_lines.as<int>();
+  for (int s = c->covered; s < cover; ++s)
+    for (size_t j = 0; j < mc; ++j)
+      lines[(size_t)s * mc + j] = (int)j < c->h_col_cnt[s] ? h_sel[c->h_cols[(size_t)s * mc + j]] : -1;
+  IR_CUDA(cudaMemcpyAsync(c->d_cols_c + (size_t)c->covered * mc, lines + (size_t)c->covered * mc,
+                          (size_t)(cover - c->covered) * mc * sizeof(int), cudaMemcpyHostToDevice, st));
+  IR_CUDA(cudaEventRecord(c->ev_stage, st));
+  if (!newcols.empty()) {
+    if ((int64_t)newcols.size() > c->newcols_cap) {
+      if (c->d_newcols) cudaFree(c->d_newcols);
+      c->d_newcols = nullptr;
+      const int64_t want = std::max<int64_t>((int64_t)newcols.size(), 16 * (int64_t)mc);
+      IR_CUDA(cudaMalloc(&c->d_newcols, (size_t)want * sizeof(int)));
+      c->newcols_cap = want;
+    }
+    // (pageable source: the copy is staged before the call returns)
+    IR_CUDA(cudaMemcpyAsync(c->d_newcols, newcols.data(), newcols.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (c->dtype == IRCUR_F32)
+      IR_CUDA(launch_gather_cols<float>((const float*)c->D, c->ldd, c->nloc, c->d_newcols, (int)newcols.size(),
+                                        (float*)c->Dt, c->ldt, c->dt_used, st));
+    else
+      IR_CUDA(launch_gather_cols<double>((const double*)c->D, c->ldd, c->nloc, c->d_newcols, (int)newcols.size(),
+                                         (double*)c->Dt, c->ldt, c->dt_used, st));
+  }
+  c->h_sel.swap(h_sel);
+  c->dt_used = nl;
+  c->covered = cover;
+  return IRCUR_OK;
+}
+
 // Before iteration on `set`: extend the sampled copy when the loop has run
-// past the sets it covers (the finite/max results of the re-read are unused).
+// past the sets it covers.
 int ensure_cover(ircur_ctx* c, int set) {
   if (c->dt_mode != 2 || set < c->covered) return IRCUR_OK;
-  const int grow = std::max(8, c->covered / 2);
-  return build_cover(c, set + grow, c->maxbits, c->flags + 4);
+  const int grow = std::max(4, c->covered / 4);
+  return extend_cover(c, set + grow);
 }
 
 // One single-device iteration: core -> gram+svd -> fused strips -> finalize.
@@ -693,10 +769,15 @@ int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max
   };
   // column copy must cover the set before any stream reads it; a rebuild
   // (rare: the loop ran past the covered sets) drains both streams first
+  bool stop_seen = false;  // the drain before an extension found the loop finished
   auto cover = [&](int set) -> int {
     if (c->dt_mode != 2 || set < c->covered) return IRCUR_OK;
     IR_CUDA(cudaStreamSynchronize(sA));
     IR_CUDA(cudaStreamSynchronize(sB));
+    if (c->h_flags && c->h_flags[0] != 0) {  // (the run-ahead got here; nothing more to launch)
+      stop_seen = true;
+      return IRCUR_OK;
+    }
     if (int rc = ensure_cover(c, set)) return rc;
     IR_CUDA(cudaEventRecord(c->ov_cover, us));
     IR_CUDA(cudaStreamWaitEvent(sA, c->ov_cover, 0));
@@ -724,6 +805,7 @@ int run_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, int max
       cs_next = svd_cluster_size(qn.nJ, qn.mI_all, svd_args<float>(c, 1, qn).kk);
     } else if (next) {
       if (int rc = cover(set_of(k + 1))) return rc;
+      if (stop_seen) break;
       if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 2), 0));
       IR_CUDA(launch_sampled_factors(sampled_args(c, k, q, set_of(k + 1), zetas[k]), R, sA));
       if (c->profiling) IR_CUDA(cudaEventRecord(c->evp[(size_t)k * 5 + 4], sA));
@@ -1035,10 +1117,15 @@ int run_shard_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, i
     return IRCUR_OK;
   };
   (void)Ucore;
+  bool stop_seen = false;  // the drain before an extension found the loop finished
   auto cover = [&](int set) -> int {
     if (c->dt_mode != 2 || set < c->covered) return IRCUR_OK;
     IR_CUDA(cudaStreamSynchronize(sA));
     IR_CUDA(cudaStreamSynchronize(sB));
+    if (c->h_flags && c->h_flags[0] != 0) {  // (the run-ahead got here; nothing more to launch)
+      stop_seen = true;
+      return IRCUR_OK;
+    }
     if (int rc = ensure_cover(c, set)) return rc;
     IR_CUDA(cudaEventRecord(c->ov_cover, us));
     IR_CUDA(cudaStreamWaitEvent(sA, c->ov_cover, 0));
@@ -1071,6 +1158,9 @@ int run_shard_overlap(ircur_ctx* c, const double* zetas, double eps, int mode, i
       const IterSets qn = iter_sets(c, set_of(1));
       cs_next = svd_cluster_size(qn.nJ, qn.mI_all, svd_args<float>(c, 1, qn).kk);
     } else if (next) {
+      // (every rank launches the same seen + ahead iterations: if the drain before an
+      // extension finds the loop finished, the copy stays as it is and the remaining
+      // launches return on the done flag; the flag is the same on every rank here)
       if (int rc = cover(set_of(k + 1))) return rc;
       if (k >= 1) IR_CUDA(cudaStreamWaitEvent(sA, ev(k - 1, 2), 0));  // Q_{k-1} complete (the finish pass)
       SampledArgs sm = sampled_args(c, k, q, set_of(k + 1), zetas[k]);
@@ -1274,7 +1364,7 @@ int ircur_ctx_destroy(ircur_ctx_t c) {
                   c->W[1], c->sigma[1], c->V[1], c->inv[1],
                   c->G, c->svd_scratch, c->partials, c->errors, c->flags, c->maxbits, c->svd_steps,
                   c->rowmap[0], c->colmap[0], c->rowmap[1], c->colmap[1], c->svd_dbg, c->Qpart, c->scal,
-                  c->d_colsel, c->d_cols_c, c->dbg_counter};
+                  c->d_colsel, c->d_cols_c, c->d_newcols, c->dbg_counter};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -1676,6 +1766,10 @@ int ircur_run(ircur_ctx_t c, const double* zetas, double eps, int mode, int max_
     const bool fin = hf[0] != 0;
     while (!fin && launched < max_iter && launched < seen + kAhead) {
       const int set = mode == IRCUR_FIXED ? 0 : launched;
+      if (c->dt_mode == 2 && set >= c->covered) {  // extend only if the loop is really still running
+        IR_CUDA(cudaStreamSynchronize(st));
+        if (hf[0] != 0) break;
+      }
       if (int rc = ensure_cover(c, set)) return rc;
       int rc = iteration(c, launched, set, zetas[launched], eps, max_iter, true);
       if (rc) return rc;
@@ -1738,7 +1832,7 @@ int solve_setup(ircur_ctx* c, const void* D, int64_t ldd, const uint64_t* pcg, d
   // copy plan (solver._copy_plan): 3 = full copy when the covered columns exceed 70% of D
   int cm = colmajor, cover = 0;
   if (cm >= 2) {
-    cover = resampled ? std::max(1, std::min(n_first, est + 8)) : 1;
+    cover = resampled ? std::max(1, std::min(n_first, cover_sets_for(est))) : 1;
     if (cm == 3) {
       std::vector<unsigned char> mark((size_t)c->n2, 0);
       int64_t u = 0;
@@ -1921,7 +2015,7 @@ int ircur_batch_prepare_many(ircur_ctx_t* ctxs, int n, const void* const* D, int
       const int n_first = resampled ? std::min(n_sets, est + 8) : n_sets;
       int cm = colmajor, cover = 0;
       if (cm >= 2) {  // solver._copy_plan, as solve_setup
-        cover = resampled ? std::max(1, std::min(n_first, est + 8)) : 1;
+        cover = resampled ? std::max(1, std::min(n_first, cover_sets_for(est))) : 1;
         if (cm == 3) {
           std::vector<unsigned char> mark((size_t)c->n2, 0);
           int64_t u = 0;

@@ -809,6 +809,45 @@ cudaError_t launch_prep_batched(const PrepBatchArg* d_args, const PrepBatchArg* 
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------ column gather
+// Columns cols[0, ncols) of the row-major D into lines [slot0, slot0 + ncols)
+// of the column-major copy (extend_cover: the loop ran past the sets the prep
+// pass covered).  64 x 32 tiles through shared memory: the reads are one
+// 32-byte sector per element (strided columns), the writes 256-byte runs.
+constexpr int kGcRows = 64, kGcCols = 32;
+template <typename T>
+__global__ void __launch_bounds__(256) gather_cols_kernel(const T* __restrict__ D, int64_t ldd, int64_t nloc,
+                                                          const int* __restrict__ cols, int ncols,
+                                                          T* __restrict__ Dt, int64_t ldt, int64_t slot0) {
+  __shared__ T tile[kGcRows][kGcCols + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * kGcRows;
+  const int c0 = blockIdx.y * kGcCols;
+  const int tid = threadIdx.x;
+  {
+    const int cc = tid & (kGcCols - 1);
+    const int64_t col = c0 + cc < ncols ? cols[c0 + cc] : -1;
+#pragma unroll
+    for (int rr = tid / kGcCols; rr < kGcRows; rr += 256 / kGcCols)
+      tile[rr][cc] = (col >= 0 && r0 + rr < nloc) ? D[(r0 + rr) * ldd + col] : T(0);
+  }
+  __syncthreads();
+  {
+    const int rr = tid & (kGcRows - 1);
+#pragma unroll
+    for (int cc = tid / kGcRows; cc < kGcCols; cc += 256 / kGcRows)
+      if (c0 + cc < ncols && r0 + rr < nloc) Dt[(slot0 + c0 + cc) * ldt + r0 + rr] = tile[rr][cc];
+  }
+}
+
+template <typename T>
+cudaError_t launch_gather_cols(const T* D, int64_t ldd, int64_t nloc, const int* cols, int ncols, T* Dt,
+                               int64_t ldt, int64_t slot0, cudaStream_t st) {
+  if (ncols <= 0 || nloc <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)((nloc + kGcRows - 1) / kGcRows), (unsigned)((ncols + kGcCols - 1) / kGcCols));
+  gather_cols_kernel<T><<<grid, 256, 0, st>>>(D, ldd, nloc, cols, ncols, Dt, ldt, slot0);
+  return cudaGetLastError();
+}
+
 #define IRCUR_PREP_INST(T)                                                                       \
   template cudaError_t launch_prep<T>(const T*, int64_t, int64_t, int64_t, T*, int64_t,          \
                                       unsigned long long*, int*, int, cudaStream_t);              \
@@ -817,7 +856,8 @@ cudaError_t launch_prep_batched(const PrepBatchArg* d_args, const PrepBatchArg* 
   template cudaError_t launch_slab_sq<T>(const T*, int64_t, int64_t, int64_t, int64_t, const int*, \
                                          int, const int*, int, int, int, double*, const T*, int64_t, \
                                          const int*, cudaStream_t);                                      \
-  template cudaError_t launch_prep_batched<T>(const PrepBatchArg*, const PrepBatchArg*, int, double*, cudaStream_t);
+  template cudaError_t launch_prep_batched<T>(const PrepBatchArg*, const PrepBatchArg*, int, double*, cudaStream_t); \
+  template cudaError_t launch_gather_cols<T>(const T*, int64_t, int64_t, const int*, int, T*, int64_t, int64_t, cudaStream_t);
 IRCUR_PREP_INST(float)
 IRCUR_PREP_INST(double)
 

@@ -131,6 +131,10 @@ template <typename T>
 cudaError_t launch_prep_select(const T* D, int64_t ldd, int64_t nloc, int64_t n2, const int* colsel, T* Dt,
                                int64_t ldt, unsigned long long* maxbits, int* nonfinite, int num_sms,
                                cudaStream_t st);
+// columns cols[0, ncols) of the row-major D into lines [slot0, slot0 + ncols) of Dt (kernels_prep.cu)
+template <typename T>
+cudaError_t launch_gather_cols(const T* D, int64_t ldd, int64_t nloc, const int* cols, int ncols, T* Dt,
+                               int64_t ldt, int64_t slot0, cudaStream_t st);
 template <typename T>
 cudaError_t launch_slab_sq(const T* D, int64_t ldd, int64_t row0, int64_t nloc, int64_t n2,
                            const int* I, int mI, const int* J, int nJ, int nb_rows, int nb_cols,

@@ -146,6 +146,27 @@ def test_colmajor_copy_and_strided_paths_agree(ir, dtype, mode):
             np.testing.assert_array_equal(x, y)
 
 
+@pytest.mark.parametrize("overlap", [True, False])
+def test_sampled_copy_extensions_agree(ir, overlap):
+    """A sampled copy that covers fewer sets than the loop runs is extended on
+    the way: by gathering the new columns from the row-major D into the copy's
+    free lines (extend_cover), or by a full prep pass when those run out.  Both
+    happen here (6 -> 10 sets does not fit the first allocation, 10 -> 14 does);
+    the results are those of the full copy, bit for bit, on either loop."""
+    from oracle.ircur_oracle import baseline_problem_blocked
+    D = baseline_problem_blocked(3000, 2500, 5, 0.2, 75, dtype=np.float32)[0]
+    linf = float(np.abs(D).max()) * 0.5
+    cfg = ir.SolverConfig(rank=5, gamma=0.7, eps=1e-5, zeta0=linf, mode="resampled", max_iter=80, seed=ir.RngSeed(5))
+    ref = ir.solve(D, cfg, device=0, colmajor="full", overlap=overlap)
+    assert ref[2].iterations > 16 and ref[2].converged
+    for cm in ("sampled:6", "sampled:15", "sampled"):
+        b = ir.solve(D, cfg, device=0, colmajor=cm, overlap=overlap)
+        assert b[2].iterations == ref[2].iterations and b[2].errors == ref[2].errors, cm
+        for x, y in ((b[0].C, ref[0].C), (b[0].R, ref[0].R), (b[1].col_values, ref[1].col_values)):
+            np.testing.assert_array_equal(x, y)
+    ir.clear_cache()
+
+
 def test_materialize_matches_oracle(ir):
     from oracle import ircur_oracle as orc
     D, meta, g = load_golden("bl_sq120_r3_resampled")

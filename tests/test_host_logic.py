@@ -89,7 +89,8 @@ def test_copy_plan(monkeypatch):
     m = ir.sample_count(n, 10, 4.0)
     sets = ir.draw_index_sets(n, n, m, m, ir.RngSeed(1), 100)
     mode, cover = _copy_plan("auto", n, m, sets, cfg)
-    assert mode == 2 and cover == int(np.ceil(np.log(1e-5) / np.log(0.7))) + 8
+    est = int(np.ceil(np.log(1e-5) / np.log(0.7)))  # 33: the schedule's iteration estimate
+    assert mode == 2 and cover == (3 * est + 3) // 4 + 2 == 27  # (capi.cu cover_sets_for, the same rule)
     assert _copy_plan("full", n, m, sets, cfg) == (1, 0)
     assert _copy_plan(False, n, m, sets, cfg) == (0, 0)
     assert _copy_plan("sampled:3", n, m, sets, cfg) == (2, 3)
@@ -165,7 +166,7 @@ def test_native_copy_code_matches_copy_plan(monkeypatch):
     """solver._native_copy_code (the code ircur_solve receives) makes the
     same copy-plan decision as solver._copy_plan for every colmajor form;
     code 3 is the covered-column rule, evaluated here like ircur_solve does."""
-    from paper_2010_07422_b200.solver import _copy_plan, _cover_estimate, _native_copy_code
+    from paper_2010_07422_b200.solver import _copy_plan, _cover_sets, _native_copy_code
     monkeypatch.delenv("IRCUR_COLMAJOR", raising=False)
     monkeypatch.delenv("IRCUR_NATIVE", raising=False)
     for (n, m, ns) in ((100000, 461, 49), (200, 60, 100), (10000, 185, 49)):
@@ -176,7 +177,7 @@ def test_native_copy_code_matches_copy_plan(monkeypatch):
                 want = _copy_plan(cm, n, m, sets, cfg)
                 code = _native_copy_code(cm, n, m, cfg)
                 assert code is not None
-                cover = 1 if mode == "fixed" else max(1, min(len(sets), _cover_estimate(cfg) + 8))
+                cover = 1 if mode == "fixed" else max(1, min(len(sets), _cover_sets(cfg)))
                 if code == 3:
                     u = len(set(np.concatenate([sets[k][1] for k in range(cover)]).tolist()))
                     got = (1, 0) if u > 0.7 * n else (2, cover)
