@@ -1810,7 +1810,8 @@ int solve_setup(ircur_ctx* c, const void* D, int64_t ldd, const uint64_t* pcg, d
   const bool resampled = mode == IRCUR_RESAMPLED;
   const int n_sets = resampled ? max_iter : 1;
   const int est = (int)std::ceil(std::log(eps) / std::log(gamma));
-  const int n_first = resampled ? std::min(n_sets, est + 8) : n_sets;
+  // (the sets the prep pass's column copy covers are drawn first, the rest while it runs)
+  const int n_first = resampled ? std::min(n_sets, cover_sets_for(est)) : n_sets;
   const int mr = c->max_rows, mc = c->max_cols;
   std::memset(rows, 0, (size_t)n_sets * mr * sizeof(int64_t));
   std::memset(cols, 0, (size_t)n_sets * mc * sizeof(int64_t));

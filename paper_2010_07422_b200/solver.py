@@ -666,7 +666,7 @@ def _solve_device(D, config: SolverConfig, observer=None, *, device=None, comput
         return _solve_native(ctx, Dd, cfg, pcg, code, fetch_factors, dtype, n1, n2, m_rows, m_cols, profile)
     # Draw the sets the prep pass needs first; the rest of the sequence is
     # drawn by a worker thread while the (host-blocking) prep pass runs.
-    n_first = min(n_sets, _cover_estimate(cfg) + 8) if resampled else n_sets
+    n_first = min(n_sets, _cover_sets(cfg)) if resampled else n_sets
     if pcg is None:
         sets, pcg_next = draw_index_sets(n1, n2, m_rows, m_cols, cfg.seed, n_sets), None
         n_first = n_sets
