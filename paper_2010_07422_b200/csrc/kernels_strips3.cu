@@ -5,13 +5,22 @@
 // solver.py:375-400).  What bounds those kernels is shared-memory wavefronts,
 // dominated by the per-line vectors A | W | Res that every warp broadcasts
 // for each line it processes (LDS.128 broadcast = 2 wavefronts, 8 bytes
-// each).  Here each lane owns TWO positions (2 lane and 2 lane + 1 of a 64-position
-// tile, packed in FFMA2 pairs), so every line-vector load feeds 2x the
-// entries of kernels_strips2.cu (the two positions are adjacent, 2 lane and
-// 2 lane + 1, so every stage access is one 8-byte load or store).  The price is shared memory: all sampled
-// lines of a 64-position tile are resident in ONE single-buffered stage per
-// CTA (16 warps on the same tile), so the next tile is prefetched into L2
-// (cp.async.bulk.prefetch) while the current one is computed.
+// each).  Here each lane owns TWO adjacent positions (2 lane and 2 lane + 1 of
+// a 64-position tile, packed in FFMA2 pairs), so every line-vector load feeds
+// 2x the entries of kernels_strips2.cu and every stage access is one 8-byte
+// load or store.  The price is shared memory: all sampled lines of a
+// 64-position tile are resident in ONE single-buffered stage per CTA (16 warps
+// on the same tile), filled in two halves with cp.async.
+//
+// Two instantiations:
+//   TC = false  pass 2 (the stopping residual) as FFMA2 chains; the next
+//               tile's halves are issued as pass 2 frees them.
+//   TC = true   pass 2 on the tensor cores: the thresholded tile moves to TMEM
+//               (tcgen05.st) and tcgen05.mma kind::tf32 accumulates
+//               -Res' F'^T onto it, with Res' in TMEM and F' in shared memory,
+//               both split exactly into three tf32 pieces; the next tile's
+//               fill is issued under the MMAs.  Taken for row strips of at
+//               least 32768 positions.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
