@@ -585,6 +585,7 @@ int extend_cover(ircur_ctx* c, int cover) {
     else
       IR_CUDA(launch_gather_cols<double>((const double*)c->D, c->ldd, c->nloc, c->d_newcols, (int)newcols.size(),
                                          (double*)c->Dt, c->ldt, c->dt_used, st));
+    c->kernel_launches += 1;
   }
   c->h_sel.swap(h_sel);
   c->dt_used = nl;
