@@ -184,6 +184,35 @@ def test_native_overlapped_shard_loop_equals_single_gpu(gloo1, monkeypatch, mode
     ir.clear_cache()
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_run_ahead_reaching_the_column_cover(gloo1, monkeypatch, split):
+    """With a loose eps the host's run-ahead (3 iterations) reaches the last
+    set the sampled column copy covers (3/4 of the schedule's estimate + 2)
+    although the solve has finished.  The single-GPU loops stop there; the
+    sharded loop, whose ranks must launch the same count, goes on without
+    extending the copy.  Results: the full copy's and the single GPU's, bit
+    for bit."""
+    from paper_2010_07422_b200.dist import run_collective
+    from paper_2010_07422_b200.solver import _cover_sets
+
+    monkeypatch.setenv("IRCUR_SHARD_SPLIT", split)
+    D, linf = _problem(2000, 1800, 5, seed=23, alpha=0.2)
+    cfg = _cfg(5, linf, "resampled", eps=1e-3)
+    Dd = torch.from_numpy(D.astype(np.float32)).cuda()
+    full = ir.solve(Dd, cfg, colmajor="full")
+    assert full[2].converged and full[2].iterations + 3 >= _cover_sets(cfg) > full[2].iterations
+    outs = [ir.solve(Dd, cfg, overlap=ov) for ov in (True, False)]
+    res = run_collective(solve_shard_program(Dd, cfg, n1=2000, row0=0, native=True, overlap=True))
+    outs.append(run_collective(gather_program(res)))
+    again = ir.solve(Dd, cfg)  # (the contexts stay usable)
+    outs.append(again)
+    for cur, sp, tr in outs:
+        assert tr.iterations == full[2].iterations and tr.converged and tr.errors == full[2].errors
+        for a, b in ((cur.C, full[0].C), (cur.R, full[0].R), (sp.col_values, full[1].col_values)):
+            np.testing.assert_array_equal(a, b)
+    ir.clear_cache()
+
+
 def test_native_loop_edge_cases(gloo1):
     """fp64 with the default overlap request takes the library's sequential
     loop (the overlapped one is fp32); a den == 0 problem leaves the loop
