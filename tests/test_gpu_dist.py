@@ -213,6 +213,34 @@ def test_run_ahead_reaching_the_column_cover(gloo1, monkeypatch, split):
     ir.clear_cache()
 
 
+def test_native_sharded_loop_extends_the_column_copy(gloo1):
+    """A sampled copy that covers 6 sets, extended while the library's sharded
+    loop runs (gathers from the row-major shard, or a second prep pass when
+    the copy's free lines run out): bitwise the single-GPU solve."""
+    from paper_2010_07422_b200.dist import run_collective
+
+    D, linf = _problem(2000, 1800, 5, seed=29, alpha=0.2)
+    cfg = _cfg(5, linf, "resampled", eps=1e-5)
+    Dd = torch.from_numpy(D.astype(np.float32)).cuda()
+    cur1, sp1, tr1 = ir.solve(Dd, cfg)
+    assert tr1.iterations > 14
+
+    def sharded(ov, cm):
+        res = run_collective(solve_shard_program(Dd, cfg, n1=2000, row0=0, native=True, overlap=ov, colmajor=cm))
+        return run_collective(gather_program(res))
+
+    for ov in (True, False):
+        # (the sequential sharded loop takes its SVD tolerance from e_{k-1}, the overlapped
+        # loops from e_{k-2}: each is compared with the full copy on its own loop)
+        ref = (cur1, sp1, tr1) if ov else sharded(ov, "full")
+        cur, sp, tr = sharded(ov, "sampled:6")
+        assert tr.iterations == ref[2].iterations and tr.converged == ref[2].converged
+        assert tr.errors == ref[2].errors, ov
+        for a, b in ((cur.C, ref[0].C), (cur.R, ref[0].R), (sp.col_values, ref[1].col_values)):
+            np.testing.assert_array_equal(a, b)
+    ir.clear_cache()
+
+
 def test_native_loop_edge_cases(gloo1):
     """fp64 with the default overlap request takes the library's sequential
     loop (the overlapped one is fp32); a den == 0 problem leaves the loop
